@@ -1,0 +1,223 @@
+/*
+ * mpkg — B200-native level-blocked matrix power kernel (MPK), C ABI.
+ *
+ * This is the drop-in boundary for the reference's C++ MPK interface (namespace mpk, header-only,
+ * /root/reference/proj/include/mpk/).  Every entry point below names the reference symbol it
+ * replaces (file:line).  The C++ facade in include/mpkg.hpp restores the reference's types,
+ * names and exceptions on top of these functions, so a reference call site switches with
+ * `namespace mpk = mpkg;`.
+ *
+ * Conventions
+ *  - Every function returns an int status (MPKG_OK on success).  No exception crosses the ABI;
+ *    the facade maps MPKG_EINVAL -> std::invalid_argument, MPKG_ERANGE -> std::out_of_range,
+ *    everything else -> std::runtime_error.  mpkg_last_error() holds a thread-local message.
+ *  - Indices are uint32 (reference index_t, csr.hpp:41); values are IEEE fp64.
+ *  - Power workspaces ("blocks") are slice-major: slice p of a block with `rows` rows starts at
+ *    block + p*rows (reference VectorBlock, vector_block.hpp:38-57).  Slice 0 receives x.
+ *  - Functions without a suffix take HOST pointers and are synchronous (they mirror the
+ *    reference's synchronous calls).  `_dev` variants take DEVICE pointers and enqueue on the
+ *    context's stream without synchronising.
+ *  - Handles are not thread-safe; use one context per device ("safe to call from
+ *    one thread at a time per plan").  Immutable objects (csr, levels, plan) may be shared.
+ *  - There is no CPU fallback: with no usable CUDA device every compute entry point fails with
+ *    MPKG_ECUDA.
+ */
+#ifndef MPKG_H
+#define MPKG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPKG_ABI_VERSION 1
+
+/* Status codes. */
+#define MPKG_OK 0
+#define MPKG_EINVAL 1    /* reference: std::invalid_argument */
+#define MPKG_ERANGE 2    /* reference: std::out_of_range (VectorBlock::slice) */
+#define MPKG_ECUDA 3     /* CUDA runtime failure / no device */
+#define MPKG_ENOMEM 4    /* device or host allocation failed */
+#define MPKG_EINTERNAL 5 /* anything else */
+
+/* Arithmetic modes (mpkg_ctx_set_mode). */
+#define MPKG_MODE_BITWISE 0 /* one sequential accumulator per row in stored column order,
+                               __dmul_rn + __dadd_rn: bit-identical to the reference CPU build */
+#define MPKG_MODE_FAST 1    /* reserved: DFMA / split long rows; checked to 1e-12 (inf-norm) */
+
+typedef struct mpkg_ctx_s* mpkg_ctx_t;
+typedef struct mpkg_csr_s* mpkg_csr_t;
+typedef struct mpkg_levels_s* mpkg_levels_t;
+typedef struct mpkg_plan_s* mpkg_plan_t;
+typedef struct mpkg_host_csr_s* mpkg_host_csr_t;
+
+/* ---- errors / version ------------------------------------------------------------------- */
+const char* mpkg_last_error(void);
+int mpkg_abi_version(void);
+
+/* ---- context (replaces threading.hpp:34-46 resolve_threads: device + stream selection) --- */
+int mpkg_ctx_create(int device, mpkg_ctx_t* out);
+int mpkg_ctx_destroy(mpkg_ctx_t ctx);
+int mpkg_ctx_stream(mpkg_ctx_t ctx, void** cuda_stream);
+int mpkg_ctx_synchronize(mpkg_ctx_t ctx);
+int mpkg_ctx_set_mode(mpkg_ctx_t ctx, int mode);
+/* Device facts the planner uses: SM count, L2 bytes, max persisting-L2 bytes. */
+int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t* persist_max);
+/* Executor tuning knobs: "slack" (tickets between a dependency and its
+ * consumer in the list schedule), "order", "tile_rows"; "kernel_timing" = 1 records a CUDA
+ * event pair around every power-kernel launch on the context stream. */
+int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value);
+/* Reads (and clears) the event pairs recorded with "kernel_timing": sum, count and max of the
+ * per-launch device durations in milliseconds.  Synchronises on the recorded events. */
+int mpkg_ctx_kernel_times(mpkg_ctx_t ctx, double* total_ms, uint64_t* count, double* max_ms);
+/* Kernel launches issued by this context since creation (instrumentation for bench.py). */
+int mpkg_ctx_launch_count(mpkg_ctx_t ctx, uint64_t* launches);
+
+/* ---- device CSR (csr.hpp:57-65 CsrMatrix) ------------------------------------------------- */
+/* Uploads a square or rectangular CSR (row_ptr[n_rows+1], col_idx[nnz], values[nnz]).
+ * Validates the csr.hpp:53-56 invariants (row_ptr monotone from 0, columns in range, strictly
+ * ascending within each row) and fails with MPKG_EINVAL otherwise. */
+int mpkg_csr_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, const uint32_t* row_ptr,
+                    const uint32_t* col_idx, const double* values, mpkg_csr_t* out);
+int mpkg_csr_create_from_host(mpkg_ctx_t ctx, mpkg_host_csr_t h, mpkg_csr_t* out);
+int mpkg_csr_info(mpkg_csr_t A, uint32_t* n_rows, uint32_t* n_cols, uint32_t* nnz);
+int mpkg_csr_download(mpkg_csr_t A, uint32_t* row_ptr, uint32_t* col_idx, double* values);
+int mpkg_csr_destroy(mpkg_csr_t A);
+
+/* csr.hpp:126-142 spmv: y = A x (bitwise row formula of csr.hpp:115-123). */
+int mpkg_spmv(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, double* y);
+int mpkg_spmv_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, double* d_y);
+
+/* ---- level engine (levels.hpp) ------------------------------------------------------------ */
+/* levels.hpp:65-147 build_levels: GPU BFS, bit-exact levels / perm / inv_perm / level_ptr. */
+int mpkg_build_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t* out);
+/* Build a level structure from host arrays (used to hand an externally built structure, e.g. a
+ * reference LevelStructure, to group_levels / validate_levels). level_ptr has n_levels+1. */
+int mpkg_levels_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_levels,
+                       const uint32_t* levels, const uint32_t* perm, const uint32_t* inv_perm,
+                       const uint32_t* level_ptr, mpkg_levels_t* out);
+int mpkg_levels_info(mpkg_levels_t L, uint32_t* n_rows, uint32_t* n_levels);
+/* Any output pointer may be NULL.  level_ptr receives n_levels+1 entries. */
+int mpkg_levels_get(mpkg_levels_t L, uint32_t* levels, uint32_t* perm, uint32_t* inv_perm,
+                    uint32_t* level_ptr);
+int mpkg_levels_destroy(mpkg_levels_t L);
+/* levels.hpp:151-164 validate_levels: *ok = 1 iff every nonzero couples levels <= 1 apart. */
+int mpkg_validate_levels(mpkg_ctx_t ctx, mpkg_csr_t A_perm, mpkg_levels_t L, int* ok);
+
+/* ---- permutation (csr.hpp:145-204) -------------------------------------------------------- */
+/* csr.hpp:159-188 permute with a host permutation (old -> new).  MPKG_EINVAL if not square or
+ * perm is not a permutation (csr.hpp:145-155). */
+int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t* out);
+/* Same, with the device-resident perm of a level structure (no host round trip). */
+int mpkg_permute_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t L, mpkg_csr_t* out);
+/* csr.hpp:191-204: out[perm[i]] = in[i] / out[i] = in[perm[i]] (host arrays). */
+int mpkg_permute_vector(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm,
+                        double* out);
+int mpkg_unpermute_vector(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm,
+                          double* out);
+
+/* ---- plan (plan.hpp) ----------------------------------------------------------------------- */
+/* plan.hpp:59-64 row_range_footprint over a device CSR. */
+int mpkg_row_range_footprint(mpkg_csr_t A_perm, uint32_t row_s, uint32_t row_e, int p_m,
+                             uint64_t* bytes);
+/* plan.hpp:70-85 greedy_group (pure host function).  bounds holds n_levels+1 entries. */
+int mpkg_greedy_group(const uint64_t* level_fp, uint32_t n_levels, uint64_t target,
+                      uint32_t* bounds, uint32_t* n_bounds);
+/* plan.hpp:88-115 group_levels. */
+int mpkg_group_levels(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A_perm, uint64_t cache_bytes,
+                      int p_m, mpkg_plan_t* out);
+int mpkg_plan_info(mpkg_plan_t P, int* p_m, int* sub_powers, uint32_t* n_rows,
+                   uint64_t* cache_bytes, uint64_t* target_bytes, uint32_t* n_groups);
+/* Any output may be NULL: group_rows / group_level_ptr have n_groups+1, footprint n_groups. */
+int mpkg_plan_get(mpkg_plan_t P, uint32_t* group_rows, uint32_t* group_level_ptr,
+                  uint64_t* group_footprint);
+int mpkg_plan_destroy(mpkg_plan_t P);
+/* Executor statistics for the GPU schedule attached to a plan (after the first mpkg_mpk):
+ * tiles, tickets, dependency ranges. */
+int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets,
+                        uint64_t* n_dep_ranges);
+
+/* execute.hpp:59-72 wavefront_schedule (pure host function; arrays hold n_groups*stages). */
+int mpkg_wavefront_schedule(uint32_t n_groups, int stages, uint32_t* group, int* stage,
+                            uint64_t* n_cells);
+
+/* ---- power kernels (mpk.hpp) --------------------------------------------------------------- */
+/* mpk.hpp:59-75 baseline_mpk: p_m back-to-back SpMV launches.  block has block_rows x
+ * block_slices; MPKG_EINVAL unless A square, p_m >= 1, block_rows == n and
+ * block_slices >= p_m+1 (mpk.hpp:44-53). */
+int mpkg_baseline_mpk(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, int p_m, double* block,
+                      uint64_t block_rows, uint64_t block_slices);
+int mpkg_baseline_mpk_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, int p_m,
+                          double* d_block, uint64_t block_rows, uint64_t block_slices);
+
+/* mpk.hpp:81-106 mpk: one fused, temporally blocked kernel (device-side dependency flags).
+ * A_perm must be level-permuted, x in permuted order; p_m <= the plan's p_m (execute.hpp:81-83).
+ * Bitwise equal to mpkg_baseline_mpk on A_perm in MPKG_MODE_BITWISE. */
+int mpkg_mpk(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* x, int p_m,
+             double* block, uint64_t block_rows, uint64_t block_slices);
+int mpkg_mpk_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* d_x, int p_m,
+                 double* d_block, uint64_t block_rows, uint64_t block_slices);
+
+/* mpk.hpp:111-127 check_shift_chain over shifts re[i] + i*im[i]. */
+int mpkg_check_shift_chain(const double* re, const double* im, int n_shifts);
+
+/* mpk.hpp:160-180 baseline_mpk_shifted / mpk.hpp:184-207 mpk_shifted (Newton basis
+ * y_p = (A - lambda_p I) y_{p-1}; conjugate pairs via the two-step real formulation). */
+int mpkg_baseline_mpk_shifted(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, const double* re,
+                              const double* im, int n_shifts, double* block, uint64_t block_rows,
+                              uint64_t block_slices);
+int mpkg_baseline_mpk_shifted_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x,
+                                  const double* re, const double* im, int n_shifts,
+                                  double* d_block, uint64_t block_rows, uint64_t block_slices);
+int mpkg_mpk_shifted(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* x,
+                     const double* re, const double* im, int n_shifts, double* block,
+                     uint64_t block_rows, uint64_t block_slices);
+int mpkg_mpk_shifted_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* d_x,
+                         const double* re, const double* im, int n_shifts, double* d_block,
+                         uint64_t block_rows, uint64_t block_slices);
+
+/* Coefficient-form polynomial z = sum_{k=0..d} c_k A^k x (the reference has
+ * no such API).  Accumulated inside the fused kernel in ascending k, each term a
+ * multiply then an add.  block may be NULL (then an internal workspace holds y_1..y_d). */
+int mpkg_mpk_poly(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* x,
+                  const double* c, int d, double* z, double* block, uint64_t block_rows,
+                  uint64_t block_slices);
+int mpkg_mpk_poly_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* d_x,
+                      const double* c, int d, double* d_z, double* d_block, uint64_t block_rows,
+                      uint64_t block_slices);
+
+/* mpk.hpp:211-258 tune_p: plan per p, one warm-up, median of max(reps,3) CUDA-event-timed runs,
+ * GF/s = 2*nnz*p/t; argmax with ties toward the smaller p.  gflops_table has p_hi-p_lo+1. */
+int mpkg_tune_p(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A_perm, uint64_t cache_bytes,
+                int p_lo, int p_hi, int reps, int* p_opt, double* gflops_table);
+/* mpk.hpp:219-233 tune_p(trial) selection rule over a given throughput table. */
+int mpkg_tune_select(const double* gflops_table, int p_lo, int p_hi, int* p_opt);
+
+/* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
+/* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]
+ *        4 random_csr(a=n, b=nnz_per_row, seed) 5 random_spd(a, b, seed) [generators.hpp:96-146]
+ *        6 stencil27(a,b,c; diag 26, off -1) [config C4]
+ *        7 stencil27 with off-diagonal -U[0.9,1.1] (seeded), then (A+A^T)/2 [config C2, before
+ *          the scramble]
+ *        8 rmat(scale=a, edge_factor=b, seed) with a,b,c,d = .57,.19,.19,.05, symmetrised,
+ *          self loops / duplicates removed, off-diagonal -U[0.1,1], diag 1+sum|off| [config C3] */
+int mpkg_gen(int kind, uint32_t a, uint32_t b, uint32_t c, uint64_t seed, mpkg_host_csr_t* out);
+/* Seeded symmetric scramble B = P A P^T (same semantics as permute) with a Fisher-Yates
+ * permutation drawn from mt19937_64(seed); perm_out (n entries, may be NULL) receives it. */
+int mpkg_host_csr_scramble(mpkg_host_csr_t A, uint64_t seed, uint32_t* perm_out,
+                           mpkg_host_csr_t* out);
+int mpkg_host_csr_info(mpkg_host_csr_t h, uint32_t* n_rows, uint32_t* n_cols, uint64_t* nnz);
+/* Borrowed pointers into the handle's arrays (valid until mpkg_host_csr_destroy). */
+int mpkg_host_csr_arrays(mpkg_host_csr_t h, uint32_t** row_ptr, uint32_t** col_idx,
+                         double** values);
+int mpkg_host_csr_destroy(mpkg_host_csr_t h);
+/* x_i ~ U[-1,1] from std::mt19937_64(seed) (acceptance.cpp:84-90 random_vector). */
+int mpkg_random_vector(uint64_t n, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPKG_H */

@@ -1,0 +1,405 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — CPU oracle restating the reference's level-blocked MPK path.
+ * See oracle.h for the contract and the pinning story.  Never linked by the product library.
+ *
+ * Build: cc -std=c99 -O2 (no -march: x86-64 baseline has no FMA, so `acc += v * x` is a mulsd
+ * followed by an addsd, exactly like the reference build, proj/CMakeLists.txt:8-21).
+ */
+#include "oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------------------------------------
+ * csr.hpp:207-227 — transpose with sorted rows (walking A in row order writes each transposed
+ * row in ascending original-row order).  Pattern only: build_levels never reads the values.
+ * ------------------------------------------------------------------------------------------- */
+static void transpose_pattern(uint32_t n, const uint32_t* rp, const uint32_t* ci, uint32_t* trp,
+                              uint32_t* tci) {
+    const uint32_t nnz = rp[n];
+    memset(trp, 0, sizeof(uint32_t) * ((size_t)n + 1));
+    for (uint32_t k = 0; k < nnz; ++k) trp[ci[k] + 1]++;
+    for (uint32_t r = 0; r < n; ++r) trp[r + 1] += trp[r];
+    uint32_t* cursor = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    memcpy(cursor, trp, sizeof(uint32_t) * n);
+    for (uint32_t r = 0; r < n; ++r)
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) tci[cursor[ci[k]]++] = r;
+    free(cursor);
+}
+
+static int cmp_u64(const void* a, const void* b) {
+    const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* levels.hpp:65-147 */
+int orc_build_levels(uint32_t n, const uint32_t* rp, const uint32_t* ci, uint32_t* levels,
+                     uint32_t* perm, uint32_t* inv_perm, uint32_t* level_ptr,
+                     uint32_t* n_levels) {
+    const uint32_t nnz = rp[n];
+    uint32_t* trp = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    uint32_t* tci = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)nnz + 1));
+    transpose_pattern(n, rp, ci, trp, tci);
+
+    /* levels.hpp:73-92 — per row the sorted union of the patterns of A and A^T, self-loops
+     * dropped. */
+    uint32_t* xadj = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    uint32_t* adj = (uint32_t*)malloc(sizeof(uint32_t) * (2 * (size_t)nnz + 1));
+    size_t m = 0;
+    xadj[0] = 0;
+    for (uint32_t r = 0; r < n; ++r) {
+        uint32_t a = rp[r], ae = rp[r + 1], b = trp[r], be = trp[r + 1];
+        while (a < ae || b < be) {
+            uint32_t c;
+            if (b >= be || (a < ae && ci[a] <= tci[b])) {
+                c = ci[a];
+                if (a < ae && b < be && ci[a] == tci[b]) ++b;
+                ++a;
+            } else {
+                c = tci[b];
+                ++b;
+            }
+            if (c != r) adj[m++] = c;
+        }
+        xadj[r + 1] = (uint32_t)m;
+    }
+    free(trp);
+    free(tci);
+
+    /* levels.hpp:101-107 — candidates in (degree, index) order. */
+    uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)n + 1));
+    for (uint32_t i = 0; i < n; ++i)
+        order[i] = ((uint64_t)(xadj[i + 1] - xadj[i]) << 32) | (uint64_t)i;
+    qsort(order, n, sizeof(uint64_t), cmp_u64);
+
+    /* levels.hpp:109-129 — the first unvisited candidate roots the next component; FIFO BFS. */
+    char* visited = (char*)calloc((size_t)n + 1, 1);
+    uint32_t* queue = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    uint32_t max_level = 0;
+    for (uint32_t i = 0; i < n; ++i) levels[i] = 0;
+    for (uint32_t t = 0; t < n; ++t) {
+        const uint32_t cand = (uint32_t)(order[t] & 0xffffffffu);
+        if (visited[cand]) continue;
+        visited[cand] = 1;
+        levels[cand] = 0;
+        uint32_t head = 0, tail = 0;
+        queue[tail++] = cand;
+        while (head < tail) {
+            const uint32_t u = queue[head++];
+            for (uint32_t k = xadj[u]; k < xadj[u + 1]; ++k) {
+                const uint32_t v = adj[k];
+                if (!visited[v]) {
+                    visited[v] = 1;
+                    levels[v] = levels[u] + 1;
+                    if (levels[v] > max_level) max_level = levels[v];
+                    queue[tail++] = v;
+                }
+            }
+        }
+    }
+    free(order);
+    free(visited);
+    free(queue);
+    free(xadj);
+    free(adj);
+
+    /* levels.hpp:131-145 — counting sort by (level, original index). */
+    const uint32_t nl = n == 0 ? 0 : max_level + 1;
+    memset(level_ptr, 0, sizeof(uint32_t) * ((size_t)nl + 1));
+    for (uint32_t r = 0; r < n; ++r) level_ptr[levels[r] + 1]++;
+    for (uint32_t l = 0; l < nl; ++l) level_ptr[l + 1] += level_ptr[l];
+    uint32_t* cursor = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)nl + 1));
+    memcpy(cursor, level_ptr, sizeof(uint32_t) * nl);
+    for (uint32_t r = 0; r < n; ++r) {
+        const uint32_t pos = cursor[levels[r]]++;
+        perm[r] = pos;
+        inv_perm[pos] = r;
+    }
+    free(cursor);
+    *n_levels = nl;
+    return ORC_OK;
+}
+
+/* csr.hpp:145-155 */
+int orc_check_permutation(const uint32_t* perm, uint32_t n) {
+    char* seen = (char*)calloc((size_t)n + 1, 1);
+    int ok = ORC_OK;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (perm[i] >= n || seen[perm[i]]) {
+            ok = ORC_EINVAL;
+            break;
+        }
+        seen[perm[i]] = 1;
+    }
+    free(seen);
+    return ok;
+}
+
+typedef struct {
+    uint32_t c;
+    double v;
+} entry_t;
+
+static int cmp_entry(const void* a, const void* b) {
+    const uint32_t x = ((const entry_t*)a)->c, y = ((const entry_t*)b)->c;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* csr.hpp:159-188 — B[perm[i], perm[j]] = A[i, j]; each row's (new col, value) pairs sorted.
+ * Columns are unique within a row, so ordering by column alone equals std::sort on the pairs. */
+int orc_permute(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                const uint32_t* perm, uint32_t* orp, uint32_t* oci, double* ov) {
+    if (orc_check_permutation(perm, n) != ORC_OK) return ORC_EINVAL;
+    memset(orp, 0, sizeof(uint32_t) * ((size_t)n + 1));
+    for (uint32_t r = 0; r < n; ++r) orp[perm[r] + 1] = rp[r + 1] - rp[r];
+    for (uint32_t r = 0; r < n; ++r) orp[r + 1] += orp[r];
+    size_t cap = 64;
+    entry_t* scratch = (entry_t*)malloc(sizeof(entry_t) * cap);
+    for (uint32_t r = 0; r < n; ++r) {
+        const uint32_t len = rp[r + 1] - rp[r];
+        if (len > cap) {
+            cap = len;
+            scratch = (entry_t*)realloc(scratch, sizeof(entry_t) * cap);
+        }
+        for (uint32_t k = 0; k < len; ++k) {
+            scratch[k].c = perm[ci[rp[r] + k]];
+            scratch[k].v = vals[rp[r] + k];
+        }
+        qsort(scratch, len, sizeof(entry_t), cmp_entry);
+        uint32_t out = orp[perm[r]];
+        for (uint32_t k = 0; k < len; ++k, ++out) {
+            oci[out] = scratch[k].c;
+            ov[out] = scratch[k].v;
+        }
+    }
+    free(scratch);
+    return ORC_OK;
+}
+
+/* csr.hpp:191-204 */
+void orc_permute_vector(uint32_t n, const double* in, const uint32_t* perm, double* out) {
+    for (uint32_t i = 0; i < n; ++i) out[perm[i]] = in[i];
+}
+void orc_unpermute_vector(uint32_t n, const double* in, const uint32_t* perm, double* out) {
+    for (uint32_t i = 0; i < n; ++i) out[i] = in[perm[i]];
+}
+
+/* levels.hpp:151-164 */
+int orc_validate_levels(uint32_t n, const uint32_t* rp, const uint32_t* ci, const uint32_t* levels,
+                        const uint32_t* inv_perm) {
+    uint32_t* lvl_new = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    for (uint32_t i = 0; i < n; ++i) lvl_new[i] = levels[inv_perm[i]];
+    int ok = 1;
+    for (uint32_t r = 0; r < n && ok; ++r) {
+        const uint32_t lr = lvl_new[r];
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const uint32_t lc = lvl_new[ci[k]];
+            const uint32_t d = lr > lc ? lr - lc : lc - lr;
+            if (d > 1) {
+                ok = 0;
+                break;
+            }
+        }
+    }
+    free(lvl_new);
+    return ok;
+}
+
+/* plan.hpp:59-64 */
+uint64_t orc_row_range_footprint(const uint32_t* rp, uint32_t row_s, uint32_t row_e, int p_m) {
+    const uint64_t nnz = (uint64_t)(rp[row_e] - rp[row_s]);
+    const uint64_t rows = (uint64_t)(row_e - row_s);
+    return 12 * nnz + 4 * rows + 8 * (uint64_t)(p_m + 1) * rows;
+}
+
+/* plan.hpp:70-85 */
+uint32_t orc_greedy_group(const uint64_t* fp, uint32_t nl, uint64_t target, uint32_t* bounds) {
+    uint32_t nb = 0;
+    bounds[nb++] = 0;
+    uint64_t acc = 0;
+    for (uint32_t l = 0; l < nl; ++l) {
+        if (l > bounds[nb - 1] && acc + fp[l] > target) {
+            bounds[nb++] = l;
+            acc = 0;
+        }
+        acc += fp[l];
+    }
+    if (nl > 0) bounds[nb++] = nl;
+    return nb;
+}
+
+/* plan.hpp:88-115 */
+int orc_group_levels(uint32_t n, const uint32_t* level_ptr, uint32_t nl, const uint32_t* rp_perm,
+                     uint64_t cache_bytes, int p_m, uint32_t* group_rows,
+                     uint32_t* group_level_ptr, uint64_t* group_fp, uint32_t* n_groups,
+                     uint64_t* target_bytes) {
+    (void)n;
+    if (p_m < 1) return ORC_EINVAL;
+    const uint64_t target = cache_bytes / (uint64_t)(p_m + 1);
+    uint64_t* lfp = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)nl + 1));
+    for (uint32_t l = 0; l < nl; ++l)
+        lfp[l] = orc_row_range_footprint(rp_perm, level_ptr[l], level_ptr[l + 1], p_m);
+    const uint32_t nb = orc_greedy_group(lfp, nl, target, group_level_ptr);
+    for (uint32_t b = 0; b < nb; ++b) group_rows[b] = level_ptr[group_level_ptr[b]];
+    for (uint32_t g = 0; g + 1 < nb; ++g) {
+        uint64_t s = 0;
+        for (uint32_t l = group_level_ptr[g]; l < group_level_ptr[g + 1]; ++l) s += lfp[l];
+        group_fp[g] = s;
+    }
+    free(lfp);
+    *n_groups = nb > 0 ? nb - 1 : 0;
+    *target_bytes = target;
+    return ORC_OK;
+}
+
+/* execute.hpp:59-72 */
+uint64_t orc_wavefront_schedule(uint32_t ng, int stages, uint32_t* group, int* stage) {
+    uint64_t cnt = 0;
+    if (ng == 0 || stages <= 0) return 0;
+    for (int64_t d = 0; d <= (int64_t)ng + stages - 2; ++d)
+        for (int q = 1; q <= stages; ++q) {
+            const int64_t g = d - (q - 1);
+            if (g >= 0 && g < (int64_t)ng) {
+                group[cnt] = (uint32_t)g;
+                stage[cnt] = q;
+                ++cnt;
+            }
+        }
+    return cnt;
+}
+
+/* csr.hpp:115-123 */
+void orc_spmv_rows(const uint32_t* rp, const uint32_t* ci, const double* vals, const double* x,
+                   double* y, uint32_t row_s, uint32_t row_e) {
+    for (uint32_t r = row_s; r < row_e; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) acc += vals[k] * x[ci[k]];
+        y[r] = acc;
+    }
+}
+
+/* mpk.hpp:59-75 */
+int orc_baseline_mpk(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                     const double* x, int p_m, double* block) {
+    if (p_m < 1) return ORC_EINVAL;
+    memcpy(block, x, sizeof(double) * n);
+    for (int p = 1; p <= p_m; ++p)
+        orc_spmv_rows(rp, ci, vals, block + (size_t)(p - 1) * n, block + (size_t)p * n, 0, n);
+    return ORC_OK;
+}
+
+/* mpk.hpp:81-106 over execute.hpp:79-113 with a single worker: the cells run in wavefront
+ * order, each over its whole group row range. */
+int orc_mpk(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+            const uint32_t* group_rows, uint32_t ng, int plan_p_m, const double* x, int p_m,
+            double* block) {
+    if (p_m < 1 || p_m > plan_p_m) return ORC_EINVAL;
+    memcpy(block, x, sizeof(double) * n);
+    const uint64_t cells = (uint64_t)ng * (uint64_t)p_m;
+    uint32_t* g = (uint32_t*)malloc(sizeof(uint32_t) * (cells + 1));
+    int* q = (int*)malloc(sizeof(int) * (cells + 1));
+    const uint64_t cnt = orc_wavefront_schedule(ng, p_m, g, q);
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const int p = q[i];
+        orc_spmv_rows(rp, ci, vals, block + (size_t)(p - 1) * n, block + (size_t)p * n,
+                      group_rows[g[i]], group_rows[g[i] + 1]);
+    }
+    free(g);
+    free(q);
+    return ORC_OK;
+}
+
+/* mpk.hpp:111-127 */
+int orc_check_shift_chain(const double* re, const double* im, int ns) {
+    for (int i = 0; i < ns; ++i) {
+        const double b = im[i];
+        if (b == 0.0) continue;
+        if (b < 0.0) return ORC_EINVAL;
+        if (i + 1 == ns) return ORC_EINVAL;
+        if (!(re[i + 1] == re[i] && im[i + 1] == -b)) return ORC_EINVAL;
+        ++i;
+    }
+    return ORC_OK;
+}
+
+/* mpk.hpp:135-153 */
+static void shifted_rows(const uint32_t* rp, const uint32_t* ci, const double* vals, double* dst,
+                         const double* src, const double* src2, double a, double b2,
+                         uint32_t row_s, uint32_t row_e) {
+    for (uint32_t r = row_s; r < row_e; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) acc += vals[k] * src[ci[k]];
+        if (b2 == 0.0)
+            dst[r] = acc - a * src[r];
+        else
+            dst[r] = acc - a * src[r] + b2 * src2[r];
+    }
+}
+
+static void shift_params(const double* re, const double* im, int p, double* a, double* b2) {
+    const double bi = im[p - 1];
+    *a = re[p - 1];
+    *b2 = bi < 0.0 ? bi * bi : 0.0; /* mpk.hpp:171 / 201 */
+}
+
+/* mpk.hpp:160-180 */
+int orc_baseline_mpk_shifted(uint32_t n, const uint32_t* rp, const uint32_t* ci,
+                             const double* vals, const double* x, const double* re,
+                             const double* im, int ns, double* block) {
+    if (ns < 1) return ORC_EINVAL;
+    if (orc_check_shift_chain(re, im, ns) != ORC_OK) return ORC_EINVAL;
+    memcpy(block, x, sizeof(double) * n);
+    for (int p = 1; p <= ns; ++p) {
+        double a, b2;
+        shift_params(re, im, p, &a, &b2);
+        const double* src2 = p >= 2 ? block + (size_t)(p - 2) * n : NULL;
+        shifted_rows(rp, ci, vals, block + (size_t)p * n, block + (size_t)(p - 1) * n, src2, a,
+                     b2, 0, n);
+    }
+    return ORC_OK;
+}
+
+/* mpk.hpp:184-207 */
+int orc_mpk_shifted(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                    const uint32_t* group_rows, uint32_t ng, int plan_p_m, const double* x,
+                    const double* re, const double* im, int ns, double* block) {
+    if (ns < 1 || ns > plan_p_m) return ORC_EINVAL;
+    if (orc_check_shift_chain(re, im, ns) != ORC_OK) return ORC_EINVAL;
+    memcpy(block, x, sizeof(double) * n);
+    const uint64_t cells = (uint64_t)ng * (uint64_t)ns;
+    uint32_t* g = (uint32_t*)malloc(sizeof(uint32_t) * (cells + 1));
+    int* q = (int*)malloc(sizeof(int) * (cells + 1));
+    const uint64_t cnt = orc_wavefront_schedule(ng, ns, g, q);
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const int p = q[i];
+        double a, b2;
+        shift_params(re, im, p, &a, &b2);
+        const double* src2 = p >= 2 ? block + (size_t)(p - 2) * n : NULL;
+        shifted_rows(rp, ci, vals, block + (size_t)p * n, block + (size_t)(p - 1) * n, src2, a,
+                     b2, group_rows[g[i]], group_rows[g[i] + 1]);
+    }
+    free(g);
+    free(q);
+    return ORC_OK;
+}
+
+/* SURVEY §8(a) A23 restatement (coefficient form; the reference has none). */
+void orc_poly_combine(uint32_t n, const double* block, const double* c, int d, double* z) {
+    for (uint32_t r = 0; r < n; ++r) {
+        double acc = c[0] * block[r];
+        for (int k = 1; k <= d; ++k) acc += c[k] * block[(size_t)k * n + r];
+        z[r] = acc;
+    }
+}
+
+/* mpk.hpp:219-233 */
+int orc_tune_select(const double* gflops, int p_lo, int p_hi) {
+    int best_p = p_lo;
+    double best = -1.0;
+    for (int p = p_lo; p <= p_hi; ++p)
+        if (gflops[p - p_lo] > best) {
+            best = gflops[p - p_lo];
+            best_p = p;
+        }
+    return best_p;
+}

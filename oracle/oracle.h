@@ -1,0 +1,108 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — the CPU oracle for the level-blocked MPK path.
+ *
+ * A plain-C99 restatement of the reference algorithm (the mpk headers under /root/reference/proj/include),
+ * each function citing the reference file:line it follows.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library, and only as the
+ * checker or the CPU baseline.  The product path (paper_2309_02228_b200/libmpkg.so) never links
+ * or calls it.
+ *
+ * Pinning: the restatement is checked bit-for-bit against (a) oracle/_ref/libmpkref.so, the
+ * reference's own headers compiled in place with the reference flags (no -march => no FMA), and
+ * (b) the golden fixtures in tests/golden/ generated from that library by
+ * tests/golden/make_golden.py.
+ *
+ * Floating point contract (proj/include/mpk/mpk.hpp:68-73): each row is summed sequentially in
+ * stored column order starting from 0.0 as `acc += v * x[c]` (a multiply then an add; this file
+ * is compiled without -march so no FMA contraction is possible on x86-64).
+ */
+#ifndef MPK_ORACLE_H
+#define MPK_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes mirror the reference's exception classes. */
+#define ORC_OK 0
+#define ORC_EINVAL 1 /* std::invalid_argument */
+
+/* levels.hpp:65-147.  level_ptr must hold n+1 entries; *n_levels receives the level count. */
+int orc_build_levels(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                     uint32_t* levels, uint32_t* perm, uint32_t* inv_perm,
+                     uint32_t* level_ptr, uint32_t* n_levels);
+
+/* csr.hpp:145-155 (returns ORC_EINVAL if perm is not a permutation of [0,n)). */
+int orc_check_permutation(const uint32_t* perm, uint32_t n);
+
+/* csr.hpp:159-188.  Output arrays sized n+1 / nnz / nnz. */
+int orc_permute(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                const double* values, const uint32_t* perm, uint32_t* out_row_ptr,
+                uint32_t* out_col_idx, double* out_values);
+
+/* csr.hpp:191-204. */
+void orc_permute_vector(uint32_t n, const double* in, const uint32_t* perm, double* out);
+void orc_unpermute_vector(uint32_t n, const double* in, const uint32_t* perm, double* out);
+
+/* levels.hpp:151-164: 1 if every nonzero of A_perm couples levels at most one apart. */
+int orc_validate_levels(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                        const uint32_t* levels, const uint32_t* inv_perm);
+
+/* plan.hpp:59-64. */
+uint64_t orc_row_range_footprint(const uint32_t* row_ptr, uint32_t row_s, uint32_t row_e, int p_m);
+
+/* plan.hpp:70-85.  bounds must hold n_levels+1 entries; returns the number of bounds. */
+uint32_t orc_greedy_group(const uint64_t* level_fp, uint32_t n_levels, uint64_t target,
+                          uint32_t* bounds);
+
+/* plan.hpp:88-115.  group arrays sized n_levels+1 (group_fp: n_levels). */
+int orc_group_levels(uint32_t n, const uint32_t* level_ptr, uint32_t n_levels,
+                     const uint32_t* row_ptr_perm, uint64_t cache_bytes, int p_m,
+                     uint32_t* group_rows, uint32_t* group_level_ptr, uint64_t* group_fp,
+                     uint32_t* n_groups, uint64_t* target_bytes);
+
+/* execute.hpp:59-72.  Arrays sized n_groups*stages; returns the cell count. */
+uint64_t orc_wavefront_schedule(uint32_t n_groups, int stages, uint32_t* group, int* stage);
+
+/* csr.hpp:115-123. */
+void orc_spmv_rows(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
+                   const double* x, double* y, uint32_t row_s, uint32_t row_e);
+
+/* mpk.hpp:59-75.  block is slice-major (p_m+1)*n. */
+int orc_baseline_mpk(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                     const double* values, const double* x, int p_m, double* block);
+
+/* mpk.hpp:81-106 driven by execute.hpp:79-113 (serial wavefront). */
+int orc_mpk(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
+            const uint32_t* group_rows, uint32_t n_groups, int plan_p_m, const double* x,
+            int p_m, double* block);
+
+/* mpk.hpp:111-127: ORC_OK or ORC_EINVAL. */
+int orc_check_shift_chain(const double* re, const double* im, int n_shifts);
+
+/* mpk.hpp:160-180. */
+int orc_baseline_mpk_shifted(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                             const double* values, const double* x, const double* re,
+                             const double* im, int n_shifts, double* block);
+
+/* mpk.hpp:184-207. */
+int orc_mpk_shifted(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                    const double* values, const uint32_t* group_rows, uint32_t n_groups,
+                    int plan_p_m, const double* x, const double* re, const double* im,
+                    int n_shifts, double* block);
+
+/* SURVEY §8(a) A23 (not in the reference): z = c_0*y_0, then z += c_k*y_k for
+ * k = 1..d ascending, each a multiply then an add, over a power block from orc_baseline_mpk. */
+void orc_poly_combine(uint32_t n, const double* block, const double* c, int d, double* z);
+
+/* mpk.hpp:219-233: argmax over the table, ties toward the smaller p. */
+int orc_tune_select(const double* gflops, int p_lo, int p_hi);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

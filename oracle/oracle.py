@@ -1,0 +1,360 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the CPU oracle.
+
+* `Oracle` wraps liboracle.so, the plain-C restatement (oracle.c) of the reference path.
+* `Reference` wraps _ref/libmpkref.so, the reference's own headers compiled in place with the
+  reference flags (oracle/Makefile); it is optional (absent when /root/reference was not
+  available at build time).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may use
+this module, and only as the checker / CPU baseline.  The product (paper_2309_02228_b200) never
+imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+from typing import Optional
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libmpkref.so"
+
+P = C.c_void_p
+u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Oracle:
+    """The C restatement (one thread)."""
+
+    def __init__(self, path: pathlib.Path = ORACLE_SO):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        L = self.lib = C.CDLL(str(path))
+        sig = {
+            "orc_build_levels": [u32, P, P, P, P, P, P, P],
+            "orc_check_permutation": [P, u32],
+            "orc_permute": [u32, P, P, P, P, P, P, P],
+            "orc_permute_vector": [u32, P, P, P],
+            "orc_unpermute_vector": [u32, P, P, P],
+            "orc_validate_levels": [u32, P, P, P, P],
+            "orc_row_range_footprint": [P, u32, u32, i32],
+            "orc_greedy_group": [P, u32, u64, P],
+            "orc_group_levels": [u32, P, u32, P, u64, i32, P, P, P, P, P],
+            "orc_wavefront_schedule": [u32, i32, P, P],
+            "orc_baseline_mpk": [u32, P, P, P, P, i32, P],
+            "orc_mpk": [u32, P, P, P, P, u32, i32, P, i32, P],
+            "orc_check_shift_chain": [P, P, i32],
+            "orc_baseline_mpk_shifted": [u32, P, P, P, P, P, P, i32, P],
+            "orc_mpk_shifted": [u32, P, P, P, P, u32, i32, P, P, P, i32, P],
+            "orc_poly_combine": [u32, P, P, i32, P],
+            "orc_tune_select": [P, i32, i32],
+        }
+        res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
+               "orc_wavefront_schedule": u64, "orc_permute_vector": None,
+               "orc_unpermute_vector": None, "orc_poly_combine": None}
+        for k, v in sig.items():
+            f = getattr(L, k)
+            f.argtypes = v
+            f.restype = res.get(k, C.c_int)
+
+    # levels.hpp:65
+    def build_levels(self, rp, ci):
+        rp, ci = _u32(rp), _u32(ci)
+        n = len(rp) - 1
+        lv, pm, ip = (np.empty(n, np.uint32) for _ in range(3))
+        lp = np.empty(n + 1, np.uint32)
+        nl = C.c_uint32()
+        assert self.lib.orc_build_levels(n, _p(rp), _p(ci), _p(lv), _p(pm), _p(ip), _p(lp),
+                                         C.byref(nl)) == 0
+        return lv, pm, ip, lp[: nl.value + 1].copy()
+
+    # csr.hpp:159
+    def permute(self, rp, ci, v, perm):
+        rp, ci, v, perm = _u32(rp), _u32(ci), _f64(v), _u32(perm)
+        n = len(rp) - 1
+        orp, oci, ov = np.empty(n + 1, np.uint32), np.empty(len(ci), np.uint32), np.empty(len(v))
+        rc = self.lib.orc_permute(n, _p(rp), _p(ci), _p(v), _p(perm), _p(orp), _p(oci), _p(ov))
+        if rc:
+            raise ValueError("permute: not a permutation")
+        return orp, oci, ov
+
+    def validate_levels(self, rp, ci, levels, inv_perm) -> bool:
+        rp, ci = _u32(rp), _u32(ci)
+        return bool(self.lib.orc_validate_levels(len(rp) - 1, _p(rp), _p(ci), _p(_u32(levels)),
+                                                 _p(_u32(inv_perm))))
+
+    def greedy_group(self, fp, target):
+        fp = np.ascontiguousarray(fp, dtype=np.uint64)
+        out = np.empty(len(fp) + 1, np.uint32)
+        nb = self.lib.orc_greedy_group(_p(fp), len(fp), int(target), _p(out))
+        return out[:nb].tolist()
+
+    # plan.hpp:88
+    def group_levels(self, level_ptr, rp_perm, cache_bytes, p_m):
+        lp, rp = _u32(level_ptr), _u32(rp_perm)
+        nl = len(lp) - 1
+        gr, glp = np.empty(nl + 1, np.uint32), np.empty(nl + 1, np.uint32)
+        gfp = np.empty(max(nl, 1), np.uint64)
+        ng, tgt = C.c_uint32(), C.c_uint64()
+        rc = self.lib.orc_group_levels(len(rp) - 1, _p(lp), nl, _p(rp), int(cache_bytes), p_m,
+                                       _p(gr), _p(glp), _p(gfp), C.byref(ng), C.byref(tgt))
+        if rc:
+            raise ValueError("group_levels: p_m must be >= 1")
+        g = ng.value
+        return gr[: g + 1].copy(), glp[: g + 1].copy(), gfp[:g].copy(), tgt.value
+
+    def wavefront_schedule(self, ng, stages):
+        n = max(ng * max(stages, 0), 1)
+        g, q = np.empty(n, np.uint32), np.empty(n, np.int32)
+        cnt = self.lib.orc_wavefront_schedule(ng, stages, _p(g), _p(q))
+        return list(zip(g[:cnt].tolist(), q[:cnt].tolist()))
+
+    # mpk.hpp:59
+    def baseline_mpk(self, rp, ci, v, x, p_m):
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        n = len(rp) - 1
+        blk = np.empty((p_m + 1) * n)
+        assert self.lib.orc_baseline_mpk(n, _p(rp), _p(ci), _p(v), _p(x), p_m, _p(blk)) == 0
+        return blk.reshape(p_m + 1, n)
+
+    # mpk.hpp:81
+    def mpk(self, rp, ci, v, group_rows, plan_p_m, x, p_m):
+        rp, ci, v, x, gr = _u32(rp), _u32(ci), _f64(v), _f64(x), _u32(group_rows)
+        n = len(rp) - 1
+        blk = np.empty((p_m + 1) * n)
+        rc = self.lib.orc_mpk(n, _p(rp), _p(ci), _p(v), _p(gr), len(gr) - 1, plan_p_m, _p(x),
+                              p_m, _p(blk))
+        if rc:
+            raise ValueError("mpk: bad arguments")
+        return blk.reshape(p_m + 1, n)
+
+    def _shifts(self, shifts):
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        return _f64(s.real), _f64(s.imag)
+
+    def check_shift_chain(self, shifts) -> bool:
+        re, im = self._shifts(shifts)
+        return self.lib.orc_check_shift_chain(_p(re), _p(im), len(re)) == 0
+
+    def baseline_mpk_shifted(self, rp, ci, v, x, shifts):
+        re, im = self._shifts(shifts)
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        n, s = len(rp) - 1, len(re)
+        blk = np.empty((s + 1) * n)
+        rc = self.lib.orc_baseline_mpk_shifted(n, _p(rp), _p(ci), _p(v), _p(x), _p(re), _p(im),
+                                               s, _p(blk))
+        if rc:
+            raise ValueError("baseline_mpk_shifted: bad shift chain")
+        return blk.reshape(s + 1, n)
+
+    def mpk_shifted(self, rp, ci, v, group_rows, plan_p_m, x, shifts):
+        re, im = self._shifts(shifts)
+        rp, ci, v, x, gr = _u32(rp), _u32(ci), _f64(v), _f64(x), _u32(group_rows)
+        n, s = len(rp) - 1, len(re)
+        blk = np.empty((s + 1) * n)
+        rc = self.lib.orc_mpk_shifted(n, _p(rp), _p(ci), _p(v), _p(gr), len(gr) - 1, plan_p_m,
+                                      _p(x), _p(re), _p(im), s, _p(blk))
+        if rc:
+            raise ValueError("mpk_shifted: bad arguments")
+        return blk.reshape(s + 1, n)
+
+    def poly(self, rp, ci, v, x, coef):
+        c = _f64(coef)
+        d = len(c) - 1
+        blk = np.ascontiguousarray(self.baseline_mpk(rp, ci, v, x, d))
+        n = blk.shape[1]
+        z = np.empty(n)
+        self.lib.orc_poly_combine(n, _p(blk), _p(c), d, _p(z))
+        return z, blk
+
+    def tune_select(self, table, p_lo, p_hi):
+        t = _f64(table)
+        return self.lib.orc_tune_select(_p(t), p_lo, p_hi)
+
+
+class Reference:
+    """The reference's own header-only implementation, compiled in place (OpenMP)."""
+
+    def __init__(self, path: pathlib.Path = REF_SO):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing (needs /root/reference at build time)")
+        L = self.lib = C.CDLL(str(path))
+        sig = {
+            "ref_gen": ([i32, u32, u32, u32, u64], P),
+            "ref_csr_info": ([P, P, P], None),
+            "ref_csr_copy": ([P, P, P, P], None),
+            "ref_csr_free": ([P], None),
+            "ref_random_vector": ([u64, u64, P], None),
+            "ref_build_levels": ([u32, P, P, P, P, P, P, P, P], C.c_int),
+            "ref_permute": ([u32, P, P, P, P, P, P, P], C.c_int),
+            "ref_validate_levels": ([u32, P, P, P, P, P, P, P, u32], C.c_int),
+            "ref_group_levels": ([u32, P, P, P, P, u32, u64, i32, P, P, P, P, P], C.c_int),
+            "ref_greedy_group": ([P, u32, u64, P], u32),
+            "ref_wavefront_schedule": ([u32, i32, P, P], u64),
+            "ref_csr_wrap": ([u32, P, P, P], P),
+            "ref_baseline_mpk_h": ([P, P, i32, P, i32], C.c_int),
+            "ref_mpk_h": ([P, P, u32, i32, P, i32, P, i32], C.c_int),
+            "ref_block_new": ([u64, u64], P),
+            "ref_block_free": ([P], None),
+            "ref_block_data": ([P], C.POINTER(C.c_double)),
+            "ref_vec_new": ([P, u64], P),
+            "ref_vec_free": ([P], None),
+            "ref_plan_new": ([u32, P, u32, i32], P),
+            "ref_plan_free": ([P], None),
+            "ref_baseline_mpk_t": ([P, P, i32, P, i32], C.c_int),
+            "ref_mpk_t": ([P, P, P, i32, P, i32], C.c_int),
+            "ref_baseline_mpk_shifted_h": ([P, P, P, P, i32, P, i32], C.c_int),
+            "ref_mpk_shifted_h": ([P, P, u32, i32, P, P, P, i32, P, i32], C.c_int),
+            "ref_check_shift_chain": ([P, P, i32], C.c_int),
+            "ref_tune_select": ([P, i32, i32], C.c_int),
+            "ref_resolve_threads": ([i32], C.c_int),
+            "ref_last_error": ([], C.c_char_p),
+        }
+        for k, (a, r) in sig.items():
+            f = getattr(L, k)
+            f.argtypes = a
+            f.restype = r
+
+    def gen(self, kind, a, b=0, c=0, seed=0):
+        h = self.lib.ref_gen(kind, a, b, c, seed)
+        if not h:
+            raise ValueError(self.lib.ref_last_error().decode())
+        n, nnz = C.c_uint32(), C.c_uint32()
+        self.lib.ref_csr_info(h, C.byref(n), C.byref(nnz))
+        rp = np.empty(n.value + 1, np.uint32)
+        ci = np.empty(nnz.value, np.uint32)
+        v = np.empty(nnz.value)
+        self.lib.ref_csr_copy(h, _p(rp), _p(ci), _p(v))
+        self.lib.ref_csr_free(h)
+        return rp, ci, v
+
+    def random_vector(self, n, seed):
+        out = np.empty(n)
+        self.lib.ref_random_vector(n, seed, _p(out))
+        return out
+
+    def build_levels(self, rp, ci, v):
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        n = len(rp) - 1
+        lv, pm, ip = (np.empty(n, np.uint32) for _ in range(3))
+        lp = np.empty(n + 1, np.uint32)
+        nl = C.c_uint32()
+        assert self.lib.ref_build_levels(n, _p(rp), _p(ci), _p(v), _p(lv), _p(pm), _p(ip),
+                                         _p(lp), C.byref(nl)) == 0
+        return lv, pm, ip, lp[: nl.value + 1].copy()
+
+    def permute(self, rp, ci, v, perm):
+        rp, ci, v, perm = _u32(rp), _u32(ci), _f64(v), _u32(perm)
+        n = len(rp) - 1
+        orp, oci, ov = np.empty(n + 1, np.uint32), np.empty(len(ci), np.uint32), np.empty(len(v))
+        if self.lib.ref_permute(n, _p(rp), _p(ci), _p(v), _p(perm), _p(orp), _p(oci), _p(ov)):
+            raise ValueError(self.lib.ref_last_error().decode())
+        return orp, oci, ov
+
+    def group_levels(self, rp, ci, v, level_ptr, cache_bytes, p_m):
+        rp, ci, v, lp = _u32(rp), _u32(ci), _f64(v), _u32(level_ptr)
+        nl = len(lp) - 1
+        gr, glp = np.empty(nl + 1, np.uint32), np.empty(nl + 1, np.uint32)
+        gfp = np.empty(max(nl, 1), np.uint64)
+        ng, tgt = C.c_uint32(), C.c_uint64()
+        if self.lib.ref_group_levels(len(rp) - 1, _p(rp), _p(ci), _p(v), _p(lp), nl,
+                                     int(cache_bytes), p_m, _p(gr), _p(glp), _p(gfp),
+                                     C.byref(ng), C.byref(tgt)):
+            raise ValueError(self.lib.ref_last_error().decode())
+        g = ng.value
+        return gr[: g + 1].copy(), glp[: g + 1].copy(), gfp[:g].copy(), tgt.value
+
+    def wrap(self, rp, ci, v):
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        return self.lib.ref_csr_wrap(len(rp) - 1, _p(rp), _p(ci), _p(v))
+
+    def baseline_mpk(self, rp, ci, v, x, p_m, threads=0):
+        h = self.wrap(rp, ci, v)
+        n = len(rp) - 1
+        blk = np.empty((p_m + 1) * n)
+        rc = self.lib.ref_baseline_mpk_h(h, _p(_f64(x)), p_m, _p(blk), threads)
+        self.lib.ref_csr_free(h)
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return blk.reshape(p_m + 1, n)
+
+    def mpk(self, rp, ci, v, group_rows, plan_p_m, x, p_m, threads=0):
+        h = self.wrap(rp, ci, v)
+        n = len(rp) - 1
+        gr = _u32(group_rows)
+        blk = np.empty((p_m + 1) * n)
+        rc = self.lib.ref_mpk_h(h, _p(gr), len(gr) - 1, plan_p_m, _p(_f64(x)), p_m, _p(blk),
+                                threads)
+        self.lib.ref_csr_free(h)
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return blk.reshape(p_m + 1, n)
+
+    def baseline_mpk_shifted(self, rp, ci, v, x, shifts, threads=0):
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        re, im = _f64(s.real), _f64(s.imag)
+        h = self.wrap(rp, ci, v)
+        n = len(rp) - 1
+        blk = np.empty((len(re) + 1) * n)
+        rc = self.lib.ref_baseline_mpk_shifted_h(h, _p(_f64(x)), _p(re), _p(im), len(re),
+                                                 _p(blk), threads)
+        self.lib.ref_csr_free(h)
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return blk.reshape(len(re) + 1, n)
+
+    def mpk_shifted(self, rp, ci, v, group_rows, plan_p_m, x, shifts, threads=0):
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        re, im = _f64(s.real), _f64(s.imag)
+        h = self.wrap(rp, ci, v)
+        n = len(rp) - 1
+        gr = _u32(group_rows)
+        blk = np.empty((len(re) + 1) * n)
+        rc = self.lib.ref_mpk_shifted_h(h, _p(gr), len(gr) - 1, plan_p_m, _p(_f64(x)), _p(re),
+                                        _p(im), len(re), _p(blk), threads)
+        self.lib.ref_csr_free(h)
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return blk.reshape(len(re) + 1, n)
+
+    def check_shift_chain(self, shifts) -> bool:
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        re, im = _f64(s.real), _f64(s.imag)
+        return self.lib.ref_check_shift_chain(_p(re), _p(im), len(re)) == 0
+
+    def greedy_group(self, fp, target):
+        fp = np.ascontiguousarray(fp, dtype=np.uint64)
+        out = np.empty(len(fp) + 1, np.uint32)
+        nb = self.lib.ref_greedy_group(_p(fp), len(fp), int(target), _p(out))
+        return out[:nb].tolist()
+
+    def wavefront_schedule(self, ng, stages):
+        n = max(ng * max(stages, 0), 1)
+        g, q = np.empty(n, np.uint32), np.empty(n, np.int32)
+        cnt = self.lib.ref_wavefront_schedule(ng, stages, _p(g), _p(q))
+        return list(zip(g[:cnt].tolist(), q[:cnt].tolist()))
+
+    def tune_select(self, table, p_lo, p_hi):
+        t = _f64(table)
+        return self.lib.ref_tune_select(_p(t), p_lo, p_hi)
+
+    def resolve_threads(self, requested=0):
+        return self.lib.ref_resolve_threads(requested)
+
+
+def reference_available() -> bool:
+    return REF_SO.exists()

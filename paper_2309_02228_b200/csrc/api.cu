@@ -1,0 +1,844 @@
+// The mpkg C ABI (include/mpkg.h): argument validation with the reference's error semantics,
+// host<->device staging, and dispatch to the sm_100a kernels.  No CPU fallback exists: every
+// compute entry point runs on the GPU or fails with MPKG_ECUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "device.h"
+
+using namespace mpkg_detail;
+
+namespace mpkg_detail {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> timing_begin(mpkg_ctx_s* ctx) {
+    if (!ctx->kernel_timing) return {nullptr, nullptr};
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!ctx->event_pool.empty()) {
+        ev = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+    } else {
+        MPKG_CUDA(cudaEventCreate(&ev.first));
+        MPKG_CUDA(cudaEventCreate(&ev.second));
+    }
+    MPKG_CUDA(cudaEventRecord(ev.first, ctx->stream));
+    return ev;
+}
+
+void timing_end(mpkg_ctx_s* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev) {
+    if (!ev.first) return;
+    MPKG_CUDA(cudaEventRecord(ev.second, ctx->stream));
+    ctx->timed.push_back(ev);
+}
+
+namespace {
+
+void use_device(mpkg_ctx_s* ctx) { MPKG_CUDA(cudaSetDevice(ctx->device)); }
+
+// csr.hpp:53-56 invariants, checked on the host copy before upload.
+void validate_csr_host(uint32_t n_rows, uint32_t n_cols, const uint32_t* rp, const uint32_t* ci) {
+    require(rp != nullptr, "csr: null row_ptr");
+    require(rp[0] == 0, "csr: row_ptr[0] must be 0");
+    require(rp[n_rows] < (1u << 31), "csr: nnz exceeds the 32-bit index range");
+    for (uint32_t r = 0; r < n_rows; ++r) {
+        require(rp[r] <= rp[r + 1], "csr: row_ptr must be monotone");
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            require(ci[k] < n_cols, "csr: column index out of range");
+            if (k > rp[r]) require(ci[k - 1] < ci[k], "csr: columns must be strictly ascending");
+        }
+    }
+}
+
+void check_workspace(const mpkg_csr_s* A, int p_m, uint64_t rows, uint64_t slices,
+                     const char* who) {
+    // mpk.hpp:44-53 check_power_workspace
+    require(A->n_rows == A->n_cols, std::string(who) + ": matrix must be square");
+    require(p_m >= 1, std::string(who) + ": p_m must be >= 1");
+    require(rows == A->n_rows && slices >= (uint64_t)p_m + 1,
+            std::string(who) + ": workspace too small");
+}
+
+void shift_chain(const double* re, const double* im, int ns, const char* who) {
+    // mpk.hpp:111-127 check_shift_chain
+    for (int i = 0; i < ns; ++i) {
+        const double b = im[i];
+        if (b == 0.0) continue;
+        if (b < 0.0)
+            fail(MPKG_EINVAL, std::string(who) + ": conjugate pair member without its partner");
+        if (i + 1 == ns)
+            fail(MPKG_EINVAL, std::string(who) + ": conjugate pair straddles the block end");
+        if (!(re[i + 1] == re[i] && im[i + 1] == -b))
+            fail(MPKG_EINVAL, std::string(who) + ": conjugate pairs must be stored adjacently");
+        ++i;
+    }
+}
+
+void shift_coeffs(const double* re, const double* im, int ns, std::vector<double>& a,
+                  std::vector<double>& b2) {
+    a.resize(ns);
+    b2.resize(ns);
+    for (int i = 0; i < ns; ++i) {
+        a[i] = re[i];
+        b2[i] = im[i] < 0.0 ? im[i] * im[i] : 0.0;  // mpk.hpp:171 / 201
+    }
+}
+
+// Host-pointer wrapper: stage x, run `body(d_x, d_block)`, copy the block back.
+template <class F>
+void with_host_block(mpkg_ctx_s* ctx, uint32_t n, const double* x, int p_m, double* block,
+                     F&& body) {
+    const uint64_t elems = (uint64_t)n * (p_m + 1);
+    ctx->scratch_block.ensure(std::max<uint64_t>(elems, 1));
+    ctx->scratch_x.ensure(std::max<uint32_t>(n, 1));
+    if (n) MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_x.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    body(ctx->scratch_x.p, ctx->scratch_block.p);
+    if (elems)
+        MPKG_CUDA(cudaMemcpyAsync(block, ctx->scratch_block.p, sizeof(double) * elems,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void baseline_dev(mpkg_ctx_s* ctx, mpkg_csr_s* A, const double* d_x, int p_m, double* d_block,
+                  uint64_t rows, uint64_t slices, const double* re, const double* im) {
+    const char* who = re ? "baseline_mpk_shifted" : "baseline_mpk";
+    check_workspace(A, p_m, rows, slices, who);
+    if (re) shift_chain(re, im, p_m, who);
+    use_device(ctx);
+    const uint32_t n = A->n_rows;
+    if (n == 0) return;
+    MPKG_CUDA(cudaMemcpyAsync(d_block, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    Sell& S = csr_sell(A);
+    std::vector<double> a, b2;
+    if (re) shift_coeffs(re, im, p_m, a, b2);
+    for (int p = 1; p <= p_m; ++p) {
+        const double* src = d_block + (uint64_t)(p - 1) * n;
+        double* dst = d_block + (uint64_t)p * n;
+        if (re)
+            launch_spmv_sell(ctx, S, true, src, dst, p >= 2 ? d_block + (uint64_t)(p - 2) * n : src,
+                             a[p - 1], b2[p - 1]);
+        else
+            launch_spmv_sell(ctx, S, false, src, dst, nullptr, 0.0, 0.0);
+    }
+}
+
+void mpk_dev(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const double* d_x, int p_m,
+             double* d_block, uint64_t rows, uint64_t slices, const double* re, const double* im,
+             const double* coef, double* d_z, const char* who) {
+    require(P != nullptr && A != nullptr, std::string(who) + ": null argument");
+    check_workspace(A, p_m, rows, slices, who);
+    require(P->n_rows == A->n_rows, std::string(who) + ": plan does not match matrix");
+    // execute.hpp:81-83
+    require(p_m <= P->p_m, "execute: p_m exceeds the plan's power budget");
+    if (re) shift_chain(re, im, p_m, who);
+    use_device(ctx);
+    const uint32_t n = A->n_rows;
+    if (n == 0) return;
+    MPKG_CUDA(cudaMemcpyAsync(d_block, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    FusedArgs fa;
+    fa.kind = re ? 1 : (coef ? 2 : 0);
+    fa.p = p_m;
+    fa.block = d_block;
+    fa.rows = rows;
+    std::vector<double> a, b2;
+    if (re) {
+        shift_coeffs(re, im, p_m, a, b2);
+        fa.shift_a = a.data();
+        fa.shift_b2 = b2.data();
+    }
+    fa.coef = coef;
+    fa.z = d_z;
+    run_fused(ctx, P, A, fa);
+}
+
+}  // namespace
+}  // namespace mpkg_detail
+
+extern "C" {
+
+const char* mpkg_last_error(void) { return mpkg_detail::g_last_error.c_str(); }
+int mpkg_abi_version(void) { return MPKG_ABI_VERSION; }
+
+// ---- context ----------------------------------------------------------------------------------
+int mpkg_ctx_create(int device, mpkg_ctx_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "ctx_create: null output");
+        int count = 0;
+        MPKG_CUDA(cudaGetDeviceCount(&count));
+        if (count <= 0) fail(MPKG_ECUDA, "no CUDA device visible (no CPU fallback exists)");
+        require(device >= 0 && device < count, "ctx_create: device index out of range");
+        MPKG_CUDA(cudaSetDevice(device));
+        auto* c = new mpkg_ctx_s();
+        c->device = device;
+        cudaDeviceProp prop{};
+        MPKG_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) {
+            delete c;
+            fail(MPKG_ECUDA, "mpkg is built for sm_100a (B200); device is sm_" +
+                                 std::to_string(prop.major) + std::to_string(prop.minor));
+        }
+        c->sm_count = prop.multiProcessorCount;
+        c->l2_bytes = prop.l2CacheSize;
+        c->persist_max = prop.persistingL2CacheMaxSize;
+        MPKG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+int mpkg_ctx_destroy(mpkg_ctx_t ctx) {
+    if (!ctx) return MPKG_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->scratch_x.release();
+    ctx->scratch_block.release();
+    for (auto& e : ctx->timed) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    for (auto& e : ctx->event_pool) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MPKG_OK;
+}
+
+int mpkg_ctx_stream(mpkg_ctx_t ctx, void** s) {
+    return guarded([&] {
+        require(ctx && s, "ctx_stream: null argument");
+        *s = (void*)ctx->stream;
+    });
+}
+
+int mpkg_ctx_synchronize(mpkg_ctx_t ctx) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_synchronize: null context");
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_ctx_set_mode(mpkg_ctx_t ctx, int mode) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_set_mode: null context");
+        require(mode == MPKG_MODE_BITWISE, "ctx_set_mode: only MPKG_MODE_BITWISE is implemented");
+        ctx->mode = mode;
+    });
+}
+
+int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm, size_t* l2, size_t* persist) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_device_info: null context");
+        if (sm) *sm = ctx->sm_count;
+        if (l2) *l2 = ctx->l2_bytes;
+        if (persist) *persist = ctx->persist_max;
+    });
+}
+
+int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
+    return guarded([&] {
+        require(ctx && key, "ctx_set_param: null argument");
+        const std::string k(key);
+        if (k == "slack")
+            ctx->slack = value;
+        else if (k == "order")
+            ctx->order = value;
+        else if (k == "kernel_timing")
+            ctx->kernel_timing = value != 0;
+        else if (k == "tile_rows")
+            require(value == 256, "ctx_set_param: tile_rows is fixed at 256 in this build");
+        else
+            fail(MPKG_EINVAL, "ctx_set_param: unknown key " + k);
+    });
+}
+
+int mpkg_ctx_kernel_times(mpkg_ctx_t ctx, double* total_ms, uint64_t* count, double* max_ms) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_kernel_times: null context");
+        double tot = 0.0, mx = 0.0;
+        uint64_t cnt = 0;
+        for (auto& e : ctx->timed) {
+            MPKG_CUDA(cudaEventSynchronize(e.second));
+            float ms = 0.f;
+            MPKG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+            tot += ms;
+            mx = std::max(mx, (double)ms);
+            ++cnt;
+            ctx->event_pool.push_back(e);
+        }
+        ctx->timed.clear();
+        if (total_ms) *total_ms = tot;
+        if (count) *count = cnt;
+        if (max_ms) *max_ms = mx;
+    });
+}
+
+int mpkg_ctx_launch_count(mpkg_ctx_t ctx, uint64_t* launches) {
+    return guarded([&] {
+        require(ctx && launches, "ctx_launch_count: null argument");
+        *launches = ctx->launches;
+    });
+}
+
+// ---- CSR --------------------------------------------------------------------------------------
+int mpkg_csr_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, const uint32_t* rp,
+                    const uint32_t* ci, const double* v, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && out, "csr_create: null argument");
+        validate_csr_host(n_rows, n_cols, rp, ci);
+        use_device(ctx);
+        auto* A = new mpkg_csr_s();
+        A->ctx = ctx;
+        A->n_rows = n_rows;
+        A->n_cols = n_cols;
+        A->nnz = rp[n_rows];
+        try {
+            A->row_ptr.alloc((uint64_t)n_rows + 1);
+            A->col_idx.alloc((uint64_t)A->nnz + 1);
+            A->values.alloc((uint64_t)A->nnz + 1);
+            MPKG_CUDA(cudaMemcpyAsync(A->row_ptr.p, rp, sizeof(uint32_t) * (n_rows + 1ull),
+                                      cudaMemcpyHostToDevice, ctx->stream));
+            if (A->nnz) {
+                MPKG_CUDA(cudaMemcpyAsync(A->col_idx.p, ci, sizeof(uint32_t) * A->nnz,
+                                          cudaMemcpyHostToDevice, ctx->stream));
+                MPKG_CUDA(cudaMemcpyAsync(A->values.p, v, sizeof(double) * A->nnz,
+                                          cudaMemcpyHostToDevice, ctx->stream));
+            }
+            MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete A;
+            throw;
+        }
+        *out = A;
+    });
+}
+
+int mpkg_csr_create_from_host(mpkg_ctx_t ctx, mpkg_host_csr_t h, mpkg_csr_t* out) {
+    if (!h) {
+        set_error("csr_create_from_host: null host matrix");
+        return MPKG_EINVAL;
+    }
+    return mpkg_csr_create(ctx, h->n_rows, h->n_cols, h->row_ptr.p, h->col_idx.p, h->values.p, out);
+}
+
+int mpkg_csr_info(mpkg_csr_t A, uint32_t* n_rows, uint32_t* n_cols, uint32_t* nnz) {
+    return guarded([&] {
+        require(A != nullptr, "csr_info: null matrix");
+        if (n_rows) *n_rows = A->n_rows;
+        if (n_cols) *n_cols = A->n_cols;
+        if (nnz) *nnz = A->nnz;
+    });
+}
+
+int mpkg_csr_download(mpkg_csr_t A, uint32_t* rp, uint32_t* ci, double* v) {
+    return guarded([&] {
+        require(A != nullptr, "csr_download: null matrix");
+        use_device(A->ctx);
+        cudaStream_t st = A->ctx->stream;
+        if (rp) MPKG_CUDA(cudaMemcpyAsync(rp, A->row_ptr.p, sizeof(uint32_t) * (A->n_rows + 1ull), cudaMemcpyDeviceToHost, st));
+        if (ci && A->nnz) MPKG_CUDA(cudaMemcpyAsync(ci, A->col_idx.p, sizeof(uint32_t) * A->nnz, cudaMemcpyDeviceToHost, st));
+        if (v && A->nnz) MPKG_CUDA(cudaMemcpyAsync(v, A->values.p, sizeof(double) * A->nnz, cudaMemcpyDeviceToHost, st));
+        MPKG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int mpkg_csr_destroy(mpkg_csr_t A) {
+    if (!A) return MPKG_OK;
+    cudaSetDevice(A->ctx->device);
+    cudaStreamSynchronize(A->ctx->stream);
+    delete A;
+    return MPKG_OK;
+}
+
+int mpkg_spmv_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, double* d_y) {
+    return guarded([&] {
+        require(ctx && A, "spmv: null argument");
+        use_device(ctx);
+        launch_spmv_sell(ctx, csr_sell(A), false, d_x, d_y, nullptr, 0.0, 0.0);
+    });
+}
+
+int mpkg_spmv(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, double* y) {
+    return guarded([&] {
+        require(ctx && A, "spmv: null argument");
+        use_device(ctx);
+        DevBuf<double> dx(std::max<uint32_t>(A->n_cols, 1)), dy(std::max<uint32_t>(A->n_rows, 1));
+        if (A->n_cols) MPKG_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * A->n_cols, cudaMemcpyHostToDevice, ctx->stream));
+        launch_spmv_sell(ctx, csr_sell(A), false, dx.p, dy.p, nullptr, 0.0, 0.0);
+        if (A->n_rows) MPKG_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * A->n_rows, cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- levels -----------------------------------------------------------------------------------
+int mpkg_build_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t* out) {
+    return guarded([&] {
+        require(ctx && A && out, "build_levels: null argument");
+        require(A->n_rows == A->n_cols, "build_levels: matrix must be square");  // levels.hpp:66-67
+        use_device(ctx);
+        auto* L = new mpkg_levels_s();
+        L->ctx = ctx;
+        try {
+            gpu_build_levels(ctx, A, L);
+        } catch (...) {
+            delete L;
+            throw;
+        }
+        *out = L;
+    });
+}
+
+int mpkg_levels_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_levels, const uint32_t* levels,
+                       const uint32_t* perm, const uint32_t* inv_perm, const uint32_t* level_ptr,
+                       mpkg_levels_t* out) {
+    return guarded([&] {
+        require(ctx && out && level_ptr, "levels_create: null argument");
+        require(level_ptr[n_levels] == n_rows, "levels_create: level_ptr does not cover the rows");
+        use_device(ctx);
+        auto* L = new mpkg_levels_s();
+        L->ctx = ctx;
+        L->n_rows = n_rows;
+        L->n_levels = n_levels;
+        L->level_ptr.assign(level_ptr, level_ptr + n_levels + 1);
+        L->levels.alloc(n_rows);
+        L->perm.alloc(n_rows);
+        L->inv_perm.alloc(n_rows);
+        L->d_level_ptr.alloc(n_levels + 1);
+        cudaStream_t st = ctx->stream;
+        if (n_rows) {
+            if (levels) MPKG_CUDA(cudaMemcpyAsync(L->levels.p, levels, 4ull * n_rows, cudaMemcpyHostToDevice, st));
+            if (perm) MPKG_CUDA(cudaMemcpyAsync(L->perm.p, perm, 4ull * n_rows, cudaMemcpyHostToDevice, st));
+            if (inv_perm) MPKG_CUDA(cudaMemcpyAsync(L->inv_perm.p, inv_perm, 4ull * n_rows, cudaMemcpyHostToDevice, st));
+        }
+        MPKG_CUDA(cudaMemcpyAsync(L->d_level_ptr.p, level_ptr, 4ull * (n_levels + 1), cudaMemcpyHostToDevice, st));
+        MPKG_CUDA(cudaStreamSynchronize(st));
+        *out = L;
+    });
+}
+
+int mpkg_levels_info(mpkg_levels_t L, uint32_t* n_rows, uint32_t* n_levels) {
+    return guarded([&] {
+        require(L != nullptr, "levels_info: null handle");
+        if (n_rows) *n_rows = L->n_rows;
+        if (n_levels) *n_levels = L->n_levels;
+    });
+}
+
+int mpkg_levels_get(mpkg_levels_t L, uint32_t* levels, uint32_t* perm, uint32_t* inv_perm,
+                    uint32_t* level_ptr) {
+    return guarded([&] {
+        require(L != nullptr, "levels_get: null handle");
+        use_device(L->ctx);
+        cudaStream_t st = L->ctx->stream;
+        const uint64_t b = 4ull * L->n_rows;
+        if (b) {
+            if (levels) MPKG_CUDA(cudaMemcpyAsync(levels, L->levels.p, b, cudaMemcpyDeviceToHost, st));
+            if (perm) MPKG_CUDA(cudaMemcpyAsync(perm, L->perm.p, b, cudaMemcpyDeviceToHost, st));
+            if (inv_perm) MPKG_CUDA(cudaMemcpyAsync(inv_perm, L->inv_perm.p, b, cudaMemcpyDeviceToHost, st));
+        }
+        MPKG_CUDA(cudaStreamSynchronize(st));
+        if (level_ptr) std::memcpy(level_ptr, L->level_ptr.data(), 4ull * L->level_ptr.size());
+    });
+}
+
+int mpkg_levels_destroy(mpkg_levels_t L) {
+    if (!L) return MPKG_OK;
+    cudaSetDevice(L->ctx->device);
+    cudaStreamSynchronize(L->ctx->stream);
+    delete L;
+    return MPKG_OK;
+}
+
+int mpkg_validate_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t L, int* ok) {
+    return guarded([&] {
+        require(ctx && A && L && ok, "validate_levels: null argument");
+        use_device(ctx);
+        *ok = gpu_validate_levels(ctx, A, L) ? 1 : 0;
+    });
+}
+
+// ---- permutation ------------------------------------------------------------------------------
+int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && A && out, "permute: null argument");
+        require(A->n_rows == A->n_cols, "permute: matrix must be square");
+        require(perm != nullptr || A->n_rows == 0, "permute: null permutation");
+        use_device(ctx);
+        DevBuf<uint32_t> d(std::max<uint32_t>(A->n_rows, 1));
+        if (A->n_rows)
+            MPKG_CUDA(cudaMemcpyAsync(d.p, perm, 4ull * A->n_rows, cudaMemcpyHostToDevice, ctx->stream));
+        gpu_check_permutation(ctx, d.p, A->n_rows);
+        auto* B = new mpkg_csr_s();
+        try {
+            gpu_permute(ctx, A, d.p, B);
+        } catch (...) {
+            delete B;
+            throw;
+        }
+        *out = B;
+    });
+}
+
+int mpkg_permute_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t L, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && A && L && out, "permute: null argument");
+        require(A->n_rows == A->n_cols, "permute: matrix must be square");
+        require(L->n_rows == A->n_rows, "permute: permutation size mismatch");
+        use_device(ctx);
+        auto* B = new mpkg_csr_s();
+        try {
+            gpu_permute(ctx, A, L->perm.p, B);
+        } catch (...) {
+            delete B;
+            throw;
+        }
+        *out = B;
+    });
+}
+
+static int permute_vec_common(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm,
+                              double* out, bool inverse) {
+    return guarded([&] {
+        require(ctx != nullptr, "permute_vector: null context");
+        if (n == 0) return;
+        require(in && perm && out, "permute_vector: null argument");
+        use_device(ctx);
+        DevBuf<double> di(n), dout(n);
+        DevBuf<uint32_t> dp(n);
+        MPKG_CUDA(cudaMemcpyAsync(di.p, in, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        MPKG_CUDA(cudaMemcpyAsync(dp.p, perm, 4ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        gpu_permute_vector(ctx, n, di.p, dp.p, dout.p, inverse);
+        MPKG_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_permute_vector(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm, double* out) {
+    return permute_vec_common(ctx, n, in, perm, out, false);
+}
+int mpkg_unpermute_vector(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm, double* out) {
+    return permute_vec_common(ctx, n, in, perm, out, true);
+}
+
+// ---- plan -------------------------------------------------------------------------------------
+int mpkg_row_range_footprint(mpkg_csr_t A, uint32_t row_s, uint32_t row_e, int p_m, uint64_t* bytes) {
+    return guarded([&] {
+        require(A && bytes, "row_range_footprint: null argument");
+        require(row_s <= row_e && row_e <= A->n_rows, "row_range_footprint: bad row range");
+        use_device(A->ctx);
+        uint32_t rs = 0, re = 0;
+        MPKG_CUDA(cudaMemcpy(&rs, A->row_ptr.p + row_s, 4, cudaMemcpyDeviceToHost));
+        MPKG_CUDA(cudaMemcpy(&re, A->row_ptr.p + row_e, 4, cudaMemcpyDeviceToHost));
+        // plan.hpp:59-64
+        *bytes = 12ull * (re - rs) + 4ull * (row_e - row_s) + 8ull * (uint64_t)(p_m + 1) * (row_e - row_s);
+    });
+}
+
+int mpkg_greedy_group(const uint64_t* fp, uint32_t nl, uint64_t target, uint32_t* bounds, uint32_t* nb) {
+    return guarded([&] {
+        require(bounds && nb && (fp || nl == 0), "greedy_group: null argument");
+        // plan.hpp:70-85
+        uint32_t k = 0;
+        bounds[k++] = 0;
+        uint64_t acc = 0;
+        for (uint32_t l = 0; l < nl; ++l) {
+            if (l > bounds[k - 1] && acc + fp[l] > target) {
+                bounds[k++] = l;
+                acc = 0;
+            }
+            acc += fp[l];
+        }
+        if (nl > 0) bounds[k++] = nl;
+        *nb = k;
+    });
+}
+
+int mpkg_group_levels(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A, uint64_t cache_bytes, int p_m,
+                      mpkg_plan_t* out) {
+    return guarded([&] {
+        require(ctx && L && A && out, "group_levels: null argument");
+        // plan.hpp:90-92
+        require(p_m >= 1, "group_levels: p_m must be >= 1");
+        require(A->n_rows == L->n_rows, "group_levels: level structure does not match matrix");
+        use_device(ctx);
+        const uint32_t nl = L->n_levels;
+        // row_ptr of A_perm at every level boundary, gathered on the device
+        std::vector<uint32_t> nnz_at(nl + 1, 0);
+        gpu_gather_row_ptr(ctx, A, L->d_level_ptr.p, nl + 1, nnz_at.data());
+        auto* P = new mpkg_plan_s();
+        P->p_m = p_m;
+        P->n_rows = L->n_rows;
+        P->cache_bytes = cache_bytes;
+        P->target_bytes = cache_bytes / (uint64_t)(p_m + 1);
+        P->level_ptr = L->level_ptr;
+        std::vector<uint64_t> lfp(nl);
+        for (uint32_t l = 0; l < nl; ++l) {
+            const uint64_t rows = L->level_ptr[l + 1] - L->level_ptr[l];
+            lfp[l] = 12ull * (nnz_at[l + 1] - nnz_at[l]) + 4ull * rows + 8ull * (uint64_t)(p_m + 1) * rows;
+        }
+        std::vector<uint32_t> bounds(nl + 1);
+        uint32_t nb = 0;
+        mpkg_greedy_group(lfp.data(), nl, P->target_bytes, bounds.data(), &nb);
+        bounds.resize(nb);
+        P->group_level_ptr = bounds;
+        for (uint32_t b : bounds) P->group_rows.push_back(L->level_ptr[b]);
+        for (size_t g = 0; g + 1 < bounds.size(); ++g) {
+            uint64_t s = 0;
+            for (uint32_t l = bounds[g]; l < bounds[g + 1]; ++l) s += lfp[l];
+            P->group_footprint.push_back(s);
+        }
+        *out = P;
+    });
+}
+
+int mpkg_plan_info(mpkg_plan_t P, int* p_m, int* sub, uint32_t* n_rows, uint64_t* cache,
+                   uint64_t* target, uint32_t* n_groups) {
+    return guarded([&] {
+        require(P != nullptr, "plan_info: null plan");
+        if (p_m) *p_m = P->p_m;
+        if (sub) *sub = P->sub_powers;
+        if (n_rows) *n_rows = P->n_rows;
+        if (cache) *cache = P->cache_bytes;
+        if (target) *target = P->target_bytes;
+        if (n_groups) *n_groups = P->group_rows.empty() ? 0 : (uint32_t)(P->group_rows.size() - 1);
+    });
+}
+
+int mpkg_plan_get(mpkg_plan_t P, uint32_t* gr, uint32_t* glp, uint64_t* gfp) {
+    return guarded([&] {
+        require(P != nullptr, "plan_get: null plan");
+        if (gr) std::copy(P->group_rows.begin(), P->group_rows.end(), gr);
+        if (glp) std::copy(P->group_level_ptr.begin(), P->group_level_ptr.end(), glp);
+        if (gfp) std::copy(P->group_footprint.begin(), P->group_footprint.end(), gfp);
+    });
+}
+
+int mpkg_plan_destroy(mpkg_plan_t P) {
+    delete P;
+    return MPKG_OK;
+}
+
+int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps) {
+    return guarded([&] {
+        require(P != nullptr, "plan_exec_info: null plan");
+        exec_info(P, n_tiles, n_tickets, n_deps);
+    });
+}
+
+int mpkg_wavefront_schedule(uint32_t ng, int stages, uint32_t* group, int* stage, uint64_t* n_cells) {
+    return guarded([&] {
+        require(n_cells != nullptr, "wavefront_schedule: null argument");
+        // execute.hpp:59-72
+        uint64_t cnt = 0;
+        if (ng != 0 && stages > 0) {
+            for (int64_t d = 0; d <= (int64_t)ng + stages - 2; ++d)
+                for (int q = 1; q <= stages; ++q) {
+                    const int64_t g = d - (q - 1);
+                    if (g >= 0 && g < (int64_t)ng) {
+                        if (group) group[cnt] = (uint32_t)g;
+                        if (stage) stage[cnt] = q;
+                        ++cnt;
+                    }
+                }
+        }
+        *n_cells = cnt;
+    });
+}
+
+// ---- power kernels ----------------------------------------------------------------------------
+int mpkg_baseline_mpk_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, int p_m, double* d_block,
+                          uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && A, "baseline_mpk: null argument");
+        baseline_dev(ctx, A, d_x, p_m, d_block, rows, slices, nullptr, nullptr);
+    });
+}
+
+int mpkg_baseline_mpk(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, int p_m, double* block,
+                      uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && A, "baseline_mpk: null argument");
+        check_workspace(A, p_m, rows, slices, "baseline_mpk");
+        use_device(ctx);
+        with_host_block(ctx, A->n_rows, x, p_m, block, [&](const double* dx, double* dblk) {
+            baseline_dev(ctx, A, dx, p_m, dblk, A->n_rows, (uint64_t)p_m + 1, nullptr, nullptr);
+        });
+    });
+}
+
+int mpkg_mpk_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* d_x, int p_m,
+                 double* d_block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx != nullptr, "mpk: null context");
+        mpk_dev(ctx, P, A, d_x, p_m, d_block, rows, slices, nullptr, nullptr, nullptr, nullptr, "mpk");
+    });
+}
+
+int mpkg_mpk(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* x, int p_m, double* block,
+             uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && P && A, "mpk: null argument");
+        check_workspace(A, p_m, rows, slices, "mpk");
+        require(P->n_rows == A->n_rows, "mpk: plan does not match matrix");
+        require(p_m <= P->p_m, "execute: p_m exceeds the plan's power budget");
+        use_device(ctx);
+        with_host_block(ctx, A->n_rows, x, p_m, block, [&](const double* dx, double* dblk) {
+            mpk_dev(ctx, P, A, dx, p_m, dblk, A->n_rows, (uint64_t)p_m + 1, nullptr, nullptr,
+                    nullptr, nullptr, "mpk");
+        });
+    });
+}
+
+int mpkg_check_shift_chain(const double* re, const double* im, int ns) {
+    return guarded([&] {
+        require((re && im) || ns == 0, "check_shift_chain: null argument");
+        shift_chain(re, im, ns, "check_shift_chain");
+    });
+}
+
+int mpkg_baseline_mpk_shifted_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, const double* re,
+                                  const double* im, int ns, double* d_block, uint64_t rows,
+                                  uint64_t slices) {
+    return guarded([&] {
+        require(ctx && A && re && im, "baseline_mpk_shifted: null argument");
+        baseline_dev(ctx, A, d_x, ns, d_block, rows, slices, re, im);
+    });
+}
+
+int mpkg_baseline_mpk_shifted(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, const double* re,
+                              const double* im, int ns, double* block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && A && re && im, "baseline_mpk_shifted: null argument");
+        check_workspace(A, ns, rows, slices, "baseline_mpk_shifted");
+        shift_chain(re, im, ns, "baseline_mpk_shifted");
+        use_device(ctx);
+        with_host_block(ctx, A->n_rows, x, ns, block, [&](const double* dx, double* dblk) {
+            baseline_dev(ctx, A, dx, ns, dblk, A->n_rows, (uint64_t)ns + 1, re, im);
+        });
+    });
+}
+
+int mpkg_mpk_shifted_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* d_x, const double* re,
+                         const double* im, int ns, double* d_block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && re && im, "mpk_shifted: null argument");
+        mpk_dev(ctx, P, A, d_x, ns, d_block, rows, slices, re, im, nullptr, nullptr, "mpk_shifted");
+    });
+}
+
+int mpkg_mpk_shifted(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* x, const double* re,
+                     const double* im, int ns, double* block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && P && A && re && im, "mpk_shifted: null argument");
+        check_workspace(A, ns, rows, slices, "mpk_shifted");
+        require(P->n_rows == A->n_rows, "mpk_shifted: plan does not match matrix");
+        shift_chain(re, im, ns, "mpk_shifted");
+        require(ns <= P->p_m, "execute: p_m exceeds the plan's power budget");
+        use_device(ctx);
+        with_host_block(ctx, A->n_rows, x, ns, block, [&](const double* dx, double* dblk) {
+            mpk_dev(ctx, P, A, dx, ns, dblk, A->n_rows, (uint64_t)ns + 1, re, im, nullptr, nullptr,
+                    "mpk_shifted");
+        });
+    });
+}
+
+int mpkg_mpk_poly_dev(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* d_x, const double* c,
+                      int d, double* d_z, double* d_block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && P && A && c && d_z, "mpk_poly: null argument");
+        DevBuf<double> own;
+        if (!d_block) {
+            own.alloc((uint64_t)A->n_rows * (d + 1) + 1);
+            d_block = own.p;
+            rows = A->n_rows;
+            slices = (uint64_t)d + 1;
+        }
+        mpk_dev(ctx, P, A, d_x, d, d_block, rows, slices, nullptr, nullptr, c, d_z, "mpk_poly");
+        if (own.p) MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_mpk_poly(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* x, const double* c, int d,
+                  double* z, double* block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && P && A && c && z, "mpk_poly: null argument");
+        if (block) check_workspace(A, d, rows, slices, "mpk_poly");
+        use_device(ctx);
+        const uint32_t n = A->n_rows;
+        DevBuf<double> dz(std::max<uint32_t>(n, 1));
+        ctx->scratch_x.ensure(std::max<uint32_t>(n, 1));
+        ctx->scratch_block.ensure((uint64_t)n * (d + 1) + 1);
+        if (n) MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_x.p, x, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        mpk_dev(ctx, P, A, ctx->scratch_x.p, d, ctx->scratch_block.p, n, (uint64_t)d + 1, nullptr,
+                nullptr, c, dz.p, "mpk_poly");
+        if (n) MPKG_CUDA(cudaMemcpyAsync(z, dz.p, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (block && n)
+            MPKG_CUDA(cudaMemcpyAsync(block, ctx->scratch_block.p, 8ull * n * (d + 1),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_tune_select(const double* table, int p_lo, int p_hi, int* p_opt) {
+    return guarded([&] {
+        require(table && p_opt, "tune_select: null argument");
+        require(p_lo >= 1 && p_hi >= p_lo, "tune_p: bad range");  // mpk.hpp:221
+        double best = -1.0;
+        int bp = p_lo;
+        for (int p = p_lo; p <= p_hi; ++p)
+            if (table[p - p_lo] > best) {
+                best = table[p - p_lo];
+                bp = p;
+            }
+        *p_opt = bp;
+    });
+}
+
+int mpkg_tune_p(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A, uint64_t cache_bytes, int p_lo,
+                int p_hi, int reps, int* p_opt, double* table) {
+    return guarded([&] {
+        require(ctx && L && A && p_opt && table, "tune_p: null argument");
+        require(p_lo >= 1 && p_hi >= p_lo, "tune_p: bad range");
+        if (reps < 3) reps = 3;  // mpk.hpp:241
+        use_device(ctx);
+        const uint32_t n = A->n_rows;
+        DevBuf<double> x(std::max<uint32_t>(n, 1)), blk((uint64_t)n * (p_hi + 1) + 1);
+        std::vector<double> ones(n, 1.0);  // mpk.hpp:242
+        if (n) MPKG_CUDA(cudaMemcpy(x.p, ones.data(), 8ull * n, cudaMemcpyHostToDevice));
+        cudaEvent_t e0, e1;
+        MPKG_CUDA(cudaEventCreate(&e0));
+        MPKG_CUDA(cudaEventCreate(&e1));
+        for (int p = p_lo; p <= p_hi; ++p) {
+            mpkg_plan_t P = nullptr;
+            int rc = mpkg_group_levels(ctx, L, A, cache_bytes, p, &P);
+            if (rc) fail(rc, mpkg_last_error());
+            std::unique_ptr<mpkg_plan_s> guard(P);
+            mpk_dev(ctx, P, A, x.p, p, blk.p, n, (uint64_t)p + 1, nullptr, nullptr, nullptr, nullptr, "tune_p");
+            std::vector<double> t(reps);
+            for (int r = 0; r < reps; ++r) {
+                MPKG_CUDA(cudaEventRecord(e0, ctx->stream));
+                mpk_dev(ctx, P, A, x.p, p, blk.p, n, (uint64_t)p + 1, nullptr, nullptr, nullptr, nullptr, "tune_p");
+                MPKG_CUDA(cudaEventRecord(e1, ctx->stream));
+                MPKG_CUDA(cudaEventSynchronize(e1));
+                float ms = 0.f;
+                MPKG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                t[r] = ms * 1e-3;
+            }
+            std::nth_element(t.begin(), t.begin() + reps / 2, t.end());
+            table[p - p_lo] = 2.0 * A->nnz * p / t[reps / 2] * 1e-9;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        mpkg_tune_select(table, p_lo, p_hi, p_opt);
+    });
+}
+
+}  // extern "C"

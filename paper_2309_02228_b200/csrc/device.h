@@ -1,0 +1,190 @@
+// Internal device-side types of the mpkg library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "host_csr.h"
+
+namespace mpkg_detail {
+
+#define MPKG_CUDA(call)                                                                        \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            (void)cudaGetLastError();                                                          \
+            ::mpkg_detail::fail(e_ == cudaErrorMemoryAllocation ? MPKG_ENOMEM : MPKG_ECUDA,    \
+                                std::string(#call) + ": " + cudaGetErrorString(e_));           \
+        }                                                                                      \
+    } while (0)
+
+#define MPKG_LAUNCH_CHECK() MPKG_CUDA(cudaGetLastError())
+
+// Owning device allocation.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    uint64_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(uint64_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(uint64_t count) {
+        release();
+        if (count) MPKG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count));
+        n = count;
+    }
+    // Grow-only reuse for scratch buffers.
+    void ensure(uint64_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    uint64_t bytes() const { return sizeof(T) * n; }
+};
+
+struct Ctx;
+
+// Sliced-ELLPACK (SELL-32) copy of a CSR in a given slot order: the storage the row kernels
+// read.  Rows keep their stored entry order (bitwise parity), slot s holds row slot_row[s]
+// (identity when slot_row is empty).  Layout per 32-row chunk c starting at entry off[c]:
+//   cols  (lane, k) -> off + (k/4)*128 + lane*4 + k%4   (one 16-byte load = 4 columns)
+//   vals  (lane, k) -> off + (k/2)*64  + lane*2 + k%2   (one 16-byte load = 2 values)
+struct Sell {
+    uint32_t n_rows = 0;
+    uint32_t n_slots = 0;  // multiple of 32
+    uint32_t n_chunks = 0;
+    uint64_t n_entries = 0;  // padded
+    DevBuf<uint64_t> chunk_off;
+    DevBuf<uint32_t> row_len;   // per slot
+    DevBuf<uint32_t> slot_row;  // per slot, optional (padding slots hold 0xffffffff)
+    DevBuf<uint32_t> cols;
+    DevBuf<double> vals;
+};
+
+struct Executor;  // fused-kernel schedule (mpk_exec.cu)
+
+}  // namespace mpkg_detail
+
+struct mpkg_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+    size_t l2_bytes = 0;
+    size_t persist_max = 0;
+    int mode = MPKG_MODE_BITWISE;
+    // executor knobs (mpkg_ctx_set_param)
+    int64_t tile_rows = 256;
+    int64_t slack = -1;  // -1: resident CTA count
+    int64_t order = 1;   // 0: reference wavefront of the plan's groups, 1: list schedule
+    uint64_t launches = 0;
+    // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
+    bool kernel_timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;  // recorded, not yet read
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
+    // scratch
+    mpkg_detail::DevBuf<double> scratch_x;
+    mpkg_detail::DevBuf<double> scratch_block;
+};
+
+struct mpkg_csr_s {
+    mpkg_ctx_s* ctx = nullptr;
+    uint32_t n_rows = 0;
+    uint32_t n_cols = 0;
+    uint32_t nnz = 0;
+    mpkg_detail::DevBuf<uint32_t> row_ptr;
+    mpkg_detail::DevBuf<uint32_t> col_idx;
+    mpkg_detail::DevBuf<double> values;
+    std::unique_ptr<mpkg_detail::Sell> sell;  // lazily built identity-order SELL copy
+};
+
+struct mpkg_levels_s {
+    mpkg_ctx_s* ctx = nullptr;
+    uint32_t n_rows = 0;
+    uint32_t n_levels = 0;
+    mpkg_detail::DevBuf<uint32_t> levels;
+    mpkg_detail::DevBuf<uint32_t> perm;
+    mpkg_detail::DevBuf<uint32_t> inv_perm;
+    std::vector<uint32_t> level_ptr;  // host copy (n_levels+1)
+    mpkg_detail::DevBuf<uint32_t> d_level_ptr;
+};
+
+struct mpkg_plan_s {
+    int p_m = 1;
+    int sub_powers = 1;
+    uint32_t n_rows = 0;
+    uint64_t cache_bytes = 0;
+    uint64_t target_bytes = 0;
+    std::vector<uint32_t> group_rows;
+    std::vector<uint32_t> group_level_ptr;
+    std::vector<uint64_t> group_footprint;
+    std::vector<uint32_t> level_ptr;  // the level structure the plan was built on
+    std::shared_ptr<mpkg_detail::Executor> exec;
+    const mpkg_csr_s* exec_csr = nullptr;  // matrix the executor was built for
+};
+
+namespace mpkg_detail {
+
+// Event pair around one kernel launch when ctx->kernel_timing is on (api.cu).
+std::pair<cudaEvent_t, cudaEvent_t> timing_begin(mpkg_ctx_s* ctx);
+void timing_end(mpkg_ctx_s* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev);
+
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 32u) {
+    uint64_t g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+// sell.cu
+Sell& csr_sell(mpkg_csr_s* A);
+void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row, Sell& out);
+void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
+                      double* dst, const double* src2, double shift_a, double shift_b2);
+
+// levels.cu
+void gpu_build_levels(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_levels_s* L);
+bool gpu_validate_levels(mpkg_ctx_s* ctx, const mpkg_csr_s* A_perm, const mpkg_levels_s* L);
+
+// permute.cu
+void gpu_check_permutation(mpkg_ctx_s* ctx, const uint32_t* d_perm, uint32_t n);
+void gpu_permute(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_perm, mpkg_csr_s* B);
+void gpu_permute_vector(mpkg_ctx_s* ctx, uint32_t n, const double* d_in, const uint32_t* d_perm,
+                        double* d_out, bool inverse);
+void gpu_gather_row_ptr(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_idx, uint32_t m,
+                        uint32_t* h_out);
+
+// mpk_exec.cu
+struct FusedArgs {
+    int kind = 0;  // 0 plain, 1 shifted, 2 poly
+    int p = 0;
+    const double* x = nullptr;
+    double* block = nullptr;  // slice-major, stride = rows
+    uint64_t rows = 0;
+    const double* shift_a = nullptr;   // host arrays, p entries
+    const double* shift_b2 = nullptr;  // host arrays, p entries
+    const double* coef = nullptr;      // host, p+1 entries
+    double* z = nullptr;
+};
+void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& a);
+void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps);
+
+}  // namespace mpkg_detail

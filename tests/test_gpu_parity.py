@@ -1,0 +1,320 @@
+"""GPU parity: every output of the sm_100a path against the pinned CPU oracle, bit for bit.
+
+Restates the reference's hot-path tests (proj/tests/test_levels.cpp, test_mpk.cpp,
+acceptance.cpp C1-C3) against the mpkg C ABI.  Levels/perm/inv_perm/level_ptr/A_perm must be
+bit-identical; basis vectors are bitwise equal in MPKG_MODE_BITWISE (the north star's 1e-12
+inf-norm tolerance is the looser bar, asserted too where stated)."""
+import numpy as np
+import pytest
+
+import paper_2309_02228_b200 as mpkg
+from conftest import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def corpus():
+    """The acceptance C1/C2 corpus (acceptance.cpp:118-160) plus irregular / scrambled cases."""
+    return {
+        "poisson1d_1000": mpkg.poisson1d(1000),
+        "poisson2d_256": mpkg.poisson2d(256, 256),
+        "poisson3d_32": mpkg.poisson3d(32, 32, 32),
+        "random_spd_50k": mpkg.random_spd(50000, 5, 777),
+        "random_spd_4000": mpkg.random_spd(4000, 6, 123),
+        "random_csr_2000": mpkg.random_csr(2000, 5, 3),  # nonsymmetric pattern
+        "stencil27_scrambled_20": mpkg.scramble(mpkg.stencil27_random_sym(20, 20, 20, 1), 2),
+        "rmat_12": mpkg.rmat(12, 8, 3),
+    }
+
+
+@pytest.fixture(scope="module")
+def cases(oracle):
+    out = {}
+    for name, A in corpus().items():
+        lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+        prp, pci, pv = oracle.permute(A.row_ptr, A.col_idx, A.values, pm)
+        out[name] = dict(A=A, levels=lv, perm=pm, inv_perm=ip, level_ptr=lp,
+                         P=mpkg.HostCsr.from_arrays(prp, pci, pv))
+    return out
+
+
+# ---- level engine -----------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tridiag5", "grid3x3", "poisson2d_20x17", "poisson3d_7x8x9",
+                                  "random_spd_200_5_77", "random_csr_300_5_11", "diag6",
+                                  "two_paths"] + [f"random_csr_120_4_{s}" for s in range(1, 6)])
+def test_levels_golden(ctx, golden, name):
+    g = lambda k: golden[f"lev.{name}.{k}"]
+    A = ctx.csr(mpkg.HostCsr.from_arrays(g("rp"), g("ci"), g("v")))
+    ls = ctx.build_levels(A)
+    for key in ("levels", "perm", "inv_perm", "level_ptr"):
+        np.testing.assert_array_equal(getattr(ls, key), g(key), err_msg=key)
+    P = ctx.permute(A, ls).download()
+    np.testing.assert_array_equal(P.row_ptr, g("prp"))
+    np.testing.assert_array_equal(P.col_idx, g("pci"))
+    assert_bitwise(P.values, g("pv"))
+    assert ctx.validate_levels(ctx.csr(P), ls)
+
+
+def test_levels_corpus_bit_exact(ctx, cases):
+    for name, c in cases.items():
+        A = ctx.csr(c["A"])
+        ls = ctx.build_levels(A)
+        for key in ("levels", "perm", "inv_perm", "level_ptr"):
+            np.testing.assert_array_equal(getattr(ls, key), c[key], err_msg=f"{name} {key}")
+        P = ctx.permute(A, ls).download()
+        np.testing.assert_array_equal(P.row_ptr, c["P"].row_ptr, err_msg=name)
+        np.testing.assert_array_equal(P.col_idx, c["P"].col_idx, err_msg=name)
+        assert_bitwise(P.values, c["P"].values, name)
+        # host-perm permute path (csr.hpp:159 signature) agrees too
+        P2 = ctx.permute(A, c["perm"]).download()
+        np.testing.assert_array_equal(P2.col_idx, c["P"].col_idx)
+        assert ctx.validate_levels(ctx.csr(c["P"]), ls)
+
+
+def test_validate_levels_detects_violation(ctx):
+    # test_levels.cpp:95-107
+    A = ctx.csr(mpkg.HostCsr.from_arrays([0, 2, 3, 4, 5], [0, 3, 1, 2, 3], [1.0] * 5))
+    ident = np.arange(4)
+    fake = ctx.levels_from_host(ident, ident, ident, [0, 1, 2, 3, 4])
+    assert not ctx.validate_levels(A, fake)
+
+
+def test_permute_rejects_non_permutation(ctx):
+    A = ctx.csr(mpkg.poisson1d(5))
+    with pytest.raises(ValueError):
+        ctx.permute(A, [0, 1, 2, 2, 4])
+    with pytest.raises(ValueError):
+        ctx.permute(A, [0, 1, 2, 3, 7])
+    with pytest.raises(ValueError):
+        ctx.build_levels(ctx.csr(mpkg.HostCsr.from_arrays([0, 1], [1], [1.0], n_cols=2)))
+
+
+def test_permute_vector_roundtrip(ctx, oracle):
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(1000).astype(np.uint32)
+    v = rng.standard_normal(1000)
+    pv = ctx.permute_vector(v, perm)
+    assert_bitwise(pv[perm], v)
+    assert_bitwise(ctx.unpermute_vector(pv, perm), v)
+
+
+def test_group_levels_golden(ctx, golden, oracle):
+    g = lambda k: golden[f"plan.poisson2d_64.{k}"]
+    A = ctx.csr(mpkg.poisson2d(64, 64))
+    ls = ctx.build_levels(A)
+    Ap = ctx.permute(A, ls)
+    plan = ctx.group_levels(ls, Ap, 100 * 1024, 4)
+    np.testing.assert_array_equal(plan.group_rows, g("group_rows"))
+    np.testing.assert_array_equal(plan.group_level_ptr, g("group_level_ptr"))
+    np.testing.assert_array_equal(plan.group_footprint, g("group_footprint"))
+    assert plan.target_bytes == 100 * 1024 // 5
+    # test_levels.cpp:124-147 plan invariants
+    for gi in range(plan.n_groups()):
+        assert plan.group_footprint[gi] == ctx.row_range_footprint(
+            Ap, int(plan.group_rows[gi]), int(plan.group_rows[gi + 1]), 4)
+        if plan.group_footprint[gi] > plan.target_bytes:
+            assert plan.group_level_ptr[gi + 1] - plan.group_level_ptr[gi] == 1
+    with pytest.raises(ValueError):
+        ctx.group_levels(ls, Ap, 1024, 0)  # test_levels.cpp:149-155
+    with pytest.raises(ValueError):
+        ctx.group_levels(ls, ctx.csr(mpkg.poisson1d(11)), 1024, 2)
+
+
+def test_group_levels_corpus(ctx, cases, oracle):
+    for name, c in cases.items():
+        ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+        Ap = ctx.csr(c["P"])
+        for cache, p in ((1 << 20, 3), (64 << 10, 8), (1 << 30, 1)):
+            plan = ctx.group_levels(ls, Ap, cache, p)
+            gr, glp, gfp, tgt = oracle.group_levels(c["level_ptr"], c["P"].row_ptr, cache, p)
+            np.testing.assert_array_equal(plan.group_rows, gr, err_msg=name)
+            np.testing.assert_array_equal(plan.group_footprint, gfp, err_msg=name)
+
+
+# ---- power kernels ----------------------------------------------------------------------------
+def test_spmv_and_baseline_golden(ctx, golden):
+    g = lambda k: golden[f"mpk.poisson2d_12x9_p5.{k}"]
+    A = ctx.csr(mpkg.HostCsr.from_arrays(g("rp"), g("ci"), g("v")))
+    blk = ctx.baseline_mpk(A, g("x"), 5)
+    assert_bitwise(blk.as_matrix(), g("block"))
+    assert_bitwise(ctx.spmv(A, g("x")), g("block")[1])
+
+
+@pytest.mark.parametrize("name", ["poisson2d_48x37", "poisson3d_9x10x11", "random_csr_2000_5_3"])
+@pytest.mark.parametrize("p", [1, 3, 6])
+def test_fused_mpk_golden(ctx, golden, name, p):
+    h = lambda k: golden[f"mpk.{name}_p{p}.{k}"]
+    A = ctx.csr(mpkg.HostCsr.from_arrays(h("rp"), h("ci"), h("v")))
+    ls = ctx.build_levels(A)
+    np.testing.assert_array_equal(ls.perm, h("perm"))
+    Ap = ctx.permute(A, ls)
+    plan = ctx.group_levels(ls, Ap, 64 * 1024, p)
+    np.testing.assert_array_equal(plan.group_rows, h("group_rows"))
+    assert_bitwise(ctx.mpk(plan, Ap, h("x"), p).as_matrix(), h("block"), "fused")
+    assert_bitwise(ctx.baseline_mpk(Ap, h("x"), p).as_matrix(), h("block"), "baseline")
+
+
+def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
+    """acceptance.cpp C1: blocked == baseline bitwise, corpus x p 1..8 (here both GPU paths also
+    equal the oracle)."""
+    for name, c in cases.items():
+        P = c["P"]
+        Ap = ctx.csr(P)
+        ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+        x = mpkg.random_vector(P.n_rows, 42)
+        ref8 = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 8)
+        for p in range(1, 9):
+            plan = ctx.group_levels(ls, Ap, 1 << 20, p)
+            assert_bitwise(ctx.mpk(plan, Ap, x, p).as_matrix(), ref8[: p + 1], f"{name} p={p}")
+        assert_bitwise(ctx.baseline_mpk(Ap, x, 8).as_matrix(), ref8, f"{name} baseline")
+
+
+def test_fused_repeatable_and_plan_reuse(ctx, cases):
+    c = cases["stencil27_scrambled_20"]
+    Ap = ctx.csr(c["P"])
+    ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+    plan = ctx.group_levels(ls, Ap, 1 << 20, 8)
+    x = mpkg.random_vector(Ap.n_rows, 7)
+    first = ctx.mpk(plan, Ap, x, 8).as_matrix().copy()
+    for p in (8, 5, 8, 2):  # p below the plan budget reuses the plan (execute.hpp:74-83)
+        assert_bitwise(ctx.mpk(plan, Ap, x, p).as_matrix(), first[: p + 1])
+    info = plan.exec_info()
+    assert info["tiles"] == (Ap.n_rows + 255) // 256
+
+
+def test_shifted_golden(ctx, golden):
+    g = lambda k: golden[f"shift.random_csr_150.{k}"]
+    A = ctx.csr(mpkg.HostCsr.from_arrays(g("rp"), g("ci"), g("v")))
+    assert_bitwise(ctx.baseline_mpk_shifted(A, g("x"), g("shifts")).as_matrix(), g("block"))
+    h = lambda k: golden[f"shift.poisson2d_30.{k}"]
+    A = ctx.csr(mpkg.HostCsr.from_arrays(h("rp"), h("ci"), h("v")))
+    ls = ctx.build_levels(A)
+    Ap = ctx.permute(A, ls)
+    plan = ctx.group_levels(ls, Ap, 16 * 1024, 5)
+    assert_bitwise(ctx.mpk_shifted(plan, Ap, h("x"), h("shifts")).as_matrix(), h("block"))
+
+
+def test_newton_basis_config4_shape(ctx, oracle):
+    """C4's Newton basis (real Chebyshev shifts on [0,52]) on a reduced 27-point grid."""
+    A = mpkg.stencil27(24, 24, 24)
+    lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+    P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
+    Ap = ctx.csr(P)
+    ls = ctx.levels_from_host(lv, pm, ip, lp)
+    theta = [26 + 26 * np.cos(np.pi * (2 * k - 1) / 16) for k in range(1, 9)]
+    x = mpkg.random_vector(P.n_rows, 5)
+    plan = ctx.group_levels(ls, Ap, 32 << 20, 8)
+    ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, theta)
+    assert_bitwise(ctx.mpk_shifted(plan, Ap, x, theta).as_matrix(), ref)
+    assert_bitwise(ctx.baseline_mpk_shifted(Ap, x, theta).as_matrix(), ref)
+
+
+def test_poly_coefficient_form(ctx, cases, oracle):
+    rng = np.random.default_rng(11)
+    for name in ("poisson3d_32", "stencil27_scrambled_20", "random_spd_4000"):
+        c = cases[name]
+        P = c["P"]
+        Ap = ctx.csr(P)
+        ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+        coef = rng.uniform(-1, 1, 9)
+        x = mpkg.random_vector(P.n_rows, 3)
+        plan = ctx.group_levels(ls, Ap, 1 << 20, 8)
+        z_ref, blk_ref = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+        z, blk = ctx.mpk_poly(plan, Ap, x, coef, return_block=True)
+        assert_bitwise(z, z_ref, name)
+        assert_bitwise(blk.as_matrix(), blk_ref, name)
+        assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), z_ref, name + " no block")
+
+
+def test_spec_examples(ctx):
+    A = ctx.csr(mpkg.HostCsr.from_arrays([0, 2, 3], [0, 1, 1], [2.0, 1.0, 3.0]))
+    blk = ctx.baseline_mpk(A, [1.0, 1.0], 2)
+    assert blk.slice(1).tolist() == [3.0, 3.0] and blk.slice(2).tolist() == [9.0, 9.0]
+    D = ctx.csr(mpkg.HostCsr.from_arrays([0, 1, 2], [0, 1], [1.0, 3.0]))
+    assert ctx.baseline_mpk_shifted(D, [1.0, 1.0], [2.0]).slice(1).tolist() == [-1.0, 1.0]
+    I = ctx.csr(mpkg.HostCsr.from_arrays([0, 1, 2, 3], [0, 1, 2], [1.0] * 3))
+    ls = ctx.build_levels(I)
+    Ip = ctx.permute(I, ls)
+    plan = ctx.group_levels(ls, Ip, 1 << 20, 4)
+    blk = ctx.mpk(plan, Ip, [1.0, 2.0, 3.0], 4)
+    assert all(blk.slice(p).tolist() == [1.0, 2.0, 3.0] for p in range(5))
+
+
+def test_argument_errors(ctx):
+    # test_mpk.cpp:247-259
+    A = ctx.csr(mpkg.poisson1d(10))
+    ls = ctx.build_levels(A)
+    P = ctx.permute(A, ls)
+    plan = ctx.group_levels(ls, P, 1024, 2)
+    x = np.ones(10)
+    with pytest.raises(ValueError):
+        ctx.mpk(plan, P, x, 2, mpkg.VectorBlock(10, 2))  # needs 3 slices
+    with pytest.raises(ValueError):
+        ctx.mpk(plan, P, x, 3, mpkg.VectorBlock(10, 4))  # p_m > plan
+    with pytest.raises(ValueError):
+        ctx.baseline_mpk(A, np.ones(9), 2)
+    with pytest.raises(ValueError):
+        ctx.baseline_mpk_shifted(A, x, [1.0, 2.0 + 1.0j])
+    with pytest.raises(ValueError):
+        ctx.mpk_shifted(plan, P, x, [2.0 - 1.0j, 2.0 + 1.0j])
+    with pytest.raises(ValueError):
+        ctx.mpk(plan, ctx.csr(mpkg.poisson1d(11)), np.ones(11), 2)
+
+
+def test_empty_and_edge_matrices(ctx):
+    # empty rows, a single row, a matrix with no entries at all
+    E = mpkg.HostCsr.from_arrays([0, 0, 1, 1], [1], [2.0])
+    A = ctx.csr(E)
+    ls = ctx.build_levels(A)
+    assert ls.n_levels() == 2
+    blk = ctx.baseline_mpk(A, [1.0, 3.0, 5.0], 2)
+    assert blk.slice(1).tolist() == [0.0, 6.0, 0.0]
+    Z = ctx.csr(mpkg.HostCsr.from_arrays([0, 0, 0], [], []))
+    lz = ctx.build_levels(Z)
+    assert list(lz.level_ptr) == [0, 2]
+    Zp = ctx.permute(Z, lz)
+    plan = ctx.group_levels(lz, Zp, 1 << 20, 3)
+    assert ctx.mpk(plan, Zp, [4.0, -1.0], 3).as_matrix()[1:].tolist() == [[0.0, 0.0]] * 3
+
+
+def test_special_values_propagate(ctx, oracle):
+    """0*Inf = NaN must appear exactly where the reference's row loop produces it."""
+    A = mpkg.poisson2d(40, 40)
+    x = mpkg.random_vector(A.n_rows, 1)
+    x[17] = np.inf
+    x[1000] = np.nan
+    ref = oracle.baseline_mpk(A.row_ptr, A.col_idx, A.values, x, 3)
+    assert_bitwise(ctx.baseline_mpk(ctx.csr(A), x, 3).as_matrix(), ref)
+
+
+def test_tune_p_measured(ctx):
+    # test_mpk.cpp:236-245
+    A = ctx.csr(mpkg.poisson2d(48, 48))
+    ls = ctx.build_levels(A)
+    Ap = ctx.permute(A, ls)
+    res = ctx.tune_p(ls, Ap, 256 * 1024, 1, 3)
+    assert 1 <= res.p_opt <= 3 and len(res.table) == 3
+    assert all(g > 0 for _, g in res.table)
+    with pytest.raises(ValueError):
+        ctx.tune_p(ls, Ap, 256 * 1024, 0, 3)
+
+
+def test_config1_full_size_bitwise(ctx, oracle):
+    """BASELINE config C1 (64^3 7-point, p=4) at full size, end to end on the GPU, against the
+    oracle: levels/perm bit-exact, all 4 basis vectors bit-exact."""
+    A = mpkg.poisson3d(64, 64, 64)
+    assert A.n_rows == 262144 and A.nnz == 1810432
+    lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+    assert len(lp) - 1 == 190
+    dA = ctx.csr(A)
+    ls = ctx.build_levels(dA)
+    np.testing.assert_array_equal(ls.perm, pm)
+    np.testing.assert_array_equal(ls.level_ptr, lp)
+    Ap = ctx.permute(dA, ls)
+    P = Ap.download()
+    prp, pci, pv = oracle.permute(A.row_ptr, A.col_idx, A.values, pm)
+    np.testing.assert_array_equal(P.col_idx, pci)
+    x = mpkg.random_vector(A.n_rows, 42)
+    plan = ctx.group_levels(ls, Ap, 100 << 20, 4)
+    ref = oracle.baseline_mpk(prp, pci, pv, x, 4)
+    assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref)

@@ -1,0 +1,163 @@
+"""Pins the CPU oracle (oracle/oracle.c) before it is trusted as the checker:
+(1) against the golden fixtures generated from the reference itself (tests/golden/), and
+(2) against the reference compiled in place (oracle/_ref) on fresh inputs, bit for bit, and
+(3) against the literal known answers of the reference's own tests / SPEC examples."""
+import numpy as np
+import pytest
+
+from conftest import assert_bitwise
+
+LEV_CASES = ["tridiag5", "grid3x3", "poisson2d_20x17", "poisson3d_7x8x9", "random_spd_200_5_77",
+             "random_csr_300_5_11", "diag6", "two_paths"] + [f"random_csr_120_4_{s}" for s in range(1, 6)]
+
+
+@pytest.mark.parametrize("name", LEV_CASES)
+def test_levels_and_permute_match_golden(oracle, golden, name):
+    g = lambda k: golden[f"lev.{name}.{k}"]
+    lv, pm, ip, lp = oracle.build_levels(g("rp"), g("ci"))
+    for got, key in ((lv, "levels"), (pm, "perm"), (ip, "inv_perm"), (lp, "level_ptr")):
+        np.testing.assert_array_equal(got, g(key), err_msg=key)
+    prp, pci, pv = oracle.permute(g("rp"), g("ci"), g("v"), pm)
+    np.testing.assert_array_equal(prp, g("prp"))
+    np.testing.assert_array_equal(pci, g("pci"))
+    assert_bitwise(pv, g("pv"), "values")
+    assert oracle.validate_levels(prp, pci, lv, ip)
+
+
+def test_known_answer_levels(oracle, golden):
+    # test_levels.cpp:15-24 tridiagonal: 5 levels of one row, identity perm
+    lv, pm, ip, lp = oracle.build_levels(golden["lev.tridiag5.rp"], golden["lev.tridiag5.ci"])
+    assert list(np.diff(lp)) == [1] * 5 and list(pm) == list(range(5))
+    # test_levels.cpp:26-33 3x3 grid -> [1,2,3,2,1]
+    lp = oracle.build_levels(golden["lev.grid3x3.rp"], golden["lev.grid3x3.ci"])[3]
+    assert list(np.diff(lp)) == [1, 2, 3, 2, 1]
+    # test_levels.cpp:35-46 diagonal -> one level
+    lp = oracle.build_levels(golden["lev.diag6.rp"], golden["lev.diag6.ci"])[3]
+    assert list(lp) == [0, 6]
+    # test_levels.cpp:58-72 two disjoint paths -> [2,2,1]
+    lp = oracle.build_levels(golden["lev.two_paths.rp"], golden["lev.two_paths.ci"])[3]
+    assert list(np.diff(lp)) == [2, 2, 1]
+
+
+def test_validate_levels_detects_violation(oracle):
+    # test_levels.cpp:95-107
+    rp = np.array([0, 2, 3, 4, 5]); ci = np.array([0, 3, 1, 2, 3])
+    ident = np.arange(4)
+    assert not oracle.validate_levels(rp, ci, ident, ident)
+
+
+def test_greedy_group_known_answers(oracle, golden):
+    # test_levels.cpp:109-122
+    assert oracle.greedy_group([1000] * 10, 2500) == [0, 2, 4, 6, 8, 10] == list(golden["greedy.a"])
+    assert oracle.greedy_group([1000, 5000, 1000, 1000], 2500) == [0, 1, 2, 4] == list(golden["greedy.b"])
+    assert oracle.greedy_group([10, 10, 10], 0) == [0, 1, 2, 3] == list(golden["greedy.c"])
+
+
+def test_group_levels_matches_golden(oracle, golden):
+    g = lambda k: golden[f"plan.poisson2d_64.{k}"]
+    gr, glp, gfp, tgt = oracle.group_levels(g("level_ptr"), g("prp"), 100 * 1024, 4)
+    np.testing.assert_array_equal(gr, g("group_rows"))
+    np.testing.assert_array_equal(glp, g("group_level_ptr"))
+    np.testing.assert_array_equal(gfp, g("group_footprint"))
+    assert tgt == int(g("target")) == 100 * 1024 // 5
+    with pytest.raises(ValueError):
+        oracle.group_levels(g("level_ptr"), g("prp"), 1024, 0)
+
+
+def test_wavefront_known_answer(oracle):
+    # test_mpk.cpp:47-58 / SPEC.md:232
+    assert oracle.wavefront_schedule(3, 2) == [(0, 1), (1, 1), (0, 2), (2, 1), (1, 2), (2, 2)]
+    for ng in range(1, 11):
+        for pm in range(1, 9):
+            order = oracle.wavefront_schedule(ng, pm)
+            assert len(order) == ng * pm and len(set(order)) == ng * pm
+            done = set()
+            for g, q in order:  # test_mpk.cpp:72-102 dependency audit
+                if q > 1:
+                    for nb in (g - 1, g, g + 1):
+                        if 0 <= nb < ng:
+                            assert (nb, q - 1) in done
+                done.add((g, q))
+
+
+def test_mpk_matches_golden(oracle, golden):
+    g = lambda k: golden[f"mpk.poisson2d_12x9_p5.{k}"]
+    assert_bitwise(oracle.baseline_mpk(g("rp"), g("ci"), g("v"), g("x"), 5), g("block"))
+    for name in ("poisson2d_48x37", "poisson3d_9x10x11", "random_csr_2000_5_3"):
+        for p in (1, 3, 6):
+            h = lambda k: golden[f"mpk.{name}_p{p}.{k}"]
+            prp, pci, pv = oracle.permute(h("rp"), h("ci"), h("v"), h("perm"))
+            blk = oracle.mpk(prp, pci, pv, h("group_rows"), p, h("x"), p)
+            assert_bitwise(blk, h("block"), f"{name} p={p} blocked")
+            assert_bitwise(oracle.baseline_mpk(prp, pci, pv, h("x"), p), h("block"), "baseline")
+
+
+def test_shifted_matches_golden(oracle, golden):
+    g = lambda k: golden[f"shift.random_csr_150.{k}"]
+    assert_bitwise(oracle.baseline_mpk_shifted(g("rp"), g("ci"), g("v"), g("x"), g("shifts")),
+                   g("block"))
+    h = lambda k: golden[f"shift.poisson2d_30.{k}"]
+    prp, pci, pv = oracle.permute(h("rp"), h("ci"), h("v"), h("perm"))
+    blk = oracle.mpk_shifted(prp, pci, pv, h("group_rows"), 5, h("x"), h("shifts"))
+    assert_bitwise(blk, h("block"))
+    assert_bitwise(oracle.baseline_mpk_shifted(prp, pci, pv, h("x"), h("shifts")), h("block"))
+
+
+def test_shift_chain_rules(oracle):
+    # test_mpk.cpp:208-222
+    assert not oracle.check_shift_chain([1.0, 2.0 + 1.0j])
+    assert not oracle.check_shift_chain([2.0 + 1.0j, 0.5, 2.0 - 1.0j])
+    assert not oracle.check_shift_chain([2.0 - 1.0j, 2.0 + 1.0j, 0.0])
+    assert oracle.check_shift_chain([0.4, 1.2 + 0.7j, 1.2 - 0.7j, -0.3])
+
+
+def test_spec_examples(oracle):
+    # SPEC.md:242 [[2,1],[0,3]], x=(1,1), p=2 -> (3,3), (9,9)
+    blk = oracle.baseline_mpk([0, 2, 3], [0, 1, 1], [2.0, 1.0, 3.0], [1.0, 1.0], 2)
+    assert blk[1].tolist() == [3.0, 3.0] and blk[2].tolist() == [9.0, 9.0]
+    # SPEC.md:262 diag(1,3), lambda=2 -> (-1,1)
+    blk = oracle.baseline_mpk_shifted([0, 1, 2], [0, 1], [1.0, 3.0], [1.0, 1.0], [2.0])
+    assert blk[1].tolist() == [-1.0, 1.0]
+    # SPEC.md:241 A=I -> y_p = x
+    blk = oracle.baseline_mpk([0, 1, 2, 3], [0, 1, 2], [1.0] * 3, [1.0, 2.0, 3.0], 4)
+    assert all(blk[p].tolist() == [1.0, 2.0, 3.0] for p in range(5))
+
+
+def test_tune_select(oracle):
+    # test_mpk.cpp:224-234
+    assert oracle.tune_select([1.0, 1.8, 2.1, 2.0], 1, 4) == 3
+    assert oracle.tune_select([1.0, 2.1, 1.5, 2.1], 1, 4) == 2
+
+
+def test_dense_power_oracle(oracle, golden):
+    """test_mpk.cpp:125-139: baseline vs a dense restatement, |d| <= 1e-13 max|ref|."""
+    g = lambda k: golden[f"mpk.poisson2d_12x9_p5.{k}"]
+    rp, ci, v, x = g("rp"), g("ci"), g("v"), g("x")
+    n = len(rp) - 1
+    D = np.zeros((n, n))
+    for r in range(n):
+        D[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
+    blk = oracle.baseline_mpk(rp, ci, v, x, 5)
+    y = x.copy()
+    for p in range(1, 6):
+        y = D @ y
+        assert np.max(np.abs(blk[p] - y)) <= 1e-13 * np.max(np.abs(y))
+
+
+def test_oracle_vs_reference_fresh(oracle, ref):
+    """Fresh (non-fixture) inputs: the restatement equals the reference bit for bit."""
+    for args in [(5, 5000, 7, 0, 9), (4, 3000, 6, 0, 17), (3, 11, 9, 7)]:
+        rp, ci, v = ref.gen(*args)
+        a = oracle.build_levels(rp, ci)
+        b = ref.build_levels(rp, ci, v)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+        po = oracle.permute(rp, ci, v, a[1])
+        pr = ref.permute(rp, ci, v, a[1])
+        for x, y in zip(po, pr):
+            np.testing.assert_array_equal(x, y)
+        x = ref.random_vector(len(rp) - 1, 42)
+        for p in (2, 5):
+            gr = oracle.group_levels(a[3], po[0], 256 * 1024, p)
+            np.testing.assert_array_equal(gr[0], ref.group_levels(*pr, a[3], 256 * 1024, p)[0])
+            assert_bitwise(oracle.mpk(*po, gr[0], p, x, p), ref.mpk(*pr, gr[0], p, x, p, threads=4))
