@@ -1,0 +1,521 @@
+#!/usr/bin/env python
+"""Benchmark of the level-blocked MPK path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl mpkg|reference]
+
+A step is one MPK call y_k = A^k x, k = 1..p (BASELINE.json metric: GFLOP/s = 2*nnz*p / t, the
+reference convention of proj/include/mpk/mpk.hpp:256), on the permuted matrix with x and the
+output block resident in HBM; level construction / permutation / planning are preprocessing,
+timed separately (the reference's level_preprocessing_s, solver.cpp:543-567).  `e2e` is the same
+metric through the host-pointer C ABI call (mpkg_mpk): H2D of x and D2H of all p+1 vectors from
+pinned memory inside the timed region.  `--impl reference` times the reference's own OpenMP CPU
+implementation (oracle/_ref, compiled from the reference headers) on this box's host cores.
+
+Workloads (BASELINE.json configs; synthetic inputs generated from seeds):
+  c1  3D 7-pt 64^3, p=4            c2  27-pt 160^3, -U[.9,1.1] sym + seeded scramble, p=8 (default)
+  c3  R-MAT scale 21 ef 16, p=4    c4  27-pt 192^3 Newton basis s=8   c4poly  same, sum c_k A^k x
+  c5  3D 7-pt 512^3, p=8
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+os.environ.setdefault("OMP_PLACES", "cores")  # reference CPU arm
+os.environ.setdefault("OMP_PROC_BIND", "close")
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "MPK A^p·x GFLOP/s (fp64 CRS), % of HBM roofline, DRAM bytes/nnz; 1–8 B200"
+
+CONFIGS = {
+    "c1": dict(desc="C1: 3D 7-point Laplacian 64^3, lexicographic, p=4", p=4, kind="plain"),
+    "c2": dict(desc="C2: 27-point 160^3, off-diag -U[0.9,1.1], (A+A^T)/2, seeded scramble, p=8",
+               p=8, kind="plain"),
+    "c3": dict(desc="C3: R-MAT scale 21, edge factor 16, symmetrised, p=4", p=4, kind="plain"),
+    "c4": dict(desc="C4: 27-point 192^3, Newton basis s=8, theta_k=26+26cos(pi(2k-1)/16)", p=8,
+               kind="shifted"),
+    "c4poly": dict(desc="C4: 27-point 192^3, z = sum_{k=0..8} c_k A^k x", p=8, kind="poly"),
+    "c5": dict(desc="C5: 3D 7-point Laplacian 512^3, p=8", p=8, kind="plain"),
+}
+
+
+def make_matrix(cfg: str, seed: int):
+    import paper_2309_02228_b200 as mpkg
+    if cfg == "c1":
+        return mpkg.poisson3d(64, 64, 64)
+    if cfg == "c2":
+        return mpkg.scramble(mpkg.stencil27_random_sym(160, 160, 160, seed), seed + 1)
+    if cfg == "c3":
+        return mpkg.rmat(21, 16, seed)
+    if cfg in ("c4", "c4poly"):
+        return mpkg.stencil27(192, 192, 192)
+    if cfg == "c5":
+        return mpkg.poisson3d(512, 512, 512)
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def newton_shifts(s=8):
+    return [26.0 + 26.0 * np.cos(np.pi * (2 * k - 1) / 16.0) for k in range(1, s + 1)]
+
+
+def poly_coefs(seed, d=8):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, d + 1)
+
+
+def measured_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_llc_bytes():
+    try:
+        v = os.sysconf("SC_LEVEL3_CACHE_SIZE")  # acceptance.cpp:691
+        if v and v > 0:
+            return int(v)
+    except (ValueError, OSError):
+        pass
+    return 32 << 20  # solver.cpp:117-121 CLI default
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=None)
+        pg = dist
+    return rank, world, local, pg
+
+
+def ref_preprocess(R, A, p, cache):
+    """Reference preprocessing on the host (build_levels + permute + group_levels)."""
+    t0 = time.perf_counter()
+    lv, pm, ip, lp = R.build_levels(A.row_ptr, A.col_idx, A.values)
+    t1 = time.perf_counter()
+    prp, pci, pv = R.permute(A.row_ptr, A.col_idx, A.values, pm)
+    t2 = time.perf_counter()
+    gr, _, _, _ = R.group_levels(prp, pci, pv, lp, cache, p)
+    t3 = time.perf_counter()
+    return (prp, pci, pv), pm, gr, {"build_levels_s": t1 - t0, "permute_s": t2 - t1,
+                                    "group_levels_s": t3 - t2}
+
+
+def time_reference_mpk(R, P, gr, p, x, kind, steps, warmup):
+    """Times the reference's blocked mpk / mpk_shifted through its own API (wall clock)."""
+    import ctypes as C
+    prp, pci, pv = P
+    n = len(prp) - 1
+    h = R.wrap(prp, pci, pv)
+    xv = R.lib.ref_vec_new(np.ascontiguousarray(x).ctypes.data, n)
+    plan = R.lib.ref_plan_new(n, np.ascontiguousarray(gr, np.uint32).ctypes.data, len(gr) - 1, p)
+    blk = R.lib.ref_block_new(n, p + 1)
+    times = []
+    try:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            if kind == "shifted":
+                sh = np.array(newton_shifts(p))
+                out = np.empty((p + 1) * n)
+                rc = R.lib.ref_mpk_shifted_h(h, np.ascontiguousarray(gr, np.uint32).ctypes.data,
+                                             len(gr) - 1, p, np.ascontiguousarray(x).ctypes.data,
+                                             sh.ctypes.data, np.zeros(p).ctypes.data, p,
+                                             out.ctypes.data, 0)
+            else:
+                rc = R.lib.ref_mpk_t(plan, h, xv, p, blk, 0)
+            t1 = time.perf_counter()
+            assert rc == 0, R.lib.ref_last_error()
+            if i >= warmup:
+                times.append(t1 - t0)
+    finally:
+        R.lib.ref_block_free(blk)
+        R.lib.ref_plan_free(plan)
+        R.lib.ref_vec_free(xv)
+        R.lib.ref_csr_free(h)
+    _ = C
+    return times
+
+
+def run_reference(args, cfgd):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return  # N>1: rank 0 alone runs the CPU reference
+    from oracle.oracle import Reference, reference_available
+    import paper_2309_02228_b200 as mpkg
+    p = cfgd["p"]
+    base = {"metric": METRIC, "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+            "higher_is_better": True, "config": {"workload": cfgd["desc"]}}
+    if not reference_available():
+        print(json.dumps({**base, "unavailable": "oracle/_ref/libmpkref.so not built"}), flush=True)
+        return
+    R = Reference()
+    A = make_matrix(args.config, args.seed)
+    cache = host_llc_bytes()
+    P, perm, gr, prep = ref_preprocess(R, A, p, cache)
+    x = np.empty(A.n_rows)
+    x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)  # permute_vector (csr.hpp:191)
+    kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
+    times = time_reference_mpk(R, P, gr, p, x, kind, args.steps, args.warmup)
+    nnz = A.nnz
+    med = statistics.median(times)
+    gf = 2.0 * nnz * p / med * 1e-9
+    cores = R.resolve_threads(0)
+    line = {**base, "value": gf, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": med * 1e3, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, DESIGN.md §6)",
+            "config": {"workload": cfgd["desc"], "n": A.n_rows, "nnz": nnz, "p": p,
+                       "cache_bytes": cache, "threads": cores, "cpu": cpu_model(),
+                       "preprocess_s": prep},
+            "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                             "sample": f"full {args.config} workload, reference blocked "
+                                       f"{'mpk_shifted' if kind == 'shifted' else 'mpk'} "
+                                       f"(p={p}, LLC budget {cache >> 20} MiB), median of "
+                                       f"{args.steps} after {args.warmup} warm-up"},
+            "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_reference(A_perm_host, perm_unused, ls_level_ptr, p, x, kind, nnz, ctx=None):
+    """Reference CPU path on the host cores (bounded: full workload, 1 warm-up + median of 3)."""
+    from oracle.oracle import Oracle, Reference, reference_available
+    cache = host_llc_bytes()
+    if reference_available():
+        R = Reference()
+        P = (A_perm_host.row_ptr, A_perm_host.col_idx, A_perm_host.values)
+        gr, _, _, _ = R.group_levels(*P, ls_level_ptr, cache, p)
+        times = time_reference_mpk(R, P, gr, p, x, kind, 3, 1)
+        med = statistics.median(times)
+        return {"value": 2.0 * nnz * p / med * 1e-9, "unit": "GFLOP/s",
+                "cores": R.resolve_threads(0), "kind": "reference",
+                "sample": f"full workload, reference blocked mpk (OpenMP, p={p}, LLC budget "
+                          f"{cache >> 20} MiB): 1 warm-up + median of 3 ({med:.3f} s each); "
+                          f"cpu: {cpu_model()}"}
+    O = Oracle()
+    t0 = time.perf_counter()
+    O.baseline_mpk(A_perm_host.row_ptr, A_perm_host.col_idx, A_perm_host.values, x, 1)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * nnz / dt * 1e-9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": "one SpMV sweep of the oracle port (single thread)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="mpkg", choices=["mpkg", "reference"])
+    ap.add_argument("--seed", type=int, default=2309)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slack", type=int, default=-1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfgd)
+
+    import torch
+
+    import paper_2309_02228_b200 as mpkg
+
+    rank, world, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    p = cfgd["p"]
+    t0 = time.perf_counter()
+    A = make_matrix(args.config, args.seed)
+    t_gen = time.perf_counter() - t0
+    n, nnz = A.n_rows, A.nnz
+
+    ctx = mpkg.Context(local)
+    if args.slack >= 0:
+        ctx.set_param("slack", args.slack)
+    info = ctx.device_info()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    def sync():
+        ctx.synchronize()
+        torch.cuda.synchronize()
+
+    prep = {"generate_host_s": t_gen}
+    t0 = time.perf_counter()
+    dA = ctx.csr(A)
+    sync()
+    prep["upload_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ls = ctx.build_levels(dA)
+    sync()
+    prep["build_levels_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Ap = ctx.permute(dA, ls)
+    sync()
+    prep["permute_s"] = time.perf_counter() - t0
+    cache = info["l2_bytes"]
+    t0 = time.perf_counter()
+    plan = ctx.group_levels(ls, Ap, cache, p)
+    prep["group_levels_s"] = time.perf_counter() - t0
+    del dA
+
+    x_host = mpkg.random_vector(n, args.seed + 2)
+    x_perm = ctx.permute_vector(x_host, ls.perm)  # csr.hpp:191 permute_vector
+    dev = torch.device("cuda", local)
+    d_x = torch.from_numpy(x_perm).to(dev)
+    d_blk = torch.empty((p + 1) * n, dtype=torch.float64, device=dev)
+    d_z = torch.empty(n, dtype=torch.float64, device=dev)
+    shifts = newton_shifts(p)
+    coefs = poly_coefs(args.seed + 3, p)
+
+    def step(block_ptr=None):
+        bp = d_blk.data_ptr() if block_ptr is None else block_ptr
+        if cfgd["kind"] == "shifted":
+            ctx.mpk_shifted_dev(plan, Ap, d_x.data_ptr(), shifts, bp, n, p + 1)
+        elif cfgd["kind"] == "poly":
+            ctx.mpk_poly_dev(plan, Ap, d_x.data_ptr(), coefs, d_z.data_ptr(), bp, n, p + 1)
+        else:
+            ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, bp, n, p + 1)
+
+    t0 = time.perf_counter()
+    step()  # builds the GPU schedule (SELL copy, tile dependencies, ticket order) once
+    sync()
+    prep["executor_build_s"] = time.perf_counter() - t0
+    exec_info = plan.exec_info()
+
+    # ---- parity at full size: fused == one-launch-per-power baseline, bit for bit -------------
+    ref_blk = torch.empty_like(d_blk)
+    if cfgd["kind"] == "shifted":
+        import ctypes
+        from paper_2309_02228_b200._lib import check, lib
+        re = np.ascontiguousarray(shifts, np.float64)
+        im = np.zeros(p)
+        check(lib.mpkg_baseline_mpk_shifted_dev(ctx.h, Ap.h, d_x.data_ptr(), re.ctypes.data,
+                                                im.ctypes.data, p, ref_blk.data_ptr(), n, p + 1))
+        _ = ctypes
+    else:
+        ctx.baseline_mpk_dev(Ap, d_x.data_ptr(), p, ref_blk.data_ptr(), n, p + 1)
+    sync()
+    parity = bool(torch.equal(ref_blk.view(torch.int64), d_blk.view(torch.int64)))
+    if cfgd["kind"] == "poly":
+        zr = torch.from_numpy(coefs[0] * ref_blk[:n].cpu().numpy())
+        # the oracle's A23 order (c0*y0, then += c_k*y_k) checked on the host copy
+        rb = ref_blk.view(p + 1, n).cpu().numpy()
+        acc = coefs[0] * rb[0]
+        for k in range(1, p + 1):
+            acc = acc + coefs[k] * rb[k]
+        parity = parity and np.array_equal(acc.view(np.uint64), d_z.cpu().numpy().view(np.uint64))
+        del zr
+    # baseline kernel timing for reference (p back-to-back launches)
+    ctx.set_param("kernel_timing", 1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(3):
+        ctx.baseline_mpk_dev(Ap, d_x.data_ptr(), p, ref_blk.data_ptr(), n, p + 1)
+    ev1.record(stream)
+    sync()
+    baseline_ms = ev0.elapsed_time(ev1) / 3
+    ctx.kernel_times()
+    del ref_blk
+    torch.cuda.empty_cache()
+
+    # ---- warm-up + timed region ---------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    sync()
+    ctx.kernel_times()  # discard warm-up records
+    if dist:
+        dist.barrier()
+    sync()
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        sync()
+    if dist:
+        dist.barrier()
+    launches = ctx.launch_count() - launches0
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    k_total, k_count, k_max = ctx.kernel_times()
+    kernel_ms = k_total / max(k_count, 1)
+    ctx.set_param("kernel_timing", 0)
+    if dist:
+        t = torch.tensor([step_ms, kernel_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, kernel_ms = t.tolist()
+    clocks = clk.summary()
+
+    flops = 2.0 * nnz * p
+    if cfgd["kind"] == "poly":
+        flops += 2.0 * n * (p + 1)
+    value = world * flops / (step_ms * 1e-3) * 1e-9
+
+    # ---- e2e through the host-pointer C ABI (pinned buffers, copies inside the timed region) --
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(x_perm).pin_memory()
+        hblk = torch.empty((p + 1) * n, dtype=torch.float64).pin_memory()
+        hz = torch.empty(n, dtype=torch.float64).pin_memory()
+        vb = mpkg.VectorBlock(n, p + 1, hblk.numpy())
+        xn = hx.numpy()
+
+        def e2e_step():
+            if cfgd["kind"] == "shifted":
+                ctx.mpk_shifted(plan, Ap, xn, shifts, vb)
+            elif cfgd["kind"] == "poly":
+                from paper_2309_02228_b200._lib import check, lib
+                c = np.ascontiguousarray(coefs)
+                check(lib.mpkg_mpk_poly(ctx.h, plan.h, Ap.h, xn.ctypes.data, c.ctypes.data, p,
+                                        hz.numpy().ctypes.data, hblk.numpy().ctypes.data, n, p + 1))
+            else:
+                ctx.mpk(plan, Ap, xn, p, vb)
+
+        e2e_step()
+        e_steps = max(3, min(args.steps, 10))
+        ts = []
+        for _ in range(e_steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        e_ms = statistics.median(ts)
+        if dist:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = t.item()
+        e2e = {"value": world * flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n * (p + 1) + (8 * n if cfgd["kind"] == "poly" else 0),
+               "ms_per_step": e_ms, "steps": e_steps}
+
+    # ---- roofline of the dominant (fused) kernel -----------------------------------------------
+    p_out = p
+    b_alg = 12 * nnz + 4 * (n + 1) + 8 * n * (1 + p_out)
+    if cfgd["kind"] == "poly":
+        b_alg += 8 * n
+    peak, peak_src = measured_peak()
+    achieved = b_alg / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        P_host = Ap.download()
+        kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
+        cpu = cpu_baseline_reference(P_host, None, ls.level_ptr, p, x_perm, kind, nnz)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
+            "config": {"workload": cfgd["desc"], "n": n, "nnz": nnz, "p": p,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2 ({(12 * nnz) / 1e9:.2f} GB matrix vs "
+                             f"{info['l2_bytes'] >> 20} MiB L2)" if 12 * nnz > info["l2_bytes"]
+                       else "matrix fits L2; no flush between steps (latency-bound config)",
+                       "mode": "bitwise", "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
+                       "plan_cache_bytes": cache, "executor": exec_info,
+                       "preprocess_s": prep, "parity": "fused == baseline bitwise" if parity
+                       else "MISMATCH", "baseline_back_to_back_ms": baseline_ms,
+                       "baseline_gflops": flops / (baseline_ms * 1e-3) * 1e-9},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms,
+                         "kernel_launches_timed": k_count, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+        if not parity:
+            sys.exit(3)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -297,6 +297,7 @@ int mpkg_csr_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, const uint
         use_device(ctx);
         auto* A = new mpkg_csr_s();
         A->ctx = ctx;
+        A->device = ctx->device;
         A->n_rows = n_rows;
         A->n_cols = n_cols;
         A->nnz = rp[n_rows];
@@ -352,8 +353,9 @@ int mpkg_csr_download(mpkg_csr_t A, uint32_t* rp, uint32_t* ci, double* v) {
 
 int mpkg_csr_destroy(mpkg_csr_t A) {
     if (!A) return MPKG_OK;
-    cudaSetDevice(A->ctx->device);
-    cudaStreamSynchronize(A->ctx->stream);
+    // The owning context may already be gone (destruction order is the caller's); cudaFree in
+    // the DevBuf destructors synchronises the device, so no stream is touched here.
+    cudaSetDevice(A->device);
     delete A;
     return MPKG_OK;
 }
@@ -386,6 +388,7 @@ int mpkg_build_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t* out) {
         use_device(ctx);
         auto* L = new mpkg_levels_s();
         L->ctx = ctx;
+        L->device = ctx->device;
         try {
             gpu_build_levels(ctx, A, L);
         } catch (...) {
@@ -405,6 +408,7 @@ int mpkg_levels_create(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_levels, const
         use_device(ctx);
         auto* L = new mpkg_levels_s();
         L->ctx = ctx;
+        L->device = ctx->device;
         L->n_rows = n_rows;
         L->n_levels = n_levels;
         L->level_ptr.assign(level_ptr, level_ptr + n_levels + 1);
@@ -451,8 +455,7 @@ int mpkg_levels_get(mpkg_levels_t L, uint32_t* levels, uint32_t* perm, uint32_t*
 
 int mpkg_levels_destroy(mpkg_levels_t L) {
     if (!L) return MPKG_OK;
-    cudaSetDevice(L->ctx->device);
-    cudaStreamSynchronize(L->ctx->stream);
+    cudaSetDevice(L->device);
     delete L;
     return MPKG_OK;
 }

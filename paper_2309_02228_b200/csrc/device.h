@@ -107,6 +107,7 @@ struct mpkg_ctx_s {
 
 struct mpkg_csr_s {
     mpkg_ctx_s* ctx = nullptr;
+    int device = 0;
     uint32_t n_rows = 0;
     uint32_t n_cols = 0;
     uint32_t nnz = 0;
@@ -118,6 +119,7 @@ struct mpkg_csr_s {
 
 struct mpkg_levels_s {
     mpkg_ctx_s* ctx = nullptr;
+    int device = 0;
     uint32_t n_rows = 0;
     uint32_t n_levels = 0;
     mpkg_detail::DevBuf<uint32_t> levels;

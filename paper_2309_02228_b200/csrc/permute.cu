@@ -137,6 +137,7 @@ void gpu_permute(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_perm, m
     const uint32_t n = A->n_rows;
     cudaStream_t st = ctx->stream;
     B->ctx = ctx;
+    B->device = ctx->device;
     B->n_rows = n;
     B->n_cols = n;
     B->nnz = A->nnz;
