@@ -284,6 +284,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slack", type=int, default=-1)
+    ap.add_argument("--order", type=int, default=1, help="0: A_perm order, 1: CM inside levels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
@@ -305,6 +306,7 @@ def main():
     ctx = mpkg.Context(local)
     if args.slack >= 0:
         ctx.set_param("slack", args.slack)
+    ctx.set_param("order", args.order)
     info = ctx.device_info()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
@@ -496,7 +498,7 @@ def main():
                        "l2": f"inputs larger than L2 ({(12 * nnz) / 1e9:.2f} GB matrix vs "
                              f"{info['l2_bytes'] >> 20} MiB L2)" if 12 * nnz > info["l2_bytes"]
                        else "matrix fits L2; no flush between steps (latency-bound config)",
-                       "mode": "bitwise", "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
+                       "mode": "bitwise", "order": args.order, "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
                        "plan_cache_bytes": cache, "executor": exec_info,
                        "preprocess_s": prep, "parity": "fused == baseline bitwise" if parity
                        else "MISMATCH", "baseline_back_to_back_ms": baseline_ms,

@@ -158,7 +158,13 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 32
 
 // sell.cu
 Sell& csr_sell(mpkg_csr_s* A);
-void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row, Sell& out);
+// d_slot_row: slot -> row (nullptr = identity); d_col_map: column relabel (nullptr = none).
+void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row,
+                const uint32_t* d_col_map, Sell& out);
+
+// reorder.cu: GPU-private Cuthill-McKee order inside BFS levels.
+void gpu_level_cm_order(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const std::vector<uint32_t>& level_ptr,
+                        uint32_t n_slots, DevBuf<uint32_t>& slot_row, DevBuf<uint32_t>& pos);
 void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
                       double* dst, const double* src2, double shift_a, double shift_b2);
 

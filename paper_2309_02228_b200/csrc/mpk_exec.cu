@@ -3,23 +3,28 @@
 // Reference behaviour replaced: execute.hpp:79-113 runs every (group, power) cell of the
 // diagonal wavefront (execute.hpp:59-72) with an OpenMP team and a barrier after every cell;
 // mpk.hpp:81-106 / 184-207 are its kernels.  Here:
-//   * the unit of work is a (tile, power) pair, a tile being 256 consecutive rows of A_perm
-//     (one thread per row, SELL-32 storage, bitwise row formula: rowdot.cuh);
+//   * rows of A_perm are executed in a GPU-private order sigma that stays inside each BFS level
+//     (reorder.cu: Cuthill-McKee within levels, or the identity); the executor keeps its own
+//     SELL-32 copy of A_perm in sigma order with columns relabelled to sigma slots and keeps the
+//     working vectors in sigma order, so 32 consecutive rows gather from a few cache lines;
+//     every result is also stored at its A_perm position in the caller's block;
+//   * the unit of work is a (tile, power) pair, a tile being 256 consecutive sigma slots (one
+//     thread per row, bitwise row formula: rowdot.cuh);
 //   * dependencies are tile-granular and derived from the sparsity pattern: tile T at power q
-//     needs power q-1 finished on every tile holding a column of T's rows (plus T itself), a
-//     contiguous tile range [dep_lo[T], dep_hi[T]] because A_perm is in level order.  This is the
-//     "boundary-level" refinement the reference leaves as future work and is
-//     strictly finer than its whole-neighbour-group rule (execute.hpp:23-28);
-//   * a per-tile completion flag done[T] = last finished power is published with st.release.gpu
-//     and polled with ld.acquire.gpu; no grid-wide barrier exists;
-//   * tickets (tile, power) are handed out by one global atomic counter in a host-computed
+//     needs power q-1 finished on every tile holding a column of T's rows, recorded per
+//     neighbouring level as a few tile ranges ("runs").  This is the boundary-level refinement
+//     the reference leaves as future work, strictly finer than its
+//     whole-neighbour-group rule (execute.hpp:23-28);
+//   * a per-tile flag done[T] = last finished power is published with st.release.gpu and polled
+//     with ld.acquire.gpu (L1 invalidated: LDG.E.STRONG.GPU + CCTL.IVALL); no grid barrier;
+//   * tickets (tile, power) are claimed through one global atomic counter in a host-computed
 //     topological order (list schedule: power q of T is placed `slack` tickets after the latest
-//     of its dependencies at power q-1), so a CTA only ever waits on tickets claimed earlier by
-//     running CTAs -> deadlock-free without co-residency assumptions;
-//   * the order keeps the active window of the matrix small so that each tile's matrix slice is
-//     re-read from L2 (not HBM) for powers 2..p.
-// Results are bit-identical to the one-launch-per-power baseline (and so to the reference)
-// because every row is computed by the same formula from the same inputs, in any order.
+//     of its power-(q-1) dependencies), so a CTA only waits on tickets claimed earlier by running
+//     CTAs: deadlock-free without any co-residency assumption;
+//   * the order keeps a narrow band of tiles active so each tile's matrix slice is re-read from
+//     L2, not HBM, for powers 2..p.
+// Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
+// every row is computed by the same formula, from the same inputs, in any order.
 #include <algorithm>
 #include <map>
 #include <numeric>
@@ -31,19 +36,24 @@
 
 namespace mpkg_detail {
 
-constexpr int kTile = 256;      // rows per tile == threads per CTA
+constexpr int kTile = 256;      // slots per tile == threads per CTA
 constexpr int kMaxFusedP = 32;  // powers per fused launch
+constexpr int kBuckets = 4;     // neighbouring-level buckets per tile
 
 struct Executor {
-    uint32_t n_tiles = 0;
-    uint32_t n_slots = 0;
+    int order = 0;  // 0: A_perm order, 1: Cuthill-McKee inside levels
+    uint32_t n_rows = 0, n_slots = 0, n_tiles = 0;
     int grid = 0;
     int64_t slack = 0;
-    DevBuf<uint32_t> dep_lo, dep_hi;
-    std::vector<uint32_t> h_lo, h_hi;
+    Sell own;               // sigma-order SELL (order 1)
+    const Sell* S = nullptr;
+    DevBuf<uint32_t> slot_row, pos;  // order 1
+    DevBuf<uint32_t> dep_ptr, dep_lo, dep_hi;
+    std::vector<uint32_t> h_ptr, h_lo, h_hi;
     std::map<int, DevBuf<uint32_t>> tickets;  // by p
-    DevBuf<uint32_t> done;
-    DevBuf<uint32_t> counter;
+    DevBuf<uint32_t> done, counter;
+    DevBuf<double> V;   // sigma-order working vectors (order 1)
+    DevBuf<double> zs;  // sigma-order polynomial accumulator (order 1)
 };
 
 struct FusedParams {
@@ -51,15 +61,22 @@ struct FusedParams {
     const double* vals;
     const uint64_t* chunk_off;
     const uint32_t* row_len;
+    const uint32_t* slot_row;  // nullptr: identity
     const uint32_t* tickets;
+    const uint32_t* dep_ptr;
     const uint32_t* dep_lo;
     const uint32_t* dep_hi;
     uint32_t* done;
     uint32_t* counter;
     uint32_t n_tickets;
     uint32_t n_rows;
-    uint64_t rows;  // slice stride
-    double* block;
+    uint32_t n_slots;
+    uint32_t p;
+    uint64_t vstride;  // stride of V slices
+    double* V;         // working vectors (== out when identity)
+    uint64_t rows;     // stride of the caller's block
+    double* out;
+    double* zs;
     double* z;
     double shift_a[kMaxFusedP];
     double shift_b2[kMaxFusedP];
@@ -77,26 +94,53 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void k_dep_init(uint32_t* lo, uint32_t* hi, uint32_t n_tiles) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_tiles;
-         t += (uint64_t)gridDim.x * blockDim.x)
-        lo[t] = hi[t] = (uint32_t)t;
+__device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
+    uint32_t lo = 0, hi = nl;  // largest l with lp[l] <= s
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (lp[mid] <= s)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
 }
 
-// Row r (== slot) of tile r/kTile reads columns [ci[rp[r]], ci[rp[r+1]-1]] (sorted rows).
-__global__ void k_dep_ranges(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-                             uint32_t n, uint32_t* lo, uint32_t* hi) {
-    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
-         r += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = rp[r], e = rp[r + 1];
-        if (b == e) continue;
-        const uint32_t t = (uint32_t)(r / kTile);
-        atomicMin(lo + t, ci[b] / kTile);
-        atomicMax(hi + t, ci[e - 1] / kTile);
+// Per tile and per neighbouring level bucket (level of the tile's first slot - 1 .. +2), the
+// min / max sigma slot of any column read by the tile's rows.
+__global__ void k_dep_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                              uint32_t n, const uint32_t* __restrict__ slot_row,
+                              const uint32_t* __restrict__ pos, const uint32_t* __restrict__ lp,
+                              uint32_t nl, uint32_t* __restrict__ bmin, uint32_t* __restrict__ bmax) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = slot_row ? slot_row[s] : (uint32_t)s;
+        const uint32_t T = (uint32_t)(s / kTile);
+        const uint32_t lt = level_of(lp, nl, T * kTile);
+        const uint32_t L = level_of(lp, nl, (uint32_t)s);
+        const uint32_t lb = lp[L], le = lp[L + 1];
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const uint32_t c = ci[k];
+            const uint32_t lc = c < lb ? L - 1 : (c >= le ? L + 1 : L);
+            int b = (int)lc - (int)lt + 1;
+            b = b < 0 ? 0 : (b >= kBuckets ? kBuckets - 1 : b);
+            const uint32_t sc = pos ? pos[c] : c;
+            atomicMin(bmin + (uint64_t)T * kBuckets + b, sc);
+            atomicMax(bmax + (uint64_t)T * kBuckets + b, sc);
+        }
     }
 }
 
-template <int KIND>  // 0 plain, 1 shifted (Newton), 2 polynomial
+__global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restrict__ slot_row,
+                           uint32_t n_slots, uint32_t n, double* __restrict__ xs) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = slot_row[s];
+        xs[s] = r < n ? x[r] : 0.0;
+    }
+}
+
+template <int KIND, bool SIGMA>  // KIND 0 plain, 1 shifted (Newton), 2 polynomial
 __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ FusedParams P) {
     __shared__ uint32_t s_ticket;
     const uint32_t tid = threadIdx.x;
@@ -109,43 +153,49 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
         const uint32_t T = code & 0xffffffu;
         const uint32_t q = code >> 24;
         if (q > 1) {
-            const uint32_t lo = P.dep_lo[T], hi = P.dep_hi[T];
+            const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
             for (;;) {
                 int ok = 1;
-                for (uint32_t u = lo + tid; u <= hi; u += kTile)
-                    if (ld_acquire(P.done + u) < q - 1) {
-                        ok = 0;
-                        break;
-                    }
+                for (uint32_t run = r0; run < r1 && ok; ++run) {
+                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
+                    for (uint32_t u = lo + tid; u <= hi; u += kTile)
+                        if (ld_acquire(P.done + u) < q - 1) {
+                            ok = 0;
+                            break;
+                        }
+                }
                 if (__syncthreads_and(ok)) break;
                 __nanosleep(32);
             }
         }
         const uint32_t s = T * kTile + tid;
-        if (s < P.n_rows) {
+        const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+        if (r < P.n_rows) {
             const uint32_t len = P.row_len[s];
             const uint64_t c = s >> 5;
             const uint64_t off = P.chunk_off[c];
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
-            const double* src = P.block + (uint64_t)(q - 1) * P.rows;
+            const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
             double acc = q == 1
                              ? sell_row_dot<true>(P.cols, P.vals, off, L, s & 31, len, src)
                              : sell_row_dot<false>(P.cols, P.vals, off, L, s & 31, len, src);
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
                 const double own = src[s];
-                const double own2 = b2 != 0.0 ? P.block[(uint64_t)(q - 2) * P.rows + s] : 0.0;
+                const double own2 = b2 != 0.0 ? P.V[(uint64_t)(q - 2) * P.vstride + s] : 0.0;
                 acc = shift_epilogue(acc, a, b2, own, own2);
             }
-            P.block[(uint64_t)q * P.rows + s] = acc;
+            P.V[(uint64_t)q * P.vstride + s] = acc;
+            if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
             if constexpr (KIND == 2) {
                 // z = c0*y0 + c1*y1 (+ c2*y2 ...), ascending k, mul then add.
                 double zr;
                 if (q == 1)
                     zr = __dadd_rn(__dmul_rn(P.coef[0], src[s]), __dmul_rn(P.coef[1], acc));
                 else
-                    zr = __dadd_rn(P.z[s], __dmul_rn(P.coef[q], acc));
-                P.z[s] = zr;
+                    zr = __dadd_rn(P.zs[s], __dmul_rn(P.coef[q], acc));
+                P.zs[s] = zr;
+                if (SIGMA && q == P.p) P.z[r] = zr;
             }
         }
         __syncthreads();
@@ -168,40 +218,94 @@ struct RangeMax {
     }
     int64_t query(uint32_t lo, uint32_t hi) const {  // inclusive
         const uint32_t len = hi - lo + 1;
-        int k = 31 - __builtin_clz(len);
+        const int k = 31 - __builtin_clz(len);
         return std::max(t[k][lo], t[k][hi - (1u << k) + 1]);
     }
 };
 
-Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
-    if (P->exec && P->exec_csr == A) return *P->exec;
-    auto E = std::make_shared<Executor>();
-    Sell& S = csr_sell(A);
-    cudaStream_t st = ctx->stream;
-    E->n_slots = S.n_slots;
-    E->n_tiles = (A->n_rows + kTile - 1) / kTile;
+template <class K>
+int occupancy(K kernel) {
     int occ = 0;
-    MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0>, kTile, 0));
-    E->grid = std::max(1, occ) * ctx->sm_count;
-    E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
-    E->dep_lo.alloc(E->n_tiles);
-    E->dep_hi.alloc(E->n_tiles);
-    if (E->n_tiles) {
-        k_dep_init<<<grid_for(E->n_tiles, 256), 256, 0, st>>>(E->dep_lo.p, E->dep_hi.p, E->n_tiles);
-        k_dep_ranges<<<grid_for(A->n_rows, 256), 256, 0, st>>>(A->row_ptr.p, A->col_idx.p,
-                                                              A->n_rows, E->dep_lo.p, E->dep_hi.p);
-        MPKG_LAUNCH_CHECK();
-        ctx->launches += 2;
-        E->h_lo.resize(E->n_tiles);
-        E->h_hi.resize(E->n_tiles);
-        MPKG_CUDA(cudaMemcpyAsync(E->h_lo.data(), E->dep_lo.p, sizeof(uint32_t) * E->n_tiles,
-                                  cudaMemcpyDeviceToHost, st));
-        MPKG_CUDA(cudaMemcpyAsync(E->h_hi.data(), E->dep_hi.p, sizeof(uint32_t) * E->n_tiles,
-                                  cudaMemcpyDeviceToHost, st));
-        MPKG_CUDA(cudaStreamSynchronize(st));
+    MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTile, 0));
+    return std::max(1, occ);
+}
+
+Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
+    if (P->exec && P->exec_csr == A && P->exec->order == (int)ctx->order) return *P->exec;
+    auto E = std::make_shared<Executor>();
+    cudaStream_t st = ctx->stream;
+    E->order = ctx->order == 0 ? 0 : 1;
+    E->n_rows = A->n_rows;
+    E->n_slots = (A->n_rows + 31u) & ~31u;
+    E->n_tiles = (A->n_rows + kTile - 1) / kTile;
+    if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
+    if (E->order == 1) {
+        gpu_level_cm_order(ctx, A, P->level_ptr, E->n_slots, E->slot_row, E->pos);
+        build_sell(ctx, A, E->slot_row.p, E->pos.p, E->own);
+        E->S = &E->own;
+    } else {
+        E->S = &csr_sell(A);
     }
-    E->done.alloc(std::max<uint32_t>(E->n_tiles, 1));
+    E->grid = occupancy(k_mpk_fused<0, true>) * ctx->sm_count;
+    E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
+    // dependency runs
+    const uint32_t nt = E->n_tiles;
+    std::vector<uint32_t> lp = P->level_ptr;
+    if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
+    const uint32_t nl = (uint32_t)lp.size() - 1;
+    DevBuf<uint32_t> d_lp(lp.size()), bmin((uint64_t)nt * kBuckets), bmax((uint64_t)nt * kBuckets);
+    MPKG_CUDA(cudaMemcpyAsync(d_lp.p, lp.data(), 4 * lp.size(), cudaMemcpyHostToDevice, st));
+    MPKG_CUDA(cudaMemsetAsync(bmin.p, 0xff, bmin.bytes(), st));
+    MPKG_CUDA(cudaMemsetAsync(bmax.p, 0, bmax.bytes(), st));
+    if (nt) {
+        k_dep_buckets<<<grid_for(A->n_rows, 256), 256, 0, st>>>(
+            A->row_ptr.p, A->col_idx.p, A->n_rows, E->order ? E->slot_row.p : nullptr,
+            E->order ? E->pos.p : nullptr, d_lp.p, nl, bmin.p, bmax.p);
+        MPKG_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    std::vector<uint32_t> hmin((uint64_t)nt * kBuckets), hmax((uint64_t)nt * kBuckets);
+    MPKG_CUDA(cudaMemcpyAsync(hmin.data(), bmin.p, bmin.bytes(), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaMemcpyAsync(hmax.data(), bmax.p, bmax.bytes(), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaStreamSynchronize(st));
+    E->h_ptr.assign(nt + 1, 0);
+    E->h_lo.clear();
+    E->h_hi.clear();
+    std::vector<std::pair<uint32_t, uint32_t>> runs;
+    for (uint32_t T = 0; T < nt; ++T) {
+        runs.clear();
+        runs.push_back({T, T});
+        for (int b = 0; b < kBuckets; ++b) {
+            const uint64_t i = (uint64_t)T * kBuckets + b;
+            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i] / kTile, hmax[i] / kTile});
+        }
+        std::sort(runs.begin(), runs.end());
+        uint32_t lo = runs[0].first, hi = runs[0].second;
+        for (size_t k = 1; k < runs.size(); ++k) {
+            if (runs[k].first <= hi + 1) {
+                hi = std::max(hi, runs[k].second);
+            } else {
+                E->h_lo.push_back(lo);
+                E->h_hi.push_back(hi);
+                lo = runs[k].first;
+                hi = runs[k].second;
+            }
+        }
+        E->h_lo.push_back(lo);
+        E->h_hi.push_back(hi);
+        E->h_ptr[T + 1] = (uint32_t)E->h_lo.size();
+    }
+    E->dep_ptr.alloc(nt + 1);
+    E->dep_lo.alloc(std::max<size_t>(E->h_lo.size(), 1));
+    E->dep_hi.alloc(std::max<size_t>(E->h_hi.size(), 1));
+    MPKG_CUDA(cudaMemcpyAsync(E->dep_ptr.p, E->h_ptr.data(), 4ull * (nt + 1), cudaMemcpyHostToDevice, st));
+    if (!E->h_lo.empty()) {
+        MPKG_CUDA(cudaMemcpyAsync(E->dep_lo.p, E->h_lo.data(), 4 * E->h_lo.size(), cudaMemcpyHostToDevice, st));
+        MPKG_CUDA(cudaMemcpyAsync(E->dep_hi.p, E->h_hi.data(), 4 * E->h_hi.size(), cudaMemcpyHostToDevice, st));
+    }
+    E->done.alloc(std::max<uint32_t>(nt, 1));
     E->counter.alloc(1);
+    MPKG_CUDA(cudaStreamSynchronize(st));
     P->exec = E;
     P->exec_csr = A;
     return *E;
@@ -211,7 +315,6 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     auto it = E.tickets.find(p);
     if (it != E.tickets.end()) return it->second;
     const uint32_t nt = E.n_tiles;
-    if (nt >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
     // List schedule: ready time of (T, q).
     std::vector<int64_t> r(nt), rn(nt);
     std::vector<uint64_t> keys;
@@ -220,8 +323,12 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     for (int q = 1; q <= p; ++q) {
         if (q > 1) {
             RangeMax rm(r);
-            for (uint32_t T = 0; T < nt; ++T)
-                rn[T] = std::max(r[T] + 1, rm.query(E.h_lo[T], E.h_hi[T]) + E.slack);
+            for (uint32_t T = 0; T < nt; ++T) {
+                int64_t m = r[T] + 1;
+                for (uint32_t k = E.h_ptr[T]; k < E.h_ptr[T + 1]; ++k)
+                    m = std::max(m, rm.query(E.h_lo[k], E.h_hi[k]) + E.slack);
+                rn[T] = m;
+            }
             r.swap(rn);
         }
         for (uint32_t T = 0; T < nt; ++T)
@@ -234,8 +341,15 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     MPKG_CUDA(cudaMemcpyAsync(d.p, codes.data(), sizeof(uint32_t) * codes.size(),
                               cudaMemcpyHostToDevice, ctx->stream));
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
-    (void)ctx;
     return E.tickets.emplace(p, std::move(d)).first->second;
+}
+
+template <int KIND>
+void launch_kind(bool sigma, int grid, cudaStream_t st, const FusedParams& P) {
+    if (sigma)
+        k_mpk_fused<KIND, true><<<grid, kTile, 0, st>>>(P);
+    else
+        k_mpk_fused<KIND, false><<<grid, kTile, 0, st>>>(P);
 }
 
 }  // namespace
@@ -245,23 +359,45 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     Executor& E = get_executor(ctx, Pl, A);
     if (E.n_tiles == 0) return;
     const DevBuf<uint32_t>& tk = get_tickets(ctx, E, a.p);
-    Sell& S = csr_sell(A);
+    const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
+    const bool sigma = E.order == 1;
     FusedParams P{};
     P.cols = S.cols.p;
     P.vals = S.vals.p;
     P.chunk_off = S.chunk_off.p;
     P.row_len = S.row_len.p;
+    P.slot_row = sigma ? E.slot_row.p : nullptr;
     P.tickets = tk.p;
+    P.dep_ptr = E.dep_ptr.p;
     P.dep_lo = E.dep_lo.p;
     P.dep_hi = E.dep_hi.p;
     P.done = E.done.p;
     P.counter = E.counter.p;
     P.n_tickets = (uint32_t)tk.n;
     P.n_rows = A->n_rows;
+    P.n_slots = E.n_slots;
+    P.p = (uint32_t)a.p;
     P.rows = a.rows;
-    P.block = a.block;
+    P.out = a.block;
     P.z = a.z;
+    if (sigma) {
+        E.V.ensure((uint64_t)E.n_slots * (a.p + 1));
+        P.V = E.V.p;
+        P.vstride = E.n_slots;
+        if (a.kind == 2) {
+            E.zs.ensure(E.n_slots);
+            P.zs = E.zs.p;
+        }
+        k_gather_x<<<grid_for(E.n_slots, 256), 256, 0, st>>>(a.block, E.slot_row.p, E.n_slots,
+                                                             A->n_rows, E.V.p);
+        MPKG_LAUNCH_CHECK();
+        ctx->launches += 1;
+    } else {
+        P.V = a.block;
+        P.vstride = a.rows;
+        P.zs = a.z;
+    }
     for (int i = 0; i < a.p; ++i) {
         P.shift_a[i] = a.shift_a ? a.shift_a[i] : 0.0;
         P.shift_b2[i] = a.shift_b2 ? a.shift_b2[i] : 0.0;
@@ -271,9 +407,9 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     const auto ev = timing_begin(ctx);
     switch (a.kind) {
-        case 0: k_mpk_fused<0><<<E.grid, kTile, 0, st>>>(P); break;
-        case 1: k_mpk_fused<1><<<E.grid, kTile, 0, st>>>(P); break;
-        default: k_mpk_fused<2><<<E.grid, kTile, 0, st>>>(P); break;
+        case 0: launch_kind<0>(sigma, E.grid, st, P); break;
+        case 1: launch_kind<1>(sigma, E.grid, st, P); break;
+        default: launch_kind<2>(sigma, E.grid, st, P); break;
     }
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);
@@ -286,7 +422,7 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
     if (P->exec) {
         t = P->exec->n_tiles;
         for (const auto& kv : P->exec->tickets) k = std::max<uint64_t>(k, kv.second.n);
-        for (uint32_t i = 0; i < t; ++i) d += P->exec->h_hi[i] - P->exec->h_lo[i] + 1;
+        for (size_t i = 0; i < P->exec->h_lo.size(); ++i) d += P->exec->h_hi[i] - P->exec->h_lo[i] + 1;
     }
     if (n_tiles) *n_tiles = t;
     if (n_tickets) *n_tickets = k;

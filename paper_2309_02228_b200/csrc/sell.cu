@@ -37,7 +37,8 @@ __global__ void k_sell_fill(const uint32_t* __restrict__ rp, const uint32_t* __r
                             const uint32_t* __restrict__ slot_row,
                             const uint64_t* __restrict__ chunk_off,
                             const uint32_t* __restrict__ row_len, uint32_t n_slots,
-                            uint32_t* __restrict__ cols, double* __restrict__ vals) {
+                            const uint32_t* __restrict__ col_map, uint32_t* __restrict__ cols,
+                            double* __restrict__ vals) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t len = row_len[s];
@@ -54,7 +55,7 @@ __global__ void k_sell_fill(const uint32_t* __restrict__ rp, const uint32_t* __r
                                        : off + Lq * 32ull + (k - Lq) * 32ull + lane;
             const uint64_t pv = k < Lp ? off + (k >> 1) * 64ull + lane * 2 + (k & 1)
                                        : off + Lp * 32ull + lane;
-            cols[pc] = ci[b + k];
+            cols[pc] = col_map ? col_map[ci[b + k]] : ci[b + k];
             vals[pv] = v[b + k];
         }
     }
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(256) k_spmv_sell(
 
 }  // namespace
 
-void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row, Sell& S) {
+void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row,
+                const uint32_t* d_col_map, Sell& S) {
     cudaStream_t st = ctx->stream;
     S.n_rows = A->n_rows;
     S.n_slots = (A->n_rows + 31u) & ~31u;
@@ -126,7 +128,7 @@ void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row
     }
     k_sell_fill<<<grid_for(S.n_slots, 256), 256, 0, st>>>(
         A->row_ptr.p, A->col_idx.p, A->values.p, A->n_rows, d_slot_row, S.chunk_off.p,
-        S.row_len.p, S.n_slots, S.cols.p, S.vals.p);
+        S.row_len.p, S.n_slots, d_col_map, S.cols.p, S.vals.p);
     MPKG_LAUNCH_CHECK();
     ctx->launches += 3;
 }
@@ -134,7 +136,7 @@ void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row
 Sell& csr_sell(mpkg_csr_s* A) {
     if (!A->sell) {
         auto S = std::make_unique<Sell>();
-        build_sell(A->ctx, A, nullptr, *S);
+        build_sell(A->ctx, A, nullptr, nullptr, *S);
         A->sell = std::move(S);
     }
     return *A->sell;

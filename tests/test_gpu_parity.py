@@ -169,6 +169,34 @@ def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
         assert_bitwise(ctx.baseline_mpk(Ap, x, 8).as_matrix(), ref8, f"{name} baseline")
 
 
+@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("slack", [0, 1, 7, -1])
+def test_fused_orders_and_schedules(ctx, cases, oracle, order, slack):
+    """Every executor order (identity / Cuthill-McKee inside levels) and ticket schedule gives
+    the same bits: the schedule changes only which tiles run concurrently."""
+    try:
+        ctx.set_param("order", order)
+        ctx.set_param("slack", slack)
+        for name in ("stencil27_scrambled_20", "random_csr_2000", "rmat_12", "poisson2d_256"):
+            c = cases[name]
+            P = c["P"]
+            Ap = ctx.csr(P)
+            ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+            x = mpkg.random_vector(P.n_rows, 9)
+            plan = ctx.group_levels(ls, Ap, 1 << 20, 6)
+            ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 6)
+            assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} order={order}")
+            sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0, 3.0, 0.25]
+            ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+            assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, f"{name} shifted")
+            coef = np.linspace(-1, 1, 7)
+            zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+            assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, f"{name} poly")
+    finally:
+        ctx.set_param("order", 1)
+        ctx.set_param("slack", -1)
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
