@@ -285,6 +285,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slack", type=int, default=-1)
     ap.add_argument("--order", type=int, default=1, help="0: A_perm order, 1: CM inside levels")
+    ap.add_argument("--pass-powers", type=int, default=0, help="force powers per fused pass")
+    ap.add_argument("--l2-budget", type=int, default=0, help="live-window bytes (0: L2/2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
@@ -307,6 +309,8 @@ def main():
     if args.slack >= 0:
         ctx.set_param("slack", args.slack)
     ctx.set_param("order", args.order)
+    ctx.set_param("pass", args.pass_powers)
+    ctx.set_param("l2_budget", args.l2_budget)
     info = ctx.device_info()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 

@@ -66,8 +66,10 @@ int mpkg_ctx_set_mode(mpkg_ctx_t ctx, int mode);
 /* Device facts the planner uses: SM count, L2 bytes, max persisting-L2 bytes. */
 int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t* persist_max);
 /* Executor tuning knobs: "slack" (tickets between a dependency and its
- * consumer in the list schedule), "order", "tile_rows"; "kernel_timing" = 1 records a CUDA
- * event pair around every power-kernel launch on the context stream. */
+ * consumer in the list schedule; -1 = auto), "order" (0: A_perm order, 1: Cuthill-McKee inside
+ * levels), "pass" (force powers per fused pass; 0 = auto from the L2 budget), "l2_budget" (live
+ * window bytes; 0 = L2/2), "tile_rows" (fixed 256); "kernel_timing" = 1 records a CUDA event
+ * pair around every power-kernel launch on the context stream. */
 int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value);
 /* Reads (and clears) the event pairs recorded with "kernel_timing": sum, count and max of the
  * per-launch device durations in milliseconds.  Synchronises on the recorded events. */
@@ -137,7 +139,7 @@ int mpkg_plan_destroy(mpkg_plan_t P);
 /* Executor statistics for the GPU schedule attached to a plan (after the first mpkg_mpk):
  * tiles, tickets, dependency ranges. */
 int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets,
-                        uint64_t* n_dep_ranges);
+                        uint64_t* n_dep_tiles, uint32_t* pass_powers);
 
 /* execute.hpp:59-72 wavefront_schedule (pure host function; arrays hold n_groups*stages). */
 int mpkg_wavefront_schedule(uint32_t n_groups, int stages, uint32_t* group, int* stage,

@@ -52,7 +52,7 @@ _SIGS = {
     "mpkg_plan_info": [P, pint, pint, pu32, pu64, pu64, pu32],
     "mpkg_plan_get": [P, P, P, P],
     "mpkg_plan_destroy": [P],
-    "mpkg_plan_exec_info": [P, pu32, pu64, pu64],
+    "mpkg_plan_exec_info": [P, pu32, pu64, pu64, pu32],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],
     "mpkg_baseline_mpk": [P, P, P, i32, P, u64, u64],
     "mpkg_baseline_mpk_dev": [P, P, P, i32, P, u64, u64],

@@ -282,9 +282,10 @@ class ExecutionPlan:
         return len(self.group_rows) - 1
 
     def exec_info(self) -> dict:
-        t, k, d = C.c_uint32(), C.c_uint64(), C.c_uint64()
-        check(lib.mpkg_plan_exec_info(self.h, C.byref(t), C.byref(k), C.byref(d)))
-        return {"tiles": t.value, "tickets": k.value, "dep_tiles": d.value}
+        t, k, d, pp = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
+        check(lib.mpkg_plan_exec_info(self.h, C.byref(t), C.byref(k), C.byref(d), C.byref(pp)))
+        return {"tiles": t.value, "tickets": k.value, "dep_tiles": d.value,
+                "pass_powers": pp.value}
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -251,6 +251,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->slack = value;
         else if (k == "order")
             ctx->order = value;
+        else if (k == "pass")
+            ctx->pass_powers = value;
+        else if (k == "l2_budget")
+            ctx->l2_budget = value;
         else if (k == "kernel_timing")
             ctx->kernel_timing = value != 0;
         else if (k == "tile_rows")
@@ -629,10 +633,11 @@ int mpkg_plan_destroy(mpkg_plan_t P) {
     return MPKG_OK;
 }
 
-int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps) {
+int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
+                        uint32_t* pass_powers) {
     return guarded([&] {
         require(P != nullptr, "plan_exec_info: null plan");
-        exec_info(P, n_tiles, n_tickets, n_deps);
+        exec_info(P, n_tiles, n_tickets, n_deps, pass_powers);
     });
 }
 

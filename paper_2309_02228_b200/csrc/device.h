@@ -94,7 +94,9 @@ struct mpkg_ctx_s {
     // executor knobs (mpkg_ctx_set_param)
     int64_t tile_rows = 256;
     int64_t slack = -1;  // -1: resident CTA count
-    int64_t order = 1;   // 0: reference wavefront of the plan's groups, 1: list schedule
+    int64_t order = 1;        // 0: A_perm order, 1: Cuthill-McKee inside levels
+    int64_t pass_powers = 0;  // >0: force powers per fused pass
+    int64_t l2_budget = 0;    // >0: live-window budget in bytes (default L2/2)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;
@@ -193,6 +195,7 @@ struct FusedArgs {
     double* z = nullptr;
 };
 void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& a);
-void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps);
+void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
+               uint32_t* pass_powers);
 
 }  // namespace mpkg_detail

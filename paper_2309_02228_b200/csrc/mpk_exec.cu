@@ -26,6 +26,7 @@
 // Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
 // every row is computed by the same formula, from the same inputs, in any order.
 #include <algorithm>
+#include <array>
 #include <map>
 #include <numeric>
 #include <parallel/algorithm>
@@ -51,6 +52,9 @@ struct Executor {
     DevBuf<uint32_t> dep_ptr, dep_lo, dep_hi;
     std::vector<uint32_t> h_ptr, h_lo, h_hi;
     std::map<int, DevBuf<uint32_t>> tickets;  // by p
+    std::map<int, int> pass_len;              // powers per pass, by p
+    std::vector<uint64_t> tile_bytes;         // matrix + vector bytes one tile-power touches
+    std::array<int64_t, 3> knobs{};           // slack, pass, l2_budget the schedule was built for
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
     DevBuf<double> zs;  // sigma-order polynomial accumulator (order 1)
@@ -231,8 +235,18 @@ int occupancy(K kernel) {
 }
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
-    if (P->exec && P->exec_csr == A && P->exec->order == (int)ctx->order) return *P->exec;
+    if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1)) {
+        Executor& E = *P->exec;
+        if (E.knobs[0] != ctx->slack || E.knobs[1] != ctx->pass_powers || E.knobs[2] != ctx->l2_budget) {
+            E.tickets.clear();  // schedule knobs changed: re-plan the ticket order
+            E.pass_len.clear();
+            E.slack = ctx->slack >= 0 ? ctx->slack : std::max(1, E.grid / 16);
+            E.knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget};
+        }
+        return E;
+    }
     auto E = std::make_shared<Executor>();
+    E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget};
     cudaStream_t st = ctx->stream;
     E->order = ctx->order == 0 ? 0 : 1;
     E->n_rows = A->n_rows;
@@ -247,7 +261,15 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->S = &csr_sell(A);
     }
     E->grid = occupancy(k_mpk_fused<0, true>) * ctx->sm_count;
-    E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
+    E->slack = ctx->slack >= 0 ? ctx->slack : std::max(1, E->grid / 16);
+    {  // per-tile bytes from the SELL chunk offsets (padded entries are fetched too)
+        std::vector<uint64_t> off(E->S->n_chunks + 1);
+        MPKG_CUDA(cudaMemcpyAsync(off.data(), E->S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
+        MPKG_CUDA(cudaStreamSynchronize(st));
+        E->tile_bytes.assign(E->n_tiles, 0);
+        for (uint32_t c = 0; c < E->S->n_chunks; ++c)
+            E->tile_bytes[c / (kTile / 32)] += 12 * (off[c + 1] - off[c]) + 32 * 8 * 3;
+    }
     // dependency runs
     const uint32_t nt = E->n_tiles;
     std::vector<uint32_t> lp = P->level_ptr;
@@ -311,17 +333,13 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     return *E;
 }
 
-const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
-    auto it = E.tickets.find(p);
-    if (it != E.tickets.end()) return it->second;
+// One pass of the list schedule over powers q0..q1: keys (pass, ready time, q, tile), sorted.
+void pass_keys(const Executor& E, uint32_t pass, int q0, int q1, std::vector<uint64_t>& keys) {
     const uint32_t nt = E.n_tiles;
-    // List schedule: ready time of (T, q).
     std::vector<int64_t> r(nt), rn(nt);
-    std::vector<uint64_t> keys;
-    keys.reserve((uint64_t)nt * p);
     for (uint32_t T = 0; T < nt; ++T) r[T] = T;
-    for (int q = 1; q <= p; ++q) {
-        if (q > 1) {
+    for (int q = q0; q <= q1; ++q) {
+        if (q > q0) {
             RangeMax rm(r);
             for (uint32_t T = 0; T < nt; ++T) {
                 int64_t m = r[T] + 1;
@@ -332,8 +350,59 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
             r.swap(rn);
         }
         for (uint32_t T = 0; T < nt; ++T)
-            keys.push_back(((uint64_t)r[T] << 32) | ((uint64_t)q << 24) | T);
+            keys.push_back(((uint64_t)pass << 59) | ((uint64_t)r[T] << 32) | ((uint64_t)q << 24) | T);
     }
+}
+
+// Peak bytes of matrix + working vectors that one pass of P powers keeps live, measured on the
+// ticket order: tile T is live from its first to its last ticket of the pass.
+uint64_t pass_window_bytes(const Executor& E, int P) {
+    std::vector<uint64_t> keys;
+    keys.reserve((uint64_t)E.n_tiles * P);
+    pass_keys(E, 0, 1, P, keys);
+    __gnu_parallel::sort(keys.begin(), keys.end());
+    const uint32_t nt = E.n_tiles;
+    std::vector<int64_t> first(nt, -1), last(nt, -1);
+    for (size_t i = 0; i < keys.size(); ++i) {
+        const uint32_t T = (uint32_t)(keys[i] & 0xffffffu);
+        if (first[T] < 0) first[T] = (int64_t)i;
+        last[T] = (int64_t)i;
+    }
+    std::vector<int64_t> diff(keys.size() + 1, 0);
+    for (uint32_t T = 0; T < nt; ++T) {
+        const int64_t b = (int64_t)E.tile_bytes[T];
+        diff[first[T]] += b;
+        diff[last[T] + 1] -= b;
+    }
+    int64_t cur = 0, peak = 0;
+    for (size_t i = 0; i < keys.size(); ++i) peak = std::max(peak, cur += diff[i]);
+    return (uint64_t)peak;
+}
+
+const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
+    auto it = E.tickets.find(p);
+    if (it != E.tickets.end()) return it->second;
+    const uint32_t nt = E.n_tiles;
+    // Pass length: the largest P whose live window fits the L2 budget (the paper's p_opt
+    // slicing into ceil(p/P) consecutive MPKs, chosen here by simulating the
+    // schedule instead of by timing), unless forced with the "pass" knob.
+    int P = p;
+    if (ctx->pass_powers > 0) {
+        P = std::min<int>(p, (int)ctx->pass_powers);
+    } else {
+        const uint64_t budget = ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes / 2;
+        while (P > 1 && pass_window_bytes(E, P) > budget) --P;
+    }
+    const int n_pass = (p + P - 1) / P;
+    std::vector<uint64_t> keys;
+    keys.reserve((uint64_t)nt * p);
+    int q0 = 1;
+    for (int j = 0; j < n_pass; ++j) {
+        const int len = p / n_pass + (j < p % n_pass ? 1 : 0);  // balanced passes
+        pass_keys(E, (uint32_t)j, q0, q0 + len - 1, keys);
+        q0 += len;
+    }
+    E.pass_len[p] = P;
     __gnu_parallel::sort(keys.begin(), keys.end());
     std::vector<uint32_t> codes(keys.size());
     for (size_t i = 0; i < keys.size(); ++i) codes[i] = (uint32_t)(keys[i] & 0xffffffffu);
@@ -416,17 +485,20 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     ctx->launches += 1;
 }
 
-void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps) {
-    uint32_t t = 0;
+void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
+               uint32_t* pass_powers) {
+    uint32_t t = 0, pp = 0;
     uint64_t k = 0, d = 0;
     if (P->exec) {
         t = P->exec->n_tiles;
         for (const auto& kv : P->exec->tickets) k = std::max<uint64_t>(k, kv.second.n);
+        for (const auto& kv : P->exec->pass_len) pp = (uint32_t)kv.second;
         for (size_t i = 0; i < P->exec->h_lo.size(); ++i) d += P->exec->h_hi[i] - P->exec->h_lo[i] + 1;
     }
     if (n_tiles) *n_tiles = t;
     if (n_tickets) *n_tickets = k;
     if (n_deps) *n_deps = d;
+    if (pass_powers) *pass_powers = pp;
 }
 
 }  // namespace mpkg_detail
