@@ -94,6 +94,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -146,31 +151,42 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
 
 template <int KIND, bool SIGMA>  // KIND 0 plain, 1 shifted (Newton), 2 polynomial
 __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ FusedParams P) {
-    __shared__ uint32_t s_ticket;
+    // Double-buffered claims: the next ticket is claimed while this one runs.  Still
+    // deadlock-free: the lowest unfinished ticket can never be one that is merely claimed,
+    // because its holder is busy with a smaller (hence unfinished) ticket.
+    __shared__ uint32_t s_ticket[2];
     const uint32_t tid = threadIdx.x;
-    for (;;) {
-        if (tid == 0) s_ticket = atomicAdd(P.counter, 1u);
-        __syncthreads();
-        const uint32_t t = s_ticket;
+    if (tid == 0) s_ticket[0] = atomicAdd(P.counter, 1u);
+    __syncthreads();
+    for (uint32_t buf = 0;; buf ^= 1u) {
+        const uint32_t t = s_ticket[buf];
         if (t >= P.n_tickets) return;
+        if (tid == 0) s_ticket[buf ^ 1u] = atomicAdd(P.counter, 1u);
         const uint32_t code = P.tickets[t];
         const uint32_t T = code & 0xffffffu;
         const uint32_t q = code >> 24;
         if (q > 1) {
+            // Poll with relaxed loads (LDG.STRONG.GPU, no L1 invalidation), then acquire every
+            // observed flag once (flags are monotone): one CCTL.IVALL burst per ticket instead
+            // of one per poll, which would wipe the L1 of every co-resident CTA while spinning.
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
             for (;;) {
                 int ok = 1;
                 for (uint32_t run = r0; run < r1 && ok; ++run) {
                     const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
                     for (uint32_t u = lo + tid; u <= hi; u += kTile)
-                        if (ld_acquire(P.done + u) < q - 1) {
+                        if (ld_relaxed(P.done + u) < q - 1) {
                             ok = 0;
                             break;
                         }
                 }
                 if (__syncthreads_and(ok)) break;
-                __nanosleep(32);
+                __nanosleep(64);
             }
+            for (uint32_t run = r0; run < r1; ++run)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += kTile)
+                    (void)ld_acquire(P.done + u);
+            __syncthreads();
         }
         const uint32_t s = T * kTile + tid;
         const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
