@@ -8,21 +8,24 @@
 //     SELL-32 copy of A_perm in sigma order with columns relabelled to sigma slots and keeps the
 //     working vectors in sigma order, so 32 consecutive rows gather from a few cache lines;
 //     every result is also stored at its A_perm position in the caller's block;
-//   * the unit of work is a (tile, power) pair, a tile being 256 consecutive sigma slots (one
-//     thread per row, bitwise row formula: rowdot.cuh);
+//   * the unit of work is a (tile, power) ticket, a tile being 128 consecutive sigma slots (one
+//     thread per row, bitwise row formula: rowdot.cuh).  A tile's SELL slice is one contiguous
+//     range of the column and value arrays, so it is staged into shared memory with two 1D TMA
+//     bulk copies (cp.async.bulk + mbarrier, double buffered); the copy for the NEXT claimed
+//     ticket is issued before the current ticket waits for its dependencies, so the matrix
+//     stream overlaps dependency waits and compute.  L2 hints: evict_last while the tile will be
+//     re-read in this pass, evict_first on its last use;
 //   * dependencies are tile-granular and derived from the sparsity pattern: tile T at power q
 //     needs power q-1 finished on every tile holding a column of T's rows, recorded per
 //     neighbouring level as a few tile ranges ("runs").  This is the boundary-level refinement
 //     the reference leaves as future work, strictly finer than its
 //     whole-neighbour-group rule (execute.hpp:23-28);
-//   * a per-tile flag done[T] = last finished power is published with st.release.gpu and polled
-//     with ld.acquire.gpu (L1 invalidated: LDG.E.STRONG.GPU + CCTL.IVALL); no grid barrier;
-//   * tickets (tile, power) are claimed through one global atomic counter in a host-computed
-//     topological order (list schedule: power q of T is placed `slack` tickets after the latest
-//     of its power-(q-1) dependencies), so a CTA only waits on tickets claimed earlier by running
-//     CTAs: deadlock-free without any co-residency assumption;
-//   * the order keeps a narrow band of tiles active so each tile's matrix slice is re-read from
-//     L2, not HBM, for powers 2..p.
+//   * a per-tile flag done[T] = last finished power is published with st.release.gpu; waiters
+//     poll it with relaxed loads and acquire once; there is no grid-wide barrier;
+//   * tickets are claimed through one global atomic counter in a host-computed topological order
+//     (list schedule, powers sliced into passes whose live window fits the L2 budget), so a CTA
+//     only waits on tickets claimed earlier by running CTAs: deadlock-free without any
+//     co-residency assumption.
 // Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
 // every row is computed by the same formula, from the same inputs, in any order.
 #include <algorithm>
@@ -37,20 +40,27 @@
 
 namespace mpkg_detail {
 
-constexpr int kTile = 256;      // slots per tile == threads per CTA
-constexpr int kMaxFusedP = 32;  // powers per fused launch
-constexpr int kBuckets = 4;     // neighbouring-level buckets per tile
+constexpr int kTile = 128;               // slots per tile == threads per CTA
+constexpr int kChunksPerTile = kTile / 32;
+constexpr int kMaxFusedP = 32;           // powers per fused launch
+constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
+constexpr uint32_t kLastUse = 1u << 30;  // ticket flag: last use of the tile in its pass
+constexpr uint32_t kBig = 1u << 31;      // ticket flag: tile too large for the smem buffer
+constexpr uint32_t kMaxBufBytes = 96 * 1024;
 
 struct Executor {
     int order = 0;  // 0: A_perm order, 1: Cuthill-McKee inside levels
     uint32_t n_rows = 0, n_slots = 0, n_tiles = 0;
     int grid = 0;
     int64_t slack = 0;
-    Sell own;               // sigma-order SELL (order 1)
+    uint32_t buf_bytes = 0;  // one smem staging buffer (cols + vals of the largest tile)
+    Sell own;                // sigma-order SELL (order 1)
     const Sell* S = nullptr;
     DevBuf<uint32_t> slot_row, pos;  // order 1
     DevBuf<uint32_t> dep_ptr, dep_lo, dep_hi;
+    DevBuf<uint64_t> tile_off;  // entry offset of every tile (n_tiles + 1)
     std::vector<uint32_t> h_ptr, h_lo, h_hi;
+    std::vector<uint8_t> big;
     std::map<int, DevBuf<uint32_t>> tickets;  // by p
     std::map<int, int> pass_len;              // powers per pass, by p
     std::vector<uint64_t> tile_bytes;         // matrix + vector bytes one tile-power touches
@@ -64,6 +74,7 @@ struct FusedParams {
     const uint32_t* cols;
     const double* vals;
     const uint64_t* chunk_off;
+    const uint64_t* tile_off;
     const uint32_t* row_len;
     const uint32_t* slot_row;  // nullptr: identity
     const uint32_t* tickets;
@@ -76,6 +87,7 @@ struct FusedParams {
     uint32_t n_rows;
     uint32_t n_slots;
     uint32_t p;
+    uint32_t buf_bytes;
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -101,6 +113,52 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred P; mbarrier.try_wait.parity.shared.b64 P, [%1], %2; selp.u32 %0,1,0,P; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+}
+
+// Thread 0 only: stage one tile (cols then vals, each one contiguous range) into `buf`.
+__device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool last_use,
+                                         char* buf, uint64_t* bar) {
+    const uint64_t e0 = P.tile_off[T], e1 = P.tile_off[T + 1];
+    const uint32_t ne = (uint32_t)(e1 - e0);
+    const uint32_t cb = ne * 4u, vb = ne * 8u;
+    const uint32_t cb_pad = (cb + 127u) & ~127u;
+    uint64_t pol;
+    if (last_use)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    // order earlier generic-proxy reads of this buffer before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(cb + vb)
+                 : "memory");
+    if (ne) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf)),
+            "l"(P.cols + e0), "r"(cb), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf + cb_pad)),
+            "l"(P.vals + e0), "r"(vb), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+    }
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -151,24 +209,45 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
 
 template <int KIND, bool SIGMA>  // KIND 0 plain, 1 shifted (Newton), 2 polynomial
 __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ FusedParams P) {
-    // Double-buffered claims: the next ticket is claimed while this one runs.  Still
-    // deadlock-free: the lowest unfinished ticket can never be one that is merely claimed,
-    // because its holder is busy with a smaller (hence unfinished) ticket.
+    extern __shared__ __align__(128) char smem[];
+    __shared__ __align__(8) uint64_t bars[2];
+    // Double-buffered claims: the next ticket is claimed (and its tile staged) while this one
+    // runs.  Still deadlock-free: the lowest unfinished ticket can never be one that is merely
+    // claimed, because its holder is busy with a smaller (hence unfinished) ticket.
     __shared__ uint32_t s_ticket[2];
     const uint32_t tid = threadIdx.x;
-    if (tid == 0) s_ticket[0] = atomicAdd(P.counter, 1u);
+    if (tid == 0) {
+        mbar_init(&bars[0]);
+        mbar_init(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t t0 = atomicAdd(P.counter, 1u);
+        s_ticket[0] = t0;
+        if (t0 < P.n_tickets) {
+            const uint32_t c0 = P.tickets[t0];
+            if (!(c0 & kBig)) tma_tile(P, c0 & 0xffffffu, c0 & kLastUse, smem, &bars[0]);
+        }
+    }
     __syncthreads();
+    uint32_t phase0 = 0, phase1 = 0;
     for (uint32_t buf = 0;; buf ^= 1u) {
         const uint32_t t = s_ticket[buf];
         if (t >= P.n_tickets) return;
-        if (tid == 0) s_ticket[buf ^ 1u] = atomicAdd(P.counter, 1u);
         const uint32_t code = P.tickets[t];
         const uint32_t T = code & 0xffffffu;
-        const uint32_t q = code >> 24;
+        const uint32_t q = (code >> 24) & 63u;
+        if (tid == 0) {
+            const uint32_t t2 = atomicAdd(P.counter, 1u);
+            s_ticket[buf ^ 1u] = t2;
+            if (t2 < P.n_tickets) {
+                const uint32_t c2 = P.tickets[t2];
+                if (!(c2 & kBig))
+                    tma_tile(P, c2 & 0xffffffu, c2 & kLastUse, smem + (buf ^ 1u) * P.buf_bytes,
+                             &bars[buf ^ 1u]);
+            }
+        }
         if (q > 1) {
-            // Poll with relaxed loads (LDG.STRONG.GPU, no L1 invalidation), then acquire every
-            // observed flag once (flags are monotone): one CCTL.IVALL burst per ticket instead
-            // of one per poll, which would wipe the L1 of every co-resident CTA while spinning.
+            // Poll with relaxed loads (no L1 invalidation), then acquire each observed flag
+            // once (flags are monotone).
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
             for (;;) {
                 int ok = 1;
@@ -186,8 +265,18 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
             for (uint32_t run = r0; run < r1; ++run)
                 for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += kTile)
                     (void)ld_acquire(P.done + u);
-            __syncthreads();
         }
+        const bool big = code & kBig;
+        if (!big) {
+            if (buf == 0) {
+                mbar_wait(&bars[0], phase0);
+                phase0 ^= 1u;
+            } else {
+                mbar_wait(&bars[1], phase1);
+                phase1 ^= 1u;
+            }
+        }
+        __syncthreads();
         const uint32_t s = T * kTile + tid;
         const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
         if (r < P.n_rows) {
@@ -196,9 +285,21 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
             const uint64_t off = P.chunk_off[c];
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
             const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
-            double acc = q == 1
-                             ? sell_row_dot<true>(P.cols, P.vals, off, L, s & 31, len, src)
+            double acc;
+            if (!big) {
+                const char* b = smem + buf * P.buf_bytes;
+                const uint64_t e0 = P.tile_off[T];
+                const uint32_t ne = (uint32_t)(P.tile_off[T + 1] - e0);
+                const uint32_t cb_pad = (ne * 4u + 127u) & ~127u;
+                const uint32_t* cs = reinterpret_cast<const uint32_t*>(b);
+                const double* vs = reinterpret_cast<const double*>(b + cb_pad);
+                const uint32_t rel = (uint32_t)(off - e0);
+                acc = q == 1 ? sell_row_dot_smem<true>(cs, vs, rel, L, s & 31, len, src)
+                             : sell_row_dot_smem<false>(cs, vs, rel, L, s & 31, len, src);
+            } else {
+                acc = q == 1 ? sell_row_dot<true>(P.cols, P.vals, off, L, s & 31, len, src)
                              : sell_row_dot<false>(P.cols, P.vals, off, L, s & 31, len, src);
+            }
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
                 const double own = src[s];
@@ -243,11 +344,12 @@ struct RangeMax {
     }
 };
 
-template <class K>
-int occupancy(K kernel) {
-    int occ = 0;
-    MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTile, 0));
-    return std::max(1, occ);
+void configure_kernels(uint32_t smem_bytes) {
+    const void* ks[] = {(const void*)k_mpk_fused<0, false>, (const void*)k_mpk_fused<0, true>,
+                        (const void*)k_mpk_fused<1, false>, (const void*)k_mpk_fused<1, true>,
+                        (const void*)k_mpk_fused<2, false>, (const void*)k_mpk_fused<2, true>};
+    for (const void* k : ks)
+        MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
 }
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
@@ -256,7 +358,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         if (E.knobs[0] != ctx->slack || E.knobs[1] != ctx->pass_powers || E.knobs[2] != ctx->l2_budget) {
             E.tickets.clear();  // schedule knobs changed: re-plan the ticket order
             E.pass_len.clear();
-            E.slack = ctx->slack >= 0 ? ctx->slack : std::max(1, E.grid / 16);
+            E.slack = ctx->slack >= 0 ? ctx->slack : E.grid;
             E.knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget};
         }
         return E;
@@ -276,18 +378,37 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     } else {
         E->S = &csr_sell(A);
     }
-    E->grid = occupancy(k_mpk_fused<0, true>) * ctx->sm_count;
-    E->slack = ctx->slack >= 0 ? ctx->slack : std::max(1, E->grid / 16);
-    {  // per-tile bytes from the SELL chunk offsets (padded entries are fetched too)
+    const uint32_t nt = E->n_tiles;
+    {  // tile extents in the SELL arrays; staging buffer size; oversized tiles
         std::vector<uint64_t> off(E->S->n_chunks + 1);
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E->S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
         MPKG_CUDA(cudaStreamSynchronize(st));
-        E->tile_bytes.assign(E->n_tiles, 0);
-        for (uint32_t c = 0; c < E->S->n_chunks; ++c)
-            E->tile_bytes[c / (kTile / 32)] += 12 * (off[c + 1] - off[c]) + 32 * 8 * 3;
+        std::vector<uint64_t> toff(nt + 1);
+        E->tile_bytes.assign(nt, 0);
+        E->big.assign(nt, 0);
+        uint64_t max_buf = 256;
+        for (uint32_t T = 0; T <= nt; ++T)
+            toff[T] = off[std::min<uint64_t>((uint64_t)T * kChunksPerTile, E->S->n_chunks)];
+        for (uint32_t T = 0; T < nt; ++T) {
+            const uint64_t ne = toff[T + 1] - toff[T];
+            const uint64_t bytes = ((4 * ne + 127) & ~127ull) + 8 * ne;
+            E->tile_bytes[T] = 12 * ne + kTile * 8 * 3;
+            if (bytes > kMaxBufBytes)
+                E->big[T] = 1;
+            else
+                max_buf = std::max(max_buf, bytes);
+        }
+        E->buf_bytes = (uint32_t)((max_buf + 127) & ~127ull);
+        E->tile_off.alloc(nt + 1);
+        MPKG_CUDA(cudaMemcpyAsync(E->tile_off.p, toff.data(), 8ull * (nt + 1), cudaMemcpyHostToDevice, st));
     }
+    const uint32_t smem = 2 * E->buf_bytes;
+    configure_kernels(smem);
+    int occ = 0;
+    MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true>, kTile, smem));
+    E->grid = std::max(1, occ) * ctx->sm_count;
+    E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
     // dependency runs
-    const uint32_t nt = E->n_tiles;
     std::vector<uint32_t> lp = P->level_ptr;
     if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
     const uint32_t nl = (uint32_t)lp.size() - 1;
@@ -349,7 +470,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     return *E;
 }
 
-// One pass of the list schedule over powers q0..q1: keys (pass, ready time, q, tile), sorted.
+// One pass of the list schedule over powers q0..q1: keys (pass, ready time, q, tile), unsorted.
 void pass_keys(const Executor& E, uint32_t pass, int q0, int q1, std::vector<uint64_t>& keys) {
     const uint32_t nt = E.n_tiles;
     std::vector<int64_t> r(nt), rn(nt);
@@ -360,13 +481,16 @@ void pass_keys(const Executor& E, uint32_t pass, int q0, int q1, std::vector<uin
             for (uint32_t T = 0; T < nt; ++T) {
                 int64_t m = r[T] + 1;
                 for (uint32_t k = E.h_ptr[T]; k < E.h_ptr[T + 1]; ++k)
-                    m = std::max(m, rm.query(E.h_lo[k], E.h_hi[k]) + E.slack);
+                    // strictly later than every dependency: keeps the order topological
+                    m = std::max(m, rm.query(E.h_lo[k], E.h_hi[k]) + std::max<int64_t>(E.slack, 1));
                 rn[T] = m;
             }
             r.swap(rn);
         }
+        const uint64_t last = q == q1 ? kLastUse : 0;
         for (uint32_t T = 0; T < nt; ++T)
-            keys.push_back(((uint64_t)pass << 59) | ((uint64_t)r[T] << 32) | ((uint64_t)q << 24) | T);
+            keys.push_back(((uint64_t)pass << 59) | ((uint64_t)r[T] << 32) |
+                           (last | (E.big[T] ? kBig : 0) | ((uint64_t)q << 24) | T));
     }
 }
 
@@ -406,7 +530,8 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     if (ctx->pass_powers > 0) {
         P = std::min<int>(p, (int)ctx->pass_powers);
     } else {
-        const uint64_t budget = ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes / 2;
+        const uint64_t budget =
+            ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes * 6 / 10;
         while (P > 1 && pass_window_bytes(E, P) > budget) --P;
     }
     const int n_pass = (p + P - 1) / P;
@@ -418,7 +543,7 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
         pass_keys(E, (uint32_t)j, q0, q0 + len - 1, keys);
         q0 += len;
     }
-    E.pass_len[p] = P;
+    E.pass_len[p] = (p + n_pass - 1) / n_pass;
     __gnu_parallel::sort(keys.begin(), keys.end());
     std::vector<uint32_t> codes(keys.size());
     for (size_t i = 0; i < keys.size(); ++i) codes[i] = (uint32_t)(keys[i] & 0xffffffffu);
@@ -430,11 +555,11 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
 }
 
 template <int KIND>
-void launch_kind(bool sigma, int grid, cudaStream_t st, const FusedParams& P) {
+void launch_kind(bool sigma, int grid, uint32_t smem, cudaStream_t st, const FusedParams& P) {
     if (sigma)
-        k_mpk_fused<KIND, true><<<grid, kTile, 0, st>>>(P);
+        k_mpk_fused<KIND, true><<<grid, kTile, smem, st>>>(P);
     else
-        k_mpk_fused<KIND, false><<<grid, kTile, 0, st>>>(P);
+        k_mpk_fused<KIND, false><<<grid, kTile, smem, st>>>(P);
 }
 
 }  // namespace
@@ -451,6 +576,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.cols = S.cols.p;
     P.vals = S.vals.p;
     P.chunk_off = S.chunk_off.p;
+    P.tile_off = E.tile_off.p;
     P.row_len = S.row_len.p;
     P.slot_row = sigma ? E.slot_row.p : nullptr;
     P.tickets = tk.p;
@@ -463,6 +589,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.n_rows = A->n_rows;
     P.n_slots = E.n_slots;
     P.p = (uint32_t)a.p;
+    P.buf_bytes = E.buf_bytes;
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
@@ -490,11 +617,12 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     for (int i = 0; i <= a.p; ++i) P.coef[i] = a.coef ? a.coef[i] : 0.0;
     MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
+    const uint32_t smem = 2 * E.buf_bytes;
     const auto ev = timing_begin(ctx);
     switch (a.kind) {
-        case 0: launch_kind<0>(sigma, E.grid, st, P); break;
-        case 1: launch_kind<1>(sigma, E.grid, st, P); break;
-        default: launch_kind<2>(sigma, E.grid, st, P); break;
+        case 0: launch_kind<0>(sigma, E.grid, smem, st, P); break;
+        case 1: launch_kind<1>(sigma, E.grid, smem, st, P); break;
+        default: launch_kind<2>(sigma, E.grid, smem, st, P); break;
     }
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);

@@ -100,6 +100,43 @@ __device__ __forceinline__ double sell_row_dot(const uint32_t* __restrict__ cols
     return acc;
 }
 
+// Same formula over a tile staged in shared memory by TMA (identical SELL layout, offsets
+// relative to the tile start).  Gathers go through L1 (see ld_vec).
+template <bool READONLY>
+__device__ __forceinline__ double sell_row_dot_smem(const uint32_t* cols, const double* vals,
+                                                    uint32_t off, uint32_t L, uint32_t lane,
+                                                    uint32_t len, const double* src) {
+    double acc = 0.0;
+    const uint32_t Lq = L & ~3u;
+    const uint32_t Lp = L & ~1u;
+    const uint4* cq = reinterpret_cast<const uint4*>(cols + off) + lane;
+    const double2* vp = reinterpret_cast<const double2*>(vals + off) + lane;
+    uint32_t k = 0;
+    const uint32_t full_q = (len < Lq ? len : Lq) & ~3u;
+#pragma unroll 2
+    for (; k < full_q; k += 4) {
+        const uint4 c = cq[(k >> 2) * 32];
+        const double2 v0 = vp[(k >> 1) * 32];
+        const double2 v1 = vp[((k >> 1) + 1) * 32];
+        const double x0 = ld_vec<READONLY>(src + c.x);
+        const double x1 = ld_vec<READONLY>(src + c.y);
+        const double x2 = ld_vec<READONLY>(src + c.z);
+        const double x3 = ld_vec<READONLY>(src + c.w);
+        acc = __dadd_rn(acc, __dmul_rn(v0.x, x0));
+        acc = __dadd_rn(acc, __dmul_rn(v0.y, x1));
+        acc = __dadd_rn(acc, __dmul_rn(v1.x, x2));
+        acc = __dadd_rn(acc, __dmul_rn(v1.y, x3));
+    }
+    for (; k < len; ++k) {
+        const uint32_t c = k < Lq ? cols[off + (k >> 2) * 128 + lane * 4 + (k & 3)]
+                                  : cols[off + Lq * 32 + (k - Lq) * 32 + lane];
+        const double v = k < Lp ? vals[off + (k >> 1) * 64 + lane * 2 + (k & 1)]
+                                : vals[off + Lp * 32 + lane];
+        acc = __dadd_rn(acc, __dmul_rn(v, ld_vec<READONLY>(src + c)));
+    }
+    return acc;
+}
+
 // Epilogues (mpk.hpp:135-153): real shift dst = acc - a*src[r]; second member of a conjugate
 // pair dst = acc - a*src[r] + b2*src2[r] (left to right, no contraction).
 __device__ __forceinline__ double shift_epilogue(double acc, double a, double b2, double own,
