@@ -286,7 +286,8 @@ def main():
     ap.add_argument("--slack", type=int, default=-1)
     ap.add_argument("--order", type=int, default=1, help="0: A_perm order, 1: CM inside levels")
     ap.add_argument("--pass-powers", type=int, default=0, help="force powers per fused pass")
-    ap.add_argument("--l2-budget", type=int, default=0, help="live-window bytes (0: L2/2)")
+    ap.add_argument("--l2-budget", type=int, default=0, help="live-window bytes (0: 0.6 L2)")
+    ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on fused CTAs per SM")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
@@ -311,6 +312,7 @@ def main():
     ctx.set_param("order", args.order)
     ctx.set_param("pass", args.pass_powers)
     ctx.set_param("l2_budget", args.l2_budget)
+    ctx.set_param("ctas_per_sm", args.ctas_per_sm)
     info = ctx.device_info()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 

@@ -64,7 +64,8 @@ struct Executor {
     std::map<int, DevBuf<uint32_t>> tickets;  // by p
     std::map<int, int> pass_len;              // powers per pass, by p
     std::vector<uint64_t> tile_bytes;         // matrix + vector bytes one tile-power touches
-    std::array<int64_t, 3> knobs{};           // slack, pass, l2_budget the schedule was built for
+    std::array<int64_t, 4> knobs{};           // slack, pass, l2_budget, ctas/SM in effect
+    int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
     DevBuf<double> zs;  // sigma-order polynomial accumulator (order 1)
@@ -130,35 +131,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
             : "memory");
 }
 
-// Thread 0 only: stage one tile (cols then vals, each one contiguous range) into `buf`.
-__device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool last_use,
-                                         char* buf, uint64_t* bar) {
-    const uint64_t e0 = P.tile_off[T], e1 = P.tile_off[T + 1];
-    const uint32_t ne = (uint32_t)(e1 - e0);
-    const uint32_t cb = ne * 4u, vb = ne * 8u;
-    const uint32_t cb_pad = (cb + 127u) & ~127u;
+__device__ __forceinline__ uint64_t l2_policy(bool last_use) {
     uint64_t pol;
     if (last_use)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     else
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// Thread 0 only: stage one tile's column indices (one contiguous range) into `buf` with a 1D
+// TMA bulk copy completing on `bar`.
+__device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool last_use,
+                                         char* buf, uint64_t* bar) {
+    const uint64_t e0 = P.tile_off[T], e1 = P.tile_off[T + 1];
+    const uint32_t cb = (uint32_t)(e1 - e0) * 4u;
+    const uint64_t pol = l2_policy(last_use);
     // order earlier generic-proxy reads of this buffer before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(cb + vb)
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cb)
                  : "memory");
-    if (ne) {
+    if (cb)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
             "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf)),
             "l"(P.cols + e0), "r"(cb), "r"(smem_u32(bar)), "l"(pol)
             : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf + cb_pad)),
-            "l"(P.vals + e0), "r"(vb), "r"(smem_u32(bar)), "l"(pol)
-            : "memory");
-    }
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -287,15 +285,12 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
             const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
             double acc;
             if (!big) {
-                const char* b = smem + buf * P.buf_bytes;
-                const uint64_t e0 = P.tile_off[T];
-                const uint32_t ne = (uint32_t)(P.tile_off[T + 1] - e0);
-                const uint32_t cb_pad = (ne * 4u + 127u) & ~127u;
-                const uint32_t* cs = reinterpret_cast<const uint32_t*>(b);
-                const double* vs = reinterpret_cast<const double*>(b + cb_pad);
-                const uint32_t rel = (uint32_t)(off - e0);
-                acc = q == 1 ? sell_row_dot_smem<true>(cs, vs, rel, L, s & 31, len, src)
-                             : sell_row_dot_smem<false>(cs, vs, rel, L, s & 31, len, src);
+                const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
+                const uint32_t rel = (uint32_t)(off - P.tile_off[T]);
+                const uint64_t pol = l2_policy(code & kLastUse);
+                acc = q == 1
+                          ? sell_row_dot_smem<true>(cs, P.vals, rel, off, L, s & 31, len, src, pol)
+                          : sell_row_dot_smem<false>(cs, P.vals, rel, off, L, s & 31, len, src, pol);
             } else {
                 acc = q == 1 ? sell_row_dot<true>(P.cols, P.vals, off, L, s & 31, len, src)
                              : sell_row_dot<false>(P.cols, P.vals, off, L, s & 31, len, src);
@@ -355,16 +350,19 @@ void configure_kernels(uint32_t smem_bytes) {
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1)) {
         Executor& E = *P->exec;
-        if (E.knobs[0] != ctx->slack || E.knobs[1] != ctx->pass_powers || E.knobs[2] != ctx->l2_budget) {
+        const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
+        if (E.knobs != k) {
             E.tickets.clear();  // schedule knobs changed: re-plan the ticket order
             E.pass_len.clear();
+            const int occ = ctx->ctas_per_sm > 0 ? std::min<int>(E.occ_max, (int)ctx->ctas_per_sm) : E.occ_max;
+            E.grid = occ * ctx->sm_count;
             E.slack = ctx->slack >= 0 ? ctx->slack : E.grid;
-            E.knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget};
+            E.knobs = k;
         }
         return E;
     }
     auto E = std::make_shared<Executor>();
-    E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget};
+    E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
     cudaStream_t st = ctx->stream;
     E->order = ctx->order == 0 ? 0 : 1;
     E->n_rows = A->n_rows;
@@ -391,7 +389,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             toff[T] = off[std::min<uint64_t>((uint64_t)T * kChunksPerTile, E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
             const uint64_t ne = toff[T + 1] - toff[T];
-            const uint64_t bytes = ((4 * ne + 127) & ~127ull) + 8 * ne;
+            const uint64_t bytes = 4 * ne;  // staged: column indices only
             E->tile_bytes[T] = 12 * ne + kTile * 8 * 3;
             if (bytes > kMaxBufBytes)
                 E->big[T] = 1;
@@ -406,7 +404,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     configure_kernels(smem);
     int occ = 0;
     MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true>, kTile, smem));
-    E->grid = std::max(1, occ) * ctx->sm_count;
+    occ = std::max(1, occ);
+    E->occ_max = occ;
+    if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
+    E->grid = occ * ctx->sm_count;
     E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
     // dependency runs
     std::vector<uint32_t> lp = P->level_ptr;

@@ -100,24 +100,44 @@ __device__ __forceinline__ double sell_row_dot(const uint32_t* __restrict__ cols
     return acc;
 }
 
-// Same formula over a tile staged in shared memory by TMA (identical SELL layout, offsets
-// relative to the tile start).  Gathers go through L1 (see ld_vec).
+// Value loads with an L2 eviction-priority hint (evict_last while the tile is re-read later in
+// the pass, evict_first on its last use).
+__device__ __forceinline__ double2 ld_mat_d2_hint(const double2* p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_mat_d_hint(const double* p, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(r)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
+// Same formula with the tile's COLUMN indices staged in shared memory by TMA (identical SELL
+// layout, offsets relative to the tile start) and the values streamed from global memory: the
+// gather addresses are available at shared-memory latency, so the x gathers (the long-latency
+// chain) issue immediately while the value loads overlap them.
 template <bool READONLY>
-__device__ __forceinline__ double sell_row_dot_smem(const uint32_t* cols, const double* vals,
-                                                    uint32_t off, uint32_t L, uint32_t lane,
-                                                    uint32_t len, const double* src) {
+__device__ __forceinline__ double sell_row_dot_smem(const uint32_t* cols_s, const double* __restrict__ vals,
+                                                    uint32_t off_rel, uint64_t off, uint32_t L,
+                                                    uint32_t lane, uint32_t len, const double* src,
+                                                    uint64_t pol) {
     double acc = 0.0;
     const uint32_t Lq = L & ~3u;
     const uint32_t Lp = L & ~1u;
-    const uint4* cq = reinterpret_cast<const uint4*>(cols + off) + lane;
+    const uint4* cq = reinterpret_cast<const uint4*>(cols_s + off_rel) + lane;
     const double2* vp = reinterpret_cast<const double2*>(vals + off) + lane;
     uint32_t k = 0;
     const uint32_t full_q = (len < Lq ? len : Lq) & ~3u;
 #pragma unroll 2
     for (; k < full_q; k += 4) {
         const uint4 c = cq[(k >> 2) * 32];
-        const double2 v0 = vp[(k >> 1) * 32];
-        const double2 v1 = vp[((k >> 1) + 1) * 32];
+        const double2 v0 = ld_mat_d2_hint(vp + (k >> 1) * 32, pol);
+        const double2 v1 = ld_mat_d2_hint(vp + ((k >> 1) + 1) * 32, pol);
         const double x0 = ld_vec<READONLY>(src + c.x);
         const double x1 = ld_vec<READONLY>(src + c.y);
         const double x2 = ld_vec<READONLY>(src + c.z);
@@ -128,10 +148,10 @@ __device__ __forceinline__ double sell_row_dot_smem(const uint32_t* cols, const 
         acc = __dadd_rn(acc, __dmul_rn(v1.y, x3));
     }
     for (; k < len; ++k) {
-        const uint32_t c = k < Lq ? cols[off + (k >> 2) * 128 + lane * 4 + (k & 3)]
-                                  : cols[off + Lq * 32 + (k - Lq) * 32 + lane];
-        const double v = k < Lp ? vals[off + (k >> 1) * 64 + lane * 2 + (k & 1)]
-                                : vals[off + Lp * 32 + lane];
+        const uint32_t c = k < Lq ? cols_s[off_rel + (k >> 2) * 128 + lane * 4 + (k & 3)]
+                                  : cols_s[off_rel + Lq * 32 + (k - Lq) * 32 + lane];
+        const double v = k < Lp ? ld_mat_d_hint(vals + off + (k >> 1) * 64 + lane * 2 + (k & 1), pol)
+                                : ld_mat_d_hint(vals + off + Lp * 32 + lane, pol);
         acc = __dadd_rn(acc, __dmul_rn(v, ld_vec<READONLY>(src + c)));
     }
     return acc;

@@ -207,7 +207,7 @@ def test_fused_repeatable_and_plan_reuse(ctx, cases):
     for p in (8, 5, 8, 2):  # p below the plan budget reuses the plan (execute.hpp:74-83)
         assert_bitwise(ctx.mpk(plan, Ap, x, p).as_matrix(), first[: p + 1])
     info = plan.exec_info()
-    assert info["tiles"] == (Ap.n_rows + 255) // 256
+    assert info["tiles"] == (Ap.n_rows + 127) // 128
 
 
 def test_shifted_golden(ctx, golden):
