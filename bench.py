@@ -288,6 +288,7 @@ def main():
     ap.add_argument("--pass-powers", type=int, default=0, help="force powers per fused pass")
     ap.add_argument("--l2-budget", type=int, default=0, help="live-window bytes (0: 0.6 L2)")
     ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on fused CTAs per SM")
+    ap.add_argument("--group", type=int, default=16, help="row entries issued together (8|16)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
@@ -313,6 +314,7 @@ def main():
     ctx.set_param("pass", args.pass_powers)
     ctx.set_param("l2_budget", args.l2_budget)
     ctx.set_param("ctas_per_sm", args.ctas_per_sm)
+    ctx.set_param("group", args.group)
     info = ctx.device_info()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 

@@ -47,6 +47,10 @@ constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
 constexpr uint32_t kLastUse = 1u << 30;  // ticket flag: last use of the tile in its pass
 constexpr uint32_t kBig = 1u << 31;      // ticket flag: tile too large for the smem buffer
 constexpr uint32_t kMaxBufBytes = 96 * 1024;
+#ifndef MPKG_GROUP
+#define MPKG_GROUP 16
+#endif
+constexpr int kGroup = MPKG_GROUP;       // entries per row issued together (rowdot.cuh)
 
 struct Executor {
     int order = 0;  // 0: A_perm order, 1: Cuthill-McKee inside levels
@@ -65,6 +69,7 @@ struct Executor {
     std::map<int, int> pass_len;              // powers per pass, by p
     std::vector<uint64_t> tile_bytes;         // matrix + vector bytes one tile-power touches
     std::array<int64_t, 4> knobs{};           // slack, pass, l2_budget, ctas/SM in effect
+    int group = 16;                           // row group width G of the kernel instance
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -205,7 +210,8 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
     }
 }
 
-template <int KIND, bool SIGMA>  // KIND 0 plain, 1 shifted (Newton), 2 polynomial
+// KIND 0 plain, 1 shifted (Newton), 2 polynomial; SIGMA: private row order; G: row group width
+template <int KIND, bool SIGMA, int G>
 __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(128) char smem[];
     __shared__ __align__(8) uint64_t bars[2];
@@ -284,16 +290,19 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
             const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
             double acc;
+            const uint64_t pol = l2_policy(code & kLastUse);
             if (!big) {
                 const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
                 const uint32_t rel = (uint32_t)(off - P.tile_off[T]);
-                const uint64_t pol = l2_policy(code & kLastUse);
-                acc = q == 1
-                          ? sell_row_dot_smem<true>(cs, P.vals, rel, off, L, s & 31, len, src, pol)
-                          : sell_row_dot_smem<false>(cs, P.vals, rel, off, L, s & 31, len, src, pol);
+                acc = q == 1 ? sell_row_dot_mlp<true, true, G>(cs, P.vals, rel, off, L, s & 31, len,
+                                                                src, pol)
+                             : sell_row_dot_mlp<false, true, G>(cs, P.vals, rel, off, L, s & 31, len,
+                                                                 src, pol);
             } else {
-                acc = q == 1 ? sell_row_dot<true>(P.cols, P.vals, off, L, s & 31, len, src)
-                             : sell_row_dot<false>(P.cols, P.vals, off, L, s & 31, len, src);
+                acc = q == 1 ? sell_row_dot_mlp<true, false, G>(P.cols, P.vals, off, off, L, s & 31,
+                                                                 len, src, pol)
+                             : sell_row_dot_mlp<false, false, G>(P.cols, P.vals, off, off, L, s & 31,
+                                                                  len, src, pol);
             }
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
@@ -339,16 +348,18 @@ struct RangeMax {
     }
 };
 
+template <int G>
 void configure_kernels(uint32_t smem_bytes) {
-    const void* ks[] = {(const void*)k_mpk_fused<0, false>, (const void*)k_mpk_fused<0, true>,
-                        (const void*)k_mpk_fused<1, false>, (const void*)k_mpk_fused<1, true>,
-                        (const void*)k_mpk_fused<2, false>, (const void*)k_mpk_fused<2, true>};
+    const void* ks[] = {(const void*)k_mpk_fused<0, false, G>, (const void*)k_mpk_fused<0, true, G>,
+                        (const void*)k_mpk_fused<1, false, G>, (const void*)k_mpk_fused<1, true, G>,
+                        (const void*)k_mpk_fused<2, false, G>, (const void*)k_mpk_fused<2, true, G>};
     for (const void* k : ks)
         MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
 }
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
-    if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1)) {
+    if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
+        P->exec->group == (ctx->group == 8 ? 8 : 16)) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -401,9 +412,15 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         MPKG_CUDA(cudaMemcpyAsync(E->tile_off.p, toff.data(), 8ull * (nt + 1), cudaMemcpyHostToDevice, st));
     }
     const uint32_t smem = 2 * E->buf_bytes;
-    configure_kernels(smem);
+    E->group = ctx->group == 8 ? 8 : 16;
     int occ = 0;
-    MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true>, kTile, smem));
+    if (E->group == 8) {
+        configure_kernels<8>(smem);
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, kTile, smem));
+    } else {
+        configure_kernels<16>(smem);
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, kTile, smem));
+    }
     occ = std::max(1, occ);
     E->occ_max = occ;
     if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
@@ -555,12 +572,21 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.tickets.emplace(p, std::move(d)).first->second;
 }
 
-template <int KIND>
-void launch_kind(bool sigma, int grid, uint32_t smem, cudaStream_t st, const FusedParams& P) {
+template <int KIND, int G>
+void launch_g(bool sigma, int grid, uint32_t smem, cudaStream_t st, const FusedParams& P) {
     if (sigma)
-        k_mpk_fused<KIND, true><<<grid, kTile, smem, st>>>(P);
+        k_mpk_fused<KIND, true, G><<<grid, kTile, smem, st>>>(P);
     else
-        k_mpk_fused<KIND, false><<<grid, kTile, smem, st>>>(P);
+        k_mpk_fused<KIND, false, G><<<grid, kTile, smem, st>>>(P);
+}
+
+template <int KIND>
+void launch_kind(bool sigma, int group, int grid, uint32_t smem, cudaStream_t st,
+                 const FusedParams& P) {
+    if (group == 8)
+        launch_g<KIND, 8>(sigma, grid, smem, st, P);
+    else
+        launch_g<KIND, 16>(sigma, grid, smem, st, P);
 }
 
 }  // namespace
@@ -621,9 +647,9 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const uint32_t smem = 2 * E.buf_bytes;
     const auto ev = timing_begin(ctx);
     switch (a.kind) {
-        case 0: launch_kind<0>(sigma, E.grid, smem, st, P); break;
-        case 1: launch_kind<1>(sigma, E.grid, smem, st, P); break;
-        default: launch_kind<2>(sigma, E.grid, smem, st, P); break;
+        case 0: launch_kind<0>(sigma, E.group, E.grid, smem, st, P); break;
+        case 1: launch_kind<1>(sigma, E.group, E.grid, smem, st, P); break;
+        default: launch_kind<2>(sigma, E.group, E.grid, smem, st, P); break;
     }
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);

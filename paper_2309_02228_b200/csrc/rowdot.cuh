@@ -157,6 +157,67 @@ __device__ __forceinline__ double sell_row_dot_smem(const uint32_t* cols_s, cons
     return acc;
 }
 
+// Memory-level-parallel variant: the row is processed in groups of G entries (G % 4 == 0).
+// All G column indices, G x-gathers and G values of a group are issued before the group's
+// strictly sequential accumulation, so one row keeps up to 2G independent loads in flight
+// instead of one quad.  Loads are predicated on k < L (the chunk's stored width: in bounds for
+// every lane, padding entries hold column 0 / value 0); accumulation on k < len, in stored
+// order: bit-identical to sell_row_dot.
+template <bool READONLY, bool STAGED, int G>
+__device__ __forceinline__ double sell_row_dot_mlp(const uint32_t* cols, const double* __restrict__ vals,
+                                                   uint64_t off_c, uint64_t off_v, uint32_t L,
+                                                   uint32_t lane, uint32_t len, const double* src,
+                                                   uint64_t pol) {
+    static_assert(G % 4 == 0, "group must be a multiple of 4");
+    double acc = 0.0;
+    const uint32_t Lq = L & ~3u;
+    const uint32_t Lp = L & ~1u;
+    for (uint32_t k0 = 0; k0 < len; k0 += G) {
+        uint32_t c[G];
+        double v[G], x[G];
+#pragma unroll
+        for (int j = 0; j < G; j += 4) {
+            const uint32_t k = k0 + j;
+            if (k + 3 < Lq) {
+                const uint4* cq = reinterpret_cast<const uint4*>(cols + off_c) + (k >> 2) * 32 + lane;
+                const uint4 q4 = STAGED ? *cq : ld_mat_u4(cq);
+                c[j] = q4.x, c[j + 1] = q4.y, c[j + 2] = q4.z, c[j + 3] = q4.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t kk = k + i;
+                    const uint32_t* pc = kk < Lq ? cols + off_c + (kk >> 2) * 128 + lane * 4 + (kk & 3)
+                                                 : cols + off_c + Lq * 32 + (kk - Lq) * 32 + lane;
+                    c[j + i] = kk < L ? (STAGED ? *pc : ld_mat_u32(pc)) : 0u;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < G; j += 2) {
+            const uint32_t k = k0 + j;
+            if (k + 1 < Lp) {
+                const double2 d = ld_mat_d2_hint(
+                    reinterpret_cast<const double2*>(vals + off_v) + (k >> 1) * 32 + lane, pol);
+                v[j] = d.x, v[j + 1] = d.y;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t kk = k + i;
+                    const double* pv = kk < Lp ? vals + off_v + (kk >> 1) * 64 + lane * 2 + (kk & 1)
+                                               : vals + off_v + Lp * 32 + lane;
+                    v[j + i] = kk < L ? ld_mat_d_hint(pv, pol) : 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) x[j] = (k0 + j < len) ? ld_vec<READONLY>(src + c[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+            if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+    }
+    return acc;
+}
+
 // Epilogues (mpk.hpp:135-153): real shift dst = acc - a*src[r]; second member of a conjugate
 // pair dst = acc - a*src[r] + b2*src2[r] (left to right, no contraction).
 __device__ __forceinline__ double shift_epilogue(double acc, double a, double b2, double own,

@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(256) k_spmv_sell(
         const uint64_t off = chunk_off[c];
         const uint32_t L = (uint32_t)((chunk_off[c + 1] - off) >> 5);
         if (r >= n_rows) continue;  // padding slot
-        double acc = sell_row_dot<true>(cols, vals, off, L, (uint32_t)(s & 31), len, src);
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        double acc = sell_row_dot_mlp<true, false, 16>(cols, vals, off, off, L, (uint32_t)(s & 31),
+                                                       len, src, pol);
         if (KIND == 1)
             acc = shift_epilogue(acc, a, b2, __ldg(src + r), b2 != 0.0 ? __ldg(src2 + r) : 0.0);
         dst[r] = acc;
