@@ -65,9 +65,9 @@ struct Ctx;
 
 // Sliced-ELLPACK (SELL-32) copy of a CSR in a given slot order: the storage the row kernels
 // read.  Rows keep their stored entry order (bitwise parity), slot s holds row slot_row[s]
-// (identity when slot_row is empty).  Layout per 32-row chunk c starting at entry off[c]:
-//   cols  (lane, k) -> off + (k/4)*128 + lane*4 + k%4   (one 16-byte load = 4 columns)
-//   vals  (lane, k) -> off + (k/2)*64  + lane*2 + k%2   (one 16-byte load = 2 values)
+// (identity when slot_row is empty).  Layout per 32-row chunk c starting at entry off[c], the
+// same for columns and values (rowdot.cuh sell_pos):
+//   (lane, k) -> off + (k/2)*64 + lane*2 + k%2, the odd tail entry at off + Lp*32 + lane
 struct Sell {
     uint32_t n_rows = 0;
     uint32_t n_slots = 0;  // multiple of 32

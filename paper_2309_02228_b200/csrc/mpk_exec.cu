@@ -40,7 +40,8 @@
 
 namespace mpkg_detail {
 
-constexpr int kTile = 128;               // slots per tile == threads per CTA
+constexpr int kTile = 128;               // slots (rows) per tile
+constexpr int kThreads = 256;            // threads per CTA (phase 1 is entry-parallel)
 constexpr int kChunksPerTile = kTile / 32;
 constexpr int kMaxFusedP = 32;           // powers per fused launch
 constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
@@ -137,31 +138,54 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 __device__ __forceinline__ uint64_t l2_policy(bool last_use) {
-    uint64_t pol;
-    if (last_use)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    else
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
+    return last_use ? l2_policy_first() : l2_policy_last();
 }
 
-// Thread 0 only: stage one tile's column indices (one contiguous range) into `buf` with a 1D
-// TMA bulk copy completing on `bar`.
+// Thread 0 only: stage one tile (its column indices, then its values: each one contiguous
+// range of the SELL arrays) into `buf` with two 1D TMA bulk copies completing on `bar`.
 __device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool last_use,
                                          char* buf, uint64_t* bar) {
     const uint64_t e0 = P.tile_off[T], e1 = P.tile_off[T + 1];
-    const uint32_t cb = (uint32_t)(e1 - e0) * 4u;
+    const uint32_t ne = (uint32_t)(e1 - e0);
+    const uint32_t cb = ne * 4u, vb = ne * 8u, cb_pad = (cb + 127u) & ~127u;
     const uint64_t pol = l2_policy(last_use);
-    // order earlier generic-proxy reads of this buffer before the async-proxy writes
+    // order earlier generic-proxy accesses of this buffer before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cb)
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(cb + vb)
                  : "memory");
-    if (cb)
+    if (ne) {
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
             "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf)),
             "l"(P.cols + e0), "r"(cb), "r"(smem_u32(bar)), "l"(pol)
             : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf + cb_pad)),
+            "l"(P.vals + e0), "r"(vb), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+    }
+}
+
+// Phase 1 of the tile kernel: every entry's product v*x[col] (all gathers independent, U per
+// thread in flight), written in place over the staged values.
+template <bool READONLY, int U>
+__device__ __forceinline__ void tile_products(const uint32_t* cs, double* ps, uint32_t ne,
+                                              const double* src, uint32_t tid, uint32_t nthreads) {
+    for (uint32_t base = 0; base < ne; base += nthreads * U) {
+        double xv[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t e = base + j * nthreads + tid;
+            xv[j] = e < ne ? ld_vec<READONLY>(src + cs[e]) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t e = base + j * nthreads + tid;
+            if (e < ne) ps[e] = __dmul_rn(ps[e], xv[j]);
+        }
+    }
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -212,7 +236,7 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
 
 // KIND 0 plain, 1 shifted (Newton), 2 polynomial; SIGMA: private row order; G: row group width
 template <int KIND, bool SIGMA, int G>
-__global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(128) char smem[];
     __shared__ __align__(8) uint64_t bars[2];
     // Double-buffered claims: the next ticket is claimed (and its tile staged) while this one
@@ -257,7 +281,7 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
                 int ok = 1;
                 for (uint32_t run = r0; run < r1 && ok; ++run) {
                     const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += kTile)
+                    for (uint32_t u = lo + tid; u <= hi; u += kThreads)
                         if (ld_relaxed(P.done + u) < q - 1) {
                             ok = 0;
                             break;
@@ -267,7 +291,7 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
                 __nanosleep(64);
             }
             for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += kTile)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += kThreads)
                     (void)ld_acquire(P.done + u);
         }
         const bool big = code & kBig;
@@ -280,29 +304,38 @@ __global__ void __launch_bounds__(kTile) k_mpk_fused(const __grid_constant__ Fus
                 phase1 ^= 1u;
             }
         }
-        __syncthreads();
+        __syncthreads();  // also publishes every thread's acquires to the whole CTA
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        const uint64_t e0 = P.tile_off[T];
+        double* ps = nullptr;
+        if (!big) {
+            // phase 1: all products of the tile, entry-parallel over 256 threads
+            const uint32_t ne = (uint32_t)(P.tile_off[T + 1] - e0);
+            const uint32_t cb_pad = (ne * 4u + 127u) & ~127u;
+            const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
+            ps = reinterpret_cast<double*>(smem + buf * P.buf_bytes + cb_pad);
+            if (q == 1)
+                tile_products<true, G>(cs, ps, ne, src, tid, kThreads);
+            else
+                tile_products<false, G>(cs, ps, ne, src, tid, kThreads);
+            __syncthreads();
+        }
+        // phase 2: one thread per row, stored-order sequential sum + epilogue
         const uint32_t s = T * kTile + tid;
-        const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+        const uint32_t r =
+            tid >= kTile ? 0xffffffffu : (SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s);
         if (r < P.n_rows) {
             const uint32_t len = P.row_len[s];
             const uint64_t c = s >> 5;
             const uint64_t off = P.chunk_off[c];
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
-            const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
             double acc;
-            const uint64_t pol = l2_policy(code & kLastUse);
             if (!big) {
-                const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
-                const uint32_t rel = (uint32_t)(off - P.tile_off[T]);
-                acc = q == 1 ? sell_row_dot_mlp<true, true, G>(cs, P.vals, rel, off, L, s & 31, len,
-                                                                src, pol)
-                             : sell_row_dot_mlp<false, true, G>(cs, P.vals, rel, off, L, s & 31, len,
-                                                                 src, pol);
+                acc = sell_row_sum_smem(ps, (uint32_t)(off - e0), L, s & 31, len);
             } else {
-                acc = q == 1 ? sell_row_dot_mlp<true, false, G>(P.cols, P.vals, off, off, L, s & 31,
-                                                                 len, src, pol)
-                             : sell_row_dot_mlp<false, false, G>(P.cols, P.vals, off, off, L, s & 31,
-                                                                  len, src, pol);
+                const uint64_t pol = l2_policy(code & kLastUse);
+                acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                             : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
             }
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
@@ -400,7 +433,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             toff[T] = off[std::min<uint64_t>((uint64_t)T * kChunksPerTile, E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
             const uint64_t ne = toff[T + 1] - toff[T];
-            const uint64_t bytes = 4 * ne;  // staged: column indices only
+            const uint64_t bytes = ((4 * ne + 127) & ~127ull) + 8 * ne;  // staged cols + vals
             E->tile_bytes[T] = 12 * ne + kTile * 8 * 3;
             if (bytes > kMaxBufBytes)
                 E->big[T] = 1;
@@ -416,10 +449,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     int occ = 0;
     if (E->group == 8) {
         configure_kernels<8>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, kTile, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, kThreads, smem));
     } else {
         configure_kernels<16>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, kTile, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, kThreads, smem));
     }
     occ = std::max(1, occ);
     E->occ_max = occ;
@@ -575,9 +608,9 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
 template <int KIND, int G>
 void launch_g(bool sigma, int grid, uint32_t smem, cudaStream_t st, const FusedParams& P) {
     if (sigma)
-        k_mpk_fused<KIND, true, G><<<grid, kTile, smem, st>>>(P);
+        k_mpk_fused<KIND, true, G><<<grid, kThreads, smem, st>>>(P);
     else
-        k_mpk_fused<KIND, false, G><<<grid, kTile, smem, st>>>(P);
+        k_mpk_fused<KIND, false, G><<<grid, kThreads, smem, st>>>(P);
 }
 
 template <int KIND>

@@ -48,15 +48,12 @@ __global__ void k_sell_fill(const uint32_t* __restrict__ rp, const uint32_t* __r
         const uint32_t lane = (uint32_t)(s & 31);
         const uint64_t off = chunk_off[c];
         const uint32_t L = (uint32_t)((chunk_off[c + 1] - off) >> 5);
-        const uint32_t Lq = L & ~3u, Lp = L & ~1u;
+        const uint32_t Lp = L & ~1u;
         const uint32_t b = rp[r];
         for (uint32_t k = 0; k < len; ++k) {
-            const uint64_t pc = k < Lq ? off + (k >> 2) * 128ull + lane * 4 + (k & 3)
-                                       : off + Lq * 32ull + (k - Lq) * 32ull + lane;
-            const uint64_t pv = k < Lp ? off + (k >> 1) * 64ull + lane * 2 + (k & 1)
-                                       : off + Lp * 32ull + lane;
-            cols[pc] = col_map ? col_map[ci[b + k]] : ci[b + k];
-            vals[pv] = v[b + k];
+            const uint64_t e = off + sell_pos(k, Lp, lane);
+            cols[e] = col_map ? col_map[ci[b + k]] : ci[b + k];
+            vals[e] = v[b + k];
         }
     }
 }
@@ -77,10 +74,8 @@ __global__ void __launch_bounds__(256) k_spmv_sell(
         const uint64_t off = chunk_off[c];
         const uint32_t L = (uint32_t)((chunk_off[c + 1] - off) >> 5);
         if (r >= n_rows) continue;  // padding slot
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        double acc = sell_row_dot_mlp<true, false, 16>(cols, vals, off, off, L, (uint32_t)(s & 31),
-                                                       len, src, pol);
+        double acc = sell_row_dot<true, 8>(cols, vals, off, L, (uint32_t)(s & 31), len, src,
+                                           l2_policy_first());
         if (KIND == 1)
             acc = shift_epilogue(acc, a, b2, __ldg(src + r), b2 != 0.0 ? __ldg(src2 + r) : 0.0);
         dst[r] = acc;

@@ -19,16 +19,21 @@ def main():
     ap.add_argument("--order", type=int, default=1)
     ap.add_argument("--slack", type=int, default=-1)
     ap.add_argument("--launches", type=int, default=2)
+    ap.add_argument("--group", type=int, default=8)
+    ap.add_argument("--pass-powers", type=int, default=0)
+    ap.add_argument("--p", type=int, default=0, help="override the config's p")
     ap.add_argument("--seed", type=int, default=2309)
     args = ap.parse_args()
     import torch
 
     import paper_2309_02228_b200 as mpkg
     cfgd = bench.CONFIGS[args.config]
-    p = cfgd["p"]
+    p = args.p or cfgd["p"]
     A = bench.make_matrix(args.config, args.seed)
     ctx = mpkg.Context(0)
     ctx.set_param("order", args.order)
+    ctx.set_param("group", args.group)
+    ctx.set_param("pass", args.pass_powers)
     if args.slack >= 0:
         ctx.set_param("slack", args.slack)
     dA = ctx.csr(A)
