@@ -259,6 +259,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->ctas_per_sm = value;
         else if (k == "group")
             ctx->group = value;
+        else if (k == "stages")
+            ctx->stages = value;
         else if (k == "kernel_timing")
             ctx->kernel_timing = value != 0;
         else if (k == "tile_rows")

@@ -98,7 +98,8 @@ struct mpkg_ctx_s {
     int64_t pass_powers = 0;  // >0: force powers per fused pass
     int64_t l2_budget = 0;    // >0: live-window budget in bytes (default 0.6 L2)
     int64_t ctas_per_sm = 0;  // >0: cap on resident fused-kernel CTAs per SM
-    int64_t group = 16;       // entries per row issued together (8 or 16)
+    int64_t group = 8;        // phase-1 gathers in flight per thread (8 or 16)
+    int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;

@@ -42,6 +42,7 @@ namespace mpkg_detail {
 
 constexpr int kTile = 128;               // slots (rows) per tile
 constexpr int kThreads = 256;            // threads per CTA (phase 1 is entry-parallel)
+constexpr int kMaxStages = 8;            // staged tickets per CTA
 constexpr int kChunksPerTile = kTile / 32;
 constexpr int kMaxFusedP = 32;           // powers per fused launch
 constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
@@ -59,6 +60,7 @@ struct Executor {
     int grid = 0;
     int64_t slack = 0;
     uint32_t buf_bytes = 0;  // one smem staging buffer (cols + vals of the largest tile)
+    uint32_t stages = 2;     // staging buffers (claimed tickets) per CTA
     Sell own;                // sigma-order SELL (order 1)
     const Sell* S = nullptr;
     DevBuf<uint32_t> slot_row, pos;  // order 1
@@ -71,6 +73,7 @@ struct Executor {
     std::vector<uint64_t> tile_bytes;         // matrix + vector bytes one tile-power touches
     std::array<int64_t, 4> knobs{};           // slack, pass, l2_budget, ctas/SM in effect
     int group = 16;                           // row group width G of the kernel instance
+    int64_t stage_knob = 0;                   // ctx->stages the executor was built with
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -95,6 +98,7 @@ struct FusedParams {
     uint32_t n_slots;
     uint32_t p;
     uint32_t buf_bytes;
+    uint32_t stages;
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -238,41 +242,35 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
 template <int KIND, bool SIGMA, int G>
 __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(128) char smem[];
-    __shared__ __align__(8) uint64_t bars[2];
-    // Double-buffered claims: the next ticket is claimed (and its tile staged) while this one
-    // runs.  Still deadlock-free: the lowest unfinished ticket can never be one that is merely
-    // claimed, because its holder is busy with a smaller (hence unfinished) ticket.
-    __shared__ uint32_t s_ticket[2];
+    __shared__ __align__(8) uint64_t bars[kMaxStages];
+    // A ring of P.stages claimed tickets per CTA: their tiles are staged by TMA while the CTA
+    // works on the oldest one, so up to stages*buf_bytes of matrix are in flight per CTA.
+    // Still deadlock-free: each CTA processes its claims in increasing order, so the lowest
+    // unfinished ticket is always the one its holder is working on.
+    __shared__ uint32_t s_ticket[kMaxStages];
     const uint32_t tid = threadIdx.x;
+    const uint32_t S = P.stages;
     if (tid == 0) {
-        mbar_init(&bars[0]);
-        mbar_init(&bars[1]);
+        for (uint32_t i = 0; i < S; ++i) mbar_init(&bars[i]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t t0 = atomicAdd(P.counter, 1u);
-        s_ticket[0] = t0;
-        if (t0 < P.n_tickets) {
-            const uint32_t c0 = P.tickets[t0];
-            if (!(c0 & kBig)) tma_tile(P, c0 & 0xffffffu, c0 & kLastUse, smem, &bars[0]);
+        for (uint32_t i = 0; i < S; ++i) {
+            const uint32_t t0 = atomicAdd(P.counter, 1u);
+            s_ticket[i] = t0;
+            if (t0 < P.n_tickets) {
+                const uint32_t c0 = P.tickets[t0];
+                if (!(c0 & kBig))
+                    tma_tile(P, c0 & 0xffffffu, c0 & kLastUse, smem + i * P.buf_bytes, &bars[i]);
+            }
         }
     }
     __syncthreads();
-    uint32_t phase0 = 0, phase1 = 0;
-    for (uint32_t buf = 0;; buf ^= 1u) {
+    uint32_t phases = 0;  // bit i: parity of stage i's next completion
+    for (uint32_t buf = 0;; buf = (buf + 1 == S) ? 0 : buf + 1) {
         const uint32_t t = s_ticket[buf];
         if (t >= P.n_tickets) return;
         const uint32_t code = P.tickets[t];
         const uint32_t T = code & 0xffffffu;
         const uint32_t q = (code >> 24) & 63u;
-        if (tid == 0) {
-            const uint32_t t2 = atomicAdd(P.counter, 1u);
-            s_ticket[buf ^ 1u] = t2;
-            if (t2 < P.n_tickets) {
-                const uint32_t c2 = P.tickets[t2];
-                if (!(c2 & kBig))
-                    tma_tile(P, c2 & 0xffffffu, c2 & kLastUse, smem + (buf ^ 1u) * P.buf_bytes,
-                             &bars[buf ^ 1u]);
-            }
-        }
         if (q > 1) {
             // Poll with relaxed loads (no L1 invalidation), then acquire each observed flag
             // once (flags are monotone).
@@ -296,13 +294,8 @@ __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ 
         }
         const bool big = code & kBig;
         if (!big) {
-            if (buf == 0) {
-                mbar_wait(&bars[0], phase0);
-                phase0 ^= 1u;
-            } else {
-                mbar_wait(&bars[1], phase1);
-                phase1 ^= 1u;
-            }
+            mbar_wait(&bars[buf], (phases >> buf) & 1u);
+            phases ^= 1u << buf;
         }
         __syncthreads();  // also publishes every thread's acquires to the whole CTA
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
@@ -357,7 +350,18 @@ __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ 
             }
         }
         __syncthreads();
-        if (tid == 0) st_release(P.done + T, q);
+        if (tid == 0) {
+            st_release(P.done + T, q);
+            // refill the freed stage with the next claim
+            const uint32_t t2 = atomicAdd(P.counter, 1u);
+            s_ticket[buf] = t2;
+            if (t2 < P.n_tickets) {
+                const uint32_t c2 = P.tickets[t2];
+                if (!(c2 & kBig))
+                    tma_tile(P, c2 & 0xffffffu, c2 & kLastUse, smem + buf * P.buf_bytes, &bars[buf]);
+            }
+        }
+        // s_ticket[buf] is read again only S iterations later, after S more barriers.
     }
 }
 
@@ -392,7 +396,7 @@ void configure_kernels(uint32_t smem_bytes) {
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
-        P->exec->group == (ctx->group == 8 ? 8 : 16)) {
+        P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -400,7 +404,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             E.pass_len.clear();
             const int occ = ctx->ctas_per_sm > 0 ? std::min<int>(E.occ_max, (int)ctx->ctas_per_sm) : E.occ_max;
             E.grid = occ * ctx->sm_count;
-            E.slack = ctx->slack >= 0 ? ctx->slack : E.grid;
+            E.slack = ctx->slack >= 0 ? ctx->slack : (int64_t)E.grid * E.stages;
             E.knobs = k;
         }
         return E;
@@ -444,8 +448,16 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->tile_off.alloc(nt + 1);
         MPKG_CUDA(cudaMemcpyAsync(E->tile_off.p, toff.data(), 8ull * (nt + 1), cudaMemcpyHostToDevice, st));
     }
-    const uint32_t smem = 2 * E->buf_bytes;
+    // Stages: enough staged bytes per SM to cover DRAM latency (~200 KB of the 228 KB), at
+    // least 2 (prefetch), at most kMaxStages; "stages" knob overrides.
+    if (ctx->stages > 0)
+        E->stages = (uint32_t)std::min<int64_t>(ctx->stages, kMaxStages);
+    else
+        E->stages = std::max<uint32_t>(2, std::min<uint32_t>(kMaxStages, (200u << 10) / E->buf_bytes));
+    while (E->stages > 1 && E->stages * E->buf_bytes > (220u << 10)) --E->stages;
+    const uint32_t smem = E->stages * E->buf_bytes;
     E->group = ctx->group == 8 ? 8 : 16;
+    E->stage_knob = ctx->stages;
     int occ = 0;
     if (E->group == 8) {
         configure_kernels<8>(smem);
@@ -458,7 +470,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->occ_max = occ;
     if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
     E->grid = occ * ctx->sm_count;
-    E->slack = ctx->slack >= 0 ? ctx->slack : E->grid;
+    E->slack = ctx->slack >= 0 ? ctx->slack : (int64_t)E->grid * E->stages;
     // dependency runs
     std::vector<uint32_t> lp = P->level_ptr;
     if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
@@ -650,6 +662,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.n_slots = E.n_slots;
     P.p = (uint32_t)a.p;
     P.buf_bytes = E.buf_bytes;
+    P.stages = E.stages;
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
@@ -677,7 +690,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     for (int i = 0; i <= a.p; ++i) P.coef[i] = a.coef ? a.coef[i] : 0.0;
     MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
-    const uint32_t smem = 2 * E.buf_bytes;
+    const uint32_t smem = E.stages * E.buf_bytes;
     const auto ev = timing_begin(ctx);
     switch (a.kind) {
         case 0: launch_kind<0>(sigma, E.group, E.grid, smem, st, P); break;
