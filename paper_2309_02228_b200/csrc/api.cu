@@ -263,8 +263,13 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->stages = value;
         else if (k == "kernel_timing")
             ctx->kernel_timing = value != 0;
-        else if (k == "tile_rows")
-            require(value == 256, "ctx_set_param: tile_rows is fixed at 256 in this build");
+        else if (k == "tile_rows") {
+            require(value == 64 || value == 128 || value == 256, "ctx_set_param: tile_rows must be 64, 128 or 256");
+            ctx->tile_rows = value;
+        } else if (k == "threads") {
+            require(value == 256 || value == 512, "ctx_set_param: threads must be 256 or 512");
+            ctx->threads = value;
+        }
         else
             fail(MPKG_EINVAL, "ctx_set_param: unknown key " + k);
     });

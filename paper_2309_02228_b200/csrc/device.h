@@ -92,7 +92,7 @@ struct mpkg_ctx_s {
     size_t persist_max = 0;
     int mode = MPKG_MODE_BITWISE;
     // executor knobs (mpkg_ctx_set_param)
-    int64_t tile_rows = 256;
+    int64_t tile_rows = 128;  // rows per fused-kernel tile (64, 128 or 256)
     int64_t slack = -1;  // -1: resident CTA count
     int64_t order = 1;        // 0: A_perm order, 1: Cuthill-McKee inside levels
     int64_t pass_powers = 0;  // >0: force powers per fused pass
@@ -100,6 +100,7 @@ struct mpkg_ctx_s {
     int64_t ctas_per_sm = 0;  // >0: cap on resident fused-kernel CTAs per SM
     int64_t group = 8;        // phase-1 gathers in flight per thread (8 or 16)
     int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
+    int64_t threads = 256;    // fused-kernel threads per CTA (256 or 512)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;

@@ -40,10 +40,8 @@
 
 namespace mpkg_detail {
 
-constexpr int kTile = 128;               // slots (rows) per tile
-constexpr int kThreads = 256;            // threads per CTA (phase 1 is entry-parallel)
+constexpr int kMaxThreads = 512;         // threads per CTA: 256 or 512 (knob "threads")
 constexpr int kMaxStages = 8;            // staged tickets per CTA
-constexpr int kChunksPerTile = kTile / 32;
 constexpr int kMaxFusedP = 32;           // powers per fused launch
 constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
 constexpr uint32_t kLastUse = 1u << 30;  // ticket flag: last use of the tile in its pass
@@ -61,6 +59,8 @@ struct Executor {
     int64_t slack = 0;
     uint32_t buf_bytes = 0;  // one smem staging buffer (cols + vals of the largest tile)
     uint32_t stages = 2;     // staging buffers (claimed tickets) per CTA
+    uint32_t tile_rows = 128;
+    uint32_t threads = 256;
     Sell own;                // sigma-order SELL (order 1)
     const Sell* S = nullptr;
     DevBuf<uint32_t> slot_row, pos;  // order 1
@@ -74,6 +74,7 @@ struct Executor {
     std::array<int64_t, 4> knobs{};           // slack, pass, l2_budget, ctas/SM in effect
     int group = 16;                           // row group width G of the kernel instance
     int64_t stage_knob = 0;                   // ctx->stages the executor was built with
+    int64_t tile_knob = 0, thread_knob = 0;   // ctx->tile_rows / ctx->threads likewise
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -99,6 +100,7 @@ struct FusedParams {
     uint32_t p;
     uint32_t buf_bytes;
     uint32_t stages;
+    uint32_t tile_rows;
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -209,12 +211,13 @@ __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, ui
 __global__ void k_dep_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                               uint32_t n, const uint32_t* __restrict__ slot_row,
                               const uint32_t* __restrict__ pos, const uint32_t* __restrict__ lp,
-                              uint32_t nl, uint32_t* __restrict__ bmin, uint32_t* __restrict__ bmax) {
+                              uint32_t nl, uint32_t tile_rows, uint32_t* __restrict__ bmin,
+                              uint32_t* __restrict__ bmax) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t r = slot_row ? slot_row[s] : (uint32_t)s;
-        const uint32_t T = (uint32_t)(s / kTile);
-        const uint32_t lt = level_of(lp, nl, T * kTile);
+        const uint32_t T = (uint32_t)(s / tile_rows);
+        const uint32_t lt = level_of(lp, nl, T * tile_rows);
         const uint32_t L = level_of(lp, nl, (uint32_t)s);
         const uint32_t lb = lp[L], le = lp[L + 1];
         for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
@@ -240,7 +243,7 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
 
 // KIND 0 plain, 1 shifted (Newton), 2 polynomial; SIGMA: private row order; G: row group width
 template <int KIND, bool SIGMA, int G>
-__global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kMaxThreads) k_mpk_fused(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(128) char smem[];
     __shared__ __align__(8) uint64_t bars[kMaxStages];
     // A ring of P.stages claimed tickets per CTA: their tiles are staged by TMA while the CTA
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ 
                 int ok = 1;
                 for (uint32_t run = r0; run < r1 && ok; ++run) {
                     const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += kThreads)
+                    for (uint32_t u = lo + tid; u <= hi; u += blockDim.x)
                         if (ld_relaxed(P.done + u) < q - 1) {
                             ok = 0;
                             break;
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ 
                 __nanosleep(64);
             }
             for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += kThreads)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += blockDim.x)
                     (void)ld_acquire(P.done + u);
         }
         const bool big = code & kBig;
@@ -308,15 +311,15 @@ __global__ void __launch_bounds__(kThreads) k_mpk_fused(const __grid_constant__ 
             const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
             ps = reinterpret_cast<double*>(smem + buf * P.buf_bytes + cb_pad);
             if (q == 1)
-                tile_products<true, G>(cs, ps, ne, src, tid, kThreads);
+                tile_products<true, G>(cs, ps, ne, src, tid, blockDim.x);
             else
-                tile_products<false, G>(cs, ps, ne, src, tid, kThreads);
+                tile_products<false, G>(cs, ps, ne, src, tid, blockDim.x);
             __syncthreads();
         }
         // phase 2: one thread per row, stored-order sequential sum + epilogue
-        const uint32_t s = T * kTile + tid;
+        const uint32_t s = T * P.tile_rows + tid;
         const uint32_t r =
-            tid >= kTile ? 0xffffffffu : (SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s);
+            tid >= P.tile_rows ? 0xffffffffu : (SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s);
         if (r < P.n_rows) {
             const uint32_t len = P.row_len[s];
             const uint64_t c = s >> 5;
@@ -396,7 +399,8 @@ void configure_kernels(uint32_t smem_bytes) {
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
-        P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages) {
+        P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
+        P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -415,7 +419,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->order = ctx->order == 0 ? 0 : 1;
     E->n_rows = A->n_rows;
     E->n_slots = (A->n_rows + 31u) & ~31u;
-    E->n_tiles = (A->n_rows + kTile - 1) / kTile;
+    E->tile_rows = ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
+    E->threads = ctx->threads == 512 ? 512u : 256u;
+    if (E->threads < E->tile_rows) E->threads = E->tile_rows;
+    E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
     if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
     if (E->order == 1) {
         gpu_level_cm_order(ctx, A, P->level_ptr, E->n_slots, E->slot_row, E->pos);
@@ -434,11 +441,11 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->big.assign(nt, 0);
         uint64_t max_buf = 256;
         for (uint32_t T = 0; T <= nt; ++T)
-            toff[T] = off[std::min<uint64_t>((uint64_t)T * kChunksPerTile, E->S->n_chunks)];
+            toff[T] = off[std::min<uint64_t>((uint64_t)T * (E->tile_rows / 32), E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
             const uint64_t ne = toff[T + 1] - toff[T];
             const uint64_t bytes = ((4 * ne + 127) & ~127ull) + 8 * ne;  // staged cols + vals
-            E->tile_bytes[T] = 12 * ne + kTile * 8 * 3;
+            E->tile_bytes[T] = 12 * ne + E->tile_rows * 8 * 3;
             if (bytes > kMaxBufBytes)
                 E->big[T] = 1;
             else
@@ -458,13 +465,15 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     const uint32_t smem = E->stages * E->buf_bytes;
     E->group = ctx->group == 8 ? 8 : 16;
     E->stage_knob = ctx->stages;
+    E->tile_knob = ctx->tile_rows;
+    E->thread_knob = ctx->threads;
     int occ = 0;
     if (E->group == 8) {
         configure_kernels<8>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, kThreads, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads, smem));
     } else {
         configure_kernels<16>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, kThreads, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, (int)E->threads, smem));
     }
     occ = std::max(1, occ);
     E->occ_max = occ;
@@ -482,7 +491,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (nt) {
         k_dep_buckets<<<grid_for(A->n_rows, 256), 256, 0, st>>>(
             A->row_ptr.p, A->col_idx.p, A->n_rows, E->order ? E->slot_row.p : nullptr,
-            E->order ? E->pos.p : nullptr, d_lp.p, nl, bmin.p, bmax.p);
+            E->order ? E->pos.p : nullptr, d_lp.p, nl, E->tile_rows, bmin.p, bmax.p);
         MPKG_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -499,7 +508,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         runs.push_back({T, T});
         for (int b = 0; b < kBuckets; ++b) {
             const uint64_t i = (uint64_t)T * kBuckets + b;
-            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i] / kTile, hmax[i] / kTile});
+            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i] / E->tile_rows, hmax[i] / E->tile_rows});
         }
         std::sort(runs.begin(), runs.end());
         uint32_t lo = runs[0].first, hi = runs[0].second;
@@ -618,20 +627,21 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
 }
 
 template <int KIND, int G>
-void launch_g(bool sigma, int grid, uint32_t smem, cudaStream_t st, const FusedParams& P) {
+void launch_g(bool sigma, int grid, int threads, uint32_t smem, cudaStream_t st,
+              const FusedParams& P) {
     if (sigma)
-        k_mpk_fused<KIND, true, G><<<grid, kThreads, smem, st>>>(P);
+        k_mpk_fused<KIND, true, G><<<grid, threads, smem, st>>>(P);
     else
-        k_mpk_fused<KIND, false, G><<<grid, kThreads, smem, st>>>(P);
+        k_mpk_fused<KIND, false, G><<<grid, threads, smem, st>>>(P);
 }
 
 template <int KIND>
-void launch_kind(bool sigma, int group, int grid, uint32_t smem, cudaStream_t st,
+void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
                  const FusedParams& P) {
-    if (group == 8)
-        launch_g<KIND, 8>(sigma, grid, smem, st, P);
+    if (E.group == 8)
+        launch_g<KIND, 8>(sigma, E.grid, (int)E.threads, smem, st, P);
     else
-        launch_g<KIND, 16>(sigma, grid, smem, st, P);
+        launch_g<KIND, 16>(sigma, E.grid, (int)E.threads, smem, st, P);
 }
 
 }  // namespace
@@ -663,6 +673,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.p = (uint32_t)a.p;
     P.buf_bytes = E.buf_bytes;
     P.stages = E.stages;
+    P.tile_rows = E.tile_rows;
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
@@ -693,9 +704,9 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const uint32_t smem = E.stages * E.buf_bytes;
     const auto ev = timing_begin(ctx);
     switch (a.kind) {
-        case 0: launch_kind<0>(sigma, E.group, E.grid, smem, st, P); break;
-        case 1: launch_kind<1>(sigma, E.group, E.grid, smem, st, P); break;
-        default: launch_kind<2>(sigma, E.group, E.grid, smem, st, P); break;
+        case 0: launch_kind<0>(sigma, E, smem, st, P); break;
+        case 1: launch_kind<1>(sigma, E, smem, st, P); break;
+        default: launch_kind<2>(sigma, E, smem, st, P); break;
     }
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);
