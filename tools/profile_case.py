@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--group", type=int, default=8)
     ap.add_argument("--pass-powers", type=int, default=0)
     ap.add_argument("--p", type=int, default=0, help="override the config's p")
+    ap.add_argument("--knobs", default="", help="k=v,k=v executor knobs")
     ap.add_argument("--seed", type=int, default=2309)
     args = ap.parse_args()
     import torch
@@ -34,6 +35,9 @@ def main():
     ctx.set_param("order", args.order)
     ctx.set_param("group", args.group)
     ctx.set_param("pass", args.pass_powers)
+    for kv in filter(None, args.knobs.split(",")):
+        k, v = kv.split("=")
+        ctx.set_param(k, int(v))
     if args.slack >= 0:
         ctx.set_param("slack", args.slack)
     dA = ctx.csr(A)
