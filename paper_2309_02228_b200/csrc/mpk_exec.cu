@@ -241,37 +241,80 @@ __global__ void k_gather_x(const double* __restrict__ x, const uint32_t* __restr
     }
 }
 
-// KIND 0 plain, 1 shifted (Newton), 2 polynomial; SIGMA: private row order; G: row group width
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Consumer-only barrier (named barrier 1; the producer warp never joins it).
+__device__ __forceinline__ void consumers_sync(uint32_t n) {
+    asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+__device__ __forceinline__ int consumers_and(int v, uint32_t n) {
+    int r;
+    asm volatile(
+        "{ .reg .pred p; setp.ne.s32 p, %1, 0; bar.red.and.pred p, 1, %2, p; selp.s32 %0, 1, 0, p; }"
+        : "=r"(r)
+        : "r"(v), "r"(n)
+        : "memory");
+    return r;
+}
+
+constexpr uint32_t kNoTicket = 0xffffffffu;
+
+// KIND 0 plain, 1 shifted (Newton), 2 polynomial; SIGMA: private row order; G: gathers in
+// flight per thread in phase 1.
+//
+// Warp-specialised CTA: the LAST warp is the producer, the first blockDim.x-32 threads are
+// consumers.  The producer claims tickets (global atomic, in order), stashes ticket + code in a
+// ring of P.stages smem slots and stages each tile with TMA into the slot's buffer (mbarrier
+// full[slot]); consumers process the slots in order and hand each buffer back through
+// empty[slot].  Claims stay in increasing order per CTA and consumers process them in order, so
+// the lowest unfinished ticket is always being processed: deadlock-free.
 template <int KIND, bool SIGMA, int G>
-__global__ void __launch_bounds__(kMaxThreads) k_mpk_fused(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(128) char smem[];
-    __shared__ __align__(8) uint64_t bars[kMaxStages];
-    // A ring of P.stages claimed tickets per CTA: their tiles are staged by TMA while the CTA
-    // works on the oldest one, so up to stages*buf_bytes of matrix are in flight per CTA.
-    // Still deadlock-free: each CTA processes its claims in increasing order, so the lowest
-    // unfinished ticket is always the one its holder is working on.
-    __shared__ uint32_t s_ticket[kMaxStages];
+    __shared__ __align__(8) uint64_t full[kMaxStages];
+    __shared__ __align__(8) uint64_t empty[kMaxStages];
+    __shared__ uint32_t s_tick[kMaxStages], s_code[kMaxStages];
     const uint32_t tid = threadIdx.x;
+    const uint32_t nc = blockDim.x - 32;  // consumer threads
     const uint32_t S = P.stages;
     if (tid == 0) {
-        for (uint32_t i = 0; i < S; ++i) mbar_init(&bars[i]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t i = 0; i < S; ++i) {
-            const uint32_t t0 = atomicAdd(P.counter, 1u);
-            s_ticket[i] = t0;
-            if (t0 < P.n_tickets) {
-                const uint32_t c0 = P.tickets[t0];
-                if (!(c0 & kBig))
-                    tma_tile(P, c0 & 0xffffffu, c0 & kLastUse, smem + i * P.buf_bytes, &bars[i]);
-            }
+            mbar_init(&full[i]);
+            mbar_init(&empty[i]);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t phases = 0;  // bit i: parity of stage i's next completion
-    for (uint32_t buf = 0;; buf = (buf + 1 == S) ? 0 : buf + 1) {
-        const uint32_t t = s_ticket[buf];
-        if (t >= P.n_tickets) return;
-        const uint32_t code = P.tickets[t];
+    if (tid >= nc) {
+        // ---------------- producer warp (one lane) ----------------
+        if (tid == nc) {
+            for (uint32_t i = 0;; ++i) {
+                const uint32_t slot = i % S;
+                if (i >= S) mbar_wait(&empty[slot], ((i / S) - 1u) & 1u);
+                const uint32_t t = atomicAdd(P.counter, 1u);
+                if (t >= P.n_tickets) {
+                    s_tick[slot] = kNoTicket;
+                    mbar_arrive(&full[slot]);
+                    break;
+                }
+                const uint32_t code = P.tickets[t];
+                s_tick[slot] = t;
+                s_code[slot] = code;
+                if (!(code & kBig))
+                    tma_tile(P, code & 0xffffffu, code & kLastUse, smem + slot * P.buf_bytes, &full[slot]);
+                else
+                    mbar_arrive(&full[slot]);
+            }
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    for (uint32_t i = 0;; ++i) {
+        const uint32_t buf = i % S;
+        mbar_wait(&full[buf], (i / S) & 1u);
+        if (s_tick[buf] == kNoTicket) return;
+        const uint32_t code = s_code[buf];
         const uint32_t T = code & 0xffffffu;
         const uint32_t q = (code >> 24) & 63u;
         if (q > 1) {
@@ -282,45 +325,41 @@ __global__ void __launch_bounds__(kMaxThreads) k_mpk_fused(const __grid_constant
                 int ok = 1;
                 for (uint32_t run = r0; run < r1 && ok; ++run) {
                     const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += blockDim.x)
+                    for (uint32_t u = lo + tid; u <= hi; u += nc)
                         if (ld_relaxed(P.done + u) < q - 1) {
                             ok = 0;
                             break;
                         }
                 }
-                if (__syncthreads_and(ok)) break;
-                __nanosleep(64);
+                if (consumers_and(ok, nc)) break;
+                __nanosleep(32);
             }
             for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += blockDim.x)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += nc)
                     (void)ld_acquire(P.done + u);
+            consumers_sync(nc);  // publishes every consumer's acquires to all consumers
         }
         const bool big = code & kBig;
-        if (!big) {
-            mbar_wait(&bars[buf], (phases >> buf) & 1u);
-            phases ^= 1u << buf;
-        }
-        __syncthreads();  // also publishes every thread's acquires to the whole CTA
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
         const uint64_t e0 = P.tile_off[T];
         double* ps = nullptr;
         if (!big) {
-            // phase 1: all products of the tile, entry-parallel over 256 threads
+            // phase 1: all products of the tile, entry-parallel over the consumer threads
             const uint32_t ne = (uint32_t)(P.tile_off[T + 1] - e0);
             const uint32_t cb_pad = (ne * 4u + 127u) & ~127u;
             const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
             ps = reinterpret_cast<double*>(smem + buf * P.buf_bytes + cb_pad);
             if (q == 1)
-                tile_products<true, G>(cs, ps, ne, src, tid, blockDim.x);
+                tile_products<true, G>(cs, ps, ne, src, tid, nc);
             else
-                tile_products<false, G>(cs, ps, ne, src, tid, blockDim.x);
-            __syncthreads();
+                tile_products<false, G>(cs, ps, ne, src, tid, nc);
+            consumers_sync(nc);
         }
         // phase 2: one thread per row, stored-order sequential sum + epilogue
-        const uint32_t s = T * P.tile_rows + tid;
-        const uint32_t r =
-            tid >= P.tile_rows ? 0xffffffffu : (SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s);
-        if (r < P.n_rows) {
+        for (uint32_t row = tid; row < P.tile_rows; row += nc) {
+            const uint32_t s = T * P.tile_rows + row;
+            const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+            if (r >= P.n_rows) continue;
             const uint32_t len = P.row_len[s];
             const uint64_t c = s >> 5;
             const uint64_t off = P.chunk_off[c];
@@ -352,19 +391,11 @@ __global__ void __launch_bounds__(kMaxThreads) k_mpk_fused(const __grid_constant
                 if (SIGMA && q == P.p) P.z[r] = zr;
             }
         }
-        __syncthreads();
+        consumers_sync(nc);  // tile done: results written, buffer no longer read
         if (tid == 0) {
             st_release(P.done + T, q);
-            // refill the freed stage with the next claim
-            const uint32_t t2 = atomicAdd(P.counter, 1u);
-            s_ticket[buf] = t2;
-            if (t2 < P.n_tickets) {
-                const uint32_t c2 = P.tickets[t2];
-                if (!(c2 & kBig))
-                    tma_tile(P, c2 & 0xffffffu, c2 & kLastUse, smem + buf * P.buf_bytes, &bars[buf]);
-            }
+            mbar_arrive(&empty[buf]);
         }
-        // s_ticket[buf] is read again only S iterations later, after S more barriers.
     }
 }
 
@@ -470,10 +501,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     int occ = 0;
     if (E->group == 8) {
         configure_kernels<8>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads + 32, smem));
     } else {
         configure_kernels<16>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, (int)E->threads, smem));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, (int)E->threads + 32, smem));
     }
     occ = std::max(1, occ);
     E->occ_max = occ;
@@ -639,9 +670,9 @@ template <int KIND>
 void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
                  const FusedParams& P) {
     if (E.group == 8)
-        launch_g<KIND, 8>(sigma, E.grid, (int)E.threads, smem, st, P);
+        launch_g<KIND, 8>(sigma, E.grid, (int)E.threads + 32, smem, st, P);
     else
-        launch_g<KIND, 16>(sigma, E.grid, (int)E.threads, smem, st, P);
+        launch_g<KIND, 16>(sigma, E.grid, (int)E.threads + 32, smem, st, P);
 }
 
 }  // namespace
