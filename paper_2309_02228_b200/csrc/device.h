@@ -100,7 +100,7 @@ struct mpkg_ctx_s {
     int64_t ctas_per_sm = 0;  // >0: cap on resident fused-kernel CTAs per SM
     int64_t group = 8;        // phase-1 gathers in flight per thread (8 or 16)
     int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
-    int64_t threads = 256;    // fused-kernel threads per CTA (256 or 512)
+    int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;

@@ -147,51 +147,23 @@ __device__ __forceinline__ uint64_t l2_policy(bool last_use) {
     return last_use ? l2_policy_first() : l2_policy_last();
 }
 
-// Thread 0 only: stage one tile (its column indices, then its values: each one contiguous
-// range of the SELL arrays) into `buf` with two 1D TMA bulk copies completing on `bar`.
+// Producer lane only: stage one tile's column indices (one contiguous range of the SELL column
+// array) into `buf` with a 1D TMA bulk copy completing on `bar`.
 __device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool last_use,
                                          char* buf, uint64_t* bar) {
     const uint64_t e0 = P.tile_off[T], e1 = P.tile_off[T + 1];
-    const uint32_t ne = (uint32_t)(e1 - e0);
-    const uint32_t cb = ne * 4u, vb = ne * 8u, cb_pad = (cb + 127u) & ~127u;
+    const uint32_t cb = (uint32_t)(e1 - e0) * 4u;
     const uint64_t pol = l2_policy(last_use);
     // order earlier generic-proxy accesses of this buffer before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(cb + vb)
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cb)
                  : "memory");
-    if (ne) {
+    if (cb)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
             "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf)),
             "l"(P.cols + e0), "r"(cb), "r"(smem_u32(bar)), "l"(pol)
             : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf + cb_pad)),
-            "l"(P.vals + e0), "r"(vb), "r"(smem_u32(bar)), "l"(pol)
-            : "memory");
-    }
-}
-
-// Phase 1 of the tile kernel: every entry's product v*x[col] (all gathers independent, U per
-// thread in flight), written in place over the staged values.
-template <bool READONLY, int U>
-__device__ __forceinline__ void tile_products(const uint32_t* cs, double* ps, uint32_t ne,
-                                              const double* src, uint32_t tid, uint32_t nthreads) {
-    for (uint32_t base = 0; base < ne; base += nthreads * U) {
-        double xv[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const uint32_t e = base + j * nthreads + tid;
-            xv[j] = e < ne ? ld_vec<READONLY>(src + cs[e]) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const uint32_t e = base + j * nthreads + tid;
-            if (e < ne) ps[e] = __dmul_rn(ps[e], xv[j]);
-        }
-    }
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -342,20 +314,9 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
         const bool big = code & kBig;
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
         const uint64_t e0 = P.tile_off[T];
-        double* ps = nullptr;
-        if (!big) {
-            // phase 1: all products of the tile, entry-parallel over the consumer threads
-            const uint32_t ne = (uint32_t)(P.tile_off[T + 1] - e0);
-            const uint32_t cb_pad = (ne * 4u + 127u) & ~127u;
-            const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
-            ps = reinterpret_cast<double*>(smem + buf * P.buf_bytes + cb_pad);
-            if (q == 1)
-                tile_products<true, G>(cs, ps, ne, src, tid, nc);
-            else
-                tile_products<false, G>(cs, ps, ne, src, tid, nc);
-            consumers_sync(nc);
-        }
-        // phase 2: one thread per row, stored-order sequential sum + epilogue
+        const uint32_t* cs = reinterpret_cast<const uint32_t*>(smem + buf * P.buf_bytes);
+        const uint64_t pol = l2_policy(code & kLastUse);
+        // one thread per row: stored-order sequential accumulation + epilogue
         for (uint32_t row = tid; row < P.tile_rows; row += nc) {
             const uint32_t s = T * P.tile_rows + row;
             const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
@@ -366,9 +327,10 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
             double acc;
             if (!big) {
-                acc = sell_row_sum_smem(ps, (uint32_t)(off - e0), L, s & 31, len);
+                const uint32_t rel = (uint32_t)(off - e0);
+                acc = q == 1 ? sell_row_dot_staged<true, G>(cs, P.vals, rel, off, L, s & 31, len, src, pol)
+                             : sell_row_dot_staged<false, G>(cs, P.vals, rel, off, L, s & 31, len, src, pol);
             } else {
-                const uint64_t pol = l2_policy(code & kLastUse);
                 acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
                              : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
             }
@@ -451,7 +413,8 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->n_rows = A->n_rows;
     E->n_slots = (A->n_rows + 31u) & ~31u;
     E->tile_rows = ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
-    E->threads = ctx->threads == 512 ? 512u : 256u;
+    // consumer threads: one per tile row unless forced
+    E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
     if (E->threads < E->tile_rows) E->threads = E->tile_rows;
     E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
     if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
@@ -475,7 +438,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             toff[T] = off[std::min<uint64_t>((uint64_t)T * (E->tile_rows / 32), E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
             const uint64_t ne = toff[T + 1] - toff[T];
-            const uint64_t bytes = ((4 * ne + 127) & ~127ull) + 8 * ne;  // staged cols + vals
+            const uint64_t bytes = (4 * ne + 127) & ~127ull;  // staged: column indices
             E->tile_bytes[T] = 12 * ne + E->tile_rows * 8 * 3;
             if (bytes > kMaxBufBytes)
                 E->big[T] = 1;

@@ -122,6 +122,48 @@ __device__ __forceinline__ double sell_row_dot(const uint32_t* __restrict__ cols
     return acc;
 }
 
+// Same as sell_row_dot with the tile's COLUMN indices staged in shared memory (TMA, identical
+// layout, offsets relative to the tile start `rel`) and the values streamed from global memory:
+// gather addresses are available at shared-memory latency, so each group's G gathers issue at
+// once and overlap the value loads.
+template <bool READONLY, int G>
+__device__ __forceinline__ double sell_row_dot_staged(const uint32_t* cols_s,
+                                                      const double* __restrict__ vals,
+                                                      uint32_t rel, uint64_t off, uint32_t L,
+                                                      uint32_t lane, uint32_t len,
+                                                      const double* src, uint64_t pol) {
+    static_assert(G % 2 == 0, "group must be even");
+    double acc = 0.0;
+    const uint32_t Lp = L & ~1u;
+    for (uint32_t k0 = 0; k0 < len; k0 += G) {
+        double v[G], x[G];
+#pragma unroll
+        for (int j = 0; j < G; j += 2) {
+            const uint32_t k = k0 + j;
+            if (k + 1 < Lp) {
+                const uint32_t e = (k >> 1) * 64u + lane * 2u;
+                const uint2 cc = *reinterpret_cast<const uint2*>(cols_s + rel + e);
+                const double2 vv = ld_mat_d2(reinterpret_cast<const double2*>(vals + off + e), pol);
+                v[j] = vv.x, v[j + 1] = vv.y;
+                x[j] = k < len ? ld_vec<READONLY>(src + cc.x) : 0.0;
+                x[j + 1] = k + 1 < len ? ld_vec<READONLY>(src + cc.y) : 0.0;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t kk = k + i;
+                    const uint32_t e = sell_pos(kk, Lp, lane);
+                    v[j + i] = kk < len ? ld_mat_d(vals + off + e, pol) : 0.0;
+                    x[j + i] = kk < len ? ld_vec<READONLY>(src + cols_s[rel + e]) : 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+            if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+    }
+    return acc;
+}
+
 // Sequential, stored-order sum of a row's products already computed in shared memory in the
 // SELL layout (two-phase tile kernel): same additions in the same order as sell_row_dot.
 __device__ __forceinline__ double sell_row_sum_smem(const double* prod, uint32_t rel, uint32_t L,
