@@ -267,7 +267,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             require(value == 64 || value == 128 || value == 256, "ctx_set_param: tile_rows must be 64, 128 or 256");
             ctx->tile_rows = value;
         } else if (k == "threads") {
-            require(value == 256 || value == 512, "ctx_set_param: threads must be 256 or 512");
+            require(value == 0 || value == 256 || value == 512,
+                    "ctx_set_param: threads must be 0 (one per tile row), 256 or 512");
             ctx->threads = value;
         }
         else
