@@ -261,6 +261,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->group = value;
         else if (k == "stages")
             ctx->stages = value;
+        else if (k == "kernel") {
+            require(value == 0 || value == 1, "ctx_set_param: kernel must be 0 (lean) or 1 (staged)");
+            ctx->kernel = value;
+        }
         else if (k == "kernel_timing")
             ctx->kernel_timing = value != 0;
         else if (k == "tile_rows") {

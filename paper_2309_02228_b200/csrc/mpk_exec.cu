@@ -75,6 +75,7 @@ struct Executor {
     int group = 16;                           // row group width G of the kernel instance
     int64_t stage_knob = 0;                   // ctx->stages the executor was built with
     int64_t tile_knob = 0, thread_knob = 0;   // ctx->tile_rows / ctx->threads likewise
+    int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused (staged)
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -361,6 +362,79 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
     }
 }
 
+// Lean variant ("kernel" knob 0): no shared-memory staging and no producer warp, so registers
+// stay low and many warps are resident (the row loop is latency-bound: throughput follows
+// resident warps).  One thread per tile row; thread 0 claims the next ticket while the current
+// one runs (double-buffered claim, deadlock-free for the same reason as above).
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_mpk_lean(const __grid_constant__ FusedParams P) {
+    __shared__ uint32_t s_ticket[2];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t nt = blockDim.x;
+    if (tid == 0) s_ticket[0] = atomicAdd(P.counter, 1u);
+    __syncthreads();
+    for (uint32_t buf = 0;; buf ^= 1u) {
+        const uint32_t t = s_ticket[buf];
+        if (t >= P.n_tickets) return;
+        if (tid == 0) s_ticket[buf ^ 1u] = atomicAdd(P.counter, 1u);
+        const uint32_t code = P.tickets[t];
+        const uint32_t T = code & 0xffffffu;
+        const uint32_t q = (code >> 24) & 63u;
+        if (q > 1) {
+            const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
+            for (;;) {
+                int ok = 1;
+                for (uint32_t run = r0; run < r1 && ok; ++run) {
+                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
+                    for (uint32_t u = lo + tid; u <= hi; u += nt)
+                        if (ld_relaxed(P.done + u) < q - 1) {
+                            ok = 0;
+                            break;
+                        }
+                }
+                if (__syncthreads_and(ok)) break;
+                __nanosleep(32);
+            }
+            for (uint32_t run = r0; run < r1; ++run)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += nt)
+                    (void)ld_acquire(P.done + u);
+            __syncthreads();
+        }
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        const uint64_t pol = l2_policy(code & kLastUse);
+        for (uint32_t row = tid; row < P.tile_rows; row += nt) {
+            const uint32_t s = T * P.tile_rows + row;
+            const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+            if (r >= P.n_rows) continue;
+            const uint32_t len = P.row_len[s];
+            const uint64_t c = s >> 5;
+            const uint64_t off = P.chunk_off[c];
+            const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
+            double acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                                : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+            if constexpr (KIND == 1) {
+                const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
+                const double own = src[s];
+                const double own2 = b2 != 0.0 ? P.V[(uint64_t)(q - 2) * P.vstride + s] : 0.0;
+                acc = shift_epilogue(acc, a, b2, own, own2);
+            }
+            P.V[(uint64_t)q * P.vstride + s] = acc;
+            if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
+            if constexpr (KIND == 2) {
+                double zr;
+                if (q == 1)
+                    zr = __dadd_rn(__dmul_rn(P.coef[0], src[s]), __dmul_rn(P.coef[1], acc));
+                else
+                    zr = __dadd_rn(P.zs[s], __dmul_rn(P.coef[q], acc));
+                P.zs[s] = zr;
+                if (SIGMA && q == P.p) P.z[r] = zr;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) st_release(P.done + T, q);
+    }
+}
+
 // Sparse-table range maximum over r[0..n).
 struct RangeMax {
     std::vector<std::vector<int64_t>> t;
@@ -393,7 +467,8 @@ void configure_kernels(uint32_t smem_bytes) {
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
         P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
-        P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads) {
+        P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads &&
+        P->exec->kernel == (int)ctx->kernel) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -462,7 +537,12 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->tile_knob = ctx->tile_rows;
     E->thread_knob = ctx->threads;
     int occ = 0;
-    if (E->group == 8) {
+    E->kernel = (int)ctx->kernel;
+    if (E->kernel == 0) {
+        E->threads = E->tile_rows;
+        E->stages = 1;
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true>, (int)E->tile_rows, 0));
+    } else if (E->group == 8) {
         configure_kernels<8>(smem);
         MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads + 32, smem));
     } else {
@@ -697,10 +777,22 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     const uint32_t smem = E.stages * E.buf_bytes;
     const auto ev = timing_begin(ctx);
-    switch (a.kind) {
-        case 0: launch_kind<0>(sigma, E, smem, st, P); break;
-        case 1: launch_kind<1>(sigma, E, smem, st, P); break;
-        default: launch_kind<2>(sigma, E, smem, st, P); break;
+    if (E.kernel == 0) {
+        const int nt = (int)E.tile_rows;
+        switch (a.kind * 2 + (sigma ? 1 : 0)) {
+            case 0: k_mpk_lean<0, false><<<E.grid, nt, 0, st>>>(P); break;
+            case 1: k_mpk_lean<0, true><<<E.grid, nt, 0, st>>>(P); break;
+            case 2: k_mpk_lean<1, false><<<E.grid, nt, 0, st>>>(P); break;
+            case 3: k_mpk_lean<1, true><<<E.grid, nt, 0, st>>>(P); break;
+            case 4: k_mpk_lean<2, false><<<E.grid, nt, 0, st>>>(P); break;
+            default: k_mpk_lean<2, true><<<E.grid, nt, 0, st>>>(P); break;
+        }
+    } else {
+        switch (a.kind) {
+            case 0: launch_kind<0>(sigma, E, smem, st, P); break;
+            case 1: launch_kind<1>(sigma, E, smem, st, P); break;
+            default: launch_kind<2>(sigma, E, smem, st, P); break;
+        }
     }
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);

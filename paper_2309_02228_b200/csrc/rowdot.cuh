@@ -122,6 +122,43 @@ __device__ __forceinline__ double sell_row_dot(const uint32_t* __restrict__ cols
     return acc;
 }
 
+// Register-light, software-pipelined row dot straight from global memory: the next pair's
+// column indices and values are loaded while the current pair's x-gathers are in flight, so
+// each pair costs one dependent round trip instead of two.  Same additions, same order.
+template <bool READONLY>
+__device__ __forceinline__ double sell_row_dot_pipe(const uint32_t* __restrict__ cols,
+                                                    const double* __restrict__ vals, uint64_t off,
+                                                    uint32_t L, uint32_t lane, uint32_t len,
+                                                    const double* src, uint64_t pol) {
+    double acc = 0.0;
+    const uint32_t Lp = L & ~1u;
+    const uint32_t npairs = (len < Lp ? len : Lp) >> 1;  // full pairs inside this row
+    const uint2* cp = reinterpret_cast<const uint2*>(cols + off) + lane;
+    const double2* vp = reinterpret_cast<const double2*>(vals + off) + lane;
+    uint32_t k = 0;
+    if (npairs) {
+        uint2 c = ld_mat_u2(cp, pol);
+        double2 v = ld_mat_d2(vp, pol);
+        for (uint32_t j = 0; j < npairs; ++j) {
+            const double x0 = ld_vec<READONLY>(src + c.x);
+            const double x1 = ld_vec<READONLY>(src + c.y);
+            const double2 vc = v;
+            if (j + 1 < npairs) {  // prefetch the next pair while the gathers are in flight
+                c = ld_mat_u2(cp + (j + 1) * 32, pol);
+                v = ld_mat_d2(vp + (j + 1) * 32, pol);
+            }
+            acc = __dadd_rn(acc, __dmul_rn(vc.x, x0));
+            acc = __dadd_rn(acc, __dmul_rn(vc.y, x1));
+        }
+        k = npairs * 2;
+    }
+    for (; k < len; ++k) {
+        const uint64_t e = off + sell_pos(k, Lp, lane);
+        acc = __dadd_rn(acc, __dmul_rn(ld_mat_d(vals + e, pol), ld_vec<READONLY>(src + ld_mat_u32(cols + e, pol))));
+    }
+    return acc;
+}
+
 // Same as sell_row_dot with the tile's COLUMN indices staged in shared memory (TMA, identical
 // layout, offsets relative to the tile start `rel`) and the values streamed from global memory:
 // gather addresses are available at shared-memory latency, so each group's G gathers issue at
