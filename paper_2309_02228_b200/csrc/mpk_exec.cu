@@ -75,7 +75,8 @@ struct Executor {
     int group = 16;                           // row group width G of the kernel instance
     int64_t stage_knob = 0;                   // ctx->stages the executor was built with
     int64_t tile_knob = 0, thread_knob = 0;   // ctx->tile_rows / ctx->threads likewise
-    int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused (staged)
+    int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused, 2: k_mpk_warptile
+    uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -102,6 +103,7 @@ struct FusedParams {
     uint32_t buf_bytes;
     uint32_t stages;
     uint32_t tile_rows;
+    uint32_t wt_lmax;  // warp-tile kernel: widest chunk handled flat (smem slice per warp)
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -435,6 +437,119 @@ __global__ void __launch_bounds__(256) k_mpk_lean(const __grid_constant__ FusedP
     }
 }
 
+// Warp-tile variant ("kernel" knob 2): each warp owns one 32-row SELL chunk of the tile.
+// Phase 1 walks the chunk's entries FLAT (lane l takes entries l, l+32, ...: coalesced column /
+// value loads, all x-gathers independent, software-pipelined in batches of U) and writes every
+// product v*x[col] to the warp's shared-memory slice at the same flat position; after
+// __syncwarp, phase 2 lets lane r sum ITS row's products in stored order (bitwise identical to
+// the row loop: same products, same additions, same order).  A row costs ~L/(32U) pipelined
+// round trips instead of ~L/2 dependent ones; no CTA-wide barrier inside the tile.  Chunks wider
+// than `wt_lmax` fall back to the row loop.
+template <int KIND, bool SIGMA, int U>
+__global__ void __launch_bounds__(128) k_mpk_warptile(const __grid_constant__ FusedParams P) {
+    extern __shared__ __align__(16) double prod[];  // [4 warps][32 * wt_lmax]
+    __shared__ uint32_t s_ticket[2];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    double* my = prod + (uint64_t)warp * 32u * P.wt_lmax;
+    if (tid == 0) s_ticket[0] = atomicAdd(P.counter, 1u);
+    __syncthreads();
+    for (uint32_t buf = 0;; buf ^= 1u) {
+        const uint32_t t = s_ticket[buf];
+        if (t >= P.n_tickets) return;
+        if (tid == 0) s_ticket[buf ^ 1u] = atomicAdd(P.counter, 1u);
+        const uint32_t code = P.tickets[t];
+        const uint32_t T = code & 0xffffffu;
+        const uint32_t q = (code >> 24) & 63u;
+        if (q > 1) {
+            const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
+            for (;;) {
+                int ok = 1;
+                for (uint32_t run = r0; run < r1 && ok; ++run) {
+                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
+                    for (uint32_t u = lo + tid; u <= hi; u += 128u)
+                        if (ld_relaxed(P.done + u) < q - 1) {
+                            ok = 0;
+                            break;
+                        }
+                }
+                if (__syncthreads_and(ok)) break;
+                __nanosleep(32);
+            }
+            for (uint32_t run = r0; run < r1; ++run)
+                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += 128u)
+                    (void)ld_acquire(P.done + u);
+            __syncthreads();
+        }
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        const uint64_t pol = l2_policy(code & kLastUse);
+        const uint32_t s = T * 128u + tid;  // this lane's row slot; the warp's chunk = s >> 5
+        const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+        const bool chunk_ok = (T * 128u + warp * 32u) < P.n_slots;
+        uint64_t off = 0;
+        uint32_t L = 0;
+        if (chunk_ok) {
+            off = P.chunk_off[s >> 5];
+            L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
+        }
+        double acc = 0.0;
+        const uint32_t len = (r < P.n_rows) ? P.row_len[s] : 0u;
+        if (chunk_ok && L <= P.wt_lmax) {
+            // phase 1: flat products of the chunk (32*L entries), U gathers in flight per lane
+            const uint32_t ne = 32u * L;
+            const uint32_t* cc = P.cols + off;
+            const double* vv = P.vals + off;
+            for (uint32_t e0 = 0; e0 < ne; e0 += 32u * U) {
+                uint32_t c[U];
+                double v[U], x[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t e = e0 + j * 32u + lane;
+                    c[j] = e < ne ? ld_mat_u32(cc + e, pol) : 0u;
+                    v[j] = e < ne ? ld_mat_d(vv + e, pol) : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t e = e0 + j * 32u + lane;
+                    x[j] = e < ne ? (q == 1 ? ld_vec<true>(src + c[j]) : ld_vec<false>(src + c[j])) : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t e = e0 + j * 32u + lane;
+                    if (e < ne) my[e] = __dmul_rn(v[j], x[j]);
+                }
+            }
+            __syncwarp();
+            // phase 2: lane = row, stored-order sum of its products
+            if (r < P.n_rows) acc = sell_row_sum_smem(my, 0u, L, lane, len);
+            __syncwarp();
+        } else if (r < P.n_rows) {
+            acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, lane, len, src, pol)
+                         : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, lane, len, src, pol);
+        }
+        if (r < P.n_rows) {
+            if constexpr (KIND == 1) {
+                const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
+                const double own = src[s];
+                const double own2 = b2 != 0.0 ? P.V[(uint64_t)(q - 2) * P.vstride + s] : 0.0;
+                acc = shift_epilogue(acc, a, b2, own, own2);
+            }
+            P.V[(uint64_t)q * P.vstride + s] = acc;
+            if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
+            if constexpr (KIND == 2) {
+                double zr;
+                if (q == 1)
+                    zr = __dadd_rn(__dmul_rn(P.coef[0], src[s]), __dmul_rn(P.coef[1], acc));
+                else
+                    zr = __dadd_rn(P.zs[s], __dmul_rn(P.coef[q], acc));
+                P.zs[s] = zr;
+                if (SIGMA && q == P.p) P.z[r] = zr;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) st_release(P.done + T, q);
+    }
+}
+
 // Sparse-table range maximum over r[0..n).
 struct RangeMax {
     std::vector<std::vector<int64_t>> t;
@@ -464,6 +579,32 @@ void configure_kernels(uint32_t smem_bytes) {
         MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
 }
 
+void configure_warptile(uint32_t lmax) {
+    const int smem = (int)(128 * lmax * 8);
+    const void* ks[] = {
+        (const void*)k_mpk_warptile<0, false, 4>, (const void*)k_mpk_warptile<0, true, 4>,
+        (const void*)k_mpk_warptile<1, false, 4>, (const void*)k_mpk_warptile<1, true, 4>,
+        (const void*)k_mpk_warptile<2, false, 4>, (const void*)k_mpk_warptile<2, true, 4>,
+        (const void*)k_mpk_warptile<0, false, 8>, (const void*)k_mpk_warptile<0, true, 8>,
+        (const void*)k_mpk_warptile<1, false, 8>, (const void*)k_mpk_warptile<1, true, 8>,
+        (const void*)k_mpk_warptile<2, false, 8>, (const void*)k_mpk_warptile<2, true, 8>};
+    for (const void* k : ks)
+        MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+}
+
+template <int U>
+void launch_warptile(int kind, bool sigma, int grid, uint32_t smem, cudaStream_t st,
+                     const FusedParams& P) {
+    switch (kind * 2 + (sigma ? 1 : 0)) {
+        case 0: k_mpk_warptile<0, false, U><<<grid, 128, smem, st>>>(P); break;
+        case 1: k_mpk_warptile<0, true, U><<<grid, 128, smem, st>>>(P); break;
+        case 2: k_mpk_warptile<1, false, U><<<grid, 128, smem, st>>>(P); break;
+        case 3: k_mpk_warptile<1, true, U><<<grid, 128, smem, st>>>(P); break;
+        case 4: k_mpk_warptile<2, false, U><<<grid, 128, smem, st>>>(P); break;
+        default: k_mpk_warptile<2, true, U><<<grid, 128, smem, st>>>(P); break;
+    }
+}
+
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
         P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
@@ -488,6 +629,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->n_rows = A->n_rows;
     E->n_slots = (A->n_rows + 31u) & ~31u;
     E->tile_rows = ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
+    if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
     // consumer threads: one per tile row unless forced
     E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
     if (E->threads < E->tile_rows) E->threads = E->tile_rows;
@@ -521,6 +663,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
                 max_buf = std::max(max_buf, bytes);
         }
         E->buf_bytes = (uint32_t)((max_buf + 127) & ~127ull);
+        uint64_t lmax = 1;  // widest chunk (entries per lane), capped for the warp-tile slice
+        for (uint32_t c = 0; c < E->S->n_chunks; ++c)
+            lmax = std::max<uint64_t>(lmax, std::min<uint64_t>((off[c + 1] - off[c]) / 32, 64));
+        E->wt_lmax = (uint32_t)lmax;
         E->tile_off.alloc(nt + 1);
         MPKG_CUDA(cudaMemcpyAsync(E->tile_off.p, toff.data(), 8ull * (nt + 1), cudaMemcpyHostToDevice, st));
     }
@@ -538,7 +684,15 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->thread_knob = ctx->threads;
     int occ = 0;
     E->kernel = (int)ctx->kernel;
-    if (E->kernel == 0) {
+    if (E->kernel == 2) {
+        E->threads = 128;
+        E->stages = 1;
+        configure_warptile(E->wt_lmax);
+        if (E->group == 16)
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 8>, 128, 128 * E->wt_lmax * 8));
+        else
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 4>, 128, 128 * E->wt_lmax * 8));
+    } else if (E->kernel == 0) {
         E->threads = E->tile_rows;
         E->stages = 1;
         MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true>, (int)E->tile_rows, 0));
@@ -748,6 +902,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.buf_bytes = E.buf_bytes;
     P.stages = E.stages;
     P.tile_rows = E.tile_rows;
+    P.wt_lmax = E.wt_lmax;
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
@@ -777,7 +932,13 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     const uint32_t smem = E.stages * E.buf_bytes;
     const auto ev = timing_begin(ctx);
-    if (E.kernel == 0) {
+    if (E.kernel == 2) {
+        const uint32_t wsmem = 128 * E.wt_lmax * 8;
+        if (E.group == 16)
+            launch_warptile<8>(a.kind, sigma, E.grid, wsmem, st, P);
+        else
+            launch_warptile<4>(a.kind, sigma, E.grid, wsmem, st, P);
+    } else if (E.kernel == 0) {
         const int nt = (int)E.tile_rows;
         switch (a.kind * 2 + (sigma ? 1 : 0)) {
             case 0: k_mpk_lean<0, false><<<E.grid, nt, 0, st>>>(P); break;
