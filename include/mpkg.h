@@ -130,6 +130,13 @@ int mpkg_greedy_group(const uint64_t* level_fp, uint32_t n_levels, uint64_t targ
 /* plan.hpp:88-115 group_levels. */
 int mpkg_group_levels(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A_perm, uint64_t cache_bytes,
                       int p_m, mpkg_plan_t* out);
+/* Builds a plan from host fields (plan.hpp:41-54 ExecutionPlan), e.g. one made by hand as in
+ * the reference's schedule tests.  level_ptr (n_levels+1 entries) may be NULL: the executor
+ * then derives dependencies without level buckets (still exact, coarser). */
+int mpkg_plan_create(int p_m, int sub_powers, uint32_t n_rows, uint64_t cache_bytes,
+                     uint64_t target_bytes, uint32_t n_groups, const uint32_t* group_rows,
+                     const uint32_t* group_level_ptr, const uint64_t* group_footprint,
+                     uint32_t n_levels, const uint32_t* level_ptr, mpkg_plan_t* out);
 int mpkg_plan_info(mpkg_plan_t P, int* p_m, int* sub_powers, uint32_t* n_rows,
                    uint64_t* cache_bytes, uint64_t* target_bytes, uint32_t* n_groups);
 /* Any output may be NULL: group_rows / group_level_ptr have n_groups+1, footprint n_groups. */

@@ -1,0 +1,517 @@
+// mpkg.hpp — C++ facade with the reference's interface over the mpkg C ABI.
+//
+// Mirrors namespace `mpk` of the reference (proj/include/mpk/{csr,levels,plan,execute,mpk,
+// vector_block,generators}.hpp) name for name, type for type and exception for exception, so a
+// reference call site switches with `namespace mpk = mpkg;` and links libmpkg.so.  All compute
+// (build_levels, permute, validate_levels, spmv, baseline_mpk, mpk, *_shifted, tune_p) runs on
+// the GPU through include/mpkg.h; status codes come back as the reference's exceptions:
+// MPKG_EINVAL -> std::invalid_argument, MPKG_ERANGE -> std::out_of_range, else runtime_error.
+//
+// Host-side types own host arrays exactly like the reference; device copies are made on first
+// use and cached per object (the reference treats these structures as immutable after
+// construction).  Call `invalidate()` after mutating one in place.
+//
+// Exception: `execute(plan, kernel)` (execute.hpp:79-113) takes an arbitrary host callback and
+// therefore cannot cross to the GPU; it runs the callback in the reference's wavefront order on
+// the calling thread.  The GPU power kernels never use it.
+#pragma once
+
+#include <algorithm>
+#include <complex>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mpkg.h"
+
+namespace mpkg {
+
+using index_t = std::uint32_t;  // csr.hpp:41
+
+namespace detail {
+
+inline void check(int rc) {
+    if (rc == MPKG_OK) return;
+    const std::string msg = mpkg_last_error();
+    if (rc == MPKG_EINVAL) throw std::invalid_argument(msg);
+    if (rc == MPKG_ERANGE) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+
+struct CtxHolder {
+    mpkg_ctx_t h = nullptr;
+    explicit CtxHolder(int device) { check(mpkg_ctx_create(device, &h)); }
+    ~CtxHolder() { mpkg_ctx_destroy(h); }
+};
+
+struct CsrHolder {
+    mpkg_csr_t h = nullptr;
+    const void *rp = nullptr, *ci = nullptr, *v = nullptr;
+    std::size_t nnz = 0;
+    ~CsrHolder() { mpkg_csr_destroy(h); }
+};
+struct LevelsHolder {
+    mpkg_levels_t h = nullptr;
+    ~LevelsHolder() { mpkg_levels_destroy(h); }
+};
+struct PlanHolder {
+    mpkg_plan_t h = nullptr;
+    ~PlanHolder() { mpkg_plan_destroy(h); }
+};
+
+}  // namespace detail
+
+/// The device the facade runs on (replaces resolve_threads, threading.hpp:34-46): device 0, or
+/// the index in MPKG_DEVICE.
+inline mpkg_ctx_t device_context() {
+    static detail::CtxHolder ctx([] {
+        const char* e = std::getenv("MPKG_DEVICE");
+        return e ? std::atoi(e) : 0;
+    }());
+    return ctx.h;
+}
+
+/// csr.hpp:44-48
+struct Triplet {
+    index_t row = 0;
+    index_t col = 0;
+    double val = 0.0;
+};
+
+/// csr.hpp:57-65
+struct CsrMatrix {
+    index_t n_rows = 0;
+    index_t n_cols = 0;
+    std::vector<index_t> row_ptr;
+    std::vector<index_t> col_idx;
+    std::vector<double> values;
+
+    index_t nnz() const { return row_ptr.empty() ? 0 : row_ptr[n_rows]; }
+    void invalidate() const { dev_.reset(); }
+
+    /// Device copy (uploaded on first use; re-uploaded if the arrays were reallocated).
+    mpkg_csr_t device() const {
+        if (!dev_ || dev_->rp != row_ptr.data() || dev_->ci != col_idx.data() ||
+            dev_->v != values.data() || dev_->nnz != col_idx.size()) {
+            auto d = std::make_shared<detail::CsrHolder>();
+            detail::check(mpkg_csr_create(device_context(), n_rows, n_cols, row_ptr.data(),
+                                          col_idx.data(), values.data(), &d->h));
+            d->rp = row_ptr.data(), d->ci = col_idx.data(), d->v = values.data();
+            d->nnz = col_idx.size();
+            dev_ = d;
+        }
+        return dev_->h;
+    }
+
+   private:
+    mutable std::shared_ptr<detail::CsrHolder> dev_;
+};
+
+/// levels.hpp:43-57
+struct LevelStructure {
+    index_t n_rows = 0;
+    std::vector<index_t> levels;
+    std::vector<index_t> perm;
+    std::vector<index_t> inv_perm;
+    std::vector<index_t> level_ptr;
+
+    index_t n_levels() const {
+        return level_ptr.empty() ? 0 : static_cast<index_t>(level_ptr.size() - 1);
+    }
+    index_t level_of_permuted(index_t new_row) const { return levels[inv_perm[new_row]]; }
+    void invalidate() const { dev_.reset(); }
+
+    mpkg_levels_t device() const {
+        if (!dev_) {
+            auto d = std::make_shared<detail::LevelsHolder>();
+            detail::check(mpkg_levels_create(device_context(), n_rows, n_levels(),
+                                             levels.empty() ? nullptr : levels.data(),
+                                             perm.empty() ? nullptr : perm.data(),
+                                             inv_perm.empty() ? nullptr : inv_perm.data(),
+                                             level_ptr.data(), &d->h));
+            dev_ = d;
+        }
+        return dev_->h;
+    }
+
+   private:
+    mutable std::shared_ptr<detail::LevelsHolder> dev_;
+    friend LevelStructure build_levels(const CsrMatrix&);
+};
+
+/// plan.hpp:41-54 (plus the level offsets the GPU executor derives dependencies from)
+struct ExecutionPlan {
+    int p_m = 1;
+    int sub_powers = 1;
+    index_t n_rows = 0;
+    std::size_t cache_bytes = 0;
+    std::size_t target_bytes = 0;
+    std::vector<index_t> group_rows;
+    std::vector<index_t> group_level_ptr;
+    std::vector<std::size_t> group_footprint;
+    std::vector<index_t> level_ptr;  // optional: level offsets of the structure it was built on
+
+    index_t n_groups() const {
+        return group_rows.empty() ? 0 : static_cast<index_t>(group_rows.size() - 1);
+    }
+    void invalidate() const { dev_.reset(); }
+
+    mpkg_plan_t device() const {
+        if (!dev_) {
+            auto d = std::make_shared<detail::PlanHolder>();
+            std::vector<std::uint64_t> fp(group_footprint.begin(), group_footprint.end());
+            detail::check(mpkg_plan_create(
+                p_m, sub_powers, n_rows, cache_bytes, target_bytes, n_groups(),
+                group_rows.empty() ? nullptr : group_rows.data(),
+                group_level_ptr.empty() ? nullptr : group_level_ptr.data(),
+                fp.empty() ? nullptr : fp.data(),
+                level_ptr.empty() ? 0u : static_cast<index_t>(level_ptr.size() - 1),
+                level_ptr.empty() ? nullptr : level_ptr.data(), &d->h));
+            dev_ = d;
+        }
+        return dev_->h;
+    }
+
+   private:
+    mutable std::shared_ptr<detail::PlanHolder> dev_;
+};
+
+/// vector_block.hpp:38-57
+struct VectorBlock {
+    std::size_t rows = 0;
+    std::size_t slices = 0;
+    std::vector<double> data;
+
+    VectorBlock() = default;
+    VectorBlock(std::size_t rows_, std::size_t slices_)
+        : rows(rows_), slices(slices_), data(rows_ * slices_, 0.0) {}
+
+    double* slice(std::size_t p) {
+        if (p >= slices) throw std::out_of_range("VectorBlock::slice");
+        return data.data() + p * rows;
+    }
+    const double* slice(std::size_t p) const {
+        if (p >= slices) throw std::out_of_range("VectorBlock::slice");
+        return data.data() + p * rows;
+    }
+    void zero() { std::fill(data.begin(), data.end(), 0.0); }
+};
+
+// ---- csr.hpp ---------------------------------------------------------------------------------
+/// csr.hpp:72-110 (host construction helper: stable sort by (row, col), duplicates summed in
+/// input order, starting from 0.0).
+inline CsrMatrix from_coo(index_t n_rows, index_t n_cols, std::vector<Triplet> entries) {
+    if (entries.size() >= (std::size_t{1} << 31))
+        throw std::invalid_argument("from_coo: entry count exceeds 32-bit index range");
+    for (const Triplet& t : entries)
+        if (t.row >= n_rows || t.col >= n_cols)
+            throw std::invalid_argument("from_coo: entry index out of range");
+    std::vector<std::size_t> idx(entries.size());
+    for (std::size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a, std::size_t b) {
+        return entries[a].row != entries[b].row ? entries[a].row < entries[b].row
+                                                : entries[a].col < entries[b].col;
+    });
+    CsrMatrix A;
+    A.n_rows = n_rows;
+    A.n_cols = n_cols;
+    A.row_ptr.assign(static_cast<std::size_t>(n_rows) + 1, 0);
+    for (std::size_t i = 0; i < idx.size();) {
+        const index_t r = entries[idx[i]].row, c = entries[idx[i]].col;
+        double sum = 0.0;
+        for (; i < idx.size() && entries[idx[i]].row == r && entries[idx[i]].col == c; ++i)
+            sum += entries[idx[i]].val;
+        A.col_idx.push_back(c);
+        A.values.push_back(sum);
+        A.row_ptr[r + 1] = static_cast<index_t>(A.col_idx.size());
+    }
+    for (index_t r = 0; r < n_rows; ++r) A.row_ptr[r + 1] = std::max(A.row_ptr[r + 1], A.row_ptr[r]);
+    return A;
+}
+
+/// csr.hpp:126-142
+inline void spmv(const CsrMatrix& A, const std::vector<double>& x, std::vector<double>& y,
+                 int /*threads*/ = 0) {
+    if (x.size() != A.n_cols || y.size() != A.n_rows)
+        throw std::invalid_argument("spmv: vector size mismatch");
+    detail::check(mpkg_spmv(device_context(), A.device(), x.data(), y.data()));
+}
+
+inline CsrMatrix download(mpkg_csr_t h) {
+    CsrMatrix B;
+    index_t nnz = 0;
+    detail::check(mpkg_csr_info(h, &B.n_rows, &B.n_cols, &nnz));
+    B.row_ptr.resize(static_cast<std::size_t>(B.n_rows) + 1);
+    B.col_idx.resize(nnz);
+    B.values.resize(nnz);
+    detail::check(mpkg_csr_download(h, B.row_ptr.data(), B.col_idx.data(), B.values.data()));
+    return B;
+}
+
+/// csr.hpp:159-188 (GPU permutation, bit-exact)
+inline CsrMatrix permute(const CsrMatrix& A, const std::vector<index_t>& perm) {
+    if (A.n_rows != A.n_cols) throw std::invalid_argument("permute: matrix must be square");
+    if (perm.size() != A.n_rows) throw std::invalid_argument("permute: permutation size mismatch");
+    mpkg_csr_t out = nullptr;
+    detail::check(mpkg_permute(device_context(), A.device(), perm.data(), &out));
+    CsrMatrix B = download(out);
+    mpkg_csr_destroy(out);
+    return B;
+}
+
+/// csr.hpp:191-204
+inline std::vector<double> permute_vector(const std::vector<double>& in,
+                                          const std::vector<index_t>& perm) {
+    std::vector<double> out(in.size());
+    detail::check(mpkg_permute_vector(device_context(), static_cast<std::uint32_t>(in.size()),
+                                      in.data(), perm.data(), out.data()));
+    return out;
+}
+inline std::vector<double> unpermute_vector(const std::vector<double>& in,
+                                            const std::vector<index_t>& perm) {
+    std::vector<double> out(in.size());
+    detail::check(mpkg_unpermute_vector(device_context(), static_cast<std::uint32_t>(in.size()),
+                                        in.data(), perm.data(), out.data()));
+    return out;
+}
+
+// ---- levels.hpp ------------------------------------------------------------------------------
+/// levels.hpp:65-147 (GPU BFS, bit-exact)
+inline LevelStructure build_levels(const CsrMatrix& A) {
+    if (A.n_rows != A.n_cols) throw std::invalid_argument("build_levels: matrix must be square");
+    auto d = std::make_shared<detail::LevelsHolder>();
+    detail::check(mpkg_build_levels(device_context(), A.device(), &d->h));
+    LevelStructure ls;
+    index_t n = 0, nl = 0;
+    detail::check(mpkg_levels_info(d->h, &n, &nl));
+    ls.n_rows = n;
+    ls.levels.resize(n);
+    ls.perm.resize(n);
+    ls.inv_perm.resize(n);
+    ls.level_ptr.resize(static_cast<std::size_t>(nl) + 1);
+    detail::check(mpkg_levels_get(d->h, ls.levels.data(), ls.perm.data(), ls.inv_perm.data(),
+                                  ls.level_ptr.data()));
+    ls.dev_ = d;
+    return ls;
+}
+
+/// levels.hpp:151-164
+inline bool validate_levels(const CsrMatrix& A_perm, const LevelStructure& ls) {
+    if (A_perm.n_rows != ls.n_rows || A_perm.n_rows != A_perm.n_cols) return false;
+    int ok = 0;
+    detail::check(mpkg_validate_levels(device_context(), A_perm.device(), ls.device(), &ok));
+    return ok != 0;
+}
+
+// ---- plan.hpp --------------------------------------------------------------------------------
+/// plan.hpp:59-64
+inline std::size_t row_range_footprint(const CsrMatrix& A_perm, index_t row_s, index_t row_e,
+                                       int p_m) {
+    const std::size_t nnz = A_perm.row_ptr[row_e] - A_perm.row_ptr[row_s];
+    const std::size_t rows = row_e - row_s;
+    return 12 * nnz + 4 * rows + 8 * static_cast<std::size_t>(p_m + 1) * rows;
+}
+
+/// plan.hpp:70-85
+inline std::vector<index_t> greedy_group(const std::vector<std::size_t>& level_fp,
+                                         std::size_t target) {
+    std::vector<std::uint64_t> fp(level_fp.begin(), level_fp.end());
+    std::vector<index_t> bounds(level_fp.size() + 1);
+    index_t nb = 0;
+    detail::check(mpkg_greedy_group(fp.empty() ? nullptr : fp.data(),
+                                    static_cast<index_t>(fp.size()), target, bounds.data(), &nb));
+    bounds.resize(nb);
+    return bounds;
+}
+
+/// plan.hpp:88-115
+inline ExecutionPlan group_levels(const LevelStructure& ls, const CsrMatrix& A_perm,
+                                  std::size_t cache_bytes, int p_m) {
+    mpkg_plan_t h = nullptr;
+    detail::check(mpkg_group_levels(device_context(), ls.device(), A_perm.device(), cache_bytes,
+                                    p_m, &h));
+    ExecutionPlan plan;
+    index_t n = 0, ng = 0;
+    std::uint64_t cb = 0, tb = 0;
+    detail::check(mpkg_plan_info(h, &plan.p_m, &plan.sub_powers, &n, &cb, &tb, &ng));
+    plan.n_rows = n;
+    plan.cache_bytes = cb;
+    plan.target_bytes = tb;
+    plan.group_rows.resize(static_cast<std::size_t>(ng) + 1);
+    plan.group_level_ptr.resize(static_cast<std::size_t>(ng) + 1);
+    std::vector<std::uint64_t> fp(ng);
+    detail::check(mpkg_plan_get(h, plan.group_rows.data(), plan.group_level_ptr.data(),
+                                fp.empty() ? nullptr : fp.data()));
+    mpkg_plan_destroy(h);
+    plan.group_footprint.assign(fp.begin(), fp.end());
+    plan.level_ptr = ls.level_ptr;
+    return plan;
+}
+
+// ---- execute.hpp -----------------------------------------------------------------------------
+/// execute.hpp:52-55
+struct ScheduleCell {
+    index_t group;
+    int stage;
+};
+
+/// execute.hpp:59-72
+inline std::vector<ScheduleCell> wavefront_schedule(index_t n_groups, int stages) {
+    std::uint64_t cnt = 0;
+    const std::size_t cap = stages > 0 ? static_cast<std::size_t>(n_groups) * stages : 0;
+    std::vector<index_t> g(cap + 1);
+    std::vector<int> q(cap + 1);
+    detail::check(mpkg_wavefront_schedule(n_groups, stages, g.data(), q.data(), &cnt));
+    std::vector<ScheduleCell> out(cnt);
+    for (std::size_t i = 0; i < cnt; ++i) out[i] = {g[i], q[i]};
+    return out;
+}
+
+/// execute.hpp:79-113 — generic host callback hook (host-side; see the header comment).
+template <typename Kernel>
+void execute(const ExecutionPlan& plan, Kernel&& kernel, int /*threads*/ = 0, int p_m = 0) {
+    if (p_m <= 0) p_m = plan.p_m;
+    if (p_m > plan.p_m) throw std::invalid_argument("execute: p_m exceeds the plan's power budget");
+    const int sub = plan.sub_powers;
+    for (const ScheduleCell& cell : wavefront_schedule(plan.n_groups(), p_m * sub)) {
+        const index_t rs = plan.group_rows[cell.group], re = plan.group_rows[cell.group + 1];
+        if (re > rs) kernel(rs, re, (cell.stage - 1) / sub + 1, (cell.stage - 1) % sub);
+    }
+}
+
+// ---- mpk.hpp ---------------------------------------------------------------------------------
+/// mpk.hpp:59-75
+inline void baseline_mpk(const CsrMatrix& A, const std::vector<double>& x, int p_m,
+                         VectorBlock& block, int /*threads*/ = 0) {
+    if (x.size() != A.n_rows) throw std::invalid_argument("baseline_mpk: input size mismatch");
+    detail::check(mpkg_baseline_mpk(device_context(), A.device(), x.data(), p_m,
+                                    block.data.data(), block.rows, block.slices));
+}
+
+/// mpk.hpp:81-106 (one fused, temporally blocked GPU launch)
+inline void mpk(const ExecutionPlan& plan, const CsrMatrix& A_perm, const std::vector<double>& x,
+                int p_m, VectorBlock& block, int /*threads*/ = 0) {
+    if (x.size() != A_perm.n_rows) throw std::invalid_argument("mpk: input size mismatch");
+    detail::check(mpkg_mpk(device_context(), plan.device(), A_perm.device(), x.data(), p_m,
+                           block.data.data(), block.rows, block.slices));
+}
+
+/// mpk.hpp:111-127
+inline void check_shift_chain(const std::vector<std::complex<double>>& shifts, const char* who) {
+    std::vector<double> re(shifts.size()), im(shifts.size());
+    for (std::size_t i = 0; i < shifts.size(); ++i) re[i] = shifts[i].real(), im[i] = shifts[i].imag();
+    const int rc = mpkg_check_shift_chain(re.data(), im.data(), static_cast<int>(shifts.size()));
+    if (rc == MPKG_EINVAL) throw std::invalid_argument(std::string(who) + ": " + mpkg_last_error());
+    detail::check(rc);
+}
+
+namespace detail {
+inline void split(const std::vector<std::complex<double>>& s, std::vector<double>& re,
+                  std::vector<double>& im) {
+    re.resize(s.size());
+    im.resize(s.size());
+    for (std::size_t i = 0; i < s.size(); ++i) re[i] = s[i].real(), im[i] = s[i].imag();
+}
+}  // namespace detail
+
+/// mpk.hpp:160-180
+inline void baseline_mpk_shifted(const CsrMatrix& A, const std::vector<double>& x,
+                                 const std::vector<std::complex<double>>& shifts,
+                                 VectorBlock& block, int /*threads*/ = 0) {
+    if (x.size() != A.n_rows) throw std::invalid_argument("baseline_mpk_shifted: input size mismatch");
+    std::vector<double> re, im;
+    detail::split(shifts, re, im);
+    detail::check(mpkg_baseline_mpk_shifted(device_context(), A.device(), x.data(), re.data(),
+                                            im.data(), static_cast<int>(shifts.size()),
+                                            block.data.data(), block.rows, block.slices));
+}
+
+/// mpk.hpp:184-207
+inline void mpk_shifted(const ExecutionPlan& plan, const CsrMatrix& A_perm,
+                        const std::vector<double>& x,
+                        const std::vector<std::complex<double>>& shifts, VectorBlock& block,
+                        int /*threads*/ = 0) {
+    if (x.size() != A_perm.n_rows) throw std::invalid_argument("mpk_shifted: input size mismatch");
+    std::vector<double> re, im;
+    detail::split(shifts, re, im);
+    detail::check(mpkg_mpk_shifted(device_context(), plan.device(), A_perm.device(), x.data(),
+                                   re.data(), im.data(), static_cast<int>(shifts.size()),
+                                   block.data.data(), block.rows, block.slices));
+}
+
+/// Coefficient-form polynomial z = sum_k c_k A^k x (not in the reference).
+inline std::vector<double> mpk_poly(const ExecutionPlan& plan, const CsrMatrix& A_perm,
+                                    const std::vector<double>& x, const std::vector<double>& c) {
+    std::vector<double> z(A_perm.n_rows);
+    detail::check(mpkg_mpk_poly(device_context(), plan.device(), A_perm.device(), x.data(),
+                                c.data(), static_cast<int>(c.size()) - 1, z.data(), nullptr, 0, 0));
+    return z;
+}
+
+/// mpk.hpp:211-215
+struct TuneResult {
+    int p_opt = 1;
+    std::vector<std::pair<int, double>> table;
+};
+
+/// mpk.hpp:219-233
+template <typename TrialFn>
+TuneResult tune_p(int p_lo, int p_hi, TrialFn&& trial) {
+    if (p_lo < 1 || p_hi < p_lo) throw std::invalid_argument("tune_p: bad range");
+    TuneResult res;
+    std::vector<double> t;
+    for (int p = p_lo; p <= p_hi; ++p) {
+        t.push_back(trial(p));
+        res.table.emplace_back(p, t.back());
+    }
+    detail::check(mpkg_tune_select(t.data(), p_lo, p_hi, &res.p_opt));
+    return res;
+}
+
+/// mpk.hpp:238-258 (GPU timing with CUDA events)
+inline TuneResult tune_p(const LevelStructure& ls, const CsrMatrix& A_perm,
+                         std::size_t cache_bytes, int p_lo, int p_hi, int /*threads*/ = 0,
+                         int reps = 3) {
+    if (p_lo < 1 || p_hi < p_lo) throw std::invalid_argument("tune_p: bad range");
+    std::vector<double> t(static_cast<std::size_t>(p_hi - p_lo + 1));
+    TuneResult res;
+    detail::check(mpkg_tune_p(device_context(), ls.device(), A_perm.device(), cache_bytes, p_lo,
+                              p_hi, reps, &res.p_opt, t.data()));
+    for (int p = p_lo; p <= p_hi; ++p) res.table.emplace_back(p, t[p - p_lo]);
+    return res;
+}
+
+// ---- generators.hpp (harness inputs, produced by the library's host generators) -------------
+namespace detail {
+inline CsrMatrix gen(int kind, index_t a, index_t b, index_t c, std::uint64_t seed) {
+    mpkg_host_csr_t h = nullptr;
+    check(mpkg_gen(kind, a, b, c, seed, &h));
+    index_t n = 0, m = 0;
+    std::uint64_t nnz = 0;
+    check(mpkg_host_csr_info(h, &n, &m, &nnz));
+    index_t *rp = nullptr, *ci = nullptr;
+    double* v = nullptr;
+    check(mpkg_host_csr_arrays(h, &rp, &ci, &v));
+    CsrMatrix A;
+    A.n_rows = n;
+    A.n_cols = m;
+    A.row_ptr.assign(rp, rp + n + 1);
+    A.col_idx.assign(ci, ci + nnz);
+    A.values.assign(v, v + nnz);
+    mpkg_host_csr_destroy(h);
+    return A;
+}
+}  // namespace detail
+
+inline CsrMatrix poisson1d(index_t n) { return detail::gen(1, n, 0, 0, 0); }
+inline CsrMatrix poisson2d(index_t nx, index_t ny) { return detail::gen(2, nx, ny, 0, 0); }
+inline CsrMatrix poisson3d(index_t nx, index_t ny, index_t nz) { return detail::gen(3, nx, ny, nz, 0); }
+inline CsrMatrix random_csr(index_t n, index_t k, std::uint64_t seed) { return detail::gen(4, n, k, 0, seed); }
+inline CsrMatrix random_spd(index_t n, index_t k, std::uint64_t seed) { return detail::gen(5, n, k, 0, seed); }
+
+}  // namespace mpkg

@@ -49,6 +49,7 @@ _SIGS = {
     "mpkg_row_range_footprint": [P, u32, u32, i32, pu64],
     "mpkg_greedy_group": [P, u32, u64, P, pu32],
     "mpkg_group_levels": [P, P, P, u64, i32, C.POINTER(P)],
+    "mpkg_plan_create": [i32, i32, u32, u64, u64, u32, P, P, P, u32, P, C.POINTER(P)],
     "mpkg_plan_info": [P, pint, pint, pu32, pu64, pu64, pu32],
     "mpkg_plan_get": [P, P, P, P],
     "mpkg_plan_destroy": [P],

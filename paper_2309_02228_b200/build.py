@@ -66,6 +66,24 @@ def build(force: bool = False) -> pathlib.Path:
     return LIB
 
 
+CPP_TEST_SRC = ROOT / "tests" / "cpp" / "test_facade.cpp"
+CPP_TEST_BIN = ROOT / "build" / "test_facade"
+
+
+def build_cpp_tests() -> pathlib.Path:
+    """The reference's hot-path tests restated against include/mpkg.hpp (links libmpkg.so)."""
+    deps = [CPP_TEST_SRC, ROOT / "include" / "mpkg.hpp", ROOT / "include" / "mpkg.h", LIB]
+    if CPP_TEST_BIN.exists() and CPP_TEST_BIN.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return CPP_TEST_BIN
+    CPP_TEST_BIN.parent.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", f"-I{ROOT / 'include'}", str(CPP_TEST_SRC),
+           "-o", str(CPP_TEST_BIN), f"-L{PKG}", "-lmpkg", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../paper_2309_02228_b200"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"C++ facade test build failed:\n{res.stdout}\n{res.stderr}")
+    return CPP_TEST_BIN
+
+
 def build_oracle() -> None:
     """Test infrastructure: oracle/liboracle.so and (when /root/reference exists) oracle/_ref."""
     res = subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], capture_output=True, text=True)
@@ -76,3 +94,4 @@ def build_oracle() -> None:
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv))
     build_oracle()
+    print(build_cpp_tests())

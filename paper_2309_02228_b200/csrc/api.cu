@@ -623,6 +623,29 @@ int mpkg_group_levels(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A, uint64_t ca
     });
 }
 
+int mpkg_plan_create(int p_m, int sub_powers, uint32_t n_rows, uint64_t cache_bytes,
+                     uint64_t target_bytes, uint32_t n_groups, const uint32_t* group_rows,
+                     const uint32_t* group_level_ptr, const uint64_t* group_footprint,
+                     uint32_t n_levels, const uint32_t* level_ptr, mpkg_plan_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "plan_create: null output");
+        require(p_m >= 1, "plan_create: p_m must be >= 1");
+        require(sub_powers >= 1, "plan_create: sub_powers must be >= 1");
+        require(group_rows != nullptr || n_groups == 0, "plan_create: null group_rows");
+        auto* P = new mpkg_plan_s();
+        P->p_m = p_m;
+        P->sub_powers = sub_powers;
+        P->n_rows = n_rows;
+        P->cache_bytes = cache_bytes;
+        P->target_bytes = target_bytes;
+        if (group_rows) P->group_rows.assign(group_rows, group_rows + n_groups + 1);
+        if (group_level_ptr) P->group_level_ptr.assign(group_level_ptr, group_level_ptr + n_groups + 1);
+        if (group_footprint) P->group_footprint.assign(group_footprint, group_footprint + n_groups);
+        if (level_ptr) P->level_ptr.assign(level_ptr, level_ptr + n_levels + 1);
+        *out = P;
+    });
+}
+
 int mpkg_plan_info(mpkg_plan_t P, int* p_m, int* sub, uint32_t* n_rows, uint64_t* cache,
                    uint64_t* target, uint32_t* n_groups) {
     return guarded([&] {
