@@ -261,6 +261,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->group = value;
         else if (k == "stages")
             ctx->stages = value;
+        else if (k == "rowfn")
+            ctx->rowfn = value;
         else if (k == "kernel") {
             require(value >= 0 && value <= 2,
                     "ctx_set_param: kernel must be 0 (lean), 1 (staged) or 2 (warp-tile)");

@@ -77,6 +77,7 @@ struct Executor {
     int64_t tile_knob = 0, thread_knob = 0;   // ctx->tile_rows / ctx->threads likewise
     int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused, 2: k_mpk_warptile
     uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
+    int rowfn = 0;                            // lean kernel row loop (0 pipelined, 1 grouped)
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -368,8 +369,10 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
 // stay low and many warps are resident (the row loop is latency-bound: throughput follows
 // resident warps).  One thread per tile row; thread 0 claims the next ticket while the current
 // one runs (double-buffered claim, deadlock-free for the same reason as above).
-template <int KIND, bool SIGMA>
-__global__ void __launch_bounds__(256) k_mpk_lean(const __grid_constant__ FusedParams P) {
+// RF 0: software-pipelined pairs (sell_row_dot_pipe); RF 1: groups of 8 entries
+// (sell_row_dot<.,8>) with a 32-register cap so 16 CTAs of 128 threads (64 warps) fit per SM.
+template <int KIND, bool SIGMA, int RF>
+__global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_constant__ FusedParams P) {
     __shared__ uint32_t s_ticket[2];
     const uint32_t tid = threadIdx.x;
     const uint32_t nt = blockDim.x;
@@ -412,8 +415,13 @@ __global__ void __launch_bounds__(256) k_mpk_lean(const __grid_constant__ FusedP
             const uint64_t c = s >> 5;
             const uint64_t off = P.chunk_off[c];
             const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
-            double acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
-                                : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+            double acc;
+            if constexpr (RF == 0)
+                acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                             : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+            else
+                acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                             : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
                 const double own = src[s];
@@ -592,6 +600,14 @@ void configure_warptile(uint32_t lmax) {
         MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 }
 
+template <int KIND, bool SIGMA>
+void launch_lean(int rowfn, int grid, int nt, cudaStream_t st, const FusedParams& P) {
+    if (rowfn)
+        k_mpk_lean<KIND, SIGMA, 1><<<grid, nt, 0, st>>>(P);
+    else
+        k_mpk_lean<KIND, SIGMA, 0><<<grid, nt, 0, st>>>(P);
+}
+
 template <int U>
 void launch_warptile(int kind, bool sigma, int grid, uint32_t smem, cudaStream_t st,
                      const FusedParams& P) {
@@ -609,7 +625,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
         P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
         P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads &&
-        P->exec->kernel == (int)ctx->kernel) {
+        P->exec->kernel == (int)ctx->kernel && P->exec->rowfn == (ctx->rowfn == 1 ? 1 : 0)) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -695,7 +711,12 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     } else if (E->kernel == 0) {
         E->threads = E->tile_rows;
         E->stages = 1;
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true>, (int)E->tile_rows, 0));
+        E->rowfn = ctx->rowfn == 1 ? 1 : 0;
+        const int nt = (int)std::min<uint32_t>(E->tile_rows, 128u);
+        if (E->rowfn)
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true, 1>, nt, 0));
+        else
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true, 0>, nt, 0));
     } else if (E->group == 8) {
         configure_kernels<8>(smem);
         MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads + 32, smem));
@@ -939,14 +960,14 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         else
             launch_warptile<4>(a.kind, sigma, E.grid, wsmem, st, P);
     } else if (E.kernel == 0) {
-        const int nt = (int)E.tile_rows;
+        const int nt = (int)std::min<uint32_t>(E.tile_rows, 128u);
         switch (a.kind * 2 + (sigma ? 1 : 0)) {
-            case 0: k_mpk_lean<0, false><<<E.grid, nt, 0, st>>>(P); break;
-            case 1: k_mpk_lean<0, true><<<E.grid, nt, 0, st>>>(P); break;
-            case 2: k_mpk_lean<1, false><<<E.grid, nt, 0, st>>>(P); break;
-            case 3: k_mpk_lean<1, true><<<E.grid, nt, 0, st>>>(P); break;
-            case 4: k_mpk_lean<2, false><<<E.grid, nt, 0, st>>>(P); break;
-            default: k_mpk_lean<2, true><<<E.grid, nt, 0, st>>>(P); break;
+            case 0: launch_lean<0, false>(E.rowfn, E.grid, nt, st, P); break;
+            case 1: launch_lean<0, true>(E.rowfn, E.grid, nt, st, P); break;
+            case 2: launch_lean<1, false>(E.rowfn, E.grid, nt, st, P); break;
+            case 3: launch_lean<1, true>(E.rowfn, E.grid, nt, st, P); break;
+            case 4: launch_lean<2, false>(E.rowfn, E.grid, nt, st, P); break;
+            default: launch_lean<2, true>(E.rowfn, E.grid, nt, st, P); break;
         }
     } else {
         switch (a.kind) {
