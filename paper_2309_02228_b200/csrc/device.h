@@ -102,7 +102,7 @@ struct mpkg_ctx_s {
     int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile
-    int64_t rowfn = 1;        // lean row loop: 0 pipelined pairs, 1 groups of 8 (32 regs)
+    int64_t rowfn = 0;        // lean row loop: 0 pipelined pairs, 1 groups of 8 (32 regs)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;

@@ -1,0 +1,176 @@
+"""Multi-GPU MPK: contiguous BFS-level ranges per rank with p-deep ghost levels.
+
+The level adjacency property (levels.hpp:17-24) confines row i's columns to levels
+level(i)-1 .. level(i)+1.  Rank r owns the levels [L_r, L_{r+1}) (balanced by nnz) and also
+holds p ghost levels on each side, i.e. the rows of levels [L_r - p, L_{r+1} + p).  Power k is
+valid on own rows plus ghost depth p-k (redundant-compute, communication-avoiding MPK), so the
+only exchange is ONE halo of x before the sweep; no collective runs inside the p powers.  The
+local matrix is A_perm restricted to the local rows with columns outside the local range
+dropped: rows that lose a column are exactly the outermost ghost rows, whose (wrong) values can
+reach at most ghost depth p-k at power k and never an own row.  Own rows are therefore computed
+by the same formula from the same inputs as on one GPU: bit-identical results for any N.
+
+The host logic (partition, halo plan, local matrix, exchange, assembly) is independent of the
+device; `DistributedMPK` runs the local MPK through a callable (default: the sm_100a path of
+this package).  Communication uses torch.distributed point-to-point (NCCL on GPUs, gloo in the
+CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+
+def partition_levels(level_ptr: Sequence[int], row_ptr: Sequence[int], world: int) -> List[Tuple[int, int]]:
+    """Contiguous level ranges [L_r, L_{r+1}) balancing nnz (row count breaks ties)."""
+    lp = np.asarray(level_ptr, dtype=np.int64)
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    nl = len(lp) - 1
+    if world < 1:
+        raise ValueError("partition_levels: world must be >= 1")
+    cum = rp[lp]  # nnz before each level boundary
+    total = cum[-1]
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        L = int(np.searchsorted(cum, target, side="left"))
+        L = max(L, bounds[-1])
+        bounds.append(min(L, nl))
+    bounds.append(nl)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    levels: Tuple[int, int]      # own level range
+    own_rows: Tuple[int, int]    # own rows [o0, o1) of A_perm
+    local_rows: Tuple[int, int]  # rows held locally [g0, g1) (own + p ghost levels each side)
+    pieces: List[Tuple[int, int, int]]  # (owner rank, row0, row1) covering local_rows
+
+    @property
+    def n_local(self) -> int:
+        return self.local_rows[1] - self.local_rows[0]
+
+
+def halo_plan(level_ptr: Sequence[int], parts: Sequence[Tuple[int, int]], rank: int, p: int) -> HaloPlan:
+    lp = list(int(v) for v in level_ptr)
+    nl = len(lp) - 1
+    L0, L1 = parts[rank]
+    o0, o1 = lp[L0], lp[L1]
+    g0, g1 = lp[max(0, L0 - p)], lp[min(nl, L1 + p)]
+    if o0 == o1:  # empty rank: holds nothing
+        g0 = g1 = o0
+    pieces = []
+    for s, (a, b) in enumerate(parts):
+        r0, r1 = max(lp[a], g0), min(lp[b], g1)
+        if r0 < r1:
+            pieces.append((s, r0, r1))
+    return HaloPlan(rank, (L0, L1), (o0, o1), (g0, g1), pieces)
+
+
+def local_matrix(row_ptr, col_idx, values, g0: int, g1: int):
+    """Rows [g0, g1) of A_perm, columns outside [g0, g1) dropped, indices shifted by -g0 (the
+    stored order of the kept entries is unchanged)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    ci = np.asarray(col_idx, dtype=np.int64)
+    v = np.asarray(values)
+    b, e = rp[g0], rp[g1]
+    cols = ci[b:e]
+    keep = (cols >= g0) & (cols < g1)
+    rows = np.repeat(np.arange(g1 - g0), np.diff(rp[g0:g1 + 1]))
+    counts = np.bincount(rows[keep], minlength=g1 - g0)
+    lrp = np.zeros(g1 - g0 + 1, dtype=np.uint32)
+    np.cumsum(counts, out=lrp[1:])
+    return lrp, (cols[keep] - g0).astype(np.uint32), np.ascontiguousarray(v[b:e][keep])
+
+
+def local_level_ptr(level_ptr, L0: int, L1: int, p: int):
+    lp = np.asarray(level_ptr, dtype=np.int64)
+    nl = len(lp) - 1
+    a, b = max(0, L0 - p), min(nl, L1 + p)
+    return (lp[a:b + 1] - lp[a]).astype(np.uint32)
+
+
+def exchange_x(x_own: np.ndarray, plans: Sequence[HaloPlan], rank: int, dist, group=None) -> np.ndarray:
+    """Builds the local x (rows [g0, g1)) from the owners' pieces with point-to-point sends.
+    Every rank runs this with its own x_own (rows [o0, o1))."""
+    import torch
+    me = plans[rank]
+    g0, g1 = me.local_rows
+    out = np.empty(g1 - g0, dtype=np.float64)
+    reqs, keep = [], []
+    o0 = me.own_rows[0]
+    # sends: my own rows to every rank whose local range overlaps them
+    for other in plans:
+        if other.rank == rank:
+            continue
+        for s, r0, r1 in other.pieces:
+            if s == rank:
+                buf = torch.from_numpy(np.ascontiguousarray(x_own[r0 - o0:r1 - o0]))
+                keep.append(buf)
+                reqs.append(dist.isend(buf, dst=other.rank, group=group))
+    recv = []
+    for s, r0, r1 in me.pieces:
+        if s == rank:
+            out[r0 - g0:r1 - g0] = x_own[r0 - o0:r1 - o0]
+        else:
+            buf = torch.empty(r1 - r0, dtype=torch.float64)
+            recv.append((buf, r0, r1))
+            reqs.append(dist.irecv(buf, src=s, group=group))
+    for rq in reqs:
+        rq.wait()
+    for buf, r0, r1 in recv:
+        out[r0 - g0:r1 - g0] = buf.numpy()
+    return out
+
+
+LocalMPK = Callable[[np.ndarray, np.ndarray, np.ndarray, np.ndarray, np.ndarray, int], np.ndarray]
+
+
+def gpu_local_mpk(ctx=None, cache_bytes: Optional[int] = None) -> LocalMPK:
+    """The default local compute: this package's fused sm_100a MPK on the rank's GPU."""
+    from . import api
+
+    def run(rp, ci, v, lp, x, p):
+        c = ctx or api.Context(0)
+        A = c.csr(api.HostCsr.from_arrays(rp, ci, v))
+        n = len(rp) - 1
+        ident = np.arange(n, dtype=np.uint32)
+        ls = c.levels_from_host(np.zeros(n, np.uint32), ident, ident, lp)
+        plan = c.group_levels(ls, A, cache_bytes or c.device_info()["l2_bytes"], p)
+        return c.mpk(plan, A, x, p).as_matrix()
+
+    return run
+
+
+class DistributedMPK:
+    """One rank's share of a level-partitioned MPK over A_perm (global arrays on every rank for
+    simplicity of setup; only the local slice is kept)."""
+
+    def __init__(self, row_ptr, col_idx, values, level_ptr, p: int, rank: int, world: int,
+                 local_mpk: Optional[LocalMPK] = None):
+        self.p, self.rank, self.world = p, rank, world
+        self.parts = partition_levels(level_ptr, row_ptr, world)
+        self.plans = [halo_plan(level_ptr, self.parts, r, p) for r in range(world)]
+        me = self.plans[rank]
+        g0, g1 = me.local_rows
+        self.local = local_matrix(row_ptr, col_idx, values, g0, g1)
+        self.local_lp = local_level_ptr(level_ptr, me.levels[0], me.levels[1], p)
+        self.local_mpk = local_mpk or gpu_local_mpk()
+
+    @property
+    def plan(self) -> HaloPlan:
+        return self.plans[self.rank]
+
+    def run(self, x_own: np.ndarray, dist, group=None) -> np.ndarray:
+        """Returns this rank's own rows of y_0..y_p, shape (p+1, n_own)."""
+        me = self.plan
+        x_loc = exchange_x(x_own, self.plans, self.rank, dist, group)
+        if me.n_local == 0:
+            return np.zeros((self.p + 1, 0))
+        blk = self.local_mpk(*self.local, self.local_lp, x_loc, self.p)
+        o0 = me.own_rows[0] - me.local_rows[0]
+        return blk[:, o0:o0 + (me.own_rows[1] - me.own_rows[0])]
