@@ -73,6 +73,7 @@ struct Sell {
     uint32_t n_slots = 0;  // multiple of 32
     uint32_t n_chunks = 0;
     uint64_t n_entries = 0;  // padded
+    uint32_t long_cap = 0xffffffffu;  // rows longer than this are not stored (fused long path)
     DevBuf<uint64_t> chunk_off;
     DevBuf<uint32_t> row_len;   // per slot
     DevBuf<uint32_t> slot_row;  // per slot, optional (padding slots hold 0xffffffff)
@@ -94,7 +95,7 @@ struct mpkg_ctx_s {
     // executor knobs (mpkg_ctx_set_param)
     int64_t tile_rows = 128;  // rows per fused-kernel tile (64, 128 or 256)
     int64_t slack = -1;  // -1: resident CTA count
-    int64_t order = 1;        // 0: A_perm order, 1: Cuthill-McKee inside levels
+    int64_t order = -1;       // -1 auto, 0 A_perm order, 1 Cuthill-McKee, 2 longest rows first
     int64_t pass_powers = 0;  // >0: force powers per fused pass
     int64_t l2_budget = 0;    // >0: live-window budget in bytes (default 0.6 L2)
     int64_t ctas_per_sm = 0;  // >0: cap on resident fused-kernel CTAs per SM
@@ -167,12 +168,15 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 32
 // sell.cu
 Sell& csr_sell(mpkg_csr_s* A);
 // d_slot_row: slot -> row (nullptr = identity); d_col_map: column relabel (nullptr = none).
+// Rows longer than long_cap are left out of the SELL arrays (row_len keeps their true length).
 void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row,
-                const uint32_t* d_col_map, Sell& out);
+                const uint32_t* d_col_map, Sell& out, uint32_t long_cap);
 
 // reorder.cu: GPU-private Cuthill-McKee order inside BFS levels.
 void gpu_level_cm_order(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const std::vector<uint32_t>& level_ptr,
-                        uint32_t n_slots, DevBuf<uint32_t>& slot_row, DevBuf<uint32_t>& pos);
+                        uint32_t n_slots, DevBuf<uint32_t>& slot_row, DevBuf<uint32_t>& pos,
+                        int mode);
+uint32_t gpu_max_row_len(mpkg_ctx_s* ctx, const mpkg_csr_s* A);
 void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
                       double* dst, const double* src2, double shift_a, double shift_b2);
 

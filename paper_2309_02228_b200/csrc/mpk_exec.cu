@@ -47,6 +47,8 @@ constexpr int kBuckets = 4;              // neighbouring-level buckets per tile
 constexpr uint32_t kLastUse = 1u << 30;  // ticket flag: last use of the tile in its pass
 constexpr uint32_t kBig = 1u << 31;      // ticket flag: tile too large for the smem buffer
 constexpr uint32_t kMaxBufBytes = 96 * 1024;
+constexpr uint32_t kLongCap = 1024;    // rows longer than this take the CTA-cooperative path
+constexpr uint32_t kLongChunk = 4096;  // products per chunk of a long row
 #ifndef MPKG_GROUP
 #define MPKG_GROUP 16
 #endif
@@ -78,6 +80,14 @@ struct Executor {
     int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused, 2: k_mpk_warptile
     uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
     int rowfn = 0;                            // lean kernel row loop (0 pipelined, 1 grouped)
+    int64_t order_knob = -1;                  // ctx->order the executor was built with
+    uint32_t long_cap = 0xffffffffu;          // rows above this length: CTA-cooperative path
+    uint64_t long_rows = 0;                   // how many
+    bool kernel_forced_lean = false;          // variable tiles need the lean kernel
+    int64_t kernel_knob = 0;                  // ctx->kernel the executor was built with
+    std::vector<uint32_t> h_tile_start;       // variable tiles (empty: fixed tile_rows)
+    DevBuf<uint32_t> tile_start;
+    DevBuf<double> long_prod;                 // grid * kLongChunk product scratch
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<double> V;   // sigma-order working vectors (order 1)
@@ -105,6 +115,12 @@ struct FusedParams {
     uint32_t stages;
     uint32_t tile_rows;
     uint32_t wt_lmax;  // warp-tile kernel: widest chunk handled flat (smem slice per warp)
+    const uint32_t* tile_start;  // variable tiles (n_tiles+1 slot offsets) or nullptr
+    uint32_t long_cap;           // rows longer than this are not in the SELL arrays
+    const uint32_t* csr_rp;      // A_perm CSR (long rows)
+    const uint32_t* csr_ci;
+    const double* csr_v;
+    double* long_prod;           // per-CTA product scratch for long rows (grid * kLongChunk)
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -187,13 +203,15 @@ __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, ui
 __global__ void k_dep_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                               uint32_t n, const uint32_t* __restrict__ slot_row,
                               const uint32_t* __restrict__ pos, const uint32_t* __restrict__ lp,
-                              uint32_t nl, uint32_t tile_rows, uint32_t* __restrict__ bmin,
-                              uint32_t* __restrict__ bmax) {
+                              uint32_t nl, uint32_t tile_rows,
+                              const uint32_t* __restrict__ tile_start, uint32_t n_tiles,
+                              uint32_t* __restrict__ bmin, uint32_t* __restrict__ bmax) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t r = slot_row ? slot_row[s] : (uint32_t)s;
-        const uint32_t T = (uint32_t)(s / tile_rows);
-        const uint32_t lt = level_of(lp, nl, T * tile_rows);
+        // tile of slot s: fixed-size tiles, or the variable tiles of tile_start
+        const uint32_t T = tile_start ? level_of(tile_start, n_tiles, (uint32_t)s) : (uint32_t)(s / tile_rows);
+        const uint32_t lt = level_of(lp, nl, tile_start ? tile_start[T] : T * tile_rows);
         const uint32_t L = level_of(lp, nl, (uint32_t)s);
         const uint32_t lb = lp[L], le = lp[L + 1];
         for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
@@ -407,21 +425,55 @@ __global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_con
         }
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
         const uint64_t pol = l2_policy(code & kLastUse);
-        for (uint32_t row = tid; row < P.tile_rows; row += nt) {
-            const uint32_t s = T * P.tile_rows + row;
+        const uint32_t s0 = P.tile_start ? P.tile_start[T] : T * P.tile_rows;
+        const uint32_t s1 = P.tile_start ? P.tile_start[T + 1] : s0 + P.tile_rows;
+        bool long_row = false;
+        double long_acc = 0.0;
+        if (s1 - s0 == 1 && P.long_prod) {
+            // A single-row tile holding a long row (len > SELL long_cap, e.g. an R-MAT hub): the
+            // CTA computes the products from the row's contiguous A_perm CSR slice in chunks,
+            // gathering from the A_perm-order copy of y_{q-1} in the caller's block, and one
+            // thread adds them in stored order (same formula, same order: bitwise).
+            const uint32_t r = SIGMA ? P.slot_row[s0] : s0;
+            const uint32_t len = r < P.n_rows ? P.row_len[s0] : 0u;
+            if (len > P.long_cap) {
+                long_row = true;
+                const uint32_t b = P.csr_rp[r];
+                const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;
+                for (uint32_t base = 0; base < len; base += kLongChunk) {
+                    const uint32_t m = min(kLongChunk, len - base);
+                    for (uint32_t i = tid; i < m; i += nt) {
+                        const uint32_t k = b + base + i;
+                        const double xv = q == 1 ? ld_vec<true>(srcA + P.csr_ci[k]) : ld_vec<false>(srcA + P.csr_ci[k]);
+                        P.long_prod[blockIdx.x * kLongChunk + i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
+                    }
+                    __syncthreads();
+                    if (tid == 0)
+                        for (uint32_t i = 0; i < m; ++i)
+                            long_acc = __dadd_rn(long_acc, P.long_prod[blockIdx.x * kLongChunk + i]);
+                    __syncthreads();
+                }
+            }
+        }
+        for (uint32_t s = s0 + tid; s < s1; s += nt) {
+            if (long_row && tid != 0) break;
             const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
             if (r >= P.n_rows) continue;
             const uint32_t len = P.row_len[s];
-            const uint64_t c = s >> 5;
-            const uint64_t off = P.chunk_off[c];
-            const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
             double acc;
-            if constexpr (RF == 0)
-                acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
-                             : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
-            else
-                acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
-                             : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+            if (long_row) {
+                acc = long_acc;
+            } else {
+                const uint64_t c = s >> 5;
+                const uint64_t off = P.chunk_off[c];
+                const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
+                if constexpr (RF == 0)
+                    acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                                 : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+                else
+                    acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                                 : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+            }
             if constexpr (KIND == 1) {
                 const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
                 const double own = src[s];
@@ -622,10 +674,10 @@ void launch_warptile(int kind, bool sigma, int grid, uint32_t smem, cudaStream_t
 }
 
 Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
-    if (P->exec && P->exec_csr == A && P->exec->order == (int)(ctx->order == 0 ? 0 : 1) &&
+    if (P->exec && P->exec_csr == A && P->exec->order_knob == ctx->order &&
         P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
         P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads &&
-        P->exec->kernel == (int)ctx->kernel && P->exec->rowfn == (ctx->rowfn == 1 ? 1 : 0)) {
+        P->exec->kernel_knob == ctx->kernel && P->exec->rowfn == (ctx->rowfn == 1 ? 1 : 0)) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -640,25 +692,87 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     }
     auto E = std::make_shared<Executor>();
     E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
+    E->order_knob = ctx->order;
+    E->kernel_knob = ctx->kernel;
     cudaStream_t st = ctx->stream;
-    E->order = ctx->order == 0 ? 0 : 1;
     E->n_rows = A->n_rows;
     E->n_slots = (A->n_rows + 31u) & ~31u;
+    // Row order: explicit, or auto: longest-rows-first (SELL-C-sigma) for power-law row lengths,
+    // Cuthill-McKee inside levels otherwise.
+    if (ctx->order >= 0 && ctx->order <= 2) {
+        E->order = (int)ctx->order;
+    } else {
+        const uint32_t mx = gpu_max_row_len(ctx, A);
+        const double avg = A->n_rows ? (double)A->nnz / A->n_rows : 0.0;
+        E->order = (mx > 64 && mx > 16.0 * avg) ? 2 : 1;
+    }
     E->tile_rows = ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
     if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
     // consumer threads: one per tile row unless forced
     E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
     if (E->threads < E->tile_rows) E->threads = E->tile_rows;
-    E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
-    if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
-    if (E->order == 1) {
-        gpu_level_cm_order(ctx, A, P->level_ptr, E->n_slots, E->slot_row, E->pos);
-        build_sell(ctx, A, E->slot_row.p, E->pos.p, E->own);
+    if (E->order >= 1) {
+        gpu_level_cm_order(ctx, A, P->level_ptr, E->n_slots, E->slot_row, E->pos, E->order);
+        build_sell(ctx, A, E->slot_row.p, E->pos.p, E->own, kLongCap);
         E->S = &E->own;
     } else {
         E->S = &csr_sell(A);
     }
+    E->long_cap = E->S->long_cap;
+    {  // tiles: fixed tile_rows slots, except that a 32-row chunk holding a long row is split
+       // into single-row tiles (each long row gets its own ticket and the whole CTA).
+        std::vector<uint32_t> rl(E->S->n_slots);
+        bool has_long = false;
+        if (E->long_cap != 0xffffffffu && E->S->n_slots) {
+            MPKG_CUDA(cudaMemcpyAsync(rl.data(), E->S->row_len.p, 4ull * rl.size(), cudaMemcpyDeviceToHost, st));
+            MPKG_CUDA(cudaStreamSynchronize(st));
+            for (uint32_t v : rl)
+                if (v > E->long_cap) {
+                    has_long = true;
+                    break;
+                }
+        }
+        E->h_tile_start.clear();
+        if (has_long) {
+            const uint32_t per = E->tile_rows / 32;
+            uint32_t c = 0, nch = E->S->n_chunks;
+            while (c < nch) {
+                bool lg = false;
+                for (uint32_t i = 0; i < 32; ++i) lg |= rl[c * 32 + i] > E->long_cap;
+                if (lg) {
+                    for (uint32_t i = 0; i < 32; ++i) E->h_tile_start.push_back(c * 32 + i);
+                    ++c;
+                    continue;
+                }
+                E->h_tile_start.push_back(c * 32);
+                uint32_t k = 1;
+                ++c;
+                while (k < per && c < nch) {
+                    bool lg2 = false;
+                    for (uint32_t i = 0; i < 32; ++i) lg2 |= rl[c * 32 + i] > E->long_cap;
+                    if (lg2) break;
+                    ++k;
+                    ++c;
+                }
+            }
+            E->h_tile_start.push_back(E->S->n_slots);
+            E->n_tiles = (uint32_t)E->h_tile_start.size() - 1;
+            E->tile_start.alloc(E->h_tile_start.size());
+            MPKG_CUDA(cudaMemcpyAsync(E->tile_start.p, E->h_tile_start.data(), 4ull * E->h_tile_start.size(),
+                                      cudaMemcpyHostToDevice, st));
+            E->long_rows = 0;
+            for (uint32_t v : rl) E->long_rows += v > E->long_cap;
+        } else {
+            E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
+        }
+    }
+    if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
+    if (!E->h_tile_start.empty()) E->kernel_forced_lean = true;
     const uint32_t nt = E->n_tiles;
+    auto tile_first = [&](uint32_t T) -> uint32_t {
+        return E->h_tile_start.empty() ? std::min<uint64_t>((uint64_t)T * E->tile_rows, E->n_slots)
+                                       : E->h_tile_start[T];
+    };
     {  // tile extents in the SELL arrays; staging buffer size; oversized tiles
         std::vector<uint64_t> off(E->S->n_chunks + 1);
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E->S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
@@ -667,12 +781,11 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->tile_bytes.assign(nt, 0);
         E->big.assign(nt, 0);
         uint64_t max_buf = 256;
-        for (uint32_t T = 0; T <= nt; ++T)
-            toff[T] = off[std::min<uint64_t>((uint64_t)T * (E->tile_rows / 32), E->S->n_chunks)];
+        for (uint32_t T = 0; T <= nt; ++T) toff[T] = off[std::min<uint64_t>((tile_first(T) + 31) / 32, E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
-            const uint64_t ne = toff[T + 1] - toff[T];
+            const uint64_t ne = toff[T + 1] >= toff[T] ? toff[T + 1] - toff[T] : 0;
             const uint64_t bytes = (4 * ne + 127) & ~127ull;  // staged: column indices
-            E->tile_bytes[T] = 12 * ne + E->tile_rows * 8 * 3;
+            E->tile_bytes[T] = 12 * ne + (uint64_t)(tile_first(T + 1) - tile_first(T)) * 8 * 3;
             if (bytes > kMaxBufBytes)
                 E->big[T] = 1;
             else
@@ -699,7 +812,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->tile_knob = ctx->tile_rows;
     E->thread_knob = ctx->threads;
     int occ = 0;
-    E->kernel = (int)ctx->kernel;
+    E->kernel = E->kernel_forced_lean ? 0 : (int)ctx->kernel;  // long rows: lean kernel only
     if (E->kernel == 2) {
         E->threads = 128;
         E->stages = 1;
@@ -740,7 +853,8 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (nt) {
         k_dep_buckets<<<grid_for(A->n_rows, 256), 256, 0, st>>>(
             A->row_ptr.p, A->col_idx.p, A->n_rows, E->order ? E->slot_row.p : nullptr,
-            E->order ? E->pos.p : nullptr, d_lp.p, nl, E->tile_rows, bmin.p, bmax.p);
+            E->order ? E->pos.p : nullptr, d_lp.p, nl, E->tile_rows,
+            E->h_tile_start.empty() ? nullptr : E->tile_start.p, nt, bmin.p, bmax.p);
         MPKG_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -751,13 +865,18 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->h_ptr.assign(nt + 1, 0);
     E->h_lo.clear();
     E->h_hi.clear();
+    auto slot_tile = [&](uint32_t sl) -> uint32_t {
+        if (E->h_tile_start.empty()) return sl / E->tile_rows;
+        return (uint32_t)(std::upper_bound(E->h_tile_start.begin(), E->h_tile_start.end(), sl) -
+                          E->h_tile_start.begin()) - 1;
+    };
     std::vector<std::pair<uint32_t, uint32_t>> runs;
     for (uint32_t T = 0; T < nt; ++T) {
         runs.clear();
         runs.push_back({T, T});
         for (int b = 0; b < kBuckets; ++b) {
             const uint64_t i = (uint64_t)T * kBuckets + b;
-            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i] / E->tile_rows, hmax[i] / E->tile_rows});
+            if (hmin[i] <= hmax[i]) runs.push_back({slot_tile(hmin[i]), slot_tile(hmax[i])});
         }
         std::sort(runs.begin(), runs.end());
         uint32_t lo = runs[0].first, hi = runs[0].second;
@@ -785,6 +904,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     }
     E->done.alloc(std::max<uint32_t>(nt, 1));
     E->counter.alloc(1);
+    if (E->long_rows) E->long_prod.alloc((uint64_t)E->grid * kLongChunk);
     MPKG_CUDA(cudaStreamSynchronize(st));
     P->exec = E;
     P->exec_csr = A;
@@ -924,6 +1044,12 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.stages = E.stages;
     P.tile_rows = E.tile_rows;
     P.wt_lmax = E.wt_lmax;
+    P.tile_start = E.h_tile_start.empty() ? nullptr : E.tile_start.p;
+    P.long_cap = E.long_cap;
+    P.csr_rp = A->row_ptr.p;
+    P.csr_ci = A->col_idx.p;
+    P.csr_v = A->values.p;
+    P.long_prod = E.long_rows ? E.long_prod.p : nullptr;
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;

@@ -20,12 +20,15 @@ __global__ void k_sell_lengths(const uint32_t* __restrict__ rp, uint32_t n_rows,
 }
 
 // One warp per chunk: L = max row length in the chunk; entries = 32*L.
+// Rows longer than `cap` ("long rows") are left out of the SELL arrays; the fused kernel
+// processes them CTA-cooperatively from the CSR (mpk_exec.cu).
 __global__ void k_sell_chunk_sizes(const uint32_t* __restrict__ row_len, uint32_t n_chunks,
-                                   uint64_t* __restrict__ chunk_entries) {
+                                   uint32_t cap, uint64_t* __restrict__ chunk_entries) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; c < n_chunks;
          c += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         uint32_t L = row_len[c * 32 + lane];
+        if (L > cap) L = 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) L = max(L, __shfl_xor_sync(0xffffffffu, L, o));
         if (lane == 0) chunk_entries[c] = 32ull * L;
@@ -36,13 +39,13 @@ __global__ void k_sell_fill(const uint32_t* __restrict__ rp, const uint32_t* __r
                             const double* __restrict__ v, uint32_t n_rows,
                             const uint32_t* __restrict__ slot_row,
                             const uint64_t* __restrict__ chunk_off,
-                            const uint32_t* __restrict__ row_len, uint32_t n_slots,
+                            const uint32_t* __restrict__ row_len, uint32_t n_slots, uint32_t cap,
                             const uint32_t* __restrict__ col_map, uint32_t* __restrict__ cols,
                             double* __restrict__ vals) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t len = row_len[s];
-        if (len == 0) continue;
+        if (len == 0 || len > cap) continue;
         const uint32_t r = slot_row ? slot_row[s] : (uint32_t)s;
         const uint64_t c = s >> 5;
         const uint32_t lane = (uint32_t)(s & 31);
@@ -85,7 +88,8 @@ __global__ void __launch_bounds__(256) k_spmv_sell(
 }  // namespace
 
 void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row,
-                const uint32_t* d_col_map, Sell& S) {
+                const uint32_t* d_col_map, Sell& S, uint32_t long_cap) {
+    S.long_cap = long_cap;
     cudaStream_t st = ctx->stream;
     S.n_rows = A->n_rows;
     S.n_slots = (A->n_rows + 31u) & ~31u;
@@ -103,7 +107,7 @@ void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row
     DevBuf<uint64_t> sizes(S.n_chunks + 1);
     MPKG_CUDA(cudaMemsetAsync(sizes.p + S.n_chunks, 0, sizeof(uint64_t), st));
     k_sell_chunk_sizes<<<grid_for((uint64_t)S.n_chunks * 32, 256), 256, 0, st>>>(
-        S.row_len.p, S.n_chunks, sizes.p);
+        S.row_len.p, S.n_chunks, long_cap, sizes.p);
     MPKG_LAUNCH_CHECK();
     S.chunk_off.alloc(S.n_chunks + 1);
     size_t tmp_bytes = 0;
@@ -126,7 +130,7 @@ void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row
     }
     k_sell_fill<<<grid_for(S.n_slots, 256), 256, 0, st>>>(
         A->row_ptr.p, A->col_idx.p, A->values.p, A->n_rows, d_slot_row, S.chunk_off.p,
-        S.row_len.p, S.n_slots, d_col_map, S.cols.p, S.vals.p);
+        S.row_len.p, S.n_slots, long_cap, d_col_map, S.cols.p, S.vals.p);
     MPKG_LAUNCH_CHECK();
     ctx->launches += 3;
 }
@@ -134,7 +138,7 @@ void build_sell(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_slot_row
 Sell& csr_sell(mpkg_csr_s* A) {
     if (!A->sell) {
         auto S = std::make_unique<Sell>();
-        build_sell(A->ctx, A, nullptr, nullptr, *S);
+        build_sell(A->ctx, A, nullptr, nullptr, *S, 0xffffffffu);
         A->sell = std::move(S);
     }
     return *A->sell;

@@ -197,6 +197,53 @@ def test_fused_orders_and_schedules(ctx, cases, oracle, order, slack):
         ctx.set_param("slack", -1)
 
 
+def _arrow_matrix(n=6000, hubs=(0, 17, 2500), seed=5):
+    """Tridiagonal band plus a few dense hub rows/columns (rows far longer than the SELL long-row
+    cap), symmetric pattern."""
+    rng = np.random.default_rng(seed)
+    rows = {i: {i: 4.0} for i in range(n)}
+    for i in range(n - 1):
+        rows[i][i + 1] = rows[i + 1][i] = -1.0
+    for h in hubs:
+        for j in rng.choice(n, size=n // 2, replace=False):
+            if j != h:
+                v = -float(rng.uniform(0.1, 1.0))
+                rows[h][int(j)] = v
+                rows[int(j)][h] = v
+    rp, ci, vv = [0], [], []
+    for i in range(n):
+        for j in sorted(rows[i]):
+            ci.append(j)
+            vv.append(rows[i][j])
+        rp.append(len(ci))
+    return mpkg.HostCsr.from_arrays(rp, ci, vv)
+
+
+@pytest.mark.parametrize("order", [-1, 0, 1, 2])
+def test_long_rows_and_length_order(ctx, oracle, order):
+    """Hub rows (>1024 entries) take the CTA-cooperative path; every order gives the same bits."""
+    try:
+        ctx.set_param("order", order)
+        for A in (_arrow_matrix(), mpkg.rmat(15, 16, 7)):
+            lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+            P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
+            assert np.diff(P.row_ptr.astype(np.int64)).max() > 1024
+            Ap = ctx.csr(P)
+            ls = ctx.levels_from_host(lv, pm, ip, lp)
+            x = mpkg.random_vector(P.n_rows, 3)
+            plan = ctx.group_levels(ls, Ap, 8 << 20, 4)
+            ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4)
+            assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref, f"order={order}")
+            sh = [1.0, 2.0 + 0.5j, 2.0 - 0.5j, 0.5]
+            ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+            assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, "shifted")
+            coef = [0.5, -1.0, 0.25, 2.0, -0.125]
+            zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+            assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, "poly")
+    finally:
+        ctx.set_param("order", -1)
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
