@@ -48,6 +48,7 @@ constexpr uint32_t kLastUse = 1u << 30;  // ticket flag: last use of the tile in
 constexpr uint32_t kBig = 1u << 31;      // ticket flag: tile too large for the smem buffer
 constexpr uint32_t kMaxBufBytes = 96 * 1024;
 constexpr uint32_t kLongCap = 1024;    // rows longer than this take the CTA-cooperative path
+constexpr uint32_t kSB = 64;           // tiles per completion-counter superblock
 constexpr uint32_t kLongChunk = 4096;  // products per chunk of a long row
 #ifndef MPKG_GROUP
 #define MPKG_GROUP 16
@@ -90,6 +91,7 @@ struct Executor {
     DevBuf<double> long_prod;                 // grid * kLongChunk product scratch
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
+    DevBuf<uint32_t> sb_count;                // (kMaxFusedP+1) x n_sb superblock counters
     DevBuf<double> V;   // sigma-order working vectors (order 1)
     DevBuf<double> zs;  // sigma-order polynomial accumulator (order 1)
 };
@@ -121,6 +123,9 @@ struct FusedParams {
     const uint32_t* csr_ci;
     const double* csr_v;
     double* long_prod;           // per-CTA product scratch for long rows (grid * kLongChunk)
+    uint32_t* sb_count;          // [(p+1) * n_sb] completions per power and superblock
+    uint32_t n_sb;
+    uint32_t n_tiles;
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -184,6 +189,57 @@ __device__ __forceinline__ void tma_tile(const FusedParams& P, uint32_t T, bool 
             "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(buf)),
             "l"(P.cols + e0), "r"(cb), "r"(smem_u32(bar)), "l"(pol)
             : "memory");
+}
+
+// Dependency check over the runs of tile T for power `need` (= q-1).  A run [lo, hi] is walked
+// as units: whole superblocks of kSB tiles (one completion counter per power and superblock,
+// incremented by every tile that finishes that power) and the individual flags of the tiles at
+// its ragged ends, thread-strided.  Power-law matrices (R-MAT) have runs of ~10^4-10^5 tiles;
+// counters bound the poll to O(run/kSB + 2*kSB) loads.
+template <bool ACQUIRE>
+__device__ __forceinline__ int deps_ready(const FusedParams& P, uint32_t r0, uint32_t r1,
+                                          uint32_t need, uint32_t tid, uint32_t nt) {
+    for (uint32_t run = r0; run < r1; ++run) {
+        const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run] + 1;  // [lo, hi)
+        const uint32_t sb_lo = (lo + kSB - 1) / kSB, sb_hi = hi / kSB;
+        uint32_t head, n_sb;
+        if (sb_lo < sb_hi) {
+            head = sb_lo * kSB - lo;
+            n_sb = sb_hi - sb_lo;
+        } else {
+            head = hi - lo;
+            n_sb = 0;
+        }
+        const uint32_t tail_lo = n_sb ? sb_hi * kSB : hi;
+        const uint32_t units = head + n_sb + (hi - tail_lo);
+        for (uint32_t u = tid; u < units; u += nt) {
+            uint32_t v;
+            bool ok;
+            if (u < head) {
+                const uint32_t* f = P.done + lo + u;
+                v = ACQUIRE ? ld_acquire(f) : ld_relaxed(f);
+                ok = v >= need;
+            } else if (u < head + n_sb) {
+                const uint32_t sb = sb_lo + (u - head);
+                const uint32_t* f = P.sb_count + (uint64_t)need * P.n_sb + sb;
+                v = ACQUIRE ? ld_acquire(f) : ld_relaxed(f);
+                ok = v >= min(kSB, P.n_tiles - sb * kSB);
+            } else {
+                const uint32_t* f = P.done + tail_lo + (u - head - n_sb);
+                v = ACQUIRE ? ld_acquire(f) : ld_relaxed(f);
+                ok = v >= need;
+            }
+            if (!ACQUIRE && !ok) return 0;
+        }
+    }
+    return 1;
+}
+
+// Publishes "tile T finished power q": the tile flag and its superblock's counter for q.
+__device__ __forceinline__ void publish(const FusedParams& P, uint32_t T, uint32_t q) {
+    st_release(P.done + T, q);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.sb_count + (uint64_t)q * P.n_sb + T / kSB)
+                 : "memory");
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -315,22 +371,8 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
             // Poll with relaxed loads (no L1 invalidation), then acquire each observed flag
             // once (flags are monotone).
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
-            for (;;) {
-                int ok = 1;
-                for (uint32_t run = r0; run < r1 && ok; ++run) {
-                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += nc)
-                        if (ld_relaxed(P.done + u) < q - 1) {
-                            ok = 0;
-                            break;
-                        }
-                }
-                if (consumers_and(ok, nc)) break;
-                __nanosleep(32);
-            }
-            for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += nc)
-                    (void)ld_acquire(P.done + u);
+            while (!consumers_and(deps_ready<false>(P, r0, r1, q - 1, tid, nc), nc)) __nanosleep(32);
+            (void)deps_ready<true>(P, r0, r1, q - 1, tid, nc);  // acquire each unit once
             consumers_sync(nc);  // publishes every consumer's acquires to all consumers
         }
         const bool big = code & kBig;
@@ -377,7 +419,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
         }
         consumers_sync(nc);  // tile done: results written, buffer no longer read
         if (tid == 0) {
-            st_release(P.done + T, q);
+            publish(P, T, q);
             mbar_arrive(&empty[buf]);
         }
     }
@@ -405,22 +447,8 @@ __global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_con
         const uint32_t q = (code >> 24) & 63u;
         if (q > 1) {
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
-            for (;;) {
-                int ok = 1;
-                for (uint32_t run = r0; run < r1 && ok; ++run) {
-                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += nt)
-                        if (ld_relaxed(P.done + u) < q - 1) {
-                            ok = 0;
-                            break;
-                        }
-                }
-                if (__syncthreads_and(ok)) break;
-                __nanosleep(32);
-            }
-            for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += nt)
-                    (void)ld_acquire(P.done + u);
+            while (!__syncthreads_and(deps_ready<false>(P, r0, r1, q - 1, tid, nt))) __nanosleep(32);
+            (void)deps_ready<true>(P, r0, r1, q - 1, tid, nt);  // acquire each unit once
             __syncthreads();
         }
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
@@ -493,7 +521,7 @@ __global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_con
             }
         }
         __syncthreads();
-        if (tid == 0) st_release(P.done + T, q);
+        if (tid == 0) publish(P, T, q);
     }
 }
 
@@ -522,22 +550,8 @@ __global__ void __launch_bounds__(128) k_mpk_warptile(const __grid_constant__ Fu
         const uint32_t q = (code >> 24) & 63u;
         if (q > 1) {
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
-            for (;;) {
-                int ok = 1;
-                for (uint32_t run = r0; run < r1 && ok; ++run) {
-                    const uint32_t lo = P.dep_lo[run], hi = P.dep_hi[run];
-                    for (uint32_t u = lo + tid; u <= hi; u += 128u)
-                        if (ld_relaxed(P.done + u) < q - 1) {
-                            ok = 0;
-                            break;
-                        }
-                }
-                if (__syncthreads_and(ok)) break;
-                __nanosleep(32);
-            }
-            for (uint32_t run = r0; run < r1; ++run)
-                for (uint32_t u = P.dep_lo[run] + tid; u <= P.dep_hi[run]; u += 128u)
-                    (void)ld_acquire(P.done + u);
+            while (!__syncthreads_and(deps_ready<false>(P, r0, r1, q - 1, tid, 128u))) __nanosleep(32);
+            (void)deps_ready<true>(P, r0, r1, q - 1, tid, 128u);  // acquire each unit once
             __syncthreads();
         }
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
@@ -606,7 +620,7 @@ __global__ void __launch_bounds__(128) k_mpk_warptile(const __grid_constant__ Fu
             }
         }
         __syncthreads();
-        if (tid == 0) st_release(P.done + T, q);
+        if (tid == 0) publish(P, T, q);
     }
 }
 
@@ -1022,7 +1036,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const DevBuf<uint32_t>& tk = get_tickets(ctx, E, a.p);
     const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
-    const bool sigma = E.order == 1;
+    const bool sigma = E.order >= 1;  // any private order (CM or length-sorted)
     FusedParams P{};
     P.cols = S.cols.p;
     P.vals = S.vals.p;
@@ -1050,6 +1064,11 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.csr_ci = A->col_idx.p;
     P.csr_v = A->values.p;
     P.long_prod = E.long_rows ? E.long_prod.p : nullptr;
+    P.n_tiles = E.n_tiles;
+    P.n_sb = (E.n_tiles + kSB - 1) / kSB;
+    E.sb_count.ensure((uint64_t)(kMaxFusedP + 1) * P.n_sb + 1);
+    P.sb_count = E.sb_count.p;
+    MPKG_CUDA(cudaMemsetAsync(E.sb_count.p, 0, 4ull * (a.p + 1) * P.n_sb, st));
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
