@@ -54,6 +54,7 @@ _SIGS = {
     "mpkg_plan_get": [P, P, P, P],
     "mpkg_plan_destroy": [P],
     "mpkg_plan_exec_info": [P, pu32, pu64, pu64, pu32],
+    "mpkg_plan_exec_mode": [P, pint, pint, pint, pu64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],
     "mpkg_baseline_mpk": [P, P, P, i32, P, u64, u64],
     "mpkg_baseline_mpk_dev": [P, P, P, i32, P, u64, u64],

@@ -284,8 +284,12 @@ class ExecutionPlan:
     def exec_info(self) -> dict:
         t, k, d, pp = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
         check(lib.mpkg_plan_exec_info(self.h, C.byref(t), C.byref(k), C.byref(d), C.byref(pp)))
+        o, sw, kn, lr = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
+        check(lib.mpkg_plan_exec_mode(self.h, C.byref(o), C.byref(sw), C.byref(kn), C.byref(lr)))
         return {"tiles": t.value, "tickets": k.value, "dep_tiles": d.value,
-                "pass_powers": pp.value}
+                "pass_powers": pp.value, "order": o.value,
+                "schedule": "sweeps" if sw.value else "fused", "kernel": kn.value,
+                "long_rows": lr.value}
 
     def __del__(self):
         if getattr(self, "h", None):

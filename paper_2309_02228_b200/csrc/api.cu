@@ -261,17 +261,28 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->group = value;
         else if (k == "stages")
             ctx->stages = value;
-        else if (k == "rowfn")
-            ctx->rowfn = value;
         else if (k == "kernel") {
-            require(value >= 0 && value <= 2,
-                    "ctx_set_param: kernel must be 0 (lean), 1 (staged) or 2 (warp-tile)");
+            require(value >= 0 && value <= 5 && value != 3,
+                    "ctx_set_param: kernel must be 0 (lean), 1 (staged), 2 (warp-tile) or 4 (async gather)");
             ctx->kernel = value;
+        }
+        else if (k == "schedule") {
+            require(value >= 0 && value <= 2, "ctx_set_param: schedule must be 0 (auto), 1 (fused) or 2 (sweeps)");
+            ctx->schedule = value;
+        }
+        else if (k == "producers") {
+            require(value >= 0 && value <= 8, "ctx_set_param: producers must be in [0, 8]");
+            ctx->producers = value;
+        }
+        else if (k == "cgroups") {
+            require(value >= 0 && value <= 8, "ctx_set_param: cgroups must be in [0, 8]");
+            ctx->cgroups = value;
         }
         else if (k == "kernel_timing")
             ctx->kernel_timing = value != 0;
         else if (k == "tile_rows") {
-            require(value == 64 || value == 128 || value == 256, "ctx_set_param: tile_rows must be 64, 128 or 256");
+            require(value == 32 || value == 64 || value == 128 || value == 256,
+                    "ctx_set_param: tile_rows must be 32 (async kernel), 64, 128 or 256");
             ctx->tile_rows = value;
         } else if (k == "threads") {
             require(value == 0 || value == 256 || value == 512,
@@ -680,6 +691,13 @@ int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets, u
     return guarded([&] {
         require(P != nullptr, "plan_exec_info: null plan");
         exec_info(P, n_tiles, n_tickets, n_deps, pass_powers);
+    });
+}
+
+int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uint64_t* long_rows) {
+    return guarded([&] {
+        require(P != nullptr, "plan_exec_mode: null plan");
+        exec_mode(P, order, sweeps, kernel, long_rows);
     });
 }
 

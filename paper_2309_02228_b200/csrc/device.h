@@ -93,7 +93,7 @@ struct mpkg_ctx_s {
     size_t persist_max = 0;
     int mode = MPKG_MODE_BITWISE;
     // executor knobs (mpkg_ctx_set_param)
-    int64_t tile_rows = 128;  // rows per fused-kernel tile (64, 128 or 256)
+    int64_t tile_rows = 128;  // rows per fused-kernel tile (32, 64, 128 or 256)
     int64_t slack = -1;  // -1: resident CTA count
     int64_t order = -1;       // -1 auto, 0 A_perm order, 1 Cuthill-McKee, 2 longest rows first
     int64_t pass_powers = 0;  // >0: force powers per fused pass
@@ -102,8 +102,10 @@ struct mpkg_ctx_s {
     int64_t group = 8;        // phase-1 gathers in flight per thread (8 or 16)
     int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
-    int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile
-    int64_t rowfn = 0;        // lean row loop: 0 pipelined pairs, 1 groups of 8 (32 regs)
+    int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
+    int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power (mpk_exec.cu)
+    int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
+    int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)
     uint64_t launches = 0;
     // live timing of the fused / power kernels (mpkg_ctx_set_param "kernel_timing")
     bool kernel_timing = false;
@@ -177,6 +179,7 @@ void gpu_level_cm_order(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const std::vector<
                         uint32_t n_slots, DevBuf<uint32_t>& slot_row, DevBuf<uint32_t>& pos,
                         int mode);
 uint32_t gpu_max_row_len(mpkg_ctx_s* ctx, const mpkg_csr_s* A);
+double gpu_mean_first_col_jump(mpkg_ctx_s* ctx, const mpkg_csr_s* A);
 void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
                       double* dst, const double* src2, double shift_a, double shift_b2);
 
@@ -207,5 +210,6 @@ struct FusedArgs {
 void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& a);
 void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
                uint32_t* pass_powers);
+void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
 
 }  // namespace mpkg_detail

@@ -78,9 +78,13 @@ struct Executor {
     int group = 16;                           // row group width G of the kernel instance
     int64_t stage_knob = 0;                   // ctx->stages the executor was built with
     int64_t tile_knob = 0, thread_knob = 0;   // ctx->tile_rows / ctx->threads likewise
-    int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused, 2: k_mpk_warptile
+    int kernel = 0;                           // 0: k_mpk_lean, 1: k_mpk_fused, 2: k_mpk_warptile, 4: k_mpk_async
+    uint64_t ne_max = 0;                      // most SELL entries in one tile
+    uint32_t n_prod = 0, n_cgroups = 0;       // k_mpk_async roles
+    bool sb = false;                          // poll dependencies through superblock counters
+    bool last_sweep = false;                  // the last run used one launch per power
+    int64_t prod_knob = 0, cg_knob = 0;
     uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
-    int rowfn = 0;                            // lean kernel row loop (0 pipelined, 1 grouped)
     int64_t order_knob = -1;                  // ctx->order the executor was built with
     uint32_t long_cap = 0xffffffffu;          // rows above this length: CTA-cooperative path
     uint64_t long_rows = 0;                   // how many
@@ -126,6 +130,8 @@ struct FusedParams {
     uint32_t* sb_count;          // [(p+1) * n_sb] completions per power and superblock
     uint32_t n_sb;
     uint32_t n_tiles;
+    uint32_t n_prod;        // async kernel: producer warps per CTA
+    uint32_t n_cgroups;     // async kernel: consumer groups (tile_rows threads each) per CTA
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -235,10 +241,27 @@ __device__ __forceinline__ int deps_ready(const FusedParams& P, uint32_t r0, uin
     return 1;
 }
 
-// Publishes "tile T finished power q": the tile flag and its superblock's counter for q.
+// Dependency check over tile flags only (short runs: every 3D stencil after the level order).
+template <bool ACQUIRE>
+__device__ __forceinline__ int deps_ready_flags(const FusedParams& P, uint32_t r0, uint32_t r1,
+                                                uint32_t need, uint32_t tid, uint32_t nt) {
+    for (uint32_t run = r0; run < r1; ++run) {
+        const uint32_t hi = P.dep_hi[run];
+        for (uint32_t u = P.dep_lo[run] + tid; u <= hi; u += nt) {
+            const uint32_t v = ACQUIRE ? ld_acquire(P.done + u) : ld_relaxed(P.done + u);
+            if (!ACQUIRE && v < need) return 0;
+        }
+    }
+    return 1;
+}
+
+// Publishes "tile T finished power q": the tile flag and its superblock's counter for q.  One
+// release fence covers both strong writes (fence + relaxed store / reduction = two release
+// patterns), so the publishing thread pays for a single fence.
 __device__ __forceinline__ void publish(const FusedParams& P, uint32_t T, uint32_t q) {
-    st_release(P.done + T, q);
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.sb_count + (uint64_t)q * P.n_sb + T / kSB)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + T), "r"(q) : "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(P.sb_count + (uint64_t)q * P.n_sb + T / kSB)
                  : "memory");
 }
 
@@ -425,14 +448,85 @@ __global__ void __launch_bounds__(kMaxThreads + 32) k_mpk_fused(const __grid_con
     }
 }
 
+// Epilogue of one finished row (slot s, A_perm row r) at power q: shift, stores, polynomial.
+template <int KIND, bool SIGMA>
+__device__ __forceinline__ void row_epilogue(const FusedParams& P, uint32_t s, uint32_t r, uint32_t q,
+                                             const double* src, double acc) {
+    if constexpr (KIND == 1) {
+        const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
+        const double own = src[s];
+        const double own2 = b2 != 0.0 ? P.V[(uint64_t)(q - 2) * P.vstride + s] : 0.0;
+        acc = shift_epilogue(acc, a, b2, own, own2);
+    }
+    P.V[(uint64_t)q * P.vstride + s] = acc;
+    if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
+    if constexpr (KIND == 2) {
+        double zr;
+        if (q == 1)
+            zr = __dadd_rn(__dmul_rn(P.coef[0], src[s]), __dmul_rn(P.coef[1], acc));
+        else
+            zr = __dadd_rn(P.zs[s], __dmul_rn(P.coef[q], acc));
+        P.zs[s] = zr;
+        if (SIGMA && q == P.p) P.z[r] = zr;
+    }
+}
+
+// Long row of a single-row tile (see k_mpk_lean): CTA-wide products, thread 0 sums in order.
+// Returns true (and the sum in thread 0's `acc`) when slot s0 holds a long row.
+template <bool SIGMA>
+__device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, uint32_t q,
+                                             uint64_t pol, uint32_t tid, uint32_t nt, double& acc) {
+    const uint32_t r = SIGMA ? P.slot_row[s0] : s0;
+    const uint32_t len = r < P.n_rows ? P.row_len[s0] : 0u;
+    if (len <= P.long_cap) return false;
+    const uint32_t b = P.csr_rp[r];
+    const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;
+    acc = 0.0;
+    for (uint32_t base = 0; base < len; base += kLongChunk) {
+        const uint32_t m = min(kLongChunk, len - base);
+        for (uint32_t i = tid; i < m; i += nt) {
+            const uint32_t k = b + base + i;
+            const double xv = q == 1 ? ld_vec<true>(srcA + P.csr_ci[k]) : ld_vec<false>(srcA + P.csr_ci[k]);
+            P.long_prod[blockIdx.x * kLongChunk + i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (uint32_t i = 0; i < m; ++i) acc = __dadd_rn(acc, P.long_prod[blockIdx.x * kLongChunk + i]);
+        __syncthreads();
+    }
+    return true;
+}
+
+// Sweep schedule: one launch per power over the executor's SELL (private order), grid-stride
+// rows, the grouped row loop (8 gathers in flight per thread).  Slice q-1 is complete before the
+// launch, so every gather takes the read-only path.  Used when no temporal blocking fits in L2
+// (the fused kernel would only add ticket and dependency overhead), see run_fused.
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_mpk_sweep(const __grid_constant__ FusedParams P, uint32_t q) {
+    const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    const uint64_t pol = l2_policy_first();
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < P.n_slots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = SIGMA ? P.slot_row[s] : (uint32_t)s;
+        if (r >= P.n_rows) continue;
+        const uint32_t len = P.row_len[s];
+        const uint64_t off = P.chunk_off[s >> 5];
+        const uint32_t L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
+        const double acc = sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+    }
+}
+
 // Lean variant ("kernel" knob 0): no shared-memory staging and no producer warp, so registers
 // stay low and many warps are resident (the row loop is latency-bound: throughput follows
 // resident warps).  One thread per tile row; thread 0 claims the next ticket while the current
 // one runs (double-buffered claim, deadlock-free for the same reason as above).
-// RF 0: software-pipelined pairs (sell_row_dot_pipe); RF 1: groups of 8 entries
-// (sell_row_dot<.,8>) with a 32-register cap so 16 CTAs of 128 threads (64 warps) fit per SM.
-template <int KIND, bool SIGMA, int RF>
-__global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_constant__ FusedParams P) {
+// Row loop: software-pipelined pairs (sell_row_dot_pipe), ~40 registers -> 12 CTAs per SM.
+// No minimum-blocks bound: capping ptxas at 40 registers makes it spill, left alone it fits.
+// VT: variable tiles (long rows, single-row tiles); SB: wide dependency runs polled through the
+// superblock counters (otherwise tile flags only).
+template <int KIND, bool SIGMA, bool VT, bool SB>
+__global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedParams P) {
     __shared__ uint32_t s_ticket[2];
     const uint32_t tid = threadIdx.x;
     const uint32_t nt = blockDim.x;
@@ -447,81 +541,237 @@ __global__ void __launch_bounds__(128, RF ? 16 : 12) k_mpk_lean(const __grid_con
         const uint32_t q = (code >> 24) & 63u;
         if (q > 1) {
             const uint32_t r0 = P.dep_ptr[T], r1 = P.dep_ptr[T + 1];
-            while (!__syncthreads_and(deps_ready<false>(P, r0, r1, q - 1, tid, nt))) __nanosleep(32);
-            (void)deps_ready<true>(P, r0, r1, q - 1, tid, nt);  // acquire each unit once
+            if constexpr (SB) {
+                while (!__syncthreads_and(deps_ready<false>(P, r0, r1, q - 1, tid, nt))) __nanosleep(32);
+                (void)deps_ready<true>(P, r0, r1, q - 1, tid, nt);  // acquire each unit once
+            } else {
+                while (!__syncthreads_and(deps_ready_flags<false>(P, r0, r1, q - 1, tid, nt))) __nanosleep(32);
+                (void)deps_ready_flags<true>(P, r0, r1, q - 1, tid, nt);
+            }
             __syncthreads();
         }
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
         const uint64_t pol = l2_policy(code & kLastUse);
-        const uint32_t s0 = P.tile_start ? P.tile_start[T] : T * P.tile_rows;
-        const uint32_t s1 = P.tile_start ? P.tile_start[T + 1] : s0 + P.tile_rows;
-        bool long_row = false;
+        const uint32_t s0 = VT ? P.tile_start[T] : T * P.tile_rows;
+        const uint32_t s1 = VT ? P.tile_start[T + 1] : s0 + P.tile_rows;
         double long_acc = 0.0;
-        if (s1 - s0 == 1 && P.long_prod) {
+        if (VT && s1 - s0 == 1 && long_row_dot<SIGMA>(P, s0, q, pol, tid, nt, long_acc)) {
             // A single-row tile holding a long row (len > SELL long_cap, e.g. an R-MAT hub): the
             // CTA computes the products from the row's contiguous A_perm CSR slice in chunks,
             // gathering from the A_perm-order copy of y_{q-1} in the caller's block, and one
             // thread adds them in stored order (same formula, same order: bitwise).
-            const uint32_t r = SIGMA ? P.slot_row[s0] : s0;
-            const uint32_t len = r < P.n_rows ? P.row_len[s0] : 0u;
-            if (len > P.long_cap) {
-                long_row = true;
-                const uint32_t b = P.csr_rp[r];
-                const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;
-                for (uint32_t base = 0; base < len; base += kLongChunk) {
-                    const uint32_t m = min(kLongChunk, len - base);
-                    for (uint32_t i = tid; i < m; i += nt) {
-                        const uint32_t k = b + base + i;
-                        const double xv = q == 1 ? ld_vec<true>(srcA + P.csr_ci[k]) : ld_vec<false>(srcA + P.csr_ci[k]);
-                        P.long_prod[blockIdx.x * kLongChunk + i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
-                    }
-                    __syncthreads();
-                    if (tid == 0)
-                        for (uint32_t i = 0; i < m; ++i)
-                            long_acc = __dadd_rn(long_acc, P.long_prod[blockIdx.x * kLongChunk + i]);
-                    __syncthreads();
-                }
-            }
-        }
-        for (uint32_t s = s0 + tid; s < s1; s += nt) {
-            if (long_row && tid != 0) break;
-            const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
-            if (r >= P.n_rows) continue;
-            const uint32_t len = P.row_len[s];
-            double acc;
-            if (long_row) {
-                acc = long_acc;
-            } else {
+            if (tid == 0) row_epilogue<KIND, SIGMA>(P, s0, SIGMA ? P.slot_row[s0] : s0, q, src, long_acc);
+        } else {
+            const uint32_t nrows = VT ? s1 - s0 : P.tile_rows;
+            for (uint32_t row = tid; row < nrows; row += nt) {
+                const uint32_t s = (VT ? s0 : T * P.tile_rows) + row;
+                const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+                if (r >= P.n_rows) continue;
+                const uint32_t len = P.row_len[s];
                 const uint64_t c = s >> 5;
                 const uint64_t off = P.chunk_off[c];
                 const uint32_t L = (uint32_t)((P.chunk_off[c + 1] - off) >> 5);
-                if constexpr (RF == 0)
-                    acc = q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
-                                 : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
-                else
-                    acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol)
-                                 : sell_row_dot<false, 8>(P.cols, P.vals, off, L, s & 31, len, src, pol);
-            }
-            if constexpr (KIND == 1) {
-                const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
-                const double own = src[s];
-                const double own2 = b2 != 0.0 ? P.V[(uint64_t)(q - 2) * P.vstride + s] : 0.0;
-                acc = shift_epilogue(acc, a, b2, own, own2);
-            }
-            P.V[(uint64_t)q * P.vstride + s] = acc;
-            if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
-            if constexpr (KIND == 2) {
-                double zr;
-                if (q == 1)
-                    zr = __dadd_rn(__dmul_rn(P.coef[0], src[s]), __dmul_rn(P.coef[1], acc));
-                else
-                    zr = __dadd_rn(P.zs[s], __dmul_rn(P.coef[q], acc));
-                P.zs[s] = zr;
-                if (SIGMA && q == P.p) P.z[r] = zr;
+                const double acc =
+                    q == 1 ? sell_row_dot_pipe<true>(P.cols, P.vals, off, L, s & 31, len, src, pol)
+                           : sell_row_dot_pipe<false>(P.cols, P.vals, off, L, s & 31, len, src, pol);
+                row_epilogue<KIND, SIGMA>(P, s, r, q, src, acc);
             }
         }
         __syncthreads();
         if (tid == 0) publish(P, T, q);
+    }
+}
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+// 8-byte asynchronous gather global -> shared (no register destination).
+__device__ __forceinline__ void gather8(void* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// Arrives on `bar` once all of this thread's earlier cp.async copies have landed.
+__device__ __forceinline__ void gather_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Asynchronous-gather variant ("kernel" knob 4).  The row loop of the other variants holds its
+// in-flight loads in registers, so memory parallelism per SM is capped by the register file and
+// a row needs ~len/2 dependent round trips: ~230K rows (~74 MB of C2's matrix) must be in flight
+// to cover HBM latency, which leaves no L2 room for reuse across powers.  Here each CTA runs a
+// ring of P.stages shared-memory slots, each holding one tile:
+//   cols[ne_max] u32 | vals[ne_max] f64 | xs[ne_max] f64   (the tile's SELL entries, in order)
+// P.n_prod producer warps fill slots: per ticket, (1) bulk-copy the tile's columns and values
+// (TMA, mbarrier complete_tx), (2) poll + acquire the tile's dependencies for power q-1,
+// (3) gather every x_{q-1}[col] of the tile into the slot with 8-byte cp.async copies (landing in
+// shared memory: no registers held) and (4) signal the slot.  P.n_cgroups consumer groups of
+// tile_rows threads (one thread per row) sum their rows' products in stored order straight from
+// shared memory (bitwise identical to the row loop) and publish the tile.
+// Tickets are assigned statically: iteration i of CTA b is ticket i*gridDim.x + b; producer warp
+// j owns iterations i = j mod n_prod, consumer group g owns i = g mod n_cgroups, and every role
+// walks its iterations in increasing order.  The lowest unfinished ticket's CTA has finished all
+// its earlier iterations, so its producer (slot free, dependencies all lower) and its consumer
+// group both make progress: deadlock-free.
+constexpr uint32_t kMaxSlots = 16;
+
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(512) k_mpk_async(const __grid_constant__ FusedParams P) {
+    extern __shared__ __align__(128) char smem[];
+    __shared__ __align__(8) uint64_t full_mat[kMaxSlots];
+    __shared__ __align__(8) uint64_t full_x[kMaxSlots];
+    __shared__ __align__(8) uint64_t empty[kMaxSlots];
+    __shared__ uint32_t s_code[kMaxSlots];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tr = P.tile_rows;
+    const uint32_t nc = P.n_cgroups * tr;  // consumer threads
+    const uint32_t S = P.stages;
+    const uint32_t ne_max = P.buf_bytes / 20u;
+    if (tid == 0) {
+        for (uint32_t i = 0; i < S; ++i) {
+            mbar_init_n(&full_mat[i], 1);
+            mbar_init_n(&full_x[i], 32);
+            mbar_init_n(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t b = blockIdx.x;
+    const uint32_t i_end = b < P.n_tickets ? (P.n_tickets - b + gridDim.x - 1) / gridDim.x : 0u;
+    if (tid >= nc) {
+        // ---------------- producer warps ----------------
+        // Iteration i: prepare (slot free -> ticket code -> TMA of columns + values), then, one
+        // iteration later in this warp's order, dependencies -> gathers.  The next iteration's
+        // TMA is issued right after the current gathers, so it overlaps their round trip.
+        const uint32_t lane = tid & 31u;
+        const uint32_t w = (tid - nc) >> 5;
+        struct Prep {
+            uint32_t code, T, q, ne;
+        };
+        auto prepare = [&](uint32_t i) -> Prep {
+            const uint32_t slot = i % S;
+            if (i >= S) mbar_wait(&empty[slot], ((i / S) - 1u) & 1u);
+            Prep pr{kNoTicket, 0, 0, 0};
+            if (i >= i_end) {
+                if (lane == 0) {
+                    s_code[slot] = kNoTicket;
+                    mbar_arrive(&full_mat[slot]);
+                }
+                gather_arrive(&full_x[slot]);
+                return pr;
+            }
+            pr.code = P.tickets[i * gridDim.x + b];
+            pr.T = pr.code & 0xffffffu;
+            pr.q = (pr.code >> 24) & 63u;
+            const uint64_t e0 = P.tile_off[pr.T];
+            pr.ne = (uint32_t)(P.tile_off[pr.T + 1] - e0);
+            if (lane == 0) {
+                char* st = smem + slot * P.buf_bytes;
+                s_code[slot] = pr.code;
+                const uint64_t pol = l2_policy(pr.code & kLastUse);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&full_mat[slot], pr.ne * 12u);
+                if (pr.ne) {
+                    bulk_g2s(st, P.cols + e0, pr.ne * 4u, &full_mat[slot], pol);
+                    bulk_g2s(st + ne_max * 4u, P.vals + e0, pr.ne * 8u, &full_mat[slot], pol);
+                }
+            }
+            return pr;
+        };
+        uint32_t i = w;
+        Prep cur = prepare(i);
+        while (i < i_end) {
+            const uint32_t slot = i % S;
+            if (cur.q > 1) {
+                const uint32_t r0 = P.dep_ptr[cur.T], r1 = P.dep_ptr[cur.T + 1];
+                while (!__all_sync(0xffffffffu, deps_ready<false>(P, r0, r1, cur.q - 1, lane, 32u))) __nanosleep(32);
+                (void)deps_ready<true>(P, r0, r1, cur.q - 1, lane, 32u);  // acquire each unit once
+                __syncwarp();
+            }
+            // release (cta) after the acquires: consumers waiting on full_mat may read data of the
+            // dependency tiles (own-row values, polynomial accumulator) from global memory
+            if (lane == 0) mbar_arrive(&full_mat[slot]);
+            mbar_wait(&full_mat[slot], (i / S) & 1u);  // columns landed
+            const char* st = smem + slot * P.buf_bytes;
+            const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+            double* xs = reinterpret_cast<double*>(const_cast<char*>(st) + ne_max * 12u);
+            const double* src = P.V + (uint64_t)(cur.q - 1) * P.vstride;
+            uint32_t e = lane;
+            for (; e + 7u * 32u < cur.ne; e += 8u * 32u) {  // ne is a multiple of 32
+                uint32_t c[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) c[j] = cs[e + j * 32u];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) gather8(xs + e + j * 32u, src + c[j]);
+            }
+            for (; e < cur.ne; e += 32u) gather8(xs + e, src + cs[e]);
+            gather_arrive(&full_x[slot]);
+            i += P.n_prod;
+            cur = prepare(i);
+        }
+        // terminal markers for every consumer group's first iteration past the end
+        for (i += P.n_prod; i < i_end + P.n_cgroups; i += P.n_prod) (void)prepare(i);
+        return;
+    }
+    // ---------------- consumer groups: one thread per tile row ----------------
+    const uint32_t g = tid / tr, row = tid - g * tr;
+    for (uint32_t i = g;; i += P.n_cgroups) {
+        const uint32_t slot = i % S;
+        const uint32_t ph = (i / S) & 1u;
+        mbar_wait(&full_mat[slot], ph);
+        const uint32_t code = s_code[slot];
+        if (code == kNoTicket) {
+            if (row == 0) mbar_arrive(&empty[slot]);
+            return;
+        }
+        const uint32_t T = code & 0xffffffu;
+        const uint32_t q = (code >> 24) & 63u;
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        const uint32_t s = T * tr + row;
+        const uint32_t r = SIGMA ? (s < P.n_slots ? P.slot_row[s] : 0xffffffffu) : s;
+        uint32_t len = 0, rb = 0, L = 0;
+        if (r < P.n_rows) {
+            len = P.row_len[s];
+            const uint64_t off = P.chunk_off[s >> 5];
+            L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
+            rb = (uint32_t)(off - P.tile_off[T]);
+        }
+        mbar_wait(&full_x[slot], ph);
+        if (r < P.n_rows) {
+            const char* st = smem + slot * P.buf_bytes;
+            const double* vs = reinterpret_cast<const double*>(st + ne_max * 4u) + rb;
+            const double* xs = vs + ne_max;
+            const uint32_t lane = s & 31u;
+            const uint32_t Lp = L & ~1u;
+            double acc = 0.0;
+            uint32_t k = 0;
+            for (; k + 1 < len && k < Lp; k += 2) {  // whole pairs
+                const double2 v = *reinterpret_cast<const double2*>(vs + (k >> 1) * 64u + lane * 2u);
+                const double2 x = *reinterpret_cast<const double2*>(xs + (k >> 1) * 64u + lane * 2u);
+                acc = __dadd_rn(acc, __dmul_rn(v.x, x.x));
+                acc = __dadd_rn(acc, __dmul_rn(v.y, x.y));
+            }
+            for (; k < len; ++k) {
+                const uint32_t e = sell_pos(k, Lp, lane);
+                acc = __dadd_rn(acc, __dmul_rn(vs[e], xs[e]));
+            }
+            row_epilogue<KIND, SIGMA>(P, s, r, q, src, acc);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1u + g), "r"(tr) : "memory");  // group done with the slot
+        if (row == 0) {
+            mbar_arrive(&empty[slot]);  // the slot can be refilled while the publish fence drains
+            publish(P, T, q);
+        }
     }
 }
 
@@ -666,13 +916,27 @@ void configure_warptile(uint32_t lmax) {
         MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 }
 
-template <int KIND, bool SIGMA>
-void launch_lean(int rowfn, int grid, int nt, cudaStream_t st, const FusedParams& P) {
-    if (rowfn)
-        k_mpk_lean<KIND, SIGMA, 1><<<grid, nt, 0, st>>>(P);
-    else
-        k_mpk_lean<KIND, SIGMA, 0><<<grid, nt, 0, st>>>(P);
+// Variable tiles (long rows) always come with wide dependency runs (superblock counters).
+template <bool SIGMA, bool VT, bool SB>
+std::array<const void*, 3> lean_kinds() {
+    return {(const void*)k_mpk_lean<0, SIGMA, VT, SB>, (const void*)k_mpk_lean<1, SIGMA, VT, SB>,
+            (const void*)k_mpk_lean<2, SIGMA, VT, SB>};
 }
+std::array<const void*, 3> lean_variants(bool sigma, bool vt, bool sb) {
+    if (sigma) return vt ? lean_kinds<true, true, true>() : sb ? lean_kinds<true, false, true>() : lean_kinds<true, false, false>();
+    return vt ? lean_kinds<false, true, true>() : sb ? lean_kinds<false, false, true>() : lean_kinds<false, false, false>();
+}
+
+template <int KIND, bool SIGMA>
+void launch_lean(bool sb, int grid, int nt, cudaStream_t st, const FusedParams& P) {
+    if (P.tile_start)
+        k_mpk_lean<KIND, SIGMA, true, true><<<grid, nt, 0, st>>>(P);
+    else if (sb)
+        k_mpk_lean<KIND, SIGMA, false, true><<<grid, nt, 0, st>>>(P);
+    else
+        k_mpk_lean<KIND, SIGMA, false, false><<<grid, nt, 0, st>>>(P);
+}
+
 
 template <int U>
 void launch_warptile(int kind, bool sigma, int grid, uint32_t smem, cudaStream_t st,
@@ -691,7 +955,9 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     if (P->exec && P->exec_csr == A && P->exec->order_knob == ctx->order &&
         P->exec->group == (ctx->group == 8 ? 8 : 16) && P->exec->stage_knob == ctx->stages &&
         P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads &&
-        P->exec->kernel_knob == ctx->kernel && P->exec->rowfn == (ctx->rowfn == 1 ? 1 : 0)) {
+        P->exec->kernel_knob == ctx->kernel &&
+        P->exec->prod_knob == ctx->producers &&
+        P->exec->cg_knob == ctx->cgroups) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k) {
@@ -718,9 +984,15 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     } else {
         const uint32_t mx = gpu_max_row_len(ctx, A);
         const double avg = A->n_rows ? (double)A->nnz / A->n_rows : 0.0;
-        E->order = (mx > 64 && mx > 16.0 * avg) ? 2 : 1;
+        if (mx > 64 && mx > 16.0 * avg)
+            E->order = 2;
+        else  // A_perm order already local (e.g. lexicographic grids): keep it, no private copies
+            E->order = gpu_mean_first_col_jump(ctx, A) > 256.0 ? 1 : 0;
     }
-    E->tile_rows = ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
+    E->prod_knob = ctx->producers;
+    E->cg_knob = ctx->cgroups;
+    E->tile_rows = ctx->tile_rows == 32 ? 32u : ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
+    if (E->tile_rows == 32 && ctx->kernel != 4) E->tile_rows = 64;  // 32-row tiles: async kernel only
     if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
     // consumer threads: one per tile row unless forced
     E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
@@ -798,6 +1070,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         for (uint32_t T = 0; T <= nt; ++T) toff[T] = off[std::min<uint64_t>((tile_first(T) + 31) / 32, E->S->n_chunks)];
         for (uint32_t T = 0; T < nt; ++T) {
             const uint64_t ne = toff[T + 1] >= toff[T] ? toff[T + 1] - toff[T] : 0;
+            E->ne_max = std::max(E->ne_max, ne);
             const uint64_t bytes = (4 * ne + 127) & ~127ull;  // staged: column indices
             E->tile_bytes[T] = 12 * ne + (uint64_t)(tile_first(T + 1) - tile_first(T)) * 8 * 3;
             if (bytes > kMaxBufBytes)
@@ -813,49 +1086,6 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->tile_off.alloc(nt + 1);
         MPKG_CUDA(cudaMemcpyAsync(E->tile_off.p, toff.data(), 8ull * (nt + 1), cudaMemcpyHostToDevice, st));
     }
-    // Stages: enough staged bytes per SM to cover DRAM latency (~200 KB of the 228 KB), at
-    // least 2 (prefetch), at most kMaxStages; "stages" knob overrides.
-    if (ctx->stages > 0)
-        E->stages = (uint32_t)std::min<int64_t>(ctx->stages, kMaxStages);
-    else
-        E->stages = std::max<uint32_t>(2, std::min<uint32_t>(kMaxStages, (200u << 10) / E->buf_bytes));
-    while (E->stages > 1 && E->stages * E->buf_bytes > (220u << 10)) --E->stages;
-    const uint32_t smem = E->stages * E->buf_bytes;
-    E->group = ctx->group == 8 ? 8 : 16;
-    E->stage_knob = ctx->stages;
-    E->tile_knob = ctx->tile_rows;
-    E->thread_knob = ctx->threads;
-    int occ = 0;
-    E->kernel = E->kernel_forced_lean ? 0 : (int)ctx->kernel;  // long rows: lean kernel only
-    if (E->kernel == 2) {
-        E->threads = 128;
-        E->stages = 1;
-        configure_warptile(E->wt_lmax);
-        if (E->group == 16)
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 8>, 128, 128 * E->wt_lmax * 8));
-        else
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 4>, 128, 128 * E->wt_lmax * 8));
-    } else if (E->kernel == 0) {
-        E->threads = E->tile_rows;
-        E->stages = 1;
-        E->rowfn = ctx->rowfn == 1 ? 1 : 0;
-        const int nt = (int)std::min<uint32_t>(E->tile_rows, 128u);
-        if (E->rowfn)
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true, 1>, nt, 0));
-        else
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_lean<0, true, 0>, nt, 0));
-    } else if (E->group == 8) {
-        configure_kernels<8>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads + 32, smem));
-    } else {
-        configure_kernels<16>(smem);
-        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, (int)E->threads + 32, smem));
-    }
-    occ = std::max(1, occ);
-    E->occ_max = occ;
-    if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
-    E->grid = occ * ctx->sm_count;
-    E->slack = ctx->slack >= 0 ? ctx->slack : (int64_t)E->grid * E->stages;
     // dependency runs
     std::vector<uint32_t> lp = P->level_ptr;
     if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
@@ -908,6 +1138,80 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->h_hi.push_back(hi);
         E->h_ptr[T + 1] = (uint32_t)E->h_lo.size();
     }
+    {  // superblock polling pays when tiles wait on many tiles on average (R-MAT hubs: ~10^4);
+       // a 3D stencil has ~30 and a few wide runs, which the tile-flag loop handles fine
+        uint64_t dep_tiles = 0;
+        for (size_t k = 0; k < E->h_lo.size(); ++k) dep_tiles += E->h_hi[k] - E->h_lo[k] + 1;
+        E->sb = nt && dep_tiles > (uint64_t)nt * 4 * kSB;
+    }
+    // Stages: enough staged bytes per SM to cover DRAM latency (~200 KB of the 228 KB), at
+    // least 2 (prefetch), at most kMaxStages; "stages" knob overrides.
+    if (ctx->stages > 0)
+        E->stages = (uint32_t)std::min<int64_t>(ctx->stages, kMaxStages);
+    else
+        E->stages = std::max<uint32_t>(2, std::min<uint32_t>(kMaxStages, (200u << 10) / E->buf_bytes));
+    while (E->stages > 1 && E->stages * E->buf_bytes > (220u << 10)) --E->stages;
+    const uint32_t smem = E->stages * E->buf_bytes;
+    E->group = ctx->group == 8 ? 8 : 16;
+    E->stage_knob = ctx->stages;
+    E->tile_knob = ctx->tile_rows;
+    E->thread_knob = ctx->threads;
+    int occ = 0;
+    // variable tiles (long rows): the lean kernel
+    E->kernel = E->kernel_forced_lean ? 0 : (int)ctx->kernel;
+    const uint64_t async_stage = ((E->ne_max + 31) & ~31ull) * 20;  // cols + vals + gathered x
+    if (E->kernel == 4 && (async_stage > (110u << 10) || E->tile_rows > 256)) E->kernel = 0;
+    if (E->kernel == 4) {
+        E->buf_bytes = (uint32_t)std::max<uint64_t>(async_stage, 640);
+        E->n_prod = ctx->producers > 0 ? (uint32_t)ctx->producers : 4u;
+        E->n_cgroups = ctx->cgroups > 0 ? (uint32_t)ctx->cgroups : std::max<uint32_t>(1u, 128u / E->tile_rows);
+        while (E->n_cgroups * E->tile_rows + 32 * E->n_prod > 512) E->n_cgroups > 1 ? --E->n_cgroups : --E->n_prod;
+        const uint32_t unit = std::max(E->n_prod, E->n_cgroups);
+        uint32_t S = ctx->stages > 0 ? (uint32_t)ctx->stages : (210u << 10) / E->buf_bytes;
+        S = std::min<uint32_t>(S, kMaxSlots) / unit * unit;
+        while (S > unit && S * E->buf_bytes > (225u << 10)) S -= unit;
+        E->stages = std::max(S, unit);
+        E->threads = E->n_cgroups * E->tile_rows + 32 * E->n_prod;
+        const int sm = (int)(E->stages * E->buf_bytes);
+        if (sm > (225 << 10)) fail(MPKG_EINVAL, "mpk: async kernel stages do not fit shared memory");
+        const void* ks[] = {(const void*)k_mpk_async<0, false>, (const void*)k_mpk_async<0, true>,
+                            (const void*)k_mpk_async<1, false>, (const void*)k_mpk_async<1, true>,
+                            (const void*)k_mpk_async<2, false>, (const void*)k_mpk_async<2, true>};
+        for (const void* k : ks)
+            MPKG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_async<0, true>, (int)E->threads, sm));
+    } else if (E->kernel == 2) {
+        E->threads = 128;
+        E->stages = 1;
+        configure_warptile(E->wt_lmax);
+        if (E->group == 16)
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 8>, 128, 128 * E->wt_lmax * 8));
+        else
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_warptile<0, true, 4>, 128, 128 * E->wt_lmax * 8));
+    } else if (E->kernel == 0) {
+        E->threads = E->tile_rows;
+        E->stages = 1;
+        // resident CTAs of the variant this executor launches (all three kinds)
+        const int nt = (int)std::min<uint32_t>(E->tile_rows, 128u);
+        const bool vt = !E->h_tile_start.empty();
+        occ = 1 << 30;
+        for (const void* k : lean_variants(E->order >= 1, vt, vt || E->sb)) {
+            int o = 0;
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, nt, 0));
+            occ = std::min(occ, o);
+        }
+    } else if (E->group == 8) {
+        configure_kernels<8>(smem);
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 8>, (int)E->threads + 32, smem));
+    } else {
+        configure_kernels<16>(smem);
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpk_fused<0, true, 16>, (int)E->threads + 32, smem));
+    }
+    occ = std::max(1, occ);
+    E->occ_max = occ;
+    if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
+    E->grid = occ * ctx->sm_count;
+    E->slack = ctx->slack >= 0 ? ctx->slack : (int64_t)E->grid * E->stages;
     E->dep_ptr.alloc(nt + 1);
     E->dep_lo.alloc(std::max<size_t>(E->h_lo.size(), 1));
     E->dep_hi.alloc(std::max<size_t>(E->h_hi.size(), 1));
@@ -1029,6 +1333,18 @@ void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
 
 }  // namespace
 
+// Schedule choice ("schedule" knob: 0 auto, 1 fused, 2 sweeps).  Measured on B200 (DESIGN.md
+// §5): the fused tile-DAG kernel never reuses L2 across powers at C2..C5 sizes (the in-flight
+// window needed to saturate HBM plus the level lag exceeds the 126 MB L2) and even at C1 its
+// level-by-level critical path costs more than p launches, so auto runs one launch per power
+// over the executor's SELL -- except for matrices with long rows, whose CTA-cooperative path
+// exists only in the fused kernel.
+bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
+    if (ctx->schedule == 1) return false;
+    if (E.long_rows) return false;  // long rows live outside the SELL arrays: fused path only
+    return true;
+}
+
 void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs& a) {
     if (a.p > kMaxFusedP) fail(MPKG_EINVAL, "mpk: at most 32 powers per fused launch");
     Executor& E = get_executor(ctx, Pl, A);
@@ -1065,6 +1381,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.csr_v = A->values.p;
     P.long_prod = E.long_rows ? E.long_prod.p : nullptr;
     P.n_tiles = E.n_tiles;
+    P.n_prod = E.n_prod;
+    P.n_cgroups = E.n_cgroups;
     P.n_sb = (E.n_tiles + kSB - 1) / kSB;
     E.sb_count.ensure((uint64_t)(kMaxFusedP + 1) * P.n_sb + 1);
     P.sb_count = E.sb_count.p;
@@ -1097,8 +1415,35 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
     MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     const uint32_t smem = E.stages * E.buf_bytes;
+    const bool sweep = use_sweeps(ctx, E, a.p);
+    E.last_sweep = sweep;
     const auto ev = timing_begin(ctx);
-    if (E.kernel == 2) {
+    if (sweep) {
+        const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
+        for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
+            switch (a.kind * 2 + (sigma ? 1 : 0)) {
+                case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
+                case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
+                case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
+                case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
+                case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
+                default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
+            }
+            MPKG_LAUNCH_CHECK();
+        }
+        ctx->launches += (uint64_t)a.p - 1;
+    } else if (E.kernel == 4) {
+        const int nt = (int)E.threads;
+        const uint32_t sm = E.stages * E.buf_bytes;
+        switch (a.kind * 2 + (sigma ? 1 : 0)) {
+            case 0: k_mpk_async<0, false><<<E.grid, nt, sm, st>>>(P); break;
+            case 1: k_mpk_async<0, true><<<E.grid, nt, sm, st>>>(P); break;
+            case 2: k_mpk_async<1, false><<<E.grid, nt, sm, st>>>(P); break;
+            case 3: k_mpk_async<1, true><<<E.grid, nt, sm, st>>>(P); break;
+            case 4: k_mpk_async<2, false><<<E.grid, nt, sm, st>>>(P); break;
+            default: k_mpk_async<2, true><<<E.grid, nt, sm, st>>>(P); break;
+        }
+    } else if (E.kernel == 2) {
         const uint32_t wsmem = 128 * E.wt_lmax * 8;
         if (E.group == 16)
             launch_warptile<8>(a.kind, sigma, E.grid, wsmem, st, P);
@@ -1107,12 +1452,12 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (E.kernel == 0) {
         const int nt = (int)std::min<uint32_t>(E.tile_rows, 128u);
         switch (a.kind * 2 + (sigma ? 1 : 0)) {
-            case 0: launch_lean<0, false>(E.rowfn, E.grid, nt, st, P); break;
-            case 1: launch_lean<0, true>(E.rowfn, E.grid, nt, st, P); break;
-            case 2: launch_lean<1, false>(E.rowfn, E.grid, nt, st, P); break;
-            case 3: launch_lean<1, true>(E.rowfn, E.grid, nt, st, P); break;
-            case 4: launch_lean<2, false>(E.rowfn, E.grid, nt, st, P); break;
-            default: launch_lean<2, true>(E.rowfn, E.grid, nt, st, P); break;
+            case 0: launch_lean<0, false>(E.sb, E.grid, nt, st, P); break;
+            case 1: launch_lean<0, true>(E.sb, E.grid, nt, st, P); break;
+            case 2: launch_lean<1, false>(E.sb, E.grid, nt, st, P); break;
+            case 3: launch_lean<1, true>(E.sb, E.grid, nt, st, P); break;
+            case 4: launch_lean<2, false>(E.sb, E.grid, nt, st, P); break;
+            default: launch_lean<2, true>(E.sb, E.grid, nt, st, P); break;
         }
     } else {
         switch (a.kind) {
@@ -1140,6 +1485,14 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
     if (n_tickets) *n_tickets = k;
     if (n_deps) *n_deps = d;
     if (pass_powers) *pass_powers = pp;
+}
+
+void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows) {
+    const Executor* E = P->exec.get();
+    if (order) *order = E ? E->order : -1;
+    if (sweeps) *sweeps = E ? (int)E->last_sweep : 0;
+    if (kernel) *kernel = E ? E->kernel : -1;
+    if (long_rows) *long_rows = E ? E->long_rows : 0;
 }
 
 }  // namespace mpkg_detail

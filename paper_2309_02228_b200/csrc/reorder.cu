@@ -77,7 +77,38 @@ __global__ void k_max_len(const uint32_t* __restrict__ rp, uint32_t n, uint32_t*
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// Sum over consecutive rows of |first column(r+1) - first column(r)| (first column = the row's
+// smallest neighbour, normally in the previous level): small when consecutive rows of A_perm
+// gather from nearby x, ~level width / 3 when the order inside levels is random.
+__global__ void k_first_col_jump(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                                 uint32_t n, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r + 1 < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        if (rp[r] == rp[r + 1] || rp[r + 1] == rp[r + 2]) continue;
+        const uint32_t a = ci[rp[r]], b = ci[rp[r + 1]];
+        acc += a > b ? a - b : b - a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 }  // namespace
+
+double gpu_mean_first_col_jump(mpkg_ctx_s* ctx, const mpkg_csr_s* A) {
+    if (A->n_rows < 2) return 0.0;
+    DevBuf<unsigned long long> d(1);
+    MPKG_CUDA(cudaMemsetAsync(d.p, 0, 8, ctx->stream));
+    k_first_col_jump<<<grid_for(A->n_rows, 256, (unsigned)ctx->sm_count * 4u), 256, 0, ctx->stream>>>(
+        A->row_ptr.p, A->col_idx.p, A->n_rows, d.p);
+    MPKG_LAUNCH_CHECK();
+    ctx->launches += 1;
+    unsigned long long h = 0;
+    MPKG_CUDA(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return (double)h / (double)(A->n_rows - 1);
+}
 
 uint32_t gpu_max_row_len(mpkg_ctx_s* ctx, const mpkg_csr_s* A) {
     if (A->n_rows == 0) return 0;

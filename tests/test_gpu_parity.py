@@ -169,14 +169,37 @@ def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
         assert_bitwise(ctx.baseline_mpk(Ap, x, 8).as_matrix(), ref8, f"{name} baseline")
 
 
-@pytest.mark.parametrize("order", [0, 1])
-@pytest.mark.parametrize("slack", [0, 1, 7, -1])
-def test_fused_orders_and_schedules(ctx, cases, oracle, order, slack):
-    """Every executor order (identity / Cuthill-McKee inside levels) and ticket schedule gives
-    the same bits: the schedule changes only which tiles run concurrently."""
+DEFAULT_KNOBS = {"order": -1, "slack": -1, "schedule": 0, "kernel": 0, "tile_rows": 128,
+                 "producers": 0, "cgroups": 0, "stages": 0}
+
+SCHEDULES = {
+    "sweeps": {"schedule": 2},
+    "fused-lean": {"schedule": 1},
+    "fused-lean-slack0": {"schedule": 1, "slack": 0},
+    "fused-lean-slack1": {"schedule": 1, "slack": 1},
+    "fused-lean-slack7": {"schedule": 1, "slack": 7},
+    "fused-lean-tile64": {"schedule": 1, "tile_rows": 64},
+    "fused-staged": {"schedule": 1, "kernel": 1},
+    "fused-warptile": {"schedule": 1, "kernel": 2},
+    "fused-async": {"schedule": 1, "kernel": 4},
+    "fused-async-tile32": {"schedule": 1, "kernel": 4, "tile_rows": 32, "producers": 2, "cgroups": 4},
+    "fused-async-tile64": {"schedule": 1, "kernel": 4, "tile_rows": 64, "producers": 8},
+}
+
+
+def set_knobs(ctx, knobs):
+    for k, v in {**DEFAULT_KNOBS, **knobs}.items():
+        ctx.set_param(k, v)
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+@pytest.mark.parametrize("sched", list(SCHEDULES))
+def test_orders_and_schedules(ctx, cases, oracle, order, sched):
+    """Every private row order (A_perm / Cuthill-McKee / longest-first inside levels), schedule
+    (one launch per power, or the fused tile-DAG kernel with any ticket slack) and fused-kernel
+    variant gives the same bits: they change only which rows run where and when."""
     try:
-        ctx.set_param("order", order)
-        ctx.set_param("slack", slack)
+        set_knobs(ctx, {"order": order, **SCHEDULES[sched]})
         for name in ("stencil27_scrambled_20", "random_csr_2000", "rmat_12", "poisson2d_256"):
             c = cases[name]
             P = c["P"]
@@ -185,7 +208,10 @@ def test_fused_orders_and_schedules(ctx, cases, oracle, order, slack):
             x = mpkg.random_vector(P.n_rows, 9)
             plan = ctx.group_levels(ls, Ap, 1 << 20, 6)
             ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 6)
-            assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} order={order}")
+            assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} {sched} order={order}")
+            info = plan.exec_info()
+            assert info["order"] == order
+            assert info["schedule"] == ("sweeps" if sched == "sweeps" else "fused")
             sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0, 3.0, 0.25]
             ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
             assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, f"{name} shifted")
@@ -193,8 +219,7 @@ def test_fused_orders_and_schedules(ctx, cases, oracle, order, slack):
             zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
             assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, f"{name} poly")
     finally:
-        ctx.set_param("order", 1)
-        ctx.set_param("slack", -1)
+        set_knobs(ctx, {})
 
 
 def _arrow_matrix(n=6000, hubs=(0, 17, 2500), seed=5):
@@ -221,9 +246,10 @@ def _arrow_matrix(n=6000, hubs=(0, 17, 2500), seed=5):
 
 @pytest.mark.parametrize("order", [-1, 0, 1, 2])
 def test_long_rows_and_length_order(ctx, oracle, order):
-    """Hub rows (>1024 entries) take the CTA-cooperative path; every order gives the same bits."""
+    """Hub rows (>1024 entries) take the CTA-cooperative path of the fused kernel (auto schedule
+    keeps the fused kernel for them); every order gives the same bits."""
     try:
-        ctx.set_param("order", order)
+        set_knobs(ctx, {"order": order})
         for A in (_arrow_matrix(), mpkg.rmat(15, 16, 7)):
             lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
             P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
@@ -234,6 +260,9 @@ def test_long_rows_and_length_order(ctx, oracle, order):
             plan = ctx.group_levels(ls, Ap, 8 << 20, 4)
             ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4)
             assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref, f"order={order}")
+            info = plan.exec_info()
+            if order != 0:  # the private-order SELL leaves hub rows out: fused long-row path
+                assert info["schedule"] == "fused" and info["long_rows"] > 0
             sh = [1.0, 2.0 + 0.5j, 2.0 - 0.5j, 0.5]
             ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
             assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, "shifted")
@@ -241,7 +270,7 @@ def test_long_rows_and_length_order(ctx, oracle, order):
             zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
             assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, "poly")
     finally:
-        ctx.set_param("order", -1)
+        set_knobs(ctx, {})
 
 
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
