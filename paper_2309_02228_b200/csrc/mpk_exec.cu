@@ -1166,6 +1166,9 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         E->n_prod = ctx->producers > 0 ? (uint32_t)ctx->producers : 4u;
         E->n_cgroups = ctx->cgroups > 0 ? (uint32_t)ctx->cgroups : std::max<uint32_t>(1u, 128u / E->tile_rows);
         while (E->n_cgroups * E->tile_rows + 32 * E->n_prod > 512) E->n_cgroups > 1 ? --E->n_cgroups : --E->n_prod;
+        const uint32_t fit = std::max<uint32_t>(1u, (225u << 10) / E->buf_bytes);  // slots that fit
+        E->n_prod = std::min(E->n_prod, fit);
+        E->n_cgroups = std::min(E->n_cgroups, fit);
         const uint32_t unit = std::max(E->n_prod, E->n_cgroups);
         uint32_t S = ctx->stages > 0 ? (uint32_t)ctx->stages : (210u << 10) / E->buf_bytes;
         S = std::min<uint32_t>(S, kMaxSlots) / unit * unit;
