@@ -284,11 +284,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slack", type=int, default=-1)
-    ap.add_argument("--order", type=int, default=1, help="0: A_perm order, 1: CM inside levels")
+    ap.add_argument("--order", type=int, default=-1,
+                    help="-1 auto, 0 A_perm order, 1 CM inside levels, 2 longest rows first")
+    ap.add_argument("--schedule", type=int, default=0,
+                    help="0 auto, 1 fused tile-DAG kernel, 2 one launch per power")
+    ap.add_argument("--kernel", type=int, default=0, help="fused variant: 0 lean, 1 staged, 2 warp-tile, 4 async")
     ap.add_argument("--pass-powers", type=int, default=0, help="force powers per fused pass")
     ap.add_argument("--l2-budget", type=int, default=0, help="live-window bytes (0: 0.6 L2)")
     ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on fused CTAs per SM")
-    ap.add_argument("--group", type=int, default=16, help="row entries issued together (8|16)")
+    ap.add_argument("--group", type=int, default=8, help="staged variant: gathers in flight (8|16)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
@@ -311,6 +315,8 @@ def main():
     if args.slack >= 0:
         ctx.set_param("slack", args.slack)
     ctx.set_param("order", args.order)
+    ctx.set_param("schedule", args.schedule)
+    ctx.set_param("kernel", args.kernel)
     ctx.set_param("pass", args.pass_powers)
     ctx.set_param("l2_budget", args.l2_budget)
     ctx.set_param("ctas_per_sm", args.ctas_per_sm)
@@ -364,6 +370,9 @@ def main():
     sync()
     prep["executor_build_s"] = time.perf_counter() - t0
     exec_info = plan.exec_info()
+    kname = ("k_mpk_sweep" if exec_info["schedule"] == "sweeps" else
+             {0: "k_mpk_lean", 1: "k_mpk_fused", 2: "k_mpk_warptile", 4: "k_mpk_async"}.get(exec_info["kernel"], "?"))
+    exec_info["dominant_kernel"] = kname
 
     # ---- parity at full size: fused == one-launch-per-power baseline, bit for bit -------------
     ref_blk = torch.empty_like(d_blk)
@@ -411,11 +420,13 @@ def main():
     sync()
     launches0 = ctx.launch_count()
     with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("mpk_timed")  # ncu --nvtx --nvtx-include "mpk_timed/"
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         sync()
+        torch.cuda.nvtx.range_pop()
     if dist:
         dist.barrier()
     launches = ctx.launch_count() - launches0
@@ -481,11 +492,17 @@ def main():
         b_alg += 8 * n
     peak, peak_src = measured_peak()
     achieved = b_alg / (kernel_ms * 1e-3) / 1e9
+    # one power = one pass over the matrix: its own algorithmic bytes (matrix + x read + y written)
+    sweep_bytes = 12 * nnz + 4 * (n + 1) + 16 * n
+    sweep = {"algorithmic_bytes": sweep_bytes, "ms": kernel_ms / p,
+             "achieved": sweep_bytes / (kernel_ms / p * 1e-3) / 1e9}
+    sweep["frac"] = sweep["achieved"] / peak
     traffic = None
     prof = ROOT / "profiles" / f"ncu_{args.config}.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            traffic = pj.get("dram_bytes_per_step", pj.get("dram_bytes_per_launch"))
         except Exception:
             traffic = None
 
@@ -506,7 +523,7 @@ def main():
                        "l2": f"inputs larger than L2 ({(12 * nnz) / 1e9:.2f} GB matrix vs "
                              f"{info['l2_bytes'] >> 20} MiB L2)" if 12 * nnz > info["l2_bytes"]
                        else "matrix fits L2; no flush between steps (latency-bound config)",
-                       "mode": "bitwise", "order": args.order, "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
+                       "mode": "bitwise", "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
                        "plan_cache_bytes": cache, "executor": exec_info,
                        "preprocess_s": prep, "parity": "fused == baseline bitwise" if parity
                        else "MISMATCH", "baseline_back_to_back_ms": baseline_ms,
@@ -514,7 +531,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms,
-                         "kernel_launches_timed": k_count, "peak_source": peak_src},
+                         "kernel_launches_timed": k_count, "peak_source": peak_src,
+                         "per_power": sweep,
+                         "note": "achieved = single-pass B_alg (SURVEY 8d) / MPK kernel time; "
+                                 "per_power = one pass over the matrix per power"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

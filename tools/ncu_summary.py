@@ -66,6 +66,12 @@ def main():
     main_k = next((k for k in res["kernels"] if a.kernel in k["name"]), res["kernels"][0])
     rd, wr = main_k.get("dram__bytes_read.sum", 0.0), main_k.get("dram__bytes_write.sum", 0.0)
     res["dram_bytes_per_launch"] = rd + wr
+    # one MPK step = every captured launch of the kernel (one launch per power in sweep mode)
+    steps = [k for k in res["kernels"] if a.kernel in k["name"]]
+    res["launches_per_step"] = len(steps)
+    res["dram_bytes_per_step"] = sum(k.get("dram__bytes_read.sum", 0.0) + k.get("dram__bytes_write.sum", 0.0)
+                                     for k in steps)
+    res["kernel_s_per_step"] = sum(k.get("gpu__time_duration.sum", 0.0) for k in steps)
     res["dram_read_bytes_per_launch"] = rd
     res["dram_write_bytes_per_launch"] = wr
     if a.launches:

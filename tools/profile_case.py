@@ -16,7 +16,7 @@ import bench  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--order", type=int, default=1)
+    ap.add_argument("--order", type=int, default=-1)
     ap.add_argument("--slack", type=int, default=-1)
     ap.add_argument("--launches", type=int, default=2)
     ap.add_argument("--group", type=int, default=8)
