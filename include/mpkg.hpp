@@ -22,8 +22,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -40,6 +42,7 @@ inline void check(int rc) {
     const std::string msg = mpkg_last_error();
     if (rc == MPKG_EINVAL) throw std::invalid_argument(msg);
     if (rc == MPKG_ERANGE) throw std::out_of_range(msg);
+    if (rc == MPKG_ENOMEM) throw std::bad_alloc();
     throw std::runtime_error(msg);
 }
 
@@ -240,6 +243,43 @@ inline void spmv(const CsrMatrix& A, const std::vector<double>& x, std::vector<d
     if (x.size() != A.n_cols || y.size() != A.n_rows)
         throw std::invalid_argument("spmv: vector size mismatch");
     detail::check(mpkg_spmv(device_context(), A.device(), x.data(), y.data()));
+}
+
+/// csr.hpp:207-227 transpose (host; the level engine forms the union pattern on the GPU without
+/// it).  Counting pass per column, then rows of A are walked in order, so every row of the
+/// result lists its columns (= rows of A) ascending.
+inline CsrMatrix transpose(const CsrMatrix& A) {
+    CsrMatrix T;
+    T.n_rows = A.n_cols;
+    T.n_cols = A.n_rows;
+    T.row_ptr.assign(static_cast<std::size_t>(A.n_cols) + 1, 0);
+    const index_t nz = A.nnz();
+    for (index_t k = 0; k < nz; ++k) ++T.row_ptr[static_cast<std::size_t>(A.col_idx[k]) + 1];
+    for (std::size_t i = 1; i < T.row_ptr.size(); ++i) T.row_ptr[i] += T.row_ptr[i - 1];
+    T.col_idx.resize(nz);
+    T.values.resize(nz);
+    std::vector<index_t> next(T.row_ptr.begin(), T.row_ptr.end() - 1);
+    for (index_t r = 0; r < A.n_rows; ++r)
+        for (index_t k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k) {
+            const index_t dst = next[A.col_idx[k]]++;
+            T.col_idx[dst] = r;
+            T.values[dst] = A.values[k];
+        }
+    return T;
+}
+
+/// threading.hpp:34-46 resolve_threads: explicit request > MPK_NUM_THREADS > hardware
+/// concurrency, >= 1.  Kept for reference call sites that report the team size; the GPU path
+/// has no thread team and ignores every `threads` argument.
+inline int resolve_threads(int requested = 0) {
+    if (requested > 0) return requested;
+    if (const char* env = std::getenv("MPK_NUM_THREADS")) {
+        char* end = nullptr;
+        const long v = std::strtol(env, &end, 10);
+        if (end != env && v > 0 && v < (1L << 30)) return static_cast<int>(v);
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw ? static_cast<int>(hw) : 1;
 }
 
 inline CsrMatrix download(mpkg_csr_t h) {

@@ -289,7 +289,31 @@ static void test_mpk() {
     }
 }
 
+// csr.hpp:207-227 transpose and threading.hpp:34-46 resolve_threads (host helpers).
+static void test_host_helpers() {
+    const CsrMatrix A = mpk::random_csr(300, 5, 11);  // nonsymmetric pattern
+    const CsrMatrix T = mpk::transpose(A);
+    EXPECT(T.n_rows == A.n_cols && T.n_cols == A.n_rows && T.nnz() == A.nnz());
+    bool sorted = true, match = true;
+    for (index_t r = 0; r < T.n_rows; ++r)
+        for (index_t k = T.row_ptr[r]; k < T.row_ptr[r + 1]; ++k) {
+            if (k + 1 < T.row_ptr[r + 1] && T.col_idx[k] >= T.col_idx[k + 1]) sorted = false;
+            const index_t c = T.col_idx[k];  // A(c, r) must hold the same value
+            bool found = false;
+            for (index_t j = A.row_ptr[c]; j < A.row_ptr[c + 1]; ++j)
+                if (A.col_idx[j] == r) found = std::memcmp(&A.values[j], &T.values[k], 8) == 0;
+            match = match && found;
+        }
+    EXPECT(sorted);
+    EXPECT(match);
+    const CsrMatrix TT = mpk::transpose(T);
+    EXPECT(TT.row_ptr == A.row_ptr && TT.col_idx == A.col_idx);
+    EXPECT(mpk::resolve_threads(7) == 7);
+    EXPECT(mpk::resolve_threads() >= 1);
+}
+
 int main() {
+    test_host_helpers();
     test_levels();
     test_wavefront();
     test_mpk();
