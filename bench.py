@@ -158,7 +158,9 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=None)
+        # NCCL between GPUs; MPKG_DIST_BACKEND=gloo only for the single-GPU smoke test of the
+        # sharded path (tests/test_gpu_sharded.py), where ranks share one device
+        dist.init_process_group(os.environ.get("MPKG_DIST_BACKEND", "nccl"))
         pg = dist
     return rank, world, local, pg
 
@@ -273,6 +275,129 @@ def cpu_baseline_reference(A_perm_host, perm_unused, ls_level_ptr, p, x, kind, n
             "sample": "one SpMV sweep of the oracle port (single thread)"}
 
 
+def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist, info, prep,
+                stream, sync):
+    """N > 1: the matrix is row-partitioned along contiguous BFS-level ranges (balanced by nnz)
+    with p ghost levels per side (multi.py).  A step = one halo exchange of x
+    (NCCL point-to-point over NVLink) + the local MPK; every rank owns a fixed share of ONE
+    matrix (strong scaling).  value = the global MPK flops / the slowest rank's step time."""
+    import torch
+
+    from paper_2309_02228_b200 import multi
+    if cfgd["kind"] != "plain":
+        raise SystemExit("multi-GPU bench runs the plain MPK configs (c1, c2, c3, c5)")
+    n, nnz = A.n_rows, A.nnz
+    dev = torch.device("cuda", local)
+    lens = np.diff(A.row_ptr.astype(np.int64))[ls.inv_perm.astype(np.int64)]
+    prefix = np.concatenate([[0], np.cumsum(lens)])
+    t0 = time.perf_counter()
+    shard = multi.ShardedMPK(ctx, Ap, ls.level_ptr, prefix, p, rank, world)
+    sync()
+    prep["shard_setup_s"] = time.perf_counter() - t0
+    hp = shard.halo_plan
+    o0, o1 = hp.own_rows
+    x_own = torch.from_numpy(np.ascontiguousarray(x_perm[o0:o1])).to(dev)
+    blk = torch.empty((p + 1) * max(shard.n_local, 1), dtype=torch.float64, device=dev)
+
+    def step():
+        return shard.step(x_own, blk, dist)
+
+    step()
+    sync()
+    # parity: own rows == the single-GPU one-launch-per-power result, bit for bit
+    ref = torch.empty((p + 1) * n, dtype=torch.float64, device=dev)
+    ctx.baseline_mpk_dev(Ap, torch.from_numpy(x_perm).to(dev).data_ptr(), p, ref.data_ptr(), n, p + 1)
+    sync()
+    a0, a1 = shard.own
+    mine = blk.view(p + 1, -1)[:, a0:a1] if shard.n_local else blk[:0].view(p + 1, 0)
+    parity = bool(torch.equal(mine.contiguous().view(torch.int64),
+                              ref.view(p + 1, n)[:, o0:o1].contiguous().view(torch.int64)))
+    del ref
+    torch.cuda.empty_cache()
+    ctx.set_param("kernel_timing", 1)
+    for _ in range(args.warmup):
+        step()
+    sync()
+    ctx.kernel_times()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    sync()
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("mpk_timed")
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        sync()
+        torch.cuda.nvtx.range_pop()
+    dist.barrier()
+    launches = ctx.launch_count() - launches0
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    k_total, k_count, _ = ctx.kernel_times()
+    kernel_ms = k_total / max(k_count, 1)
+    ctx.set_param("kernel_timing", 0)
+    # e2e: own x from pinned host memory, exchange + local MPK, own rows back to the host
+    hx = torch.from_numpy(np.ascontiguousarray(x_perm[o0:o1])).pin_memory()
+    hout = torch.empty((p + 1, o1 - o0), dtype=torch.float64).pin_memory()
+    ts = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            x_own.copy_(hx, non_blocking=True)
+            step()
+            hout.copy_(blk.view(p + 1, -1)[:, a0:a1], non_blocking=True)
+            b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    e_ms = statistics.median(ts)
+    t = torch.tensor([step_ms, kernel_ms, e_ms, float(not parity)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, kernel_ms, e_ms, bad = t.tolist()
+    parity = bad == 0.0
+    flops = 2.0 * nnz * p
+    value = flops / (step_ms * 1e-3) * 1e-9
+    clocks = clk.summary()
+    nnz_loc = shard.A.nnz
+    b_loc = 12 * nnz_loc + 4 * (shard.n_local + 1) + 8 * shard.n_local * (1 + p)
+    peak, peak_src = measured_peak()
+    achieved = b_loc / (kernel_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
+            "config": {"workload": cfgd["desc"], "n": n, "nnz": nnz, "p": p,
+                       "parallelism": f"level-range shards x{world}, p-deep ghost levels, "
+                                      "one NCCL halo exchange of x per step",
+                       "l2": "inputs larger than L2" if 12 * nnz > info["l2_bytes"] else "fits L2",
+                       "mode": "bitwise", "rank0_shard": {"own_rows": [o0, o1],
+                                                         "local_rows": list(hp.local_rows),
+                                                         "local_nnz": nnz_loc},
+                       "executor": shard.plan.exec_info(), "preprocess_s": prep,
+                       "parity": "own rows == single-GPU baseline bitwise (all ranks)" if parity
+                       else "MISMATCH"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes": b_loc, "kernel_ms": kernel_ms,
+                         "kernel_launches_timed": k_count, "peak_source": peak_src,
+                         "note": "per rank (slowest): local single-pass bytes / local MPK time"},
+            "cpu_baseline": None,
+            "e2e": {"value": flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * (p + 1),
+                    "ms_per_step": e_ms, "note": "per rank: own x in, own rows of y_0..y_p out"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    if not parity:
+        sys.exit(3)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -304,6 +429,7 @@ def main():
     import paper_2309_02228_b200 as mpkg
 
     rank, world, local, dist = dist_setup(args.gpus)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     p = cfgd["p"]
     t0 = time.perf_counter()
@@ -349,6 +475,9 @@ def main():
 
     x_host = mpkg.random_vector(n, args.seed + 2)
     x_perm = ctx.permute_vector(x_host, ls.perm)  # csr.hpp:191 permute_vector
+    if world > 1:
+        return run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist, info,
+                           prep, stream, sync)
     dev = torch.device("cuda", local)
     d_x = torch.from_numpy(x_perm).to(dev)
     d_blk = torch.empty((p + 1) * n, dtype=torch.float64, device=dev)

@@ -113,6 +113,10 @@ int mpkg_validate_levels(mpkg_ctx_t ctx, mpkg_csr_t A_perm, mpkg_levels_t L, int
  * perm is not a permutation (csr.hpp:145-155). */
 int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t* out);
 /* Same, with the device-resident perm of a level structure (no host round trip). */
+/* Shard support (multi-GPU level ranges): B = A[r0:r1, c0:c1] on the device,
+ * column indices shifted by -c0, kept entries in stored order. */
+int mpkg_csr_block(mpkg_ctx_t ctx, mpkg_csr_t A, uint32_t r0, uint32_t r1, uint32_t c0,
+                   uint32_t c1, mpkg_csr_t* out);
 int mpkg_permute_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t L, mpkg_csr_t* out);
 /* csr.hpp:191-204: out[perm[i]] = in[i] / out[i] = in[perm[i]] (host arrays). */
 int mpkg_permute_vector(mpkg_ctx_t ctx, uint32_t n, const double* in, const uint32_t* perm,

@@ -34,6 +34,7 @@ _SIGS = {
     "mpkg_csr_info": [P, pu32, pu32, pu32],
     "mpkg_csr_download": [P, P, P, P],
     "mpkg_csr_destroy": [P],
+    "mpkg_csr_block": [P, P, u32, u32, u32, u32, C.POINTER(P)],
     "mpkg_spmv": [P, P, P, P],
     "mpkg_spmv_dev": [P, P, P, P],
     "mpkg_build_levels": [P, P, C.POINTER(P)],

@@ -391,6 +391,12 @@ class Context:
             check(lib.mpkg_permute(self.h, A.h, _ptr(p), C.byref(h)))
         return DeviceCsr(self, h.value)
 
+    def csr_block(self, A: DeviceCsr, r0: int, r1: int, c0: int, c1: int) -> DeviceCsr:
+        """A[r0:r1, c0:c1] on the device (columns shifted by -c0): a level-range shard."""
+        h = _P()
+        check(lib.mpkg_csr_block(self.h, A.h, r0, r1, c0, c1, C.byref(h)))
+        return DeviceCsr(self, h.value)
+
     def permute_vector(self, v, perm) -> np.ndarray:  # csr.hpp:191
         v, p = _f64(v), _u32(perm)
         out = np.empty_like(v)

@@ -524,6 +524,24 @@ int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t*
     });
 }
 
+int mpkg_csr_block(mpkg_ctx_t ctx, mpkg_csr_t A, uint32_t r0, uint32_t r1, uint32_t c0, uint32_t c1,
+                   mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && A && out, "csr_block: null argument");
+        require(r0 <= r1 && r1 <= A->n_rows, "csr_block: row range outside the matrix");
+        require(c0 <= c1 && c1 <= A->n_cols, "csr_block: column range outside the matrix");
+        use_device(ctx);
+        auto* B = new mpkg_csr_s();
+        try {
+            gpu_csr_block(ctx, A, r0, r1, c0, c1, B);
+        } catch (...) {
+            delete B;
+            throw;
+        }
+        *out = B;
+    });
+}
+
 int mpkg_permute_levels(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_levels_t L, mpkg_csr_t* out) {
     return guarded([&] {
         require(ctx && A && L && out, "permute: null argument");

@@ -192,6 +192,8 @@ void gpu_check_permutation(mpkg_ctx_s* ctx, const uint32_t* d_perm, uint32_t n);
 void gpu_permute(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_perm, mpkg_csr_s* B);
 void gpu_permute_vector(mpkg_ctx_s* ctx, uint32_t n, const double* d_in, const uint32_t* d_perm,
                         double* d_out, bool inverse);
+void gpu_csr_block(mpkg_ctx_s* ctx, const mpkg_csr_s* A, uint32_t r0, uint32_t r1, uint32_t c0,
+                   uint32_t c1, mpkg_csr_s* B);
 void gpu_gather_row_ptr(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_idx, uint32_t m,
                         uint32_t* h_out);
 

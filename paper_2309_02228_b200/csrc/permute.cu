@@ -203,6 +203,67 @@ void gpu_permute_vector(mpkg_ctx_s* ctx, uint32_t n, const double* d_in, const u
     ctx->launches += 1;
 }
 
+namespace {
+// Entries of row r0+i with column in [c0, c1).
+__global__ void k_block_counts(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                               uint32_t r0, uint32_t m, uint32_t c0, uint32_t c1,
+                               uint32_t* __restrict__ cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = 0;
+        for (uint32_t k = rp[r0 + i]; k < rp[r0 + i + 1]; ++k) c += ci[k] >= c0 && ci[k] < c1;
+        cnt[i] = c;
+    }
+}
+__global__ void k_block_fill(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                             const double* __restrict__ v, uint32_t r0, uint32_t m, uint32_t c0,
+                             uint32_t c1, const uint32_t* __restrict__ brp, uint32_t* __restrict__ bci,
+                             double* __restrict__ bv) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t o = brp[i];
+        for (uint32_t k = rp[r0 + i]; k < rp[r0 + i + 1]; ++k)
+            if (ci[k] >= c0 && ci[k] < c1) {
+                bci[o] = ci[k] - c0;
+                bv[o++] = v[k];
+            }
+    }
+}
+}  // namespace
+
+// B = A[r0:r1, c0:c1] with column indices shifted by -c0; kept entries stay in stored order (the
+// local matrix of a level-range shard, multi.py).
+void gpu_csr_block(mpkg_ctx_s* ctx, const mpkg_csr_s* A, uint32_t r0, uint32_t r1, uint32_t c0,
+                   uint32_t c1, mpkg_csr_s* B) {
+    cudaStream_t st = ctx->stream;
+    const uint32_t m = r1 - r0;
+    B->ctx = ctx;
+    B->device = ctx->device;
+    B->n_rows = m;
+    B->n_cols = c1 - c0;
+    B->row_ptr.alloc(m + 1);
+    DevBuf<uint32_t> cnt(m + 1);
+    MPKG_CUDA(cudaMemsetAsync(cnt.p + m, 0, sizeof(uint32_t), st));
+    if (m)
+        k_block_counts<<<grid_for(m, 256), 256, 0, st>>>(A->row_ptr.p, A->col_idx.p, r0, m, c0, c1, cnt.p);
+    MPKG_LAUNCH_CHECK();
+    size_t tb = 0;
+    MPKG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, B->row_ptr.p, (int)(m + 1), st));
+    DevBuf<uint8_t> tmp(tb);
+    MPKG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, B->row_ptr.p, (int)(m + 1), st));
+    uint32_t nnz = 0;
+    MPKG_CUDA(cudaMemcpyAsync(&nnz, B->row_ptr.p + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaStreamSynchronize(st));
+    B->nnz = nnz;
+    B->col_idx.alloc((uint64_t)nnz + 1);
+    B->values.alloc((uint64_t)nnz + 1);
+    if (m)
+        k_block_fill<<<grid_for(m, 256), 256, 0, st>>>(A->row_ptr.p, A->col_idx.p, A->values.p, r0, m, c0,
+                                                      c1, B->row_ptr.p, B->col_idx.p, B->values.p);
+    MPKG_LAUNCH_CHECK();
+    ctx->launches += 3;
+}
+
 void gpu_gather_row_ptr(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_idx, uint32_t m,
                         uint32_t* h_out) {
     if (m == 0) return;

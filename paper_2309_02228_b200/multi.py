@@ -94,37 +94,41 @@ def local_level_ptr(level_ptr, L0: int, L1: int, p: int):
     return (lp[a:b + 1] - lp[a]).astype(np.uint32)
 
 
-def exchange_x(x_own: np.ndarray, plans: Sequence[HaloPlan], rank: int, dist, group=None) -> np.ndarray:
-    """Builds the local x (rows [g0, g1)) from the owners' pieces with point-to-point sends.
-    Every rank runs this with its own x_own (rows [o0, o1))."""
+def exchange_halo(x_own, plans: Sequence[HaloPlan], rank: int, dist, group=None):
+    """The one collective of the level-partitioned MPK: builds this rank's local x (rows
+    [g0, g1)) from the owners' pieces with grouped point-to-point transfers.  `x_own` is a torch
+    tensor holding rows [o0, o1); the result lives on the same device (NCCL over NVLink between
+    GPUs, gloo in the CPU tests).  Every rank calls this with its own x_own."""
     import torch
+    if x_own.is_cuda and dist.get_backend(group) == "gloo":  # gloo moves host tensors only
+        return exchange_halo(x_own.cpu(), plans, rank, dist, group).to(x_own.device)
     me = plans[rank]
     g0, g1 = me.local_rows
-    out = np.empty(g1 - g0, dtype=np.float64)
-    reqs, keep = [], []
     o0 = me.own_rows[0]
-    # sends: my own rows to every rank whose local range overlaps them
-    for other in plans:
+    out = torch.empty(g1 - g0, dtype=x_own.dtype, device=x_own.device)
+    ops = []
+    for other in plans:  # my own rows to every rank whose local range overlaps them
         if other.rank == rank:
             continue
         for s, r0, r1 in other.pieces:
             if s == rank:
-                buf = torch.from_numpy(np.ascontiguousarray(x_own[r0 - o0:r1 - o0]))
-                keep.append(buf)
-                reqs.append(dist.isend(buf, dst=other.rank, group=group))
-    recv = []
+                ops.append(dist.P2POp(dist.isend, x_own[r0 - o0:r1 - o0].contiguous(), other.rank, group))
     for s, r0, r1 in me.pieces:
         if s == rank:
             out[r0 - g0:r1 - g0] = x_own[r0 - o0:r1 - o0]
         else:
-            buf = torch.empty(r1 - r0, dtype=torch.float64)
-            recv.append((buf, r0, r1))
-            reqs.append(dist.irecv(buf, src=s, group=group))
-    for rq in reqs:
-        rq.wait()
-    for buf, r0, r1 in recv:
-        out[r0 - g0:r1 - g0] = buf.numpy()
+            ops.append(dist.P2POp(dist.irecv, out[r0 - g0:r1 - g0], s, group))
+    if ops:
+        for rq in dist.batch_isend_irecv(ops):
+            rq.wait()
     return out
+
+
+def exchange_x(x_own: np.ndarray, plans: Sequence[HaloPlan], rank: int, dist, group=None) -> np.ndarray:
+    """Host-array form of exchange_halo."""
+    import torch
+    return exchange_halo(torch.from_numpy(np.ascontiguousarray(x_own, dtype=np.float64)), plans, rank,
+                         dist, group).numpy()
 
 
 LocalMPK = Callable[[np.ndarray, np.ndarray, np.ndarray, np.ndarray, np.ndarray, int], np.ndarray]
@@ -174,3 +178,46 @@ class DistributedMPK:
         blk = self.local_mpk(*self.local, self.local_lp, x_loc, self.p)
         o0 = me.own_rows[0] - me.local_rows[0]
         return blk[:, o0:o0 + (me.own_rows[1] - me.own_rows[0])]
+
+
+class ShardedMPK:
+    """One rank's device-resident share of a level-partitioned MPK (the multi-GPU path of
+    bench.py).  The global A_perm is on this rank's GPU only for setup: the local matrix
+    A_perm[g0:g1, g0:g1] is cut on the device (mpkg_csr_block), its level structure is the
+    global one restricted to the local levels, and every step is one halo exchange of x on the
+    context's stream followed by the local MPK (one launch per power or the fused kernel, as on
+    one GPU).  Own rows are bit-identical to the single-GPU result."""
+
+    def __init__(self, ctx, A_perm, level_ptr, row_nnz_prefix, p: int, rank: int, world: int,
+                 cache_bytes: Optional[int] = None):
+        from . import api
+        self.ctx, self.p, self.rank, self.world = ctx, p, rank, world
+        lp = np.asarray(level_ptr, dtype=np.int64)
+        self.parts = partition_levels(lp, row_nnz_prefix, world)
+        self.plans = [halo_plan(lp, self.parts, r, p) for r in range(world)]
+        me = self.plans[rank]
+        g0, g1 = me.local_rows
+        self.n_local = g1 - g0
+        self.own = (me.own_rows[0] - g0, me.own_rows[1] - g0)  # own rows inside the local block
+        self.A = ctx.csr_block(A_perm, g0, g1, g0, g1)
+        llp = local_level_ptr(lp, me.levels[0], me.levels[1], p)
+        ident = np.arange(self.n_local, dtype=np.uint32)
+        ls = ctx.levels_from_host(np.zeros(self.n_local, np.uint32), ident, ident, llp)
+        self.plan = ctx.group_levels(ls, self.A, cache_bytes or ctx.device_info()["l2_bytes"], p)
+        self._api = api
+
+    @property
+    def halo_plan(self) -> HaloPlan:
+        return self.plans[self.rank]
+
+    def step(self, x_own, block, dist, group=None):
+        """x_own: torch tensor of this rank's own rows of x (device); block: torch tensor of
+        (p+1) * n_local doubles.  Runs on the context's stream (the exchange joins it)."""
+        import torch
+        stream = torch.cuda.ExternalStream(self.ctx.stream, device=x_own.device)
+        with torch.cuda.stream(stream):
+            x_loc = exchange_halo(x_own, self.plans, self.rank, dist, group)
+            if self.n_local:
+                self.ctx.mpk_dev(self.plan, self.A, x_loc.data_ptr(), self.p, block.data_ptr(),
+                                 self.n_local, self.p + 1)
+        return x_loc
