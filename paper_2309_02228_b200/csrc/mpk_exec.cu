@@ -49,7 +49,8 @@ constexpr uint32_t kBig = 1u << 31;      // ticket flag: tile too large for the 
 constexpr uint32_t kMaxBufBytes = 96 * 1024;
 constexpr uint32_t kLongCap = 1024;    // rows longer than this take the CTA-cooperative path
 constexpr uint32_t kSB = 64;           // tiles per completion-counter superblock
-constexpr uint32_t kLongChunk = 4096;  // products per chunk of a long row
+constexpr uint32_t kLongChunk = 1024;  // products per chunk of a long row (x2 smem ring)
+constexpr uint32_t kLeanRingBytes = 2 * kLongChunk * sizeof(double);
 #ifndef MPKG_GROUP
 #define MPKG_GROUP 16
 #endif
@@ -83,6 +84,7 @@ struct Executor {
     uint32_t n_prod = 0, n_cgroups = 0;       // k_mpk_async roles
     bool sb = false;                          // poll dependencies through superblock counters
     bool last_sweep = false;                  // the last run used one launch per power
+    bool fused_ready = false;                 // build_fused() has run
     int64_t prod_knob = 0, cg_knob = 0;
     uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
     int64_t order_knob = -1;                  // ctx->order the executor was built with
@@ -92,7 +94,6 @@ struct Executor {
     int64_t kernel_knob = 0;                  // ctx->kernel the executor was built with
     std::vector<uint32_t> h_tile_start;       // variable tiles (empty: fixed tile_rows)
     DevBuf<uint32_t> tile_start;
-    DevBuf<double> long_prod;                 // grid * kLongChunk product scratch
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
     DevBuf<uint32_t> sb_count;                // (kMaxFusedP+1) x n_sb superblock counters
@@ -126,7 +127,6 @@ struct FusedParams {
     const uint32_t* csr_rp;      // A_perm CSR (long rows)
     const uint32_t* csr_ci;
     const double* csr_v;
-    double* long_prod;           // per-CTA product scratch for long rows (grid * kLongChunk)
     uint32_t* sb_count;          // [(p+1) * n_sb] completions per power and superblock
     uint32_t n_sb;
     uint32_t n_tiles;
@@ -471,27 +471,55 @@ __device__ __forceinline__ void row_epilogue(const FusedParams& P, uint32_t s, u
     }
 }
 
-// Long row of a single-row tile (see k_mpk_lean): CTA-wide products, thread 0 sums in order.
-// Returns true (and the sum in thread 0's `acc`) when slot s0 holds a long row.
+// Long row of a single-row tile (see k_mpk_lean).  Bitwise mode must add the row's products
+// in stored order, so a hub row is a chain of `len` dependent DADDs (R-MAT scale 21: 102,493):
+// that chain is the critical path, and everything else is arranged around it.  Warps 1..3
+// compute the products of chunk c+1 (coalesced CSR reads, x gathers) into one half of a
+// double-buffered shared-memory ring while thread 0 adds chunk c from the other half at
+// shared-memory latency, two products per LDS.128.  Returns true (sum in thread 0's `acc`)
+// when slot s0 holds a long row.
 template <bool SIGMA>
 __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, uint32_t q,
-                                             uint64_t pol, uint32_t tid, uint32_t nt, double& acc) {
+                                             uint64_t pol, uint32_t tid, uint32_t nt, double& acc,
+                                             double* ring) {
     const uint32_t r = SIGMA ? P.slot_row[s0] : s0;
     const uint32_t len = r < P.n_rows ? P.row_len[s0] : 0u;
     if (len <= P.long_cap) return false;
     const uint32_t b = P.csr_rp[r];
     const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;
-    acc = 0.0;
-    for (uint32_t base = 0; base < len; base += kLongChunk) {
-        const uint32_t m = min(kLongChunk, len - base);
-        for (uint32_t i = tid; i < m; i += nt) {
+    const uint32_t nchunks = (len + kLongChunk - 1) / kLongChunk;
+    auto produce = [&](uint32_t c) {  // warps 1.. only
+        const uint32_t base = c * kLongChunk, m = min(kLongChunk, len - base);
+        double* buf = ring + (c & 1u) * kLongChunk;
+        for (uint32_t i = tid - 32u; i < m; i += nt - 32u) {
             const uint32_t k = b + base + i;
             const double xv = q == 1 ? ld_vec<true>(srcA + P.csr_ci[k]) : ld_vec<false>(srcA + P.csr_ci[k]);
-            P.long_prod[blockIdx.x * kLongChunk + i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
+            buf[i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
         }
-        __syncthreads();
-        if (tid == 0)
-            for (uint32_t i = 0; i < m; ++i) acc = __dadd_rn(acc, P.long_prod[blockIdx.x * kLongChunk + i]);
+    };
+    acc = 0.0;
+    if (tid >= 32) produce(0);
+    __syncthreads();
+    for (uint32_t c = 0; c < nchunks; ++c) {
+        if (tid >= 32) {
+            if (c + 1 < nchunks) produce(c + 1);
+        } else if (tid == 0) {
+            const uint32_t m = min(kLongChunk, len - c * kLongChunk);
+            const double2* cur = reinterpret_cast<const double2*>(ring + (c & 1u) * kLongChunk);
+            uint32_t i = 0;
+            for (; i + 8 <= m; i += 8) {
+                double2 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = cur[i / 2 + j];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc = __dadd_rn(acc, v[j].x);
+                    acc = __dadd_rn(acc, v[j].y);
+                }
+            }
+            const double* tail = ring + (c & 1u) * kLongChunk;
+            for (; i < m; ++i) acc = __dadd_rn(acc, tail[i]);
+        }
         __syncthreads();
     }
     return true;
@@ -527,6 +555,7 @@ __global__ void __launch_bounds__(256) k_mpk_sweep(const __grid_constant__ Fused
 // superblock counters (otherwise tile flags only).
 template <int KIND, bool SIGMA, bool VT, bool SB>
 __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedParams P) {
+    extern __shared__ __align__(16) double lring[];  // VT: 2 x kLongChunk long-row products
     __shared__ uint32_t s_ticket[2];
     const uint32_t tid = threadIdx.x;
     const uint32_t nt = blockDim.x;
@@ -555,7 +584,7 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
         const uint32_t s0 = VT ? P.tile_start[T] : T * P.tile_rows;
         const uint32_t s1 = VT ? P.tile_start[T + 1] : s0 + P.tile_rows;
         double long_acc = 0.0;
-        if (VT && s1 - s0 == 1 && long_row_dot<SIGMA>(P, s0, q, pol, tid, nt, long_acc)) {
+        if (VT && s1 - s0 == 1 && long_row_dot<SIGMA>(P, s0, q, pol, tid, nt, long_acc, lring)) {
             // A single-row tile holding a long row (len > SELL long_cap, e.g. an R-MAT hub): the
             // CTA computes the products from the row's contiguous A_perm CSR slice in chunks,
             // gathering from the A_perm-order copy of y_{q-1} in the caller's block, and one
@@ -930,7 +959,7 @@ std::array<const void*, 3> lean_variants(bool sigma, bool vt, bool sb) {
 template <int KIND, bool SIGMA>
 void launch_lean(bool sb, int grid, int nt, cudaStream_t st, const FusedParams& P) {
     if (P.tile_start)
-        k_mpk_lean<KIND, SIGMA, true, true><<<grid, nt, 0, st>>>(P);
+        k_mpk_lean<KIND, SIGMA, true, true><<<grid, nt, kLeanRingBytes, st>>>(P);
     else if (sb)
         k_mpk_lean<KIND, SIGMA, false, true><<<grid, nt, 0, st>>>(P);
     else
@@ -960,7 +989,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         P->exec->cg_knob == ctx->cgroups) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
-        if (E.knobs != k) {
+        if (E.knobs != k && E.fused_ready) {
             E.tickets.clear();  // schedule knobs changed: re-plan the ticket order
             E.pass_len.clear();
             const int occ = ctx->ctas_per_sm > 0 ? std::min<int>(E.occ_max, (int)ctx->ctas_per_sm) : E.occ_max;
@@ -1054,6 +1083,16 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     }
     if (E->n_tiles >= (1u << 24)) fail(MPKG_EINVAL, "mpk: more than 2^24 tiles");
     if (!E->h_tile_start.empty()) E->kernel_forced_lean = true;
+    MPKG_CUDA(cudaStreamSynchronize(st));
+    P->exec = E;
+    P->exec_csr = A;
+    return *E;
+}
+
+// Fused-kernel state (first fused run only: the sweep schedule never needs it): tile extents in
+// the SELL arrays, tile dependency runs, kernel variant, occupancy, grid.
+void build_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, Executor* E) {
+    cudaStream_t st = ctx->stream;
     const uint32_t nt = E->n_tiles;
     auto tile_first = [&](uint32_t T) -> uint32_t {
         return E->h_tile_start.empty() ? std::min<uint64_t>((uint64_t)T * E->tile_rows, E->n_slots)
@@ -1200,7 +1239,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         occ = 1 << 30;
         for (const void* k : lean_variants(E->order >= 1, vt, vt || E->sb)) {
             int o = 0;
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, nt, 0));
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, nt, vt ? kLeanRingBytes : 0));
             occ = std::min(occ, o);
         }
     } else if (E->group == 8) {
@@ -1225,11 +1264,9 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     }
     E->done.alloc(std::max<uint32_t>(nt, 1));
     E->counter.alloc(1);
-    if (E->long_rows) E->long_prod.alloc((uint64_t)E->grid * kLongChunk);
     MPKG_CUDA(cudaStreamSynchronize(st));
-    P->exec = E;
-    P->exec_csr = A;
-    return *E;
+    E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
+    E->fused_ready = true;
 }
 
 // One pass of the list schedule over powers q0..q1: keys (pass, ready time, q, tile), unsorted.
@@ -1352,7 +1389,10 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (a.p > kMaxFusedP) fail(MPKG_EINVAL, "mpk: at most 32 powers per fused launch");
     Executor& E = get_executor(ctx, Pl, A);
     if (E.n_tiles == 0) return;
-    const DevBuf<uint32_t>& tk = get_tickets(ctx, E, a.p);
+    const bool sweep = use_sweeps(ctx, E, a.p);
+    if (!sweep && !E.fused_ready) build_fused(ctx, Pl, A, &E);
+    static const DevBuf<uint32_t> no_tickets;
+    const DevBuf<uint32_t>& tk = sweep ? no_tickets : get_tickets(ctx, E, a.p);
     const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
     const bool sigma = E.order >= 1;  // any private order (CM or length-sorted)
@@ -1382,14 +1422,15 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.csr_rp = A->row_ptr.p;
     P.csr_ci = A->col_idx.p;
     P.csr_v = A->values.p;
-    P.long_prod = E.long_rows ? E.long_prod.p : nullptr;
     P.n_tiles = E.n_tiles;
     P.n_prod = E.n_prod;
     P.n_cgroups = E.n_cgroups;
     P.n_sb = (E.n_tiles + kSB - 1) / kSB;
-    E.sb_count.ensure((uint64_t)(kMaxFusedP + 1) * P.n_sb + 1);
-    P.sb_count = E.sb_count.p;
-    MPKG_CUDA(cudaMemsetAsync(E.sb_count.p, 0, 4ull * (a.p + 1) * P.n_sb, st));
+    if (!sweep) {
+        E.sb_count.ensure((uint64_t)(kMaxFusedP + 1) * P.n_sb + 1);
+        P.sb_count = E.sb_count.p;
+        MPKG_CUDA(cudaMemsetAsync(E.sb_count.p, 0, 4ull * (a.p + 1) * P.n_sb, st));
+    }
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
@@ -1415,10 +1456,11 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         P.shift_b2[i] = a.shift_b2 ? a.shift_b2[i] : 0.0;
     }
     for (int i = 0; i <= a.p; ++i) P.coef[i] = a.coef ? a.coef[i] : 0.0;
-    MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
-    MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
+    if (!sweep) {
+        MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
+        MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
+    }
     const uint32_t smem = E.stages * E.buf_bytes;
-    const bool sweep = use_sweeps(ctx, E, a.p);
     E.last_sweep = sweep;
     const auto ev = timing_begin(ctx);
     if (sweep) {
