@@ -45,7 +45,12 @@ extern "C" {
 /* Arithmetic modes (mpkg_ctx_set_mode). */
 #define MPKG_MODE_BITWISE 0 /* one sequential accumulator per row in stored column order,
                                __dmul_rn + __dadd_rn: bit-identical to the reference CPU build */
-#define MPKG_MODE_FAST 1    /* reserved: DFMA / split long rows; checked to 1e-12 (inf-norm) */
+#define MPKG_MODE_FAST 1    /* mpk / mpk_shifted / mpk_poly only: rows longer than the SELL
+                               long-row cap (1024) are reduced in parallel (fixed-shape tree,
+                               deterministic) instead of in stored order, so power-law hubs no
+                               longer serialise a power; every other row and every baseline_*
+                               result stays bitwise.  Checked to the north star's 1e-12
+                               inf-norm relative bound per basis vector. */
 
 typedef struct mpkg_ctx_s* mpkg_ctx_t;
 typedef struct mpkg_csr_s* mpkg_csr_t;

@@ -332,6 +332,13 @@ class Context:
     def set_param(self, key: str, value: int):
         check(lib.mpkg_ctx_set_param(self.h, key.encode(), int(value)))
 
+    MODE_BITWISE, MODE_FAST = 0, 1
+
+    def set_mode(self, mode: int):
+        """MODE_BITWISE (default): bit-identical to the reference.  MODE_FAST: long rows reduced
+        in parallel; within the north star's 1e-12 inf-norm bound (include/mpkg.h)."""
+        check(lib.mpkg_ctx_set_mode(self.h, int(mode)))
+
     def kernel_times(self) -> tuple:
         """(total_ms, count, max_ms) of the launches recorded since the last call."""
         t, n, m = C.c_double(), C.c_uint64(), C.c_double()

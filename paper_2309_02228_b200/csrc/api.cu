@@ -229,7 +229,8 @@ int mpkg_ctx_synchronize(mpkg_ctx_t ctx) {
 int mpkg_ctx_set_mode(mpkg_ctx_t ctx, int mode) {
     return guarded([&] {
         require(ctx != nullptr, "ctx_set_mode: null context");
-        require(mode == MPKG_MODE_BITWISE, "ctx_set_mode: only MPKG_MODE_BITWISE is implemented");
+        require(mode == MPKG_MODE_BITWISE || mode == MPKG_MODE_FAST,
+                "ctx_set_mode: mode must be MPKG_MODE_BITWISE or MPKG_MODE_FAST");
         ctx->mode = mode;
     });
 }

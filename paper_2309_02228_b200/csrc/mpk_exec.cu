@@ -93,6 +93,7 @@ struct Executor {
     bool kernel_forced_lean = false;          // variable tiles need the lean kernel
     int64_t kernel_knob = 0;                  // ctx->kernel the executor was built with
     std::vector<uint32_t> h_tile_start;       // variable tiles (empty: fixed tile_rows)
+    DevBuf<uint32_t> long_slots;              // slots of the long rows
     DevBuf<uint32_t> tile_start;
     int occ_max = 1;                          // resident CTAs per SM the smem/regs allow
     DevBuf<uint32_t> done, counter;
@@ -130,6 +131,8 @@ struct FusedParams {
     uint32_t* sb_count;          // [(p+1) * n_sb] completions per power and superblock
     uint32_t n_sb;
     uint32_t n_tiles;
+    const uint32_t* long_slots;  // fast mode: slots of the long rows (n_long)
+    uint32_t n_long;
     uint32_t n_prod;        // async kernel: producer warps per CTA
     uint32_t n_cgroups;     // async kernel: consumer groups (tile_rows threads each) per CTA
     uint64_t vstride;  // stride of V slices
@@ -538,10 +541,43 @@ __global__ void __launch_bounds__(256) k_mpk_sweep(const __grid_constant__ Fused
         const uint32_t r = SIGMA ? P.slot_row[s] : (uint32_t)s;
         if (r >= P.n_rows) continue;
         const uint32_t len = P.row_len[s];
+        if (len > P.long_cap) continue;  // long rows: k_long_rows_fast (fast mode only)
         const uint64_t off = P.chunk_off[s >> 5];
         const uint32_t L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
         const double acc = sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
         row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+    }
+}
+
+// MPKG_MODE_FAST, sweep schedule: the long rows of power q (left out of the SELL arrays), one
+// CTA per row.  Each thread adds its strided share of the products, then a fixed-shape tree
+// (warp shuffles, then the per-warp partials in order) combines them: deterministic run to run,
+// not the reference's summation order.  Error vs the sequential sum <= ~(log2(len)+nt) * eps
+// * sum|products| (below the sequential sum's own len * eps bound); checked
+// against the oracle at the north star's 1e-12 inf-norm tolerance.
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_long_rows_fast(const __grid_constant__ FusedParams P, uint32_t q) {
+    __shared__ double part[8];
+    const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;  // A_perm-order copy of y_{q-1}
+    const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    const uint64_t pol = l2_policy_first();
+    for (uint32_t i = blockIdx.x; i < P.n_long; i += gridDim.x) {
+        const uint32_t s = P.long_slots[i];
+        const uint32_t r = SIGMA ? P.slot_row[s] : s;
+        const uint32_t b = P.csr_rp[r], e = P.csr_rp[r + 1];
+        double acc = 0.0;
+        for (uint32_t k = b + threadIdx.x; k < e; k += blockDim.x)
+            acc = __fma_rn(ld_mat_d(P.csr_v + k, pol), __ldg(srcA + P.csr_ci[k]), acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += part[w];
+            row_epilogue<KIND, SIGMA>(P, s, r, q, src, t);
+        }
+        __syncthreads();
     }
 }
 
@@ -1020,6 +1056,11 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     }
     E->prod_knob = ctx->producers;
     E->cg_knob = ctx->cgroups;
+    // every knob the cache check in this function compares (build_fused reads them later)
+    E->group = ctx->group == 8 ? 8 : 16;
+    E->stage_knob = ctx->stages;
+    E->tile_knob = ctx->tile_rows;
+    E->thread_knob = ctx->threads;
     E->tile_rows = ctx->tile_rows == 32 ? 32u : ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
     if (E->tile_rows == 32 && ctx->kernel != 4) E->tile_rows = 64;  // 32-row tiles: async kernel only
     if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
@@ -1076,7 +1117,13 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             MPKG_CUDA(cudaMemcpyAsync(E->tile_start.p, E->h_tile_start.data(), 4ull * E->h_tile_start.size(),
                                       cudaMemcpyHostToDevice, st));
             E->long_rows = 0;
-            for (uint32_t v : rl) E->long_rows += v > E->long_cap;
+            std::vector<uint32_t> ls;
+            for (uint32_t i = 0; i < (uint32_t)rl.size(); ++i)
+                if (rl[i] > E->long_cap) ls.push_back(i);
+            E->long_rows = ls.size();
+            E->long_slots.alloc(std::max<size_t>(ls.size(), 1));
+            if (!ls.empty())
+                MPKG_CUDA(cudaMemcpyAsync(E->long_slots.p, ls.data(), 4ull * ls.size(), cudaMemcpyHostToDevice, st));
         } else {
             E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
         }
@@ -1191,10 +1238,6 @@ void build_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, Executor* E) {
         E->stages = std::max<uint32_t>(2, std::min<uint32_t>(kMaxStages, (200u << 10) / E->buf_bytes));
     while (E->stages > 1 && E->stages * E->buf_bytes > (220u << 10)) --E->stages;
     const uint32_t smem = E->stages * E->buf_bytes;
-    E->group = ctx->group == 8 ? 8 : 16;
-    E->stage_knob = ctx->stages;
-    E->tile_knob = ctx->tile_rows;
-    E->thread_knob = ctx->threads;
     int occ = 0;
     // variable tiles (long rows): the lean kernel
     E->kernel = E->kernel_forced_lean ? 0 : (int)ctx->kernel;
@@ -1381,7 +1424,9 @@ void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
 // exists only in the fused kernel.
 bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
     if (ctx->schedule == 1) return false;
-    if (E.long_rows) return false;  // long rows live outside the SELL arrays: fused path only
+    // Long rows live outside the SELL arrays: bitwise mode runs them through the fused kernel's
+    // stored-order path; fast mode reduces them in k_long_rows_fast between sweeps.
+    if (E.long_rows && ctx->mode != MPKG_MODE_FAST) return false;
     return true;
 }
 
@@ -1423,6 +1468,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.csr_ci = A->col_idx.p;
     P.csr_v = A->values.p;
     P.n_tiles = E.n_tiles;
+    P.long_slots = E.long_slots.p;
+    P.n_long = (uint32_t)E.long_rows;
     P.n_prod = E.n_prod;
     P.n_cgroups = E.n_cgroups;
     P.n_sb = (E.n_tiles + kSB - 1) / kSB;
@@ -1465,6 +1512,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const auto ev = timing_begin(ctx);
     if (sweep) {
         const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
+        const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
         for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
             switch (a.kind * 2 + (sigma ? 1 : 0)) {
                 case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
@@ -1475,6 +1523,18 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
                 default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
             }
             MPKG_LAUNCH_CHECK();
+            if (E.long_rows) {  // fast mode only (use_sweeps)
+                switch (a.kind * 2 + (sigma ? 1 : 0)) {
+                    case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
+                    case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
+                    case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
+                    case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
+                    case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
+                    default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
+                }
+                MPKG_LAUNCH_CHECK();
+                ctx->launches += 1;
+            }
         }
         ctx->launches += (uint64_t)a.p - 1;
     } else if (E.kernel == 4) {

@@ -273,6 +273,49 @@ def test_long_rows_and_length_order(ctx, oracle, order):
         set_knobs(ctx, {})
 
 
+def _rel_inf_err(got, ref):
+    """max|got - ref| / max|ref| per basis vector (the north star's 1e-12 bar)."""
+    got, ref = np.atleast_2d(got), np.atleast_2d(ref)
+    return [float(np.abs(g - r).max() / max(np.abs(r).max(), 1e-300)) for g, r in zip(got, ref)]
+
+
+@pytest.mark.parametrize("schedule", [0, 1])
+def test_fast_mode_long_rows_within_tolerance(ctx, oracle, schedule):
+    """MPKG_MODE_FAST reduces hub rows in parallel (sweep schedule) -- or, with the fused
+    schedule forced, keeps the stored-order path: every basis vector within 1e-12 of the oracle
+    in the inf-norm relative sense, run-to-run deterministic, and the baseline still bitwise."""
+    try:
+        set_knobs(ctx, {"schedule": schedule})
+        ctx.set_mode(ctx.MODE_FAST)
+        for A in (_arrow_matrix(), mpkg.rmat(15, 16, 7)):
+            lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+            P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
+            Ap = ctx.csr(P)
+            ls = ctx.levels_from_host(lv, pm, ip, lp)
+            x = mpkg.random_vector(P.n_rows, 3)
+            plan = ctx.group_levels(ls, Ap, 8 << 20, 4)
+            ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4)
+            got = ctx.mpk(plan, Ap, x, 4).as_matrix()
+            errs = _rel_inf_err(got, ref)
+            assert max(errs) <= 1e-12, errs
+            assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), got, "deterministic")
+            info = plan.exec_info()
+            assert info["schedule"] == ("fused" if schedule == 1 else "sweeps")
+            if schedule == 1:
+                assert_bitwise(got, ref, "fused keeps stored order")
+            sh = [1.0, 2.0 + 0.5j, 2.0 - 0.5j, 0.5]
+            ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+            assert max(_rel_inf_err(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref)) <= 1e-12
+            coef = [0.5, -1.0, 0.25, 2.0, -0.125]
+            zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+            assert max(_rel_inf_err(ctx.mpk_poly(plan, Ap, x, coef), zr)) <= 1e-12
+            assert_bitwise(ctx.baseline_mpk(Ap, x, 4).as_matrix(),
+                           oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4), "baseline")
+    finally:
+        ctx.set_mode(ctx.MODE_BITWISE)
+        set_knobs(ctx, {})
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
