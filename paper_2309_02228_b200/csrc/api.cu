@@ -267,6 +267,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
                     "ctx_set_param: kernel must be 0 (lean), 1 (staged), 2 (warp-tile) or 4 (async gather)");
             ctx->kernel = value;
         }
+        else if (k == "graphs")
+            ctx->graphs = value != 0;
         else if (k == "schedule") {
             require(value >= 0 && value <= 2, "ctx_set_param: schedule must be 0 (auto), 1 (fused) or 2 (sweeps)");
             ctx->schedule = value;

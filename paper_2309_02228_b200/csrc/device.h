@@ -103,6 +103,7 @@ struct mpkg_ctx_s {
     int64_t stages = 0;       // >0: staged tickets per CTA (default from smem)
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
+    bool graphs = true;       // sweep schedule: replay the p launches as one CUDA graph
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power (mpk_exec.cu)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
     int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)

@@ -29,6 +29,7 @@
 // Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
 // every row is computed by the same formula, from the same inputs, in any order.
 #include <algorithm>
+#include <cstring>
 #include <array>
 #include <map>
 #include <numeric>
@@ -85,6 +86,14 @@ struct Executor {
     bool sb = false;                          // poll dependencies through superblock counters
     bool last_sweep = false;                  // the last run used one launch per power
     bool fused_ready = false;                 // build_fused() has run
+    // sweep schedule: instantiated CUDA graphs by launch parameters (run_fused)
+    std::vector<std::pair<std::vector<unsigned char>, cudaGraphExec_t>> graphs;
+    Executor() = default;
+    Executor(const Executor&) = delete;
+    Executor& operator=(const Executor&) = delete;
+    ~Executor() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    }
     int64_t prod_knob = 0, cg_knob = 0;
     uint32_t wt_lmax = 0;                     // warp-tile: chunk width handled flat
     int64_t order_knob = -1;                  // ctx->order the executor was built with
@@ -1441,7 +1450,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
     const bool sigma = E.order >= 1;  // any private order (CM or length-sorted)
-    FusedParams P{};
+    FusedParams P;
+    std::memset(&P, 0, sizeof(P));  // padding too: the bytes key the CUDA-graph cache
     P.cols = S.cols.p;
     P.vals = S.vals.p;
     P.chunk_off = S.chunk_off.p;
@@ -1511,32 +1521,67 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     E.last_sweep = sweep;
     const auto ev = timing_begin(ctx);
     if (sweep) {
-        const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
-        const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
-        for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
-            switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
-                case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
-                case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
-                case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
-                case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
-                default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
-            }
-            MPKG_LAUNCH_CHECK();
-            if (E.long_rows) {  // fast mode only (use_sweeps)
+        auto launch_all = [&]() {
+            const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
+            const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
+            for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
                 switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                    case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
-                    case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
-                    case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
-                    case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
-                    case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
-                    default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
+                    case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
+                    case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
+                    case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
+                    case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
+                    case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
+                    default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
                 }
                 MPKG_LAUNCH_CHECK();
-                ctx->launches += 1;
+                if (E.long_rows) {  // fast mode only (use_sweeps)
+                    switch (a.kind * 2 + (sigma ? 1 : 0)) {
+                        case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
+                        case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
+                        case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
+                        case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
+                        case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
+                        default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
+                    }
+                    MPKG_LAUNCH_CHECK();
+                }
             }
+        };
+        if (ctx->graphs) {
+            // One CUDA graph per distinct launch set (parameters, p, kind): repeated calls with
+            // the same buffers replay all p sweeps with a single launch (C1 is launch-bound).
+            std::vector<unsigned char> key(sizeof(FusedParams) + 16);
+            std::memcpy(key.data(), &P, sizeof(FusedParams));
+            const int32_t extra[4] = {a.kind, a.p, sigma ? 1 : 0, (int32_t)E.long_rows};
+            std::memcpy(key.data() + sizeof(FusedParams), extra, sizeof(extra));
+            cudaGraphExec_t exec = nullptr;
+            for (auto& gr : E.graphs)
+                if (gr.first == key) exec = gr.second;
+            if (!exec) {
+                MPKG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                cudaGraph_t graph = nullptr;
+                try {
+                    launch_all();
+                } catch (...) {
+                    (void)cudaStreamEndCapture(st, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                MPKG_CUDA(cudaStreamEndCapture(st, &graph));
+                const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+                cudaGraphDestroy(graph);
+                MPKG_CUDA(e);
+                if (E.graphs.size() >= 8) {
+                    cudaGraphExecDestroy(E.graphs.front().second);
+                    E.graphs.erase(E.graphs.begin());
+                }
+                E.graphs.emplace_back(std::move(key), exec);
+            }
+            MPKG_CUDA(cudaGraphLaunch(exec, st));
+        } else {
+            launch_all();
         }
-        ctx->launches += (uint64_t)a.p - 1;
+        ctx->launches += (uint64_t)a.p * (E.long_rows ? 2 : 1) - 1;  // kernels the step ran
     } else if (E.kernel == 4) {
         const int nt = (int)E.threads;
         const uint32_t sm = E.stages * E.buf_bytes;
