@@ -403,3 +403,120 @@ int orc_tune_select(const double* gflops, int p_lo, int p_hi) {
         }
     return best_p;
 }
+
+/* ---- Jacobi-preconditioned chains ------------------------------------------------------------ */
+
+/* csr.hpp:233-243 + jacobi.hpp:48-64 */
+int orc_diag_info(uint32_t n_rows, uint32_t n_cols, const uint32_t* rp, const uint32_t* ci,
+                  const double* vals, uint32_t* pos, double* inv, uint32_t* bad_row) {
+    if (n_rows != n_cols) return ORC_EINVAL;
+    for (uint32_t r = 0; r < n_rows; ++r) {
+        /* binary search for column r in the sorted row (lower_bound) */
+        uint32_t lo = rp[r], hi = rp[r + 1];
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if (ci[mid] < r)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        pos[r] = (lo < rp[r + 1] && ci[lo] == r) ? lo : ORC_NO_DIAG;
+        if (pos[r] == ORC_NO_DIAG || vals[pos[r]] == 0.0) {
+            if (bad_row) *bad_row = r;
+            return ORC_ERUNTIME;
+        }
+        inv[r] = 1.0 / vals[pos[r]];
+    }
+    return ORC_OK;
+}
+
+/* jacobi.hpp:83-96 jacobi_sweep_rows: z_i = d_i v_i - d_i * sum_{k != diag} a_ik z_prev_k */
+static void jacobi_sweep(const uint32_t* rp, const uint32_t* ci, const double* vals,
+                         const uint32_t* pos, const double* inv, const double* v,
+                         const double* z_prev, double* z_out, uint32_t n) {
+    for (uint32_t r = 0; r < n; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            if (k == pos[r]) continue;
+            acc += vals[k] * z_prev[ci[k]];
+        }
+        z_out[r] = inv[r] * v[r] - inv[r] * acc;
+    }
+}
+
+/* jacobi.hpp:155-174 */
+void orc_jacobi_apply(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                      const uint32_t* pos, const double* inv, int sweeps, const double* v,
+                      double* z) {
+    for (uint32_t r = 0; r < n; ++r) z[r] = inv[r] * v[r];
+    if (sweeps <= 1) return;
+    double* tmp = (double*)malloc(sizeof(double) * (n ? n : 1));
+    for (int s = 2; s <= sweeps; ++s) {
+        jacobi_sweep(rp, ci, vals, pos, inv, v, z, tmp, n);
+        memcpy(z, tmp, sizeof(double) * n);
+    }
+    free(tmp);
+}
+
+/* jacobi.hpp:100-110 scaled_spmv_rows: y_r = sum_k a_rk * (d_c * x_c) */
+static void scaled_spmv(const uint32_t* rp, const uint32_t* ci, const double* vals,
+                        const double* inv, const double* x, double* y, uint32_t n) {
+    for (uint32_t r = 0; r < n; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) acc += vals[k] * (inv[ci[k]] * x[ci[k]]);
+        y[r] = acc;
+    }
+}
+
+/* jacobi.hpp:120-149 chain stages, run in order (jacobi.hpp:177-192) */
+void orc_jacobi_op(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                   const uint32_t* pos, const double* inv, int sweeps, const double* v,
+                   double* y) {
+    if (sweeps <= 1) {
+        scaled_spmv(rp, ci, vals, inv, v, y, n);
+        return;
+    }
+    /* z^1 = D^{-1} v, z^{j+1} = sweep(z^j), y = A z^sweeps */
+    double* z = (double*)malloc(sizeof(double) * (size_t)sweeps * (n ? n : 1));
+    for (uint32_t r = 0; r < n; ++r) z[r] = inv[r] * v[r];
+    for (int j = 1; j < sweeps; ++j)
+        jacobi_sweep(rp, ci, vals, pos, inv, v, z + (size_t)(j - 1) * n, z + (size_t)j * n, n);
+    orc_spmv_rows(rp, ci, vals, z + (size_t)(sweeps - 1) * n, y, 0, n);
+    free(z);
+}
+
+/* sstep.hpp:68-157 (shifted_terminal_rows, scaled_shifted_spmv_rows, SstepJacobiChain) run by
+ * run_chain_sequential (sstep.hpp:203-216) */
+int orc_sstep_jacobi_block(uint32_t n, const uint32_t* rp, const uint32_t* ci,
+                           const double* vals, const uint32_t* pos, const double* inv,
+                           int sweeps, const double* re, const double* im, int ns,
+                           double* block) {
+    if (ns < 1) return ORC_EINVAL;
+    if (orc_check_shift_chain(re, im, ns) != ORC_OK) return ORC_EINVAL;
+    double* z = (double*)malloc(sizeof(double) * (size_t)(sweeps > 1 ? sweeps : 1) * (n ? n : 1));
+    double* t = (double*)malloc(sizeof(double) * (n ? n : 1));
+    for (int p = 1; p <= ns; ++p) {
+        double a, b2;
+        shift_params(re, im, p, &a, &b2);
+        const double* src = block + (size_t)(p - 1) * n;
+        const double* src2 = p >= 2 ? block + (size_t)(p - 2) * n : NULL;
+        double* dst = block + (size_t)p * n;
+        const double* zin;
+        if (sweeps <= 1) {
+            scaled_spmv(rp, ci, vals, inv, src, t, n); /* acc of scaled_shifted_spmv_rows */
+            for (uint32_t r = 0; r < n; ++r)
+                dst[r] = b2 == 0.0 ? t[r] - a * src[r] : t[r] - a * src[r] + b2 * src2[r];
+            continue;
+        }
+        for (uint32_t r = 0; r < n; ++r) z[r] = inv[r] * src[r];
+        for (int j = 1; j < sweeps; ++j)
+            jacobi_sweep(rp, ci, vals, pos, inv, src, z + (size_t)(j - 1) * n, z + (size_t)j * n, n);
+        zin = z + (size_t)(sweeps - 1) * n;
+        orc_spmv_rows(rp, ci, vals, zin, t, 0, n);
+        for (uint32_t r = 0; r < n; ++r)
+            dst[r] = b2 == 0.0 ? t[r] - a * src[r] : t[r] - a * src[r] + b2 * src2[r];
+    }
+    free(z);
+    free(t);
+    return ORC_OK;
+}

@@ -98,6 +98,39 @@ int orc_mpk_shifted(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx
  * k = 1..d ascending, each a multiply then an add, over a power block from orc_baseline_mpk. */
 void orc_poly_combine(uint32_t n, const double* block, const double* c, int d, double* z);
 
+/* ---- Jacobi-preconditioned chains ------------------------------------ */
+#define ORC_ERUNTIME 2 /* std::runtime_error (missing / zero diagonal) */
+#define ORC_NO_DIAG 0xffffffffu /* csr.hpp:231 kNoDiag */
+
+/* csr.hpp:233-243 diagonal_positions + jacobi.hpp:48-64 build_diag_info: pos[r] = index of
+ * A(r,r) in col_idx (ORC_NO_DIAG if absent), inv[r] = 1.0 / A(r,r).  ORC_EINVAL if not square,
+ * ORC_ERUNTIME (row in *bad_row) if a diagonal is missing or zero. */
+int orc_diag_info(uint32_t n_rows, uint32_t n_cols, const uint32_t* row_ptr,
+                  const uint32_t* col_idx, const double* values, uint32_t* pos, double* inv,
+                  uint32_t* bad_row);
+
+/* jacobi.hpp:155-174 jacobi_apply: z = M^{-1} v with `sweeps` zero-guess Jacobi sweeps. */
+void orc_jacobi_apply(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                      const double* values, const uint32_t* pos, const double* inv, int sweeps,
+                      const double* v, double* z);
+
+/* jacobi.hpp:177-192 jacobi_op (== jacobi_op_blocked, jacobi.hpp:196-209): y = A (M^{-1} v)
+ * through the chain stages of JacobiOpChain (jacobi.hpp:120-149). */
+void orc_jacobi_op(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                   const double* values, const uint32_t* pos, const double* inv, int sweeps,
+                   const double* v, double* y);
+
+/* sstep.hpp:122-157 SstepJacobiChain run in order (sstep.hpp:203-216 run_chain_sequential,
+ * the ordered twin of the blocked executor): w_p = (A M^{-1} - a_p) w_{p-1} (+ b2_p w_{p-2}),
+ * p = 1..ns; block slice 0 holds the start vector on entry.  ORC_EINVAL for a bad shift chain.
+ * sstep.hpp needs Eigen (absent here), so this chain is pinned by composition: with zero shifts
+ * it is jacobi_op applied ns times (pinned against the compiled jacobi.hpp) and its terminal is
+ * mpk.hpp's shifted row formula (pinned through orc_baseline_mpk_shifted). */
+int orc_sstep_jacobi_block(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                           const double* values, const uint32_t* pos, const double* inv,
+                           int sweeps, const double* re, const double* im, int ns,
+                           double* block);
+
 /* mpk.hpp:219-233: argmax over the table, ties toward the smaller p. */
 int orc_tune_select(const double* gflops, int p_lo, int p_hi);
 

@@ -62,10 +62,15 @@ class Oracle:
             "orc_mpk_shifted": [u32, P, P, P, P, u32, i32, P, P, P, i32, P],
             "orc_poly_combine": [u32, P, P, i32, P],
             "orc_tune_select": [P, i32, i32],
+            "orc_diag_info": [u32, u32, P, P, P, P, P, P],
+            "orc_jacobi_apply": [u32, P, P, P, P, P, i32, P, P],
+            "orc_jacobi_op": [u32, P, P, P, P, P, i32, P, P],
+            "orc_sstep_jacobi_block": [u32, P, P, P, P, P, i32, P, P, i32, P],
         }
         res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
                "orc_wavefront_schedule": u64, "orc_permute_vector": None,
-               "orc_unpermute_vector": None, "orc_poly_combine": None}
+               "orc_unpermute_vector": None, "orc_poly_combine": None,
+               "orc_jacobi_apply": None, "orc_jacobi_op": None}
         for k, v in sig.items():
             f = getattr(L, k)
             f.argtypes = v
@@ -185,6 +190,49 @@ class Oracle:
         t = _f64(table)
         return self.lib.orc_tune_select(_p(t), p_lo, p_hi)
 
+    # ---- Jacobi chains (jacobi.hpp, sstep.hpp:122-157) ------------------------------------------
+    def diag_info(self, rp, ci, v, n_cols=None):
+        """(pos, inv); raises ValueError (not square) / RuntimeError (missing or zero diagonal)."""
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        n = len(rp) - 1
+        pos, inv, bad = np.empty(n, np.uint32), np.empty(n), np.zeros(1, np.uint32)
+        rc = self.lib.orc_diag_info(n, n if n_cols is None else n_cols, _p(rp), _p(ci), _p(v),
+                                    _p(pos), _p(inv), _p(bad))
+        if rc == 1:
+            raise ValueError("jacobi_setup: matrix must be square")
+        if rc == 2:
+            raise RuntimeError(f"jacobi_setup: missing or zero diagonal entry at row {int(bad[0])}")
+        return pos, inv
+
+    def jacobi_apply(self, rp, ci, v, sweeps, x):
+        pos, inv = self.diag_info(rp, ci, v)
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        z = np.empty(len(rp) - 1)
+        self.lib.orc_jacobi_apply(len(rp) - 1, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), sweeps,
+                                  _p(x), _p(z))
+        return z
+
+    def jacobi_op(self, rp, ci, v, sweeps, x):
+        pos, inv = self.diag_info(rp, ci, v)
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        y = np.empty(len(rp) - 1)
+        self.lib.orc_jacobi_op(len(rp) - 1, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), sweeps,
+                               _p(x), _p(y))
+        return y
+
+    def sstep_jacobi_block(self, rp, ci, v, sweeps, x, shifts):
+        pos, inv = self.diag_info(rp, ci, v)
+        re, im = self._shifts(shifts)
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        n, s = len(rp) - 1, len(re)
+        blk = np.empty((s + 1) * n)
+        blk[:n] = x
+        rc = self.lib.orc_sstep_jacobi_block(n, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), sweeps,
+                                             _p(re), _p(im), s, _p(blk))
+        if rc:
+            raise ValueError("sstep_jacobi_block: bad shift chain")
+        return blk.reshape(s + 1, n)
+
 
 class Reference:
     """The reference's own header-only implementation, compiled in place (OpenMP)."""
@@ -222,6 +270,10 @@ class Reference:
             "ref_check_shift_chain": ([P, P, i32], C.c_int),
             "ref_tune_select": ([P, i32, i32], C.c_int),
             "ref_resolve_threads": ([i32], C.c_int),
+            "ref_jacobi_setup": ([u32, P, P, P, i32, P, P], C.c_int),
+            "ref_jacobi_apply": ([u32, P, P, P, i32, P, P], C.c_int),
+            "ref_jacobi_op": ([u32, P, P, P, i32, P, P], C.c_int),
+            "ref_jacobi_op_blocked": ([u32, P, P, P, i32, P, u32, P, P, i32], C.c_int),
             "ref_last_error": ([], C.c_char_p),
         }
         for k, (a, r) in sig.items():
@@ -354,6 +406,44 @@ class Reference:
 
     def resolve_threads(self, requested=0):
         return self.lib.ref_resolve_threads(requested)
+
+    def _raise(self, rc):
+        msg = self.lib.ref_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+    def jacobi_setup(self, rp, ci, v, sweeps=1):
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        n = len(rp) - 1
+        pos, inv = np.empty(n, np.uint32), np.empty(n)
+        rc = self.lib.ref_jacobi_setup(n, _p(rp), _p(ci), _p(v), sweeps, _p(pos), _p(inv))
+        if rc:
+            self._raise(rc)
+        return pos, inv
+
+    def jacobi_apply(self, rp, ci, v, sweeps, x):
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        z = np.empty(len(rp) - 1)
+        rc = self.lib.ref_jacobi_apply(len(rp) - 1, _p(rp), _p(ci), _p(v), sweeps, _p(x), _p(z))
+        if rc:
+            self._raise(rc)
+        return z
+
+    def jacobi_op(self, rp, ci, v, sweeps, x):
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        y = np.empty(len(rp) - 1)
+        rc = self.lib.ref_jacobi_op(len(rp) - 1, _p(rp), _p(ci), _p(v), sweeps, _p(x), _p(y))
+        if rc:
+            self._raise(rc)
+        return y
+
+    def jacobi_op_blocked(self, rp, ci, v, sweeps, group_rows, x, threads=0):
+        rp, ci, v, x, gr = _u32(rp), _u32(ci), _f64(v), _f64(x), _u32(group_rows)
+        y = np.empty(len(rp) - 1)
+        rc = self.lib.ref_jacobi_op_blocked(len(rp) - 1, _p(rp), _p(ci), _p(v), sweeps, _p(gr),
+                                            len(gr) - 1, _p(x), _p(y), threads)
+        if rc:
+            self._raise(rc)
+        return y
 
 
 def reference_available() -> bool:

@@ -17,6 +17,7 @@
 #include "mpk/csr.hpp"
 #include "mpk/execute.hpp"
 #include "mpk/generators.hpp"
+#include "mpk/jacobi.hpp"
 #include "mpk/levels.hpp"
 #include "mpk/mpk.hpp"
 #include "mpk/plan.hpp"
@@ -280,5 +281,53 @@ int ref_tune_select(const double* table, int p_lo, int p_hi) {
 }
 
 int ref_resolve_threads(int requested) { return mpk::resolve_threads(requested); }
+
+// jacobi.hpp: setup, preconditioner apply, A M^{-1} v sequential and
+// cache-blocked (plan with sub_powers = JacobiOpChain::stages(sweeps)).
+int ref_jacobi_setup(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
+                     int sweeps, uint32_t* pos, double* inv) {
+    return guard([&] {
+        const auto A = wrap(n, rp, ci, v);
+        const mpk::JacobiPrecon P = mpk::jacobi_setup(A, sweeps);
+        std::memcpy(pos, P.diag.pos.data(), sizeof(uint32_t) * n);
+        std::memcpy(inv, P.diag.inv.data(), sizeof(double) * n);
+    });
+}
+
+int ref_jacobi_apply(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
+                     int sweeps, const double* x, double* z) {
+    return guard([&] {
+        const auto A = wrap(n, rp, ci, v);
+        const mpk::JacobiPrecon P = mpk::jacobi_setup(A, sweeps);
+        std::vector<double> out;
+        mpk::jacobi_apply(P, A, std::vector<double>(x, x + n), out, 1);
+        std::memcpy(z, out.data(), sizeof(double) * n);
+    });
+}
+
+int ref_jacobi_op(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
+                  int sweeps, const double* x, double* y) {
+    return guard([&] {
+        const auto A = wrap(n, rp, ci, v);
+        const mpk::JacobiPrecon P = mpk::jacobi_setup(A, sweeps);
+        std::vector<double> out;
+        mpk::jacobi_op(P, A, std::vector<double>(x, x + n), out, 1);
+        std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
+
+int ref_jacobi_op_blocked(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
+                          int sweeps, const uint32_t* group_rows, uint32_t ng, const double* x,
+                          double* y, int threads) {
+    return guard([&] {
+        const auto A = wrap(n, rp, ci, v);
+        const mpk::JacobiPrecon P = mpk::jacobi_setup(A, sweeps);
+        auto plan = plan_from(n, group_rows, ng, 1);
+        plan.sub_powers = mpk::detail::JacobiOpChain::stages(sweeps);
+        std::vector<double> out;
+        mpk::jacobi_op_blocked(P, A, plan, std::vector<double>(x, x + n), out, threads);
+        std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
 
 }  // extern "C"

@@ -93,6 +93,20 @@ def main():
     put("shift.poisson2d_30", rp=rp, ci=ci, v=v, perm=pm, level_ptr=lp, x=x, shifts=np.array(sh),
         group_rows=gr, block=R.mpk_shifted(prp, pci, pv, gr, len(sh), x, sh))
 
+    # --- Jacobi chains (jacobi.hpp) ----------------------------------------
+    for name, args in {"random_spd_400_5_9": (5, 400, 5, 0, 9), "poisson2d_17x13": (2, 17, 13)}.items():
+        rp, ci, v = R.gen(*args)
+        lv, pm, ip, lp = R.build_levels(rp, ci, v)
+        prp, pci, pv = R.permute(rp, ci, v, pm)
+        x = np.cos(0.23 * np.arange(len(rp) - 1)) + 0.25
+        for sw in (1, 2, 4):
+            pos, inv = R.jacobi_setup(prp, pci, pv, sw)
+            gr, _, _, _ = R.group_levels(prp, pci, pv, lp, 16 * 1024, 1)
+            put(f"jac.{name}_s{sw}", prp=prp, pci=pci, pv=pv, x=x, pos=pos, inv=inv,
+                group_rows=gr, apply=R.jacobi_apply(prp, pci, pv, sw, x),
+                op=R.jacobi_op(prp, pci, pv, sw, x),
+                op_blocked=R.jacobi_op_blocked(prp, pci, pv, sw, gr, x))
+
     # acceptance.cpp:84-90 random_vector(n, 42)
     put("rv", x=R.random_vector(1000, 42))
     np.savez_compressed(OUT, **g)

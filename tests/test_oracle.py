@@ -161,3 +161,66 @@ def test_oracle_vs_reference_fresh(oracle, ref):
             gr = oracle.group_levels(a[3], po[0], 256 * 1024, p)
             np.testing.assert_array_equal(gr[0], ref.group_levels(*pr, a[3], 256 * 1024, p)[0])
             assert_bitwise(oracle.mpk(*po, gr[0], p, x, p), ref.mpk(*pr, gr[0], p, x, p, threads=4))
+
+
+# ---- Jacobi chains (jacobi.hpp) -------------------------------------------
+JAC_CASES = [f"{m}_s{s}" for m in ("random_spd_400_5_9", "poisson2d_17x13") for s in (1, 2, 4)]
+
+
+@pytest.mark.parametrize("name", JAC_CASES)
+def test_jacobi_matches_golden(oracle, golden, name):
+    g = lambda k: golden[f"jac.{name}.{k}"]
+    sw = int(name.rsplit("_s", 1)[1])
+    pos, inv = oracle.diag_info(g("prp"), g("pci"), g("pv"))
+    np.testing.assert_array_equal(pos, g("pos"))
+    assert_bitwise(inv, g("inv"))
+    assert_bitwise(oracle.jacobi_apply(g("prp"), g("pci"), g("pv"), sw, g("x")), g("apply"))
+    y = oracle.jacobi_op(g("prp"), g("pci"), g("pv"), sw, g("x"))
+    assert_bitwise(y, g("op"))
+    assert_bitwise(y, g("op_blocked"))  # jacobi.hpp:196: the blocked twin is bitwise equal
+
+
+def test_jacobi_setup_errors(oracle):
+    # jacobi.hpp:48-64: non-square -> invalid_argument; missing / zero diagonal -> runtime_error
+    with pytest.raises(ValueError):
+        oracle.diag_info([0, 1], [0], [1.0], n_cols=2)
+    with pytest.raises(RuntimeError):
+        oracle.diag_info([0, 1, 2], [1, 0], [1.0, 1.0])  # no diagonal at all
+    with pytest.raises(RuntimeError):
+        oracle.diag_info([0, 1, 2], [0, 1], [2.0, 0.0])  # zero diagonal
+
+
+def test_sstep_jacobi_chain_composition(oracle, golden):
+    """The s-step Jacobi chain (sstep.hpp:122-157, which needs Eigen and cannot be compiled here)
+    is pinned by composition: zero shifts give jacobi_op applied s times (pinned above against
+    the compiled jacobi.hpp), and the shift terms follow mpk.hpp's shifted rows."""
+    g = lambda k: golden[f"jac.random_spd_400_5_9_s2.{k}"]
+    rp, ci, v, x = g("prp"), g("pci"), g("pv"), g("x")
+    for sw in (1, 2, 3):
+        blk = oracle.sstep_jacobi_block(rp, ci, v, sw, x, [0.0] * 4)
+        y = x.copy()
+        for p in range(1, 5):
+            y = oracle.jacobi_op(rp, ci, v, sw, y)
+            assert_bitwise(blk[p], y, f"sweeps={sw} p={p}")
+        sh = [0.5, 1.5 + 0.5j, 1.5 - 0.5j, 2.0]
+        blk = oracle.sstep_jacobi_block(rp, ci, v, sw, x, sh)
+        w = [x]
+        for p, s in enumerate(sh, 1):
+            t = oracle.jacobi_op(rp, ci, v, sw, w[p - 1])
+            b2 = s.imag ** 2 if s.imag < 0 else 0.0
+            nxt = t - s.real * w[p - 1]
+            if b2 != 0.0:
+                nxt = nxt + b2 * w[p - 2]
+            w.append(nxt)
+            assert_bitwise(blk[p], nxt, f"shifted sweeps={sw} p={p}")
+    with pytest.raises(ValueError):
+        oracle.sstep_jacobi_block(rp, ci, v, 1, x, [1.0 - 1.0j, 1.0 + 1.0j])
+
+
+def test_jacobi_oracle_vs_reference_fresh(oracle, ref):
+    for args in [(5, 3000, 6, 0, 4), (3, 8, 9, 10), (4, 700, 5, 0, 8)]:
+        rp, ci, v = ref.gen(*args)
+        x = ref.random_vector(len(rp) - 1, 42)
+        for sw in (1, 3):
+            assert_bitwise(oracle.jacobi_apply(rp, ci, v, sw, x), ref.jacobi_apply(rp, ci, v, sw, x))
+            assert_bitwise(oracle.jacobi_op(rp, ci, v, sw, x), ref.jacobi_op(rp, ci, v, sw, x))
