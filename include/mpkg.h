@@ -56,6 +56,7 @@ typedef struct mpkg_ctx_s* mpkg_ctx_t;
 typedef struct mpkg_csr_s* mpkg_csr_t;
 typedef struct mpkg_levels_s* mpkg_levels_t;
 typedef struct mpkg_plan_s* mpkg_plan_t;
+typedef struct mpkg_jacobi_s* mpkg_jacobi_t;
 typedef struct mpkg_host_csr_s* mpkg_host_csr_t;
 
 /* ---- errors / version ------------------------------------------------------------------- */
@@ -216,6 +217,41 @@ int mpkg_tune_p(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A_perm, uint64_t cac
                 int p_lo, int p_hi, int reps, int* p_opt, double* gflops_table);
 /* mpk.hpp:219-233 tune_p(trial) selection rule over a given throughput table. */
 int mpkg_tune_select(const double* gflops_table, int p_lo, int p_hi, int* p_opt);
+
+/* ---- Jacobi-preconditioned chains (jacobi.hpp, sstep.hpp:68-157) ------
+ * Bitwise equal to the reference's sequential and cache-blocked paths (same per-row formulas,
+ * stored-order sums, no FMA). */
+/* jacobi.hpp:48-76 build_diag_info + jacobi_setup: EINVAL (not square, sweeps < 1),
+ * EINTERNAL = std::runtime_error (missing / zero diagonal: first failing row in the message). */
+int mpkg_jacobi_setup(mpkg_ctx_t ctx, mpkg_csr_t A, int sweeps, mpkg_jacobi_t* out);
+int mpkg_jacobi_info(mpkg_jacobi_t J, uint32_t* n, int* sweeps);
+/* DiagInfo (jacobi.hpp:41-44): pos[n] (0xffffffff = kNoDiag), inv[n]; either may be NULL. */
+int mpkg_jacobi_get(mpkg_jacobi_t J, uint32_t* pos, double* inv);
+int mpkg_jacobi_destroy(mpkg_jacobi_t J);
+/* jacobi.hpp:155-174 jacobi_apply: z = M^{-1} v. */
+int mpkg_jacobi_apply(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* v, double* z);
+int mpkg_jacobi_apply_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* d_v,
+                          double* d_z);
+/* jacobi.hpp:177-192 jacobi_op: y = A (M^{-1} v). */
+int mpkg_jacobi_op(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* v, double* y);
+int mpkg_jacobi_op_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* d_v,
+                       double* d_y);
+/* jacobi.hpp:196-209 jacobi_op_blocked: the plan must match A_perm and carry
+ * sub_powers == (sweeps == 1 ? 1 : sweeps + 1) (EINVAL otherwise). */
+int mpkg_jacobi_op_blocked(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A_perm,
+                           const double* v, double* y);
+int mpkg_jacobi_op_blocked_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P,
+                               mpkg_csr_t A_perm, const double* d_v, double* d_y);
+/* sstep.hpp:356-385 sstep_generate_block, Jacobi case: block slice 0 holds the start vector on
+ * entry; slices 1..s receive w_p = (A M^{-1} - a_p) w_{p-1} (+ b2_p w_{p-2}), b2_p = im_p^2 for
+ * the second member of a conjugate pair.  P may be NULL (sequential form); otherwise it must
+ * match A, carry the chain's sub_powers and a power budget >= s (execute.hpp:81-83). */
+int mpkg_sstep_jacobi(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                      const double* re, const double* im, int s, double* block,
+                      uint64_t block_rows, uint64_t block_slices);
+int mpkg_sstep_jacobi_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                          const double* re, const double* im, int s, double* d_block,
+                          uint64_t block_rows, uint64_t block_slices);
 
 /* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
 /* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]

@@ -66,6 +66,10 @@ struct PlanHolder {
     mpkg_plan_t h = nullptr;
     ~PlanHolder() { mpkg_plan_destroy(h); }
 };
+struct JacobiHolder {
+    mpkg_jacobi_t h = nullptr;
+    ~JacobiHolder() { mpkg_jacobi_destroy(h); }
+};
 
 }  // namespace detail
 
@@ -433,7 +437,8 @@ inline void baseline_mpk(const CsrMatrix& A, const std::vector<double>& x, int p
                                     block.data.data(), block.rows, block.slices));
 }
 
-/// mpk.hpp:81-106 (one fused, temporally blocked GPU launch)
+/// mpk.hpp:81-106 (GPU executor: one launch per power, or the fused tile-DAG kernel for
+/// matrices with long rows)
 inline void mpk(const ExecutionPlan& plan, const CsrMatrix& A_perm, const std::vector<double>& x,
                 int p_m, VectorBlock& block, int /*threads*/ = 0) {
     if (x.size() != A_perm.n_rows) throw std::invalid_argument("mpk: input size mismatch");
@@ -491,6 +496,93 @@ inline std::vector<double> mpk_poly(const ExecutionPlan& plan, const CsrMatrix& 
     detail::check(mpkg_mpk_poly(device_context(), plan.device(), A_perm.device(), x.data(),
                                 c.data(), static_cast<int>(c.size()) - 1, z.data(), nullptr, 0, 0));
     return z;
+}
+
+// ---- jacobi.hpp / csr.hpp:231-243 -----------------------------------------
+/// csr.hpp:231
+inline constexpr index_t kNoDiag = 0xffffffffu;
+
+/// csr.hpp:233-243 (host)
+inline std::vector<index_t> diagonal_positions(const CsrMatrix& A) {
+    std::vector<index_t> pos(A.n_rows, kNoDiag);
+    for (index_t r = 0; r < A.n_rows && r < A.n_cols; ++r) {
+        const auto b = A.col_idx.begin() + A.row_ptr[r], e = A.col_idx.begin() + A.row_ptr[r + 1];
+        const auto it = std::lower_bound(b, e, r);
+        if (it != e && *it == r) pos[r] = static_cast<index_t>(it - A.col_idx.begin());
+    }
+    return pos;
+}
+
+/// jacobi.hpp:41-44
+struct DiagInfo {
+    std::vector<index_t> pos;
+    std::vector<double> inv;
+};
+
+/// jacobi.hpp:66-69; the diagonal data also lives on the device (built by jacobi_setup).
+struct JacobiPrecon {
+    DiagInfo diag;
+    int sweeps = 1;
+    mpkg_jacobi_t device() const {
+        if (!dev_) throw std::invalid_argument("JacobiPrecon: not built by jacobi_setup");
+        return dev_->h;
+    }
+    std::shared_ptr<detail::JacobiHolder> dev_;
+};
+
+/// jacobi.hpp:71-75 (+ build_diag_info 48-64): std::invalid_argument / std::runtime_error.
+inline JacobiPrecon jacobi_setup(const CsrMatrix& a, int sweeps = 1) {
+    JacobiPrecon p;
+    p.sweeps = sweeps;
+    auto d = std::make_shared<detail::JacobiHolder>();
+    detail::check(mpkg_jacobi_setup(device_context(), a.device(), sweeps, &d->h));
+    p.diag.pos.resize(a.n_rows);
+    p.diag.inv.resize(a.n_rows);
+    detail::check(mpkg_jacobi_get(d->h, p.diag.pos.data(), p.diag.inv.data()));
+    p.dev_ = d;
+    return p;
+}
+
+/// jacobi.hpp:155-174
+inline void jacobi_apply(const JacobiPrecon& p, const CsrMatrix& a, const std::vector<double>& v,
+                         std::vector<double>& z, int /*threads*/ = 0) {
+    if (v.size() != a.n_rows) throw std::invalid_argument("jacobi_apply: size mismatch");
+    z.resize(a.n_rows);
+    detail::check(mpkg_jacobi_apply(device_context(), p.device(), a.device(), v.data(), z.data()));
+}
+
+/// jacobi.hpp:177-192
+inline void jacobi_op(const JacobiPrecon& p, const CsrMatrix& a, const std::vector<double>& v,
+                      std::vector<double>& y, int /*threads*/ = 0) {
+    if (v.size() != a.n_rows) throw std::invalid_argument("jacobi_op: size mismatch");
+    y.resize(a.n_rows);
+    detail::check(mpkg_jacobi_op(device_context(), p.device(), a.device(), v.data(), y.data()));
+}
+
+/// jacobi.hpp:196-209 (plan.sub_powers must be JacobiOpChain::stages(sweeps))
+inline void jacobi_op_blocked(const JacobiPrecon& p, const CsrMatrix& a_perm,
+                              const ExecutionPlan& plan, const std::vector<double>& v,
+                              std::vector<double>& y, int /*threads*/ = 0) {
+    if (v.size() != a_perm.n_rows) throw std::invalid_argument("jacobi_op_blocked: size mismatch");
+    y.resize(a_perm.n_rows);
+    detail::check(mpkg_jacobi_op_blocked(device_context(), p.device(), plan.device(), a_perm.device(),
+                                         v.data(), y.data()));
+}
+
+/// jacobi.hpp:129 JacobiOpChain::stages
+inline int jacobi_stages(int sweeps) { return sweeps == 1 ? 1 : sweeps + 1; }
+
+/// sstep.hpp:356-385 sstep_generate_block, Jacobi case: w.slice(0) holds the start vector on
+/// entry; slices 1..shifts.size() receive the Jacobi-preconditioned Newton basis.  `plan` may
+/// be null (sequential form) or carry sub_powers == jacobi_stages(sweeps).
+inline void sstep_jacobi_block(const JacobiPrecon& p, const CsrMatrix& a,
+                               const std::vector<std::complex<double>>& shifts, VectorBlock& w,
+                               const ExecutionPlan* plan = nullptr) {
+    std::vector<double> re, im;
+    detail::split(shifts, re, im);
+    detail::check(mpkg_sstep_jacobi(device_context(), p.device(), plan ? plan->device() : nullptr,
+                                    a.device(), re.data(), im.data(), static_cast<int>(shifts.size()),
+                                    w.data.data(), w.rows, w.slices));
 }
 
 /// mpk.hpp:211-215

@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     DeviceCsr,
     ExecutionPlan,
     HostCsr,
+    JacobiPrecon,
     LevelStructure,
     ScheduleCell,
     TuneResult,

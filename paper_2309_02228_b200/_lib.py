@@ -56,6 +56,18 @@ _SIGS = {
     "mpkg_plan_destroy": [P],
     "mpkg_plan_exec_info": [P, pu32, pu64, pu64, pu32],
     "mpkg_plan_exec_mode": [P, pint, pint, pint, pu64],
+    "mpkg_jacobi_setup": [P, P, i32, C.POINTER(P)],
+    "mpkg_jacobi_info": [P, pu32, pint],
+    "mpkg_jacobi_get": [P, P, P],
+    "mpkg_jacobi_destroy": [P],
+    "mpkg_jacobi_apply": [P, P, P, P, P],
+    "mpkg_jacobi_apply_dev": [P, P, P, P, P],
+    "mpkg_jacobi_op": [P, P, P, P, P],
+    "mpkg_jacobi_op_dev": [P, P, P, P, P],
+    "mpkg_jacobi_op_blocked": [P, P, P, P, P, P],
+    "mpkg_jacobi_op_blocked_dev": [P, P, P, P, P, P],
+    "mpkg_sstep_jacobi": [P, P, P, P, P, P, i32, P, u64, u64],
+    "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],
     "mpkg_baseline_mpk": [P, P, P, i32, P, u64, u64],
     "mpkg_baseline_mpk_dev": [P, P, P, i32, P, u64, u64],

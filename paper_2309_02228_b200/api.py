@@ -260,6 +260,29 @@ class LevelStructure:
             self.h = None
 
 
+class JacobiPrecon:
+    """jacobi.hpp:41-76: DiagInfo (pos, inv) + sweeps, resident on the device."""
+
+    def __init__(self, ctx: "Context", h: int):
+        self.ctx, self.h = ctx, h
+        n, sw = C.c_uint32(), C.c_int()
+        check(lib.mpkg_jacobi_info(h, C.byref(n), C.byref(sw)))
+        self.n_rows, self.sweeps = n.value, sw.value
+
+    def diag(self):
+        pos, inv = np.empty(self.n_rows, np.uint32), np.empty(self.n_rows)
+        check(lib.mpkg_jacobi_get(self.h, _ptr(pos), _ptr(inv)))
+        return pos, inv
+
+    def stages(self) -> int:  # jacobi.hpp:129 JacobiOpChain::stages
+        return 1 if self.sweeps == 1 else self.sweeps + 1
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.mpkg_jacobi_destroy(self.h)
+            self.h = None
+
+
 class ExecutionPlan:
     """plan.hpp:41-54."""
 
@@ -280,6 +303,35 @@ class ExecutionPlan:
 
     def n_groups(self) -> int:
         return len(self.group_rows) - 1
+
+    @staticmethod
+    def from_groups(n_rows: int, group_rows, p_m: int, sub_powers: int = 1, level_ptr=None,
+                    cache_bytes: int = 0) -> "ExecutionPlan":
+        """A plan from host fields (plan.hpp:41-54), e.g. one made by hand as in the reference's
+        schedule tests (mpkg_plan_create)."""
+        gr = _u32(group_rows)
+        ng = len(gr) - 1
+        lp = None if level_ptr is None else _u32(level_ptr)
+        glp = np.zeros(ng + 1, np.uint32)
+        fp = np.zeros(max(ng, 1), np.uint64)
+        h = _P()
+        check(lib.mpkg_plan_create(p_m, sub_powers, n_rows, cache_bytes, cache_bytes // (p_m + 1), ng,
+                                   _ptr(gr), _ptr(glp), _ptr(fp), 0 if lp is None else len(lp) - 1,
+                                   _ptr(lp) if lp is not None else None, C.byref(h)))
+        return ExecutionPlan(h.value)
+
+    def with_sub_powers(self, sub_powers: int, level_ptr=None) -> "ExecutionPlan":
+        """A copy with another sub_powers (chains: the reference sets plan.sub_powers by hand,
+        e.g. JacobiOpChain::stages(sweeps) for jacobi_op_blocked / the s-step chains)."""
+        h = _P()
+        lp = None if level_ptr is None else _u32(level_ptr)
+        check(lib.mpkg_plan_create(self.p_m, sub_powers, self.n_rows, self.cache_bytes,
+                                   self.target_bytes, self.n_groups(), _ptr(self.group_rows),
+                                   _ptr(self.group_level_ptr),
+                                   _ptr(self.group_footprint) if self.n_groups() else None,
+                                   0 if lp is None else len(lp) - 1, _ptr(lp) if lp is not None else None,
+                                   C.byref(h)))
+        return ExecutionPlan(h.value)
 
     def exec_info(self) -> dict:
         t, k, d, pp = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
@@ -503,6 +555,41 @@ class Context:
         c = _f64(coef)
         check(lib.mpkg_mpk_poly_dev(self.h, plan.h, A_perm.h, d_x, _ptr(c), len(c) - 1, d_z,
                                     d_block, rows, slices))
+
+    # ---- Jacobi-preconditioned chains (jacobi.hpp, sstep.hpp) ----------------------------------
+    def jacobi_setup(self, A: DeviceCsr, sweeps: int = 1) -> JacobiPrecon:  # jacobi.hpp:72
+        h = _P()
+        check(lib.mpkg_jacobi_setup(self.h, A.h, int(sweeps), C.byref(h)))
+        return JacobiPrecon(self, h.value)
+
+    def jacobi_apply(self, J: JacobiPrecon, A: DeviceCsr, v) -> np.ndarray:  # jacobi.hpp:155
+        v = _f64(v)
+        z = np.empty(A.n_rows)
+        check(lib.mpkg_jacobi_apply(self.h, J.h, A.h, _ptr(v), _ptr(z)))
+        return z
+
+    def jacobi_op(self, J: JacobiPrecon, A: DeviceCsr, v) -> np.ndarray:  # jacobi.hpp:177
+        v = _f64(v)
+        y = np.empty(A.n_rows)
+        check(lib.mpkg_jacobi_op(self.h, J.h, A.h, _ptr(v), _ptr(y)))
+        return y
+
+    def jacobi_op_blocked(self, J: JacobiPrecon, plan: ExecutionPlan, A_perm: DeviceCsr, v):
+        v = _f64(v)  # jacobi.hpp:196
+        y = np.empty(A_perm.n_rows)
+        check(lib.mpkg_jacobi_op_blocked(self.h, J.h, plan.h, A_perm.h, _ptr(v), _ptr(y)))
+        return y
+
+    def sstep_jacobi(self, J: JacobiPrecon, plan, A: DeviceCsr, x, shifts) -> VectorBlock:
+        """sstep.hpp:356-385 (Jacobi): slice 0 = x, slices 1..s the preconditioned Newton basis."""
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        re, im = _f64(s.real), _f64(s.imag)
+        n, k = A.n_rows, len(re)
+        blk = VectorBlock(n, k + 1)
+        blk.data[:n] = _f64(x)
+        check(lib.mpkg_sstep_jacobi(self.h, J.h, plan.h if plan is not None else None, A.h,
+                                    _ptr(re), _ptr(im), k, _ptr(blk.data), n, k + 1))
+        return blk
 
     def tune_p(self, ls: LevelStructure, A_perm: DeviceCsr, cache_bytes: int, p_lo: int,
                p_hi: int, reps: int = 3) -> TuneResult:  # mpk.hpp:238

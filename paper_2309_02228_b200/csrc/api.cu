@@ -930,4 +930,157 @@ int mpkg_tune_p(mpkg_ctx_t ctx, mpkg_levels_t L, mpkg_csr_t A, uint64_t cache_by
     });
 }
 
+// ---- Jacobi-preconditioned chains (precon.cu) -------------------------------------------------
+int mpkg_jacobi_setup(mpkg_ctx_t ctx, mpkg_csr_t A, int sweeps, mpkg_jacobi_t* out) {
+    return guarded([&] {
+        require(ctx && A && out, "jacobi_setup: null argument");
+        require(sweeps >= 1, "jacobi_setup: sweeps must be >= 1");           // jacobi.hpp:73
+        require(A->n_rows == A->n_cols, "jacobi_setup: matrix must be square");  // jacobi.hpp:49
+        use_device(ctx);
+        auto J = std::make_unique<mpkg_jacobi_s>();
+        J->ctx = ctx;
+        J->device = ctx->device;
+        J->sweeps = sweeps;
+        gpu_jacobi_setup(ctx, A, J.get());
+        *out = J.release();
+    });
+}
+
+int mpkg_jacobi_info(mpkg_jacobi_t J, uint32_t* n, int* sweeps) {
+    return guarded([&] {
+        require(J != nullptr, "jacobi_info: null handle");
+        if (n) *n = J->n;
+        if (sweeps) *sweeps = J->sweeps;
+    });
+}
+
+int mpkg_jacobi_get(mpkg_jacobi_t J, uint32_t* pos, double* inv) {
+    return guarded([&] {
+        require(J != nullptr, "jacobi_get: null handle");
+        MPKG_CUDA(cudaSetDevice(J->device));
+        if (pos && J->n) MPKG_CUDA(cudaMemcpy(pos, J->pos.p, 4ull * J->n, cudaMemcpyDeviceToHost));
+        if (inv && J->n) MPKG_CUDA(cudaMemcpy(inv, J->inv.p, 8ull * J->n, cudaMemcpyDeviceToHost));
+    });
+}
+
+int mpkg_jacobi_destroy(mpkg_jacobi_t J) {
+    if (J) {
+        cudaSetDevice(J->device);
+        delete J;
+    }
+    return MPKG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+void jacobi_args(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const char* who) {
+    require(ctx && J && A, std::string(who) + ": null argument");
+    require(A->n_rows == A->n_cols, std::string(who) + ": matrix must be square");
+    require(A->n_rows == J->n, std::string(who) + ": size mismatch");  // jacobi.hpp:160 / 182
+    use_device(ctx);
+}
+
+void jacobi_plan(mpkg_plan_t P, mpkg_jacobi_t J, const char* who) {
+    require(P != nullptr, std::string(who) + ": null plan");
+    require(P->n_rows == J->n, std::string(who) + ": plan does not match matrix");
+    const int stages = J->sweeps == 1 ? 1 : J->sweeps + 1;  // jacobi.hpp:129 JacobiOpChain::stages
+    require(P->sub_powers == stages, std::string(who) + ": plan sub_powers mismatch");
+}
+
+template <class F>
+void host_vec(mpkg_ctx_s* ctx, uint32_t n, const double* in, double* out, F&& body) {
+    ctx->scratch_x.ensure(std::max<uint32_t>(n, 1));
+    ctx->scratch_block.ensure(std::max<uint32_t>(n, 1));
+    if (n) MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_x.p, in, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    body(ctx->scratch_x.p, ctx->scratch_block.p);
+    if (n) MPKG_CUDA(cudaMemcpyAsync(out, ctx->scratch_block.p, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void sstep_jacobi_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                      const double* re, const double* im, int s, double* d_block, uint64_t rows,
+                      uint64_t slices) {
+    jacobi_args(ctx, J, A, "sstep_gmres");
+    require(s >= 1, "sstep_gmres: s must be >= 1");
+    require(re && im, "sstep_gmres: null shifts");
+    require(rows == A->n_rows && slices >= (uint64_t)s + 1, "sstep_gmres: workspace too small");
+    shift_chain(re, im, s, "sstep_gmres");
+    if (P) {
+        jacobi_plan(P, J, "sstep_gmres");
+        require(s <= P->p_m, "execute: p_m exceeds the plan's power budget");  // execute.hpp:81-83
+    }
+    std::vector<double> a, b2;
+    shift_coeffs(re, im, s, a, b2);
+    gpu_sstep_jacobi(ctx, J, A, d_block, rows, s, a.data(), b2.data());
+}
+}  // namespace
+
+extern "C" {
+
+int mpkg_jacobi_apply(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* v, double* z) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_apply");
+        require(v && z, "jacobi_apply: null vector");
+        host_vec(ctx, J->n, v, z, [&](const double* dv, double* dz) { gpu_jacobi_apply(ctx, J, A, dv, dz); });
+    });
+}
+int mpkg_jacobi_apply_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* d_v, double* d_z) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_apply");
+        gpu_jacobi_apply(ctx, J, A, d_v, d_z);
+    });
+}
+int mpkg_jacobi_op(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* v, double* y) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_op");
+        require(v && y, "jacobi_op: null vector");
+        host_vec(ctx, J->n, v, y, [&](const double* dv, double* dy) { gpu_jacobi_op(ctx, J, A, dv, dy); });
+    });
+}
+int mpkg_jacobi_op_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_csr_t A, const double* d_v, double* d_y) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_op");
+        gpu_jacobi_op(ctx, J, A, d_v, d_y);
+    });
+}
+int mpkg_jacobi_op_blocked(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                           const double* v, double* y) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_op_blocked");
+        jacobi_plan(P, J, "jacobi_op_blocked");
+        require(v && y, "jacobi_op_blocked: null vector");
+        host_vec(ctx, J->n, v, y, [&](const double* dv, double* dy) { gpu_jacobi_op(ctx, J, A, dv, dy); });
+    });
+}
+int mpkg_jacobi_op_blocked_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                               const double* d_v, double* d_y) {
+    return guarded([&] {
+        jacobi_args(ctx, J, A, "jacobi_op_blocked");
+        jacobi_plan(P, J, "jacobi_op_blocked");
+        gpu_jacobi_op(ctx, J, A, d_v, d_y);
+    });
+}
+int mpkg_sstep_jacobi(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                      const double* re, const double* im, int s, double* block, uint64_t rows,
+                      uint64_t slices) {
+    return guarded([&] {
+        require(block != nullptr, "sstep_gmres: null block");
+        require(ctx && A, "sstep_gmres: null argument");
+        const uint64_t elems = rows * slices;
+        ctx->scratch_block.ensure(std::max<uint64_t>(elems, 1));
+        if (elems)
+            MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_block.p, block, 8ull * elems, cudaMemcpyHostToDevice, ctx->stream));
+        sstep_jacobi_dev(ctx, J, P, A, re, im, s, ctx->scratch_block.p, rows, slices);
+        if (elems)
+            MPKG_CUDA(cudaMemcpyAsync(block, ctx->scratch_block.p, 8ull * elems, cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int mpkg_sstep_jacobi_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
+                          const double* re, const double* im, int s, double* d_block, uint64_t rows,
+                          uint64_t slices) {
+    return guarded([&] { sstep_jacobi_dev(ctx, J, P, A, re, im, s, d_block, rows, slices); });
+}
+
 }  // extern "C"

@@ -141,6 +141,17 @@ struct mpkg_levels_s {
     mpkg_detail::DevBuf<uint32_t> d_level_ptr;
 };
 
+// Jacobi preconditioner (jacobi.hpp:41-76 DiagInfo + JacobiPrecon) on the device.
+struct mpkg_jacobi_s {
+    mpkg_ctx_s* ctx = nullptr;
+    int device = 0;
+    uint32_t n = 0;
+    int sweeps = 1;
+    mpkg_detail::DevBuf<uint32_t> pos;    // index of A(r,r) in col_idx (csr.hpp:233-243)
+    mpkg_detail::DevBuf<uint32_t> kdiag;  // the same inside its row (skip index of the sweep)
+    mpkg_detail::DevBuf<double> inv;      // 1 / A(r,r)
+};
+
 struct mpkg_plan_s {
     int p_m = 1;
     int sub_powers = 1;
@@ -197,6 +208,15 @@ void gpu_csr_block(mpkg_ctx_s* ctx, const mpkg_csr_s* A, uint32_t r0, uint32_t r
                    uint32_t c1, mpkg_csr_s* B);
 void gpu_gather_row_ptr(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_idx, uint32_t m,
                         uint32_t* h_out);
+
+// precon.cu
+void gpu_jacobi_setup(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_jacobi_s* J);
+void gpu_jacobi_apply(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, const double* d_v,
+                      double* d_z);
+void gpu_jacobi_op(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, const double* d_v,
+                   double* d_y);
+void gpu_sstep_jacobi(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, double* d_block,
+                      uint64_t rows, int ns, const double* a, const double* b2);
 
 // mpk_exec.cu
 struct FusedArgs {

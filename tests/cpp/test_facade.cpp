@@ -312,8 +312,109 @@ static void test_host_helpers() {
     EXPECT(mpk::resolve_threads() >= 1);
 }
 
+// proj/tests/test_relax.cpp:112-206 (Jacobi), with a small dense recurrence standing in for the
+// Eigen oracle of MultiSweepMatchesDenseOracle.
+static std::vector<double> dense_jacobi(const CsrMatrix& a, const std::vector<double>& v, int sweeps) {
+    const std::size_t n = a.n_rows;
+    std::vector<double> d(n), z(n), t(n);
+    for (index_t r = 0; r < a.n_rows; ++r)
+        for (index_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k)
+            if (a.col_idx[k] == r) d[r] = a.values[k];
+    for (std::size_t r = 0; r < n; ++r) z[r] = v[r] / d[r];
+    for (int s = 2; s <= sweeps; ++s) {
+        for (index_t r = 0; r < a.n_rows; ++r) {
+            long double acc = 0.0L;
+            for (index_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k)
+                if (a.col_idx[k] != r) acc += (long double)a.values[k] * z[a.col_idx[k]];
+            t[r] = (double)(((long double)v[r] - acc) / d[r]);
+        }
+        z.swap(t);
+    }
+    return z;
+}
+
+static void test_jacobi() {
+    {  // SetupRejectsBadInput
+        CsrMatrix a = mpk::poisson1d(4);
+        EXPECT_THROW(mpk::jacobi_setup(a, 0), std::invalid_argument);
+        CsrMatrix zd = mpk::from_coo(2, 2, {{0, 0, 0.0}, {0, 1, 1.0}, {1, 0, 1.0}, {1, 1, 2.0}});
+        EXPECT_THROW(mpk::jacobi_setup(zd, 1), std::runtime_error);
+        CsrMatrix md = mpk::from_coo(2, 2, {{0, 1, 1.0}, {1, 0, 1.0}, {1, 1, 2.0}});
+        EXPECT_THROW(mpk::jacobi_setup(md, 1), std::runtime_error);
+    }
+    {  // IdentityAndDiagonalExamples
+        CsrMatrix i2 = mpk::from_coo(2, 2, {{0, 0, 1.0}, {1, 1, 1.0}});
+        mpk::JacobiPrecon p = mpk::jacobi_setup(i2, 1);
+        std::vector<double> z;
+        mpk::jacobi_apply(p, i2, {5.0, -7.0}, z);
+        EXPECT(z[0] == 5.0 && z[1] == -7.0);
+        CsrMatrix d = mpk::from_coo(2, 2, {{0, 0, 2.0}, {1, 1, 4.0}});
+        mpk::JacobiPrecon pd = mpk::jacobi_setup(d, 1);
+        mpk::jacobi_apply(pd, d, {2.0, 4.0}, z);
+        EXPECT(z[0] == 1.0 && z[1] == 1.0);
+    }
+    {  // TwoSweepExample: A = [[2,1],[1,2]], v = (1,1), two sweeps -> (0.25, 0.25)
+        CsrMatrix a = mpk::from_coo(2, 2, {{0, 0, 2.0}, {0, 1, 1.0}, {1, 0, 1.0}, {1, 1, 2.0}});
+        mpk::JacobiPrecon p = mpk::jacobi_setup(a, 2);
+        std::vector<double> z;
+        mpk::jacobi_apply(p, a, {1.0, 1.0}, z);
+        EXPECT(z[0] == 0.25 && z[1] == 0.25);
+        EXPECT(p.diag.pos == mpk::diagonal_positions(a));
+    }
+    {  // MultiSweepMatchesDenseOracle
+        const CsrMatrix a = mpk::random_spd(40, 4, 123);
+        const std::vector<double> v = random_vector(40, 7);
+        for (int sweeps : {1, 2, 3, 4}) {
+            mpk::JacobiPrecon p = mpk::jacobi_setup(a, sweeps);
+            std::vector<double> z;
+            mpk::jacobi_apply(p, a, v, z);
+            const std::vector<double> want = dense_jacobi(a, v, sweeps);
+            double err = 0.0, scale = 0.0;
+            for (std::size_t i = 0; i < z.size(); ++i) {
+                err = std::max(err, std::fabs(z[i] - want[i]));
+                scale = std::max(scale, std::fabs(want[i]));
+            }
+            EXPECT(err <= 1e-14 * scale);
+        }
+    }
+    {  // OpEqualsApplyThenSpmvBitwise
+        const CsrMatrix a = mpk::random_spd(60, 5, 9);
+        const std::vector<double> v = random_vector(60, 11);
+        for (int sweeps : {1, 2, 3}) {
+            mpk::JacobiPrecon p = mpk::jacobi_setup(a, sweeps);
+            std::vector<double> z, want(a.n_rows), y;
+            mpk::jacobi_apply(p, a, v, z);
+            mpk::spmv(a, z, want);
+            mpk::jacobi_op(p, a, v, y);
+            EXPECT(bitwise_equal(want, y));
+        }
+    }
+    {  // BlockedOpBitwiseEqualsSequential
+        const CsrMatrix a = mpk::poisson2d(32, 32);
+        const std::vector<double> v = random_vector(a.n_rows, 21);
+        const LevelStructure ls = mpk::build_levels(a);
+        const CsrMatrix ap = mpk::permute(a, ls.perm);
+        for (int sweeps : {1, 3}) {
+            ExecutionPlan plan = mpk::group_levels(ls, ap, 64 * 1024, 1);
+            plan.sub_powers = mpk::jacobi_stages(sweeps);
+            plan.invalidate();
+            EXPECT(plan.n_groups() > 2u);
+            mpk::JacobiPrecon p = mpk::jacobi_setup(ap, sweeps);
+            std::vector<double> y_seq, y_blk;
+            mpk::jacobi_op(p, ap, v, y_seq);
+            mpk::jacobi_op_blocked(p, ap, plan, v, y_blk);
+            EXPECT(bitwise_equal(y_seq, y_blk));
+            ExecutionPlan bad = plan;
+            bad.sub_powers = 7;
+            bad.invalidate();
+            EXPECT_THROW(mpk::jacobi_op_blocked(p, ap, bad, v, y_blk), std::invalid_argument);
+        }
+    }
+}
+
 int main() {
     test_host_helpers();
+    test_jacobi();
     test_levels();
     test_wavefront();
     test_mpk();
