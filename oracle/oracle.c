@@ -520,3 +520,98 @@ int orc_sstep_jacobi_block(uint32_t n, const uint32_t* rp, const uint32_t* ci,
     free(t);
     return ORC_OK;
 }
+
+/* ---- GS2 (gs2.hpp) ------------------------------------------------------------------------------ */
+
+/* gs2.hpp:70-82 gs2_stage0_rows */
+static void gs2_stage0(const uint32_t* rp, const uint32_t* ci, const double* vals, const double* inv,
+                       const double* v, const double* z_prev, double* g0, double* z_next, uint32_t n) {
+    for (uint32_t r = 0; r < n; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) acc += vals[k] * z_prev[ci[k]];
+        const double g = inv[r] * (v[r] - acc);
+        g0[r] = g;
+        if (z_next) z_next[r] = z_prev[r] + g;
+    }
+}
+
+/* gs2.hpp:89-104 gs2_inner_rows */
+static void gs2_inner(const uint32_t* rp, const uint32_t* ci, const double* vals, const uint32_t* pos,
+                      const double* inv, const double* g0, const double* g_prev, double* g_out,
+                      int forward, const double* z_prev, double* z_next, uint32_t n) {
+    for (uint32_t r = 0; r < n; ++r) {
+        const uint32_t ks = forward ? rp[r] : pos[r] + 1;
+        const uint32_t ke = forward ? pos[r] : rp[r + 1];
+        double acc = 0.0;
+        for (uint32_t k = ks; k < ke; ++k) acc += vals[k] * g_prev[ci[k]];
+        const double g = g0[r] - inv[r] * acc;
+        g_out[r] = g;
+        if (z_next) z_next[r] = z_prev[r] + g;
+    }
+}
+
+/* gs2.hpp:108-116 residual_rows */
+static void gs2_residual(const uint32_t* rp, const uint32_t* ci, const double* vals, const double* v,
+                         const double* z, double* out, uint32_t n) {
+    for (uint32_t r = 0; r < n; ++r) {
+        double acc = 0.0;
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) acc += vals[k] * z[ci[k]];
+        out[r] = v[r] - acc;
+    }
+}
+
+/* one K-sweep GS2 from z[0] (slices z[0..K], g[0..gamma]) : gs2.hpp:126-158 in chain order */
+static void gs2_sweeps(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                       const uint32_t* pos, const double* inv, int gamma, int sweeps, int forward,
+                       const double* v, double* z, double* g) {
+    for (int p = 1; p <= sweeps; ++p) {
+        const double* z_prev = z + (size_t)(p - 1) * n;
+        double* z_next = z + (size_t)p * n;
+        gs2_stage0(rp, ci, vals, inv, v, z_prev, g, gamma == 0 ? z_next : NULL, n);
+        for (int j = 1; j <= gamma; ++j)
+            gs2_inner(rp, ci, vals, pos, inv, g, g + (size_t)(j - 1) * n, g + (size_t)j * n, forward,
+                      z_prev, j == gamma ? z_next : NULL, n);
+    }
+}
+
+void orc_gs2_chain(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                   const uint32_t* pos, const double* inv, int gamma, int sweeps, int forward,
+                   int terminal, const double* v, double* z_io, double* out) {
+    const size_t nn = n ? n : 1;
+    double* z = (double*)malloc(sizeof(double) * nn * (size_t)(sweeps + 1));
+    double* g = (double*)malloc(sizeof(double) * nn * (size_t)(gamma + 1));
+    memcpy(z, z_io, sizeof(double) * n);
+    gs2_sweeps(n, rp, ci, vals, pos, inv, gamma, sweeps, forward, v, z, g);
+    const double* zk = z + (size_t)sweeps * n;
+    if (terminal == 1) orc_spmv_rows(rp, ci, vals, zk, out, 0, n);
+    if (terminal == 2) gs2_residual(rp, ci, vals, v, zk, out, n);
+    memcpy(z_io, zk, sizeof(double) * n);
+    free(z);
+    free(g);
+}
+
+int orc_sstep_gs2_block(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                        const uint32_t* pos, const double* inv, int gamma, int sweeps, int forward,
+                        const double* re, const double* im, int ns, double* block) {
+    if (ns < 1) return ORC_EINVAL;
+    if (orc_check_shift_chain(re, im, ns) != ORC_OK) return ORC_EINVAL;
+    const size_t nn = n ? n : 1;
+    double* z = (double*)calloc(nn * (size_t)(sweeps + 1), sizeof(double)); /* slice 0 stays 0 */
+    double* g = (double*)malloc(sizeof(double) * nn * (size_t)(gamma + 1));
+    double* t = (double*)malloc(sizeof(double) * nn);
+    for (int p = 1; p <= ns; ++p) {
+        double a, b2;
+        shift_params(re, im, p, &a, &b2);
+        const double* src = block + (size_t)(p - 1) * n;
+        const double* src2 = p >= 2 ? block + (size_t)(p - 2) * n : NULL;
+        double* dst = block + (size_t)p * n;
+        gs2_sweeps(n, rp, ci, vals, pos, inv, gamma, sweeps, forward, src, z, g);
+        orc_spmv_rows(rp, ci, vals, z + (size_t)sweeps * n, t, 0, n);
+        for (uint32_t r = 0; r < n; ++r)
+            dst[r] = b2 == 0.0 ? t[r] - a * src[r] : t[r] - a * src[r] + b2 * src2[r];
+    }
+    free(z);
+    free(g);
+    free(t);
+    return ORC_OK;
+}

@@ -131,6 +131,24 @@ int orc_sstep_jacobi_block(uint32_t n, const uint32_t* row_ptr, const uint32_t* 
                            int sweeps, const double* re, const double* im, int ns,
                            double* block);
 
+/* gs2.hpp:123-196 run_gs2_chain (K-sweep two-stage Gauss-Seidel: stage 0 scaled residual,
+ * gamma inner Jacobi-Richardson iterations over the strict lower (forward) / upper (backward)
+ * part, optional terminal on the last sweep).  terminal: 0 none, 1 apply_a (out = A z),
+ * 2 residual (out = v - A z).  z_io holds the initial guess in and the iterate out. */
+void orc_gs2_chain(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                   const double* values, const uint32_t* pos, const double* inv, int gamma,
+                   int sweeps, int forward, int terminal, const double* v, double* z_io,
+                   double* out);
+
+/* sstep.hpp:160-198 SstepGs2Chain run in order (plan power q = (p-1)*K + sweep): every basis
+ * power applies the full K-sweep zero-guess GS2 to w_{p-1}, the last sweep's terminal emits
+ * w_p = A z - a_p w_{p-1} (+ b2_p w_{p-2}).  Pinned by composition like the Jacobi chain: with
+ * zero shifts it is gs2_op applied ns times (gs2_op pinned against the compiled gs2.hpp). */
+int orc_sstep_gs2_block(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                        const double* values, const uint32_t* pos, const double* inv, int gamma,
+                        int sweeps, int forward, const double* re, const double* im, int ns,
+                        double* block);
+
 /* mpk.hpp:219-233: argmax over the table, ties toward the smaller p. */
 int orc_tune_select(const double* gflops, int p_lo, int p_hi);
 

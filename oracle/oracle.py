@@ -66,11 +66,13 @@ class Oracle:
             "orc_jacobi_apply": [u32, P, P, P, P, P, i32, P, P],
             "orc_jacobi_op": [u32, P, P, P, P, P, i32, P, P],
             "orc_sstep_jacobi_block": [u32, P, P, P, P, P, i32, P, P, i32, P],
+            "orc_gs2_chain": [u32, P, P, P, P, P, i32, i32, i32, i32, P, P, P],
+            "orc_sstep_gs2_block": [u32, P, P, P, P, P, i32, i32, i32, P, P, i32, P],
         }
         res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
                "orc_wavefront_schedule": u64, "orc_permute_vector": None,
                "orc_unpermute_vector": None, "orc_poly_combine": None,
-               "orc_jacobi_apply": None, "orc_jacobi_op": None}
+               "orc_jacobi_apply": None, "orc_jacobi_op": None, "orc_gs2_chain": None}
         for k, v in sig.items():
             f = getattr(L, k)
             f.argtypes = v
@@ -220,6 +222,33 @@ class Oracle:
                                _p(x), _p(y))
         return y
 
+    GS2_MODES = {"smooth": (0, 0), "apply": (1, 0), "smooth_residual": (0, 2), "op": (1, 1)}
+
+    def gs2(self, rp, ci, v, gamma, sweeps, forward, mode, vin, z0=None):
+        """gs2.hpp:200-235: mode smooth / apply / smooth_residual / op -> (z, out)."""
+        pos, inv = self.diag_info(rp, ci, v)
+        rp, ci, v, vin = _u32(rp), _u32(ci), _f64(v), _f64(vin)
+        n = len(rp) - 1
+        zero_guess, term = self.GS2_MODES[mode]
+        z = np.zeros(n) if (zero_guess or z0 is None) else _f64(z0).copy()
+        out = np.empty(n)
+        self.lib.orc_gs2_chain(n, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), gamma, sweeps,
+                               1 if forward else 0, term, _p(vin), _p(z), _p(out))
+        return z, (out if term else None)
+
+    def sstep_gs2_block(self, rp, ci, v, gamma, sweeps, forward, x, shifts):
+        pos, inv = self.diag_info(rp, ci, v)
+        re, im = self._shifts(shifts)
+        rp, ci, v = _u32(rp), _u32(ci), _f64(v)
+        n, s = len(rp) - 1, len(re)
+        blk = np.empty((s + 1) * n)
+        blk[:n] = x
+        rc = self.lib.orc_sstep_gs2_block(n, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), gamma, sweeps,
+                                          1 if forward else 0, _p(re), _p(im), s, _p(blk))
+        if rc:
+            raise ValueError("sstep_gs2_block: bad shift chain")
+        return blk.reshape(s + 1, n)
+
     def sstep_jacobi_block(self, rp, ci, v, sweeps, x, shifts):
         pos, inv = self.diag_info(rp, ci, v)
         re, im = self._shifts(shifts)
@@ -274,6 +303,7 @@ class Reference:
             "ref_jacobi_apply": ([u32, P, P, P, i32, P, P], C.c_int),
             "ref_jacobi_op": ([u32, P, P, P, i32, P, P], C.c_int),
             "ref_jacobi_op_blocked": ([u32, P, P, P, i32, P, u32, P, P, i32], C.c_int),
+            "ref_gs2": ([u32, P, P, P, i32, i32, i32, i32, P, u32, i32, P, P, P, i32], C.c_int),
             "ref_last_error": ([], C.c_char_p),
         }
         for k, (a, r) in sig.items():
@@ -435,6 +465,22 @@ class Reference:
         if rc:
             self._raise(rc)
         return y
+
+    GS2_MODES = {"smooth": 0, "apply": 1, "smooth_residual": 2, "op": 3}
+
+    def gs2(self, rp, ci, v, gamma, sweeps, forward, mode, vin, z0=None, group_rows=None,
+            plan_p_m=None, threads=0):
+        rp, ci, v, vin = _u32(rp), _u32(ci), _f64(v), _f64(vin)
+        n = len(rp) - 1
+        z = np.zeros(n) if z0 is None else _f64(z0).copy()
+        out = np.empty(n)
+        gr = None if group_rows is None else _u32(group_rows)
+        rc = self.lib.ref_gs2(n, _p(rp), _p(ci), _p(v), gamma, sweeps, 1 if forward else 0,
+                              self.GS2_MODES[mode], _p(gr), 0 if gr is None else len(gr) - 1,
+                              plan_p_m or sweeps, _p(vin), _p(z), _p(out), threads)
+        if rc:
+            self._raise(rc)
+        return z, (out if mode in ("smooth_residual", "op") else None)
 
     def jacobi_op_blocked(self, rp, ci, v, sweeps, group_rows, x, threads=0):
         rp, ci, v, x, gr = _u32(rp), _u32(ci), _f64(v), _f64(x), _u32(group_rows)

@@ -17,6 +17,7 @@
 #include "mpk/csr.hpp"
 #include "mpk/execute.hpp"
 #include "mpk/generators.hpp"
+#include "mpk/gs2.hpp"
 #include "mpk/jacobi.hpp"
 #include "mpk/levels.hpp"
 #include "mpk/mpk.hpp"
@@ -327,6 +328,34 @@ int ref_jacobi_op_blocked(uint32_t n, const uint32_t* rp, const uint32_t* ci, co
         std::vector<double> out;
         mpk::jacobi_op_blocked(P, A, plan, std::vector<double>(x, x + n), out, threads);
         std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
+
+// gs2.hpp: mode 0 smooth (z in/out), 1 apply (zero guess), 2 smooth_residual, 3 op; plan
+// (group_rows) NULL = sequential form, otherwise the blocked twin (sub_powers = gamma + 2).
+int ref_gs2(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v, int gamma,
+            int sweeps, int forward, int mode, const uint32_t* group_rows, uint32_t ng, int plan_p_m,
+            const double* vin, double* z_io, double* out, int threads) {
+    return guard([&] {
+        const auto A = wrap(n, rp, ci, v);
+        const mpk::Gs2Precon P = mpk::gs2_setup(A, gamma, sweeps,
+                                                forward ? mpk::SweepDirection::forward
+                                                        : mpk::SweepDirection::backward);
+        const std::vector<double> vv(vin, vin + n);
+        std::vector<double> z(z_io, z_io + n), o;
+        mpk::ExecutionPlan plan;
+        if (group_rows) {
+            plan = plan_from(n, group_rows, ng, plan_p_m);
+            plan.sub_powers = gamma + 2;
+        }
+        switch (mode) {
+            case 0: group_rows ? mpk::gs2_smooth_blocked(P, A, plan, vv, z, threads) : mpk::gs2_smooth(P, A, vv, z, threads); break;
+            case 1: group_rows ? mpk::gs2_apply_blocked(P, A, plan, vv, z, threads) : mpk::gs2_apply(P, A, vv, z, threads); break;
+            case 2: group_rows ? mpk::gs2_smooth_residual_blocked(P, A, plan, vv, z, o, threads) : mpk::gs2_smooth_residual(P, A, vv, z, o, threads); break;
+            default: group_rows ? mpk::gs2_op_blocked(P, A, plan, vv, o, threads) : mpk::gs2_op(P, A, vv, o, threads); break;
+        }
+        std::memcpy(z_io, z.data(), sizeof(double) * n);
+        if (out && !o.empty()) std::memcpy(out, o.data(), sizeof(double) * n);
     });
 }
 

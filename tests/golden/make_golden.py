@@ -107,6 +107,26 @@ def main():
                 op=R.jacobi_op(prp, pci, pv, sw, x),
                 op_blocked=R.jacobi_op_blocked(prp, pci, pv, sw, gr, x))
 
+    # --- GS2 chains (gs2.hpp) ---------------------------------------------------------------------
+    rp, ci, v = R.gen(5, 300, 5, 0, 13)
+    lv, pm, ip, lp = R.build_levels(rp, ci, v)
+    prp, pci, pv = R.permute(rp, ci, v, pm)
+    x = np.sin(0.19 * np.arange(300)) + 0.1
+    z0 = np.cos(0.07 * np.arange(300))
+    for gamma, K, fw in ((0, 1, 1), (2, 2, 1), (3, 2, 0)):
+        gr, _, _, _ = R.group_levels(prp, pci, pv, lp, 16 * 1024, K)
+        arrs = dict(prp=prp, pci=pci, pv=pv, x=x, z0=z0, group_rows=gr)
+        for mode in ("smooth", "apply", "smooth_residual", "op"):
+            z, out = R.gs2(prp, pci, pv, gamma, K, fw, mode, x, None if mode in ("apply", "op") else z0)
+            zb, outb = R.gs2(prp, pci, pv, gamma, K, fw, mode, x,
+                             None if mode in ("apply", "op") else z0, group_rows=gr, plan_p_m=K)
+            assert np.array_equal(z.view(np.uint64), zb.view(np.uint64))  # gs2.hpp: blocked == seq
+            arrs[f"{mode}_z"] = z
+            if out is not None:
+                assert np.array_equal(out.view(np.uint64), outb.view(np.uint64))
+                arrs[f"{mode}_out"] = out
+        put(f"gs2.g{gamma}_k{K}_f{fw}", **arrs)
+
     # acceptance.cpp:84-90 random_vector(n, 42)
     put("rv", x=R.random_vector(1000, 42))
     np.savez_compressed(OUT, **g)

@@ -224,3 +224,37 @@ def test_jacobi_oracle_vs_reference_fresh(oracle, ref):
         for sw in (1, 3):
             assert_bitwise(oracle.jacobi_apply(rp, ci, v, sw, x), ref.jacobi_apply(rp, ci, v, sw, x))
             assert_bitwise(oracle.jacobi_op(rp, ci, v, sw, x), ref.jacobi_op(rp, ci, v, sw, x))
+
+
+# ---- GS2 chains (gs2.hpp) -------------------------------------------------------------------------
+GS2_CASES = ["g0_k1_f1", "g2_k2_f1", "g3_k2_f0"]
+
+
+@pytest.mark.parametrize("name", GS2_CASES)
+def test_gs2_matches_golden(oracle, golden, name):
+    g = lambda k: golden[f"gs2.{name}.{k}"]
+    gamma, K, fw = (int(t[1:]) for t in name.split("_"))
+    for mode in ("smooth", "apply", "smooth_residual", "op"):
+        z, out = oracle.gs2(g("prp"), g("pci"), g("pv"), gamma, K, bool(fw), mode, g("x"), g("z0"))
+        if mode != "op":
+            assert_bitwise(z, g(f"{mode}_z"), mode)
+        if out is not None:
+            assert_bitwise(out, g(f"{mode}_out"), mode)
+
+
+def test_sstep_gs2_chain_composition(oracle, golden):
+    """sstep.hpp:160-198 (Eigen-dependent header) pinned by composition: zero shifts give gs2_op
+    applied s times; shift terms as mpk.hpp's shifted rows."""
+    g = lambda k: golden[f"gs2.g2_k2_f1.{k}"]
+    rp, ci, v, x = g("prp"), g("pci"), g("pv"), g("x")
+    for gamma, K, fw in ((0, 1, True), (2, 2, True), (1, 3, False)):
+        sh = [0.5, 1.5 + 0.5j, 1.5 - 0.5j, 2.0]
+        blk = oracle.sstep_gs2_block(rp, ci, v, gamma, K, fw, x, sh)
+        w = [x]
+        for p, s in enumerate(sh, 1):
+            _, t = oracle.gs2(rp, ci, v, gamma, K, fw, "op", w[p - 1])
+            nxt = t - s.real * w[p - 1]
+            if s.imag < 0:
+                nxt = nxt + (s.imag ** 2) * w[p - 2]
+            w.append(nxt)
+            assert_bitwise(blk[p], nxt, f"gamma={gamma} K={K} p={p}")
