@@ -57,6 +57,7 @@ typedef struct mpkg_csr_s* mpkg_csr_t;
 typedef struct mpkg_levels_s* mpkg_levels_t;
 typedef struct mpkg_plan_s* mpkg_plan_t;
 typedef struct mpkg_jacobi_s* mpkg_jacobi_t;
+typedef struct mpkg_gs2_s* mpkg_gs2_t;
 typedef struct mpkg_host_csr_s* mpkg_host_csr_t;
 
 /* ---- errors / version ------------------------------------------------------------------- */
@@ -252,6 +253,39 @@ int mpkg_sstep_jacobi(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t
 int mpkg_sstep_jacobi_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_csr_t A,
                           const double* re, const double* im, int s, double* d_block,
                           uint64_t block_rows, uint64_t block_slices);
+
+/* ---- GS2 (K-sweep two-stage Gauss-Seidel) chains (gs2.hpp; sstep.hpp:160-198) ---------------
+ * direction: 0 forward (strict lower part), 1 backward (strict upper part).  P may be NULL (the
+ * sequential form) or must match A, carry sub_powers == gamma + 2 and a power budget >= sweeps
+ * (the cache-blocked twins, bitwise equal to the sequential form). */
+int mpkg_gs2_setup(mpkg_ctx_t ctx, mpkg_csr_t A, int gamma, int sweeps, int direction,
+                   mpkg_gs2_t* out);                                       /* gs2.hpp:55-62 */
+int mpkg_gs2_info(mpkg_gs2_t G, uint32_t* n, int* gamma, int* sweeps, int* direction);
+int mpkg_gs2_get(mpkg_gs2_t G, uint32_t* pos, double* inv);
+int mpkg_gs2_destroy(mpkg_gs2_t G);
+/* gs2.hpp:200-204 gs2_smooth (z in/out) / 207-212 gs2_apply (zero guess) / 215-220
+ * gs2_smooth_residual (z in/out, r = v - A z) / 223-228 gs2_op (y = A M^{-1} v) and their
+ * *_blocked twins (gs2.hpp:233-275) when P != NULL.  Host pointers. */
+int mpkg_gs2_smooth(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v,
+                    double* z);
+int mpkg_gs2_apply(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v,
+                   double* z);
+int mpkg_gs2_smooth_residual(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A,
+                             const double* v, double* z, double* r);
+int mpkg_gs2_op(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v,
+                double* y);
+/* Device-pointer form of the four: mode 0 smooth, 1 apply, 2 smooth_residual, 3 op; d_z is
+ * in/out (ignored on input for apply / op), d_out receives r or y. */
+int mpkg_gs2_run_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, int mode,
+                     const double* d_v, double* d_z, double* d_out);
+/* sstep.hpp:356-398 sstep_generate_block, GS2 case (P: sub_powers == gamma + 2, power budget
+ * >= s * sweeps). */
+int mpkg_sstep_gs2(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* re,
+                   const double* im, int s, double* block, uint64_t block_rows,
+                   uint64_t block_slices);
+int mpkg_sstep_gs2_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A,
+                       const double* re, const double* im, int s, double* d_block,
+                       uint64_t block_rows, uint64_t block_slices);
 
 /* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
 /* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]

@@ -70,6 +70,10 @@ struct JacobiHolder {
     mpkg_jacobi_t h = nullptr;
     ~JacobiHolder() { mpkg_jacobi_destroy(h); }
 };
+struct Gs2Holder {
+    mpkg_gs2_t h = nullptr;
+    ~Gs2Holder() { mpkg_gs2_destroy(h); }
+};
 
 }  // namespace detail
 
@@ -583,6 +587,116 @@ inline void sstep_jacobi_block(const JacobiPrecon& p, const CsrMatrix& a,
     detail::check(mpkg_sstep_jacobi(device_context(), p.device(), plan ? plan->device() : nullptr,
                                     a.device(), re.data(), im.data(), static_cast<int>(shifts.size()),
                                     w.data.data(), w.rows, w.slices));
+}
+
+// ---- gs2.hpp ---------------------------------------------------------------
+/// gs2.hpp:44
+enum class SweepDirection { forward, backward };
+
+/// gs2.hpp:47-53; the diagonal data also lives on the device (built by gs2_setup).
+struct Gs2Precon {
+    DiagInfo diag;
+    int gamma = 1;
+    int sweeps = 1;
+    SweepDirection direction = SweepDirection::forward;
+    mpkg_gs2_t device() const {
+        if (!dev_) throw std::invalid_argument("Gs2Precon: not built by gs2_setup");
+        return dev_->h;
+    }
+    std::shared_ptr<detail::Gs2Holder> dev_;
+};
+
+/// gs2.hpp:55-62
+inline Gs2Precon gs2_setup(const CsrMatrix& a, int gamma, int sweeps = 1,
+                           SweepDirection direction = SweepDirection::forward) {
+    Gs2Precon p;
+    p.gamma = gamma, p.sweeps = sweeps, p.direction = direction;
+    auto d = std::make_shared<detail::Gs2Holder>();
+    detail::check(mpkg_gs2_setup(device_context(), a.device(), gamma, sweeps,
+                                 direction == SweepDirection::forward ? 0 : 1, &d->h));
+    p.diag.pos.resize(a.n_rows);
+    p.diag.inv.resize(a.n_rows);
+    detail::check(mpkg_gs2_get(d->h, p.diag.pos.data(), p.diag.inv.data()));
+    p.dev_ = d;
+    return p;
+}
+
+namespace detail {
+inline void gs2_sizes(const CsrMatrix& a, const std::vector<double>& v, const std::vector<double>* z) {
+    if (a.n_rows != a.n_cols) throw std::invalid_argument("gs2: matrix must be square");
+    if (v.size() != a.n_rows || (z && z->size() != a.n_rows))
+        throw std::invalid_argument("gs2: size mismatch");
+}
+}  // namespace detail
+
+/// gs2.hpp:200-204
+inline void gs2_smooth(const Gs2Precon& p, const CsrMatrix& a, const std::vector<double>& v,
+                       std::vector<double>& z, int /*threads*/ = 0) {
+    detail::gs2_sizes(a, v, &z);
+    detail::check(mpkg_gs2_smooth(device_context(), p.device(), nullptr, a.device(), v.data(), z.data()));
+}
+/// gs2.hpp:207-212
+inline void gs2_apply(const Gs2Precon& p, const CsrMatrix& a, const std::vector<double>& v,
+                      std::vector<double>& z, int /*threads*/ = 0) {
+    detail::gs2_sizes(a, v, nullptr);
+    z.assign(a.n_rows, 0.0);
+    detail::check(mpkg_gs2_apply(device_context(), p.device(), nullptr, a.device(), v.data(), z.data()));
+}
+/// gs2.hpp:215-220
+inline void gs2_smooth_residual(const Gs2Precon& p, const CsrMatrix& a, const std::vector<double>& v,
+                                std::vector<double>& z, std::vector<double>& r, int /*threads*/ = 0) {
+    detail::gs2_sizes(a, v, &z);
+    r.resize(a.n_rows);
+    detail::check(mpkg_gs2_smooth_residual(device_context(), p.device(), nullptr, a.device(), v.data(),
+                                           z.data(), r.data()));
+}
+/// gs2.hpp:223-228
+inline void gs2_op(const Gs2Precon& p, const CsrMatrix& a, const std::vector<double>& v,
+                   std::vector<double>& y, int /*threads*/ = 0) {
+    detail::gs2_sizes(a, v, nullptr);
+    y.resize(a.n_rows);
+    detail::check(mpkg_gs2_op(device_context(), p.device(), nullptr, a.device(), v.data(), y.data()));
+}
+/// gs2.hpp:233-275 cache-blocked twins (plan: sub_powers == gamma + 2, budget >= sweeps)
+inline void gs2_smooth_blocked(const Gs2Precon& p, const CsrMatrix& a_perm, const ExecutionPlan& plan,
+                               const std::vector<double>& v, std::vector<double>& z, int /*threads*/ = 0) {
+    detail::gs2_sizes(a_perm, v, &z);
+    detail::check(mpkg_gs2_smooth(device_context(), p.device(), plan.device(), a_perm.device(), v.data(),
+                                  z.data()));
+}
+inline void gs2_apply_blocked(const Gs2Precon& p, const CsrMatrix& a_perm, const ExecutionPlan& plan,
+                              const std::vector<double>& v, std::vector<double>& z, int /*threads*/ = 0) {
+    detail::gs2_sizes(a_perm, v, nullptr);
+    z.assign(a_perm.n_rows, 0.0);
+    detail::check(mpkg_gs2_apply(device_context(), p.device(), plan.device(), a_perm.device(), v.data(),
+                                 z.data()));
+}
+inline void gs2_smooth_residual_blocked(const Gs2Precon& p, const CsrMatrix& a_perm,
+                                        const ExecutionPlan& plan, const std::vector<double>& v,
+                                        std::vector<double>& z, std::vector<double>& r,
+                                        int /*threads*/ = 0) {
+    detail::gs2_sizes(a_perm, v, &z);
+    r.resize(a_perm.n_rows);
+    detail::check(mpkg_gs2_smooth_residual(device_context(), p.device(), plan.device(), a_perm.device(),
+                                           v.data(), z.data(), r.data()));
+}
+inline void gs2_op_blocked(const Gs2Precon& p, const CsrMatrix& a_perm, const ExecutionPlan& plan,
+                           const std::vector<double>& v, std::vector<double>& y, int /*threads*/ = 0) {
+    detail::gs2_sizes(a_perm, v, nullptr);
+    y.resize(a_perm.n_rows);
+    detail::check(mpkg_gs2_op(device_context(), p.device(), plan.device(), a_perm.device(), v.data(),
+                              y.data()));
+}
+
+/// sstep.hpp:356-398 sstep_generate_block, GS2 case (see sstep_jacobi_block).
+inline void sstep_gs2_block(const Gs2Precon& p, const CsrMatrix& a,
+                            const std::vector<std::complex<double>>& shifts, VectorBlock& w,
+                            const ExecutionPlan* plan = nullptr) {
+    std::vector<double> re, im;
+    detail::split(shifts, re, im);
+    detail::check(mpkg_sstep_gs2(device_context(), p.device(), plan ? plan->device() : nullptr,
+                                 a.device(), re.data(), im.data(), static_cast<int>(shifts.size()),
+                                 w.data.data(), w.rows, w.slices));
 }
 
 /// mpk.hpp:211-215

@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     Context,
     DeviceCsr,
     ExecutionPlan,
+    Gs2Precon,
     HostCsr,
     JacobiPrecon,
     LevelStructure,

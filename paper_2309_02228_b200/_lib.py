@@ -67,6 +67,17 @@ _SIGS = {
     "mpkg_jacobi_op_blocked": [P, P, P, P, P, P],
     "mpkg_jacobi_op_blocked_dev": [P, P, P, P, P, P],
     "mpkg_sstep_jacobi": [P, P, P, P, P, P, i32, P, u64, u64],
+    "mpkg_gs2_setup": [P, P, i32, i32, i32, C.POINTER(P)],
+    "mpkg_gs2_info": [P, pu32, pint, pint, pint],
+    "mpkg_gs2_get": [P, P, P],
+    "mpkg_gs2_destroy": [P],
+    "mpkg_gs2_smooth": [P, P, P, P, P, P],
+    "mpkg_gs2_apply": [P, P, P, P, P, P],
+    "mpkg_gs2_smooth_residual": [P, P, P, P, P, P, P],
+    "mpkg_gs2_op": [P, P, P, P, P, P],
+    "mpkg_gs2_run_dev": [P, P, P, P, i32, P, P, P],
+    "mpkg_sstep_gs2": [P, P, P, P, P, P, i32, P, u64, u64],
+    "mpkg_sstep_gs2_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],
     "mpkg_baseline_mpk": [P, P, P, i32, P, u64, u64],

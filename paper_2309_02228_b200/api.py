@@ -283,6 +283,30 @@ class JacobiPrecon:
             self.h = None
 
 
+class Gs2Precon:
+    """gs2.hpp:47-53: DiagInfo + gamma (inner iterations), sweeps (K), direction."""
+
+    def __init__(self, ctx: "Context", h: int):
+        self.ctx, self.h = ctx, h
+        n, g, k, d = C.c_uint32(), C.c_int(), C.c_int(), C.c_int()
+        check(lib.mpkg_gs2_info(h, C.byref(n), C.byref(g), C.byref(k), C.byref(d)))
+        self.n_rows, self.gamma, self.sweeps = n.value, g.value, k.value
+        self.forward = d.value == 0
+
+    def diag(self):
+        pos, inv = np.empty(self.n_rows, np.uint32), np.empty(self.n_rows)
+        check(lib.mpkg_gs2_get(self.h, _ptr(pos), _ptr(inv)))
+        return pos, inv
+
+    def stages(self) -> int:  # plan sub_powers of the chain (gs2.hpp:169)
+        return self.gamma + 2
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.mpkg_gs2_destroy(self.h)
+            self.h = None
+
+
 class ExecutionPlan:
     """plan.hpp:41-54."""
 
@@ -589,6 +613,44 @@ class Context:
         blk.data[:n] = _f64(x)
         check(lib.mpkg_sstep_jacobi(self.h, J.h, plan.h if plan is not None else None, A.h,
                                     _ptr(re), _ptr(im), k, _ptr(blk.data), n, k + 1))
+        return blk
+
+    # ---- GS2 chains (gs2.hpp, sstep.hpp:160-198) -----------------------------------------------
+    def gs2_setup(self, A: DeviceCsr, gamma: int, sweeps: int = 1, forward: bool = True) -> Gs2Precon:
+        h = _P()
+        check(lib.mpkg_gs2_setup(self.h, A.h, int(gamma), int(sweeps), 0 if forward else 1, C.byref(h)))
+        return Gs2Precon(self, h.value)
+
+    def gs2_smooth(self, G: Gs2Precon, A: DeviceCsr, v, z, plan=None) -> np.ndarray:
+        z = _f64(z).copy()
+        check(lib.mpkg_gs2_smooth(self.h, G.h, plan.h if plan else None, A.h, _ptr(_f64(v)), _ptr(z)))
+        return z
+
+    def gs2_apply(self, G: Gs2Precon, A: DeviceCsr, v, plan=None) -> np.ndarray:
+        z = np.empty(A.n_rows)
+        check(lib.mpkg_gs2_apply(self.h, G.h, plan.h if plan else None, A.h, _ptr(_f64(v)), _ptr(z)))
+        return z
+
+    def gs2_smooth_residual(self, G: Gs2Precon, A: DeviceCsr, v, z, plan=None):
+        z = _f64(z).copy()
+        r = np.empty(A.n_rows)
+        check(lib.mpkg_gs2_smooth_residual(self.h, G.h, plan.h if plan else None, A.h, _ptr(_f64(v)),
+                                           _ptr(z), _ptr(r)))
+        return z, r
+
+    def gs2_op(self, G: Gs2Precon, A: DeviceCsr, v, plan=None) -> np.ndarray:
+        y = np.empty(A.n_rows)
+        check(lib.mpkg_gs2_op(self.h, G.h, plan.h if plan else None, A.h, _ptr(_f64(v)), _ptr(y)))
+        return y
+
+    def sstep_gs2(self, G: Gs2Precon, plan, A: DeviceCsr, x, shifts) -> VectorBlock:
+        s = np.asarray(list(shifts), dtype=np.complex128)
+        re, im = _f64(s.real), _f64(s.imag)
+        n, k = A.n_rows, len(re)
+        blk = VectorBlock(n, k + 1)
+        blk.data[:n] = _f64(x)
+        check(lib.mpkg_sstep_gs2(self.h, G.h, plan.h if plan is not None else None, A.h,
+                                 _ptr(re), _ptr(im), k, _ptr(blk.data), n, k + 1))
         return blk
 
     def tune_p(self, ls: LevelStructure, A_perm: DeviceCsr, cache_bytes: int, p_lo: int,

@@ -1083,4 +1083,172 @@ int mpkg_sstep_jacobi_dev(mpkg_ctx_t ctx, mpkg_jacobi_t J, mpkg_plan_t P, mpkg_c
     return guarded([&] { sstep_jacobi_dev(ctx, J, P, A, re, im, s, d_block, rows, slices); });
 }
 
+// ---- GS2 chains (precon.cu) -------------------------------------------------------------------
+int mpkg_gs2_setup(mpkg_ctx_t ctx, mpkg_csr_t A, int gamma, int sweeps, int direction, mpkg_gs2_t* out) {
+    return guarded([&] {
+        require(ctx && A && out, "gs2_setup: null argument");
+        require(gamma >= 0, "gs2_setup: gamma must be >= 0");   // gs2.hpp:57
+        require(sweeps >= 1, "gs2_setup: sweeps must be >= 1");  // gs2.hpp:58
+        require(direction == 0 || direction == 1, "gs2_setup: direction must be 0 (forward) or 1 (backward)");
+        require(A->n_rows == A->n_cols, "gs2_setup: matrix must be square");
+        use_device(ctx);
+        auto G = std::make_unique<mpkg_gs2_s>();
+        G->diag.ctx = ctx;
+        G->diag.device = ctx->device;
+        G->gamma = gamma;
+        G->sweeps = sweeps;
+        G->forward = direction == 0;
+        try {
+            gpu_jacobi_setup(ctx, A, &G->diag);
+        } catch (const Status& e) {  // build_diag_info names its caller (jacobi.hpp:48)
+            std::string m = e.what();
+            const std::string from = "jacobi_setup", to = "gs2_setup";
+            if (m.compare(0, from.size(), from) == 0) m = to + m.substr(from.size());
+            fail(e.code, m);
+        }
+        *out = G.release();
+    });
+}
+
+int mpkg_gs2_info(mpkg_gs2_t G, uint32_t* n, int* gamma, int* sweeps, int* direction) {
+    return guarded([&] {
+        require(G != nullptr, "gs2_info: null handle");
+        if (n) *n = G->diag.n;
+        if (gamma) *gamma = G->gamma;
+        if (sweeps) *sweeps = G->sweeps;
+        if (direction) *direction = G->forward ? 0 : 1;
+    });
+}
+
+int mpkg_gs2_get(mpkg_gs2_t G, uint32_t* pos, double* inv) {
+    return guarded([&] {
+        require(G != nullptr, "gs2_get: null handle");
+        MPKG_CUDA(cudaSetDevice(G->diag.device));
+        const uint32_t n = G->diag.n;
+        if (pos && n) MPKG_CUDA(cudaMemcpy(pos, G->diag.pos.p, 4ull * n, cudaMemcpyDeviceToHost));
+        if (inv && n) MPKG_CUDA(cudaMemcpy(inv, G->diag.inv.p, 8ull * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+int mpkg_gs2_destroy(mpkg_gs2_t G) {
+    if (G) {
+        cudaSetDevice(G->diag.device);
+        delete G;
+    }
+    return MPKG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+void gs2_checks(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, int budget) {
+    require(ctx && G && A, "gs2: null argument");
+    require(A->n_rows == A->n_cols, "gs2: matrix must be square");        // gs2.hpp:165
+    require(A->n_rows == G->diag.n, "gs2: size mismatch");                 // gs2.hpp:166-167
+    if (P) {
+        require(P->n_rows == G->diag.n, "gs2: plan does not match matrix");  // gs2.hpp:174
+        require(P->sub_powers == G->gamma + 2, "gs2: plan sub_powers mismatch");
+        require(budget <= P->p_m, "execute: p_m exceeds the plan's power budget");
+    }
+    use_device(ctx);
+}
+
+void gs2_run(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, int mode, const double* d_v,
+             double* d_z, double* d_out) {
+    gs2_checks(ctx, G, P, A, G->sweeps);
+    require(mode >= 0 && mode <= 3, "gs2: mode must be 0..3");
+    if (G->diag.n == 0) return;
+    if (mode == 1 || mode == 3)  // gs2_apply / gs2_op: zero initial guess
+        MPKG_CUDA(cudaMemsetAsync(d_z, 0, 8ull * G->diag.n, ctx->stream));
+    gpu_gs2_chain(ctx, G, A, d_v, d_z, mode == 2 ? 2 : (mode == 3 ? 1 : 0), d_out);
+}
+
+void gs2_host(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, int mode, const double* v,
+              double* z, double* out) {
+    gs2_checks(ctx, G, P, A, G->sweeps);
+    require(v != nullptr, "gs2: null vector");
+    const uint32_t n = G->diag.n;
+    DevBuf<double> buf(3ull * std::max<uint32_t>(n, 1));
+    double *dv = buf.p, *dz = buf.p + n, *dout = buf.p + 2ull * n;
+    if (n) {
+        MPKG_CUDA(cudaMemcpyAsync(dv, v, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (mode == 0 || mode == 2)
+            MPKG_CUDA(cudaMemcpyAsync(dz, z, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    gs2_run(ctx, G, P, A, mode, dv, dz, dout);
+    if (n) {
+        if (z) MPKG_CUDA(cudaMemcpyAsync(z, dz, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out) MPKG_CUDA(cudaMemcpyAsync(out, dout, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void sstep_gs2_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* re,
+                   const double* im, int s, double* d_block, uint64_t rows, uint64_t slices) {
+    require(s >= 1, "sstep_gmres: s must be >= 1");
+    require(re && im, "sstep_gmres: null shifts");
+    gs2_checks(ctx, G, nullptr, A, 0);
+    if (P) {  // sstep.hpp:386-391 + sstep_plan_powers (sstep.hpp:235-247)
+        require(P->n_rows == G->diag.n, "sstep_gmres: plan does not match matrix");
+        require(P->sub_powers == G->gamma + 2, "sstep_gmres: plan sub_powers mismatch");
+        require(s * G->sweeps <= P->p_m, "execute: p_m exceeds the plan's power budget");
+    }
+    require(rows == A->n_rows && slices >= (uint64_t)s + 1, "sstep_gmres: workspace too small");
+    shift_chain(re, im, s, "sstep_gmres");
+    std::vector<double> a, b2;
+    shift_coeffs(re, im, s, a, b2);
+    gpu_sstep_gs2(ctx, G, A, d_block, rows, s, a.data(), b2.data());
+}
+}  // namespace
+
+extern "C" {
+
+int mpkg_gs2_smooth(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v, double* z) {
+    return guarded([&] {
+        require(z != nullptr, "gs2_smooth: null iterate");
+        gs2_host(ctx, G, P, A, 0, v, z, nullptr);
+    });
+}
+int mpkg_gs2_apply(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v, double* z) {
+    return guarded([&] {
+        require(z != nullptr, "gs2_apply: null output");
+        gs2_host(ctx, G, P, A, 1, v, z, nullptr);
+    });
+}
+int mpkg_gs2_smooth_residual(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A,
+                             const double* v, double* z, double* r) {
+    return guarded([&] {
+        require(z && r, "gs2_smooth_residual: null output");
+        gs2_host(ctx, G, P, A, 2, v, z, r);
+    });
+}
+int mpkg_gs2_op(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* v, double* y) {
+    return guarded([&] {
+        require(y != nullptr, "gs2_op: null output");
+        gs2_host(ctx, G, P, A, 3, v, nullptr, y);
+    });
+}
+int mpkg_gs2_run_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, int mode,
+                     const double* d_v, double* d_z, double* d_out) {
+    return guarded([&] { gs2_run(ctx, G, P, A, mode, d_v, d_z, d_out); });
+}
+int mpkg_sstep_gs2(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* re,
+                   const double* im, int s, double* block, uint64_t rows, uint64_t slices) {
+    return guarded([&] {
+        require(ctx && block, "sstep_gmres: null argument");
+        const uint64_t elems = rows * slices;
+        ctx->scratch_block.ensure(std::max<uint64_t>(elems, 1));
+        if (elems)
+            MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_block.p, block, 8ull * elems, cudaMemcpyHostToDevice, ctx->stream));
+        sstep_gs2_dev(ctx, G, P, A, re, im, s, ctx->scratch_block.p, rows, slices);
+        if (elems)
+            MPKG_CUDA(cudaMemcpyAsync(block, ctx->scratch_block.p, 8ull * elems, cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int mpkg_sstep_gs2_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A, const double* re,
+                       const double* im, int s, double* d_block, uint64_t rows, uint64_t slices) {
+    return guarded([&] { sstep_gs2_dev(ctx, G, P, A, re, im, s, d_block, rows, slices); });
+}
+
 }  // extern "C"

@@ -152,6 +152,14 @@ struct mpkg_jacobi_s {
     mpkg_detail::DevBuf<double> inv;      // 1 / A(r,r)
 };
 
+// GS2 preconditioner (gs2.hpp:47-61): DiagInfo + gamma / sweeps / direction.
+struct mpkg_gs2_s {
+    mpkg_jacobi_s diag;  // pos / kdiag / inv (n), sweeps unused
+    int gamma = 1;
+    int sweeps = 1;
+    bool forward = true;
+};
+
 struct mpkg_plan_s {
     int p_m = 1;
     int sub_powers = 1;
@@ -217,6 +225,11 @@ void gpu_jacobi_op(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, const
                    double* d_y);
 void gpu_sstep_jacobi(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, double* d_block,
                       uint64_t rows, int ns, const double* a, const double* b2);
+// terminal: 0 none, 1 apply_a (out = A z), 2 residual (out = v - A z); d_z in/out.
+void gpu_gs2_chain(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, const double* d_v,
+                   double* d_z, int terminal, double* d_out);
+void gpu_sstep_gs2(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, double* d_block,
+                   uint64_t rows, int ns, const double* a, const double* b2);
 
 // mpk_exec.cu
 struct FusedArgs {

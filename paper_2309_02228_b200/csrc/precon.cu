@@ -56,18 +56,20 @@ __global__ void k_diag_scale(uint32_t n, const double* __restrict__ d, const dou
         z[r] = __dmul_rn(d[r], v[r]);
 }
 
-enum { kPlain = 0, kScaled = 1, kSkipDiag = 2 };
-enum { kEpiStore = 0, kEpiJacobi = 1, kEpiShift = 2 };
+enum { kPlain = 0, kScaled = 1, kSkipDiag = 2, kRange = 3 };
+enum { kEpiStore = 0, kEpiJacobi = 1, kEpiShift = 2, kEpiResid = 3 };
 
 // Stored-order row dot over SELL-32 (layout in rowdot.cuh), groups of 8 entries in flight.
 // kScaled gathers d_c and x_c and forms d_c * x_c first (the reference's parenthesisation);
-// kSkipDiag leaves out the row's diagonal entry (index kskip inside the row).
+// kSkipDiag leaves out the row's diagonal entry (index kskip inside the row); kRange keeps only
+// the entries [kb, ke) of the row (GS2's strict lower / upper part).
 template <int MODE>
 __device__ __forceinline__ double pc_row_dot(const uint32_t* __restrict__ cols,
                                              const double* __restrict__ vals, uint64_t off,
                                              uint32_t L, uint32_t lane, uint32_t len,
                                              const double* __restrict__ src,
-                                             const double* __restrict__ d, uint32_t kskip) {
+                                             const double* __restrict__ d, uint32_t kskip,
+                                             uint32_t kb = 0, uint32_t ke = 0xffffffffu) {
     constexpr int G = 8;
     double acc = 0.0;
     const uint32_t Lp = L & ~1u;
@@ -83,13 +85,15 @@ __device__ __forceinline__ double pc_row_dot(const uint32_t* __restrict__ cols,
         }
 #pragma unroll
         for (int j = 0; j < G; ++j) {
-            const bool use = k0 + j < len && (MODE != kSkipDiag || k0 + j != kskip);
+            const bool use = k0 + j < len && (MODE != kSkipDiag || k0 + j != kskip) &&
+                             (MODE != kRange || (k0 + j >= kb && k0 + j < ke));
             x[j] = use ? __ldg(src + c[j]) : 0.0;
             if (MODE == kScaled && use) x[j] = __dmul_rn(__ldg(d + c[j]), x[j]);
         }
 #pragma unroll
         for (int j = 0; j < G; ++j)
-            if (k0 + j < len && (MODE != kSkipDiag || k0 + j != kskip))
+            if (k0 + j < len && (MODE != kSkipDiag || k0 + j != kskip) &&
+                (MODE != kRange || (k0 + j >= kb && k0 + j < ke)))
                 acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
     }
     return acc;
@@ -111,13 +115,44 @@ __global__ void __launch_bounds__(256) k_pc_stage(
         const double acc = pc_row_dot<MODE>(cols, vals, off, L, (uint32_t)(r & 31), len, src, d,
                                             MODE == kSkipDiag ? kd[r] : 0u);
         double out;
-        if constexpr (EPI == kEpiJacobi)
+        if constexpr (EPI == kEpiResid)
+            out = __dsub_rn(v[r], acc);
+        else if constexpr (EPI == kEpiJacobi)
             out = __dsub_rn(__dmul_rn(d[r], v[r]), __dmul_rn(d[r], acc));
         else if constexpr (EPI == kEpiShift)
             out = shift_epilogue(acc, a, b2, own[r], b2 != 0.0 ? own2[r] : 0.0);
         else
             out = acc;
         dst[r] = out;
+    }
+}
+
+// GS2 stage 0 (gs2.hpp:70-82): g = d_r (v_r - sum_k a_rk z_k) over the full row;
+// inner iteration j (gs2.hpp:89-104): g = g0_r - d_r * sum_{k in lower/upper} a_rk g_prev_k.
+// The iterate update z_next = z_prev + g is fused into the last stage of a sweep.
+template <bool INNER>
+__global__ void __launch_bounds__(256) k_gs2_stage(
+    const uint32_t* __restrict__ cols, const double* __restrict__ vals,
+    const uint64_t* __restrict__ chunk_off, const uint32_t* __restrict__ row_len, uint32_t n,
+    const double* __restrict__ src, const double* __restrict__ d, const uint32_t* __restrict__ kd,
+    bool forward, const double* __restrict__ v, const double* __restrict__ g0,
+    double* __restrict__ g_out, const double* __restrict__ z_prev, double* __restrict__ z_next) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t len = row_len[r];
+        const uint64_t off = chunk_off[r >> 5];
+        const uint32_t L = (uint32_t)((chunk_off[(r >> 5) + 1] - off) >> 5);
+        double g;
+        if constexpr (INNER) {
+            const uint32_t kb = forward ? 0u : kd[r] + 1u, ke = forward ? kd[r] : len;
+            const double acc = pc_row_dot<kRange>(cols, vals, off, L, (uint32_t)(r & 31), len, src, d, 0u, kb, ke);
+            g = __dsub_rn(g0[r], __dmul_rn(d[r], acc));
+        } else {
+            const double acc = pc_row_dot<kPlain>(cols, vals, off, L, (uint32_t)(r & 31), len, src, d, 0u);
+            g = __dmul_rn(d[r], __dsub_rn(v[r], acc));
+        }
+        g_out[r] = g;
+        if (z_next) z_next[r] = __dadd_rn(z_prev[r], g);
     }
 }
 
@@ -161,7 +196,66 @@ const double* jacobi_chain(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, const Stage&
     return cur;
 }
 
+// One K-sweep GS2 from z[0]: z holds K+1 slices, g gamma+1 slices (gs2.hpp:126-158 in order).
+void gs2_sweeps(const Stage& st, const mpkg_gs2_s* G, const double* v, double* z, double* g) {
+    const uint32_t n = st.n;
+    for (int p = 1; p <= G->sweeps; ++p) {
+        const double* z_prev = z + (uint64_t)(p - 1) * n;
+        double* z_next = z + (uint64_t)p * n;
+        auto launch = [&](auto inner, const double* src, const double* gprev, double* gout, double* zn) {
+            constexpr bool I = decltype(inner)::value;
+            const auto ev = timing_begin(st.ctx);
+            k_gs2_stage<I><<<st.grid(), 256, 0, st.ctx->stream>>>(
+                st.S.cols.p, st.S.vals.p, st.S.chunk_off.p, st.S.row_len.p, n, src, G->diag.inv.p,
+                G->diag.kdiag.p, G->forward, v, g, gout, z_prev, zn);
+            MPKG_LAUNCH_CHECK();
+            timing_end(st.ctx, ev);
+            st.ctx->launches += 1;
+            (void)gprev;
+        };
+        launch(std::false_type{}, z_prev, nullptr, g, G->gamma == 0 ? z_next : nullptr);
+        for (int j = 1; j <= G->gamma; ++j)
+            launch(std::true_type{}, g + (uint64_t)(j - 1) * n, nullptr, g + (uint64_t)j * n,
+                   j == G->gamma ? z_next : nullptr);
+    }
+}
+
 }  // namespace
+
+void gpu_gs2_chain(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, const double* d_v,
+                   double* d_z, int terminal, double* d_out) {
+    const uint32_t n = G->diag.n;
+    if (n == 0) return;
+    const Stage st{ctx, csr_sell(A), n};
+    DevBuf<double> z((uint64_t)(G->sweeps + 1) * n), g((uint64_t)(G->gamma + 1) * n);
+    MPKG_CUDA(cudaMemcpyAsync(z.p, d_z, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    gs2_sweeps(st, G, d_v, z.p, g.p);
+    const double* zk = z.p + (uint64_t)G->sweeps * n;
+    const mpkg_jacobi_s* J = &G->diag;
+    if (terminal == 1)  // gs2.hpp:147-149 apply_a
+        stage<kPlain, kEpiStore>(st, zk, J, nullptr, nullptr, nullptr, 0.0, 0.0, d_out);
+    else if (terminal == 2)  // residual_rows
+        stage<kPlain, kEpiResid>(st, zk, J, d_v, nullptr, nullptr, 0.0, 0.0, d_out);
+    MPKG_CUDA(cudaMemcpyAsync(d_z, zk, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void gpu_sstep_gs2(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, double* d_block,
+                   uint64_t rows, int ns, const double* a, const double* b2) {
+    const uint32_t n = G->diag.n;
+    if (n == 0) return;
+    const Stage st{ctx, csr_sell(A), n};
+    DevBuf<double> z((uint64_t)(G->sweeps + 1) * n), g((uint64_t)(G->gamma + 1) * n);
+    MPKG_CUDA(cudaMemsetAsync(z.p, 0, 8ull * n, ctx->stream));  // slice 0: the permanent zero guess
+    for (int p = 1; p <= ns; ++p) {
+        const double* src = d_block + (uint64_t)(p - 1) * rows;
+        const double* src2 = p >= 2 ? d_block + (uint64_t)(p - 2) * rows : src;
+        gs2_sweeps(st, G, src, z.p, g.p);
+        stage<kPlain, kEpiShift>(st, z.p + (uint64_t)G->sweeps * n, &G->diag, nullptr, src, src2,
+                                 a[p - 1], b2[p - 1], d_block + (uint64_t)p * rows);
+    }
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
 
 void gpu_jacobi_setup(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_jacobi_s* J) {
     const uint32_t n = A->n_rows;

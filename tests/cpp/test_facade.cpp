@@ -412,9 +412,155 @@ static void test_jacobi() {
     }
 }
 
+// proj/tests/test_relax.cpp:208-406 (GS2).  The Eigen dense solves of NilpotentExactness /
+// BackwardDirectionSolvesUpperTriangular are restated as plain triangular substitutions.
+static CsrMatrix random_lower(std::size_t n, unsigned seed) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(0.5, 1.5);
+    std::vector<mpk::Triplet> t;
+    for (std::size_t i = 0; i < n; ++i) {
+        t.push_back({(index_t)i, (index_t)i, 2.0 + u(rng)});
+        for (std::size_t j = 0; j < i; ++j)
+            if ((rng() & 1u) == 0) t.push_back({(index_t)i, (index_t)j, u(rng) - 1.0});
+    }
+    return mpk::from_coo((index_t)n, (index_t)n, t);
+}
+
+static std::vector<double> tri_solve(const CsrMatrix& a, const std::vector<double>& v, bool lower) {
+    const std::size_t n = a.n_rows;
+    std::vector<double> z(n, 0.0);
+    for (std::size_t s = 0; s < n; ++s) {
+        const index_t r = (index_t)(lower ? s : n - 1 - s);
+        long double acc = v[r];
+        double d = 0.0;
+        for (index_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+            if (a.col_idx[k] == r) d = a.values[k];
+            else acc -= (long double)a.values[k] * z[a.col_idx[k]];
+        }
+        z[r] = (double)(acc / d);
+    }
+    return z;
+}
+
+static double max_err(const std::vector<double>& a, const std::vector<double>& b) {
+    double e = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) e = std::max(e, std::fabs(a[i] - b[i]));
+    return e;
+}
+
+static double max_abs(const std::vector<double>& a) {
+    double m = 0.0;
+    for (double v : a) m = std::max(m, std::fabs(v));
+    return m;
+}
+
+static void test_gs2() {
+    {  // SetupRejectsBadInput
+        CsrMatrix a = mpk::poisson1d(4);
+        EXPECT_THROW(mpk::gs2_setup(a, -1), std::invalid_argument);
+        EXPECT_THROW(mpk::gs2_setup(a, 1, 0), std::invalid_argument);
+        CsrMatrix zd = mpk::from_coo(2, 2, {{0, 0, 0.0}, {1, 1, 2.0}});
+        EXPECT_THROW(mpk::gs2_setup(zd, 1), std::runtime_error);
+    }
+    {  // DiagonalMatrixIsExactForAnyGamma
+        CsrMatrix a = mpk::from_coo(3, 3, {{0, 0, 2.0}, {1, 1, -4.0}, {2, 2, 0.5}});
+        for (int gamma : {0, 1, 3}) {
+            mpk::Gs2Precon p = mpk::gs2_setup(a, gamma);
+            std::vector<double> z;
+            mpk::gs2_apply(p, a, {2.0, 8.0, 1.0}, z);
+            EXPECT(z[0] == 1.0 && z[1] == -2.0 && z[2] == 2.0);
+        }
+    }
+    {  // LowerTriangularExampleEqualsExactSolve: A = [[2,0],[1,2]], v = (2,2) -> (1, 0.5)
+        CsrMatrix a = mpk::from_coo(2, 2, {{0, 0, 2.0}, {1, 0, 1.0}, {1, 1, 2.0}});
+        mpk::Gs2Precon p = mpk::gs2_setup(a, 1);
+        std::vector<double> z;
+        mpk::gs2_apply(p, a, {2.0, 2.0}, z);
+        EXPECT(z[0] == 1.0 && z[1] == 0.5);
+    }
+    {  // GammaZeroIsDiagonalScaling
+        const CsrMatrix a = mpk::random_spd(20, 3, 31);
+        mpk::Gs2Precon p = mpk::gs2_setup(a, 0);
+        const std::vector<double> v = random_vector(20, 33);
+        std::vector<double> z;
+        mpk::gs2_apply(p, a, v, z);
+        bool ok = true;
+        for (std::size_t i = 0; i < 20; ++i) ok = ok && z[i] == p.diag.inv[i] * v[i];
+        EXPECT(ok);
+    }
+    for (unsigned seed : {1u, 2u, 3u, 4u, 5u}) {  // NilpotentExactness
+        const std::size_t n = 6;
+        const CsrMatrix a = random_lower(n, seed);
+        const std::vector<double> v = random_vector(n, seed + 100);
+        mpk::Gs2Precon p = mpk::gs2_setup(a, (int)n - 1);
+        std::vector<double> z;
+        mpk::gs2_apply(p, a, v, z);
+        const std::vector<double> want = tri_solve(a, v, true);
+        EXPECT(max_err(z, want) <= 1e-14 * max_abs(want));
+    }
+    {  // BackwardDirectionSolvesUpperTriangular
+        const CsrMatrix a = mpk::transpose(random_lower(6, 77));
+        const std::vector<double> v = random_vector(6, 78);
+        mpk::Gs2Precon p = mpk::gs2_setup(a, 5, 1, mpk::SweepDirection::backward);
+        std::vector<double> z;
+        mpk::gs2_apply(p, a, v, z);
+        const std::vector<double> want = tri_solve(a, v, false);
+        EXPECT(max_err(z, want) <= 1e-14 * max_abs(want));
+    }
+    {  // OpAndResidualShareKernelsBitwise
+        const CsrMatrix a = mpk::random_spd(50, 5, 51);
+        const std::vector<double> v = random_vector(50, 53);
+        mpk::Gs2Precon p = mpk::gs2_setup(a, 1);
+        std::vector<double> z, y_manual(a.n_rows), y;
+        mpk::gs2_apply(p, a, v, z);
+        mpk::spmv(a, z, y_manual);
+        mpk::gs2_op(p, a, v, y);
+        EXPECT(bitwise_equal(y_manual, y));
+        std::vector<double> r_manual(50), z2(50, 0.0), r;
+        for (std::size_t i = 0; i < 50; ++i) r_manual[i] = v[i] - y_manual[i];
+        mpk::gs2_smooth_residual(p, a, v, z2, r);
+        EXPECT(bitwise_equal(z, z2));
+        EXPECT(bitwise_equal(r_manual, r));
+    }
+    {  // BlockedVariantsBitwiseEqualSequential + PlanShapeMismatchRejected
+        const CsrMatrix a = mpk::poisson2d(20, 20);
+        const std::vector<double> v = random_vector(a.n_rows, 61);
+        const std::vector<double> guess = random_vector(a.n_rows, 62);
+        const LevelStructure ls = mpk::build_levels(a);
+        const CsrMatrix ap = mpk::permute(a, ls.perm);
+        for (int gamma : {0, 1, 2})
+            for (int sweeps : {1, 2})
+                for (auto dir : {mpk::SweepDirection::forward, mpk::SweepDirection::backward}) {
+                    ExecutionPlan plan = mpk::group_levels(ls, ap, 8 * 1024, sweeps);
+                    plan.sub_powers = gamma + 2;
+                    plan.invalidate();
+                    mpk::Gs2Precon p = mpk::gs2_setup(ap, gamma, sweeps, dir);
+                    std::vector<double> z_seq = guess, z_blk = guess;
+                    mpk::gs2_smooth(p, ap, v, z_seq);
+                    mpk::gs2_smooth_blocked(p, ap, plan, v, z_blk);
+                    EXPECT(bitwise_equal(z_seq, z_blk));
+                    std::vector<double> y_seq, y_blk;
+                    mpk::gs2_op(p, ap, v, y_seq);
+                    mpk::gs2_op_blocked(p, ap, plan, v, y_blk);
+                    EXPECT(bitwise_equal(y_seq, y_blk));
+                    std::vector<double> zr_seq(a.n_rows, 0.0), zr_blk(a.n_rows, 0.0), r_seq, r_blk;
+                    mpk::gs2_smooth_residual(p, ap, v, zr_seq, r_seq);
+                    mpk::gs2_smooth_residual_blocked(p, ap, plan, v, zr_blk, r_blk);
+                    EXPECT(bitwise_equal(zr_seq, zr_blk) && bitwise_equal(r_seq, r_blk));
+                }
+        ExecutionPlan plan = mpk::group_levels(ls, ap, 4 * 1024, 1);
+        plan.sub_powers = 3;
+        plan.invalidate();
+        mpk::Gs2Precon p = mpk::gs2_setup(ap, 2);  // needs sub_powers 4
+        std::vector<double> y;
+        EXPECT_THROW(mpk::gs2_op_blocked(p, ap, plan, v, y), std::invalid_argument);
+    }
+}
+
 int main() {
     test_host_helpers();
     test_jacobi();
+    test_gs2();
     test_levels();
     test_wavefront();
     test_mpk();

@@ -93,3 +93,64 @@ def test_jacobi_errors(ctx):
         ctx.sstep_jacobi(J, ok, Gp, np.ones(30), [1.0] * 5)
     with pytest.raises(ValueError):  # conjugate pair straddling the end (mpk.hpp:111-127)
         ctx.sstep_jacobi(J, None, Gp, np.ones(30), [1.0, 1.0 + 2.0j])
+
+
+# ---- GS2 (gs2.hpp) ----------------------------------------------------------------------------
+GS2_CASES = ["g0_k1_f1", "g2_k2_f1", "g3_k2_f0"]
+
+
+@pytest.mark.parametrize("name", GS2_CASES)
+def test_gs2_golden(ctx, golden, name):
+    g = lambda k: golden[f"gs2.{name}.{k}"]
+    gamma, K, fw = (int(t[1:]) for t in name.split("_"))
+    A = ctx.csr(mpkg.HostCsr.from_arrays(g("prp"), g("pci"), g("pv")))
+    G = ctx.gs2_setup(A, gamma, K, bool(fw))
+    plan = mpkg.ExecutionPlan.from_groups(A.n_rows, g("group_rows"), p_m=K, sub_powers=G.stages())
+    for pl in (None, plan):  # sequential form and the blocked twin
+        assert_bitwise(ctx.gs2_smooth(G, A, g("x"), g("z0"), pl), g("smooth_z"), "smooth")
+        assert_bitwise(ctx.gs2_apply(G, A, g("x"), pl), g("apply_z"), "apply")
+        z, r = ctx.gs2_smooth_residual(G, A, g("x"), g("z0"), pl)
+        assert_bitwise(z, g("smooth_residual_z"), "smooth_residual z")
+        assert_bitwise(r, g("smooth_residual_out"), "smooth_residual r")
+        assert_bitwise(ctx.gs2_op(G, A, g("x"), pl), g("op_out"), "op")
+
+
+@pytest.mark.parametrize("gamma,K,fw", [(0, 1, True), (1, 2, True), (2, 3, False)])
+def test_gs2_corpus_and_sstep_vs_oracle(ctx, oracle, gamma, K, fw):
+    shifts = [0.5, 2.0 + 0.75j, 2.0 - 0.75j, 1.0]
+    for name, (P, lv, pm, ip, lp) in _cases(oracle).items():
+        Ap = ctx.csr(P)
+        ls = ctx.levels_from_host(lv, pm, ip, lp)
+        G = ctx.gs2_setup(Ap, gamma, K, fw)
+        x = mpkg.random_vector(P.n_rows, 42)
+        z0 = mpkg.random_vector(P.n_rows, 43)
+        rp, ci, vv = P.row_ptr, P.col_idx, P.values
+        z, _ = oracle.gs2(rp, ci, vv, gamma, K, fw, "smooth", x, z0)
+        assert_bitwise(ctx.gs2_smooth(G, Ap, x, z0), z, f"{name} smooth")
+        _, y = oracle.gs2(rp, ci, vv, gamma, K, fw, "op", x)
+        assert_bitwise(ctx.gs2_op(G, Ap, x), y, f"{name} op")
+        ref = oracle.sstep_gs2_block(rp, ci, vv, gamma, K, fw, x, shifts)
+        assert_bitwise(ctx.sstep_gs2(G, None, Ap, x, shifts).as_matrix(), ref, f"{name} sstep")
+        plan = ctx.group_levels(ls, Ap, 1 << 20, len(shifts) * K).with_sub_powers(G.stages(), lp)
+        assert_bitwise(ctx.sstep_gs2(G, plan, Ap, x, shifts).as_matrix(), ref, f"{name} sstep plan")
+
+
+def test_gs2_errors(ctx):
+    A = ctx.csr(mpkg.poisson2d(6, 5))
+    with pytest.raises(ValueError, match="gamma"):
+        ctx.gs2_setup(A, -1)
+    with pytest.raises(ValueError, match="sweeps"):
+        ctx.gs2_setup(A, 1, 0)
+    M = ctx.csr(mpkg.HostCsr.from_arrays([0, 1, 2, 3], [1, 0, 2], [1.0, 1.0, 1.0]))
+    with pytest.raises(mpkg.MpkgError, match="gs2_setup: missing diagonal entry at row 0"):
+        ctx.gs2_setup(M, 1)
+    G = ctx.gs2_setup(A, 2, 2)
+    bad = mpkg.ExecutionPlan.from_groups(30, [0, 30], p_m=2, sub_powers=3)
+    with pytest.raises(ValueError, match="sub_powers"):
+        ctx.gs2_apply(G, A, np.ones(30), bad)
+    small = mpkg.ExecutionPlan.from_groups(30, [0, 30], p_m=1, sub_powers=4)
+    with pytest.raises(ValueError, match="p_m"):
+        ctx.gs2_apply(G, A, np.ones(30), small)
+    with pytest.raises(ValueError, match="p_m"):  # s * sweeps > budget
+        ctx.sstep_gs2(G, mpkg.ExecutionPlan.from_groups(30, [0, 30], p_m=3, sub_powers=4), A,
+                      np.ones(30), [1.0, 2.0])
