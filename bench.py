@@ -620,7 +620,9 @@ def main():
             e_ms = t.item()
         e2e = {"value": world * flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n * (p + 1) + (8 * n if cfgd["kind"] == "poly" else 0),
+               # slices 1..p stream back while later powers run; slice 0 (= x) is copied on
+               # the host (mpkg_mpk / mpkg_mpk_shifted); the poly call copies block + z
+               "d2h_bytes_per_step": (8 * n * (p + 2)) if cfgd["kind"] == "poly" else 8 * n * p,
                "ms_per_step": e_ms, "steps": e_steps}
 
     # ---- roofline of the dominant (fused) kernel -----------------------------------------------

@@ -113,6 +113,19 @@ void with_host_block(mpkg_ctx_s* ctx, uint32_t n, const double* x, int p_m, doub
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// Host-pointer mpk: stage x; the executor streams every slice back to the caller's block as it
+// completes (run_fused, FusedArgs::host_block); the final sync covers the copies.
+// Slice 0 is x itself: the host copies it while the device works (mpk.hpp:62 / 87 semantics).
+template <class F>
+void host_streamed(mpkg_ctx_s* ctx, uint32_t n, const double* x, int p_m, double* block, F&& body) {
+    ctx->scratch_block.ensure(std::max<uint64_t>((uint64_t)n * (p_m + 1), 1));
+    ctx->scratch_x.ensure(std::max<uint32_t>(n, 1));
+    if (n) MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_x.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    body(ctx->scratch_x.p, ctx->scratch_block.p);
+    if (n && block != x) std::memmove(block, x, sizeof(double) * n);
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 void baseline_dev(mpkg_ctx_s* ctx, mpkg_csr_s* A, const double* d_x, int p_m, double* d_block,
                   uint64_t rows, uint64_t slices, const double* re, const double* im) {
     const char* who = re ? "baseline_mpk_shifted" : "baseline_mpk";
@@ -138,7 +151,7 @@ void baseline_dev(mpkg_ctx_s* ctx, mpkg_csr_s* A, const double* d_x, int p_m, do
 
 void mpk_dev(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const double* d_x, int p_m,
              double* d_block, uint64_t rows, uint64_t slices, const double* re, const double* im,
-             const double* coef, double* d_z, const char* who) {
+             const double* coef, double* d_z, const char* who, double* host_block = nullptr) {
     require(P != nullptr && A != nullptr, std::string(who) + ": null argument");
     check_workspace(A, p_m, rows, slices, who);
     require(P->n_rows == A->n_rows, std::string(who) + ": plan does not match matrix");
@@ -162,6 +175,7 @@ void mpk_dev(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const double* d_x, 
     }
     fa.coef = coef;
     fa.z = d_z;
+    fa.host_block = host_block;
     run_fused(ctx, P, A, fa);
 }
 
@@ -207,6 +221,8 @@ int mpkg_ctx_destroy(mpkg_ctx_t ctx) {
     ctx->scratch_block.release();
     for (auto& e : ctx->timed) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto& e : ctx->event_pool) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    for (auto e : ctx->d2h_events) cudaEventDestroy(e);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MPKG_OK;
@@ -779,9 +795,9 @@ int mpkg_mpk(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* x, int p
         require(P->n_rows == A->n_rows, "mpk: plan does not match matrix");
         require(p_m <= P->p_m, "execute: p_m exceeds the plan's power budget");
         use_device(ctx);
-        with_host_block(ctx, A->n_rows, x, p_m, block, [&](const double* dx, double* dblk) {
+        host_streamed(ctx, A->n_rows, x, p_m, block, [&](const double* dx, double* dblk) {
             mpk_dev(ctx, P, A, dx, p_m, dblk, A->n_rows, (uint64_t)p_m + 1, nullptr, nullptr,
-                    nullptr, nullptr, "mpk");
+                    nullptr, nullptr, "mpk", block);
         });
     });
 }
@@ -832,9 +848,9 @@ int mpkg_mpk_shifted(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* 
         shift_chain(re, im, ns, "mpk_shifted");
         require(ns <= P->p_m, "execute: p_m exceeds the plan's power budget");
         use_device(ctx);
-        with_host_block(ctx, A->n_rows, x, ns, block, [&](const double* dx, double* dblk) {
+        host_streamed(ctx, A->n_rows, x, ns, block, [&](const double* dx, double* dblk) {
             mpk_dev(ctx, P, A, dx, ns, dblk, A->n_rows, (uint64_t)ns + 1, re, im, nullptr, nullptr,
-                    "mpk_shifted");
+                    "mpk_shifted", block);
         });
     });
 }

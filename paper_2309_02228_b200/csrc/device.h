@@ -112,6 +112,9 @@ struct mpkg_ctx_s {
     bool kernel_timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;  // recorded, not yet read
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
+    // device-to-host copy stream + per-slice events for host-pointer calls (run_fused)
+    cudaStream_t d2h = nullptr;
+    std::vector<cudaEvent_t> d2h_events;
     // scratch
     mpkg_detail::DevBuf<double> scratch_x;
     mpkg_detail::DevBuf<double> scratch_block;
@@ -242,6 +245,10 @@ struct FusedArgs {
     const double* shift_b2 = nullptr;  // host arrays, p entries
     const double* coef = nullptr;      // host, p+1 entries
     double* z = nullptr;
+    // host-pointer calls: the caller's host block.  run_fused copies slices 1..p there (on a
+    // second stream, each slice as soon as its power is done in the sweep schedule) and the
+    // context stream waits for the copies; slice 0 (a copy of x) is the caller's job.
+    double* host_block = nullptr;
 };
 void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& a);
 void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,

@@ -1520,7 +1520,57 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const uint32_t smem = E.stages * E.buf_bytes;
     E.last_sweep = sweep;
     const auto ev = timing_begin(ctx);
-    if (sweep) {
+    // host-pointer calls: slice q goes to the host on the copy stream once power q is written
+    const bool to_host = a.host_block != nullptr;
+    auto copy_slice = [&](uint32_t q) {
+        if (!to_host || a.rows == 0 || q == 0) return;  // slice 0 (= x): the host copies it
+        if (!ctx->d2h) MPKG_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+        while (ctx->d2h_events.size() <= q) {
+            cudaEvent_t e;
+            MPKG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->d2h_events.push_back(e);
+        }
+        MPKG_CUDA(cudaEventRecord(ctx->d2h_events[q], st));
+        MPKG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->d2h_events[q], 0));
+        MPKG_CUDA(cudaMemcpyAsync(a.host_block + (uint64_t)q * a.rows, a.block + (uint64_t)q * a.rows,
+                                  8ull * a.rows, cudaMemcpyDeviceToHost, ctx->d2h));
+    };
+    auto join_copies = [&]() {  // the context stream (and so the caller's sync) covers the copies
+        if (!to_host || a.rows == 0 || a.p < 1) return;
+        MPKG_CUDA(cudaEventRecord(ctx->d2h_events[0], ctx->d2h));
+        MPKG_CUDA(cudaStreamWaitEvent(st, ctx->d2h_events[0], 0));
+    };
+    if (sweep && to_host) {
+        // one launch per power with the copies interleaved (no graph: the copy stream waits on
+        // per-power events); the PCIe transfer of slice q overlaps the sweeps q+1..p
+        const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
+        const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
+        for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
+            switch (a.kind * 2 + (sigma ? 1 : 0)) {
+                case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
+                case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
+                case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
+                case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
+                case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
+                default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
+            }
+            MPKG_LAUNCH_CHECK();
+            if (E.long_rows) {
+                switch (a.kind * 2 + (sigma ? 1 : 0)) {
+                    case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
+                    case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
+                    case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
+                    case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
+                    case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
+                    default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
+                }
+                MPKG_LAUNCH_CHECK();
+            }
+            copy_slice(q);
+        }
+        join_copies();
+        ctx->launches += (uint64_t)a.p * (E.long_rows ? 2 : 1) - 1;
+    } else if (sweep) {
         auto launch_all = [&]() {
             const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
             const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
@@ -1619,6 +1669,10 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);
     ctx->launches += 1;
+    if (to_host && !(sweep && to_host)) {  // fused kernel or graph replay: one copy at the end
+        for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) copy_slice(q);
+        join_copies();
+    }
 }
 
 void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
