@@ -882,12 +882,11 @@ int mpkg_mpk_poly(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A, const double* x, 
         ctx->scratch_x.ensure(std::max<uint32_t>(n, 1));
         ctx->scratch_block.ensure((uint64_t)n * (d + 1) + 1);
         if (n) MPKG_CUDA(cudaMemcpyAsync(ctx->scratch_x.p, x, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        // the block (if wanted) streams back slice by slice like mpkg_mpk; z after the last power
         mpk_dev(ctx, P, A, ctx->scratch_x.p, d, ctx->scratch_block.p, n, (uint64_t)d + 1, nullptr,
-                nullptr, c, dz.p, "mpk_poly");
+                nullptr, c, dz.p, "mpk_poly", block);
         if (n) MPKG_CUDA(cudaMemcpyAsync(z, dz.p, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
-        if (block && n)
-            MPKG_CUDA(cudaMemcpyAsync(block, ctx->scratch_block.p, 8ull * n * (d + 1),
-                                      cudaMemcpyDeviceToHost, ctx->stream));
+        if (block && n && block != x) std::memmove(block, x, 8ull * n);
         MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
