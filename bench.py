@@ -47,7 +47,14 @@ CONFIGS = {
                kind="shifted"),
     "c4poly": dict(desc="C4: 27-point 192^3, z = sum_{k=0..8} c_k A^k x", p=8, kind="poly"),
     "c5": dict(desc="C5: 3D 7-point Laplacian 512^3, p=8", p=8, kind="plain"),
+    # the preconditioned s-step basis on C4's matrix (sstep.hpp:122-198)
+    "c4jac": dict(desc="C4 matrix, s-step Newton basis s=8 with a 2-sweep Jacobi preconditioner "
+                       "(w_p = (A M^-1 - theta_p) w_{p-1})", p=8, kind="sstep_jacobi", sweeps=2),
+    "c4gs2": dict(desc="C4 matrix, s-step Newton basis s=8 with GS2 (gamma=1, K=1) "
+                       "(w_p = (A M^-1 - theta_p) w_{p-1})", p=8, kind="sstep_gs2", gamma=1, sweeps=1),
 }
+
+CHAIN_KINDS = ("sstep_jacobi", "sstep_gs2")
 
 
 def make_matrix(cfg: str, seed: int):
@@ -58,7 +65,7 @@ def make_matrix(cfg: str, seed: int):
         return mpkg.scramble(mpkg.stencil27_random_sym(160, 160, 160, seed), seed + 1)
     if cfg == "c3":
         return mpkg.rmat(21, 16, seed)
-    if cfg in ("c4", "c4poly"):
+    if cfg in ("c4", "c4poly", "c4jac", "c4gs2"):
         return mpkg.stencil27(192, 192, 192)
     if cfg == "c5":
         return mpkg.poisson3d(512, 512, 512)
@@ -488,9 +495,29 @@ def main():
     shifts = newton_shifts(p)
     coefs = poly_coefs(args.seed + 3, p)
 
+    chain = None
+    if cfgd["kind"] in CHAIN_KINDS:
+        from paper_2309_02228_b200._lib import check as _check, lib as _lib
+        if cfgd["kind"] == "sstep_jacobi":
+            precon = ctx.jacobi_setup(Ap, cfgd["sweeps"])
+            budget, run = p, _lib.mpkg_sstep_jacobi_dev
+        else:
+            precon = ctx.gs2_setup(Ap, cfgd["gamma"], cfgd["sweeps"])
+            budget, run = p * cfgd["sweeps"], _lib.mpkg_sstep_gs2_dev
+        cplan = ctx.group_levels(ls, Ap, cache, budget).with_sub_powers(precon.stages(), ls.level_ptr)
+        ch_re = np.ascontiguousarray(shifts, np.float64)
+        ch_im = np.zeros(p)
+        d_blk[:n].copy_(d_x)  # slice 0 = x (the chain writes slices 1..p)
+
+        def chain(bp, pl):
+            _check(run(ctx.h, precon.h, pl.h if pl is not None else None, Ap.h, ch_re.ctypes.data,
+                       ch_im.ctypes.data, p, bp, n, p + 1))
+
     def step(block_ptr=None):
         bp = d_blk.data_ptr() if block_ptr is None else block_ptr
-        if cfgd["kind"] == "shifted":
+        if chain is not None:
+            chain(bp, cplan)
+        elif cfgd["kind"] == "shifted":
             ctx.mpk_shifted_dev(plan, Ap, d_x.data_ptr(), shifts, bp, n, p + 1)
         elif cfgd["kind"] == "poly":
             ctx.mpk_poly_dev(plan, Ap, d_x.data_ptr(), coefs, d_z.data_ptr(), bp, n, p + 1)
@@ -505,10 +532,16 @@ def main():
     kname = ("k_mpk_sweep" if exec_info["schedule"] == "sweeps" else
              {0: "k_mpk_lean", 1: "k_mpk_fused", 2: "k_mpk_warptile", 4: "k_mpk_async"}.get(exec_info["kernel"], "?"))
     exec_info["dominant_kernel"] = kname
+    if chain is not None:
+        exec_info = {"dominant_kernel": "k_pc_stage / k_gs2_stage (precon.cu)",
+                     "stages_per_power": precon.stages(), "plan_groups": cplan.n_groups()}
 
     # ---- parity at full size: fused == one-launch-per-power baseline, bit for bit -------------
     ref_blk = torch.empty_like(d_blk)
-    if cfgd["kind"] == "shifted":
+    if chain is not None:  # the plan-driven chain == its sequential form (oracle parity: tests/)
+        ref_blk[:n].copy_(d_x)
+        chain(ref_blk.data_ptr(), None)
+    elif cfgd["kind"] == "shifted":
         import ctypes
         from paper_2309_02228_b200._lib import check, lib
         re = np.ascontiguousarray(shifts, np.float64)
@@ -570,7 +603,7 @@ def main():
     launches = ctx.launch_count() - launches0
     step_ms = ev0.elapsed_time(ev1) / args.steps
     k_total, k_count, k_max = ctx.kernel_times()
-    kernel_ms = k_total / max(k_count, 1)
+    kernel_ms = k_total / args.steps  # every timed launch of the step (one per power or stage)
     ctx.set_param("kernel_timing", 0)
     if dist:
         t = torch.tensor([step_ms, kernel_ms], device=dev)
@@ -581,6 +614,10 @@ def main():
     flops = 2.0 * nnz * p
     if cfgd["kind"] == "poly":
         flops += 2.0 * n * (p + 1)
+    elif cfgd["kind"] == "sstep_jacobi":  # SpMV-shaped stages per power: (sweeps - 1) + terminal
+        flops = 2.0 * nnz * p * cfgd["sweeps"]
+    elif cfgd["kind"] == "sstep_gs2":  # per sweep: full-row stage 0 + gamma half-row inner; terminal
+        flops = p * (cfgd["sweeps"] * (2.0 * nnz + cfgd["gamma"] * nnz) + 2.0 * nnz)
     value = world * flops / (step_ms * 1e-3) * 1e-9
 
     # ---- e2e through the host-pointer C ABI (pinned buffers, copies inside the timed region) --
@@ -592,8 +629,16 @@ def main():
         vb = mpkg.VectorBlock(n, p + 1, hblk.numpy())
         xn = hx.numpy()
 
+        if chain is not None:
+            hblk.numpy()[:n] = x_perm
+
         def e2e_step():
-            if cfgd["kind"] == "shifted":
+            if chain is not None:
+                from paper_2309_02228_b200._lib import check, lib
+                f = lib.mpkg_sstep_jacobi if cfgd["kind"] == "sstep_jacobi" else lib.mpkg_sstep_gs2
+                check(f(ctx.h, precon.h, cplan.h, Ap.h, ch_re.ctypes.data, ch_im.ctypes.data, p,
+                        hblk.numpy().ctypes.data, n, p + 1))
+            elif cfgd["kind"] == "shifted":
                 ctx.mpk_shifted(plan, Ap, xn, shifts, vb)
             elif cfgd["kind"] == "poly":
                 from paper_2309_02228_b200._lib import check, lib
@@ -619,10 +664,12 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = t.item()
         e2e = {"value": world * flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": 8 * n,
-               # slices 1..p stream back while later powers run; slice 0 (= x) is copied on
-               # the host (mpkg_mpk / mpkg_mpk_shifted); the poly call copies block + z
-               "d2h_bytes_per_step": (8 * n * (p + 2)) if cfgd["kind"] == "poly" else 8 * n * p,
+               # chains stage the whole block in and out; mpk / mpk_shifted / mpk_poly stage x in
+               # and stream slices 1..p back while later powers run (slice 0 = x is copied on the
+               # host); the poly call adds z
+               "h2d_bytes_per_step": 8 * n * (p + 1) if chain is not None else 8 * n,
+               "d2h_bytes_per_step": (8 * n * (p + 1) if cfgd["kind"] in CHAIN_KINDS + ("poly",)
+                                      else 8 * n * p),
                "ms_per_step": e_ms, "steps": e_steps}
 
     # ---- roofline of the dominant (fused) kernel -----------------------------------------------
@@ -634,6 +681,10 @@ def main():
     achieved = b_alg / (kernel_ms * 1e-3) / 1e9
     # one power = one pass over the matrix: its own algorithmic bytes (matrix + x read + y written)
     sweep_bytes = 12 * nnz + 4 * (n + 1) + 16 * n
+    if cfgd["kind"] == "sstep_jacobi":  # matrix passes per power: (sweeps - 1) sweeps + terminal
+        sweep_bytes *= cfgd["sweeps"]
+    elif cfgd["kind"] == "sstep_gs2":  # K * (stage 0 + gamma inner) + terminal
+        sweep_bytes *= cfgd["sweeps"] * (1 + cfgd["gamma"]) + 1
     sweep = {"algorithmic_bytes": sweep_bytes, "ms": kernel_ms / p,
              "achieved": sweep_bytes / (kernel_ms / p * 1e-3) / 1e9}
     sweep["frac"] = sweep["achieved"] / peak
@@ -669,7 +720,10 @@ def main():
                        "parity": ("MISMATCH" if not parity else "mpk == baseline bitwise"
                                   if args.mode == "bitwise" else
                                   f"max inf-norm rel err {max_rel_err:.2e} <= 1e-12 vs baseline"), "baseline_back_to_back_ms": baseline_ms,
-                       "baseline_gflops": flops / (baseline_ms * 1e-3) * 1e-9},
+                       "baseline_gflops": flops / (baseline_ms * 1e-3) * 1e-9,
+                       "baseline_note": "p back-to-back launches of the plain SpMV (baseline_mpk)"
+                                        + ("; chains: flops of the preconditioned chain over the "
+                                           "unpreconditioned baseline's time" if chain is not None else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms,

@@ -219,6 +219,7 @@ int mpkg_ctx_destroy(mpkg_ctx_t ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->scratch_x.release();
     ctx->scratch_block.release();
+    ctx->chain_ws.release();
     for (auto& e : ctx->timed) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto& e : ctx->event_pool) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto e : ctx->d2h_events) cudaEventDestroy(e);

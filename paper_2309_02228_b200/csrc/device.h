@@ -118,6 +118,7 @@ struct mpkg_ctx_s {
     // scratch
     mpkg_detail::DevBuf<double> scratch_x;
     mpkg_detail::DevBuf<double> scratch_block;
+    mpkg_detail::DevBuf<double> chain_ws;  // preconditioned chains' workspace (precon.cu)
 };
 
 struct mpkg_csr_s {

@@ -77,11 +77,22 @@ __device__ __forceinline__ double pc_row_dot(const uint32_t* __restrict__ cols,
         uint32_t c[G];
         double v[G], x[G];
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
+        for (int j = 0; j < G; j += 2) {  // whole SELL pairs: one 8 B + one 16 B load
             const uint32_t k = k0 + j;
-            const uint64_t e = off + sell_pos(k, Lp, lane);
-            c[j] = k < len ? __ldg(cols + e) : 0u;
-            v[j] = k < len ? __ldg(vals + e) : 0.0;
+            if (k + 1 < Lp) {
+                const uint64_t e = off + (k >> 1) * 64u + lane * 2u;
+                const uint2 cc = __ldg(reinterpret_cast<const uint2*>(cols + e));
+                const double2 vv = __ldg(reinterpret_cast<const double2*>(vals + e));
+                c[j] = cc.x, c[j + 1] = cc.y, v[j] = vv.x, v[j + 1] = vv.y;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t kk = k + i;
+                    const uint64_t e = off + sell_pos(kk, Lp, lane);
+                    c[j + i] = kk < len ? __ldg(cols + e) : 0u;
+                    v[j + i] = kk < len ? __ldg(vals + e) : 0.0;
+                }
+            }
         }
 #pragma unroll
         for (int j = 0; j < G; ++j) {
@@ -156,6 +167,12 @@ __global__ void __launch_bounds__(256) k_gs2_stage(
     }
 }
 
+// Grow-only per-context workspace for the chains' intermediate vectors (no allocation per call).
+double* chain_workspace(mpkg_ctx_s* ctx, uint64_t count) {
+    ctx->chain_ws.ensure(std::max<uint64_t>(count, 1));
+    return ctx->chain_ws.p;
+}
+
 struct Stage {
     mpkg_ctx_s* ctx;
     const Sell& S;
@@ -227,10 +244,12 @@ void gpu_gs2_chain(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, const do
     const uint32_t n = G->diag.n;
     if (n == 0) return;
     const Stage st{ctx, csr_sell(A), n};
-    DevBuf<double> z((uint64_t)(G->sweeps + 1) * n), g((uint64_t)(G->gamma + 1) * n);
-    MPKG_CUDA(cudaMemcpyAsync(z.p, d_z, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
-    gs2_sweeps(st, G, d_v, z.p, g.p);
-    const double* zk = z.p + (uint64_t)G->sweeps * n;
+    double* ws = chain_workspace(ctx, (uint64_t)(G->sweeps + G->gamma + 2) * n);
+    double* zb = ws;
+    double* gb = ws + (uint64_t)(G->sweeps + 1) * n;
+    MPKG_CUDA(cudaMemcpyAsync(zb, d_z, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    gs2_sweeps(st, G, d_v, zb, gb);
+    const double* zk = zb + (uint64_t)G->sweeps * n;
     const mpkg_jacobi_s* J = &G->diag;
     if (terminal == 1)  // gs2.hpp:147-149 apply_a
         stage<kPlain, kEpiStore>(st, zk, J, nullptr, nullptr, nullptr, 0.0, 0.0, d_out);
@@ -245,13 +264,15 @@ void gpu_sstep_gs2(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, double* 
     const uint32_t n = G->diag.n;
     if (n == 0) return;
     const Stage st{ctx, csr_sell(A), n};
-    DevBuf<double> z((uint64_t)(G->sweeps + 1) * n), g((uint64_t)(G->gamma + 1) * n);
-    MPKG_CUDA(cudaMemsetAsync(z.p, 0, 8ull * n, ctx->stream));  // slice 0: the permanent zero guess
+    double* ws = chain_workspace(ctx, (uint64_t)(G->sweeps + G->gamma + 2) * n);
+    double* zb = ws;
+    double* gb = ws + (uint64_t)(G->sweeps + 1) * n;
+    MPKG_CUDA(cudaMemsetAsync(zb, 0, 8ull * n, ctx->stream));  // slice 0: the permanent zero guess
     for (int p = 1; p <= ns; ++p) {
         const double* src = d_block + (uint64_t)(p - 1) * rows;
         const double* src2 = p >= 2 ? d_block + (uint64_t)(p - 2) * rows : src;
-        gs2_sweeps(st, G, src, z.p, g.p);
-        stage<kPlain, kEpiShift>(st, z.p + (uint64_t)G->sweeps * n, &G->diag, nullptr, src, src2,
+        gs2_sweeps(st, G, src, zb, gb);
+        stage<kPlain, kEpiShift>(st, zb + (uint64_t)G->sweeps * n, &G->diag, nullptr, src, src2,
                                  a[p - 1], b2[p - 1], d_block + (uint64_t)p * rows);
     }
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -285,9 +306,9 @@ void gpu_jacobi_apply(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, co
                       double* d_z) {
     const uint32_t n = J->n;
     if (n == 0) return;
-    DevBuf<double> w(2ull * n);
+    double* w = chain_workspace(ctx, 2ull * n);
     const Stage st{ctx, csr_sell(A), n};
-    const double* z = jacobi_chain(ctx, J, st, d_v, w.p, w.p + n);
+    const double* z = jacobi_chain(ctx, J, st, d_v, w, w + n);
     MPKG_CUDA(cudaMemcpyAsync(d_z, z, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
@@ -301,8 +322,8 @@ void gpu_jacobi_op(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, const
         stage<kScaled, kEpiStore>(st, d_v, J, nullptr, nullptr, nullptr, 0.0, 0.0, d_y);
         return;
     }
-    DevBuf<double> w(2ull * n);
-    const double* z = jacobi_chain(ctx, J, st, d_v, w.p, w.p + n);
+    double* w = chain_workspace(ctx, 2ull * n);
+    const double* z = jacobi_chain(ctx, J, st, d_v, w, w + n);
     stage<kPlain, kEpiStore>(st, z, J, nullptr, nullptr, nullptr, 0.0, 0.0, d_y);
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
@@ -312,7 +333,7 @@ void gpu_sstep_jacobi(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, do
     const uint32_t n = J->n;
     if (n == 0) return;
     const Stage st{ctx, csr_sell(A), n};
-    DevBuf<double> w(J->sweeps > 1 ? 2ull * n : 1);
+    double* w = chain_workspace(ctx, 2ull * n);
     for (int p = 1; p <= ns; ++p) {
         const double* src = d_block + (uint64_t)(p - 1) * rows;
         const double* src2 = p >= 2 ? d_block + (uint64_t)(p - 2) * rows : src;
@@ -320,7 +341,7 @@ void gpu_sstep_jacobi(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, do
         if (J->sweeps == 1) {  // sstep.hpp:91-116 scaled_shifted_spmv_rows
             stage<kScaled, kEpiShift>(st, src, J, nullptr, src, src2, a[p - 1], b2[p - 1], dst);
         } else {  // stage 0, sweeps, then sstep.hpp:68-88 shifted_terminal_rows on z^sweeps
-            const double* z = jacobi_chain(ctx, J, st, src, w.p, w.p + n);
+            const double* z = jacobi_chain(ctx, J, st, src, w, w + n);
             stage<kPlain, kEpiShift>(st, z, J, nullptr, src, src2, a[p - 1], b2[p - 1], dst);
         }
     }
