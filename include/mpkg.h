@@ -120,6 +120,20 @@ int mpkg_validate_levels(mpkg_ctx_t ctx, mpkg_csr_t A_perm, mpkg_levels_t L, int
  * perm is not a permutation (csr.hpp:145-155). */
 int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t* out);
 /* Same, with the device-resident perm of a level structure (no host round trip). */
+/* csr.hpp:72-110 from_coo on the GPU: stable (row, col) sort, duplicates
+ * summed in input order from 0.0, empty rows filled; bit-identical to the reference.  EINVAL:
+ * nnz >= 2^31 or an index out of range (the first offending entry, in input order). */
+int mpkg_csr_from_coo(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, uint64_t nnz,
+                      const uint32_t* rows, const uint32_t* cols, const double* vals,
+                      mpkg_csr_t* out);
+int mpkg_csr_from_coo_dev(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, uint64_t nnz,
+                          const uint32_t* d_rows, const uint32_t* d_cols, const double* d_vals,
+                          mpkg_csr_t* out);
+/* matrix_market.hpp:48-113 read_matrix_market: the reference's format
+ * rules and messages (EINTERNAL = std::runtime_error); text parsed on the host, assembled by the
+ * GPU from_coo. */
+int mpkg_read_matrix_market(mpkg_ctx_t ctx, const char* path, mpkg_csr_t* out);
+
 /* Shard support (multi-GPU level ranges): B = A[r0:r1, c0:c1] on the device,
  * column indices shifted by -c0, kept entries in stored order. */
 int mpkg_csr_block(mpkg_ctx_t ctx, mpkg_csr_t A, uint32_t r0, uint32_t r1, uint32_t c0,

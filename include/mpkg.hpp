@@ -301,6 +301,16 @@ inline CsrMatrix download(mpkg_csr_t h) {
     return B;
 }
 
+/// matrix_market.hpp:48-113 read_matrix_market: the reference's format rules and messages
+/// (std::runtime_error); text parsed on the host, assembled by the GPU from_coo.
+inline CsrMatrix read_matrix_market(const std::string& path) {
+    mpkg_csr_t h = nullptr;
+    detail::check(mpkg_read_matrix_market(device_context(), path.c_str(), &h));
+    detail::CsrHolder guard;
+    guard.h = h;
+    return download(h);
+}
+
 /// csr.hpp:159-188 (GPU permutation, bit-exact)
 inline CsrMatrix permute(const CsrMatrix& A, const std::vector<index_t>& perm) {
     if (A.n_rows != A.n_cols) throw std::invalid_argument("permute: matrix must be square");

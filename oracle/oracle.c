@@ -615,3 +615,47 @@ int orc_sstep_gs2_block(uint32_t n, const uint32_t* rp, const uint32_t* ci, cons
     free(t);
     return ORC_OK;
 }
+
+/* ---- from_coo (csr.hpp:72-110) --------------------------------------------------------------- */
+static const uint32_t* g_sort_rows;
+static const uint32_t* g_sort_cols;
+
+/* (row, col, input index): a total order, so any sort is the stable sort of csr.hpp:86-89 */
+static int coo_cmp(const void* a, const void* b) {
+    const uint64_t i = *(const uint64_t*)a, j = *(const uint64_t*)b;
+    if (g_sort_rows[i] != g_sort_rows[j]) return g_sort_rows[i] < g_sort_rows[j] ? -1 : 1;
+    if (g_sort_cols[i] != g_sort_cols[j]) return g_sort_cols[i] < g_sort_cols[j] ? -1 : 1;
+    return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+int orc_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t* rows,
+                 const uint32_t* cols, const double* vals, uint32_t* row_ptr, uint32_t* col_idx,
+                 double* values, uint64_t* out_nnz, uint64_t* bad) {
+    if (nnz >= ((uint64_t)1 << 31)) return ORC_EINVAL;
+    for (uint64_t i = 0; i < nnz; ++i)
+        if (rows[i] >= n_rows || cols[i] >= n_cols) {
+            if (bad) *bad = i;
+            return ORC_EINVAL;
+        }
+    uint64_t* idx = (uint64_t*)malloc(sizeof(uint64_t) * (nnz ? nnz : 1));
+    for (uint64_t i = 0; i < nnz; ++i) idx[i] = i;
+    g_sort_rows = rows;
+    g_sort_cols = cols;
+    qsort(idx, nnz, sizeof(uint64_t), coo_cmp);
+    memset(row_ptr, 0, sizeof(uint32_t) * ((size_t)n_rows + 1));
+    uint64_t u = 0;
+    for (uint64_t i = 0; i < nnz;) {
+        const uint32_t r = rows[idx[i]], c = cols[idx[i]];
+        double sum = 0.0;
+        for (; i < nnz && rows[idx[i]] == r && cols[idx[i]] == c; ++i) sum += vals[idx[i]];
+        col_idx[u] = c;
+        values[u] = sum;
+        ++u;
+        row_ptr[r + 1] = (uint32_t)u;
+    }
+    for (uint32_t r = 0; r < n_rows; ++r)
+        if (row_ptr[r + 1] < row_ptr[r]) row_ptr[r + 1] = row_ptr[r];
+    *out_nnz = u;
+    free(idx);
+    return ORC_OK;
+}

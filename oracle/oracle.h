@@ -149,6 +149,13 @@ int orc_sstep_gs2_block(uint32_t n, const uint32_t* row_ptr, const uint32_t* col
                         int sweeps, int forward, const double* re, const double* im, int ns,
                         double* block);
 
+/* csr.hpp:72-110 from_coo: stable (row, col) sort, duplicates summed in input order starting
+ * from 0.0, empty rows filled.  Outputs sized n_rows+1 / nnz / nnz; *out_nnz = unique entries.
+ * ORC_EINVAL (first offending entry in *bad) when an index is out of range. */
+int orc_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t* rows,
+                 const uint32_t* cols, const double* vals, uint32_t* row_ptr, uint32_t* col_idx,
+                 double* values, uint64_t* out_nnz, uint64_t* bad);
+
 /* mpk.hpp:219-233: argmax over the table, ties toward the smaller p. */
 int orc_tune_select(const double* gflops, int p_lo, int p_hi);
 

@@ -68,6 +68,7 @@ class Oracle:
             "orc_sstep_jacobi_block": [u32, P, P, P, P, P, i32, P, P, i32, P],
             "orc_gs2_chain": [u32, P, P, P, P, P, i32, i32, i32, i32, P, P, P],
             "orc_sstep_gs2_block": [u32, P, P, P, P, P, i32, i32, i32, P, P, i32, P],
+            "orc_from_coo": [u32, u32, u64, P, P, P, P, P, P, P, P],
         }
         res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
                "orc_wavefront_schedule": u64, "orc_permute_vector": None,
@@ -222,6 +223,20 @@ class Oracle:
                                _p(x), _p(y))
         return y
 
+    def from_coo(self, n_rows, n_cols, rows, cols, vals):
+        """csr.hpp:72-110 -> (row_ptr, col_idx, values); ValueError (index, bad entry) if out of range."""
+        r, c, v = _u32(rows), _u32(cols), _f64(vals)
+        m = len(r)
+        rp = np.empty(n_rows + 1, np.uint32)
+        ci, vv = np.empty(max(m, 1), np.uint32), np.empty(max(m, 1))
+        u, bad = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        rc = self.lib.orc_from_coo(n_rows, n_cols, m, _p(r), _p(c), _p(v), _p(rp), _p(ci), _p(vv),
+                                   _p(u), _p(bad))
+        if rc:
+            raise ValueError(f"from_coo: entry index out of range at entry {int(bad[0])}")
+        k = int(u[0])
+        return rp, ci[:k].copy(), vv[:k].copy()
+
     GS2_MODES = {"smooth": (0, 0), "apply": (1, 0), "smooth_residual": (0, 2), "op": (1, 1)}
 
     def gs2(self, rp, ci, v, gamma, sweeps, forward, mode, vin, z0=None):
@@ -304,6 +319,9 @@ class Reference:
             "ref_jacobi_op": ([u32, P, P, P, i32, P, P], C.c_int),
             "ref_jacobi_op_blocked": ([u32, P, P, P, i32, P, u32, P, P, i32], C.c_int),
             "ref_gs2": ([u32, P, P, P, i32, i32, i32, i32, P, u32, i32, P, P, P, i32], C.c_int),
+            "ref_from_coo": ([u32, u32, u64, P, P, P], P),
+            "ref_read_matrix_market": ([C.c_char_p], P),
+            "ref_csr_shape": ([P, P, P], None),
             "ref_last_error": ([], C.c_char_p),
         }
         for k, (a, r) in sig.items():
@@ -465,6 +483,27 @@ class Reference:
         if rc:
             self._raise(rc)
         return y
+
+    def _take_csr(self, h):
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        nr, nc, nnz = np.zeros(1, np.uint32), np.zeros(1, np.uint32), np.zeros(1, np.uint32)
+        self.lib.ref_csr_shape(h, _p(nr), _p(nc))
+        self.lib.ref_csr_info(h, _p(nr), _p(nnz))
+        rp = np.empty(int(nr[0]) + 1, np.uint32)
+        ci, v = np.empty(max(int(nnz[0]), 1), np.uint32), np.empty(max(int(nnz[0]), 1))
+        self.lib.ref_csr_copy(h, _p(rp), _p(ci), _p(v))
+        self.lib.ref_csr_free(h)
+        k = int(nnz[0])
+        return int(nr[0]), int(nc[0]), rp, ci[:k].copy(), v[:k].copy()
+
+    def from_coo(self, n_rows, n_cols, rows, cols, vals):
+        r, c, v = _u32(rows), _u32(cols), _f64(vals)
+        return self._take_csr(self.lib.ref_from_coo(n_rows, n_cols, len(r), _p(r), _p(c), _p(v)))
+
+    def read_matrix_market(self, path):
+        """matrix_market.hpp -> (n_rows, n_cols, row_ptr, col_idx, values); RuntimeError."""
+        return self._take_csr(self.lib.ref_read_matrix_market(str(path).encode()))
 
     GS2_MODES = {"smooth": 0, "apply": 1, "smooth_residual": 2, "op": 3}
 

@@ -19,6 +19,7 @@
 #include "mpk/generators.hpp"
 #include "mpk/gs2.hpp"
 #include "mpk/jacobi.hpp"
+#include "mpk/matrix_market.hpp"
 #include "mpk/levels.hpp"
 #include "mpk/mpk.hpp"
 #include "mpk/plan.hpp"
@@ -357,6 +358,30 @@ int ref_gs2(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
         std::memcpy(z_io, z.data(), sizeof(double) * n);
         if (out && !o.empty()) std::memcpy(out, o.data(), sizeof(double) * n);
     });
+}
+
+// csr.hpp:72-110 from_coo and matrix_market.hpp read_matrix_market; results through ref_csr_*.
+void* ref_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t* rows,
+                   const uint32_t* cols, const double* vals) {
+    void* out = nullptr;
+    const int rc = guard([&] {
+        std::vector<mpk::Triplet> t(nnz);
+        for (uint64_t i = 0; i < nnz; ++i) t[i] = {rows[i], cols[i], vals[i]};
+        out = new mpk::CsrMatrix(mpk::from_coo(n_rows, n_cols, std::move(t)));
+    });
+    return rc ? nullptr : out;
+}
+
+void ref_csr_shape(void* h, uint32_t* n_rows, uint32_t* n_cols) {
+    auto* m = static_cast<mpk::CsrMatrix*>(h);
+    *n_rows = m->n_rows;
+    *n_cols = m->n_cols;
+}
+
+void* ref_read_matrix_market(const char* path) {
+    void* out = nullptr;
+    const int rc = guard([&] { out = new mpk::CsrMatrix(mpk::read_matrix_market(path)); });
+    return rc ? nullptr : out;
 }
 
 }  // extern "C"

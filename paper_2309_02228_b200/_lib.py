@@ -35,6 +35,9 @@ _SIGS = {
     "mpkg_csr_download": [P, P, P, P],
     "mpkg_csr_destroy": [P],
     "mpkg_csr_block": [P, P, u32, u32, u32, u32, C.POINTER(P)],
+    "mpkg_csr_from_coo": [P, u32, u32, u64, P, P, P, C.POINTER(P)],
+    "mpkg_csr_from_coo_dev": [P, u32, u32, u64, P, P, P, C.POINTER(P)],
+    "mpkg_read_matrix_market": [P, C.c_char_p, C.POINTER(P)],
     "mpkg_spmv": [P, P, P, P],
     "mpkg_spmv_dev": [P, P, P, P],
     "mpkg_build_levels": [P, P, C.POINTER(P)],

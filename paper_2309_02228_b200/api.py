@@ -474,6 +474,19 @@ class Context:
             check(lib.mpkg_permute(self.h, A.h, _ptr(p), C.byref(h)))
         return DeviceCsr(self, h.value)
 
+    def csr_from_coo(self, n_rows: int, n_cols: int, rows, cols, vals) -> DeviceCsr:
+        """csr.hpp:72-110 from_coo, on the GPU (bit-identical to the reference)."""
+        r, c, v = _u32(rows), _u32(cols), _f64(vals)
+        h = _P()
+        check(lib.mpkg_csr_from_coo(self.h, n_rows, n_cols, len(r), _ptr(r), _ptr(c), _ptr(v), C.byref(h)))
+        return DeviceCsr(self, h.value)
+
+    def read_matrix_market(self, path) -> DeviceCsr:
+        """matrix_market.hpp read_matrix_market: host parse, GPU assembly."""
+        h = _P()
+        check(lib.mpkg_read_matrix_market(self.h, str(path).encode(), C.byref(h)))
+        return DeviceCsr(self, h.value)
+
     def csr_block(self, A: DeviceCsr, r0: int, r1: int, c0: int, c1: int) -> DeviceCsr:
         """A[r0:r1, c0:c1] on the device (columns shifted by -c0): a level-range shard."""
         h = _P()

@@ -544,6 +544,48 @@ int mpkg_permute(mpkg_ctx_t ctx, mpkg_csr_t A, const uint32_t* perm, mpkg_csr_t*
     });
 }
 
+int mpkg_csr_from_coo_dev(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, uint64_t nnz,
+                          const uint32_t* d_r, const uint32_t* d_c, const double* d_v, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && out, "from_coo: null argument");
+        require(nnz == 0 || (d_r && d_c && d_v), "from_coo: null entry arrays");
+        use_device(ctx);
+        auto B = std::make_unique<mpkg_csr_s>();
+        gpu_from_coo(ctx, n_rows, n_cols, nnz, d_r, d_c, d_v, B.get());
+        *out = B.release();
+    });
+}
+
+int mpkg_csr_from_coo(mpkg_ctx_t ctx, uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t* r,
+                      const uint32_t* c, const double* v, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && out, "from_coo: null argument");
+        require(nnz == 0 || (r && c && v), "from_coo: null entry arrays");
+        require(nnz < (1ull << 31), "from_coo: entry count exceeds 32-bit index range");
+        use_device(ctx);
+        DevBuf<uint32_t> dr(std::max<uint64_t>(nnz, 1)), dc(std::max<uint64_t>(nnz, 1));
+        DevBuf<double> dv(std::max<uint64_t>(nnz, 1));
+        if (nnz) {
+            MPKG_CUDA(cudaMemcpyAsync(dr.p, r, 4 * nnz, cudaMemcpyHostToDevice, ctx->stream));
+            MPKG_CUDA(cudaMemcpyAsync(dc.p, c, 4 * nnz, cudaMemcpyHostToDevice, ctx->stream));
+            MPKG_CUDA(cudaMemcpyAsync(dv.p, v, 8 * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        auto B = std::make_unique<mpkg_csr_s>();
+        gpu_from_coo(ctx, n_rows, n_cols, nnz, dr.p, dc.p, dv.p, B.get());
+        *out = B.release();
+    });
+}
+
+int mpkg_read_matrix_market(mpkg_ctx_t ctx, const char* path, mpkg_csr_t* out) {
+    return guarded([&] {
+        require(ctx && path && out, "read_matrix_market: null argument");
+        use_device(ctx);
+        auto B = std::make_unique<mpkg_csr_s>();
+        read_matrix_market(ctx, path, B.get());
+        *out = B.release();
+    });
+}
+
 int mpkg_csr_block(mpkg_ctx_t ctx, mpkg_csr_t A, uint32_t r0, uint32_t r1, uint32_t c0, uint32_t c1,
                    mpkg_csr_t* out) {
     return guarded([&] {

@@ -221,6 +221,11 @@ void gpu_csr_block(mpkg_ctx_s* ctx, const mpkg_csr_s* A, uint32_t r0, uint32_t r
 void gpu_gather_row_ptr(mpkg_ctx_s* ctx, const mpkg_csr_s* A, const uint32_t* d_idx, uint32_t m,
                         uint32_t* h_out);
 
+// ingest.cu
+void gpu_from_coo(mpkg_ctx_s* ctx, uint32_t n_rows, uint32_t n_cols, uint64_t m, const uint32_t* d_r,
+                  const uint32_t* d_c, const double* d_v, mpkg_csr_s* B);
+void read_matrix_market(mpkg_ctx_s* ctx, const char* path, mpkg_csr_s* B);
+
 // precon.cu
 void gpu_jacobi_setup(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_jacobi_s* J);
 void gpu_jacobi_apply(mpkg_ctx_s* ctx, const mpkg_jacobi_s* J, mpkg_csr_s* A, const double* d_v,

@@ -309,6 +309,18 @@ static void test_host_helpers() {
     const CsrMatrix TT = mpk::transpose(T);
     EXPECT(TT.row_ptr == A.row_ptr && TT.col_idx == A.col_idx);
     EXPECT(mpk::resolve_threads(7) == 7);
+    {  // matrix_market.hpp through the GPU reader: a symmetric file with a duplicate entry
+        const char* path = "/tmp/mpkg_facade_test.mtx";
+        FILE* f = std::fopen(path, "w");
+        std::fputs("%%MatrixMarket matrix coordinate real symmetric\n% c\n3 3 4\n1 1 2.0\n2 1 -1.5\n"
+                   "3 3 4.0\n2 1 0.25\n", f);
+        std::fclose(f);
+        const CsrMatrix M = mpk::read_matrix_market(path);
+        const CsrMatrix R = mpk::from_coo(3, 3, {{0, 0, 2.0}, {1, 0, -1.5}, {0, 1, -1.5}, {2, 2, 4.0},
+                                                {1, 0, 0.25}, {0, 1, 0.25}});
+        EXPECT(M.row_ptr == R.row_ptr && M.col_idx == R.col_idx && bitwise_equal(M.values, R.values));
+        EXPECT_THROW(mpk::read_matrix_market("/tmp/does_not_exist.mtx"), std::runtime_error);
+    }
     EXPECT(mpk::resolve_threads() >= 1);
 }
 

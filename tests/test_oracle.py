@@ -258,3 +258,21 @@ def test_sstep_gs2_chain_composition(oracle, golden):
                 nxt = nxt + (s.imag ** 2) * w[p - 2]
             w.append(nxt)
             assert_bitwise(blk[p], nxt, f"gamma={gamma} K={K} p={p}")
+
+
+def test_from_coo_oracle_vs_reference(oracle, ref):
+    """csr.hpp:72-110: stable sort, input-order duplicate sums from 0.0 (-0.0 alone -> +0.0)."""
+    rng = np.random.default_rng(8)
+    for _ in range(20):
+        nr, nc = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+        m = int(rng.integers(0, 600))
+        r = rng.integers(0, nr, m).astype(np.uint32)
+        c = rng.integers(0, nc, m).astype(np.uint32)
+        v = rng.choice([-0.0, 1.0, -1.0, 2.5, 1e-300], m) * rng.uniform(0.5, 2, m)
+        a = oracle.from_coo(nr, nc, r, c, v)
+        b = ref.from_coo(nr, nc, r, c, v)
+        np.testing.assert_array_equal(a[0], b[2])
+        np.testing.assert_array_equal(a[1], b[3])
+        assert_bitwise(a[2], b[4])
+    with pytest.raises(ValueError):
+        oracle.from_coo(2, 2, [0, 2], [0, 0], [1.0, 1.0])
