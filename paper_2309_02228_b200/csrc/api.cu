@@ -284,6 +284,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
                     "ctx_set_param: kernel must be 0 (lean), 1 (staged), 2 (warp-tile) or 4 (async gather)");
             ctx->kernel = value;
         }
+        else if (k == "sweep_variant") {
+            require(value >= 0 && value <= 3, "ctx_set_param: sweep_variant must be 0..3");
+            ctx->sweep_variant = value;
+        }
         else if (k == "graphs")
             ctx->graphs = value != 0;
         else if (k == "schedule") {

@@ -104,6 +104,7 @@ struct mpkg_ctx_s {
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
     bool graphs = true;       // sweep schedule: replay the p launches as one CUDA graph
+    int64_t sweep_variant = 0;  // sweep-kernel row loop (mpk_exec.cu launch_sweep)
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power (mpk_exec.cu)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
     int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)
@@ -206,6 +207,9 @@ uint32_t gpu_max_row_len(mpkg_ctx_s* ctx, const mpkg_csr_s* A);
 double gpu_mean_first_col_jump(mpkg_ctx_s* ctx, const mpkg_csr_s* A);
 void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
                       double* dst, const double* src2, double shift_a, double shift_b2);
+// the same launch without the kernel-timing events (callers that time a whole step)
+void launch_spmv_sell_raw(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
+                          double* dst, const double* src2, double shift_a, double shift_b2);
 
 // levels.cu
 void gpu_build_levels(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_levels_s* L);

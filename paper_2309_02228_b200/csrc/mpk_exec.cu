@@ -541,9 +541,10 @@ __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, 
 // rows, the grouped row loop (8 gathers in flight per thread).  Slice q-1 is complete before the
 // launch, so every gather takes the read-only path.  Used when no temporal blocking fits in L2
 // (the fused kernel would only add ticket and dependency overhead), see run_fused.
-template <int KIND, bool SIGMA>
-__global__ void __launch_bounds__(256) k_mpk_sweep(const __grid_constant__ FusedParams P, uint32_t q) {
+template <int KIND, bool SIGMA, int V>
+__global__ void __launch_bounds__(256, V == 1 ? 5 : 0) k_mpk_sweep(const __grid_constant__ FusedParams P, uint32_t q) {
     const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    double* const dst = P.V + (uint64_t)q * P.vstride;
     const uint64_t pol = l2_policy_first();
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < P.n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
@@ -553,8 +554,29 @@ __global__ void __launch_bounds__(256) k_mpk_sweep(const __grid_constant__ Fused
         if (len > P.long_cap) continue;  // long rows: k_long_rows_fast (fast mode only)
         const uint64_t off = P.chunk_off[s >> 5];
         const uint32_t L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
-        const double acc = sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
-        row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+        double acc;
+        if constexpr (V == 2)
+            acc = sell_row_dot<true, 4>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        else if constexpr (V == 3)
+            acc = sell_row_dot_pipe<true>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        else
+            acc = sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        if constexpr (KIND == 0 && !SIGMA)
+            dst[s] = acc;  // plain powers in A_perm order: the block slice is the working vector
+        else
+            row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+    }
+}
+
+// Sweep-kernel row-loop variants ("sweep_variant" knob): 0 groups of 8 (64 regs, 4 CTAs/SM),
+// 1 the same capped at 5 CTAs/SM, 2 groups of 4, 3 software-pipelined pairs.
+template <int KIND, bool SIGMA>
+void launch_sweep(int v, unsigned g, cudaStream_t st, const FusedParams& P, uint32_t q) {
+    switch (v) {
+        case 1: k_mpk_sweep<KIND, SIGMA, 1><<<g, 256, 0, st>>>(P, q); break;
+        case 2: k_mpk_sweep<KIND, SIGMA, 2><<<g, 256, 0, st>>>(P, q); break;
+        case 3: k_mpk_sweep<KIND, SIGMA, 3><<<g, 256, 0, st>>>(P, q); break;
+        default: k_mpk_sweep<KIND, SIGMA, 0><<<g, 256, 0, st>>>(P, q); break;
     }
 }
 
@@ -1519,6 +1541,29 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     }
     const uint32_t smem = E.stages * E.buf_bytes;
     E.last_sweep = sweep;
+    const int sv = (int)ctx->sweep_variant;
+    // One power of the sweep schedule.  A_perm order with plain or shifted powers and no long
+    // rows is exactly the baseline's row kernel (k_spmv_sell, fewest instructions per row); every
+    // other case runs k_mpk_sweep (private order, polynomial accumulator, long rows skipped).
+    auto sweep_power = [&](uint32_t q) {
+        const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
+        if (!sigma && a.kind <= 1 && !E.long_rows && sv == 0) {
+            const double* src = a.block + (uint64_t)(q - 1) * a.rows;
+            const double* src2 = q >= 2 ? a.block + (uint64_t)(q - 2) * a.rows : src;
+            launch_spmv_sell_raw(ctx, S, a.kind == 1, src, a.block + (uint64_t)q * a.rows, src2,
+                                 P.shift_a[q - 1], P.shift_b2[q - 1]);
+            ctx->launches -= 1;  // counted with the step below
+            return;
+        }
+        switch (a.kind * 2 + (sigma ? 1 : 0)) {
+            case 0: launch_sweep<0, false>(sv, g, st, P, q); break;
+            case 1: launch_sweep<0, true>(sv, g, st, P, q); break;
+            case 2: launch_sweep<1, false>(sv, g, st, P, q); break;
+            case 3: launch_sweep<1, true>(sv, g, st, P, q); break;
+            case 4: launch_sweep<2, false>(sv, g, st, P, q); break;
+            default: launch_sweep<2, true>(sv, g, st, P, q); break;
+        }
+    };
     const auto ev = timing_begin(ctx);
     // host-pointer calls: slice q goes to the host on the copy stream once power q is written
     const bool to_host = a.host_block != nullptr;
@@ -1543,17 +1588,9 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (sweep && to_host) {
         // one launch per power with the copies interleaved (no graph: the copy stream waits on
         // per-power events); the PCIe transfer of slice q overlaps the sweeps q+1..p
-        const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
         const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
         for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
-            switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
-                case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
-                case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
-                case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
-                case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
-                default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
-            }
+            sweep_power(q);
             MPKG_LAUNCH_CHECK();
             if (E.long_rows) {
                 switch (a.kind * 2 + (sigma ? 1 : 0)) {
@@ -1575,14 +1612,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
             const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
             for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
-                switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                    case 0: k_mpk_sweep<0, false><<<g, 256, 0, st>>>(P, q); break;
-                    case 1: k_mpk_sweep<0, true><<<g, 256, 0, st>>>(P, q); break;
-                    case 2: k_mpk_sweep<1, false><<<g, 256, 0, st>>>(P, q); break;
-                    case 3: k_mpk_sweep<1, true><<<g, 256, 0, st>>>(P, q); break;
-                    case 4: k_mpk_sweep<2, false><<<g, 256, 0, st>>>(P, q); break;
-                    default: k_mpk_sweep<2, true><<<g, 256, 0, st>>>(P, q); break;
-                }
+                sweep_power(q);
                 MPKG_LAUNCH_CHECK();
                 if (E.long_rows) {  // fast mode only (use_sweeps)
                     switch (a.kind * 2 + (sigma ? 1 : 0)) {

@@ -147,9 +147,16 @@ Sell& csr_sell(mpkg_csr_s* A) {
 void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
                       double* dst, const double* src2, double a, double b2) {
     if (S.n_slots == 0) return;
+    const auto ev = timing_begin(ctx);
+    launch_spmv_sell_raw(ctx, S, shifted, src, dst, src2, a, b2);
+    timing_end(ctx, ev);
+}
+
+void launch_spmv_sell_raw(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
+                          double* dst, const double* src2, double a, double b2) {
+    if (S.n_slots == 0) return;
     const unsigned grid = grid_for(S.n_slots, 256, (unsigned)ctx->sm_count * 8u);
     const uint32_t* slot_row = S.slot_row.n ? S.slot_row.p : nullptr;
-    const auto ev = timing_begin(ctx);
     if (!shifted)
         k_spmv_sell<0><<<grid, 256, 0, ctx->stream>>>(S.cols.p, S.vals.p, S.chunk_off.p,
                                                       S.row_len.p, slot_row, S.n_slots, S.n_rows,
@@ -159,7 +166,6 @@ void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double
                                                       S.row_len.p, slot_row, S.n_slots, S.n_rows,
                                                       src, dst, src2, a, b2);
     MPKG_LAUNCH_CHECK();
-    timing_end(ctx, ev);
     ctx->launches += 1;
 }
 
