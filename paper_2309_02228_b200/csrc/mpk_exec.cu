@@ -500,13 +500,26 @@ __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, 
     const uint32_t b = P.csr_rp[r];
     const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;
     const uint32_t nchunks = (len + kLongChunk - 1) / kLongChunk;
-    auto produce = [&](uint32_t c) {  // warps 1.. only
+    auto produce = [&](uint32_t c) {  // warps 1.. only; 8 independent gathers in flight per thread
+        constexpr int U = 8;
         const uint32_t base = c * kLongChunk, m = min(kLongChunk, len - base);
         double* buf = ring + (c & 1u) * kLongChunk;
-        for (uint32_t i = tid - 32u; i < m; i += nt - 32u) {
-            const uint32_t k = b + base + i;
-            const double xv = q == 1 ? ld_vec<true>(srcA + P.csr_ci[k]) : ld_vec<false>(srcA + P.csr_ci[k]);
-            buf[i] = __dmul_rn(ld_mat_d(P.csr_v + k, pol), xv);
+        const uint32_t np = nt - 32u;
+        for (uint32_t i0 = tid - 32u; i0 < m; i0 += U * np) {
+            uint32_t col[U];
+            double val[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * np;
+                col[u] = i < m ? P.csr_ci[b + base + i] : 0u;
+                val[u] = i < m ? ld_mat_d(P.csr_v + b + base + i, pol) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                xv[u] = i0 + u * np < m ? (q == 1 ? ld_vec<true>(srcA + col[u]) : ld_vec<false>(srcA + col[u])) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + u * np < m) buf[i0 + u * np] = __dmul_rn(val[u], xv[u]);
         }
     };
     acc = 0.0;
@@ -597,8 +610,22 @@ __global__ void __launch_bounds__(256) k_long_rows_fast(const __grid_constant__ 
         const uint32_t r = SIGMA ? P.slot_row[s] : s;
         const uint32_t b = P.csr_rp[r], e = P.csr_rp[r + 1];
         double acc = 0.0;
-        for (uint32_t k = b + threadIdx.x; k < e; k += blockDim.x)
-            acc = __fma_rn(ld_mat_d(P.csr_v + k, pol), __ldg(srcA + P.csr_ci[k]), acc);
+        constexpr int U = 8;  // independent gathers in flight per thread
+        for (uint32_t k0 = b + threadIdx.x; k0 < e; k0 += U * blockDim.x) {
+            uint32_t col[U];
+            double val[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t k = k0 + u * blockDim.x;
+                col[u] = k < e ? P.csr_ci[k] : 0u;
+                val[u] = k < e ? ld_mat_d(P.csr_v + k, pol) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = k0 + u * blockDim.x < e ? __ldg(srcA + col[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k0 + u * blockDim.x < e) acc = __fma_rn(val[u], xv[u], acc);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
