@@ -301,6 +301,19 @@ int mpkg_sstep_gs2_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A
                        const double* re, const double* im, int s, double* d_block,
                        uint64_t block_rows, uint64_t block_slices);
 
+/* ---- product-form GMRES polynomial (poly.hpp:146-281) ------------------
+ * z = p(A M^{-1}) v for the given roots (re, im: degree entries, Leja-ordered by the caller,
+ * conjugate pairs adjacent); M^{-1} = J (Jacobi), G (GS2, one sweep) or none (both NULL).  P may
+ * be NULL (sequential form) or carry sub_powers == the inner chain's stages + terminal
+ * (poly.hpp:132-144); roots beyond its power budget are processed in further passes, bitwise
+ * equal.  The roots themselves come from an Arnoldi/harmonic-Ritz setup that needs Eigen in the
+ * reference (poly_setup_gmres) and is not part of this library. */
+int mpkg_poly_apply(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G, const double* re,
+                    const double* im, int degree, mpkg_plan_t P, const double* v, double* z);
+int mpkg_poly_apply_dev(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G,
+                        const double* re, const double* im, int degree, mpkg_plan_t P,
+                        const double* d_v, double* d_z);
+
 /* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
 /* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]
  *        4 random_csr(a=n, b=nnz_per_row, seed) 5 random_spd(a, b, seed) [generators.hpp:96-146]

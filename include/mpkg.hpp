@@ -709,6 +709,61 @@ inline void sstep_gs2_block(const Gs2Precon& p, const CsrMatrix& a,
                                  w.data.data(), w.rows, w.slices));
 }
 
+// ---- poly.hpp ---------------------------------------------------------------
+/// poly.hpp:55-61
+struct PolyInner {
+    enum class Kind { none, jacobi, gs2 };
+    Kind kind = Kind::none;
+    JacobiPrecon jacobi;
+    Gs2Precon gs2;
+};
+
+/// poly.hpp:64-70: the roots (Leja-ordered, conjugate pairs adjacent) are the caller's -- the
+/// reference computes them with an Eigen-based Arnoldi / harmonic-Ritz setup (poly_setup_gmres)
+/// that this library does not provide.
+struct PolyPrecon {
+    std::vector<std::complex<double>> theta;
+    int degree = 0;
+    bool truncated = false;
+    PolyInner inner;
+};
+
+namespace detail {
+inline void poly_call(const PolyPrecon& p, const CsrMatrix& a, const ExecutionPlan* plan,
+                      const std::vector<double>& v, std::vector<double>& z) {
+    if (v.size() != a.n_rows) throw std::invalid_argument("poly_apply: size mismatch");
+    if (p.degree < 1 || p.theta.size() != static_cast<std::size_t>(p.degree))
+        throw std::invalid_argument("poly_apply: preconditioner not set up");
+    std::vector<double> re, im;
+    split(p.theta, re, im);
+    z.assign(a.n_rows, 0.0);
+    check(mpkg_poly_apply(device_context(), a.device(),
+                          p.inner.kind == PolyInner::Kind::jacobi ? p.inner.jacobi.device() : nullptr,
+                          p.inner.kind == PolyInner::Kind::gs2 ? p.inner.gs2.device() : nullptr,
+                          re.data(), im.data(), p.degree, plan ? plan->device() : nullptr, v.data(),
+                          z.data()));
+}
+}  // namespace detail
+
+/// poly.hpp:364-373 z = p(A M^{-1}) v, sequential form
+inline void poly_apply(const PolyPrecon& p, const CsrMatrix& a, const std::vector<double>& v,
+                       std::vector<double>& z, int /*threads*/ = 0) {
+    detail::poly_call(p, a, nullptr, v, z);
+}
+/// poly.hpp:375-380 cache-blocked twin (plan.sub_powers == poly_sub_powers(p))
+inline void poly_apply_blocked(const PolyPrecon& p, const CsrMatrix& a_perm, const ExecutionPlan& plan,
+                               const std::vector<double>& v, std::vector<double>& z, int /*threads*/ = 0) {
+    detail::poly_call(p, a_perm, &plan, v, z);
+}
+/// poly.hpp:383-385
+inline int poly_sub_powers(const PolyPrecon& p) {
+    switch (p.inner.kind) {
+        case PolyInner::Kind::jacobi: return jacobi_stages(p.inner.jacobi.sweeps);
+        case PolyInner::Kind::gs2: return p.inner.gs2.gamma + 2;
+        default: return 1;
+    }
+}
+
 /// mpk.hpp:211-215
 struct TuneResult {
     int p_opt = 1;

@@ -659,3 +659,85 @@ int orc_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t*
     free(idx);
     return ORC_OK;
 }
+
+/* ---- product-form polynomial (poly.hpp:77-93, 146-281) -------------------------------------- */
+int orc_poly_apply(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* vals,
+                   const uint32_t* pos, const double* inv, int inner, int sweeps, int gamma,
+                   int forward, const double* re, const double* im, int degree, const double* v,
+                   double* z) {
+    if (degree < 1) return ORC_EINVAL;
+    unsigned char* role = (unsigned char*)malloc((size_t)degree);
+    for (int i = 0; i < degree;) { /* poly_roles: 0 real, 1 pair first, 2 pair second */
+        if (im[i] == 0.0) {
+            role[i++] = 0;
+            continue;
+        }
+        if (i + 1 >= degree || re[i + 1] != re[i] || im[i + 1] != -im[i]) {
+            free(role);
+            return ORC_EINVAL;
+        }
+        role[i] = 1, role[i + 1] = 2;
+        i += 2;
+    }
+    const size_t nn = n ? n : 1;
+    double* w = (double*)malloc(sizeof(double) * nn * (size_t)degree);
+    double* zb = (double*)calloc(nn * (size_t)(sweeps > 2 ? sweeps : 2), sizeof(double));
+    double* gb = (double*)malloc(sizeof(double) * nn * (size_t)(gamma + 1));
+    double* t = (double*)malloc(sizeof(double) * nn);
+    memcpy(w, v, sizeof(double) * n);
+    for (uint32_t r = 0; r < n; ++r) z[r] = 0.0;
+    for (int pw = 1; pw <= degree - 1; ++pw) {
+        const double* w_in = w + (size_t)(pw - 1) * n;
+        const double* z_src = w_in;
+        int fused = 0;
+        if (inner == 1) {
+            if (sweeps == 1) {
+                fused = 1;
+            } else { /* stage 0 + sweeps (jacobi.hpp:83-117) into zb slices */
+                for (uint32_t r = 0; r < n; ++r) zb[r] = inv[r] * w_in[r];
+                for (int j = 1; j < sweeps; ++j)
+                    jacobi_sweep(rp, ci, vals, pos, inv, w_in, zb + (size_t)(j - 1) * n, zb + (size_t)j * n, n);
+                z_src = zb + (size_t)(sweeps - 1) * n;
+            }
+        } else if (inner == 2) { /* single GS2 sweep from the zero guess zb[0] into zb[1] */
+            double* z0 = zb;
+            double* z1 = zb + n;
+            for (uint32_t r = 0; r < n; ++r) z0[r] = 0.0;
+            gs2_stage0(rp, ci, vals, inv, w_in, z0, gb, gamma == 0 ? z1 : NULL, n);
+            for (int j = 1; j <= gamma; ++j)
+                gs2_inner(rp, ci, vals, pos, inv, gb, gb + (size_t)(j - 1) * n, gb + (size_t)j * n, forward,
+                          z0, j == gamma ? z1 : NULL, n);
+            z_src = z1;
+        }
+        if (fused)
+            scaled_spmv(rp, ci, vals, inv, z_src, t, n);
+        else
+            orc_spmv_rows(rp, ci, vals, z_src, t, 0, n);
+        const double th_re = re[pw - 1];
+        const double mod = th_re * th_re + im[pw - 1] * im[pw - 1];
+        double* w_out = w + (size_t)pw * n;
+        for (uint32_t r = 0; r < n; ++r) {
+            if (role[pw - 1] == 0) {
+                z[r] += w_in[r] / th_re;
+                w_out[r] = w_in[r] - t[r] / th_re;
+            } else if (role[pw - 1] == 1) {
+                const double u = 2.0 * th_re * w_in[r] - t[r];
+                w_out[r] = u;
+                z[r] += u / mod;
+            } else {
+                w_out[r] = w[(size_t)(pw - 2) * n + r] - t[r] / mod;
+            }
+        }
+    }
+    if (role[degree - 1] == 0) { /* trailing real root (poly.hpp:271-278) */
+        const double th = re[degree - 1];
+        const double* wl = w + (size_t)(degree - 1) * n;
+        for (uint32_t r = 0; r < n; ++r) z[r] += wl[r] / th;
+    }
+    free(role);
+    free(w);
+    free(zb);
+    free(gb);
+    free(t);
+    return ORC_OK;
+}

@@ -149,6 +149,17 @@ int orc_sstep_gs2_block(uint32_t n, const uint32_t* row_ptr, const uint32_t* col
                         int sweeps, int forward, const double* re, const double* im, int ns,
                         double* block);
 
+/* poly.hpp:146-281 run_poly_chain (product-form GMRES polynomial):
+ * z = p(A M^{-1}) v for the given roots theta (re, im; conjugate pairs adjacent, + imaginary part
+ * first), inner: 0 none, 1 Jacobi (sweeps), 2 GS2 (gamma, forward; single sweep).  ORC_EINVAL if
+ * a conjugate pair is not adjacent (poly.hpp:77-93).  poly.hpp needs Eigen (absent here), so
+ * this restatement is checked by the polynomial identity A z = v - prod_i (I - A/theta_i) v on
+ * exactly-known spectra and by composition with the pinned Jacobi / GS2 stages. */
+int orc_poly_apply(uint32_t n, const uint32_t* row_ptr, const uint32_t* col_idx,
+                   const double* values, const uint32_t* pos, const double* inv, int inner,
+                   int sweeps, int gamma, int forward, const double* re, const double* im,
+                   int degree, const double* v, double* z);
+
 /* csr.hpp:72-110 from_coo: stable (row, col) sort, duplicates summed in input order starting
  * from 0.0, empty rows filled.  Outputs sized n_rows+1 / nnz / nnz; *out_nnz = unique entries.
  * ORC_EINVAL (first offending entry in *bad) when an index is out of range. */

@@ -69,6 +69,7 @@ class Oracle:
             "orc_gs2_chain": [u32, P, P, P, P, P, i32, i32, i32, i32, P, P, P],
             "orc_sstep_gs2_block": [u32, P, P, P, P, P, i32, i32, i32, P, P, i32, P],
             "orc_from_coo": [u32, u32, u64, P, P, P, P, P, P, P, P],
+            "orc_poly_apply": [u32, P, P, P, P, P, i32, i32, i32, i32, P, P, i32, P, P],
         }
         res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
                "orc_wavefront_schedule": u64, "orc_permute_vector": None,
@@ -222,6 +223,23 @@ class Oracle:
         self.lib.orc_jacobi_op(len(rp) - 1, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), sweeps,
                                _p(x), _p(y))
         return y
+
+    def poly_apply(self, rp, ci, v, roots, x, inner="none", sweeps=1, gamma=1, forward=True):
+        """poly.hpp:146-281: z = p(A M^{-1}) x for the given roots (product form)."""
+        rp, ci, v, x = _u32(rp), _u32(ci), _f64(v), _f64(x)
+        n = len(rp) - 1
+        if inner == "none":
+            pos, inv = np.zeros(n, np.uint32), np.zeros(n)
+        else:
+            pos, inv = self.diag_info(rp, ci, v)
+        re, im = self._shifts(roots)
+        z = np.empty(n)
+        kind = {"none": 0, "jacobi": 1, "gs2": 2}[inner]
+        rc = self.lib.orc_poly_apply(n, _p(rp), _p(ci), _p(v), _p(pos), _p(inv), kind, sweeps, gamma,
+                                     1 if forward else 0, _p(re), _p(im), len(re), _p(x), _p(z))
+        if rc:
+            raise ValueError("poly: conjugate pair not adjacent")
+        return z
 
     def from_coo(self, n_rows, n_cols, rows, cols, vals):
         """csr.hpp:72-110 -> (row_ptr, col_idx, values); ValueError (index, bad entry) if out of range."""

@@ -80,6 +80,8 @@ _SIGS = {
     "mpkg_gs2_op": [P, P, P, P, P, P],
     "mpkg_gs2_run_dev": [P, P, P, P, i32, P, P, P],
     "mpkg_sstep_gs2": [P, P, P, P, P, P, i32, P, u64, u64],
+    "mpkg_poly_apply": [P, P, P, P, P, P, i32, P, P, P],
+    "mpkg_poly_apply_dev": [P, P, P, P, P, P, i32, P, P, P],
     "mpkg_sstep_gs2_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],

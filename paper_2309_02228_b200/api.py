@@ -666,6 +666,18 @@ class Context:
                                  _ptr(re), _ptr(im), k, _ptr(blk.data), n, k + 1))
         return blk
 
+    # ---- product-form polynomial (poly.hpp:146-281) ---------------------------------------------
+    def poly_apply(self, A: DeviceCsr, roots, v, inner=None, plan=None) -> np.ndarray:
+        """z = p(A M^{-1}) v for the given roots; inner: None, a JacobiPrecon or a Gs2Precon."""
+        r = np.asarray(list(roots), dtype=np.complex128)
+        re, im = _f64(r.real), _f64(r.imag)
+        J = inner.h if isinstance(inner, JacobiPrecon) else None
+        G = inner.h if isinstance(inner, Gs2Precon) else None
+        z = np.empty(A.n_rows)
+        check(lib.mpkg_poly_apply(self.h, A.h, J, G, _ptr(re), _ptr(im), len(re),
+                                  plan.h if plan is not None else None, _ptr(_f64(v)), _ptr(z)))
+        return z
+
     def tune_p(self, ls: LevelStructure, A_perm: DeviceCsr, cache_bytes: int, p_lo: int,
                p_hi: int, reps: int = 3) -> TuneResult:  # mpk.hpp:238
         if p_lo < 1 or p_hi < p_lo:

@@ -1314,3 +1314,56 @@ int mpkg_sstep_gs2_dev(mpkg_ctx_t ctx, mpkg_gs2_t G, mpkg_plan_t P, mpkg_csr_t A
 }
 
 }  // extern "C"
+
+namespace {
+void poly_run(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G, const double* re,
+              const double* im, int degree, mpkg_plan_t P, const double* d_v, double* d_z) {
+    require(ctx && A, "poly_apply: null argument");
+    require(!(J && G), "poly_apply: one inner preconditioner at most");
+    require(A->n_rows == A->n_cols, "poly_apply: matrix must be square");
+    require(degree >= 1 && re && im, "poly_apply: preconditioner not set up");     // poly.hpp:235-236
+    require(!G || G->sweeps == 1, "poly_apply: gs2 inner must use a single sweep");  // poly.hpp:237-238
+    require(!J || J->n == A->n_rows, "poly_apply: size mismatch");
+    require(!G || G->diag.n == A->n_rows, "poly_apply: size mismatch");
+    std::vector<uint8_t> role(degree);  // poly.hpp:77-93 poly_roles
+    for (int i = 0; i < degree;) {
+        if (im[i] == 0.0) {
+            role[i++] = 0;
+            continue;
+        }
+        require(i + 1 < degree && re[i + 1] == re[i] && im[i + 1] == -im[i], "poly: conjugate pair not adjacent");
+        role[i] = 1, role[i + 1] = 2;
+        i += 2;
+    }
+    if (P) {  // poly.hpp:255-260
+        require(P->n_rows == A->n_rows, "poly_apply: plan does not match matrix");
+        const int sub = J ? (J->sweeps == 1 ? 1 : J->sweeps + 1) : (G ? G->gamma + 2 : 1);
+        require(P->sub_powers == sub, "poly_apply: plan sub_powers mismatch");
+    }
+    use_device(ctx);
+    gpu_poly_apply(ctx, A, J, G, re, im, role.data(), degree, d_v, d_z);
+}
+}  // namespace
+
+extern "C" {
+
+int mpkg_poly_apply_dev(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G, const double* re,
+                        const double* im, int degree, mpkg_plan_t P, const double* d_v, double* d_z) {
+    return guarded([&] { poly_run(ctx, A, J, G, re, im, degree, P, d_v, d_z); });
+}
+
+int mpkg_poly_apply(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G, const double* re,
+                    const double* im, int degree, mpkg_plan_t P, const double* v, double* z) {
+    return guarded([&] {
+        require(ctx && A && v && z, "poly_apply: null argument");
+        const uint32_t n = A->n_rows;
+        use_device(ctx);
+        DevBuf<double> buf(2ull * std::max<uint32_t>(n, 1));
+        if (n) MPKG_CUDA(cudaMemcpyAsync(buf.p, v, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+        poly_run(ctx, A, J, G, re, im, degree, P, buf.p, buf.p + n);
+        if (n) MPKG_CUDA(cudaMemcpyAsync(z, buf.p + n, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

@@ -243,6 +243,11 @@ void gpu_gs2_chain(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, const do
                    double* d_z, int terminal, double* d_out);
 void gpu_sstep_gs2(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, double* d_block,
                    uint64_t rows, int ns, const double* a, const double* b2);
+// poly.hpp:146-281 product-form polynomial; J / G select the inner preconditioner (both null:
+// none); role[i] 0 real, 1 / 2 first / second member of a conjugate pair.
+void gpu_poly_apply(mpkg_ctx_s* ctx, mpkg_csr_s* A, const mpkg_jacobi_s* J, const mpkg_gs2_s* G,
+                    const double* re, const double* im, const uint8_t* role, int degree,
+                    const double* d_v, double* d_z);
 
 // mpk_exec.cu
 struct FusedArgs {

@@ -173,6 +173,42 @@ double* chain_workspace(mpkg_ctx_s* ctx, uint64_t count) {
     return ctx->chain_ws.p;
 }
 
+// Product-form polynomial terminal (poly.hpp:200-224): t = A z_src (scaled for the fused
+// one-sweep Jacobi inner), then the root update for the power's role (0 real, 1 first / 2 second
+// member of a conjugate pair) into w_out and the accumulated result acc.
+template <bool FUSED>
+__global__ void __launch_bounds__(256) k_poly_terminal(
+    const uint32_t* __restrict__ cols, const double* __restrict__ vals,
+    const uint64_t* __restrict__ chunk_off, const uint32_t* __restrict__ row_len, uint32_t n,
+    const double* __restrict__ z_src, const double* __restrict__ d, int role, double re, double mod,
+    const double* __restrict__ w_in, const double* __restrict__ w_pm2, double* __restrict__ w_out,
+    double* __restrict__ acc) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t len = row_len[r];
+        const uint64_t off = chunk_off[r >> 5];
+        const uint32_t L = (uint32_t)((chunk_off[(r >> 5) + 1] - off) >> 5);
+        const double t = pc_row_dot<FUSED ? kScaled : kPlain>(cols, vals, off, L, (uint32_t)(r & 31), len,
+                                                             z_src, d, 0u);
+        if (role == 0) {
+            acc[r] = __dadd_rn(acc[r], __ddiv_rn(w_in[r], re));
+            w_out[r] = __dsub_rn(w_in[r], __ddiv_rn(t, re));
+        } else if (role == 1) {
+            const double u = __dsub_rn(__dmul_rn(__dmul_rn(2.0, re), w_in[r]), t);
+            w_out[r] = u;
+            acc[r] = __dadd_rn(acc[r], __ddiv_rn(u, mod));
+        } else {
+            w_out[r] = __dsub_rn(w_pm2[r], __ddiv_rn(t, mod));
+        }
+    }
+}
+
+__global__ void k_poly_tail(uint32_t n, const double* __restrict__ w, double th, double* __restrict__ acc) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x)
+        acc[r] = __dadd_rn(acc[r], __ddiv_rn(w[r], th));
+}
+
 struct Stage {
     mpkg_ctx_s* ctx;
     const Sell& S;
@@ -237,6 +273,25 @@ void gs2_sweeps(const Stage& st, const mpkg_gs2_s* G, const double* v, double* z
     }
 }
 
+// One zero-guess GS2 sweep z[0] (all zero) -> z[1] with the g bank (the polynomial's inner,
+// poly.hpp:168-187).
+void gs2_single_sweep(const Stage& st, const mpkg_gs2_s* G, const double* v, double* z, double* g) {
+    const uint32_t n = st.n;
+    auto launch = [&](auto inner, const double* src, double* gout, double* zn) {
+        constexpr bool I = decltype(inner)::value;
+        const auto ev = timing_begin(st.ctx);
+        k_gs2_stage<I><<<st.grid(), 256, 0, st.ctx->stream>>>(
+            st.S.cols.p, st.S.vals.p, st.S.chunk_off.p, st.S.row_len.p, n, src, G->diag.inv.p,
+            G->diag.kdiag.p, G->forward, v, g, gout, z, zn);
+        MPKG_LAUNCH_CHECK();
+        timing_end(st.ctx, ev);
+        st.ctx->launches += 1;
+    };
+    launch(std::false_type{}, z, g, G->gamma == 0 ? z + n : nullptr);
+    for (int j = 1; j <= G->gamma; ++j)
+        launch(std::true_type{}, g + (uint64_t)(j - 1) * n, g + (uint64_t)j * n, j == G->gamma ? z + n : nullptr);
+}
+
 }  // namespace
 
 void gpu_gs2_chain(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, const double* d_v,
@@ -274,6 +329,63 @@ void gpu_sstep_gs2(mpkg_ctx_s* ctx, const mpkg_gs2_s* G, mpkg_csr_s* A, double* 
         gs2_sweeps(st, G, src, zb, gb);
         stage<kPlain, kEpiShift>(st, zb + (uint64_t)G->sweeps * n, &G->diag, nullptr, src, src2,
                                  a[p - 1], b2[p - 1], d_block + (uint64_t)p * rows);
+    }
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void gpu_poly_apply(mpkg_ctx_s* ctx, mpkg_csr_s* A, const mpkg_jacobi_s* J, const mpkg_gs2_s* G,
+                    const double* re, const double* im, const uint8_t* role, int degree,
+                    const double* d_v, double* d_z) {
+    const uint32_t n = A->n_rows;
+    if (n == 0) return;
+    const Stage st{ctx, csr_sell(A), n};
+    // workspace: degree w slices | 2 inner slices (Jacobi ping-pong or GS2 {zero, z1}) | g bank
+    const int gamma = G ? G->gamma : 0;
+    double* ws = chain_workspace(ctx, (uint64_t)(degree + 2 + gamma + 1) * n);
+    double* w = ws;
+    double* zb = ws + (uint64_t)degree * n;
+    double* gb = zb + 2ull * n;
+    MPKG_CUDA(cudaMemcpyAsync(w, d_v, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    MPKG_CUDA(cudaMemsetAsync(d_z, 0, 8ull * n, ctx->stream));
+    if (G) MPKG_CUDA(cudaMemsetAsync(zb, 0, 8ull * n, ctx->stream));  // GS2's permanent zero guess
+    for (int pw = 1; pw <= degree - 1; ++pw) {
+        const double* w_in = w + (uint64_t)(pw - 1) * n;
+        const double* z_src = w_in;
+        bool fused = false;
+        const double* dinv = nullptr;
+        if (J) {  // poly.hpp:150-167
+            if (J->sweeps == 1) {
+                fused = true;
+                dinv = J->inv.p;
+            } else {
+                z_src = jacobi_chain(ctx, J, st, w_in, zb, zb + n);
+            }
+        } else if (G) {  // poly.hpp:168-187: one zero-guess GS2 sweep into zb[1]
+            gs2_single_sweep(st, G, w_in, zb, gb);
+            z_src = zb + n;
+        }
+        const double th = re[pw - 1];
+        const double mod = th * th + im[pw - 1] * im[pw - 1];  // poly.hpp:193 (host, no FMA)
+        const double* w_pm2 = pw >= 2 ? w + (uint64_t)(pw - 2) * n : w_in;
+        double* w_out = w + (uint64_t)pw * n;
+        const auto ev = timing_begin(ctx);
+        if (fused)
+            k_poly_terminal<true><<<st.grid(), 256, 0, ctx->stream>>>(
+                st.S.cols.p, st.S.vals.p, st.S.chunk_off.p, st.S.row_len.p, n, z_src, dinv, role[pw - 1], th,
+                mod, w_in, w_pm2, w_out, d_z);
+        else
+            k_poly_terminal<false><<<st.grid(), 256, 0, ctx->stream>>>(
+                st.S.cols.p, st.S.vals.p, st.S.chunk_off.p, st.S.row_len.p, n, z_src, nullptr, role[pw - 1], th,
+                mod, w_in, w_pm2, w_out, d_z);
+        MPKG_LAUNCH_CHECK();
+        timing_end(ctx, ev);
+        ctx->launches += 1;
+    }
+    if (role[degree - 1] == 0) {  // poly.hpp:271-278 trailing real root
+        k_poly_tail<<<grid_for(n, 256, (unsigned)ctx->sm_count * 8u), 256, 0, ctx->stream>>>(
+            n, w + (uint64_t)(degree - 1) * n, re[degree - 1], d_z);
+        MPKG_LAUNCH_CHECK();
+        ctx->launches += 1;
     }
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }

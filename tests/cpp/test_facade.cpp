@@ -569,10 +569,58 @@ static void test_gs2() {
     }
 }
 
+// proj/tests/test_poly.cpp with the roots given (the reference's Eigen-based setup is not part of
+// this library): ScaledIdentityDegreeOne, exactness on a known spectrum (real and complex pair),
+// blocked == sequential with root slicing, plan shape mismatch.
+static void test_poly() {
+    using cplx = std::complex<double>;
+    {
+        CsrMatrix a = mpk::from_coo(2, 2, {{0, 0, 2.0}, {1, 1, 2.0}});
+        mpk::PolyPrecon exact;
+        exact.theta = {cplx(2.0, 0.0)};
+        exact.degree = 1;
+        std::vector<double> z;
+        mpk::poly_apply(exact, a, {4.0, 6.0}, z);
+        EXPECT(z[0] == 2.0 && z[1] == 3.0);
+    }
+    {  // eigenvalues 1 +- 2i and 3: A z = v when the roots are the spectrum
+        const CsrMatrix a = mpk::from_coo(3, 3, {{0, 0, 1.0}, {0, 1, -2.0}, {1, 0, 2.0}, {1, 1, 1.0}, {2, 2, 3.0}});
+        mpk::PolyPrecon p;
+        p.theta = {cplx(3.0, 0.0), cplx(1.0, 2.0), cplx(1.0, -2.0)};
+        p.degree = 3;
+        const std::vector<double> v = {0.3, -0.7, 1.1};
+        std::vector<double> z, az(3);
+        mpk::poly_apply(p, a, v, z);
+        mpk::spmv(a, z, az);
+        EXPECT(max_err(az, v) <= 1e-10);
+    }
+    {
+        const CsrMatrix a = mpk::poisson2d(48, 48);
+        const std::vector<double> v = random_vector(a.n_rows, 95);
+        const LevelStructure ls = mpk::build_levels(a);
+        const CsrMatrix ap = mpk::permute(a, ls.perm);
+        mpk::PolyPrecon p;
+        p.theta = {cplx(7.5, 0), cplx(0.3, 0), cplx(4.0, 1.0), cplx(4.0, -1.0), cplx(2.0, 0), cplx(6.0, 0),
+                   cplx(1.0, 0.5), cplx(1.0, -0.5)};
+        p.degree = 8;
+        ExecutionPlan plan = mpk::group_levels(ls, ap, 16 * 1024, 3);  // p_m 3 < 7 powers: slicing
+        plan.sub_powers = mpk::poly_sub_powers(p);
+        plan.invalidate();
+        std::vector<double> z_seq, z_blk;
+        mpk::poly_apply(p, ap, v, z_seq);
+        mpk::poly_apply_blocked(p, ap, plan, v, z_blk);
+        EXPECT(bitwise_equal(z_seq, z_blk));
+        plan.sub_powers = 3;
+        plan.invalidate();
+        EXPECT_THROW(mpk::poly_apply_blocked(p, ap, plan, v, z_blk), std::invalid_argument);
+    }
+}
+
 int main() {
     test_host_helpers();
     test_jacobi();
     test_gs2();
+    test_poly();
     test_levels();
     test_wavefront();
     test_mpk();

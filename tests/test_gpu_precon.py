@@ -154,3 +154,48 @@ def test_gs2_errors(ctx):
     with pytest.raises(ValueError, match="p_m"):  # s * sweeps > budget
         ctx.sstep_gs2(G, mpkg.ExecutionPlan.from_groups(30, [0, 30], p_m=3, sub_powers=4), A,
                       np.ones(30), [1.0, 2.0])
+
+
+# ---- product-form polynomial (poly.hpp:146-281) -------------------------------------------------
+ROOTS = {
+    "real": [4.0, 0.7, 2.5, 1.3],
+    "pairs": [3.5, 1.0 + 0.6j, 1.0 - 0.6j, 2.2, 0.9 + 0.2j, 0.9 - 0.2j],      # ends on a pair
+    "mixed": [2.0 + 1.0j, 2.0 - 1.0j, 0.8, 3.1, 1.7 + 0.3j, 1.7 - 0.3j, 1.1],  # trailing real root
+}
+
+
+@pytest.mark.parametrize("inner", ["none", "jacobi1", "jacobi3", "gs2_0", "gs2_2b"])
+def test_poly_apply_vs_oracle(ctx, oracle, inner):
+    for name, (P, lv, pm, ip, lp) in _cases(oracle).items():
+        Ap = ctx.csr(P)
+        x = mpkg.random_vector(P.n_rows, 17)
+        kw, prec = {}, None
+        if inner.startswith("jacobi"):
+            kw = dict(inner="jacobi", sweeps=int(inner[-1]))
+            prec = ctx.jacobi_setup(Ap, kw["sweeps"])
+        elif inner.startswith("gs2"):
+            kw = dict(inner="gs2", gamma=int(inner[4]), forward=not inner.endswith("b"))
+            prec = ctx.gs2_setup(Ap, kw["gamma"], 1, kw["forward"])
+        stages = 1 if prec is None else prec.stages()
+        ls = ctx.levels_from_host(lv, pm, ip, lp)
+        for rname, roots in ROOTS.items():
+            ref = oracle.poly_apply(P.row_ptr, P.col_idx, P.values, roots, x, **kw)
+            assert_bitwise(ctx.poly_apply(Ap, roots, x, prec), ref, f"{name} {inner} {rname}")
+            plan = ctx.group_levels(ls, Ap, 1 << 20, 3).with_sub_powers(stages, lp)  # root slicing
+            assert_bitwise(ctx.poly_apply(Ap, roots, x, prec, plan), ref, f"{name} {inner} {rname} plan")
+
+
+def test_poly_apply_errors(ctx):
+    A = ctx.csr(mpkg.poisson2d(6, 5))
+    with pytest.raises(ValueError, match="conjugate pair"):
+        ctx.poly_apply(A, [1.0 + 1.0j, 2.0], np.ones(30))
+    with pytest.raises(ValueError, match="not set up"):
+        ctx.poly_apply(A, [], np.ones(30))
+    G = ctx.gs2_setup(A, 1, 2)
+    with pytest.raises(ValueError, match="single sweep"):
+        ctx.poly_apply(A, [1.0], np.ones(30), G)
+    plan = mpkg.ExecutionPlan.from_groups(30, [0, 30], p_m=2, sub_powers=3)
+    with pytest.raises(ValueError, match="sub_powers"):
+        ctx.poly_apply(A, [1.0, 2.0], np.ones(30), None, plan)
+    z = ctx.poly_apply(ctx.csr(mpkg.HostCsr.from_arrays([0, 1, 2], [0, 1], [2.0, 2.0])), [2.0], [4.0, 6.0])
+    assert z.tolist() == [2.0, 3.0]  # test_poly.cpp:160-166

@@ -276,3 +276,74 @@ def test_from_coo_oracle_vs_reference(oracle, ref):
         assert_bitwise(a[2], b[4])
     with pytest.raises(ValueError):
         oracle.from_coo(2, 2, [0, 2], [0, 0], [1.0, 1.0])
+
+
+# ---- product-form polynomial (poly.hpp:146-281; the header needs Eigen, absent here) -------------
+def _dense(rp, ci, v, n):
+    D = np.zeros((n, n))
+    for r in range(n):
+        for k in range(rp[r], rp[r + 1]):
+            D[r, ci[k]] += v[k]
+    return D
+
+
+def test_poly_known_answers(oracle):
+    # test_poly.cpp:150-167 ScaledIdentityDegreeOne: root 2 on diag(2,2): z = v / 2 exactly
+    z = oracle.poly_apply([0, 1, 2], [0, 1], [2.0, 2.0], [2.0], [4.0, 6.0])
+    assert z.tolist() == [2.0, 3.0]
+    with pytest.raises(ValueError):  # poly.hpp:85-87: pair members must be adjacent conjugates
+        oracle.poly_apply([0, 1, 2], [0, 1], [2.0, 2.0], [1.0 + 1.0j, 2.0], [1.0, 1.0])
+
+
+@pytest.mark.parametrize("case", ["diag", "complex_pair"])
+def test_poly_exact_on_known_spectrum(oracle, case):
+    """Roots = the exact spectrum: the GMRES polynomial inverts A, i.e. A z = v (test_poly.cpp:
+    187-215 restated with the roots given instead of computed by the Eigen-based setup), and more
+    generally A z = v - prod_i (I - A / theta_i) v for any roots."""
+    if case == "diag":
+        eigs = [1.0, 2.5, 3.0, 4.2, 5.0, 6.7]
+        n = 12
+        d = [eigs[i % 6] for i in range(n)]
+        rp, ci, v = list(range(n + 1)), list(range(n)), d
+        roots = [6.7, 1.0, 5.0, 2.5, 4.2, 3.0]
+    else:  # eigenvalues 1 +- 2i and 3 (test_poly.cpp:202-215)
+        rp, ci, v = [0, 2, 4, 5], [0, 1, 0, 1, 2], [1.0, -2.0, 2.0, 1.0, 3.0]
+        n = 3
+        roots = [3.0, 1.0 + 2.0j, 1.0 - 2.0j]
+    A = _dense(rp, ci, v, n)
+    x = np.linspace(-1.0, 1.3, n)
+    z = oracle.poly_apply(rp, ci, v, roots, x)
+    assert np.max(np.abs(A @ z - x)) <= 1e-10 * np.max(np.abs(x))
+    # the residual-polynomial identity with arbitrary (non-spectral) roots
+    roots2 = [0.7, 2.0 + 0.5j, 2.0 - 0.5j, 4.0]
+    z2 = oracle.poly_apply(rp, ci, v, roots2, x)
+    R = x.astype(complex)
+    for th in roots2:
+        R = R - (A @ R) / th
+    assert np.max(np.abs(A @ z2 - (x - R.real))) <= 1e-12 * max(1.0, np.max(np.abs(x)))
+
+
+def test_poly_inner_preconditioned_identity(oracle):
+    """Inner Jacobi / GS2: the same identity for the combined operator A M^{-1} (M^{-1} from the
+    pinned jacobi_apply / gs2 stages)."""
+    A_ = __import__("paper_2309_02228_b200").random_spd(60, 4, 17)
+    rp, ci, v = A_.row_ptr, A_.col_idx, A_.values
+    n = A_.n_rows
+    A = _dense(rp, ci, v, n)
+    x = np.cos(0.3 * np.arange(n))
+    roots = [0.9, 1.6 + 0.4j, 1.6 - 0.4j, 0.5, 1.2]
+    for inner, kw in (("jacobi", dict(sweeps=1)), ("jacobi", dict(sweeps=3)),
+                      ("gs2", dict(gamma=0)), ("gs2", dict(gamma=2, forward=False))):
+        z = oracle.poly_apply(rp, ci, v, roots, x, inner=inner, **kw)
+
+        def minv(y):
+            if inner == "jacobi":
+                return oracle.jacobi_apply(rp, ci, v, kw["sweeps"], y)
+            return oracle.gs2(rp, ci, v, kw["gamma"], 1, kw.get("forward", True), "apply", y)[0]
+
+        R = x.astype(complex)
+        for th in roots:
+            op = (A @ minv(R.real)) + 1j * (A @ minv(R.imag))
+            R = R - op / th
+        lhs = A @ minv(z)
+        assert np.max(np.abs(lhs - (x - R.real))) <= 1e-11 * max(1.0, np.max(np.abs(x))), inner
