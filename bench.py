@@ -247,6 +247,11 @@ def run_reference(args, cfgd):
     if not reference_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref/libmpkref.so not built"}), flush=True)
         return
+    if cfgd["kind"] in CHAIN_KINDS:
+        print(json.dumps({**base, "unavailable": "the reference's s-step / polynomial drivers "
+                          "(sstep.hpp, poly.hpp) need Eigen, which is not installed; only their "
+                          "jacobi.hpp / gs2.hpp stages compile (oracle/_ref)"}), flush=True)
+        return
     R = Reference()
     A = make_matrix(args.config, args.seed)
     cache = host_llc_bytes()
