@@ -314,6 +314,40 @@ int mpkg_poly_apply_dev(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_
                         const double* re, const double* im, int degree, mpkg_plan_t P,
                         const double* d_v, double* d_z);
 
+/* ---- block orthogonalisation (ortho.hpp) --------------------------------
+ * Blocks are column-major with leading dimension `rows` (consecutive VectorBlock slices).  The
+ * plain names take host pointers (synchronous, as the reference); _dev take device pointers and
+ * run on the context's stream.
+ *
+ * ortho.hpp:46-63 block_dots: C (qcols x vcols, column-major) = Q^T V.  MPKG_MODE_BITWISE: every
+ * entry is the reference's serial ascending-row sum (bit-identical); MPKG_MODE_FAST: fp64 tensor
+ * cores with a fixed-order reduction (deterministic, roundoff-level difference). */
+int mpkg_block_dots(mpkg_ctx_t ctx, const double* q, const double* v, uint64_t rows, uint32_t qcols,
+                    uint32_t vcols, double* c);
+int mpkg_block_dots_dev(mpkg_ctx_t ctx, const double* d_q, const double* d_v, uint64_t rows,
+                        uint32_t qcols, uint32_t vcols, double* d_c);
+/* ortho.hpp:67-92 block_update: V <- V - Q C, every element updated in ascending k with mul then
+ * sub (bit-identical in both modes). */
+int mpkg_block_update(mpkg_ctx_t ctx, const double* q, const double* c, uint64_t rows,
+                      uint32_t qcols, uint32_t vcols, double* v);
+int mpkg_block_update_dev(mpkg_ctx_t ctx, const double* d_q, const double* d_c, uint64_t rows,
+                          uint32_t qcols, uint32_t vcols, double* d_v);
+/* ortho.hpp:97-117 icgs_block_orthogonalize: `sweeps` rounds of dots + update; coeff
+ * (qcols x vcols, column-major) receives the accumulated coefficients.  qcols == 0 or vcols == 0
+ * returns at once (nothing written); otherwise MPKG_EINVAL if sweeps < 1. */
+int mpkg_icgs_block_orthogonalize(mpkg_ctx_t ctx, const double* q, uint64_t rows, uint32_t qcols,
+                                  double* v, uint32_t vcols, int sweeps, double* coeff);
+int mpkg_icgs_block_orthogonalize_dev(mpkg_ctx_t ctx, const double* d_q, uint64_t rows,
+                                      uint32_t qcols, double* d_v, uint32_t vcols, int sweeps,
+                                      double* d_coeff);
+/* ortho.hpp:136-229 tsqr: V (rows x cols) is overwritten with Q (orthonormal columns), r
+ * (cols x cols, column-major) with the upper-triangular R (non-negative diagonal, zero below),
+ * Q R = V_in.  Panels are chosen by the library (shared-memory sized); the factorisation is
+ * unique for a full-rank block, so it agrees with the reference's panel tree to roundoff.
+ * MPKG_EINVAL if rows < cols or cols > 64; cols == 0 returns at once. */
+int mpkg_tsqr(mpkg_ctx_t ctx, double* v, uint64_t rows, uint32_t cols, double* r);
+int mpkg_tsqr_dev(mpkg_ctx_t ctx, double* d_v, uint64_t rows, uint32_t cols, double* d_r);
+
 /* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
 /* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]
  *        4 random_csr(a=n, b=nnz_per_row, seed) 5 random_spd(a, b, seed) [generators.hpp:96-146]

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <complex>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -785,6 +786,56 @@ TuneResult tune_p(int p_lo, int p_hi, TrialFn&& trial) {
 }
 
 /// mpk.hpp:238-258 (GPU timing with CUDA events)
+// ---- block orthogonalisation (ortho.hpp) -------------------------------
+// Same signatures as the reference (column-major blocks, leading dimension rows).  `threads` is
+// accepted for drop-in compatibility; the device decides its own parallelism.  block_dots is
+// bit-identical to the reference in MPKG_MODE_BITWISE (the default); block_update always.
+
+// ortho.hpp:46-63
+inline void block_dots(const double* q, const double* v, std::size_t rows, std::size_t qcols,
+                       std::size_t vcols, double* c, int threads = 0) {
+    (void)threads;
+    detail::check(mpkg_block_dots(device_context(), q, v, rows, static_cast<std::uint32_t>(qcols),
+                          static_cast<std::uint32_t>(vcols), c));
+}
+
+// ortho.hpp:67-92
+inline void block_update(const double* q, const double* c, std::size_t rows, std::size_t qcols,
+                         std::size_t vcols, double* v, int threads = 0) {
+    (void)threads;
+    detail::check(mpkg_block_update(device_context(), q, c, rows, static_cast<std::uint32_t>(qcols),
+                            static_cast<std::uint32_t>(vcols), v));
+}
+
+// ortho.hpp:97-117
+inline std::vector<double> icgs_block_orthogonalize(const double* q, std::size_t rows,
+                                                    std::size_t qcols, double* v,
+                                                    std::size_t vcols, int sweeps,
+                                                    int threads = 0) {
+    (void)threads;
+    std::vector<double> coeff(qcols * vcols, 0.0);
+    detail::check(mpkg_icgs_block_orthogonalize(device_context(), q, rows, static_cast<std::uint32_t>(qcols),
+                                        v, static_cast<std::uint32_t>(vcols), sweeps,
+                                        coeff.empty() ? nullptr : coeff.data()));
+    return coeff;
+}
+
+// ortho.hpp:136-229.  panel_rows is accepted for compatibility: the device sizes its panels to
+// shared memory; (Q, R) with a non-negative R diagonal is unique, so the result agrees with any
+// panel tree to roundoff.
+inline void tsqr(double* v, std::size_t rows, std::size_t cols, double* r,
+                 std::size_t panel_rows = 4096, int threads = 0) {
+    (void)panel_rows, (void)threads;
+    detail::check(mpkg_tsqr(device_context(), v, rows, static_cast<std::uint32_t>(cols), r));
+}
+
+// ortho.hpp:231-240
+inline bool tsqr_rank_deficient(const double* r, std::size_t cols, double threshold) {
+    for (std::size_t j = 0; j < cols; ++j)
+        if (std::abs(r[j * cols + j]) < threshold) return true;
+    return false;
+}
+
 inline TuneResult tune_p(const LevelStructure& ls, const CsrMatrix& A_perm,
                          std::size_t cache_bytes, int p_lo, int p_hi, int /*threads*/ = 0,
                          int reps = 3) {

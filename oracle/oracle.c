@@ -7,6 +7,7 @@
  */
 #include "oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -739,5 +740,108 @@ int orc_poly_apply(uint32_t n, const uint32_t* rp, const uint32_t* ci, const dou
     free(zb);
     free(gb);
     free(t);
+    return ORC_OK;
+}
+
+/* ---- block orthogonalisation (ortho.hpp) ------------------------------------------------ */
+
+void orc_block_dots(const double* q, const double* v, uint64_t rows, uint32_t qcols,
+                    uint32_t vcols, double* c) {
+    /* ortho.hpp:49-62: entry e = (k = e % qcols, j = e / qcols), serial over the rows */
+    for (uint64_t e = 0; e < (uint64_t)qcols * vcols; ++e) {
+        const double* qk = q + (e % qcols) * rows;
+        const double* vj = v + (e / qcols) * rows;
+        double acc = 0.0;
+        for (uint64_t i = 0; i < rows; ++i) acc += qk[i] * vj[i];
+        c[e] = acc;
+    }
+}
+
+void orc_block_update(const double* q, const double* c, uint64_t rows, uint32_t qcols,
+                      uint32_t vcols, double* v) {
+    /* ortho.hpp:80-90 with one thread: for j, for k ascending, for i */
+    for (uint32_t j = 0; j < vcols; ++j) {
+        double* vj = v + (uint64_t)j * rows;
+        for (uint32_t k = 0; k < qcols; ++k) {
+            const double ck = c[(uint64_t)j * qcols + k];
+            const double* qk = q + (uint64_t)k * rows;
+            for (uint64_t i = 0; i < rows; ++i) vj[i] -= ck * qk[i];
+        }
+    }
+}
+
+int orc_icgs(const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+             int sweeps, double* coeff) {
+    const uint64_t ne = (uint64_t)qcols * vcols;
+    if (ne == 0) return ORC_OK;             /* ortho.hpp:102-104 */
+    if (sweeps < 1) return ORC_EINVAL;      /* ortho.hpp:105-107 */
+    double* c = (double*)malloc(sizeof(double) * ne);
+    for (uint64_t e = 0; e < ne; ++e) coeff[e] = 0.0;
+    for (int sw = 0; sw < sweeps; ++sw) {   /* ortho.hpp:110-115 */
+        orc_block_dots(q, v, rows, qcols, vcols, c);
+        orc_block_update(q, c, rows, qcols, vcols, v);
+        for (uint64_t e = 0; e < ne; ++e) coeff[e] += c[e];
+    }
+    free(c);
+    return ORC_OK;
+}
+
+int orc_tsqr(double* v, uint64_t rows, uint32_t cols, double* r) {
+    if (cols == 0) return ORC_OK;           /* ortho.hpp:148-150 */
+    if (rows < cols) return ORC_EINVAL;     /* ortho.hpp:151-153 */
+    const uint64_t c = cols;
+    double* tau = (double*)malloc(sizeof(double) * c);
+    double* a = v; /* factor in place: reflectors below the diagonal */
+    for (uint64_t j = 0; j < c; ++j) {
+        double* aj = a + j * rows;
+        double sigma = 0.0;
+        for (uint64_t i = j + 1; i < rows; ++i) sigma += aj[i] * aj[i];
+        const double alpha = aj[j];
+        double t = 0.0, beta = alpha;
+        if (sigma != 0.0) {
+            const double nrm = sqrt(alpha * alpha + sigma);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            t = (beta - alpha) / beta;
+            const double s = 1.0 / (alpha - beta);
+            for (uint64_t i = j + 1; i < rows; ++i) aj[i] *= s;
+        } else {
+            for (uint64_t i = j + 1; i < rows; ++i) aj[i] = 0.0;
+        }
+        aj[j] = beta;
+        tau[j] = t;
+        for (uint64_t l = j + 1; l < c && t != 0.0; ++l) {
+            double* al = a + l * rows;
+            double w = al[j];
+            for (uint64_t i = j + 1; i < rows; ++i) w += aj[i] * al[i];
+            w *= t;
+            al[j] -= w;
+            for (uint64_t i = j + 1; i < rows; ++i) al[i] -= w * aj[i];
+        }
+    }
+    /* R with the sign fix (ortho.hpp:204-212, 221-226) */
+    double* sg = (double*)malloc(sizeof(double) * c);
+    for (uint64_t j = 0; j < c; ++j) sg[j] = a[j * rows + j] < 0.0 ? -1.0 : 1.0;
+    for (uint64_t l = 0; l < c; ++l)
+        for (uint64_t i = 0; i < c; ++i) r[l * c + i] = i <= l ? sg[i] * a[l * rows + i] : 0.0;
+    /* explicit Q D = H_0 ... H_{c-1} [D; 0], applied right to left into a scratch block */
+    double* y = (double*)malloc(sizeof(double) * rows * c);
+    for (uint64_t l = 0; l < c; ++l)
+        for (uint64_t i = 0; i < rows; ++i) y[l * rows + i] = i == l ? sg[l] : 0.0;
+    for (uint64_t jj = c; jj-- > 0;) {
+        if (tau[jj] == 0.0) continue;
+        const double* h = a + jj * rows;
+        for (uint64_t l = 0; l < c; ++l) {
+            double* yl = y + l * rows;
+            double w = yl[jj];
+            for (uint64_t i = jj + 1; i < rows; ++i) w += h[i] * yl[i];
+            w *= tau[jj];
+            yl[jj] -= w;
+            for (uint64_t i = jj + 1; i < rows; ++i) yl[i] -= w * h[i];
+        }
+    }
+    memcpy(v, y, sizeof(double) * rows * c);
+    free(y);
+    free(sg);
+    free(tau);
     return ORC_OK;
 }

@@ -167,6 +167,28 @@ int orc_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t nnz, const uint32_t*
                  const uint32_t* cols, const double* vals, uint32_t* row_ptr, uint32_t* col_idx,
                  double* values, uint64_t* out_nnz, uint64_t* bad);
 
+/* ---- block orthogonalisation (ortho.hpp) ----------------------------
+ * ortho.hpp needs Eigen (absent here), so these restatements are pinned by the reference's own
+ * known-answer tests (test_ortho.cpp: exactly-orthogonal input untouched, coefficients that
+ * reconstruct a known projection, duplicates projecting to zero, tsqr bounds / identity R /
+ * rank deficiency / panel-tree agreement), restated in tests/test_oracle.py.
+ * Blocks are column-major with leading dimension rows. */
+/* ortho.hpp:46-63: c[j*qcols+k] = serial ascending sum of q_k[i] * v_j[i] from 0.0. */
+void orc_block_dots(const double* q, const double* v, uint64_t rows, uint32_t qcols,
+                    uint32_t vcols, double* c);
+/* ortho.hpp:67-92: v_j[i] -= c[j*qcols+k] * q_k[i] for k ascending. */
+void orc_block_update(const double* q, const double* c, uint64_t rows, uint32_t qcols,
+                      uint32_t vcols, double* v);
+/* ortho.hpp:97-117: `sweeps` x (dots, update), coeff accumulated from 0.0.  ORC_EINVAL if
+ * sweeps < 1 with a non-empty block; an empty one returns ORC_OK untouched. */
+int orc_icgs(const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+             int sweeps, double* coeff);
+/* ortho.hpp:136-229 tsqr, restated as one Householder QR of the whole block (LAPACK
+ * convention: beta = -sign(alpha) |x|, tau = (beta - alpha) / beta), then the sign fix to a
+ * non-negative R diagonal (ortho.hpp:204-212).  (Q, R) is unique for a full-rank block, so
+ * this equals the reference's panel tree to roundoff.  ORC_EINVAL if rows < cols. */
+int orc_tsqr(double* v, uint64_t rows, uint32_t cols, double* r);
+
 /* mpk.hpp:219-233: argmax over the table, ties toward the smaller p. */
 int orc_tune_select(const double* gflops, int p_lo, int p_hi);
 

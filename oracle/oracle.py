@@ -70,11 +70,16 @@ class Oracle:
             "orc_sstep_gs2_block": [u32, P, P, P, P, P, i32, i32, i32, P, P, i32, P],
             "orc_from_coo": [u32, u32, u64, P, P, P, P, P, P, P, P],
             "orc_poly_apply": [u32, P, P, P, P, P, i32, i32, i32, i32, P, P, i32, P, P],
+            "orc_block_dots": [P, P, u64, u32, u32, P],
+            "orc_block_update": [P, P, u64, u32, u32, P],
+            "orc_icgs": [P, u64, u32, P, u32, i32, P],
+            "orc_tsqr": [P, u64, u32, P],
         }
         res = {"orc_row_range_footprint": u64, "orc_greedy_group": u32,
                "orc_wavefront_schedule": u64, "orc_permute_vector": None,
                "orc_unpermute_vector": None, "orc_poly_combine": None,
-               "orc_jacobi_apply": None, "orc_jacobi_op": None, "orc_gs2_chain": None}
+               "orc_jacobi_apply": None, "orc_jacobi_op": None, "orc_gs2_chain": None,
+               "orc_block_dots": None, "orc_block_update": None}
         for k, v in sig.items():
             f = getattr(L, k)
             f.argtypes = v
@@ -240,6 +245,43 @@ class Oracle:
         if rc:
             raise ValueError("poly: conjugate pair not adjacent")
         return z
+
+    # ---- block orthogonalisation (ortho.hpp); blocks are (cols, rows) C-order = column-major
+    def block_dots(self, q, v):
+        """ortho.hpp:46-63: C = Q^T V as a (qcols, vcols) matrix.  Blocks are passed as
+        (cols, rows) arrays: row l of the array is column l of the block (column-major memory)."""
+        q, v = _f64(np.atleast_2d(q)), _f64(np.atleast_2d(v))
+        c = np.empty((v.shape[0], q.shape[0]))
+        self.lib.orc_block_dots(_p(q), _p(v), q.shape[1], q.shape[0], v.shape[0], _p(c))
+        return c.T
+
+    def block_update(self, q, c, v):
+        """ortho.hpp:67-92: returns V - Q C (v is not modified)."""
+        q, c = _f64(np.atleast_2d(q)), _f64(np.asarray(c).T)
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        self.lib.orc_block_update(_p(q), _p(c), q.shape[1], q.shape[0], out.shape[0], _p(out))
+        return out
+
+    def icgs(self, q, v, sweeps):
+        """ortho.hpp:97-117 -> (V orthogonalised, coefficients as a (qcols, vcols) matrix)."""
+        q = _f64(np.atleast_2d(q)) if q is not None and len(q) else np.zeros((0, 0))
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        qcols, rows = (q.shape[0], out.shape[1])
+        coeff = np.zeros((out.shape[0], qcols))
+        rc = self.lib.orc_icgs(_p(q) if qcols else None, rows, qcols, _p(out), out.shape[0], sweeps,
+                               _p(coeff))
+        if rc:
+            raise ValueError("icgs_block_orthogonalize: sweeps must be >= 1")
+        return out, coeff.T
+
+    def tsqr(self, v):
+        """ortho.hpp:136-229 -> (Q as a (cols, rows) block, R as a (cols, cols) matrix)."""
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        cols, rows = out.shape
+        r = np.zeros((cols, cols))
+        if self.lib.orc_tsqr(_p(out), rows, cols, _p(r)):
+            raise ValueError("tsqr: block must have at least as many rows as columns")
+        return out, r.T
 
     def from_coo(self, n_rows, n_cols, rows, cols, vals):
         """csr.hpp:72-110 -> (row_ptr, col_idx, values); ValueError (index, bad entry) if out of range."""
@@ -514,6 +556,43 @@ class Reference:
         self.lib.ref_csr_free(h)
         k = int(nnz[0])
         return int(nr[0]), int(nc[0]), rp, ci[:k].copy(), v[:k].copy()
+
+    # ---- block orthogonalisation (ortho.hpp); blocks are (cols, rows) C-order = column-major
+    def block_dots(self, q, v):
+        """ortho.hpp:46-63: C = Q^T V as a (qcols, vcols) matrix.  Blocks are passed as
+        (cols, rows) arrays: row l of the array is column l of the block (column-major memory)."""
+        q, v = _f64(np.atleast_2d(q)), _f64(np.atleast_2d(v))
+        c = np.empty((v.shape[0], q.shape[0]))
+        self.lib.orc_block_dots(_p(q), _p(v), q.shape[1], q.shape[0], v.shape[0], _p(c))
+        return c.T
+
+    def block_update(self, q, c, v):
+        """ortho.hpp:67-92: returns V - Q C (v is not modified)."""
+        q, c = _f64(np.atleast_2d(q)), _f64(np.asarray(c).T)
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        self.lib.orc_block_update(_p(q), _p(c), q.shape[1], q.shape[0], out.shape[0], _p(out))
+        return out
+
+    def icgs(self, q, v, sweeps):
+        """ortho.hpp:97-117 -> (V orthogonalised, coefficients as a (qcols, vcols) matrix)."""
+        q = _f64(np.atleast_2d(q)) if q is not None and len(q) else np.zeros((0, 0))
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        qcols, rows = (q.shape[0], out.shape[1])
+        coeff = np.zeros((out.shape[0], qcols))
+        rc = self.lib.orc_icgs(_p(q) if qcols else None, rows, qcols, _p(out), out.shape[0], sweeps,
+                               _p(coeff))
+        if rc:
+            raise ValueError("icgs_block_orthogonalize: sweeps must be >= 1")
+        return out, coeff.T
+
+    def tsqr(self, v):
+        """ortho.hpp:136-229 -> (Q as a (cols, rows) block, R as a (cols, cols) matrix)."""
+        out = np.array(np.atleast_2d(v), dtype=np.float64, order="C")
+        cols, rows = out.shape
+        r = np.zeros((cols, cols))
+        if self.lib.orc_tsqr(_p(out), rows, cols, _p(r)):
+            raise ValueError("tsqr: block must have at least as many rows as columns")
+        return out, r.T
 
     def from_coo(self, n_rows, n_cols, rows, cols, vals):
         r, c, v = _u32(rows), _u32(cols), _f64(vals)

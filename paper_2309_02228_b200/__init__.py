@@ -24,6 +24,7 @@ from .api import (  # noqa: F401
     random_csr,
     random_spd,
     random_vector,
+    tsqr_rank_deficient,
     rmat,
     scramble,
     stencil27,

@@ -82,6 +82,14 @@ _SIGS = {
     "mpkg_sstep_gs2": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_poly_apply": [P, P, P, P, P, P, i32, P, P, P],
     "mpkg_poly_apply_dev": [P, P, P, P, P, P, i32, P, P, P],
+    "mpkg_block_dots": [P, P, P, u64, u32, u32, P],
+    "mpkg_block_dots_dev": [P, P, P, u64, u32, u32, P],
+    "mpkg_block_update": [P, P, P, u64, u32, u32, P],
+    "mpkg_block_update_dev": [P, P, P, u64, u32, u32, P],
+    "mpkg_icgs_block_orthogonalize": [P, P, u64, u32, P, u32, i32, P],
+    "mpkg_icgs_block_orthogonalize_dev": [P, P, u64, u32, P, u32, i32, P],
+    "mpkg_tsqr": [P, P, u64, u32, P],
+    "mpkg_tsqr_dev": [P, P, u64, u32, P],
     "mpkg_sstep_gs2_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],

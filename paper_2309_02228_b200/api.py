@@ -129,6 +129,21 @@ def scramble(A: HostCsr, seed: int, return_perm: bool = False):
     return (B, perm) if return_perm else B
 
 
+def _block(a) -> np.ndarray:
+    return np.ascontiguousarray(np.atleast_2d(np.asarray(a, dtype=np.float64)))
+
+
+def _same_rows(a: np.ndarray, b: np.ndarray) -> None:
+    if a.shape[0] and b.shape[0] and a.shape[1] != b.shape[1]:
+        raise ValueError("ortho: blocks must have the same number of rows")
+
+
+def tsqr_rank_deficient(r, threshold: float) -> bool:
+    """ortho.hpp:231-240: any |R_jj| below the threshold."""
+    r = np.atleast_2d(np.asarray(r, dtype=np.float64))
+    return bool(np.any(np.abs(np.diag(r)) < threshold))
+
+
 def random_vector(n: int, seed: int) -> np.ndarray:
     """x_i ~ U[-1,1] from std::mt19937_64(seed) (acceptance.cpp:84-90)."""
     out = np.empty(n, np.float64)
@@ -677,6 +692,61 @@ class Context:
         check(lib.mpkg_poly_apply(self.h, A.h, J, G, _ptr(re), _ptr(im), len(re),
                                   plan.h if plan is not None else None, _ptr(_f64(v)), _ptr(z)))
         return z
+
+    # ---- block orthogonalisation (ortho.hpp) --------------------------
+    # Blocks are (cols, rows) float64 arrays: array row l is block column l (column-major memory,
+    # i.e. consecutive VectorBlock slices).  C and R are returned as ordinary matrices.
+    def block_dots(self, q, v) -> np.ndarray:
+        """ortho.hpp:46-63: C = Q^T V as a (qcols, vcols) matrix."""
+        q, v = _block(q), _block(v)
+        _same_rows(q, v)
+        c = np.zeros((v.shape[0], q.shape[0]))
+        check(lib.mpkg_block_dots(self.h, _ptr(q), _ptr(v), v.shape[1], q.shape[0], v.shape[0], _ptr(c)))
+        return c.T.copy()
+
+    def block_update(self, q, c, v) -> np.ndarray:
+        """ortho.hpp:67-92: returns V - Q C (c a (qcols, vcols) matrix); v is not modified."""
+        q, out = _block(q), np.array(_block(v), order="C")
+        _same_rows(q, out)
+        cc = _f64(np.asarray(c, dtype=np.float64).T)
+        if cc.shape != (out.shape[0], q.shape[0]):
+            raise ValueError("block_update: coefficient shape mismatch")
+        check(lib.mpkg_block_update(self.h, _ptr(q), _ptr(cc), out.shape[1], q.shape[0], out.shape[0],
+                                    _ptr(out)))
+        return out
+
+    def icgs_block_orthogonalize(self, q, v, sweeps: int):
+        """ortho.hpp:97-117 -> (V orthogonalised against Q, coefficients (qcols, vcols))."""
+        out = np.array(_block(v), order="C")
+        q = _block(q) if q is not None and np.size(q) else np.zeros((0, out.shape[1]))
+        _same_rows(q, out)
+        coeff = np.zeros((out.shape[0], q.shape[0]))
+        check(lib.mpkg_icgs_block_orthogonalize(self.h, _ptr(q) if q.size else None, out.shape[1],
+                                                q.shape[0], _ptr(out), out.shape[0], int(sweeps),
+                                                _ptr(coeff)))
+        return out, coeff.T.copy()
+
+    def tsqr(self, v):
+        """ortho.hpp:136-229 -> (Q as a (cols, rows) block, R (cols, cols) upper triangular with a
+        non-negative diagonal), Q R = V."""
+        out = np.array(_block(v), order="C")
+        cols, rows = out.shape
+        r = np.zeros((cols, cols))
+        check(lib.mpkg_tsqr(self.h, _ptr(out), rows, cols, _ptr(r)))
+        return out, r.T.copy()
+
+    def block_dots_dev(self, d_q: int, d_v: int, rows: int, qcols: int, vcols: int, d_c: int):
+        check(lib.mpkg_block_dots_dev(self.h, d_q, d_v, rows, qcols, vcols, d_c))
+
+    def block_update_dev(self, d_q: int, d_c: int, rows: int, qcols: int, vcols: int, d_v: int):
+        check(lib.mpkg_block_update_dev(self.h, d_q, d_c, rows, qcols, vcols, d_v))
+
+    def icgs_block_orthogonalize_dev(self, d_q: int, rows: int, qcols: int, d_v: int, vcols: int,
+                                     sweeps: int, d_coeff: int):
+        check(lib.mpkg_icgs_block_orthogonalize_dev(self.h, d_q, rows, qcols, d_v, vcols, sweeps, d_coeff))
+
+    def tsqr_dev(self, d_v: int, rows: int, cols: int, d_r: int):
+        check(lib.mpkg_tsqr_dev(self.h, d_v, rows, cols, d_r))
 
     def tune_p(self, ls: LevelStructure, A_perm: DeviceCsr, cache_bytes: int, p_lo: int,
                p_hi: int, reps: int = 3) -> TuneResult:  # mpk.hpp:238

@@ -1367,3 +1367,146 @@ int mpkg_poly_apply(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G,
 }
 
 }  // extern "C"
+
+// ---- block orthogonalisation (ortho.hpp) --------------------------------------------------
+namespace {
+using namespace mpkg_detail;
+
+void ortho_dims(uint64_t rows, uint32_t a, uint32_t b) {
+    require(rows < (1ull << 40) && (uint64_t)a * b < (1ull << 31), "ortho: block too large");
+}
+
+void icgs_check(mpkg_ctx_t ctx, const double* q, const double* v, uint64_t rows, uint32_t qcols, uint32_t vcols,
+                int sweeps, const double* coeff) {
+    require(ctx != nullptr, "icgs_block_orthogonalize: null context");
+    ortho_dims(rows, qcols, vcols);
+    if (qcols == 0 || vcols == 0) return;  // ortho.hpp:102-104: before the sweeps check
+    require(sweeps >= 1, "icgs_block_orthogonalize: sweeps must be >= 1");  // ortho.hpp:105-107
+    require(q && v && coeff, "icgs_block_orthogonalize: null argument");
+}
+
+void tsqr_check(mpkg_ctx_t ctx, const double* v, uint64_t rows, uint32_t cols, const double* r) {
+    require(ctx != nullptr, "tsqr: null context");
+    if (cols == 0) return;  // ortho.hpp:148-150
+    require(rows >= cols, "tsqr: block must have at least as many rows as columns");  // ortho.hpp:151-153
+    require(cols <= kTsqrMaxCols, "tsqr: at most 64 columns per block on the GPU");
+    ortho_dims(rows, cols, cols);
+    require(v && r, "tsqr: null argument");
+}
+
+// Host block of rows x cols doubles on the device for the duration of a host-pointer call.
+struct HostBlock {
+    DevBuf<double> d;
+    HostBlock(mpkg_ctx_t ctx, const double* h, uint64_t count) : d(std::max<uint64_t>(count, 1)) {
+        if (h && count) MPKG_CUDA(cudaMemcpyAsync(d.p, h, 8ull * count, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    void back(mpkg_ctx_t ctx, double* h, uint64_t count) {
+        if (count) MPKG_CUDA(cudaMemcpyAsync(h, d.p, 8ull * count, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int mpkg_block_dots_dev(mpkg_ctx_t ctx, const double* d_q, const double* d_v, uint64_t rows, uint32_t qcols,
+                        uint32_t vcols, double* d_c) {
+    return guarded([&] {
+        require(ctx != nullptr, "block_dots: null context");
+        ortho_dims(rows, qcols, vcols);
+        if (!qcols || !vcols) return;
+        require(d_q && d_v && d_c, "block_dots: null argument");
+        use_device(ctx);
+        gpu_block_dots(ctx, d_q, d_v, rows, qcols, vcols, d_c);
+    });
+}
+
+int mpkg_block_dots(mpkg_ctx_t ctx, const double* q, const double* v, uint64_t rows, uint32_t qcols,
+                    uint32_t vcols, double* c) {
+    return guarded([&] {
+        require(ctx != nullptr, "block_dots: null context");
+        ortho_dims(rows, qcols, vcols);
+        if (!qcols || !vcols) return;
+        require(q && v && c, "block_dots: null argument");
+        use_device(ctx);
+        HostBlock dq(ctx, q, rows * qcols), dv(ctx, v, rows * vcols), dc(ctx, nullptr, (uint64_t)qcols * vcols);
+        gpu_block_dots(ctx, dq.d.p, dv.d.p, rows, qcols, vcols, dc.d.p);
+        dc.back(ctx, c, (uint64_t)qcols * vcols);
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_block_update_dev(mpkg_ctx_t ctx, const double* d_q, const double* d_c, uint64_t rows, uint32_t qcols,
+                          uint32_t vcols, double* d_v) {
+    return guarded([&] {
+        require(ctx != nullptr, "block_update: null context");
+        ortho_dims(rows, qcols, vcols);
+        if (!qcols || !vcols) return;
+        require(d_q && d_c && d_v, "block_update: null argument");
+        use_device(ctx);
+        gpu_block_update(ctx, d_q, d_c, rows, qcols, vcols, d_v);
+    });
+}
+
+int mpkg_block_update(mpkg_ctx_t ctx, const double* q, const double* c, uint64_t rows, uint32_t qcols,
+                      uint32_t vcols, double* v) {
+    return guarded([&] {
+        require(ctx != nullptr, "block_update: null context");
+        ortho_dims(rows, qcols, vcols);
+        if (!qcols || !vcols) return;
+        require(q && c && v, "block_update: null argument");
+        use_device(ctx);
+        HostBlock dq(ctx, q, rows * qcols), dc(ctx, c, (uint64_t)qcols * vcols), dv(ctx, v, rows * vcols);
+        gpu_block_update(ctx, dq.d.p, dc.d.p, rows, qcols, vcols, dv.d.p);
+        dv.back(ctx, v, rows * vcols);
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_icgs_block_orthogonalize_dev(mpkg_ctx_t ctx, const double* d_q, uint64_t rows, uint32_t qcols,
+                                      double* d_v, uint32_t vcols, int sweeps, double* d_coeff) {
+    return guarded([&] {
+        icgs_check(ctx, d_q, d_v, rows, qcols, vcols, sweeps, d_coeff);
+        if (!qcols || !vcols) return;
+        use_device(ctx);
+        gpu_icgs(ctx, d_q, rows, qcols, d_v, vcols, sweeps, d_coeff);
+    });
+}
+
+int mpkg_icgs_block_orthogonalize(mpkg_ctx_t ctx, const double* q, uint64_t rows, uint32_t qcols, double* v,
+                                  uint32_t vcols, int sweeps, double* coeff) {
+    return guarded([&] {
+        icgs_check(ctx, q, v, rows, qcols, vcols, sweeps, coeff);
+        if (!qcols || !vcols) return;
+        use_device(ctx);
+        HostBlock dq(ctx, q, rows * qcols), dv(ctx, v, rows * vcols), dc(ctx, nullptr, (uint64_t)qcols * vcols);
+        gpu_icgs(ctx, dq.d.p, rows, qcols, dv.d.p, vcols, sweeps, dc.d.p);
+        dv.back(ctx, v, rows * vcols);
+        dc.back(ctx, coeff, (uint64_t)qcols * vcols);
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int mpkg_tsqr_dev(mpkg_ctx_t ctx, double* d_v, uint64_t rows, uint32_t cols, double* d_r) {
+    return guarded([&] {
+        tsqr_check(ctx, d_v, rows, cols, d_r);
+        if (!cols) return;
+        use_device(ctx);
+        gpu_tsqr(ctx, d_v, rows, cols, d_r);
+    });
+}
+
+int mpkg_tsqr(mpkg_ctx_t ctx, double* v, uint64_t rows, uint32_t cols, double* r) {
+    return guarded([&] {
+        tsqr_check(ctx, v, rows, cols, r);
+        if (!cols) return;
+        use_device(ctx);
+        HostBlock dv(ctx, v, rows * cols), dr(ctx, nullptr, (uint64_t)cols * cols);
+        gpu_tsqr(ctx, dv.d.p, rows, cols, dr.d.p);
+        dv.back(ctx, v, rows * cols);
+        dr.back(ctx, r, (uint64_t)cols * cols);
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

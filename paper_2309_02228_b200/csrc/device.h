@@ -270,4 +270,14 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
                uint32_t* pass_powers);
 void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
 
+// ortho.cu: block orthogonalisation (reference ortho.hpp)
+void gpu_block_dots(mpkg_ctx_s* ctx, const double* q, const double* v, uint64_t rows, uint32_t qcols,
+                    uint32_t vcols, double* c);
+void gpu_block_update(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_t rows, uint32_t qcols,
+                      uint32_t vcols, double* v);
+void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+              int sweeps, double* coeff);
+void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r);
+constexpr uint32_t kTsqrMaxCols = 64;
+
 }  // namespace mpkg_detail

@@ -616,7 +616,166 @@ static void test_poly() {
     }
 }
 
+// proj/tests/test_ortho.cpp (Tsqr / Icgs suites) through the facade; defects computed with
+// plain loops instead of Eigen.
+static double ortho_defect(const std::vector<double>& q, std::size_t rows, std::size_t cols) {
+    double m = 0.0;
+    for (std::size_t a = 0; a < cols; ++a)
+        for (std::size_t b = 0; b < cols; ++b) {
+            double s = 0.0;
+            for (std::size_t i = 0; i < rows; ++i) s += q[a * rows + i] * q[b * rows + i];
+            m = std::max(m, std::abs(s - (a == b ? 1.0 : 0.0)));
+        }
+    return m;
+}
+
+static double factorization_defect(const std::vector<double>& v, const std::vector<double>& q,
+                                   const std::vector<double>& r, std::size_t rows, std::size_t cols) {
+    double m = 0.0;
+    for (std::size_t j = 0; j < cols; ++j)
+        for (std::size_t i = 0; i < rows; ++i) {
+            double s = 0.0;
+            for (std::size_t k = 0; k < cols; ++k) s += q[k * rows + i] * r[j * cols + k];
+            m = std::max(m, std::abs(s - v[j * rows + i]));
+        }
+    return m;
+}
+
+static void test_ortho() {
+    {  // Tsqr.RandomBlockBounds
+        const std::size_t rows = 1000, cols = 4;
+        const std::vector<double> v_in = random_vector(rows * cols, 17);
+        std::vector<double> q = v_in, r(cols * cols);
+        mpk::tsqr(q.data(), rows, cols, r.data());
+        EXPECT(ortho_defect(q, rows, cols) <= 1e-13);
+        EXPECT(factorization_defect(v_in, q, r, rows, cols) <= 1e-13 * max_abs(v_in));
+        for (std::size_t j = 0; j < cols; ++j) {
+            EXPECT(r[j * cols + j] >= 0.0);
+            for (std::size_t i = j + 1; i < cols; ++i) EXPECT(r[j * cols + i] == 0.0);
+        }
+    }
+    {  // Tsqr.OrthonormalInputGivesIdentityR
+        const std::size_t rows = 600, cols = 5;
+        std::vector<double> q = random_vector(rows * cols, 3), r(cols * cols);
+        mpk::tsqr(q.data(), rows, cols, r.data());
+        mpk::tsqr(q.data(), rows, cols, r.data());
+        for (std::size_t j = 0; j < cols; ++j)
+            for (std::size_t i = 0; i < cols; ++i) EXPECT(std::abs(r[j * cols + i] - (i == j ? 1.0 : 0.0)) <= 1e-13);
+    }
+    {  // Tsqr.DuplicateColumnsFlagRankDeficiency
+        const std::size_t rows = 500, cols = 3;
+        std::vector<double> v = random_vector(rows * cols, 5);
+        std::copy_n(v.begin(), rows, v.begin() + rows);
+        const double vmax = max_abs(v);
+        std::vector<double> r(cols * cols);
+        mpk::tsqr(v.data(), rows, cols, r.data());
+        EXPECT(mpk::tsqr_rank_deficient(r.data(), cols, 1e-14 * vmax * std::sqrt(double(rows))));
+        const std::vector<double> full = {2.0, 0.0, 0.0, 1.0};
+        EXPECT(!mpk::tsqr_rank_deficient(full.data(), 2, 1e-14));
+    }
+    {  // Tsqr.PanelTreeMatchesSinglePanelToRoundoff
+        const std::size_t rows = 10000, cols = 5;
+        const std::vector<double> v_in = random_vector(rows * cols, 29);
+        std::vector<double> q_one = v_in, r_one(cols * cols), q_many = v_in, r_many(cols * cols);
+        mpk::tsqr(q_one.data(), rows, cols, r_one.data(), rows);
+        mpk::tsqr(q_many.data(), rows, cols, r_many.data(), 64);
+        EXPECT(ortho_defect(q_many, rows, cols) <= 1e-13);
+        EXPECT(factorization_defect(v_in, q_many, r_many, rows, cols) <= 1e-13 * max_abs(v_in));
+        double d = 0.0;
+        for (std::size_t e = 0; e < r_one.size(); ++e) d = std::max(d, std::abs(r_one[e] - r_many[e]));
+        EXPECT(d <= 1e-10 * max_abs(v_in));
+    }
+    {  // Tsqr.ThreadCountDoesNotChangeBits
+        const std::size_t rows = 8192, cols = 6;
+        const std::vector<double> v_in = random_vector(rows * cols, 41);
+        std::vector<double> q1 = v_in, r1(cols * cols);
+        mpk::tsqr(q1.data(), rows, cols, r1.data(), 1024, 1);
+        for (int threads : {2, 4, 8}) {
+            std::vector<double> q = v_in, r(cols * cols);
+            mpk::tsqr(q.data(), rows, cols, r.data(), 1024, threads);
+            EXPECT(bitwise_equal(q1, q) && bitwise_equal(r1, r));
+        }
+    }
+    {  // Tsqr.RejectsWideBlocks
+        std::vector<double> v(6, 1.0), r(9);
+        EXPECT_THROW(mpk::tsqr(v.data(), 2, 3, r.data()), std::invalid_argument);
+    }
+    {  // Icgs.ExactlyOrthogonalInputIsUntouched
+        const std::size_t rows = 64, qcols = 4, vcols = 2;
+        std::vector<double> q(rows * qcols, 0.0);
+        for (std::size_t k = 0; k < qcols; ++k) q[k * rows + k] = 1.0;
+        std::vector<double> v = random_vector(rows * vcols, 7);
+        for (std::size_t j = 0; j < vcols; ++j)
+            for (std::size_t k = 0; k < qcols; ++k) v[j * rows + k] = 0.0;
+        const std::vector<double> v_in = v;
+        auto coeff = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v.data(), vcols, 2);
+        for (double c : coeff) EXPECT(c == 0.0);
+        EXPECT(bitwise_equal(v, v_in));
+    }
+    {  // Icgs.DuplicateOfBasisColumnProjectsToZero
+        const std::size_t rows = 1000, qcols = 5;
+        std::vector<double> q = random_vector(rows * qcols, 11), r(qcols * qcols);
+        mpk::tsqr(q.data(), rows, qcols, r.data());
+        std::vector<double> v(q.begin(), q.begin() + rows);
+        auto coeff = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v.data(), 1, 1);
+        EXPECT(max_abs(v) <= 1e-13);
+        EXPECT(std::abs(coeff[0] - 1.0) <= 1e-12);
+        for (std::size_t k = 1; k < qcols; ++k) EXPECT(std::abs(coeff[k]) <= 1e-12);
+    }
+    {  // Icgs.CrossProductsAfterSweeps
+        const std::size_t rows = 1000, qcols = 8, vcols = 4;
+        std::vector<double> q = random_vector(rows * qcols, 13), rq(qcols * qcols);
+        mpk::tsqr(q.data(), rows, qcols, rq.data());
+        const std::vector<double> v_in = random_vector(rows * vcols, 19);
+        for (int sweeps : {1, 2}) {
+            std::vector<double> v = v_in, cross(qcols * vcols);
+            mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v.data(), vcols, sweeps);
+            mpk::block_dots(q.data(), v.data(), rows, qcols, vcols, cross.data());
+            EXPECT(max_abs(cross) <= (sweeps == 1 ? 1e-10 : 1e-12));
+        }
+    }
+    {  // Icgs.CoefficientsReconstructTheProjection
+        const std::size_t rows = 128, qcols = 3, vcols = 2;
+        std::vector<double> q(rows * qcols, 0.0);
+        for (std::size_t k = 0; k < qcols; ++k) q[k * rows + k] = 1.0;
+        const std::vector<double> c0 = {0.5, -2.0, 1.25, 3.0, 0.0, -0.75};
+        std::vector<double> w = random_vector(rows * vcols, 23);
+        for (std::size_t j = 0; j < vcols; ++j)
+            for (std::size_t k = 0; k < qcols; ++k) w[j * rows + k] = 0.0;
+        std::vector<double> v = w;
+        for (std::size_t j = 0; j < vcols; ++j)
+            for (std::size_t k = 0; k < qcols; ++k) v[j * rows + k] = c0[j * qcols + k];
+        auto coeff = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v.data(), vcols, 2);
+        double dc = 0.0, dv = 0.0;
+        for (std::size_t e = 0; e < c0.size(); ++e) dc = std::max(dc, std::abs(coeff[e] - c0[e]));
+        for (std::size_t e = 0; e < w.size(); ++e) dv = std::max(dv, std::abs(v[e] - w[e]));
+        EXPECT(dc <= 1e-15 && dv <= 1e-15);
+    }
+    {  // Icgs.ThreadCountDoesNotChangeBits
+        const std::size_t rows = 4096, qcols = 7, vcols = 3;
+        std::vector<double> q = random_vector(rows * qcols, 31), rq(qcols * qcols);
+        mpk::tsqr(q.data(), rows, qcols, rq.data());
+        const std::vector<double> v_in = random_vector(rows * vcols, 37);
+        std::vector<double> v1 = v_in;
+        auto c1 = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v1.data(), vcols, 2, 1);
+        for (int threads : {2, 4, 8}) {
+            std::vector<double> v = v_in;
+            auto c = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v.data(), vcols, 2, threads);
+            EXPECT(bitwise_equal(v1, v) && bitwise_equal(c1, c));
+        }
+    }
+    {  // Icgs.RejectsNonPositiveSweeps / EmptyBasisReturnsEmptyCoefficients
+        std::vector<double> q(8, 0.0), v(8, 1.0);
+        EXPECT_THROW(mpk::icgs_block_orthogonalize(q.data(), 8, 1, v.data(), 1, 0), std::invalid_argument);
+        std::vector<double> e = random_vector(64, 43);
+        const std::vector<double> e_in = e;
+        auto coeff = mpk::icgs_block_orthogonalize(nullptr, 32, 0, e.data(), 2, 1);
+        EXPECT(coeff.empty() && bitwise_equal(e, e_in));
+    }
+}
+
 int main() {
+    test_ortho();
     test_host_helpers();
     test_jacobi();
     test_gs2();
