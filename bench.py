@@ -58,6 +58,11 @@ CONFIGS["c4prod"] = dict(desc="C4 matrix, product-form GMRES polynomial z = p(A)
                               "(roots: Leja-ordered Chebyshev points on [0.5, 52] standing in for "
                               "the Eigen-computed harmonic Ritz values)", p=40, kind="polyprod")
 
+CONFIGS["c4ortho"] = dict(desc="C4-sized s-step block orthogonalisation (sstep.hpp:539-545): ICGS of an "
+                               "s=8 Newton block against a 25-column basis (2 sweeps, ortho_sweeps=1), "
+                               "then TSQR of the block; n = 192^3 rows", p=8, kind="ortho",
+                          qcols=25, sweeps=2)
+
 CHAIN_KINDS = ("sstep_jacobi", "sstep_gs2", "polyprod")
 
 
@@ -247,6 +252,11 @@ def run_reference(args, cfgd):
     if not reference_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref/libmpkref.so not built"}), flush=True)
         return
+    if cfgd["kind"] == "ortho":
+        print(json.dumps({**base, "unavailable": "the reference's ortho.hpp needs Eigen, which is "
+                          "not installed; its algorithm is restated in oracle/oracle.c (pinned by "
+                          "test_ortho.cpp's known answers)"}), flush=True)
+        return
     if cfgd["kind"] in CHAIN_KINDS:
         print(json.dumps({**base, "unavailable": "the reference's s-step / polynomial drivers "
                           "(sstep.hpp, poly.hpp) need Eigen, which is not installed; only their "
@@ -425,6 +435,135 @@ def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist,
         sys.exit(3)
 
 
+def run_ortho(args, cfgd):
+    """the step after the MPK in s-step GMRES.  A step = ICGS of the s-vector
+    Newton block V against the basis Q (`sweeps` rounds of block_dots + block_update) followed by
+    TSQR of V (sstep.hpp:539-545), with Q and V resident in HBM.  The headline runs the fast mode
+    (fp64 tensor-core block_dots); the bitwise mode (the reference's serial dot sums) is timed once
+    beside it.  Algorithmic bytes: per sweep Q and V read by the dots, Q and V read and V written by
+    the update; TSQR reads V and writes Q."""
+    import torch
+
+    import paper_2309_02228_b200 as mpkg
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, qc, s, sweeps = 192 ** 3, cfgd["qcols"], cfgd["p"], cfgd["sweeps"]
+    ctx = mpkg.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    g = torch.Generator(device=dev).manual_seed(args.seed)
+    Q = torch.rand((qc, n), dtype=torch.float64, device=dev, generator=g) * 2 - 1
+    R = torch.empty((qc, qc), dtype=torch.float64, device=dev)
+    ctx.tsqr_dev(Q.data_ptr(), n, qc, R.data_ptr())  # orthonormal basis
+    V0 = torch.rand((s, n), dtype=torch.float64, device=dev, generator=g) * 2 - 1
+    V = V0.clone()
+    coeff = torch.empty((s, qc), dtype=torch.float64, device=dev)
+    Rv = torch.empty((s, s), dtype=torch.float64, device=dev)
+
+    def sync():
+        ctx.synchronize()
+        torch.cuda.synchronize()
+
+    def step():
+        ctx.icgs_block_orthogonalize_dev(Q.data_ptr(), n, qc, V.data_ptr(), s, sweeps, coeff.data_ptr())
+        ctx.tsqr_dev(V.data_ptr(), n, s, Rv.data_ptr())
+
+    def timed(k, fn):
+        sync()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        sync()
+        return a.elapsed_time(b) / k
+
+    # bitwise (the reference's serial sums), one step, then the parity properties of both modes
+    ctx.set_mode(0)
+    V.copy_(V0)
+    sync()
+    bitwise_ms = timed(1, step)
+    Vb, cb = V.clone(), coeff.clone()
+    ctx.set_mode(1)
+    V.copy_(V0)
+    sync()
+    step()
+    sync()
+    eye = torch.eye(s, dtype=torch.float64, device=dev)
+    props = {
+        "fast_vs_bitwise_coeff_maxrel": ((coeff - cb).abs().max() / cb.abs().max()).item(),
+        "fast_vs_bitwise_q_maxabs": (V - Vb).abs().max().item(),
+        "q_orthonormal_maxabs": (V @ V.T - eye).abs().max().item(),
+        "q_perp_basis_maxabs": (Q @ V.T).abs().max().item(),
+    }
+    parity = (props["fast_vs_bitwise_coeff_maxrel"] <= 1e-12 and props["q_orthonormal_maxabs"] <= 1e-12
+              and props["q_perp_basis_maxabs"] <= 1e-12)
+    for _ in range(args.warmup):
+        V.copy_(V0)
+        step()
+    sync()
+    ctx.set_param("kernel_timing", 1)
+    ctx.kernel_times()
+    launches0 = ctx.launch_count()
+    ts = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            V.copy_(V0)  # untimed reset (V is orthogonalised in place)
+            ts.append(timed(1, step))
+    launches = ctx.launch_count() - launches0
+    k_total, k_count, _ = ctx.kernel_times()
+    ctx.set_param("kernel_timing", 0)
+    step_ms = statistics.median(ts)
+    kernel_ms = k_total / args.steps
+    flops = sweeps * 4.0 * n * qc * s + 4.0 * n * s * s  # dots + update per sweep; Householder QR + form Q
+    b_alg = 8.0 * n * (sweeps * (2 * qc + 3 * s) + 2 * s)
+    peak, peak_src = measured_peak()
+    achieved = b_alg / (kernel_ms * 1e-3) / 1e9
+
+    # e2e: the host-pointer ABI (pinned Q and V in, V and the coefficients / R out)
+    hQ = Q.cpu().pin_memory()
+    hV = torch.empty((s, n), dtype=torch.float64).pin_memory()
+    hc = np.zeros((s, qc))
+    hr = np.zeros((s, s))
+    from paper_2309_02228_b200._lib import check, lib
+    e_ts = []
+    for _ in range(max(3, min(args.steps, 10))):
+        hV.copy_(V0.cpu())
+        t0 = time.perf_counter()
+        check(lib.mpkg_icgs_block_orthogonalize(ctx.h, hQ.data_ptr(), n, qc, hV.data_ptr(), s, sweeps,
+                                                hc.ctypes.data))
+        check(lib.mpkg_tsqr(ctx.h, hV.data_ptr(), n, s, hr.ctypes.data))
+        e_ts.append((time.perf_counter() - t0) * 1e3)
+    e_ms = statistics.median(e_ts)
+    e2e = {"value": flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
+           "h2d_bytes_per_step": 8 * n * (qc + s) * 2,  # icgs + tsqr calls each stage their inputs
+           "d2h_bytes_per_step": 8 * n * s * 2 + 8 * (s * qc + s * s), "ms_per_step": e_ms,
+           "note": "two host-pointer calls (icgs, tsqr), wall clock"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": flops / (step_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] block; basis = TSQR of a seeded U[-1,1] block)",
+            "config": {"workload": cfgd["desc"], "n": n, "qcols": qc, "vcols": s, "sweeps": sweeps,
+                       "mode": "fast (tensor-core block_dots, fixed-order reduction)",
+                       "bitwise_ms_per_step": bitwise_ms,
+                       "l2": "inputs larger than L2 (%.2f GB)" % (8 * n * (qc + s) / 1e9),
+                       "parity": ("ok " if parity else "MISMATCH ") + json.dumps(props)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_alg,
+                         "kernel_ms": kernel_ms, "kernel_launches_timed": k_count,
+                         "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if not parity:
+        sys.exit(3)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -452,6 +591,8 @@ def main():
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfgd)
+    if cfgd["kind"] == "ortho":
+        return run_ortho(args, cfgd)
 
     import torch
 

@@ -285,7 +285,7 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->kernel = value;
         }
         else if (k == "sweep_variant") {
-            require(value >= 0 && value <= 3, "ctx_set_param: sweep_variant must be 0..3");
+            require(value >= 0 && value <= 5, "ctx_set_param: sweep_variant must be 0..5");
             ctx->sweep_variant = value;
         }
         else if (k == "graphs")

@@ -120,6 +120,8 @@ struct mpkg_ctx_s {
     mpkg_detail::DevBuf<double> scratch_x;
     mpkg_detail::DevBuf<double> scratch_block;
     mpkg_detail::DevBuf<double> chain_ws;  // preconditioned chains' workspace (precon.cu)
+    mpkg_detail::DevBuf<double> ortho_c;   // ICGS per-sweep coefficients (ortho.cu)
+    mpkg_detail::DevBuf<double> tsqr_ws;   // TSQR tree workspace (ortho.cu)
 };
 
 struct mpkg_csr_s {

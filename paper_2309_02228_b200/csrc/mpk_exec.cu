@@ -572,6 +572,10 @@ __global__ void __launch_bounds__(256, V == 1 ? 5 : 0) k_mpk_sweep(const __grid_
             acc = sell_row_dot<true, 4>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
         else if constexpr (V == 3)
             acc = sell_row_dot_pipe<true>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        else if constexpr (V == 4)
+            acc = sell_row_dot<true, 28>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+        else if constexpr (V == 5)
+            acc = sell_row_dot<true, 16>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
         else
             acc = sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
         if constexpr (KIND == 0 && !SIGMA)
@@ -589,6 +593,8 @@ void launch_sweep(int v, unsigned g, cudaStream_t st, const FusedParams& P, uint
         case 1: k_mpk_sweep<KIND, SIGMA, 1><<<g, 256, 0, st>>>(P, q); break;
         case 2: k_mpk_sweep<KIND, SIGMA, 2><<<g, 256, 0, st>>>(P, q); break;
         case 3: k_mpk_sweep<KIND, SIGMA, 3><<<g, 256, 0, st>>>(P, q); break;
+        case 4: k_mpk_sweep<KIND, SIGMA, 4><<<g, 256, 0, st>>>(P, q); break;
+        case 5: k_mpk_sweep<KIND, SIGMA, 5><<<g, 256, 0, st>>>(P, q); break;
         default: k_mpk_sweep<KIND, SIGMA, 0><<<g, 256, 0, st>>>(P, q); break;
     }
 }

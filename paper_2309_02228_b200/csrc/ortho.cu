@@ -384,16 +384,15 @@ void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, d
     const uint32_t ne = qcols * vcols;
     if (!ne) return;
     MPKG_CUDA(cudaMemsetAsync(coeff, 0, 8ull * ne, ctx->stream));
-    DevBuf<double> cbuf(ne);
+    ctx->ortho_c.ensure(ne);  // per-context workspace: no allocation on the steady-state path
+    double* cbuf = ctx->ortho_c.p;
     for (int sw = 0; sw < sweeps; ++sw) {
-        gpu_block_dots(ctx, q, v, rows, qcols, vcols, cbuf.p);
-        gpu_block_update(ctx, q, cbuf.p, rows, qcols, vcols, v);
-        k_accumulate<<<(ne + 255) / 256, 256, 0, ctx->stream>>>(coeff, cbuf.p, ne);
+        gpu_block_dots(ctx, q, v, rows, qcols, vcols, cbuf);
+        gpu_block_update(ctx, q, cbuf, rows, qcols, vcols, v);
+        k_accumulate<<<(ne + 255) / 256, 256, 0, ctx->stream>>>(coeff, cbuf, ne);
         MPKG_LAUNCH_CHECK();
         ctx->launches += 1;
     }
-    // cbuf is freed on return: order the free after the kernels that read it
-    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // Panel rows per level: shared memory holds two P x c panels in k_panel_formq.
@@ -422,8 +421,8 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
     }
     uint64_t ws = (uint64_t)c * c;  // M for the top panel
     for (size_t L = 0; L < lv_rows.size(); ++L) ws += lv_np[L] * c + lv_np[L] * c * c;
-    DevBuf<double> buf(ws);
-    double* p = buf.p;
+    ctx->tsqr_ws.ensure(ws);  // per-context workspace, stream-ordered reuse
+    double* p = ctx->tsqr_ws.p;
     double* mtop = p;
     p += (uint64_t)c * c;
     for (size_t L = 0; L < lv_rows.size(); ++L) {
@@ -465,7 +464,6 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
     }
     ctx->launches += 2 * lv.size() + 1;
     timing_end(ctx, ev);
-    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));  // buf is freed on return
 }
 
 }  // namespace mpkg_detail
