@@ -128,14 +128,18 @@ __global__ void __launch_bounds__(256) k_dots_mma(const double* __restrict__ q, 
 __global__ void k_dots_finish(const double* __restrict__ part, uint32_t n_parts, uint32_t tile_entries,
                               uint32_t qcols, uint32_t vcols, uint32_t mq0, uint32_t nv0,
                               double* __restrict__ c) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per tile entry: lane-strided partial sums over the CTA partials, then a fixed
+    // xor-butterfly (deterministic for a given grid)
+    const uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
     if (e >= tile_entries) return;
     const uint32_t mt = e / 64, m = (e % 64) / 8, n = e % 8;
     const uint32_t k = mq0 + mt * 8 + m, j = nv0 + n;
-    if (k >= qcols || j >= vcols) return;
+    if (k >= qcols || j >= vcols) return;  // warp-uniform
     double s = 0.0;
-    for (uint32_t b = 0; b < n_parts; ++b) s += part[(uint64_t)b * tile_entries + e];
-    c[(uint64_t)j * qcols + k] = s;
+    for (uint32_t b = lane; b < n_parts; b += 32) s += part[(uint64_t)b * tile_entries + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) c[(uint64_t)j * qcols + k] = s;
 }
 
 // ---- block_update (bitwise in both modes) --------------------------------------------------
@@ -158,17 +162,18 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ q, co
 #pragma unroll
         for (int jj = 0; jj < VT; ++jj) x[jj] = jj < (int)nv ? __ldcs(v + (uint64_t)(j0 + jj) * rows + i) : 0.0;
         uint32_t k = 0;
-        for (; k + 4 <= qcols; k += 4) {
-            double qk[4];
+        constexpr int U = 8;  // q loads in flight per thread
+        for (; k + U <= qcols; k += U) {
+            double qk[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) qk[u] = __ldg(q + (uint64_t)(k + u) * rows + i);
+            for (int u = 0; u < U; ++u) qk[u] = __ldcs(q + (uint64_t)(k + u) * rows + i);
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int jj = 0; jj < VT; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[jj * qcols + k + u], qk[u]));
         }
         for (; k < qcols; ++k) {
-            const double qk = __ldg(q + (uint64_t)k * rows + i);
+            const double qk = __ldcs(q + (uint64_t)k * rows + i);
 #pragma unroll
             for (int jj = 0; jj < VT; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[jj * qcols + k], qk));
         }
@@ -189,6 +194,8 @@ __global__ void k_accumulate(double* __restrict__ coeff, const double* __restric
 __device__ __forceinline__ uint64_t panel_bound(uint64_t rows, uint32_t np, uint32_t k) {
     return rows * k / np;
 }
+
+__device__ __forceinline__ bool lane_bit(uint32_t b) { return (threadIdx.x & b) != 0u; }
 
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
@@ -297,6 +304,223 @@ __global__ void __launch_bounds__(256) k_panel_formq(double* __restrict__ a, uin
         for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) a[l * lda + b0 + i] = Y[(uint64_t)l * P + i];
 }
 
+// Narrow blocks (c <= 8, the s-step case): one WARP per panel of up to 32*TQ_R rows, the panel
+// held in registers (lane owns rows lane + 32 r), reductions by xor-shuffle butterflies (fixed
+// order, every lane holds the sum): no shared memory and no block barriers, so many panels are in
+// flight per SM.  Same Householder convention as k_panel_qr.  FORM = false: factor the panel and
+// write its R to `rstack`.  FORM = true: factor the panel AGAIN from the untouched input (the
+// reflectors are recomputed, never stored: one read of the block instead of a write + re-read)
+// and overwrite it with Y = H_0 ... H_{c-1} [M_k; 0].
+constexpr int kTqC = 8;
+constexpr int kTqR = 4;
+constexpr uint32_t kTqPanel = 32u * kTqR;
+
+// Butterfly sums of N independent values: the N shuffle chains interleave (ILP N).
+template <int N>
+__device__ __forceinline__ void warp_sum_n(double (&v)[N]) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int n = 0; n < N; ++n) v[n] += __shfl_xor_sync(kFull, v[n], o);
+}
+
+// Sums of 8 values over the warp, returned in every lane, by reduce-scatter: lanes exchange
+// halves at distances 16, 8, 4 (4 + 2 + 1 shuffles), finish with a 2-level butterfly on the one
+// value left, then read the 8 totals back from their holder lanes (8 shuffles): 17 double
+// shuffles instead of the plain butterfly's 40.  Fixed order, the same totals in every lane.
+__device__ __forceinline__ void warp_sum8(double (&v)[8]) {
+    const bool h16 = lane_bit(16), h8 = lane_bit(8), h4 = lane_bit(4);
+    double a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = h16 ? v[i] : v[4 + i];
+        const double keep = h16 ? v[4 + i] : v[i];
+        a[i] = keep + __shfl_xor_sync(kFull, send, 16);
+    }
+    double b[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = h8 ? a[i] : a[2 + i];
+        const double keep = h8 ? a[2 + i] : a[i];
+        b[i] = keep + __shfl_xor_sync(kFull, send, 8);
+    }
+    double t = (h4 ? b[1] : b[0]) + __shfl_xor_sync(kFull, h4 ? b[0] : b[1], 4);
+    t += __shfl_xor_sync(kFull, t, 2);
+    t += __shfl_xor_sync(kFull, t, 1);
+    // lane L holds total index 4*(L>>4 & 1) + 2*(L>>3 & 1) + (L>>2 & 1)
+#pragma unroll
+    for (int l = 0; l < 8; ++l) v[l] = __shfl_sync(kFull, t, ((l & 4) ? 16 : 0) + ((l & 2) ? 8 : 0) + ((l & 1) ? 4 : 0));
+}
+
+// Factor kernel.  Columns l >= c and rows i >= P are loaded as zeros and stay zero through every
+// update, so the arithmetic needs no column / row-count predicates; only row i <= j (r = 0,
+// lane <= j) is excluded from step j's reflector.  Writes the panel's R to `rstack`, the
+// reflectors over the panel in place (LAPACK layout: v below the diagonal, R on and above) and
+// the compact-WY factor T (8 x 8 upper triangular, row-major, H_0 ... H_{c-1} = I - V T V^T) to
+// `tmat` (64 doubles per panel).
+__global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uint64_t lda, uint64_t rows,
+                                                     uint32_t np, uint32_t c, double* __restrict__ rstack,
+                                                     double* __restrict__ tmat) {
+    const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (k >= np) return;  // warp-uniform
+    const uint64_t b0 = panel_bound(rows, np, k), b1 = panel_bound(rows, np, k + 1);
+    const uint32_t P = (uint32_t)(b1 - b0);
+    double A[kTqR][kTqC];
+#pragma unroll
+    for (int l = 0; l < kTqC; ++l)
+#pragma unroll
+        for (int r = 0; r < kTqR; ++r) {
+            const uint32_t i = lane + 32u * r;
+            A[r][l] = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
+        }
+    // Lane i < 8 builds row i of T column by column (dlarft, forward, columnwise):
+    // T_jj = tau_j, T_{0:j,j} = -tau_j T_{0:j,0:j} (V_{:,0:j}^T v_j).  The Gram entries v_m . v_j
+    // (m < j) ride in the free slots of step j's 8-wide reduction (slots l > j carry w_l).
+    double trow[kTqC];
+#pragma unroll
+    for (int j = 0; j < kTqC; ++j) trow[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kTqC; ++j) {
+        if ((uint32_t)j >= c) break;  // uniform
+        const bool below = lane > (uint32_t)j, diag = lane == (uint32_t)j;
+        const double a0 = below ? A[0][j] : 0.0;
+        double sg[1] = {a0 * a0};
+#pragma unroll
+        for (int r = 1; r < kTqR; ++r) sg[0] += A[r][j] * A[r][j];
+        const double alpha = __shfl_sync(kFull, A[0][j], j);
+        warp_sum_n(sg);
+        const double sigma = sg[0];
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (sigma != 0.0) {
+            const double nrm = sqrt(alpha * alpha + sigma);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            t = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        const double vj = diag ? 1.0 : a0 * scale;  // row-0 reflector entry (0 above the diagonal)
+        A[0][j] = below ? vj : (diag ? beta : A[0][j]);
+#pragma unroll
+        for (int r = 1; r < kTqR; ++r) A[r][j] *= scale;
+        if (t != 0.0) {  // uniform; tau_j = 0 leaves T's column j zero and the block unchanged
+            double w[kTqC];
+#pragma unroll
+            for (int l = 0; l < kTqC; ++l) {
+                // l > j: v_j . A_l (the update);  l < j: v_l . v_j (T);  l == j: unused
+                const double x0 = l > j ? A[0][l] : (l < j ? (lane == (uint32_t)l ? 1.0 : (lane > (uint32_t)l ? A[0][l] : 0.0)) : 0.0);
+                w[l] = vj * x0;
+                if (l != j) {
+#pragma unroll
+                    for (int r = 1; r < kTqR; ++r) w[l] += A[r][j] * A[r][l];
+                }
+            }
+            warp_sum8(w);
+            double sT = 0.0;
+#pragma unroll
+            for (int m = 0; m < j; ++m) sT += trow[m] * w[m];
+            trow[j] = diag ? t : (lane < (uint32_t)j ? -t * sT : 0.0);
+#pragma unroll
+            for (int l = j + 1; l < kTqC; ++l) {
+                const double wl = t * w[l];
+                A[0][l] -= wl * vj;
+#pragma unroll
+                for (int r = 1; r < kTqR; ++r) A[r][l] -= wl * A[r][j];
+            }
+        }
+    }
+    if (lane < 8) {
+#pragma unroll
+        for (int j = 0; j < kTqC; ++j) tmat[(uint64_t)k * 64 + lane * 8 + j] = trow[j];
+    }
+    const uint64_t ldr = (uint64_t)np * c;
+    if (lane < c)
+#pragma unroll
+        for (int l = 0; l < kTqC; ++l)
+            if ((uint32_t)l < c) rstack[(uint64_t)l * ldr + (uint64_t)k * c + lane] = lane <= (uint32_t)l ? A[0][l] : 0.0;
+#pragma unroll
+    for (int l = 0; l < kTqC; ++l)
+#pragma unroll
+        for (int r = 0; r < kTqR; ++r) {
+            const uint32_t i = lane + 32u * r;
+            if ((uint32_t)l < c && i < P) a[(uint64_t)l * lda + b0 + i] = A[r][l];
+        }
+}
+
+// Apply kernel: Y = (I - V T V^T) [M_k; 0] = [M_k; 0] - V (T (V_top^T M_k)), V_top the panel's
+// top 8 rows (M_k is zero below row c).  No reduction over the panel: the two 8 x 8 products go
+// through per-warp shared memory, then every row is an 8 x 8 matvec.  Overwrites the reflectors.
+__global__ void __launch_bounds__(128) k_tsqr_apply(double* __restrict__ a, uint64_t lda, uint64_t rows,
+                                                    uint32_t np, uint32_t c, const double* __restrict__ tmat,
+                                                    const double* __restrict__ m, uint64_t ldm) {
+    __shared__ double sh[4][3][64];  // per warp: V_top / S, M, T
+    const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    if (k >= np) return;  // warp-uniform
+    double* Vs = sh[wib][0];
+    double* Ms = sh[wib][1];
+    double* Ts = sh[wib][2];
+    const uint64_t b0 = panel_bound(rows, np, k), b1 = panel_bound(rows, np, k + 1);
+    const uint32_t P = (uint32_t)(b1 - b0);
+    double A[kTqR][kTqC];
+#pragma unroll
+    for (int l = 0; l < kTqC; ++l)
+#pragma unroll
+        for (int r = 0; r < kTqR; ++r) {
+            const uint32_t i = lane + 32u * r;
+            double v = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
+            if (r == 0) v = lane == (uint32_t)l ? 1.0 : (lane < (uint32_t)l ? 0.0 : v);
+            A[r][l] = v;
+        }
+    double m0[kTqC];
+#pragma unroll
+    for (int l = 0; l < kTqC; ++l) m0[l] = ((uint32_t)l < c && lane < c) ? m[(uint64_t)l * ldm + (uint64_t)k * c + lane] : 0.0;
+    if (lane < 8) {
+#pragma unroll
+        for (int l = 0; l < kTqC; ++l) Vs[lane * 8 + l] = A[0][l], Ms[lane * 8 + l] = m0[l];
+    }
+    Ts[lane] = tmat[(uint64_t)k * 64 + lane];
+    Ts[lane + 32] = tmat[(uint64_t)k * 64 + lane + 32];
+    __syncwarp();
+    // W = V_top^T M (entries e = lane, lane + 32: row e/8, column e%8)
+    double wv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t e = lane + 32u * h, j = e >> 3, l = e & 7u;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += Vs[i * 8 + j] * Ms[i * 8 + l];
+        wv[h] = s;
+    }
+    __syncwarp();
+    Ms[lane] = wv[0];
+    Ms[lane + 32] = wv[1];
+    __syncwarp();
+    // S = T W (T upper triangular)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t e = lane + 32u * h, j = e >> 3, l = e & 7u;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += Ts[j * 8 + q] * Ms[q * 8 + l];
+        wv[h] = s;
+    }
+    Vs[lane] = wv[0];  // V_top no longer read (all lanes passed the W loop before the last sync)
+    Vs[lane + 32] = wv[1];
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < kTqC; ++l) {
+        if ((uint32_t)l >= c) break;
+#pragma unroll
+        for (int r = 0; r < kTqR; ++r) {
+            double y = r == 0 ? m0[l] : 0.0;
+#pragma unroll
+            for (int j = 0; j < kTqC; ++j) y -= A[r][j] * Vs[j * 8 + l];
+            const uint32_t i = lane + 32u * r;
+            if (i < P) a[(uint64_t)l * lda + b0 + i] = y;
+        }
+    }
+}
+
 // Top of the tree: R (c x c, column-major) with row j negated when R_jj < 0 and the strictly
 // lower part zero (ortho.hpp:204-212, 221-226); M = diag(sign) for the top panel's Q.
 __global__ void k_sign_fix(const double* __restrict__ rtop, uint32_t c, double* __restrict__ r,
@@ -343,7 +567,7 @@ void gpu_block_dots(mpkg_ctx_s* ctx, const double* q, const double* v, uint64_t 
                     default: k_dots_mma<8><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part); break;
                 }
                 MPKG_LAUNCH_CHECK();
-                k_dots_finish<<<(te + 127) / 128, 128, 0, ctx->stream>>>(part, grid, te, qcols, vcols, mq0, nv0, c);
+                k_dots_finish<<<(te * 32 + 255) / 256, 256, 0, ctx->stream>>>(part, grid, te, qcols, vcols, mq0, nv0, c);
                 MPKG_LAUNCH_CHECK();
                 ctx->launches += 2;
             }
@@ -400,7 +624,10 @@ uint32_t tsqr_panel_rows(uint32_t c) { return std::max<uint32_t>(4096u / c, 2u *
 
 void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) {
     if (!c) return;
-    const uint32_t Pmax = tsqr_panel_rows(c);
+    // c <= 8 (s-step blocks): warp-per-panel register kernels on 64-row panels; wider blocks: the
+    // shared-memory CTA-per-panel kernels
+    const bool narrow = c <= (uint32_t)kTqC;
+    const uint32_t Pmax = narrow ? kTqPanel : tsqr_panel_rows(c);
     struct Level {
         double* a;
         uint64_t lda, rows;
@@ -420,7 +647,8 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
         rr = np * c;
     }
     uint64_t ws = (uint64_t)c * c;  // M for the top panel
-    for (size_t L = 0; L < lv_rows.size(); ++L) ws += lv_np[L] * c + lv_np[L] * c * c;
+    const uint64_t tslot = narrow ? 64u : c;  // narrow: compact-WY T per panel, else taus
+    for (size_t L = 0; L < lv_rows.size(); ++L) ws += lv_np[L] * tslot + lv_np[L] * c * c;
     ctx->tsqr_ws.ensure(ws);  // per-context workspace, stream-ordered reuse
     double* p = ctx->tsqr_ws.p;
     double* mtop = p;
@@ -432,12 +660,34 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
         l.a = L == 0 ? v : lv[L - 1].rstack;
         l.lda = L == 0 ? rows : lv_rows[L];
         l.taus = p;
-        p += (uint64_t)l.np * c;
+        p += (uint64_t)l.np * tslot;
         l.rstack = p;
         p += (uint64_t)l.np * c * c;
         lv.push_back(l);
     }
     const auto ev = timing_begin(ctx);
+    if (narrow) {
+        for (const Level& l : lv) {
+            k_tsqr_factor<<<(l.np * 32u + 127u) / 128u, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c,
+                                                                            l.rstack, l.taus);
+            MPKG_LAUNCH_CHECK();
+        }
+        k_sign_fix<<<1, 256, 0, ctx->stream>>>(lv.back().rstack, c, r, mtop);
+        MPKG_LAUNCH_CHECK();
+        const double* m = mtop;
+        uint64_t ldm = c;
+        for (size_t L = lv.size(); L-- > 0;) {
+            const Level& l = lv[L];
+            k_tsqr_apply<<<(l.np * 32u + 127u) / 128u, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c,
+                                                                           l.taus, m, ldm);
+            MPKG_LAUNCH_CHECK();
+            m = l.a;
+            ldm = l.lda;
+        }
+        ctx->launches += 2 * lv.size() + 1;
+        timing_end(ctx, ev);
+        return;
+    }
     size_t smem_max = 0;
     for (const Level& l : lv) {
         const uint64_t pr = (l.rows + l.np - 1) / l.np;
