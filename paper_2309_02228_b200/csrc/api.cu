@@ -224,6 +224,9 @@ int mpkg_ctx_destroy(mpkg_ctx_t ctx) {
     for (auto& e : ctx->event_pool) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto e : ctx->d2h_events) cudaEventDestroy(e);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MPKG_OK;
@@ -287,6 +290,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
         else if (k == "sweep_variant") {
             require(value >= 0 && value <= 5, "ctx_set_param: sweep_variant must be 0..5");
             ctx->sweep_variant = value;
+        }
+        else if (k == "coop_variant") {
+            require(value >= 0 && value <= 3, "ctx_set_param: coop_variant must be 0..3");
+            ctx->coop_variant = value;
         }
         else if (k == "graphs")
             ctx->graphs = value != 0;

@@ -105,6 +105,7 @@ struct mpkg_ctx_s {
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
     bool graphs = true;       // sweep schedule: replay the p launches as one CUDA graph
     int64_t sweep_variant = 0;  // sweep-kernel row loop (mpk_exec.cu launch_sweep)
+    int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power (mpk_exec.cu)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
     int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)
@@ -115,6 +116,8 @@ struct mpkg_ctx_s {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
     // device-to-host copy stream + per-slice events for host-pointer calls (run_fused)
     cudaStream_t d2h = nullptr;
+    cudaStream_t aux = nullptr;             // side stream of fast-mode sweeps (k_coop_rows)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     std::vector<cudaEvent_t> d2h_events;
     // scratch
     mpkg_detail::DevBuf<double> scratch_x;

@@ -51,6 +51,8 @@ constexpr uint32_t kMaxBufBytes = 96 * 1024;
 constexpr uint32_t kLongCap = 1024;    // rows longer than this take the CTA-cooperative path
 constexpr uint32_t kSB = 64;           // tiles per completion-counter superblock
 constexpr uint32_t kLongChunk = 1024;  // products per chunk of a long row (x2 smem ring)
+constexpr uint32_t kMedCap = 64;       // fast-mode sweeps: rows longer than this go to k_coop_rows
+constexpr uint32_t kCoopSeg = 2048;    // entries per k_coop_rows work item (longer rows are split)
 constexpr uint32_t kLeanRingBytes = 2 * kLongChunk * sizeof(double);
 #ifndef MPKG_GROUP
 #define MPKG_GROUP 16
@@ -109,6 +111,12 @@ struct Executor {
     DevBuf<uint32_t> sb_count;                // (kMaxFusedP+1) x n_sb superblock counters
     DevBuf<double> V;   // sigma-order working vectors (order 1)
     DevBuf<double> zs;  // sigma-order polynomial accumulator (order 1)
+    // fast-mode cooperative rows (build_coop): work items {slot, k0, k1, part or ~0u}, rows split
+    // over several items {slot, first part, parts, 0}, and the per-item partial sums
+    bool coop_ready = false;
+    DevBuf<uint4> coop_items, coop_multi;
+    DevBuf<double> coop_part;
+    uint32_t n_coop = 0, n_multi = 0;
 };
 
 struct FusedParams {
@@ -144,6 +152,12 @@ struct FusedParams {
     uint32_t n_long;
     uint32_t n_prod;        // async kernel: producer warps per CTA
     uint32_t n_cgroups;     // async kernel: consumer groups (tile_rows threads each) per CTA
+    uint32_t sweep_cap;          // k_mpk_sweep skips rows longer than this
+    const uint4* coop_items;     // fast mode: k_coop_rows work items (n_coop)
+    const uint4* coop_multi;     // rows split over several items (n_multi)
+    double* coop_part;
+    uint32_t n_coop;
+    uint32_t n_multi;
     uint64_t vstride;  // stride of V slices
     double* V;         // working vectors (== out when identity)
     uint64_t rows;     // stride of the caller's block
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(256, V == 1 ? 5 : 0) k_mpk_sweep(const __grid_
         const uint32_t r = SIGMA ? P.slot_row[s] : (uint32_t)s;
         if (r >= P.n_rows) continue;
         const uint32_t len = P.row_len[s];
-        if (len > P.long_cap) continue;  // long rows: k_long_rows_fast (fast mode only)
+        if (len > P.sweep_cap) continue;  // long rows: k_coop_rows / k_long_rows_fast (fast mode)
         const uint64_t off = P.chunk_off[s >> 5];
         const uint32_t L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
         double acc;
@@ -642,6 +656,60 @@ __global__ void __launch_bounds__(256) k_long_rows_fast(const __grid_constant__ 
             row_epilogue<KIND, SIGMA>(P, s, r, q, src, t);
         }
         __syncthreads();
+    }
+}
+
+// MPKG_MODE_FAST, sweep schedule, rows longer than kMedCap (power-law matrices): one WARP per work
+// item -- a whole row, or a kCoopSeg-entry segment of a longer one -- lanes striding the row's
+// CSR entries with 8 gathers in flight, a per-lane FMA chain, then a fixed xor-butterfly.  A row
+// split over several items leaves its partials in coop_part; k_coop_finish adds them in item
+// order.  Deterministic run to run; checked at the north star's 1e-12 inf-norm tolerance.  Runs
+// on a side stream concurrently with the power's k_mpk_sweep (disjoint rows, same input slice).
+template <int KIND, bool SIGMA, int U, bool CG>
+__global__ void __launch_bounds__(256) k_coop_rows(const __grid_constant__ FusedParams P, uint32_t q) {
+    const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;  // A_perm-order copy of y_{q-1}
+    const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    const uint64_t pol = l2_policy_first();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.n_coop; it += nw) {
+        const uint4 d = P.coop_items[it];
+        double acc = 0.0;
+        for (uint32_t k0 = d.y + lane; k0 < d.z; k0 += U * 32) {
+            uint32_t col[U];
+            double val[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t k = k0 + 32u * u;
+                col[u] = k < d.z ? ld_mat_u32(P.csr_ci + k, pol) : 0u;
+                val[u] = k < d.z ? ld_mat_d(P.csr_v + k, pol) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                xv[u] = k0 + 32u * u < d.z ? (CG ? __ldcg(srcA + col[u]) : __ldg(srcA + col[u])) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k0 + 32u * u < d.z) acc = __fma_rn(val[u], xv[u], acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            if (d.w == 0xffffffffu)
+                row_epilogue<KIND, SIGMA>(P, d.x, SIGMA ? P.slot_row[d.x] : d.x, q, src, acc);
+            else
+                P.coop_part[d.w] = acc;
+        }
+    }
+}
+
+template <int KIND, bool SIGMA>
+__global__ void k_coop_finish(const __grid_constant__ FusedParams P, uint32_t q) {
+    const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < P.n_multi; m += gridDim.x * blockDim.x) {
+        const uint4 d = P.coop_multi[m];
+        double t = 0.0;
+        for (uint32_t i = 0; i < d.z; ++i) t += P.coop_part[d.y + i];
+        row_epilogue<KIND, SIGMA>(P, d.x, SIGMA ? P.slot_row[d.x] : d.x, q, src, t);
     }
 }
 
@@ -1486,6 +1554,53 @@ void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
 // level-by-level critical path costs more than p launches, so auto runs one launch per power
 // over the executor's SELL -- except for matrices with long rows, whose CTA-cooperative path
 // exists only in the fused kernel.
+// Fast mode: work items of k_coop_rows for every row longer than kMedCap (none for stencils), the
+// longest first so the tail of the side-stream launch is short.
+void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
+    E.coop_ready = true;
+    const Sell& S = *E.S;
+    cudaStream_t st = ctx->stream;
+    const bool sigma = E.order >= 1;
+    std::vector<uint32_t> rl(S.n_slots), sr, rp((uint64_t)A->n_rows + 1);
+    if (S.n_slots) MPKG_CUDA(cudaMemcpyAsync(rl.data(), S.row_len.p, 4ull * rl.size(), cudaMemcpyDeviceToHost, st));
+    if (sigma) {
+        sr.resize(E.n_slots);
+        MPKG_CUDA(cudaMemcpyAsync(sr.data(), E.slot_row.p, 4ull * sr.size(), cudaMemcpyDeviceToHost, st));
+    }
+    MPKG_CUDA(cudaMemcpyAsync(rp.data(), A->row_ptr.p, 4ull * rp.size(), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaStreamSynchronize(st));
+    std::vector<std::pair<uint32_t, uint32_t>> rows;  // (length, slot)
+    for (uint32_t sl = 0; sl < (uint32_t)rl.size(); ++sl) {
+        const uint32_t r = sigma ? sr[sl] : sl;
+        if (r < A->n_rows && rl[sl] > kMedCap) rows.emplace_back(rl[sl], sl);
+    }
+    std::stable_sort(rows.begin(), rows.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<uint4> items, multi;
+    uint32_t part = 0;
+    for (const auto& [len, sl] : rows) {
+        const uint32_t r = sigma ? sr[sl] : sl;
+        const uint32_t b = rp[r], e = rp[r + 1];
+        if (len <= kCoopSeg) {
+            items.push_back(make_uint4(sl, b, e, 0xffffffffu));
+        } else {
+            const uint32_t cnt = (len + kCoopSeg - 1) / kCoopSeg;
+            multi.push_back(make_uint4(sl, part, cnt, 0u));
+            for (uint32_t i = 0; i < cnt; ++i)
+                items.push_back(make_uint4(sl, b + i * kCoopSeg, std::min(e, b + (i + 1) * kCoopSeg), part++));
+        }
+    }
+    E.n_coop = (uint32_t)items.size();
+    E.n_multi = (uint32_t)multi.size();
+    E.coop_items.alloc(std::max<size_t>(items.size(), 1));
+    E.coop_multi.alloc(std::max<size_t>(multi.size(), 1));
+    E.coop_part.alloc(std::max<uint32_t>(part, 1));
+    if (!items.empty())
+        MPKG_CUDA(cudaMemcpyAsync(E.coop_items.p, items.data(), sizeof(uint4) * items.size(), cudaMemcpyHostToDevice, st));
+    if (!multi.empty())
+        MPKG_CUDA(cudaMemcpyAsync(E.coop_multi.p, multi.data(), sizeof(uint4) * multi.size(), cudaMemcpyHostToDevice, st));
+    MPKG_CUDA(cudaStreamSynchronize(st));
+}
+
 bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
     if (ctx->schedule == 1) return false;
     // Long rows live outside the SELL arrays: bitwise mode runs them through the fused kernel's
@@ -1535,6 +1650,16 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.n_tiles = E.n_tiles;
     P.long_slots = E.long_slots.p;
     P.n_long = (uint32_t)E.long_rows;
+    // fast-mode sweeps over a matrix with rows longer than kMedCap: those rows (long ones
+    // included) run in k_coop_rows on a side stream, concurrently with each power's sweep
+    if (sweep && ctx->mode == MPKG_MODE_FAST && !E.coop_ready) build_coop(ctx, E, A);
+    const bool coop = sweep && ctx->mode == MPKG_MODE_FAST && E.n_coop > 0;
+    P.sweep_cap = coop ? kMedCap : E.long_cap;
+    P.coop_items = coop ? E.coop_items.p : nullptr;
+    P.coop_multi = coop ? E.coop_multi.p : nullptr;
+    P.coop_part = coop ? E.coop_part.p : nullptr;
+    P.n_coop = coop ? E.n_coop : 0;
+    P.n_multi = coop ? E.n_multi : 0;
     P.n_prod = E.n_prod;
     P.n_cgroups = E.n_cgroups;
     P.n_sb = (E.n_tiles + kSB - 1) / kSB;
@@ -1580,7 +1705,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     // other case runs k_mpk_sweep (private order, polynomial accumulator, long rows skipped).
     auto sweep_power = [&](uint32_t q) {
         const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
-        if (!sigma && a.kind <= 1 && !E.long_rows && sv == 0) {
+        if (!sigma && a.kind <= 1 && !E.long_rows && !coop && sv == 0) {
             const double* src = a.block + (uint64_t)(q - 1) * a.rows;
             const double* src2 = q >= 2 ? a.block + (uint64_t)(q - 2) * a.rows : src;
             launch_spmv_sell_raw(ctx, S, a.kind == 1, src, a.block + (uint64_t)q * a.rows, src2,
@@ -1597,6 +1722,66 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             default: launch_sweep<2, true>(sv, g, st, P, q); break;
         }
     };
+    // One power: the sweep, plus the rows it skips in fast mode -- k_coop_rows on the side stream
+    // (forked from and joined back into the context stream, so a CUDA-graph capture records both
+    // branches) or, without cooperative items, k_long_rows_fast after the sweep.
+    const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
+    const unsigned gc = (unsigned)std::min<uint64_t>(std::max<uint64_t>((E.n_coop + 7) / 8, 1), (uint64_t)ctx->sm_count * 8u);
+    if (coop && !ctx->aux) {
+        MPKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        MPKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+        MPKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    }
+    auto power = [&](uint32_t q) {
+        const int kk = a.kind * 2 + (sigma ? 1 : 0);
+        if (coop) {
+            cudaStream_t ax = ctx->aux;
+            MPKG_CUDA(cudaEventRecord(ctx->fork_ev, st));
+            MPKG_CUDA(cudaStreamWaitEvent(ax, ctx->fork_ev, 0));
+            switch (kk * 4 + (int)(ctx->coop_variant & 3)) {
+#define MPKG_COOP_CASE(K, S)                                                        \
+    case (K * 2 + S) * 4 + 0: k_coop_rows<K, S, 8, false><<<gc, 256, 0, ax>>>(P, q); break; \
+    case (K * 2 + S) * 4 + 1: k_coop_rows<K, S, 16, false><<<gc, 256, 0, ax>>>(P, q); break; \
+    case (K * 2 + S) * 4 + 2: k_coop_rows<K, S, 8, true><<<gc, 256, 0, ax>>>(P, q); break; \
+    case (K * 2 + S) * 4 + 3: k_coop_rows<K, S, 16, true><<<gc, 256, 0, ax>>>(P, q); break;
+                MPKG_COOP_CASE(0, 0) MPKG_COOP_CASE(0, 1) MPKG_COOP_CASE(1, 0)
+                MPKG_COOP_CASE(1, 1) MPKG_COOP_CASE(2, 0) MPKG_COOP_CASE(2, 1)
+#undef MPKG_COOP_CASE
+            }
+            MPKG_LAUNCH_CHECK();
+            if (E.n_multi) {
+                const unsigned gm = grid_for(E.n_multi, 128, (unsigned)ctx->sm_count * 4u);
+                switch (kk) {
+                    case 0: k_coop_finish<0, false><<<gm, 128, 0, ax>>>(P, q); break;
+                    case 1: k_coop_finish<0, true><<<gm, 128, 0, ax>>>(P, q); break;
+                    case 2: k_coop_finish<1, false><<<gm, 128, 0, ax>>>(P, q); break;
+                    case 3: k_coop_finish<1, true><<<gm, 128, 0, ax>>>(P, q); break;
+                    case 4: k_coop_finish<2, false><<<gm, 128, 0, ax>>>(P, q); break;
+                    default: k_coop_finish<2, true><<<gm, 128, 0, ax>>>(P, q); break;
+                }
+                MPKG_LAUNCH_CHECK();
+            }
+            MPKG_CUDA(cudaEventRecord(ctx->join_ev, ax));
+            sweep_power(q);
+            MPKG_LAUNCH_CHECK();
+            MPKG_CUDA(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+            return;
+        }
+        sweep_power(q);
+        MPKG_LAUNCH_CHECK();
+        if (E.long_rows) {  // fast mode only (use_sweeps)
+            switch (kk) {
+                case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
+                case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
+                case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
+                case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
+                case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
+                default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
+            }
+            MPKG_LAUNCH_CHECK();
+        }
+    };
+    const uint64_t per_power = 1 + (coop ? 1 + (E.n_multi ? 1 : 0) : (E.long_rows ? 1 : 0));
     const auto ev = timing_begin(ctx);
     // host-pointer calls: slice q goes to the host on the copy stream once power q is written
     const bool to_host = a.host_block != nullptr;
@@ -1621,44 +1806,15 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (sweep && to_host) {
         // one launch per power with the copies interleaved (no graph: the copy stream waits on
         // per-power events); the PCIe transfer of slice q overlaps the sweeps q+1..p
-        const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
         for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
-            sweep_power(q);
-            MPKG_LAUNCH_CHECK();
-            if (E.long_rows) {
-                switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                    case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
-                    case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
-                    case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
-                    case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
-                    case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
-                    default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
-                }
-                MPKG_LAUNCH_CHECK();
-            }
+            power(q);
             copy_slice(q);
         }
         join_copies();
-        ctx->launches += (uint64_t)a.p * (E.long_rows ? 2 : 1) - 1;
+        ctx->launches += (uint64_t)a.p * per_power - 1;
     } else if (sweep) {
         auto launch_all = [&]() {
-            const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
-            const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
-            for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) {
-                sweep_power(q);
-                MPKG_LAUNCH_CHECK();
-                if (E.long_rows) {  // fast mode only (use_sweeps)
-                    switch (a.kind * 2 + (sigma ? 1 : 0)) {
-                        case 0: k_long_rows_fast<0, false><<<gl, 256, 0, st>>>(P, q); break;
-                        case 1: k_long_rows_fast<0, true><<<gl, 256, 0, st>>>(P, q); break;
-                        case 2: k_long_rows_fast<1, false><<<gl, 256, 0, st>>>(P, q); break;
-                        case 3: k_long_rows_fast<1, true><<<gl, 256, 0, st>>>(P, q); break;
-                        case 4: k_long_rows_fast<2, false><<<gl, 256, 0, st>>>(P, q); break;
-                        default: k_long_rows_fast<2, true><<<gl, 256, 0, st>>>(P, q); break;
-                    }
-                    MPKG_LAUNCH_CHECK();
-                }
-            }
+            for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) power(q);
         };
         if (ctx->graphs) {
             // One CUDA graph per distinct launch set (parameters, p, kind): repeated calls with
@@ -1694,7 +1850,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         } else {
             launch_all();
         }
-        ctx->launches += (uint64_t)a.p * (E.long_rows ? 2 : 1) - 1;  // kernels the step ran
+        ctx->launches += (uint64_t)a.p * per_power - 1;  // kernels the step ran
     } else if (E.kernel == 4) {
         const int nt = (int)E.threads;
         const uint32_t sm = E.stages * E.buf_bytes;

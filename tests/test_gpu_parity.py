@@ -316,6 +316,43 @@ def test_fast_mode_long_rows_within_tolerance(ctx, oracle, schedule):
         set_knobs(ctx, {})
 
 
+@pytest.mark.parametrize("order", [-1, 0])
+def test_fast_mode_coop_rows_graph_and_host_paths(ctx, oracle, order):
+    """Fast-mode sweeps send rows longer than 64 entries to k_coop_rows on a side stream (hub rows
+    split into 2048-entry items, partials added in order by k_coop_finish).  The device-pointer
+    call (CUDA-graph replay) and the host-pointer call (eager, streamed copies) agree bit for bit,
+    repeat bit for bit, and stay within 1e-12 of the oracle; A_perm order (order=0) too."""
+    import torch
+    try:
+        set_knobs(ctx, {"order": order})
+        ctx.set_mode(ctx.MODE_FAST)
+        for A in (_arrow_matrix(), mpkg.rmat(14, 16, 11)):
+            lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
+            P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
+            Ap = ctx.csr(P)
+            ls = ctx.levels_from_host(lv, pm, ip, lp)
+            n, p = P.n_rows, 5
+            x = mpkg.random_vector(n, 9)
+            plan = ctx.group_levels(ls, Ap, 8 << 20, p)
+            ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, p)
+            host = ctx.mpk(plan, Ap, x, p).as_matrix().copy()
+            assert max(_rel_inf_err(host, ref)) <= 1e-12
+            d_x = torch.from_numpy(x).cuda()
+            d_b = torch.empty((p + 1) * n, dtype=torch.float64, device="cuda")
+            for _ in range(2):  # capture, then replay
+                d_b.fill_(float("nan"))
+                ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, d_b.data_ptr(), n, p + 1)
+                ctx.synchronize()
+                assert_bitwise(d_b.view(p + 1, n).cpu().numpy(), host, "graph == host path")
+            sh = [1.0, 2.0 + 0.5j, 2.0 - 0.5j, 0.5, 3.0]
+            ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+            assert max(_rel_inf_err(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref)) <= 1e-12
+            assert plan.exec_info()["schedule"] == "sweeps"
+    finally:
+        ctx.set_mode(ctx.MODE_BITWISE)
+        set_knobs(ctx, {})
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
