@@ -76,7 +76,11 @@ int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t
  * consumer in the list schedule; -1 = auto), "order" (0: A_perm order, 1: Cuthill-McKee inside
  * levels), "pass" (force powers per fused pass; 0 = auto from the L2 budget), "l2_budget" (live
  * window bytes; 0 = L2/2), "tile_rows" (fixed 256); "kernel_timing" = 1 records a CUDA event
- * pair around every power-kernel launch on the context stream. */
+ * pair around every power-kernel launch on the context stream; "schedule" (0 auto, 1 fused
+ * tile-DAG kernel, 2 one launch per power); "graphs" (replay the per-power launches as one CUDA
+ * graph, default 1); "resident" (default 0; 1: a matrix that fits half the L2 together with its p+1
+ * working vectors runs all powers of a device-pointer call in one cooperative launch);
+ * "sweep_variant" (0..5) and "coop_variant" (0..3) select row-loop variants for experiments. */
 int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value);
 /* Reads (and clears) the event pairs recorded with "kernel_timing": sum, count and max of the
  * per-launch device durations in milliseconds.  Synchronises on the recorded events. */

@@ -104,6 +104,8 @@ struct mpkg_ctx_s {
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
     bool graphs = true;       // sweep schedule: replay the p launches as one CUDA graph
+    bool resident = false;    // sweep schedule, L2-resident matrix: one cooperative launch (off:
+                              // slower than the per-power graph on C1)
     int64_t sweep_variant = 0;  // sweep-kernel row loop (mpk_exec.cu launch_sweep)
     int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power (mpk_exec.cu)

@@ -114,6 +114,8 @@ struct Executor {
     // fast-mode cooperative rows (build_coop): work items {slot, k0, k1, part or ~0u}, rows split
     // over several items {slot, first part, parts, 0}, and the per-item partial sums
     bool coop_ready = false;
+    DevBuf<uint32_t> res_bar;    // k_mpk_resident grid barrier {arrivals, generation}
+    int res_grid[6] = {0, 0, 0, 0, 0, 0};  // cooperative grid per (kind, sigma)
     DevBuf<uint4> coop_items, coop_multi;
     DevBuf<double> coop_part;
     uint32_t n_coop = 0, n_multi = 0;
@@ -596,6 +598,50 @@ __global__ void __launch_bounds__(256, V == 1 ? 5 : 0) k_mpk_sweep(const __grid_
             dst[s] = acc;  // plain powers in A_perm order: the block slice is the working vector
         else
             row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+    }
+}
+
+// L2-resident matrices (matrix + p+1 working vectors within half the L2, e.g. config C1): all p
+// powers in ONE cooperative launch, a grid-wide barrier between powers instead of a kernel
+// boundary.  The matrix is read from HBM once and from L2 by every later power; the launch-gap
+// per power disappears.  Power q >= 2 reads the slice written in this launch: plain loads after
+// an acquire of the barrier generation (the fused kernels' pattern), never the nc path.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, uint32_t& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        const uint32_t a = atomicAdd(bar, 1u);
+        if (a == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
+            st_release(bar + 1, gen + 1);
+        } else {
+            while (ld_acquire(bar + 1) == gen) {
+            }
+        }
+    }
+    __syncthreads();
+    (void)ld_acquire(bar + 1);
+    ++gen;
+}
+
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_mpk_resident(const __grid_constant__ FusedParams P, uint32_t* bar) {
+    uint32_t gen = ld_acquire(bar + 1);
+    const uint64_t pol = l2_policy_last();
+    for (uint32_t q = 1; q <= P.p; ++q) {
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < P.n_slots;
+             s += (uint64_t)gridDim.x * blockDim.x) {
+            const uint32_t r = SIGMA ? P.slot_row[s] : (uint32_t)s;
+            if (r >= P.n_rows) continue;
+            const uint32_t len = P.row_len[s];
+            const uint64_t off = P.chunk_off[s >> 5];
+            const uint32_t L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
+            const double acc = q == 1 ? sell_row_dot<true, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol)
+                                      : sell_row_dot<false, 8>(P.cols, P.vals, off, L, (uint32_t)(s & 31), len, src, pol);
+            row_epilogue<KIND, SIGMA>(P, (uint32_t)s, r, q, src, acc);
+        }
+        if (q < P.p) grid_barrier(bar, gridDim.x, gen);
     }
 }
 
@@ -1655,6 +1701,10 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (sweep && ctx->mode == MPKG_MODE_FAST && !E.coop_ready) build_coop(ctx, E, A);
     const bool coop = sweep && ctx->mode == MPKG_MODE_FAST && E.n_coop > 0;
     P.sweep_cap = coop ? kMedCap : E.long_cap;
+    // matrix + the p+1 working vectors within half the L2: one cooperative launch (k_mpk_resident)
+    const uint64_t res_bytes = 12ull * A->nnz + 4ull * (A->n_rows + 1) + 8ull * E.n_slots * (a.p + 1);
+    const bool resident = sweep && ctx->resident && !coop && !E.long_rows && a.host_block == nullptr &&
+                          res_bytes <= ctx->l2_bytes / 2 && a.p >= 2;
     P.coop_items = coop ? E.coop_items.p : nullptr;
     P.coop_multi = coop ? E.coop_multi.p : nullptr;
     P.coop_part = coop ? E.coop_part.p : nullptr;
@@ -1812,6 +1862,24 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         }
         join_copies();
         ctx->launches += (uint64_t)a.p * per_power - 1;
+    } else if (sweep && resident) {
+        const int kk = a.kind * 2 + (sigma ? 1 : 0);
+        static void* const fns[6] = {(void*)k_mpk_resident<0, false>, (void*)k_mpk_resident<0, true>,
+                                     (void*)k_mpk_resident<1, false>, (void*)k_mpk_resident<1, true>,
+                                     (void*)k_mpk_resident<2, false>, (void*)k_mpk_resident<2, true>};
+        if (!E.res_bar.p) {
+            E.res_bar.alloc(2);
+            MPKG_CUDA(cudaMemsetAsync(E.res_bar.p, 0, 8, st));
+        }
+        if (!E.res_grid[kk]) {
+            int per_sm = 0;
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[kk], 256, 0));
+            const uint64_t need = (E.n_slots + 255) / 256;
+            E.res_grid[kk] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)per_sm * ctx->sm_count, need));
+        }
+        uint32_t* bar = E.res_bar.p;
+        void* args[] = {(void*)&P, (void*)&bar};
+        MPKG_CUDA(cudaLaunchCooperativeKernel(fns[kk], dim3(E.res_grid[kk]), dim3(256), args, 0, st));
     } else if (sweep) {
         auto launch_all = [&]() {
             for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) power(q);

@@ -155,6 +155,21 @@ def test_tsqr_matches_oracle(ctx, oracle, rows, cols):
     assert_bitwise(r2, r)
 
 
+def test_tsqr_ill_conditioned_newton_like_block(ctx, oracle):
+    """s-step blocks are graded and nearly dependent (cond ~1e9): the narrow (c <= 8) register /
+    compact-WY path must keep Q orthonormal to roundoff like Householder does (a Gram-based QR
+    would lose ~cond * eps of orthogonality)."""
+    rows, cols = 120_000, 8
+    base = random_block(rows, 1, 77)[0]
+    noise = random_block(rows, cols, 78)
+    v_in = np.stack([(base + 10.0 ** (-j - 1) * noise[j]) * 10.0 ** (-j) for j in range(cols)])
+    q, r = ctx.tsqr(v_in)
+    assert np.abs(q @ q.T - np.eye(cols)).max() <= 1e-13
+    assert np.abs(q.T @ r - v_in.T).max() <= 1e-13 * np.abs(v_in).max()
+    q_o, r_o = oracle.tsqr(v_in)
+    assert np.abs(r - r_o).max() <= 1e-10 * np.abs(v_in).max()
+
+
 def test_tsqr_reference_known_answers(ctx):
     # test_ortho.cpp:135-146 orthonormal input gives R = I
     q, _ = ctx.tsqr(random_block(600, 5, 3))

@@ -353,6 +353,50 @@ def test_fast_mode_coop_rows_graph_and_host_paths(ctx, oracle, order):
         set_knobs(ctx, {})
 
 
+@pytest.mark.parametrize("name", ["poisson3d_32", "stencil27_scrambled_20", "random_csr_2000",
+                                  "random_spd_50k"])
+def test_resident_single_launch_matches_oracle(ctx, cases, oracle, name):
+    """L2-resident matrices run all p powers in one cooperative launch (grid barrier between
+    powers) on the device-pointer path: plain, shifted (with a conjugate pair) and polynomial
+    results bit-identical to the oracle and to the per-power graph path (resident=0)."""
+    import torch
+    c = cases[name]
+    P = c["P"]
+    Ap = ctx.csr(P)
+    ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+    n, p = P.n_rows, 6
+    x = mpkg.random_vector(n, 21)
+    d_x = torch.from_numpy(x).cuda()
+    sh = [1.5, 2.0 + 0.5j, 2.0 - 0.5j, 0.25, -1.0, 3.0]
+    coef = [0.5, -1.0, 0.25, 2.0, -0.125, 1.0, 0.75]
+    refs = {"plain": oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, p),
+            "shifted": oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)}
+    zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+    try:
+        for resident in (1, 0, 1):
+            ctx.set_param("resident", resident)
+            plan = ctx.group_levels(ls, Ap, 8 << 20, p)
+            for kind in ("plain", "shifted", "poly"):
+                d_b = torch.full(((p + 1) * n,), float("nan"), dtype=torch.float64, device="cuda")
+                d_z = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                if kind == "plain":
+                    ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, d_b.data_ptr(), n, p + 1)
+                elif kind == "shifted":
+                    ctx.mpk_shifted_dev(plan, Ap, d_x.data_ptr(), sh, d_b.data_ptr(), n, p + 1)
+                else:
+                    ctx.mpk_poly_dev(plan, Ap, d_x.data_ptr(), coef, d_z.data_ptr(), d_b.data_ptr(), n, p + 1)
+                ctx.synchronize()
+                if kind == "poly":
+                    assert_bitwise(d_z.cpu().numpy(), zr, f"{name} poly resident={resident}")
+                    assert_bitwise(d_b.view(p + 1, n).cpu().numpy(), refs["plain"], "poly block")
+                else:
+                    assert_bitwise(d_b.view(p + 1, n).cpu().numpy(), refs[kind], f"{name} {kind} resident={resident}")
+            assert plan.exec_info()["schedule"] == "sweeps"
+    finally:
+        ctx.set_param("resident", 0)
+        set_knobs(ctx, {})
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
