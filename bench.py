@@ -435,6 +435,15 @@ def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist,
         sys.exit(3)
 
 
+def _ncu_traffic(name):
+    """DRAM read + write bytes of one step from the committed ncu summary (profiles/), or None."""
+    prof = ROOT / "profiles" / f"ncu_{name}.json"
+    try:
+        return json.loads(prof.read_text()).get("dram_bytes_per_step")
+    except Exception:
+        return None
+
+
 def run_ortho(args, cfgd):
     """the step after the MPK in s-step GMRES.  A step = ICGS of the s-vector
     Newton block V against the basis Q (`sweeps` rounds of block_dots + block_update) followed by
@@ -553,7 +562,7 @@ def run_ortho(args, cfgd):
                        "l2": "inputs larger than L2 (%.2f GB)" % (8 * n * (qc + s) / 1e9),
                        "parity": ("ok " if parity else "MISMATCH ") + json.dumps(props)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_alg,
+                         "frac": achieved / peak, "traffic": _ncu_traffic("c4ortho"), "algorithmic_bytes": b_alg,
                          "kernel_ms": kernel_ms, "kernel_launches_timed": k_count,
                          "peak_source": peak_src},
             "cpu_baseline": None,
@@ -876,7 +885,7 @@ def main():
              "achieved": sweep_bytes / (kernel_ms / p * 1e-3) / 1e9}
     sweep["frac"] = sweep["achieved"] / peak
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_{args.config}.json"
+    prof = ROOT / "profiles" / f"ncu_{args.config}{'fast' if args.mode == 'fast' else ''}.json"
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
