@@ -187,7 +187,13 @@ def dist_setup(n_gpus):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # NCCL between GPUs; MPKG_DIST_BACKEND=gloo only for the single-GPU smoke test of the
         # sharded path (tests/test_gpu_sharded.py), where ranks share one device
-        dist.init_process_group(os.environ.get("MPKG_DIST_BACKEND", "nccl"))
+        backend = os.environ.get("MPKG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            import torch
+            # NCCL needs the rank's device bound before the communicator is created
+            torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
+        dist.init_process_group(backend)
+        dist.barrier()  # the first collective involves every rank (batch_isend_irecv requirement)
         pg = dist
     return rank, world, local, pg
 

@@ -63,7 +63,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // MMA for k-step u, so the 4 k-slots of step u are rows 16b + u, +4, +8, +12.  Each column
 // read per block is one full 128-byte line.  Partial 8x8 tiles are reduced over the CTA's
 // warps in a fixed order and written per CTA.
-template <int MT>
+template <int MT, bool VEC>
 __global__ void __launch_bounds__(256) k_dots_mma(const double* __restrict__ q, const double* __restrict__ v,
                                                   uint64_t rows, uint32_t qcols, uint32_t vcols,
                                                   uint32_t mq0, uint32_t nv0, double* __restrict__ part) {
@@ -89,7 +89,20 @@ __global__ void __launch_bounds__(256) k_dots_mma(const double* __restrict__ q, 
     for (uint64_t b = blockIdx.x * 8ull + warp; b < n_blocks; b += W) {
         const uint64_t i0 = b * 16 + 4 * r;
         double a[MT][4], bv[4];
-        if (i0 + 3 < rows) {
+        if (VEC && i0 + 3 < rows) {  // 16 B-aligned columns: two LDG.128 per column and lane
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 t = vok ? __ldg(reinterpret_cast<const double2*>(vc + i0) + h) : make_double2(0.0, 0.0);
+                bv[2 * h] = t.x, bv[2 * h + 1] = t.y;
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2 t = qok[mt] ? __ldg(reinterpret_cast<const double2*>(qc[mt] + i0) + h) : make_double2(0.0, 0.0);
+                    a[mt][2 * h] = t.x, a[mt][2 * h + 1] = t.y;
+                }
+        } else if (i0 + 3 < rows) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) bv[u] = vok ? __ldg(vc + i0 + u) : 0.0;
 #pragma unroll
@@ -146,12 +159,12 @@ __global__ void k_dots_finish(const double* __restrict__ part, uint32_t n_parts,
 // v_j[i] <- v_j[i] - c_jk q_k[i] for k = 0..qcols-1 ascending (ortho.hpp:83-90).  A thread owns
 // row i for up to 8 v columns [j0, j0 + 8); the coefficients sit in shared memory.
 template <int VT>
-__global__ void __launch_bounds__(256) k_update(const double* __restrict__ q, const double* __restrict__ c,
-                                                uint64_t rows, uint32_t qcols, uint32_t vcols,
-                                                uint32_t j0, double* __restrict__ v) {
-    extern __shared__ double cs[];  // [VT][qcols]
+__global__ void __launch_bounds__(256, 3) k_update(const double* __restrict__ q, const double* __restrict__ c,
+                                                   uint64_t rows, uint32_t qcols, uint32_t vcols,
+                                                   uint32_t j0, double* __restrict__ v) {
+    extern __shared__ __align__(16) double cs[];  // [qcols][VT]: one k's coefficients are adjacent
     for (uint32_t e = threadIdx.x; e < VT * qcols; e += blockDim.x) {
-        const uint32_t jj = e / qcols, k = e % qcols;
+        const uint32_t k = e / VT, jj = e % VT;
         cs[e] = j0 + jj < vcols ? c[(uint64_t)(j0 + jj) * qcols + k] : 0.0;
     }
     __syncthreads();
@@ -161,6 +174,21 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ q, co
         double x[VT];
 #pragma unroll
         for (int jj = 0; jj < VT; ++jj) x[jj] = jj < (int)nv ? __ldcs(v + (uint64_t)(j0 + jj) * rows + i) : 0.0;
+        auto step = [&](uint32_t k, double qk) {
+            double ck[VT];
+            if constexpr (VT % 2 == 0) {
+#pragma unroll
+                for (int jj = 0; jj < VT; jj += 2) {  // LDS.128: two coefficients per load
+                    const double2 cc = *reinterpret_cast<const double2*>(cs + k * VT + jj);
+                    ck[jj] = cc.x, ck[jj + 1] = cc.y;
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < VT; ++jj) ck[jj] = cs[k * VT + jj];
+            }
+#pragma unroll
+            for (int jj = 0; jj < VT; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(ck[jj], qk));
+        };
         uint32_t k = 0;
         constexpr int U = 8;  // q loads in flight per thread
         for (; k + U <= qcols; k += U) {
@@ -168,15 +196,9 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ q, co
 #pragma unroll
             for (int u = 0; u < U; ++u) qk[u] = __ldcs(q + (uint64_t)(k + u) * rows + i);
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int jj = 0; jj < VT; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[jj * qcols + k + u], qk[u]));
+            for (int u = 0; u < U; ++u) step(k + u, qk[u]);
         }
-        for (; k < qcols; ++k) {
-            const double qk = __ldcs(q + (uint64_t)k * rows + i);
-#pragma unroll
-            for (int jj = 0; jj < VT; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[jj * qcols + k], qk));
-        }
+        for (; k < qcols; ++k) step(k, __ldcs(q + (uint64_t)k * rows + i));
 #pragma unroll
         for (int jj = 0; jj < VT; ++jj)
             if (jj < (int)nv) __stcs(v + (uint64_t)(j0 + jj) * rows + i, x[jj]);
@@ -560,12 +582,18 @@ void gpu_block_dots(mpkg_ctx_s* ctx, const double* q, const double* v, uint64_t 
                 const uint32_t te = MT * 64u;
                 ctx->chain_ws.ensure((uint64_t)grid * te);
                 double* part = ctx->chain_ws.p;
+                // every column 16 B aligned: even row count and aligned base pointers
+                const bool vec = rows % 2 == 0 && ((uintptr_t)q | (uintptr_t)v) % 16 == 0;
+#define MPKG_DOTS(M)                                                                                       \
+    (vec ? k_dots_mma<M, true><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part)    \
+         : k_dots_mma<M, false><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part))
                 switch (MT) {
-                    case 1: k_dots_mma<1><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part); break;
-                    case 2: k_dots_mma<2><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part); break;
-                    case 4: k_dots_mma<4><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part); break;
-                    default: k_dots_mma<8><<<grid, 256, 0, ctx->stream>>>(q, v, rows, qcols, vcols, mq0, nv0, part); break;
+                    case 1: MPKG_DOTS(1); break;
+                    case 2: MPKG_DOTS(2); break;
+                    case 4: MPKG_DOTS(4); break;
+                    default: MPKG_DOTS(8); break;
                 }
+#undef MPKG_DOTS
                 MPKG_LAUNCH_CHECK();
                 k_dots_finish<<<(te * 32 + 255) / 256, 256, 0, ctx->stream>>>(part, grid, te, qcols, vcols, mq0, nv0, c);
                 MPKG_LAUNCH_CHECK();
