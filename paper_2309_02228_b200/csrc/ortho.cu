@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) k_panel_formq(double* __restrict__ a, uin
 // reflectors are recomputed, never stored: one read of the block instead of a write + re-read)
 // and overwrite it with Y = H_0 ... H_{c-1} [M_k; 0].
 constexpr int kTqC = 8;
-constexpr int kTqR = 4;
+constexpr int kTqR = 8;
 constexpr uint32_t kTqPanel = 32u * kTqR;
 
 // Butterfly sums of N independent values: the N shuffle chains interleave (ILP N).
@@ -379,7 +379,7 @@ __device__ __forceinline__ void warp_sum8(double (&v)[8]) {
 // lane <= j) is excluded from step j's reflector.  Writes the panel's R to `rstack`, the
 // reflectors over the panel in place (LAPACK layout: v below the diagonal, R on and above) and
 // the compact-WY factor T (8 x 8 upper triangular, row-major, H_0 ... H_{c-1} = I - V T V^T) to
-// `tmat` (64 doubles per panel).
+// `tmat` (64 doubles per panel), followed by the panel's V_top (64 doubles).
 __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uint64_t lda, uint64_t rows,
                                                      uint32_t np, uint32_t c, double* __restrict__ rstack,
                                                      double* __restrict__ tmat) {
@@ -451,8 +451,14 @@ __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uin
         }
     }
     if (lane < 8) {
+        // T, then V_top (the panel's first 8 reflector rows: unit diagonal, zero above): the
+        // apply kernel's sub-panel warps read it from here, since sub-panel 0 overwrites those
+        // rows of the block with Y
 #pragma unroll
-        for (int j = 0; j < kTqC; ++j) tmat[(uint64_t)k * 64 + lane * 8 + j] = trow[j];
+        for (int j = 0; j < kTqC; ++j) tmat[(uint64_t)k * 128 + lane * 8 + j] = trow[j];
+#pragma unroll
+        for (int l = 0; l < kTqC; ++l)
+            tmat[(uint64_t)k * 128 + 64 + lane * 8 + l] = lane == (uint32_t)l ? 1.0 : (lane < (uint32_t)l ? 0.0 : A[0][l]);
     }
     const uint64_t ldr = (uint64_t)np * c;
     if (lane < c)
@@ -471,11 +477,15 @@ __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uin
 // Apply kernel: Y = (I - V T V^T) [M_k; 0] = [M_k; 0] - V (T (V_top^T M_k)), V_top the panel's
 // top 8 rows (M_k is zero below row c).  No reduction over the panel: the two 8 x 8 products go
 // through per-warp shared memory, then every row is an 8 x 8 matvec.  Overwrites the reflectors.
+constexpr int kAR = 4;                 // apply: rows per lane (one warp per 32*kAR-row sub-panel)
+constexpr uint32_t kSub = kTqR / kAR;  // apply warps per factor panel
+
 __global__ void __launch_bounds__(128) k_tsqr_apply(double* __restrict__ a, uint64_t lda, uint64_t rows,
                                                     uint32_t np, uint32_t c, const double* __restrict__ tmat,
                                                     const double* __restrict__ m, uint64_t ldm) {
     __shared__ double sh[4][3][64];  // per warp: V_top / S, M, T
-    const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t k = gw / kSub, r0 = (gw % kSub) * kAR;  // panel, first 32-row group of the sub-panel
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     if (k >= np) return;  // warp-uniform
     double* Vs = sh[wib][0];
@@ -483,25 +493,17 @@ __global__ void __launch_bounds__(128) k_tsqr_apply(double* __restrict__ a, uint
     double* Ts = sh[wib][2];
     const uint64_t b0 = panel_bound(rows, np, k), b1 = panel_bound(rows, np, k + 1);
     const uint32_t P = (uint32_t)(b1 - b0);
-    double A[kTqR][kTqC];
-#pragma unroll
-    for (int l = 0; l < kTqC; ++l)
-#pragma unroll
-        for (int r = 0; r < kTqR; ++r) {
-            const uint32_t i = lane + 32u * r;
-            double v = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
-            if (r == 0) v = lane == (uint32_t)l ? 1.0 : (lane < (uint32_t)l ? 0.0 : v);
-            A[r][l] = v;
-        }
     double m0[kTqC];
 #pragma unroll
     for (int l = 0; l < kTqC; ++l) m0[l] = ((uint32_t)l < c && lane < c) ? m[(uint64_t)l * ldm + (uint64_t)k * c + lane] : 0.0;
     if (lane < 8) {
 #pragma unroll
-        for (int l = 0; l < kTqC; ++l) Vs[lane * 8 + l] = A[0][l], Ms[lane * 8 + l] = m0[l];
+        for (int l = 0; l < kTqC; ++l) Ms[lane * 8 + l] = m0[l];
     }
-    Ts[lane] = tmat[(uint64_t)k * 64 + lane];
-    Ts[lane + 32] = tmat[(uint64_t)k * 64 + lane + 32];
+    Ts[lane] = tmat[(uint64_t)k * 128 + lane];
+    Ts[lane + 32] = tmat[(uint64_t)k * 128 + lane + 32];
+    Vs[lane] = tmat[(uint64_t)k * 128 + 64 + lane];  // V_top as stored by the factor kernel
+    Vs[lane + 32] = tmat[(uint64_t)k * 128 + 96 + lane];
     __syncwarp();
     // W = V_top^T M (entries e = lane, lane + 32: row e/8, column e%8)
     double wv[2];
@@ -529,16 +531,34 @@ __global__ void __launch_bounds__(128) k_tsqr_apply(double* __restrict__ a, uint
     Vs[lane] = wv[0];  // V_top no longer read (all lanes passed the W loop before the last sync)
     Vs[lane + 32] = wv[1];
     __syncwarp();
+    // Y = [M; 0] - V S on this warp's sub-panel (S recomputed per warp: two 8 x 8 products)
+    {
+        double A[kAR][kTqC];
 #pragma unroll
-    for (int l = 0; l < kTqC; ++l) {
-        if ((uint32_t)l >= c) break;
+        for (int l = 0; l < kTqC; ++l)
 #pragma unroll
-        for (int r = 0; r < kTqR; ++r) {
-            double y = r == 0 ? m0[l] : 0.0;
+            for (int r = 0; r < kAR; ++r) {
+                const uint32_t i = lane + 32u * (r0 + r);
+                double v = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
+                if (r0 + r == 0) v = lane == (uint32_t)l ? 1.0 : (lane < (uint32_t)l ? 0.0 : v);
+                A[r][l] = v;
+            }
+#pragma unroll 1
+        for (uint32_t l = 0; l < c; ++l) {  // one S column (8 LDS) at a time keeps registers low
+            double sc[kTqC];
 #pragma unroll
-            for (int j = 0; j < kTqC; ++j) y -= A[r][j] * Vs[j * 8 + l];
-            const uint32_t i = lane + 32u * r;
-            if (i < P) a[(uint64_t)l * lda + b0 + i] = y;
+            for (int j = 0; j < kTqC; ++j) sc[j] = Vs[j * 8 + l];
+            double ml = 0.0;
+#pragma unroll
+            for (int t = 0; t < kTqC; ++t) ml = (uint32_t)t == l ? m0[t] : ml;
+#pragma unroll
+            for (int r = 0; r < kAR; ++r) {
+                double y = (r0 + r == 0) ? ml : 0.0;
+#pragma unroll
+                for (int j = 0; j < kTqC; ++j) y -= A[r][j] * sc[j];
+                const uint32_t i = lane + 32u * (r0 + r);
+                if (i < P) a[(uint64_t)l * lda + b0 + i] = y;
+            }
         }
     }
 }
@@ -675,7 +695,7 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
         rr = np * c;
     }
     uint64_t ws = (uint64_t)c * c;  // M for the top panel
-    const uint64_t tslot = narrow ? 64u : c;  // narrow: compact-WY T per panel, else taus
+    const uint64_t tslot = narrow ? 128u : c;  // narrow: compact-WY T + V_top per panel, else taus
     for (size_t L = 0; L < lv_rows.size(); ++L) ws += lv_np[L] * tslot + lv_np[L] * c * c;
     ctx->tsqr_ws.ensure(ws);  // per-context workspace, stream-ordered reuse
     double* p = ctx->tsqr_ws.p;
@@ -706,7 +726,7 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
         uint64_t ldm = c;
         for (size_t L = lv.size(); L-- > 0;) {
             const Level& l = lv[L];
-            k_tsqr_apply<<<(l.np * 32u + 127u) / 128u, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c,
+            k_tsqr_apply<<<(l.np * kSub * 32u + 127u) / 128u, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c,
                                                                            l.taus, m, ldm);
             MPKG_LAUNCH_CHECK();
             m = l.a;
