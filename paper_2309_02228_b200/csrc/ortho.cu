@@ -205,6 +205,112 @@ __global__ void __launch_bounds__(256, 3) k_update(const double* __restrict__ q,
     }
 }
 
+// Fast-mode ICGS: one sweep's update fused with the NEXT sweep's dots.  A CTA takes 256-row
+// tiles: first every thread updates its row exactly like k_update (ascending k, mul then sub:
+// bit-identical; 8 Q loads in flight), writes it and parks it in shared memory; then each warp
+// runs the fp64 tensor-core products Q^T V_new for two 16-row blocks of the tile (k_dots_mma's
+// fragment layout), re-reading Q from L1/L2 where the update just brought it.  Saves one full
+// HBM read of Q and V per extra sweep.
+template <int MT>
+__global__ void __launch_bounds__(256) k_update_dots(const double* __restrict__ q, const double* __restrict__ c,
+                                                     uint64_t rows, uint32_t qcols, uint32_t vcols, uint32_t nv0,
+                                                     double* __restrict__ v, double* __restrict__ part) {
+    // the tile's updated rows (256 x 9, padded) during the sweep, the per-warp partial tiles after
+    constexpr int kBuf = 8 * MT * 64 > 256 * 9 ? 8 * MT * 64 : 256 * 9;
+    __shared__ double sbuf[kBuf];
+    double (*xs)[9] = reinterpret_cast<double (*)[9]>(sbuf);
+    double (*red)[MT * 64] = reinterpret_cast<double (*)[MT * 64]>(sbuf);
+    extern __shared__ __align__(16) double cs[];  // [qcols][8] coefficients of V columns nv0..nv0+7
+    for (uint32_t e = threadIdx.x; e < 8u * qcols; e += blockDim.x) {
+        const uint32_t k = e >> 3, jj = e & 7u;
+        cs[e] = nv0 + jj < vcols ? c[(uint64_t)(nv0 + jj) * qcols + k] : 0.0;
+    }
+    __syncthreads();
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const uint32_t g = lane >> 2, r = lane & 3u;
+    const uint32_t nv = vcols - nv0 < 8u ? vcols - nv0 : 8u;
+    const double* qc[MT];
+    bool qok[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const uint32_t col = 8 * mt + g;
+        qok[mt] = col < qcols;
+        qc[mt] = q + (uint64_t)(qok[mt] ? col : 0) * rows;
+    }
+    double acc[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const uint64_t n_tiles = (rows + 255) / 256;
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint64_t i = tile * 256 + t;
+        double x[8];
+        if (i < rows) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) x[jj] = jj < (int)nv ? __ldcs(v + (uint64_t)(nv0 + jj) * rows + i) : 0.0;
+            uint32_t k = 0;
+            constexpr int U = 8;
+            for (; k + U <= qcols; k += U) {
+                double qk[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) qk[u] = __ldg(q + (uint64_t)(k + u) * rows + i);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const double2* c2 = reinterpret_cast<const double2*>(cs + (k + u) * 8);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double2 cc = c2[h];
+                        x[2 * h] = __dsub_rn(x[2 * h], __dmul_rn(cc.x, qk[u]));
+                        x[2 * h + 1] = __dsub_rn(x[2 * h + 1], __dmul_rn(cc.y, qk[u]));
+                    }
+                }
+            }
+            for (; k < qcols; ++k) {
+                const double qk = __ldg(q + (uint64_t)k * rows + i);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[k * 8 + jj], qk));
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+                if (jj < (int)nv) __stcs(v + (uint64_t)(nv0 + jj) * rows + i, x[jj]);
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) x[jj] = 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) xs[t][jj] = jj < (int)nv ? x[jj] : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t rb = (2 * warp + h) * 16 + 4 * r;  // tile-local first row of this lane
+            const uint64_t i0 = tile * 256 + rb;
+            double a[MT][4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bv[u] = xs[rb + u][g];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[mt][u] = (qok[mt] && i0 + u < rows) ? __ldg(qc[mt] + i0 + u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], a[mt][u], bv[u]);
+        }
+        __syncthreads();  // xs is rewritten by the next tile
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        red[warp][mt * 64 + g * 8 + 2 * r] = acc[mt][0];
+        red[warp][mt * 64 + g * 8 + 2 * r + 1] = acc[mt][1];
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < MT * 64; e += blockDim.x) {
+        double s = red[0][e];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) s += red[w][e];
+        part[(uint64_t)blockIdx.x * (MT * 64) + e] = s;
+    }
+}
+
 // coeff[e] += c[e] (ortho.hpp:112-114)
 __global__ void k_accumulate(double* __restrict__ coeff, const double* __restrict__ c, uint32_t n) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -651,19 +757,61 @@ void gpu_block_update(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_
     timing_end(ctx, ev);
 }
 
+// V <- V - Q c (bitwise, as k_update) and c_next = Q^T V_new (fast-mode products), fused.
+void gpu_update_dots(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_t rows, uint32_t qcols,
+                     uint32_t vcols, double* v, double* c_next) {
+    const auto ev = timing_begin(ctx);
+    const uint64_t n_tiles = (rows + 255) / 256;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 3u, n_tiles));
+    const uint32_t left = (qcols + 7) / 8;
+    const int MT = left > 4 ? 8 : left > 2 ? 4 : left > 1 ? 2 : 1;
+    const uint32_t te = MT * 64u;
+    ctx->chain_ws.ensure((uint64_t)grid * te);
+    double* part = ctx->chain_ws.p;
+    const size_t smem = 64ull * qcols;
+    for (uint32_t nv0 = 0; nv0 < vcols; nv0 += 8) {
+        switch (MT) {
+            case 1: k_update_dots<1><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+            case 2: k_update_dots<2><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+            case 4: k_update_dots<4><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+            default: k_update_dots<8><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+        }
+        MPKG_LAUNCH_CHECK();
+        k_dots_finish<<<(te * 32 + 255) / 256, 256, 0, ctx->stream>>>(part, grid, te, qcols, vcols, 0, nv0, c_next);
+        MPKG_LAUNCH_CHECK();
+        ctx->launches += 2;
+    }
+    timing_end(ctx, ev);
+}
+
 void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
               int sweeps, double* coeff) {
     const uint32_t ne = qcols * vcols;
     if (!ne) return;
     MPKG_CUDA(cudaMemsetAsync(coeff, 0, 8ull * ne, ctx->stream));
-    ctx->ortho_c.ensure(ne);  // per-context workspace: no allocation on the steady-state path
+    ctx->ortho_c.ensure(2ull * ne);  // per-context workspace: no allocation on the steady-state path
     double* cbuf = ctx->ortho_c.p;
-    for (int sw = 0; sw < sweeps; ++sw) {
-        gpu_block_dots(ctx, q, v, rows, qcols, vcols, cbuf);
-        gpu_block_update(ctx, q, cbuf, rows, qcols, vcols, v);
-        k_accumulate<<<(ne + 255) / 256, 256, 0, ctx->stream>>>(coeff, cbuf, ne);
+    double* cnext = cbuf + ne;
+    auto accumulate = [&](const double* cc) {
+        k_accumulate<<<(ne + 255) / 256, 256, 0, ctx->stream>>>(coeff, cc, ne);
         MPKG_LAUNCH_CHECK();
         ctx->launches += 1;
+    };
+    // fast mode, several sweeps: each update but the last also produces the next sweep's dots
+    const bool fuse = ctx->mode == MPKG_MODE_FAST && sweeps >= 2 && qcols <= 64 && rows > 0;
+    bool have_c = false;  // cbuf already holds this sweep's Q^T V (from a fused update)
+    for (int sw = 0; sw < sweeps; ++sw) {
+        if (!have_c) gpu_block_dots(ctx, q, v, rows, qcols, vcols, cbuf);
+        if (fuse && sw + 1 < sweeps) {
+            gpu_update_dots(ctx, q, cbuf, rows, qcols, vcols, v, cnext);
+            accumulate(cbuf);
+            std::swap(cbuf, cnext);
+            have_c = true;
+            continue;
+        }
+        gpu_block_update(ctx, q, cbuf, rows, qcols, vcols, v);
+        accumulate(cbuf);
+        have_c = false;
     }
 }
 

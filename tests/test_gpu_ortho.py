@@ -122,13 +122,17 @@ def test_icgs_reference_known_answers(ctx, oracle, m):
         assert_bitwise(out, v)
 
 
-@pytest.mark.parametrize("rows,qcols,vcols", [(1000, 25, 8), (100_003, 9, 4)])
-def test_icgs_fast_mode_tolerance(ctx, oracle, rows, qcols, vcols):
+@pytest.mark.parametrize("sweeps", [2, 3])
+@pytest.mark.parametrize("rows,qcols,vcols", [(1000, 25, 8), (100_003, 9, 4), (20_001, 64, 12),
+                                              (5000, 70, 3), (33, 1, 1)])
+def test_icgs_fast_mode_tolerance(ctx, oracle, rows, qcols, vcols, sweeps):
+    """Fast mode: tensor-core dots, and every update but the last fused with the next sweep's
+    dots (k_update_dots; qcols <= 64).  Within tolerance of the oracle's serial ICGS."""
     q, _ = oracle.tsqr(random_block(rows, qcols, 5))
     v = random_block(rows, vcols, 6)
-    want_v, want_c = oracle.icgs(q, v, 2)
+    want_v, want_c = oracle.icgs(q, v, sweeps)
     with _mode(ctx, "fast"):
-        got_v, got_c = ctx.icgs_block_orthogonalize(q, v, 2)
+        got_v, got_c = ctx.icgs_block_orthogonalize(q, v, sweeps)
     vmax = np.abs(v).max()
     assert np.abs(got_c - want_c).max() <= 1e-12 * np.sqrt(rows) * vmax
     assert np.abs(got_v - want_v).max() <= 1e-12 * vmax
