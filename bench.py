@@ -258,15 +258,28 @@ def run_reference(args, cfgd):
     if not reference_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref/libmpkref.so not built"}), flush=True)
         return
-    if cfgd["kind"] == "ortho":
-        print(json.dumps({**base, "unavailable": "the reference's ortho.hpp needs Eigen, which is "
-                          "not installed; its algorithm is restated in oracle/oracle.c (pinned by "
-                          "test_ortho.cpp's known answers)"}), flush=True)
-        return
-    if cfgd["kind"] in CHAIN_KINDS:
-        print(json.dumps({**base, "unavailable": "the reference's s-step / polynomial drivers "
-                          "(sstep.hpp, poly.hpp) need Eigen, which is not installed; only their "
-                          "jacobi.hpp / gs2.hpp stages compile (oracle/_ref)"}), flush=True)
+    if cfgd["kind"] == "ortho" or cfgd["kind"] in CHAIN_KINDS:
+        # ortho.hpp / sstep.hpp / poly.hpp need Eigen (not installed): the reference arm times the
+        # oracle's C restatement of the same computation on the same inputs (kind "port")
+        if cfgd["kind"] == "ortho":
+            n = 192 ** 3
+            cb = port_ortho_baseline(cfgd, n, args.seed, args.steps)
+            cfg = {"workload": cfgd["desc"], "n": n, "qcols": cfgd["qcols"], "vcols": cfgd["p"]}
+        else:
+            R = Reference()
+            A = make_matrix(args.config, args.seed)
+            P, perm, _, prep = ref_preprocess(R, A, p, host_llc_bytes())
+            x = np.empty(A.n_rows)
+            x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)
+            cb = port_chain_baseline(cfgd, P, x, args.steps)
+            cfg = {"workload": cfgd["desc"], "n": A.n_rows, "nnz": A.nnz, "p": p, "preprocess_s": prep}
+        med_ms = cb.pop("ms")
+        line = {**base, "value": cb["value"], "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": med_ms, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, DESIGN.md §6)", "config": {**cfg, "cpu": cpu_model()},
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
         return
     R = Reference()
     A = make_matrix(args.config, args.seed)
@@ -293,6 +306,73 @@ def run_reference(args, cfgd):
                                        f"{args.steps} after {args.warmup} warm-up"},
             "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def chain_flops(cfgd, nnz, n):
+    """Flop convention of the chain / polynomial configs (SpMV-shaped stages, 2 per entry)."""
+    p = cfgd["p"]
+    if cfgd["kind"] == "sstep_jacobi":  # (sweeps - 1) Jacobi sweeps + the terminal product per power
+        return 2.0 * nnz * p * cfgd["sweeps"]
+    if cfgd["kind"] == "sstep_gs2":  # per sweep: full-row stage 0 + gamma half-row inner; terminal
+        return p * (cfgd["sweeps"] * (2.0 * nnz + cfgd["gamma"] * nnz) + 2.0 * nnz)
+    if cfgd["kind"] == "polyprod":  # degree-1 SpMV-shaped terminals
+        return 2.0 * nnz * (p - 1)
+    raise ValueError(cfgd["kind"])
+
+
+def port_chain_baseline(cfgd, P, x, steps):
+    """The chain configs' CPU baseline: the oracle's C restatement (one thread) of the same chain on
+    the same A_perm and x -- the reference's own sstep.hpp / poly.hpp need Eigen and do not build
+    here.  Bounded sample: 1 warm-up + min(steps, 3) timed runs of the full workload."""
+    from oracle.oracle import Oracle
+    O = Oracle()
+    rp, ci, v = P
+    p = cfgd["p"]
+    if cfgd["kind"] == "sstep_jacobi":
+        fn = lambda: O.sstep_jacobi_block(rp, ci, v, cfgd["sweeps"], x, newton_shifts(p))  # noqa: E731
+    elif cfgd["kind"] == "sstep_gs2":
+        fn = lambda: O.sstep_gs2_block(rp, ci, v, cfgd["gamma"], cfgd["sweeps"], True, x, newton_shifts(p))  # noqa: E731
+    else:
+        roots = leja_chebyshev_roots(p)
+        fn = lambda: O.poly_apply(rp, ci, v, roots, x)  # noqa: E731
+    fn()
+    k = max(1, min(steps, 3))
+    ts = []
+    for _ in range(k):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    gf = chain_flops(cfgd, len(ci), len(rp) - 1) / med * 1e-9
+    return {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "port", "ms": med * 1e3,
+            "sample": f"full workload through the oracle's C restatement (oracle/oracle.c, one thread; "
+                      f"the reference's chain driver needs Eigen): 1 warm-up + median of {k} "
+                      f"({med:.2f} s each); cpu: {cpu_model()}"}
+
+
+def port_ortho_baseline(cfgd, n, seed, steps):
+    """c4ortho's CPU baseline: ICGS + TSQR through the oracle's C restatement (one thread) on a
+    seeded block of the same shape (ortho.hpp needs Eigen).  1 warm-up-free timed run per step,
+    at most 2."""
+    from oracle.oracle import Oracle
+    O = Oracle()
+    rng = np.random.default_rng(seed)
+    Q, _ = O.tsqr(rng.uniform(-1.0, 1.0, (cfgd["qcols"], n)))
+    V0 = rng.uniform(-1.0, 1.0, (cfgd["p"], n))
+    k = max(1, min(steps, 2))
+    ts = []
+    for _ in range(k):
+        t0 = time.perf_counter()
+        Vo, _ = O.icgs(Q, V0, cfgd["sweeps"])
+        O.tsqr(Vo)
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    s, qc = cfgd["p"], cfgd["qcols"]
+    flops = cfgd["sweeps"] * 4.0 * n * qc * s + 4.0 * n * s * s
+    return {"value": flops / med * 1e-9, "unit": "GFLOP/s", "cores": 1, "kind": "port", "ms": med * 1e3,
+            "sample": f"full workload (n = {n}, {qc}-column basis, {s}-column block, {cfgd['sweeps']} "
+                      f"sweeps + TSQR) through the oracle's C restatement, one thread: median of {k} "
+                      f"({med:.2f} s each); cpu: {cpu_model()}"}
 
 
 def cpu_baseline_reference(A_perm_host, perm_unused, ls_level_ptr, p, x, kind, nnz, ctx=None):
@@ -556,6 +636,10 @@ def run_ortho(args, cfgd):
            "h2d_bytes_per_step": 8 * n * (qc + s) * 2,  # icgs + tsqr calls each stage their inputs
            "d2h_bytes_per_step": 8 * n * s * 2 + 8 * (s * qc + s * s), "ms_per_step": e_ms,
            "note": "two host-pointer calls (icgs, tsqr), wall clock"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = port_ortho_baseline(cfgd, n, args.seed, args.steps)
+        cpu.pop("ms")
     if rank == 0:
         line = {
             "metric": METRIC, "value": flops / (step_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
@@ -571,7 +655,7 @@ def run_ortho(args, cfgd):
                          "frac": achieved / peak, "traffic": _ncu_traffic("c4ortho"), "algorithmic_bytes": b_alg,
                          "kernel_ms": kernel_ms, "kernel_launches_timed": k_count,
                          "peak_source": peak_src},
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -806,12 +890,8 @@ def main():
     flops = 2.0 * nnz * p
     if cfgd["kind"] == "poly":
         flops += 2.0 * n * (p + 1)
-    elif cfgd["kind"] == "sstep_jacobi":  # SpMV-shaped stages per power: (sweeps - 1) + terminal
-        flops = 2.0 * nnz * p * cfgd["sweeps"]
-    elif cfgd["kind"] == "sstep_gs2":  # per sweep: full-row stage 0 + gamma half-row inner; terminal
-        flops = p * (cfgd["sweeps"] * (2.0 * nnz + cfgd["gamma"] * nnz) + 2.0 * nnz)
-    elif cfgd["kind"] == "polyprod":  # degree-1 SpMV-shaped terminals
-        flops = 2.0 * nnz * (p - 1)
+    elif cfgd["kind"] in CHAIN_KINDS:
+        flops = chain_flops(cfgd, nnz, n)
     value = world * flops / (step_ms * 1e-3) * 1e-9
 
     # ---- e2e through the host-pointer C ABI (pinned buffers, copies inside the timed region) --
@@ -902,8 +982,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         P_host = Ap.download()
-        kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
-        cpu = cpu_baseline_reference(P_host, None, ls.level_ptr, p, x_perm, kind, nnz)
+        if chain is not None:
+            cpu = port_chain_baseline(cfgd, (P_host.row_ptr, P_host.col_idx, P_host.values), x_perm, args.steps)
+            cpu.pop("ms")
+        else:
+            kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
+            cpu = cpu_baseline_reference(P_host, None, ls.level_ptr, p, x_perm, kind, nnz)
 
     if rank == 0:
         line = {
