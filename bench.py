@@ -803,6 +803,9 @@ def main():
     exec_info = plan.exec_info()
     kname = ("k_mpk_sweep" if exec_info["schedule"] == "sweeps" else
              {0: "k_mpk_lean", 1: "k_mpk_fused", 2: "k_mpk_warptile", 4: "k_mpk_async"}.get(exec_info["kernel"], "?"))
+    if exec_info["schedule"] == "sweeps" and exec_info.get("long_rows"):
+        kname = ("k_coop_rows (side stream) beside k_mpk_sweep" if args.mode == "fast" else
+                 "k_long_rows_bitwise (side stream, the hub row's add chain) beside k_mpk_sweep")
     exec_info["dominant_kernel"] = kname
     if chain is not None:
         exec_info = {"dominant_kernel": "k_poly_terminal" if precon is None else "k_pc_stage / k_gs2_stage (precon.cu)",

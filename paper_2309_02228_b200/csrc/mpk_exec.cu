@@ -114,6 +114,7 @@ struct Executor {
     // fast-mode cooperative rows (build_coop): work items {slot, k0, k1, part or ~0u}, rows split
     // over several items {slot, first part, parts, 0}, and the per-item partial sums
     bool coop_ready = false;
+    DevBuf<uint32_t> long_sorted;  // long slots, longest row first (k_long_rows_bitwise)
     DevBuf<uint32_t> res_bar;    // k_mpk_resident grid barrier {arrivals, generation}
     int res_grid[6] = {0, 0, 0, 0, 0, 0};  // cooperative grid per (kind, sigma)
     DevBuf<uint4> coop_items, coop_multi;
@@ -506,7 +507,7 @@ __device__ __forceinline__ void row_epilogue(const FusedParams& P, uint32_t s, u
 // double-buffered shared-memory ring while thread 0 adds chunk c from the other half at
 // shared-memory latency, two products per LDS.128.  Returns true (sum in thread 0's `acc`)
 // when slot s0 holds a long row.
-template <bool SIGMA>
+template <bool SIGMA, uint32_t kLongChunk = kLongChunk>
 __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, uint32_t q,
                                              uint64_t pol, uint32_t tid, uint32_t nt, double& acc,
                                              double* ring) {
@@ -548,10 +549,21 @@ __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, 
             const uint32_t m = min(kLongChunk, len - c * kLongChunk);
             const double2* cur = reinterpret_cast<const double2*>(ring + (c & 1u) * kLongChunk);
             uint32_t i = 0;
+            // the next 8 products are loaded while the current 8 are added: the chain pays DADD
+            // latency only, not shared-memory latency
+            double2 nx[4];
+            if (m >= 8) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) nx[j] = cur[j];
+            }
             for (; i + 8 <= m; i += 8) {
                 double2 v[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = cur[i / 2 + j];
+                for (int j = 0; j < 4; ++j) v[j] = nx[j];
+                if (i + 16 <= m) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) nx[j] = cur[(i + 8) / 2 + j];
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     acc = __dadd_rn(acc, v[j].x);
@@ -701,6 +713,27 @@ __global__ void __launch_bounds__(256) k_long_rows_fast(const __grid_constant__ 
             for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += part[w];
             row_epilogue<KIND, SIGMA>(P, s, r, q, src, t);
         }
+        __syncthreads();
+    }
+}
+
+// Bitwise mode, sweep schedule: the long rows (left out of the SELL arrays), one CTA per row,
+// longest first, on a side stream concurrently with the power's k_mpk_sweep.  Each row goes
+// through long_row_dot: warps 1.. form the products in a double-buffered shared-memory ring while
+// thread 0 adds them in stored order -- the reference's sum, bit for bit.  The longest row's add
+// chain bounds the power; the short rows' sweep runs beside it instead of behind it.
+constexpr uint32_t kBwChunk = 1024;  // k_long_rows_bitwise: products per ring half (2 x 8 KB)
+
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_long_rows_bitwise(const __grid_constant__ FusedParams P, uint32_t q) {
+    extern __shared__ __align__(16) double bw_ring[];  // 2 x kBwChunk products
+    const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    const uint64_t pol = l2_policy_first();
+    for (uint32_t i = blockIdx.x; i < P.n_long; i += gridDim.x) {
+        const uint32_t s = P.long_slots[i];
+        double acc = 0.0;
+        (void)long_row_dot<SIGMA, kBwChunk>(P, s, q, pol, threadIdx.x, blockDim.x, acc, bw_ring);
+        if (threadIdx.x == 0) row_epilogue<KIND, SIGMA>(P, s, SIGMA ? P.slot_row[s] : s, q, src, acc);
         __syncthreads();
     }
 }
@@ -1302,6 +1335,10 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
             E->long_slots.alloc(std::max<size_t>(ls.size(), 1));
             if (!ls.empty())
                 MPKG_CUDA(cudaMemcpyAsync(E->long_slots.p, ls.data(), 4ull * ls.size(), cudaMemcpyHostToDevice, st));
+            std::stable_sort(ls.begin(), ls.end(), [&](uint32_t x, uint32_t y) { return rl[x] > rl[y]; });
+            E->long_sorted.alloc(std::max<size_t>(ls.size(), 1));
+            if (!ls.empty())
+                MPKG_CUDA(cudaMemcpyAsync(E->long_sorted.p, ls.data(), 4ull * ls.size(), cudaMemcpyHostToDevice, st));
         } else {
             E->n_tiles = (A->n_rows + E->tile_rows - 1) / E->tile_rows;
         }
@@ -1649,9 +1686,10 @@ void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
 
 bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
     if (ctx->schedule == 1) return false;
-    // Long rows live outside the SELL arrays: bitwise mode runs them through the fused kernel's
-    // stored-order path; fast mode reduces them in k_long_rows_fast between sweeps.
-    if (E.long_rows && ctx->mode != MPKG_MODE_FAST) return false;
+    // Long rows live outside the SELL arrays.  Fast mode reduces them in k_coop_rows beside the
+    // sweeps; bitwise mode adds them in stored order in k_long_rows_bitwise beside the sweeps
+    // (R-MAT scale 21: 2.79 ms vs 2.93 ms for the fused kernel's CTA-cooperative path; both are
+    // bounded by the hub row's chain of 102,493 dependent adds).
     return true;
 }
 
@@ -1700,6 +1738,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     // included) run in k_coop_rows on a side stream, concurrently with each power's sweep
     if (sweep && ctx->mode == MPKG_MODE_FAST && !E.coop_ready) build_coop(ctx, E, A);
     const bool coop = sweep && ctx->mode == MPKG_MODE_FAST && E.n_coop > 0;
+    const bool bw_long = sweep && ctx->mode != MPKG_MODE_FAST && E.long_rows > 0;
     P.sweep_cap = coop ? kMedCap : E.long_cap;
     // matrix + the p+1 working vectors within half the L2: one cooperative launch (k_mpk_resident)
     const uint64_t res_bytes = 12ull * A->nnz + 4ull * (A->n_rows + 1) + 8ull * E.n_slots * (a.p + 1);
@@ -1755,7 +1794,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     // other case runs k_mpk_sweep (private order, polynomial accumulator, long rows skipped).
     auto sweep_power = [&](uint32_t q) {
         const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
-        if (!sigma && a.kind <= 1 && !E.long_rows && !coop && sv == 0) {
+        if (!sigma && a.kind <= 1 && !E.long_rows && !coop && sv == 0) {  // (bw_long implies long rows)
             const double* src = a.block + (uint64_t)(q - 1) * a.rows;
             const double* src2 = q >= 2 ? a.block + (uint64_t)(q - 2) * a.rows : src;
             launch_spmv_sell_raw(ctx, S, a.kind == 1, src, a.block + (uint64_t)q * a.rows, src2,
@@ -1777,13 +1816,42 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     // branches) or, without cooperative items, k_long_rows_fast after the sweep.
     const unsigned gl = (unsigned)std::min<uint64_t>(std::max<uint64_t>(E.long_rows, 1), (uint64_t)ctx->sm_count * 8u);
     const unsigned gc = (unsigned)std::min<uint64_t>(std::max<uint64_t>((E.n_coop + 7) / 8, 1), (uint64_t)ctx->sm_count * 8u);
-    if (coop && !ctx->aux) {
+    if ((coop || bw_long) && !ctx->aux) {
+        const void* fns[6] = {(const void*)k_long_rows_bitwise<0, false>, (const void*)k_long_rows_bitwise<0, true>,
+                              (const void*)k_long_rows_bitwise<1, false>, (const void*)k_long_rows_bitwise<1, true>,
+                              (const void*)k_long_rows_bitwise<2, false>, (const void*)k_long_rows_bitwise<2, true>};
+        for (const void* f : fns)  // once per context (device)
+            MPKG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kBwChunk * 8)));
         MPKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
         MPKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
         MPKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     }
+    // bitwise sweeps over a matrix with rows longer than the SELL cap: k_long_rows_bitwise beside
+    // the sweep, one CTA per long row, longest first
+    FusedParams Pb = P;
+    Pb.long_slots = E.long_sorted.p;
     auto power = [&](uint32_t q) {
         const int kk = a.kind * 2 + (sigma ? 1 : 0);
+        if (bw_long) {
+            cudaStream_t ax = ctx->aux;
+            MPKG_CUDA(cudaEventRecord(ctx->fork_ev, st));
+            MPKG_CUDA(cudaStreamWaitEvent(ax, ctx->fork_ev, 0));
+            const unsigned gb = (unsigned)E.long_rows;  // one CTA per long row, longest first
+            switch (kk) {
+                case 0: k_long_rows_bitwise<0, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                case 1: k_long_rows_bitwise<0, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                case 2: k_long_rows_bitwise<1, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                case 3: k_long_rows_bitwise<1, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                case 4: k_long_rows_bitwise<2, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                default: k_long_rows_bitwise<2, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+            }
+            MPKG_LAUNCH_CHECK();
+            MPKG_CUDA(cudaEventRecord(ctx->join_ev, ax));
+            sweep_power(q);
+            MPKG_LAUNCH_CHECK();
+            MPKG_CUDA(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+            return;
+        }
         if (coop) {
             cudaStream_t ax = ctx->aux;
             MPKG_CUDA(cudaEventRecord(ctx->fork_ev, st));

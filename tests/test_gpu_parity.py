@@ -244,12 +244,15 @@ def _arrow_matrix(n=6000, hubs=(0, 17, 2500), seed=5):
     return mpkg.HostCsr.from_arrays(rp, ci, vv)
 
 
+@pytest.mark.parametrize("schedule", [0, 1, 2])
 @pytest.mark.parametrize("order", [-1, 0, 1, 2])
-def test_long_rows_and_length_order(ctx, oracle, order):
-    """Hub rows (>1024 entries) take the CTA-cooperative path of the fused kernel (auto schedule
-    keeps the fused kernel for them); every order gives the same bits."""
+def test_long_rows_and_length_order(ctx, oracle, order, schedule):
+    """Hub rows (>1024 entries) are added in stored order by a CTA each: beside the sweeps on a
+    side stream (auto / schedule=2, k_long_rows_bitwise) or inside the fused kernel (schedule=1).
+    Every order and schedule gives the reference's bits, on the host- and device-pointer paths."""
+    import torch
     try:
-        set_knobs(ctx, {"order": order})
+        set_knobs(ctx, {"order": order, "schedule": schedule})
         for A in (_arrow_matrix(), mpkg.rmat(15, 16, 7)):
             lv, pm, ip, lp = oracle.build_levels(A.row_ptr, A.col_idx)
             P = mpkg.HostCsr.from_arrays(*oracle.permute(A.row_ptr, A.col_idx, A.values, pm))
@@ -261,8 +264,17 @@ def test_long_rows_and_length_order(ctx, oracle, order):
             ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4)
             assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref, f"order={order}")
             info = plan.exec_info()
-            if order != 0:  # the private-order SELL leaves hub rows out: fused long-row path
-                assert info["schedule"] == "fused" and info["long_rows"] > 0
+            if order != 0:  # the private-order SELL leaves hub rows out: CTA-cooperative path
+                assert info["long_rows"] > 0
+            want = "fused" if schedule == 1 else "sweeps"
+            assert info["schedule"] == want
+            n = P.n_rows
+            d_x = torch.from_numpy(x).cuda()
+            d_b = torch.full((5 * n,), float("nan"), dtype=torch.float64, device="cuda")
+            for _ in range(2):  # capture, then replay
+                ctx.mpk_dev(plan, Ap, d_x.data_ptr(), 4, d_b.data_ptr(), n, 5)
+                ctx.synchronize()
+                assert_bitwise(d_b.view(5, n).cpu().numpy(), ref, f"device path order={order}")
             sh = [1.0, 2.0 + 0.5j, 2.0 - 0.5j, 0.5]
             ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
             assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, "shifted")
