@@ -718,22 +718,112 @@ __global__ void __launch_bounds__(256) k_long_rows_fast(const __grid_constant__ 
 }
 
 // Bitwise mode, sweep schedule: the long rows (left out of the SELL arrays), one CTA per row,
-// longest first, on a side stream concurrently with the power's k_mpk_sweep.  Each row goes
-// through long_row_dot: warps 1.. form the products in a double-buffered shared-memory ring while
-// thread 0 adds them in stored order -- the reference's sum, bit for bit.  The longest row's add
-// chain bounds the power; the short rows' sweep runs beside it instead of behind it.
-constexpr uint32_t kBwChunk = 1024;  // k_long_rows_bitwise: products per ring half (2 x 8 KB)
+// longest first, on a side stream concurrently with the power's k_mpk_sweep.  Warps 1..7 form the
+// products of a row chunk by chunk into a kBwSlots-deep shared-memory ring; thread 0 adds them in
+// stored order -- the reference's sum, bit for bit.  Producers and the adder synchronise through
+// per-slot sequence numbers in shared memory (producers: a named barrier, then one release), so
+// the producers run up to kBwSlots chunks ahead and a slow gather round never stalls the add
+// chain.  The longest row's chain of dependent adds bounds the power.
+constexpr uint32_t kBwChunk = 1024;  // products per ring slot
+constexpr uint32_t kBwSlots = 4;     // ring depth (4 x 8 KB)
 
 template <int KIND, bool SIGMA>
 __global__ void __launch_bounds__(256) k_long_rows_bitwise(const __grid_constant__ FusedParams P, uint32_t q) {
-    extern __shared__ __align__(16) double bw_ring[];  // 2 x kBwChunk products
+    extern __shared__ __align__(16) double bw_ring[];  // kBwSlots x kBwChunk products
+    __shared__ volatile uint32_t full_seq[kBwSlots];   // chunk id + 1 produced into the slot
+    __shared__ volatile uint32_t free_seq[kBwSlots];   // chunk id + 1 consumed from the slot
     const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+    const double* srcA = P.out + (uint64_t)(q - 1) * P.rows;  // A_perm-order y_{q-1}
     const uint64_t pol = l2_policy_first();
-    for (uint32_t i = blockIdx.x; i < P.n_long; i += gridDim.x) {
-        const uint32_t s = P.long_slots[i];
-        double acc = 0.0;
-        (void)long_row_dot<SIGMA, kBwChunk>(P, s, q, pol, threadIdx.x, blockDim.x, acc, bw_ring);
-        if (threadIdx.x == 0) row_epilogue<KIND, SIGMA>(P, s, SIGMA ? P.slot_row[s] : s, q, src, acc);
+    const uint32_t tid = threadIdx.x, np = blockDim.x - 32u;
+    for (uint32_t it = blockIdx.x; it < P.n_long; it += gridDim.x) {
+        if (tid < kBwSlots) full_seq[tid] = 0u, free_seq[tid] = 0u;
+        __syncthreads();
+        const uint32_t s = P.long_slots[it];
+        const uint32_t r = SIGMA ? P.slot_row[s] : s;
+        const uint32_t b = P.csr_rp[r], len = P.csr_rp[r + 1] - b;
+        const uint32_t nchunks = (len + kBwChunk - 1) / kBwChunk;
+        if (tid >= 32) {
+            // producers: chunk c into slot c % kBwSlots once the adder has released it
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                const uint32_t slot = c % kBwSlots;
+                if (c >= kBwSlots)
+                    while (free_seq[slot] < c + 1 - kBwSlots) __nanosleep(20);
+                const uint32_t base = c * kBwChunk, m = min(kBwChunk, len - base);
+                double* buf = bw_ring + slot * kBwChunk;
+                constexpr int U = 8;
+                for (uint32_t i0 = tid - 32u; i0 < m; i0 += U * np) {
+                    uint32_t col[U];
+                    double val[U], xv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const uint32_t i = i0 + u * np;
+                        col[u] = i < m ? P.csr_ci[b + base + i] : 0u;
+                        val[u] = i < m ? ld_mat_d(P.csr_v + b + base + i, pol) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) xv[u] = i0 + u * np < m ? __ldg(srcA + col[u]) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (i0 + u * np < m) buf[i0 + u * np] = __dmul_rn(val[u], xv[u]);
+                }
+                asm volatile("bar.sync 1, %0;" ::"r"(np) : "memory");  // every producer wrote chunk c
+                if (tid == 32) {
+                    __threadfence_block();
+                    full_seq[slot] = c + 1;
+                }
+            }
+        } else if (tid == 0) {
+            double acc = 0.0;
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                const uint32_t slot = c % kBwSlots;
+                while (full_seq[slot] < c + 1) {
+                }
+                __threadfence_block();
+                const uint32_t m = min(kBwChunk, len - c * kBwChunk);
+                const double2* cur = reinterpret_cast<const double2*>(bw_ring + slot * kBwChunk);
+                uint32_t i = 0;
+                // two register groups loaded alternately, no copies: the adder issues about one
+                // instruction per add besides the DADD itself (it shares its SM sub-partition with
+                // producer and sweep warps, so every extra instruction lengthens the chain)
+                double2 ga[4], gb[4];
+                if (m >= 8) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ga[j] = cur[j];
+                }
+                for (; i + 16 <= m; i += 16) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) gb[j] = cur[(i + 8) / 2 + j];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc = __dadd_rn(acc, ga[j].x);
+                        acc = __dadd_rn(acc, ga[j].y);
+                    }
+                    if (i + 24 <= m) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) ga[j] = cur[(i + 16) / 2 + j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc = __dadd_rn(acc, gb[j].x);
+                        acc = __dadd_rn(acc, gb[j].y);
+                    }
+                }
+                if (i + 8 <= m) {  // ga holds products i .. i+7
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc = __dadd_rn(acc, ga[j].x);
+                        acc = __dadd_rn(acc, ga[j].y);
+                    }
+                    i += 8;
+                }
+                const double* tail = bw_ring + slot * kBwChunk;
+                for (; i < m; ++i) acc = __dadd_rn(acc, tail[i]);
+                __threadfence_block();
+                free_seq[slot] = c + 1;
+            }
+            row_epilogue<KIND, SIGMA>(P, s, r, q, src, acc);
+        }
         __syncthreads();
     }
 }
@@ -1821,7 +1911,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
                               (const void*)k_long_rows_bitwise<1, false>, (const void*)k_long_rows_bitwise<1, true>,
                               (const void*)k_long_rows_bitwise<2, false>, (const void*)k_long_rows_bitwise<2, true>};
         for (const void* f : fns)  // once per context (device)
-            MPKG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kBwChunk * 8)));
+            MPKG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBwSlots * kBwChunk * 8)));
         MPKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
         MPKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
         MPKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
@@ -1837,13 +1927,14 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             MPKG_CUDA(cudaEventRecord(ctx->fork_ev, st));
             MPKG_CUDA(cudaStreamWaitEvent(ax, ctx->fork_ev, 0));
             const unsigned gb = (unsigned)E.long_rows;  // one CTA per long row, longest first
+            const size_t sm = kBwSlots * kBwChunk * 8;
             switch (kk) {
-                case 0: k_long_rows_bitwise<0, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
-                case 1: k_long_rows_bitwise<0, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
-                case 2: k_long_rows_bitwise<1, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
-                case 3: k_long_rows_bitwise<1, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
-                case 4: k_long_rows_bitwise<2, false><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
-                default: k_long_rows_bitwise<2, true><<<gb, 256, 2 * kBwChunk * 8, ax>>>(Pb, q); break;
+                case 0: k_long_rows_bitwise<0, false><<<gb, 256, sm, ax>>>(Pb, q); break;
+                case 1: k_long_rows_bitwise<0, true><<<gb, 256, sm, ax>>>(Pb, q); break;
+                case 2: k_long_rows_bitwise<1, false><<<gb, 256, sm, ax>>>(Pb, q); break;
+                case 3: k_long_rows_bitwise<1, true><<<gb, 256, sm, ax>>>(Pb, q); break;
+                case 4: k_long_rows_bitwise<2, false><<<gb, 256, sm, ax>>>(Pb, q); break;
+                default: k_long_rows_bitwise<2, true><<<gb, 256, sm, ax>>>(Pb, q); break;
             }
             MPKG_LAUNCH_CHECK();
             MPKG_CUDA(cudaEventRecord(ctx->join_ev, ax));

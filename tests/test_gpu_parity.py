@@ -271,6 +271,7 @@ def test_long_rows_and_length_order(ctx, oracle, order, schedule):
             n = P.n_rows
             d_x = torch.from_numpy(x).cuda()
             d_b = torch.full((5 * n,), float("nan"), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()  # torch's stream is not ordered with the context's stream
             for _ in range(2):  # capture, then replay
                 ctx.mpk_dev(plan, Ap, d_x.data_ptr(), 4, d_b.data_ptr(), n, 5)
                 ctx.synchronize()
@@ -353,6 +354,7 @@ def test_fast_mode_coop_rows_graph_and_host_paths(ctx, oracle, order):
             d_b = torch.empty((p + 1) * n, dtype=torch.float64, device="cuda")
             for _ in range(2):  # capture, then replay
                 d_b.fill_(float("nan"))
+                torch.cuda.synchronize()  # torch's stream is not ordered with the context's stream
                 ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, d_b.data_ptr(), n, p + 1)
                 ctx.synchronize()
                 assert_bitwise(d_b.view(p + 1, n).cpu().numpy(), host, "graph == host path")
@@ -391,6 +393,7 @@ def test_resident_single_launch_matches_oracle(ctx, cases, oracle, name):
             for kind in ("plain", "shifted", "poly"):
                 d_b = torch.full(((p + 1) * n,), float("nan"), dtype=torch.float64, device="cuda")
                 d_z = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                torch.cuda.synchronize()  # torch's stream is not ordered with the context's stream
                 if kind == "plain":
                     ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, d_b.data_ptr(), n, p + 1)
                 elif kind == "shifted":
