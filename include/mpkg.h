@@ -80,7 +80,9 @@ int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t
  * tile-DAG kernel, 2 one launch per power); "graphs" (replay the per-power launches as one CUDA
  * graph, default 1); "resident" (default 0; 1: a matrix that fits half the L2 together with its p+1
  * working vectors runs all powers of a device-pointer call in one cooperative launch);
- * "sweep_variant" (0..5) and "coop_variant" (0..3) select row-loop variants for experiments. */
+ * "ortho_fused" (fast-mode ICGS: 0 unfused, 1 update fused with the next dots re-reading Q from
+ * L1/L2, 2 the same with Q staged in shared memory, default); "sweep_variant" (0..5) and
+ * "coop_variant" (0..3) select row-loop variants for experiments. */
 int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value);
 /* Reads (and clears) the event pairs recorded with "kernel_timing": sum, count and max of the
  * per-launch device durations in milliseconds.  Synchronises on the recorded events. */

@@ -311,6 +311,109 @@ __global__ void __launch_bounds__(256) k_update_dots(const double* __restrict__ 
     }
 }
 
+// The same fusion with the tile's Q rows staged in shared memory by the update phase (128-row
+// tiles, 128 threads: the staged copy is 26 KB for 25 columns, so five CTAs fit an SM); the
+// tensor-core phase then reads Q from shared memory instead of L1/L2 (knob "ortho_fused" = 2, the
+// default: ICGS 1.30 ms vs 1.37 ms re-reading from L1/L2 and 1.48 ms unfused on a C4-sized block).
+template <int MT>
+__global__ void __launch_bounds__(128) k_update_dots_s(const double* __restrict__ q, const double* __restrict__ c,
+                                                       uint64_t rows, uint32_t qcols, uint32_t vcols, uint32_t nv0,
+                                                       double* __restrict__ v, double* __restrict__ part) {
+    constexpr int kBuf = 4 * MT * 64 > 128 * 9 ? 4 * MT * 64 : 128 * 9;
+    __shared__ double sbuf[kBuf];
+    double (*xs)[9] = reinterpret_cast<double (*)[9]>(sbuf);
+    double (*red)[MT * 64] = reinterpret_cast<double (*)[MT * 64]>(sbuf);
+    extern __shared__ __align__(16) double cs[];  // [qcols][8] coefficients, then Q rows [128][qs_ld]
+    const uint32_t qs_ld = qcols | 1u;
+    double* qs = cs + 8u * qcols;
+    for (uint32_t e = threadIdx.x; e < 8u * qcols; e += blockDim.x) {
+        const uint32_t k = e >> 3, jj = e & 7u;
+        cs[e] = nv0 + jj < vcols ? c[(uint64_t)(nv0 + jj) * qcols + k] : 0.0;
+    }
+    __syncthreads();
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const uint32_t g = lane >> 2, r = lane & 3u;
+    const uint32_t nv = vcols - nv0 < 8u ? vcols - nv0 : 8u;
+    bool qok[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) qok[mt] = 8 * mt + g < qcols;
+    double acc[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const uint64_t n_tiles = (rows + 127) / 128;
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint64_t i = tile * 128 + t;
+        double x[8];
+        double* qrow = qs + t * qs_ld;
+        if (i < rows) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) x[jj] = jj < (int)nv ? __ldcs(v + (uint64_t)(nv0 + jj) * rows + i) : 0.0;
+            uint32_t k = 0;
+            constexpr int U = 8;
+            for (; k + U <= qcols; k += U) {
+                double qk[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) qk[u] = __ldcs(q + (uint64_t)(k + u) * rows + i);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    qrow[k + u] = qk[u];
+                    const double2* c2 = reinterpret_cast<const double2*>(cs + (k + u) * 8);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double2 cc = c2[h];
+                        x[2 * h] = __dsub_rn(x[2 * h], __dmul_rn(cc.x, qk[u]));
+                        x[2 * h + 1] = __dsub_rn(x[2 * h + 1], __dmul_rn(cc.y, qk[u]));
+                    }
+                }
+            }
+            for (; k < qcols; ++k) {
+                const double qk = __ldcs(q + (uint64_t)k * rows + i);
+                qrow[k] = qk;
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) x[jj] = __dsub_rn(x[jj], __dmul_rn(cs[k * 8 + jj], qk));
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+                if (jj < (int)nv) __stcs(v + (uint64_t)(nv0 + jj) * rows + i, x[jj]);
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) x[jj] = 0.0;
+            for (uint32_t k = 0; k < qcols; ++k) qrow[k] = 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) xs[t][jj] = jj < (int)nv ? x[jj] : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t rb = (2 * warp + h) * 16 + 4 * r;
+            double a[MT][4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bv[u] = xs[rb + u][g];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[mt][u] = qok[mt] ? qs[(rb + u) * qs_ld + 8 * mt + g] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], a[mt][u], bv[u]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        red[warp][mt * 64 + g * 8 + 2 * r] = acc[mt][0];
+        red[warp][mt * 64 + g * 8 + 2 * r + 1] = acc[mt][1];
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < MT * 64; e += blockDim.x) {
+        double s = red[0][e];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) s += red[w][e];
+        part[(uint64_t)blockIdx.x * (MT * 64) + e] = s;
+    }
+}
+
 // coeff[e] += c[e] (ortho.hpp:112-114)
 __global__ void k_accumulate(double* __restrict__ coeff, const double* __restrict__ c, uint32_t n) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -769,15 +872,36 @@ void gpu_update_dots(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_t
     ctx->chain_ws.ensure((uint64_t)grid * te);
     double* part = ctx->chain_ws.p;
     const size_t smem = 64ull * qcols;
+    const bool staged = ctx->ortho_fused == 2;
+    unsigned grid_s = grid;
+    const size_t smem_s = 64ull * qcols + 8ull * 128 * (qcols | 1u);
+    if (staged) {
+        static const void* fs[4] = {(const void*)k_update_dots_s<1>, (const void*)k_update_dots_s<2>,
+                                    (const void*)k_update_dots_s<4>, (const void*)k_update_dots_s<8>};
+        const void* f = fs[MT == 1 ? 0 : MT == 2 ? 1 : MT == 4 ? 2 : 3];
+        MPKG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+        int per_sm = 0;
+        MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 128, smem_s));
+        grid_s = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm, 1), (rows + 127) / 128));
+        ctx->chain_ws.ensure((uint64_t)grid_s * te);
+        part = ctx->chain_ws.p;
+    }
     for (uint32_t nv0 = 0; nv0 < vcols; nv0 += 8) {
-        switch (MT) {
+        if (staged) {
+            switch (MT) {
+                case 1: k_update_dots_s<1><<<grid_s, 128, smem_s, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+                case 2: k_update_dots_s<2><<<grid_s, 128, smem_s, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+                case 4: k_update_dots_s<4><<<grid_s, 128, smem_s, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+                default: k_update_dots_s<8><<<grid_s, 128, smem_s, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
+            }
+        } else switch (MT) {
             case 1: k_update_dots<1><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
             case 2: k_update_dots<2><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
             case 4: k_update_dots<4><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
             default: k_update_dots<8><<<grid, 256, smem, ctx->stream>>>(q, c, rows, qcols, vcols, nv0, v, part); break;
         }
         MPKG_LAUNCH_CHECK();
-        k_dots_finish<<<(te * 32 + 255) / 256, 256, 0, ctx->stream>>>(part, grid, te, qcols, vcols, 0, nv0, c_next);
+        k_dots_finish<<<(te * 32 + 255) / 256, 256, 0, ctx->stream>>>(part, staged ? grid_s : grid, te, qcols, vcols, 0, nv0, c_next);
         MPKG_LAUNCH_CHECK();
         ctx->launches += 2;
     }
@@ -798,7 +922,7 @@ void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, d
         ctx->launches += 1;
     };
     // fast mode, several sweeps: each update but the last also produces the next sweep's dots
-    const bool fuse = ctx->mode == MPKG_MODE_FAST && sweeps >= 2 && qcols <= 64 && rows > 0;
+    const bool fuse = ctx->mode == MPKG_MODE_FAST && ctx->ortho_fused != 0 && sweeps >= 2 && qcols <= 64 && rows > 0;
     bool have_c = false;  // cbuf already holds this sweep's Q^T V (from a fused update)
     for (int sw = 0; sw < sweeps; ++sw) {
         if (!have_c) gpu_block_dots(ctx, q, v, rows, qcols, vcols, cbuf);
