@@ -1020,6 +1020,11 @@ def main():
                          "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms,
                          "kernel_launches_timed": k_count, "peak_source": peak_src,
                          "per_power": sweep,
+                         # the metric's DRAM bytes/nnz: measured (ncu, one step) against
+                         # the single-pass ideal and p back-to-back passes
+                         "dram_bytes_per_nnz": (traffic / nnz) if traffic else None,
+                         "dram_bytes_per_nnz_single_pass": b_alg / nnz,
+                         "dram_bytes_per_nnz_back_to_back": p * sweep["algorithmic_bytes"] / nnz,
                          "note": "achieved = single-pass B_alg (SURVEY 8d) / MPK kernel time; "
                                  "per_power = one pass over the matrix per power"},
             "cpu_baseline": cpu,
