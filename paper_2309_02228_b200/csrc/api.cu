@@ -29,13 +29,17 @@ void set_error(const char* fmt, ...) {
 std::pair<cudaEvent_t, cudaEvent_t> timing_begin(mpkg_ctx_s* ctx) {
     if (!ctx->kernel_timing) return {nullptr, nullptr};
     std::pair<cudaEvent_t, cudaEvent_t> ev;
-    if (!ctx->event_pool.empty()) {
-        ev = ctx->event_pool.back();
-        ctx->event_pool.pop_back();
-    } else {
-        MPKG_CUDA(cudaEventCreate(&ev.first));
-        MPKG_CUDA(cudaEventCreate(&ev.second));
+    if (ctx->event_pool.empty()) {
+        // grow in batches: event creation costs microseconds of host time, which launch-bound
+        // calls (C1) would otherwise pay inside the timed region
+        for (int i = 0; i < 64; ++i) {
+            MPKG_CUDA(cudaEventCreate(&ev.first));
+            MPKG_CUDA(cudaEventCreate(&ev.second));
+            ctx->event_pool.push_back(ev);
+        }
     }
+    ev = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
     MPKG_CUDA(cudaEventRecord(ev.first, ctx->stream));
     return ev;
 }
@@ -161,8 +165,8 @@ void mpk_dev(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const double* d_x, 
     use_device(ctx);
     const uint32_t n = A->n_rows;
     if (n == 0) return;
-    MPKG_CUDA(cudaMemcpyAsync(d_block, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-    FusedArgs fa;
+    FusedArgs fa;  // run_fused writes slice 0 = x (mpk.hpp:62)
+    fa.x = d_x;
     fa.kind = re ? 1 : (coef ? 2 : 0);
     fa.p = p_m;
     fa.block = d_block;

@@ -1850,6 +1850,14 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.rows = a.rows;
     P.out = a.block;
     P.z = a.z;
+    // slice 0 = x (mpk.hpp:62).  On the graph-replayed sweep path the copy is a node of the graph
+    // (one API call less per MPK on launch-bound matrices); otherwise it is issued up front.
+    bool x_pending = a.x != nullptr && a.x != a.block;
+    auto copy_x = [&]() {
+        MPKG_CUDA(cudaMemcpyAsync(a.block, a.x, sizeof(double) * A->n_rows, cudaMemcpyDeviceToDevice, st));
+        x_pending = false;
+    };
+    if (sigma && x_pending) copy_x();  // the sigma gather below reads slice 0
     if (sigma) {
         E.V.ensure((uint64_t)E.n_slots * (a.p + 1));
         P.V = E.V.p;
@@ -1991,6 +1999,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         }
     };
     const uint64_t per_power = 1 + (coop ? 1 + (E.n_multi ? 1 : 0) : (E.long_rows ? 1 : 0));
+    if (x_pending && !(sweep && !resident && ctx->graphs && a.host_block == nullptr)) copy_x();
     const auto ev = timing_begin(ctx);
     // host-pointer calls: slice q goes to the host on the copy stream once power q is written
     const bool to_host = a.host_block != nullptr;
@@ -2040,16 +2049,20 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         void* args[] = {(void*)&P, (void*)&bar};
         MPKG_CUDA(cudaLaunchCooperativeKernel(fns[kk], dim3(E.res_grid[kk]), dim3(256), args, 0, st));
     } else if (sweep) {
+        const bool graph_x = x_pending;
         auto launch_all = [&]() {
+            if (graph_x) copy_x();
             for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) power(q);
         };
         if (ctx->graphs) {
             // One CUDA graph per distinct launch set (parameters, p, kind): repeated calls with
             // the same buffers replay all p sweeps with a single launch (C1 is launch-bound).
-            std::vector<unsigned char> key(sizeof(FusedParams) + 16);
+            std::vector<unsigned char> key(sizeof(FusedParams) + 16 + sizeof(void*));
             std::memcpy(key.data(), &P, sizeof(FusedParams));
             const int32_t extra[4] = {a.kind, a.p, sigma ? 1 : 0, (int32_t)E.long_rows};
             std::memcpy(key.data() + sizeof(FusedParams), extra, sizeof(extra));
+            const void* xk = graph_x ? (const void*)a.x : nullptr;  // the captured copy's source
+            std::memcpy(key.data() + sizeof(FusedParams) + 16, &xk, sizeof(xk));
             cudaGraphExec_t exec = nullptr;
             for (auto& gr : E.graphs)
                 if (gr.first == key) exec = gr.second;
