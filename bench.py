@@ -208,7 +208,7 @@ def ref_preprocess(R, A, p, cache):
     gr, _, _, _ = R.group_levels(prp, pci, pv, lp, cache, p)
     t3 = time.perf_counter()
     return (prp, pci, pv), pm, gr, {"build_levels_s": t1 - t0, "permute_s": t2 - t1,
-                                    "group_levels_s": t3 - t2}
+                                    "group_levels_s": t3 - t2}, lp
 
 
 def time_reference_mpk(R, P, gr, p, x, kind, steps, warmup):
@@ -268,7 +268,7 @@ def run_reference(args, cfgd):
         else:
             R = Reference()
             A = make_matrix(args.config, args.seed)
-            P, perm, _, prep = ref_preprocess(R, A, p, host_llc_bytes())
+            P, perm, _, prep, _ = ref_preprocess(R, A, p, host_llc_bytes())
             x = np.empty(A.n_rows)
             x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)
             cb = port_chain_baseline(cfgd, P, x, args.steps)
@@ -284,7 +284,7 @@ def run_reference(args, cfgd):
     R = Reference()
     A = make_matrix(args.config, args.seed)
     cache = host_llc_bytes()
-    P, perm, gr, prep = ref_preprocess(R, A, p, cache)
+    P, perm, gr, prep, ref_level_ptr = ref_preprocess(R, A, p, cache)
     x = np.empty(A.n_rows)
     x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)  # permute_vector (csr.hpp:191)
     kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
@@ -293,12 +293,42 @@ def run_reference(args, cfgd):
     med = statistics.median(times)
     gf = 2.0 * nnz * p / med * 1e-9
     cores = R.resolve_threads(0)
+    # also the reference's baseline_mpk (p plain sweeps) and the blocked mpk at the
+    # CLI's default 32 MiB budget (solver.cpp:117-121); median of 3 after one warm-up each
+    extra = {}
+    if kind == "plain":  # through pre-built handles, as time_reference_mpk does
+        h = R.wrap(*P)
+        xv = R.lib.ref_vec_new(np.ascontiguousarray(x).ctypes.data, len(x))
+        blk = R.lib.ref_block_new(len(x), p + 1)
+
+        def med3(fn):
+            fn()
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                assert fn() == 0, R.lib.ref_last_error()
+                ts.append(time.perf_counter() - t0)
+            return statistics.median(ts)
+        try:
+            t_base = med3(lambda: R.lib.ref_baseline_mpk_t(h, xv, p, blk, 0))
+            extra["reference_baseline_mpk_gflops"] = 2.0 * nnz * p / t_base * 1e-9
+            if cache != (32 << 20):
+                gr32, _, _, _ = R.group_levels(*P, ref_level_ptr, 32 << 20, p)
+                g32 = np.ascontiguousarray(gr32, np.uint32)
+                plan32 = R.lib.ref_plan_new(len(x), g32.ctypes.data, len(g32) - 1, p)
+                t32 = med3(lambda: R.lib.ref_mpk_t(plan32, h, xv, p, blk, 0))
+                R.lib.ref_plan_free(plan32)
+                extra["reference_mpk_32MiB_gflops"] = 2.0 * nnz * p / t32 * 1e-9
+        finally:
+            R.lib.ref_block_free(blk)
+            R.lib.ref_vec_free(xv)
+            R.lib.ref_csr_free(h)
     line = {**base, "value": gf, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": med * 1e3, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, DESIGN.md §6)",
             "config": {"workload": cfgd["desc"], "n": A.n_rows, "nnz": nnz, "p": p,
                        "cache_bytes": cache, "threads": cores, "cpu": cpu_model(),
-                       "preprocess_s": prep},
+                       "preprocess_s": prep, **extra},
             "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
                              "sample": f"full {args.config} workload, reference blocked "
                                        f"{'mpk_shifted' if kind == 'shifted' else 'mpk'} "
