@@ -78,7 +78,8 @@ int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t
  * window bytes; 0 = L2/2), "tile_rows" (fixed 256); "kernel_timing" = 1 records a CUDA event
  * pair around every power-kernel launch on the context stream; "schedule" (0 auto, 1 fused
  * tile-DAG kernel, 2 one launch per power); "graphs" (replay the per-power launches as one CUDA
- * graph, default 1); "resident" (default 0; 1: a matrix that fits half the L2 together with its p+1
+ * graph, default 1); "pdl" (default 1: programmatic dependent launch between consecutive
+ * powers, hiding the launch gap); "resident" (default 0; 1: a matrix that fits half the L2 together with its p+1
  * working vectors runs all powers of a device-pointer call in one cooperative launch);
  * "ortho_fused" (fast-mode ICGS: 0 unfused, 1 update fused with the next dots re-reading Q from
  * L1/L2, 2 the same with Q staged in shared memory, default); "sweep_variant" (0..5) and

@@ -307,6 +307,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->graphs = value != 0;
         else if (k == "resident")
             ctx->resident = value != 0;
+        else if (k == "pdl")
+            ctx->pdl = value != 0;
         else if (k == "schedule") {
             require(value >= 0 && value <= 2, "ctx_set_param: schedule must be 0 (auto), 1 (fused) or 2 (sweeps)");
             ctx->schedule = value;

@@ -1,5 +1,6 @@
 // Internal device-side types of the mpkg library (not part of the ABI).
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -104,6 +105,7 @@ struct mpkg_ctx_s {
     int64_t threads = 0;      // fused-kernel consumer threads (0: one per tile row)
     int64_t kernel = 0;       // 0: lean (no staging), 1: TMA-staged + producer warp, 2: warp-tile, 4: async gather
     bool graphs = true;       // sweep schedule: replay the p launches as one CUDA graph
+    bool pdl = true;          // sweep schedule: programmatic dependent launch between powers
     bool resident = false;    // sweep schedule, L2-resident matrix: one cooperative launch (off:
                               // slower than the per-power graph on C1)
     int64_t sweep_variant = 0;  // sweep-kernel row loop (mpk_exec.cu launch_sweep)
@@ -193,6 +195,33 @@ namespace mpkg_detail {
 std::pair<cudaEvent_t, cudaEvent_t> timing_begin(mpkg_ctx_s* ctx);
 void timing_end(mpkg_ctx_s* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev);
 
+// Kernel launch that may start before the previous kernel on the stream finishes (programmatic
+// dependent launch): the kernel's griddepcontrol.wait holds its reads until the predecessor has
+// completed and flushed.  Hides the launch gap between back-to-back powers.
+template <typename... Ex, typename... Act>
+inline void launch_maybe_pdl(bool pdl, void (*k)(Ex...), unsigned grid, unsigned block, cudaStream_t st,
+                             Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    MPKG_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...));
+}
+
+// In a kernel launched with launch_maybe_pdl: wait for the predecessor, then let the successor
+// launch (one kernel ahead).  Both are no-ops without the launch attribute.
+#define MPKG_PDL_ENTRY()                                              \
+    do {                                                              \
+        asm volatile("griddepcontrol.wait;" ::: "memory");            \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+
 inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 32u) {
     uint64_t g = (work + block - 1) / block;
     if (g < 1) g = 1;
@@ -217,7 +246,7 @@ void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double
                       double* dst, const double* src2, double shift_a, double shift_b2);
 // the same launch without the kernel-timing events (callers that time a whole step)
 void launch_spmv_sell_raw(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
-                          double* dst, const double* src2, double shift_a, double shift_b2);
+                          double* dst, const double* src2, double a, double b2, bool pdl = false);
 
 // levels.cu
 void gpu_build_levels(mpkg_ctx_s* ctx, const mpkg_csr_s* A, mpkg_levels_s* L);

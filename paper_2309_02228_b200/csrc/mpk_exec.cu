@@ -584,6 +584,7 @@ __device__ __forceinline__ bool long_row_dot(const FusedParams& P, uint32_t s0, 
 // (the fused kernel would only add ticket and dependency overhead), see run_fused.
 template <int KIND, bool SIGMA, int V>
 __global__ void __launch_bounds__(256, V == 1 ? 5 : 0) k_mpk_sweep(const __grid_constant__ FusedParams P, uint32_t q) {
+    MPKG_PDL_ENTRY();
     const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
     double* const dst = P.V + (uint64_t)q * P.vstride;
     const uint64_t pol = l2_policy_first();
@@ -660,7 +661,11 @@ __global__ void __launch_bounds__(256) k_mpk_resident(const __grid_constant__ Fu
 // Sweep-kernel row-loop variants ("sweep_variant" knob): 0 groups of 8 (64 regs, 4 CTAs/SM),
 // 1 the same capped at 5 CTAs/SM, 2 groups of 4, 3 software-pipelined pairs.
 template <int KIND, bool SIGMA>
-void launch_sweep(int v, unsigned g, cudaStream_t st, const FusedParams& P, uint32_t q) {
+void launch_sweep(int v, unsigned g, cudaStream_t st, const FusedParams& P, uint32_t q, bool pdl = false) {
+    if (v == 0) {
+        launch_maybe_pdl(pdl, k_mpk_sweep<KIND, SIGMA, 0>, g, 256, st, P, q);
+        return;
+    }
     switch (v) {
         case 1: k_mpk_sweep<KIND, SIGMA, 1><<<g, 256, 0, st>>>(P, q); break;
         case 2: k_mpk_sweep<KIND, SIGMA, 2><<<g, 256, 0, st>>>(P, q); break;
@@ -1890,23 +1895,26 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     // One power of the sweep schedule.  A_perm order with plain or shifted powers and no long
     // rows is exactly the baseline's row kernel (k_spmv_sell, fewest instructions per row); every
     // other case runs k_mpk_sweep (private order, polynomial accumulator, long rows skipped).
+    // programmatic dependent launch between consecutive powers on the context stream; not when a
+    // side stream joins between them (the event wait must stay a full dependency)
+    const bool pdl = ctx->pdl && sweep && !coop && !bw_long;
     auto sweep_power = [&](uint32_t q) {
         const unsigned g = grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u);
         if (!sigma && a.kind <= 1 && !E.long_rows && !coop && sv == 0) {  // (bw_long implies long rows)
             const double* src = a.block + (uint64_t)(q - 1) * a.rows;
             const double* src2 = q >= 2 ? a.block + (uint64_t)(q - 2) * a.rows : src;
             launch_spmv_sell_raw(ctx, S, a.kind == 1, src, a.block + (uint64_t)q * a.rows, src2,
-                                 P.shift_a[q - 1], P.shift_b2[q - 1]);
+                                 P.shift_a[q - 1], P.shift_b2[q - 1], pdl);
             ctx->launches -= 1;  // counted with the step below
             return;
         }
         switch (a.kind * 2 + (sigma ? 1 : 0)) {
-            case 0: launch_sweep<0, false>(sv, g, st, P, q); break;
-            case 1: launch_sweep<0, true>(sv, g, st, P, q); break;
-            case 2: launch_sweep<1, false>(sv, g, st, P, q); break;
-            case 3: launch_sweep<1, true>(sv, g, st, P, q); break;
-            case 4: launch_sweep<2, false>(sv, g, st, P, q); break;
-            default: launch_sweep<2, true>(sv, g, st, P, q); break;
+            case 0: launch_sweep<0, false>(sv, g, st, P, q, pdl); break;
+            case 1: launch_sweep<0, true>(sv, g, st, P, q, pdl); break;
+            case 2: launch_sweep<1, false>(sv, g, st, P, q, pdl); break;
+            case 3: launch_sweep<1, true>(sv, g, st, P, q, pdl); break;
+            case 4: launch_sweep<2, false>(sv, g, st, P, q, pdl); break;
+            default: launch_sweep<2, true>(sv, g, st, P, q, pdl); break;
         }
     };
     // One power: the sweep, plus the rows it skips in fast mode -- k_coop_rows on the side stream

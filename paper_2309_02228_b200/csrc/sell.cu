@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell(
     const uint32_t* __restrict__ slot_row, uint32_t n_slots, uint32_t n_rows,
     const double* __restrict__ src, double* __restrict__ dst, const double* __restrict__ src2,
     double a, double b2) {
+    MPKG_PDL_ENTRY();
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t len = row_len[s];
@@ -153,18 +154,14 @@ void launch_spmv_sell(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double
 }
 
 void launch_spmv_sell_raw(mpkg_ctx_s* ctx, const Sell& S, bool shifted, const double* src,
-                          double* dst, const double* src2, double a, double b2) {
+                          double* dst, const double* src2, double a, double b2, bool pdl) {
     if (S.n_slots == 0) return;
     const unsigned grid = grid_for(S.n_slots, 256, (unsigned)ctx->sm_count * 8u);
     const uint32_t* slot_row = S.slot_row.n ? S.slot_row.p : nullptr;
-    if (!shifted)
-        k_spmv_sell<0><<<grid, 256, 0, ctx->stream>>>(S.cols.p, S.vals.p, S.chunk_off.p,
-                                                      S.row_len.p, slot_row, S.n_slots, S.n_rows,
-                                                      src, dst, src2, a, b2);
-    else
-        k_spmv_sell<1><<<grid, 256, 0, ctx->stream>>>(S.cols.p, S.vals.p, S.chunk_off.p,
-                                                      S.row_len.p, slot_row, S.n_slots, S.n_rows,
-                                                      src, dst, src2, a, b2);
+    launch_maybe_pdl(pdl, shifted ? k_spmv_sell<1> : k_spmv_sell<0>, grid, 256, ctx->stream,
+                     (const uint32_t*)S.cols.p, (const double*)S.vals.p, (const uint64_t*)S.chunk_off.p,
+                     (const uint32_t*)S.row_len.p, slot_row, (uint32_t)S.n_slots, (uint32_t)S.n_rows,
+                     src, dst, src2, a, b2);
     MPKG_LAUNCH_CHECK();
     ctx->launches += 1;
 }
