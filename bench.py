@@ -594,9 +594,8 @@ def run_ortho(args, cfgd):
         ctx.synchronize()
         torch.cuda.synchronize()
 
-    def step():
-        ctx.icgs_block_orthogonalize_dev(Q.data_ptr(), n, qc, V.data_ptr(), s, sweeps, coeff.data_ptr())
-        ctx.tsqr_dev(V.data_ptr(), n, s, Rv.data_ptr())
+    def step():  # sstep.hpp:539-545 (icgs then tsqr) through the combined entry point
+        ctx.ortho_block_dev(Q.data_ptr(), n, qc, V.data_ptr(), s, sweeps, coeff.data_ptr(), Rv.data_ptr())
 
     def timed(k, fn):
         sync()
@@ -647,7 +646,8 @@ def run_ortho(args, cfgd):
     kernel_ms = k_total / args.steps
     flops = sweeps * 4.0 * n * qc * s + 4.0 * n * s * s  # dots + update per sweep; Householder QR + form Q
     # fast-mode ICGS: the first sweep's dots read Q and V; every update (fused with the next sweep's
-    # dots but the last) reads Q and V and writes V; TSQR reads V and writes Q
+    # dots, the last one with TSQR's first factor) reads Q and V and writes V (the last one writes
+    # the reflectors); TSQR's apply reads them and writes Q
     b_alg = 8.0 * n * ((qc + s) + sweeps * (qc + 2 * s) + 2 * s)
     peak, peak_src = measured_peak()
     achieved = b_alg / (kernel_ms * 1e-3) / 1e9
@@ -662,15 +662,14 @@ def run_ortho(args, cfgd):
     for _ in range(max(3, min(args.steps, 10))):
         hV.copy_(V0.cpu())
         t0 = time.perf_counter()
-        check(lib.mpkg_icgs_block_orthogonalize(ctx.h, hQ.data_ptr(), n, qc, hV.data_ptr(), s, sweeps,
-                                                hc.ctypes.data))
-        check(lib.mpkg_tsqr(ctx.h, hV.data_ptr(), n, s, hr.ctypes.data))
+        check(lib.mpkg_ortho_block(ctx.h, hQ.data_ptr(), n, qc, hV.data_ptr(), s, sweeps, hc.ctypes.data,
+                                   hr.ctypes.data))
         e_ts.append((time.perf_counter() - t0) * 1e3)
     e_ms = statistics.median(e_ts)
     e2e = {"value": flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
-           "h2d_bytes_per_step": 8 * n * (qc + s) * 2,  # icgs + tsqr calls each stage their inputs
-           "d2h_bytes_per_step": 8 * n * s * 2 + 8 * (s * qc + s * s), "ms_per_step": e_ms,
-           "note": "two host-pointer calls (icgs, tsqr), wall clock"}
+           "h2d_bytes_per_step": 8 * n * (qc + s),
+           "d2h_bytes_per_step": 8 * n * s + 8 * (s * qc + s * s), "ms_per_step": e_ms,
+           "note": "one host-pointer call (mpkg_ortho_block), wall clock"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = port_ortho_baseline(cfgd, n, args.seed, args.steps)

@@ -354,6 +354,14 @@ int mpkg_icgs_block_orthogonalize_dev(mpkg_ctx_t ctx, const double* d_q, uint64_
  * MPKG_EINVAL if rows < cols or cols > 64; cols == 0 returns at once. */
 int mpkg_tsqr(mpkg_ctx_t ctx, double* v, uint64_t rows, uint32_t cols, double* r);
 int mpkg_tsqr_dev(mpkg_ctx_t ctx, double* d_v, uint64_t rows, uint32_t cols, double* d_r);
+/* sstep.hpp:539-545: icgs_block_orthogonalize(q, ..., v, ..., sweeps) then tsqr(v, ..., r) in one
+ * call; for s-step blocks (vcols <= 8, qcols <= 64) ICGS's last update runs inside TSQR's first
+ * factor kernel and the updated block is never stored.  Every output is bit-identical to the two
+ * calls in sequence.  Same arguments and errors as those two. */
+int mpkg_ortho_block(mpkg_ctx_t ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+                     int sweeps, double* coeff, double* r);
+int mpkg_ortho_block_dev(mpkg_ctx_t ctx, const double* d_q, uint64_t rows, uint32_t qcols, double* d_v,
+                         uint32_t vcols, int sweeps, double* d_coeff, double* d_r);
 
 /* ---- host-side matrix generators (harness inputs; generators.hpp + SURVEY §7 step 1) ------- */
 /* kinds: 1 poisson1d(a) 2 poisson2d(a,b) 3 poisson3d(a,b,c) [generators.hpp:35-89]

@@ -829,6 +829,18 @@ inline void tsqr(double* v, std::size_t rows, std::size_t cols, double* r,
     detail::check(mpkg_tsqr(device_context(), v, rows, static_cast<std::uint32_t>(cols), r));
 }
 
+// sstep.hpp:539-545 in one call (extension): icgs_block_orthogonalize(q, rows, qcols, v, vcols,
+// sweeps) then tsqr(v, rows, vcols, r); returns the ICGS coefficients.  Bit-identical to the two
+// calls; for s-step blocks the last update is fused into the TSQR factor and never stored.
+inline std::vector<double> ortho_block(const double* q, std::size_t rows, std::size_t qcols, double* v,
+                                       std::size_t vcols, int sweeps, double* r, int threads = 0) {
+    (void)threads;
+    std::vector<double> coeff(qcols * vcols, 0.0);
+    detail::check(mpkg_ortho_block(device_context(), q, rows, static_cast<std::uint32_t>(qcols), v,
+                                   static_cast<std::uint32_t>(vcols), sweeps, coeff.data(), r));
+    return coeff;
+}
+
 // ortho.hpp:231-240
 inline bool tsqr_rank_deficient(const double* r, std::size_t cols, double threshold) {
     for (std::size_t j = 0; j < cols; ++j)

@@ -90,6 +90,8 @@ _SIGS = {
     "mpkg_icgs_block_orthogonalize_dev": [P, P, u64, u32, P, u32, i32, P],
     "mpkg_tsqr": [P, P, u64, u32, P],
     "mpkg_tsqr_dev": [P, P, u64, u32, P],
+    "mpkg_ortho_block": [P, P, u64, u32, P, u32, i32, P, P],
+    "mpkg_ortho_block_dev": [P, P, u64, u32, P, u32, i32, P, P],
     "mpkg_sstep_gs2_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],

@@ -735,6 +735,23 @@ class Context:
         check(lib.mpkg_tsqr(self.h, _ptr(out), rows, cols, _ptr(r)))
         return out, r.T.copy()
 
+    def ortho_block(self, q, v, sweeps: int):
+        """sstep.hpp:539-545: icgs_block_orthogonalize then tsqr in one call -> (Q as a (cols, rows)
+        block, coefficients (qcols, vcols), R (cols, cols)); bit-identical to the two calls."""
+        out = np.array(_block(v), order="C")
+        q = _block(q) if q is not None and np.size(q) else np.zeros((0, out.shape[1]))
+        _same_rows(q, out)
+        cols, rows = out.shape
+        coeff = np.zeros((cols, q.shape[0]))
+        r = np.zeros((cols, cols))
+        check(lib.mpkg_ortho_block(self.h, _ptr(q) if q.size else None, rows, q.shape[0], _ptr(out), cols,
+                                   int(sweeps), _ptr(coeff), _ptr(r)))
+        return out, coeff.T.copy(), r.T.copy()
+
+    def ortho_block_dev(self, d_q: int, rows: int, qcols: int, d_v: int, vcols: int, sweeps: int,
+                        d_coeff: int, d_r: int):
+        check(lib.mpkg_ortho_block_dev(self.h, d_q, rows, qcols, d_v, vcols, sweeps, d_coeff, d_r))
+
     def block_dots_dev(self, d_q: int, d_v: int, rows: int, qcols: int, vcols: int, d_c: int):
         check(lib.mpkg_block_dots_dev(self.h, d_q, d_v, rows, qcols, vcols, d_c))
 

@@ -1528,4 +1528,32 @@ int mpkg_tsqr(mpkg_ctx_t ctx, double* v, uint64_t rows, uint32_t cols, double* r
     });
 }
 
+int mpkg_ortho_block_dev(mpkg_ctx_t ctx, const double* d_q, uint64_t rows, uint32_t qcols, double* d_v,
+                         uint32_t vcols, int sweeps, double* d_coeff, double* d_r) {
+    return guarded([&] {
+        icgs_check(ctx, d_q, d_v, rows, qcols, vcols, sweeps, d_coeff);
+        tsqr_check(ctx, d_v, rows, vcols, d_r);
+        if (!vcols) return;
+        use_device(ctx);
+        gpu_ortho_block(ctx, d_q, rows, qcols, d_v, vcols, sweeps, d_coeff, d_r);
+    });
+}
+
+int mpkg_ortho_block(mpkg_ctx_t ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+                     int sweeps, double* coeff, double* r) {
+    return guarded([&] {
+        icgs_check(ctx, q, v, rows, qcols, vcols, sweeps, coeff);
+        tsqr_check(ctx, v, rows, vcols, r);
+        if (!vcols) return;
+        use_device(ctx);
+        HostBlock dq(ctx, qcols ? q : nullptr, rows * qcols), dv(ctx, v, rows * vcols),
+            dc(ctx, nullptr, (uint64_t)qcols * vcols), dr(ctx, nullptr, (uint64_t)vcols * vcols);
+        gpu_ortho_block(ctx, dq.d.p, rows, qcols, dv.d.p, vcols, sweeps, dc.d.p, dr.d.p);
+        dv.back(ctx, v, rows * vcols);
+        if (qcols) dc.back(ctx, coeff, (uint64_t)qcols * vcols);
+        dr.back(ctx, r, (uint64_t)vcols * vcols);
+        MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 }  // extern "C"

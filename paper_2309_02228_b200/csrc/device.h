@@ -313,8 +313,11 @@ void gpu_block_dots(mpkg_ctx_s* ctx, const double* q, const double* v, uint64_t 
 void gpu_block_update(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_t rows, uint32_t qcols,
                       uint32_t vcols, double* v);
 void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
-              int sweeps, double* coeff);
-void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r);
+              int sweeps, double* coeff, const double** last_c = nullptr);
+void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r, const double* upd_q = nullptr,
+              const double* upd_coef = nullptr, uint32_t upd_qcols = 0);
+void gpu_ortho_block(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+                     int sweeps, double* coeff, double* r);
 constexpr uint32_t kTsqrMaxCols = 64;
 
 }  // namespace mpkg_detail

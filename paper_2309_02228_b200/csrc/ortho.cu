@@ -589,22 +589,80 @@ __device__ __forceinline__ void warp_sum8(double (&v)[8]) {
 // reflectors over the panel in place (LAPACK layout: v below the diagonal, R on and above) and
 // the compact-WY factor T (8 x 8 upper triangular, row-major, H_0 ... H_{c-1} = I - V T V^T) to
 // `tmat` (64 doubles per panel), followed by the panel's V_top (64 doubles).
+// UPD: the panel is ICGS's last update V - Q C computed on the fly (ascending k, mul then sub:
+// block_update's arithmetic, bit for bit) instead of read -- the updated block is never written
+// (TSQR overwrites it anyway), which saves a write and a read of V (mpkg_ortho_block).
+template <bool UPD>
 __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uint64_t lda, uint64_t rows,
                                                      uint32_t np, uint32_t c, double* __restrict__ rstack,
-                                                     double* __restrict__ tmat) {
+                                                     double* __restrict__ tmat, const double* __restrict__ q,
+                                                     const double* __restrict__ coef, uint32_t qcols) {
+    extern __shared__ __align__(16) double cs[];  // UPD: [qcols][8] coefficients
+    if constexpr (UPD) {
+        for (uint32_t e = threadIdx.x; e < 8u * qcols; e += blockDim.x) {
+            const uint32_t kk = e >> 3, jj = e & 7u;
+            cs[e] = jj < c ? coef[(uint64_t)jj * qcols + kk] : 0.0;
+        }
+        __syncthreads();
+    }
     const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31u;
     if (k >= np) return;  // warp-uniform
     const uint64_t b0 = panel_bound(rows, np, k), b1 = panel_bound(rows, np, k + 1);
     const uint32_t P = (uint32_t)(b1 - b0);
     double A[kTqR][kTqC];
+    if constexpr (UPD) {
+        // A = V - Q C, k outermost: each step loads the lane's 8 rows of Q column k (and k+1) at once
 #pragma unroll
-    for (int l = 0; l < kTqC; ++l)
+        for (int l = 0; l < kTqC; ++l)
 #pragma unroll
-        for (int r = 0; r < kTqR; ++r) {
-            const uint32_t i = lane + 32u * r;
-            A[r][l] = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
+            for (int r = 0; r < kTqR; ++r) {
+                const uint32_t i = lane + 32u * r;
+                A[r][l] = ((uint32_t)l < c && i < P) ? __ldcs(a + (uint64_t)l * lda + b0 + i) : 0.0;
+            }
+        uint32_t kk = 0;
+        for (; kk + 2 <= qcols; kk += 2) {
+            double qv[2][kTqR];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int r = 0; r < kTqR; ++r) {
+                    const uint32_t i = lane + 32u * r;
+                    qv[u][r] = i < P ? __ldcs(q + (uint64_t)(kk + u) * lda + b0 + i) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int l = 0; l < kTqC; ++l) {
+                    const double cl = cs[(kk + u) * 8 + l];
+#pragma unroll
+                    for (int r = 0; r < kTqR; ++r) A[r][l] = __dsub_rn(A[r][l], __dmul_rn(cl, qv[u][r]));
+                }
         }
+        for (; kk < qcols; ++kk) {
+            double qv[kTqR];
+#pragma unroll
+            for (int r = 0; r < kTqR; ++r) {
+                const uint32_t i = lane + 32u * r;
+                qv[r] = i < P ? __ldcs(q + (uint64_t)kk * lda + b0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int l = 0; l < kTqC; ++l) {
+                const double cl = cs[kk * 8 + l];
+#pragma unroll
+                for (int r = 0; r < kTqR; ++r) A[r][l] = __dsub_rn(A[r][l], __dmul_rn(cl, qv[r]));
+            }
+        }
+        // rows past the panel and columns past c are exact zeros (0 - c * 0, and c = 0 for l >= c)
+    } else {
+#pragma unroll
+        for (int l = 0; l < kTqC; ++l)
+#pragma unroll
+            for (int r = 0; r < kTqR; ++r) {
+                const uint32_t i = lane + 32u * r;
+                A[r][l] = ((uint32_t)l < c && i < P) ? a[(uint64_t)l * lda + b0 + i] : 0.0;
+            }
+    }
     // Lane i < 8 builds row i of T column by column (dlarft, forward, columnwise):
     // T_jj = tau_j, T_{0:j,j} = -tau_j T_{0:j,0:j} (V_{:,0:j}^T v_j).  The Gram entries v_m . v_j
     // (m < j) ride in the free slots of step j's 8-wide reduction (slots l > j carry w_l).
@@ -909,7 +967,7 @@ void gpu_update_dots(mpkg_ctx_s* ctx, const double* q, const double* c, uint64_t
 }
 
 void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
-              int sweeps, double* coeff) {
+              int sweeps, double* coeff, const double** last_c) {
     const uint32_t ne = qcols * vcols;
     if (!ne) return;
     MPKG_CUDA(cudaMemsetAsync(coeff, 0, 8ull * ne, ctx->stream));
@@ -933,16 +991,37 @@ void gpu_icgs(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, d
             have_c = true;
             continue;
         }
-        gpu_block_update(ctx, q, cbuf, rows, qcols, vcols, v);
         accumulate(cbuf);
+        if (last_c && sw + 1 == sweeps) {  // the caller applies the last update (mpkg_ortho_block)
+            *last_c = cbuf;
+            return;
+        }
+        gpu_block_update(ctx, q, cbuf, rows, qcols, vcols, v);
         have_c = false;
     }
+}
+
+// sstep.hpp:539-545: ICGS against the basis, then TSQR of the block.  For s-step blocks (c <= 8,
+// q <= 64) the last ICGS update runs inside TSQR's level-0 factor kernel; every result is
+// bit-identical to the two calls in sequence.
+void gpu_ortho_block(mpkg_ctx_s* ctx, const double* q, uint64_t rows, uint32_t qcols, double* v, uint32_t vcols,
+                     int sweeps, double* coeff, double* r) {
+    if (qcols == 0 || vcols == 0 || vcols > (uint32_t)kTqC || qcols > 64 || rows < vcols ||
+        (rows + kTqPanel - 1) / kTqPanel <= 1) {
+        if (qcols) gpu_icgs(ctx, q, rows, qcols, v, vcols, sweeps, coeff);
+        gpu_tsqr(ctx, v, rows, vcols, r);
+        return;
+    }
+    const double* last_c = nullptr;
+    gpu_icgs(ctx, q, rows, qcols, v, vcols, sweeps, coeff, &last_c);
+    gpu_tsqr(ctx, v, rows, vcols, r, q, last_c, qcols);
 }
 
 // Panel rows per level: shared memory holds two P x c panels in k_panel_formq.
 uint32_t tsqr_panel_rows(uint32_t c) { return std::max<uint32_t>(4096u / c, 2u * c); }
 
-void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) {
+void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r, const double* upd_q,
+              const double* upd_coef, uint32_t upd_qcols) {
     if (!c) return;
     // c <= 8 (s-step blocks): warp-per-panel register kernels on 64-row panels; wider blocks: the
     // shared-memory CTA-per-panel kernels
@@ -988,8 +1067,13 @@ void gpu_tsqr(mpkg_ctx_s* ctx, double* v, uint64_t rows, uint32_t c, double* r) 
     const auto ev = timing_begin(ctx);
     if (narrow) {
         for (const Level& l : lv) {
-            k_tsqr_factor<<<(l.np * 32u + 127u) / 128u, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c,
-                                                                            l.rstack, l.taus);
+            const unsigned g = (l.np * 32u + 127u) / 128u;
+            if (upd_q && &l == &lv.front())  // level 0 of mpkg_ortho_block: ICGS's last update fused in
+                k_tsqr_factor<true><<<g, 128, 64ull * upd_qcols, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c, l.rstack,
+                                                                             l.taus, upd_q, upd_coef, upd_qcols);
+            else
+                k_tsqr_factor<false><<<g, 128, 0, ctx->stream>>>(l.a, l.lda, l.rows, l.np, c, l.rstack, l.taus,
+                                                              nullptr, nullptr, 0);
             MPKG_LAUNCH_CHECK();
         }
         k_sign_fix<<<1, 256, 0, ctx->stream>>>(lv.back().rstack, c, r, mtop);

@@ -228,3 +228,20 @@ def test_device_pointer_variants_and_full_size_block(ctx):
     assert (V @ V.T - torch.eye(s, device=dev, dtype=torch.float64)).abs().max().item() <= 1e-13
     assert (Rm.T @ V - Vin).abs().max().item() <= 1e-13 * Vin.abs().max().item()
     assert bool((torch.diag(Rm) >= 0).all())
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("rows,qcols,vcols,sweeps", [(200_003, 25, 8, 2), (50_000, 9, 5, 3), (70_000, 64, 8, 2),
+                                                     (1000, 3, 2, 1), (300, 4, 8, 2), (90_000, 70, 4, 2)])
+def test_ortho_block_equals_icgs_then_tsqr(ctx, oracle, mode, rows, qcols, vcols, sweeps):
+    """mpkg_ortho_block (ICGS's last update fused into TSQR's first factor kernel) returns exactly
+    what icgs_block_orthogonalize followed by tsqr returns, in both modes."""
+    q, _ = oracle.tsqr(random_block(rows, qcols, 41))
+    v = random_block(rows, vcols, 42)
+    with _mode(ctx, mode):
+        v1, c1 = ctx.icgs_block_orthogonalize(q, v, sweeps)
+        q1, r1 = ctx.tsqr(v1)
+        q2, c2, r2 = ctx.ortho_block(q, v, sweeps)
+    assert_bitwise(c2, c1, "coefficients")
+    assert_bitwise(q2, q1, "Q")
+    assert_bitwise(r2, r1, "R")
