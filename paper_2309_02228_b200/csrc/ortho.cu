@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uin
     const uint32_t P = (uint32_t)(b1 - b0);
     double A[kTqR][kTqC];
     if constexpr (UPD) {
-        // A = V - Q C, k outermost: each step loads the lane's 8 rows of Q column k (and k+1) at once
+        // A = V - Q C, k outermost: each step loads the lane's 8 rows of KU Q columns at once
 #pragma unroll
         for (int l = 0; l < kTqC; ++l)
 #pragma unroll
@@ -621,17 +621,18 @@ __global__ void __launch_bounds__(128) k_tsqr_factor(double* __restrict__ a, uin
                 A[r][l] = ((uint32_t)l < c && i < P) ? __ldcs(a + (uint64_t)l * lda + b0 + i) : 0.0;
             }
         uint32_t kk = 0;
-        for (; kk + 2 <= qcols; kk += 2) {
-            double qv[2][kTqR];
+        constexpr int KU = 4;  // Q columns per step: 32 loads in flight per lane
+        for (; kk + KU <= qcols; kk += KU) {
+            double qv[KU][kTqR];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < KU; ++u)
 #pragma unroll
                 for (int r = 0; r < kTqR; ++r) {
                     const uint32_t i = lane + 32u * r;
                     qv[u][r] = i < P ? __ldcs(q + (uint64_t)(kk + u) * lda + b0 + i) : 0.0;
                 }
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < KU; ++u)
 #pragma unroll
                 for (int l = 0; l < kTqC; ++l) {
                     const double cl = cs[(kk + u) * 8 + l];
