@@ -764,6 +764,17 @@ static void test_ortho() {
             EXPECT(bitwise_equal(v1, v) && bitwise_equal(c1, c));
         }
     }
+    {  // s-step block step (sstep.hpp:539-545): ortho_block == icgs_block_orthogonalize then tsqr
+        const std::size_t rows = 100000, qcols = 25, vcols = 8;
+        std::vector<double> q = random_vector(rows * qcols, 51), rq(qcols * qcols);
+        mpk::tsqr(q.data(), rows, qcols, rq.data());
+        const std::vector<double> v_in = random_vector(rows * vcols, 53);
+        std::vector<double> v1 = v_in, r1(vcols * vcols), v2 = v_in, r2(vcols * vcols);
+        auto c1 = mpk::icgs_block_orthogonalize(q.data(), rows, qcols, v1.data(), vcols, 2);
+        mpk::tsqr(v1.data(), rows, vcols, r1.data());
+        auto c2 = mpk::ortho_block(q.data(), rows, qcols, v2.data(), vcols, 2, r2.data());
+        EXPECT(bitwise_equal(c1, c2) && bitwise_equal(v1, v2) && bitwise_equal(r1, r2));
+    }
     {  // Icgs.RejectsNonPositiveSweeps / EmptyBasisReturnsEmptyCoefficients
         std::vector<double> q(8, 0.0), v(8, 1.0);
         EXPECT_THROW(mpk::icgs_block_orthogonalize(q.data(), 8, 1, v.data(), 1, 0), std::invalid_argument);
