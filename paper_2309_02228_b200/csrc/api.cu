@@ -165,22 +165,34 @@ void mpk_dev(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const double* d_x, 
     use_device(ctx);
     const uint32_t n = A->n_rows;
     if (n == 0) return;
-    FusedArgs fa;  // run_fused writes slice 0 = x (mpk.hpp:62)
-    fa.x = d_x;
-    fa.kind = re ? 1 : (coef ? 2 : 0);
-    fa.p = p_m;
-    fa.block = d_block;
-    fa.rows = rows;
     std::vector<double> a, b2;
-    if (re) {
-        shift_coeffs(re, im, p_m, a, b2);
-        fa.shift_a = a.data();
-        fa.shift_b2 = b2.data();
+    if (re) shift_coeffs(re, im, p_m, a, b2);
+    // The executor runs at most kFusedSegment powers per call (its launch parameters carry the
+    // per-power shifts); longer chains run segment by segment, each starting from the last slice of
+    // the previous one -- the same arithmetic, so the same bits.  A segment never starts on the
+    // second member of a conjugate pair (its epilogue reads slice q-2).  mpk_poly keeps d <= 32.
+    constexpr int kFusedSegment = 32;
+    require(!coef || p_m <= kFusedSegment, std::string(who) + ": polynomial degree above 32");
+    int done = 0;
+    while (done < p_m) {
+        int len = std::min(kFusedSegment, p_m - done);
+        if (re && done + len < p_m && b2[done + len] != 0.0) --len;
+        FusedArgs fa;  // run_fused writes slice 0 = x (mpk.hpp:62) on the first segment
+        fa.x = done == 0 ? d_x : d_block + (uint64_t)done * rows;
+        fa.kind = re ? 1 : (coef ? 2 : 0);
+        fa.p = len;
+        fa.block = d_block + (uint64_t)done * rows;
+        fa.rows = rows;
+        if (re) {
+            fa.shift_a = a.data() + done;
+            fa.shift_b2 = b2.data() + done;
+        }
+        fa.coef = coef;
+        fa.z = d_z;
+        fa.host_block = host_block ? host_block + (uint64_t)done * rows : nullptr;
+        run_fused(ctx, P, A, fa);
+        done += len;
     }
-    fa.coef = coef;
-    fa.z = d_z;
-    fa.host_block = host_block;
-    run_fused(ctx, P, A, fa);
 }
 
 }  // namespace

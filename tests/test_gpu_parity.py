@@ -412,6 +412,34 @@ def test_resident_single_launch_matches_oracle(ctx, cases, oracle, name):
         set_knobs(ctx, {})
 
 
+@pytest.mark.parametrize("name", ["poisson3d_32", "stencil27_scrambled_20"])
+def test_long_chains_run_in_segments(ctx, cases, oracle, name):
+    """p above the executor's 32 powers per call runs segment by segment (each from the previous
+    segment's last slice): plain and shifted bases of 45 powers, with a conjugate pair straddling
+    the segment boundary, are bit-identical to the oracle on the host- and device-pointer paths."""
+    import torch
+    c = cases[name]
+    P = c["P"]
+    Ap = ctx.csr(P)
+    ls = ctx.levels_from_host(c["levels"], c["perm"], c["inv_perm"], c["level_ptr"])
+    n, p = P.n_rows, 45
+    x = mpkg.random_vector(n, 13)
+    plan = ctx.group_levels(ls, Ap, 8 << 20, p)
+    # values grow like 12^45 (finite in fp64); the bits must match the oracle's arithmetic
+    ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, p)
+    assert_bitwise(ctx.mpk(plan, Ap, x, p).as_matrix(), ref, "plain host path")
+    d_x = torch.from_numpy(x).cuda()
+    d_b = torch.full(((p + 1) * n,), float("nan"), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.mpk_dev(plan, Ap, d_x.data_ptr(), p, d_b.data_ptr(), n, p + 1)
+    ctx.synchronize()
+    assert_bitwise(d_b.view(p + 1, n).cpu().numpy(), ref, "plain device path")
+    sh = [4.0 + 0.1 * k for k in range(31)] + [3.0 + 0.5j, 3.0 - 0.5j] + [2.0 + 0.05 * k for k in range(12)]
+    assert len(sh) == p and sh[31].imag > 0  # the pair occupies powers 32 and 33
+    ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+    assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, "shifted, pair across the boundary")
+
+
 def test_fused_repeatable_and_plan_reuse(ctx, cases):
     c = cases["stencil27_scrambled_20"]
     Ap = ctx.csr(c["P"])
