@@ -311,6 +311,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             require(value >= 0 && value <= 2, "ctx_set_param: ortho_fused must be 0..2");
             ctx->ortho_fused = value;
         }
+        else if (k == "coop_min") {
+            require(value >= 0 && value <= 1024, "ctx_set_param: coop_min must be 0..1024");
+            ctx->coop_min = value;
+        }
         else if (k == "coop_variant") {
             require(value >= 0 && value <= 3, "ctx_set_param: coop_variant must be 0..3");
             ctx->coop_variant = value;

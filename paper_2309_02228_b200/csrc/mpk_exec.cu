@@ -51,7 +51,7 @@ constexpr uint32_t kMaxBufBytes = 96 * 1024;
 constexpr uint32_t kLongCap = 1024;    // rows longer than this take the CTA-cooperative path
 constexpr uint32_t kSB = 64;           // tiles per completion-counter superblock
 constexpr uint32_t kLongChunk = 1024;  // products per chunk of a long row (x2 smem ring)
-constexpr uint32_t kMedCap = 64;       // fast-mode sweeps: rows longer than this go to k_coop_rows
+constexpr uint32_t kMedCap = 128;      // fast-mode sweeps: rows longer than this go to k_coop_rows (C3: 128 > 96 > 64 > 256)
 constexpr uint32_t kCoopSeg = 2048;    // entries per k_coop_rows work item (longer rows are split)
 constexpr uint32_t kLeanRingBytes = 2 * kLongChunk * sizeof(double);
 #ifndef MPKG_GROUP
@@ -114,6 +114,7 @@ struct Executor {
     // fast-mode cooperative rows (build_coop): work items {slot, k0, k1, part or ~0u}, rows split
     // over several items {slot, first part, parts, 0}, and the per-item partial sums
     bool coop_ready = false;
+    uint32_t coop_min = kMedCap;  // rows longer than this are cooperative (knob coop_min)
     DevBuf<uint32_t> long_sorted;  // long slots, longest row first (k_long_rows_bitwise)
     DevBuf<uint32_t> res_bar;    // k_mpk_resident grid barrier {arrivals, generation}
     int res_grid[6] = {0, 0, 0, 0, 0, 0};  // cooperative grid per (kind, sigma)
@@ -1736,6 +1737,7 @@ void launch_kind(bool sigma, const Executor& E, uint32_t smem, cudaStream_t st,
 // longest first so the tail of the side-stream launch is short.
 void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
     E.coop_ready = true;
+    E.coop_min = ctx->coop_min > 0 ? (uint32_t)ctx->coop_min : kMedCap;
     const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
     const bool sigma = E.order >= 1;
@@ -1750,7 +1752,7 @@ void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
     std::vector<std::pair<uint32_t, uint32_t>> rows;  // (length, slot)
     for (uint32_t sl = 0; sl < (uint32_t)rl.size(); ++sl) {
         const uint32_t r = sigma ? sr[sl] : sl;
-        if (r < A->n_rows && rl[sl] > kMedCap) rows.emplace_back(rl[sl], sl);
+        if (r < A->n_rows && rl[sl] > E.coop_min) rows.emplace_back(rl[sl], sl);
     }
     std::stable_sort(rows.begin(), rows.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
     std::vector<uint4> items, multi;
@@ -1831,10 +1833,12 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.n_long = (uint32_t)E.long_rows;
     // fast-mode sweeps over a matrix with rows longer than kMedCap: those rows (long ones
     // included) run in k_coop_rows on a side stream, concurrently with each power's sweep
-    if (sweep && ctx->mode == MPKG_MODE_FAST && !E.coop_ready) build_coop(ctx, E, A);
+    if (sweep && ctx->mode == MPKG_MODE_FAST &&
+        (!E.coop_ready || E.coop_min != (ctx->coop_min > 0 ? (uint32_t)ctx->coop_min : kMedCap)))
+        build_coop(ctx, E, A);
     const bool coop = sweep && ctx->mode == MPKG_MODE_FAST && E.n_coop > 0;
     const bool bw_long = sweep && ctx->mode != MPKG_MODE_FAST && E.long_rows > 0;
-    P.sweep_cap = coop ? kMedCap : E.long_cap;
+    P.sweep_cap = coop ? E.coop_min : E.long_cap;
     // matrix + the p+1 working vectors within half the L2: one cooperative launch (k_mpk_resident)
     const uint64_t res_bytes = 12ull * A->nnz + 4ull * (A->n_rows + 1) + 8ull * E.n_slots * (a.p + 1);
     const bool resident = sweep && ctx->resident && !coop && !E.long_rows && a.host_block == nullptr &&

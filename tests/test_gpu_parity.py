@@ -331,7 +331,7 @@ def test_fast_mode_long_rows_within_tolerance(ctx, oracle, schedule):
 
 @pytest.mark.parametrize("order", [-1, 0])
 def test_fast_mode_coop_rows_graph_and_host_paths(ctx, oracle, order):
-    """Fast-mode sweeps send rows longer than 64 entries to k_coop_rows on a side stream (hub rows
+    """Fast-mode sweeps send rows longer than 128 entries to k_coop_rows on a side stream (hub rows
     split into 2048-entry items, partials added in order by k_coop_finish).  The device-pointer
     call (CUDA-graph replay) and the host-pointer call (eager, streamed copies) agree bit for bit,
     repeat bit for bit, and stay within 1e-12 of the oracle; A_perm order (order=0) too."""
