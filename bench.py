@@ -528,7 +528,7 @@ def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist,
             "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
             "config": {"workload": cfgd["desc"], "n": n, "nnz": nnz, "p": p,
                        "parallelism": f"level-range shards x{world}, p-deep ghost levels, "
-                                      "one NCCL halo exchange of x per step",
+                                      f"one {dist.get_backend().upper()} halo exchange of x per step",
                        "l2": "inputs larger than L2" if 12 * nnz > info["l2_bytes"] else "fits L2",
                        "mode": "bitwise", "rank0_shard": {"own_rows": [o0, o1],
                                                          "local_rows": list(hp.local_rows),
