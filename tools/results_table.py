@@ -12,8 +12,8 @@ ROWS = [("c1", "C1 64³ 7-pt, p=4"), ("c2", "**C2 160³ 27-pt scrambled, p=8** (
 
 
 def main():
-    print("| config | GF/s | step ms | roofline frac | per-power HBM frac | e2e GF/s | CPU baseline GF/s (kind, cores) | parity | clocks |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("| config | GF/s | step ms | roofline frac | per-power HBM frac | DRAM B/nnz: ncu / single pass / p passes | e2e GF/s | CPU baseline GF/s (kind, cores) | parity | clocks |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for key, name in ROWS:
         f = ROOT / "profiles" / "r01" / f"bench_{key}.json"
         if not f.exists():
@@ -32,7 +32,9 @@ def main():
         print(f"| {name} | {d['value']:.1f} | {d['ms_per_step']:.3f} | {r.get('frac', 0):.3f} | "
               f"{pp:.2f} |" if pp is not None else f"| {name} | {d['value']:.1f} | {d['ms_per_step']:.3f} | "
               f"{r.get('frac', 0):.3f} | — |", end="")
-        print(f" {e.get('value', 0):.1f} | {c.get('value', 0):.2f} ({c.get('kind')}, {c.get('cores')}) | {par} | "
+        bn = [r.get("dram_bytes_per_nnz"), r.get("dram_bytes_per_nnz_single_pass"), r.get("dram_bytes_per_nnz_back_to_back")]
+        bcell = " / ".join(f"{v:.1f}" if v else "—" for v in bn) if any(bn) else "—"
+        print(f" {bcell} | {e.get('value', 0):.1f} | {c.get('value', 0):.2f} ({c.get('kind')}, {c.get('cores')}) | {par} | "
               f"{cl.get('sm_mhz')} MHz {','.join(cl.get('reasons') or []) or ''} |")
 
 
