@@ -111,13 +111,28 @@ def measured_peak():
 
 
 def host_llc_bytes():
+    """Host last-level cache for the reference's blocking budget: sysconf (acceptance.cpp:691), then
+    sysfs when sysconf reports 0; the CLI's 32 MiB default (solver.cpp:117-121) only if both fail.
+    Returns (bytes, source)."""
     try:
-        v = os.sysconf("SC_LEVEL3_CACHE_SIZE")  # acceptance.cpp:691
+        v = os.sysconf("SC_LEVEL3_CACHE_SIZE")
         if v and v > 0:
-            return int(v)
+            return int(v), "sysconf(_SC_LEVEL3_CACHE_SIZE)"
     except (ValueError, OSError):
         pass
-    return 32 << 20  # solver.cpp:117-121 CLI default
+    best = 0
+    for idx in pathlib.Path("/sys/devices/system/cpu/cpu0/cache").glob("index*"):
+        try:
+            if (idx / "level").read_text().strip() != "3":
+                continue
+            s = (idx / "size").read_text().strip().upper()
+            mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}.get(s[-1], 1)
+            best = max(best, int(s.rstrip("KMG")) * mult)
+        except (OSError, ValueError):
+            continue
+    if best:
+        return best, "sysfs cpu0/cache/index*/size (level 3)"
+    return 32 << 20, "CLI default 32 MiB (solver.cpp:117-121)"
 
 
 def cpu_model():
@@ -198,108 +213,167 @@ def dist_setup(n_gpus):
     return rank, world, local, pg
 
 
+L2_NOMINAL = 126 << 20  # B200 L2 (device-reported 126 MiB); the same string in both arms
+
+
+def config_dict(name, cfgd, n, nnz, world):
+    """The `config` object, identical in both arms (the driver compares them)."""
+    d = {"workload": cfgd["desc"], "name": name, "n": n, "nnz": nnz, "p": cfgd["p"],
+         "parallelism": "single GPU" if world == 1 else
+         f"level-range shards x{world}, p-deep ghost levels, one halo exchange of x per step"}
+    mat = 12 * nnz + 4 * (n + 1)
+    d["l2"] = (f"inputs larger than L2 ({mat / 1e9:.2f} GB matrix vs {L2_NOMINAL >> 20} MiB L2)"
+               if mat > L2_NOMINAL else
+               "matrix fits the L2; no flush between steps (L2-resident, latency-bound config)")
+    return d
+
+
 def ref_preprocess(R, A, p, cache):
-    """Reference preprocessing on the host (build_levels + permute + group_levels)."""
-    t0 = time.perf_counter()
-    lv, pm, ip, lp = R.build_levels(A.row_ptr, A.col_idx, A.values)
-    t1 = time.perf_counter()
-    prp, pci, pv = R.permute(A.row_ptr, A.col_idx, A.values, pm)
-    t2 = time.perf_counter()
-    gr, _, _, _ = R.group_levels(prp, pci, pv, lp, cache, p)
-    t3 = time.perf_counter()
-    return (prp, pci, pv), pm, gr, {"build_levels_s": t1 - t0, "permute_s": t2 - t1,
-                                    "group_levels_s": t3 - t2}, lp
-
-
-def time_reference_mpk(R, P, gr, p, x, kind, steps, warmup):
-    """Times the reference's blocked mpk / mpk_shifted through its own API (wall clock)."""
+    """Reference preprocessing on the host (build_levels + permute + group_levels), through handles
+    (no second host copy of the matrix: C5 is 11.8 GB).  A = (row_ptr, col_idx, values)."""
     import ctypes as C
-    prp, pci, pv = P
-    n = len(prp) - 1
-    h = R.wrap(prp, pci, pv)
+    rp, ci, v = A
+    n = len(rp) - 1
+    h = R.wrap(rp, ci, v)
+    lv, pm, ip = (np.empty(n, np.uint32) for _ in range(3))
+    lp = np.empty(n + 1, np.uint32)
+    nl = C.c_uint32()
+    t0 = time.perf_counter()
+    assert R.lib.ref_build_levels_h(h, lv.ctypes.data, pm.ctypes.data, ip.ctypes.data,
+                                    lp.ctypes.data, C.byref(nl)) == 0, R.lib.ref_last_error()
+    lp = lp[: nl.value + 1].copy()
+    t1 = time.perf_counter()
+    hp = R.lib.ref_permute_h(h, pm.ctypes.data)
+    assert hp, R.lib.ref_last_error()
+    t2 = time.perf_counter()
+    R.lib.ref_csr_free(h)
+    del lv, ip
+    prp, pci, pv = (C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_double)())
+    R.lib.ref_csr_views(hp, C.byref(prp), C.byref(pci), C.byref(pv))
+    nnz = len(ci)
+    P = (np.ctypeslib.as_array(prp, (n + 1,)), np.ctypeslib.as_array(pci, (nnz,)),
+         np.ctypeslib.as_array(pv, (nnz,)))
+    t3 = time.perf_counter()
+    gr, _, _, _ = R.group_levels(*P, lp, cache, p)
+    t4 = time.perf_counter()
+    return (P, hp), pm, gr, {"build_levels_s": t1 - t0, "permute_s": t2 - t1,
+                             "group_levels_s": t4 - t3}, lp
+
+
+def time_reference_mpk(R, hA, n, gr, p, x, kind, steps, warmup, budget_s=60.0, coefs=None):
+    """Times the reference's blocked mpk / mpk_shifted through its own API (wall clock), every
+    argument built once outside the loop (pre-built handles: matrix, plan, x, shift list, block).
+    kind "poly" = the blocked mpk followed by the A23 combination.  Bounded sample:
+    after the warm-ups, at most `steps` and at most ~budget_s of timed runs (>= 3).
+    Returns (times, timed_steps)."""
     xv = R.lib.ref_vec_new(np.ascontiguousarray(x).ctypes.data, n)
     plan = R.lib.ref_plan_new(n, np.ascontiguousarray(gr, np.uint32).ctypes.data, len(gr) - 1, p)
     blk = R.lib.ref_block_new(n, p + 1)
+    hs = None
+    if kind == "shifted":
+        sh = np.ascontiguousarray(newton_shifts(p))
+        hs = R.lib.ref_shifts_new(sh.ctypes.data, np.zeros(p).ctypes.data, p)
+    data = np.ctypeslib.as_array(R.lib.ref_block_data(blk), ((p + 1) * n,)).reshape(p + 1, n)
+
+    def one():
+        t0 = time.perf_counter()
+        if kind == "shifted":
+            rc = R.lib.ref_mpk_shifted_t(plan, hA, xv, hs, blk, 0)
+        else:
+            rc = R.lib.ref_mpk_t(plan, hA, xv, p, blk, 0)
+        if kind == "poly":  # A23: z = c_0 y_0, then z += c_k y_k (mul, then add)
+            z = coefs[0] * data[0]
+            for k in range(1, p + 1):
+                z += coefs[k] * data[k]
+        t1 = time.perf_counter()
+        assert rc == 0, R.lib.ref_last_error()
+        return t1 - t0
+
     times = []
     try:
-        for i in range(warmup + steps):
-            t0 = time.perf_counter()
-            if kind == "shifted":
-                sh = np.array(newton_shifts(p))
-                out = np.empty((p + 1) * n)
-                rc = R.lib.ref_mpk_shifted_h(h, np.ascontiguousarray(gr, np.uint32).ctypes.data,
-                                             len(gr) - 1, p, np.ascontiguousarray(x).ctypes.data,
-                                             sh.ctypes.data, np.zeros(p).ctypes.data, p,
-                                             out.ctypes.data, 0)
-            else:
-                rc = R.lib.ref_mpk_t(plan, h, xv, p, blk, 0)
-            t1 = time.perf_counter()
-            assert rc == 0, R.lib.ref_last_error()
-            if i >= warmup:
-                times.append(t1 - t0)
+        for _ in range(max(warmup, 1)):
+            t = one()
+        k = max(3, min(steps, int(budget_s / max(t, 1e-9))))
+        for _ in range(k):
+            times.append(one())
     finally:
+        if hs:
+            R.lib.ref_shifts_free(hs)
         R.lib.ref_block_free(blk)
         R.lib.ref_plan_free(plan)
         R.lib.ref_vec_free(xv)
-        R.lib.ref_csr_free(h)
-    _ = C
-    return times
+    return times, len(times)
 
 
 def run_reference(args, cfgd):
+    """`--impl reference`: the reference's own CPU implementation of the path (oracle/_ref, the
+    reference headers compiled in place with the reference flags) on this box's host cores, on the
+    same config.  Loads only oracle/ libraries: inputs come from the harness generators
+    (oracle/_gen), never from the product library."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return  # N>1: rank 0 alone runs the CPU reference
-    from oracle.oracle import Reference, reference_available
-    import paper_2309_02228_b200 as mpkg
+    from oracle.oracle import HarnessGen, Reference, config_matrix, reference_available
     p = cfgd["p"]
     base = {"metric": METRIC, "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-            "higher_is_better": True, "config": {"workload": cfgd["desc"]}}
+            "higher_is_better": True}
     if not reference_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref/libmpkref.so not built"}), flush=True)
         return
-    if cfgd["kind"] == "ortho" or cfgd["kind"] in CHAIN_KINDS:
-        # ortho.hpp / sstep.hpp / poly.hpp need Eigen (not installed): the reference arm times the
-        # oracle's C restatement of the same computation on the same inputs (kind "port")
-        if cfgd["kind"] == "ortho":
-            n = 192 ** 3
-            cb = port_ortho_baseline(cfgd, n, args.seed, args.steps)
-            cfg = {"workload": cfgd["desc"], "n": n, "qcols": cfgd["qcols"], "vcols": cfgd["p"]}
-        else:
-            R = Reference()
-            A = make_matrix(args.config, args.seed)
-            P, perm, _, prep, _ = ref_preprocess(R, A, p, host_llc_bytes())
-            x = np.empty(A.n_rows)
-            x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)
-            cb = port_chain_baseline(cfgd, P, x, args.steps)
-            cfg = {"workload": cfgd["desc"], "n": A.n_rows, "nnz": A.nnz, "p": p, "preprocess_s": prep}
+    G = HarnessGen()
+    if cfgd["kind"] == "ortho":
+        # ortho.hpp needs Eigen (not installed): the oracle's C restatement (kind "port")
+        n = 192 ** 3
+        cb = port_ortho_baseline(cfgd, n, args.seed, args.steps)
+        cfg = {"workload": cfgd["desc"], "name": args.config, "n": n, "qcols": cfgd["qcols"],
+               "vcols": cfgd["p"]}
         med_ms = cb.pop("ms")
         line = {**base, "value": cb["value"], "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": med_ms, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded, DESIGN.md §6)", "config": {**cfg, "cpu": cpu_model()},
-                "cpu_baseline": cb,
-                "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "data": "synthetic (seeded, DESIGN.md §6)", "config": cfg, "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
     R = Reference()
-    A = make_matrix(args.config, args.seed)
-    cache = host_llc_bytes()
-    P, perm, gr, prep, ref_level_ptr = ref_preprocess(R, A, p, cache)
-    x = np.empty(A.n_rows)
-    x[perm] = mpkg.random_vector(A.n_rows, args.seed + 2)  # permute_vector (csr.hpp:191)
-    kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
-    times = time_reference_mpk(R, P, gr, p, x, kind, args.steps, args.warmup)
-    nnz = A.nnz
-    med = statistics.median(times)
-    gf = 2.0 * nnz * p / med * 1e-9
+    t0 = time.perf_counter()
+    A = config_matrix(args.config, args.seed)
+    t_gen = time.perf_counter() - t0
+    n, nnz = len(A[0]) - 1, len(A[1])
+    cache, cache_src = host_llc_bytes()
+    (P, hA), perm, gr, prep, ref_level_ptr = ref_preprocess(R, A, p, cache)
+    prep["generate_host_s"] = t_gen
+    del A
+    x = np.empty(n)
+    x[perm] = G.random_vector(n, args.seed + 2)  # permute_vector (csr.hpp:191)
+    cfg = config_dict(args.config, cfgd, n, nnz, args.gpus)
     cores = R.resolve_threads(0)
+    details = {"cache_bytes": cache, "cache_source": cache_src, "threads": cores,
+               "cpu": cpu_model(), "preprocess_s": prep}
+    if cfgd["kind"] in CHAIN_KINDS:
+        # sstep.hpp / poly.hpp need Eigen: the oracle's C restatement of the same chain (kind "port")
+        cb = port_chain_baseline(cfgd, P, x, args.steps)
+        R.lib.ref_csr_free(hA)
+        med_ms = cb.pop("ms")
+        line = {**base, "value": cb["value"], "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": med_ms, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, DESIGN.md §6)", "config": cfg, "details": details,
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    kind = {"shifted": "shifted", "poly": "poly"}.get(cfgd["kind"], "plain")
+    coefs = poly_coefs(args.seed + 3, p) if kind == "poly" else None
+    times, k = time_reference_mpk(R, hA, n, gr, p, x, kind, args.steps, args.warmup, coefs=coefs)
+    med = statistics.median(times)
+    flops = 2.0 * nnz * p + (2.0 * n * (p + 1) if kind == "poly" else 0.0)
+    gf = flops / med * 1e-9
     # SURVEY 8(d): also the reference's baseline_mpk (p plain sweeps) and the blocked mpk at the
-    # CLI's default 32 MiB budget (solver.cpp:117-121); median of 3 after one warm-up each
-    extra = {}
-    if kind == "plain":  # through pre-built handles, as time_reference_mpk does
-        h = R.wrap(*P)
-        xv = R.lib.ref_vec_new(np.ascontiguousarray(x).ctypes.data, len(x))
-        blk = R.lib.ref_block_new(len(x), p + 1)
+    # CLI's default 32 MiB budget (solver.cpp:117-121), through the same pre-built handles
+    if kind == "plain":
+        xv = R.lib.ref_vec_new(np.ascontiguousarray(x).ctypes.data, n)
+        blk = R.lib.ref_block_new(n, p + 1)
 
         def med3(fn):
             fn()
@@ -310,30 +384,28 @@ def run_reference(args, cfgd):
                 ts.append(time.perf_counter() - t0)
             return statistics.median(ts)
         try:
-            t_base = med3(lambda: R.lib.ref_baseline_mpk_t(h, xv, p, blk, 0))
-            extra["reference_baseline_mpk_gflops"] = 2.0 * nnz * p / t_base * 1e-9
+            t_base = med3(lambda: R.lib.ref_baseline_mpk_t(hA, xv, p, blk, 0))
+            details["reference_baseline_mpk_gflops"] = 2.0 * nnz * p / t_base * 1e-9
             if cache != (32 << 20):
                 gr32, _, _, _ = R.group_levels(*P, ref_level_ptr, 32 << 20, p)
                 g32 = np.ascontiguousarray(gr32, np.uint32)
-                plan32 = R.lib.ref_plan_new(len(x), g32.ctypes.data, len(g32) - 1, p)
-                t32 = med3(lambda: R.lib.ref_mpk_t(plan32, h, xv, p, blk, 0))
+                plan32 = R.lib.ref_plan_new(n, g32.ctypes.data, len(g32) - 1, p)
+                t32 = med3(lambda: R.lib.ref_mpk_t(plan32, hA, xv, p, blk, 0))
                 R.lib.ref_plan_free(plan32)
-                extra["reference_mpk_32MiB_gflops"] = 2.0 * nnz * p / t32 * 1e-9
+                details["reference_mpk_32MiB_gflops"] = 2.0 * nnz * p / t32 * 1e-9
         finally:
             R.lib.ref_block_free(blk)
             R.lib.ref_vec_free(xv)
-            R.lib.ref_csr_free(h)
-    line = {**base, "value": gf, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+    R.lib.ref_csr_free(hA)
+    what = {"shifted": "mpk_shifted", "poly": "mpk + the A23 combination"}.get(kind, "mpk")
+    line = {**base, "value": gf, "steps": k, "warmup": max(args.warmup, 1),
             "ms_per_step": med * 1e3, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generators, DESIGN.md §6)",
-            "config": {"workload": cfgd["desc"], "n": A.n_rows, "nnz": nnz, "p": p,
-                       "cache_bytes": cache, "threads": cores, "cpu": cpu_model(),
-                       "preprocess_s": prep, **extra},
+            "data": "synthetic (seeded generators, DESIGN.md §6)", "config": cfg, "details": details,
             "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                             "sample": f"full {args.config} workload, reference blocked "
-                                       f"{'mpk_shifted' if kind == 'shifted' else 'mpk'} "
-                                       f"(p={p}, LLC budget {cache >> 20} MiB), median of "
-                                       f"{args.steps} after {args.warmup} warm-up"},
+                             "sample": f"full {args.config} workload, reference blocked {what} "
+                                       f"(p={p}, LLC budget {cache >> 20} MiB from {cache_src}), "
+                                       f"median of {k} after {max(args.warmup, 1)} warm-up "
+                                       f"({med:.3f} s each; at most ~60 s timed)"},
             "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -405,21 +477,30 @@ def port_ortho_baseline(cfgd, n, seed, steps):
                       f"({med:.2f} s each); cpu: {cpu_model()}"}
 
 
-def cpu_baseline_reference(A_perm_host, perm_unused, ls_level_ptr, p, x, kind, nnz, ctx=None):
-    """Reference CPU path on the host cores (bounded: full workload, 1 warm-up + median of 3)."""
+def cpu_baseline_reference(A_perm_host, ls_level_ptr, p, x, kind, nnz, coefs=None):
+    """cpu_baseline of the GPU arm: the reference's blocked mpk (oracle/_ref) on the host cores, on
+    the GPU path's A_perm (bit-identical to the reference's, tests/test_gpu_fullsize.py), bounded:
+    1 warm-up + median of 3 full-workload calls."""
     from oracle.oracle import Oracle, Reference, reference_available
-    cache = host_llc_bytes()
+    cache, cache_src = host_llc_bytes()
+    n = A_perm_host.n_rows
     if reference_available():
         R = Reference()
         P = (A_perm_host.row_ptr, A_perm_host.col_idx, A_perm_host.values)
         gr, _, _, _ = R.group_levels(*P, ls_level_ptr, cache, p)
-        times = time_reference_mpk(R, P, gr, p, x, kind, 3, 1)
+        hA = R.wrap(*P)
+        try:
+            times, k = time_reference_mpk(R, hA, n, gr, p, x, kind, 3, 1, budget_s=30.0, coefs=coefs)
+        finally:
+            R.lib.ref_csr_free(hA)
         med = statistics.median(times)
-        return {"value": 2.0 * nnz * p / med * 1e-9, "unit": "GFLOP/s",
+        flops = 2.0 * nnz * p + (2.0 * n * (p + 1) if kind == "poly" else 0.0)
+        what = {"shifted": "mpk_shifted", "poly": "mpk + the A23 combination"}.get(kind, "mpk")
+        return {"value": flops / med * 1e-9, "unit": "GFLOP/s",
                 "cores": R.resolve_threads(0), "kind": "reference",
-                "sample": f"full workload, reference blocked mpk (OpenMP, p={p}, LLC budget "
-                          f"{cache >> 20} MiB): 1 warm-up + median of 3 ({med:.3f} s each); "
-                          f"cpu: {cpu_model()}"}
+                "sample": f"full workload, reference blocked {what} (OpenMP, p={p}, LLC budget "
+                          f"{cache >> 20} MiB from {cache_src}): 1 warm-up + median of {k} "
+                          f"({med:.3f} s each); cpu: {cpu_model()}"}
     O = Oracle()
     t0 = time.perf_counter()
     O.baseline_mpk(A_perm_host.row_ptr, A_perm_host.col_idx, A_perm_host.values, x, 1)
@@ -526,16 +607,12 @@ def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
-            "config": {"workload": cfgd["desc"], "n": n, "nnz": nnz, "p": p,
-                       "parallelism": f"level-range shards x{world}, p-deep ghost levels, "
-                                      f"one {dist.get_backend().upper()} halo exchange of x per step",
-                       "l2": "inputs larger than L2" if 12 * nnz > info["l2_bytes"] else "fits L2",
-                       "mode": "bitwise", "rank0_shard": {"own_rows": [o0, o1],
-                                                         "local_rows": list(hp.local_rows),
-                                                         "local_nnz": nnz_loc},
-                       "executor": shard.plan.exec_info(), "preprocess_s": prep,
-                       "parity": "own rows == single-GPU baseline bitwise (all ranks)" if parity
-                       else "MISMATCH"},
+            "config": config_dict(args.config, cfgd, n, nnz, world),
+            "parity": ("own rows == single-GPU baseline bitwise (all ranks)" if parity else "MISMATCH"),
+            "details": {"mode": "bitwise", "backend": dist.get_backend(),
+                        "rank0_shard": {"own_rows": [o0, o1], "local_rows": list(hp.local_rows),
+                                        "local_nnz": nnz_loc},
+                        "executor": shard.plan.exec_info(), "preprocess_s": prep},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "algorithmic_bytes": b_loc, "kernel_ms": kernel_ms,
@@ -697,12 +774,52 @@ def run_ortho(args, cfgd):
         sys.exit(3)
 
 
+DIGESTS = ROOT / "tests" / "golden" / "config_digests.json"
+
+
+def _sha(a) -> str:
+    import hashlib
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(memoryview(a).cast("B")).hexdigest()
+
+
+def reference_digest_parity(name, seed, kind, ls, Ap, x_perm, d_blk, p, n, d_z=None):
+    """Bench-time parity against the REFERENCE: SHA-256 of this run's levels, perm, inv_perm,
+    level_ptr, A_perm, x and every basis slice (or z) against the digests of the reference's own
+    outputs on the same inputs (tests/golden/config_digests.json, made by
+    tests/golden/make_config_digests.py from oracle/_ref).  None when no digest exists for this
+    config / seed."""
+    key = {"c2": "c2", "c3": "c3", "c4": "c4", "c4poly": "c4", "c5": "c5"}.get(name)
+    if key is None or not DIGESTS.exists():
+        return None
+    d = json.loads(DIGESTS.read_text()).get(key)
+    if d is None or d.get("seed") != seed:
+        return None
+    bad = [k for k in ("levels", "perm", "inv_perm", "level_ptr") if _sha(getattr(ls, k)) != d[k]]
+    P = Ap.download()
+    bad += [f"A_perm.{k}" for k in ("row_ptr", "col_idx", "values") if _sha(getattr(P, k)) != d[f"A_perm.{k}"]]
+    del P
+    if _sha(x_perm) != d["x_perm"]:
+        bad.append("x_perm")
+    what = ["levels", "perm", "inv_perm", "level_ptr", "A_perm", "x"]
+    if kind == "poly":
+        if _sha(d_z.cpu().numpy()) != d["poly_z"]:
+            bad.append("z")
+        what.append("z")
+    ref = d["mpk_shifted"] if kind == "shifted" else d["mpk"]
+    for k in range(p + 1):
+        if _sha(d_blk[k * n:(k + 1) * n].cpu().numpy()) != ref[k]:
+            bad.append(f"slice {k}")
+    what.append(f"slices 0..{p}")
+    return {"match": not bad, "mismatches": bad, "checked": what}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="mpkg", choices=["mpkg", "reference"])
     ap.add_argument("--seed", type=int, default=2309)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -722,6 +839,21 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfgd = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch sets
+        # WORLD_SIZE and lands below)
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), str(pathlib.Path(__file__).resolve()), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    world_env = int(os.environ.get("WORLD_SIZE", 1))
+    if world_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
         return run_reference(args, cfgd)
     if cfgd["kind"] == "ortho":
@@ -1022,6 +1154,16 @@ def main():
         except Exception:
             traffic = None
 
+    # ---- parity against the reference's own outputs (digests), bitwise runs of the MPK configs
+    ref_parity = None
+    if chain is None and args.mode == "bitwise" and rank == 0:
+        step()
+        sync()
+        ref_parity = reference_digest_parity(args.config, args.seed, cfgd["kind"], ls, Ap, x_perm,
+                                             d_blk, p, n, d_z if cfgd["kind"] == "poly" else None)
+        if ref_parity is not None and not ref_parity["match"]:
+            parity = False
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         P_host = Ap.download()
@@ -1029,8 +1171,10 @@ def main():
             cpu = port_chain_baseline(cfgd, (P_host.row_ptr, P_host.col_idx, P_host.values), x_perm, args.steps)
             cpu.pop("ms")
         else:
-            kind = "shifted" if cfgd["kind"] == "shifted" else "plain"
-            cpu = cpu_baseline_reference(P_host, None, ls.level_ptr, p, x_perm, kind, nnz)
+            kind = {"shifted": "shifted", "poly": "poly"}.get(cfgd["kind"], "plain")
+            cpu = cpu_baseline_reference(P_host, ls.level_ptr, p, x_perm, kind, nnz,
+                                         coefs=coefs if kind == "poly" else None)
+        del P_host
 
     if rank == 0:
         line = {
@@ -1038,21 +1182,21 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
-            "config": {"workload": cfgd["desc"], "n": n, "nnz": nnz, "p": p,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": f"inputs larger than L2 ({(12 * nnz) / 1e9:.2f} GB matrix vs "
-                             f"{info['l2_bytes'] >> 20} MiB L2)" if 12 * nnz > info["l2_bytes"]
-                       else "matrix fits L2; no flush between steps (latency-bound config)",
-                       "mode": args.mode, "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
-                       "plan_cache_bytes": cache, "executor": exec_info,
-                       "preprocess_s": prep,
-                       "parity": ("MISMATCH" if not parity else "mpk == baseline bitwise"
-                                  if args.mode == "bitwise" else
-                                  f"max inf-norm rel err {max_rel_err:.2e} <= 1e-12 vs baseline"), "baseline_back_to_back_ms": baseline_ms,
-                       "baseline_gflops": flops / (baseline_ms * 1e-3) * 1e-9,
-                       "baseline_note": "p back-to-back launches of the plain SpMV (baseline_mpk)"
-                                        + ("; chains: flops of the preconditioned chain over the "
-                                           "unpreconditioned baseline's time" if chain is not None else "")},
+            "config": config_dict(args.config, cfgd, n, nnz, world),
+            "parity": ("MISMATCH" if not parity else
+                       ("bitwise == the reference's outputs (SHA-256 of " + ", ".join(ref_parity["checked"])
+                        + "; tests/golden/config_digests.json) and mpk == baseline_mpk bitwise")
+                       if ref_parity else "mpk == baseline bitwise" if args.mode == "bitwise" else
+                       f"max inf-norm rel err {max_rel_err:.2e} <= 1e-12 vs baseline"),
+            "details": {"mode": args.mode, "n_levels": ls.n_levels(), "n_groups": plan.n_groups(),
+                        "plan_cache_bytes": cache, "executor": exec_info, "preprocess_s": prep,
+                        "reference_digests": ref_parity,
+                        "baseline_back_to_back_ms": baseline_ms,
+                        # the chains have no one-launch-per-power twin of their own: report the
+                        # plain baseline_mpk's time only, no GF/s that mixes the two
+                        **({"baseline_mpk_gflops": 2.0 * nnz * p / (baseline_ms * 1e-3) * 1e-9}
+                           if chain is None else {}),
+                        "baseline_note": "p back-to-back launches of the plain SpMV (baseline_mpk)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms,

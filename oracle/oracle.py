@@ -372,6 +372,13 @@ class Reference:
             "ref_baseline_mpk_shifted_h": ([P, P, P, P, i32, P, i32], C.c_int),
             "ref_mpk_shifted_h": ([P, P, u32, i32, P, P, P, i32, P, i32], C.c_int),
             "ref_check_shift_chain": ([P, P, i32], C.c_int),
+            "ref_build_levels_h": ([P, P, P, P, P, P], C.c_int),
+            "ref_permute_h": ([P, P], P),
+            "ref_csr_views": ([P, P, P, P], None),
+            "ref_shifts_new": ([P, P, i32], P),
+            "ref_shifts_free": ([P], None),
+            "ref_baseline_mpk_shifted_t": ([P, P, P, P, i32], C.c_int),
+            "ref_mpk_shifted_t": ([P, P, P, P, P, i32], C.c_int),
             "ref_tune_select": ([P, i32, i32], C.c_int),
             "ref_resolve_threads": ([i32], C.c_int),
             "ref_jacobi_setup": ([u32, P, P, P, i32, P, P], C.c_int),
@@ -630,3 +637,89 @@ class Reference:
 
 def reference_available() -> bool:
     return REF_SO.exists()
+
+
+GEN_SO = HERE / "_gen" / "libmpkgen.so"
+
+
+class HarnessGen:
+    """Host-only harness generators (oracle/_gen/libmpkgen.so, built from the same generators.cpp
+    as the product's mpkg_gen) for legs that must not load the product library: bench.py's
+    `--impl reference` arm and tests/golden/make_config_digests.py.  Returns (row_ptr, col_idx,
+    values) numpy arrays."""
+
+    KINDS = {"poisson3d": 3, "stencil27": 6, "stencil27_random_sym": 7, "rmat": 8}
+
+    def __init__(self, path: pathlib.Path = GEN_SO):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing (make -C oracle)")
+        L = self.lib = C.CDLL(str(path))
+        L.mpkg_gen.argtypes = [i32, u32, u32, u32, u64, C.POINTER(P)]
+        L.mpkg_gen.restype = C.c_int
+        L.mpkg_host_csr_scramble.argtypes = [P, u64, P, C.POINTER(P)]
+        L.mpkg_host_csr_scramble.restype = C.c_int
+        L.mpkg_host_csr_info.argtypes = [P, P, P, P]
+        L.mpkg_host_csr_arrays.argtypes = [P, P, P, P]
+        L.mpkg_host_csr_destroy.argtypes = [P]
+        L.mpkg_random_vector.argtypes = [u64, u64, P]
+        L.mpkg_random_vector.restype = C.c_int
+        L.gen_last_error.restype = C.c_char_p
+
+    def _take(self, h, keep=False):
+        n, nc, nnz = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        self.lib.mpkg_host_csr_info(h, C.byref(n), C.byref(nc), C.byref(nnz))
+        rp, ci, v = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_double)()
+        self.lib.mpkg_host_csr_arrays(h, C.byref(rp), C.byref(ci), C.byref(v))
+        out = (np.ctypeslib.as_array(rp, (n.value + 1,)).copy(),
+               np.ctypeslib.as_array(ci, (nnz.value,)).copy() if nnz.value else np.empty(0, np.uint32),
+               np.ctypeslib.as_array(v, (nnz.value,)).copy() if nnz.value else np.empty(0))
+        if not keep:
+            self.lib.mpkg_host_csr_destroy(h)
+        return out
+
+    def _gen(self, kind, a, b=0, c=0, seed=0, keep=False):
+        h = P()
+        if self.lib.mpkg_gen(kind, a, b, c, seed, C.byref(h)):
+            raise ValueError(self.lib.gen_last_error().decode())
+        return (h, self._take(h, keep=True)) if keep else self._take(h)
+
+    def poisson3d(self, nx, ny, nz):
+        return self._gen(3, nx, ny, nz)
+
+    def stencil27(self, nx, ny, nz):
+        return self._gen(6, nx, ny, nz)
+
+    def rmat(self, scale, edge_factor, seed):
+        return self._gen(8, scale, edge_factor, 0, seed)
+
+    def scrambled_stencil27_random_sym(self, nx, ny, nz, seed, scramble_seed):
+        h = P()
+        if self.lib.mpkg_gen(7, nx, ny, nz, seed, C.byref(h)):
+            raise ValueError(self.lib.gen_last_error().decode())
+        h2 = P()
+        rc = self.lib.mpkg_host_csr_scramble(h, scramble_seed, None, C.byref(h2))
+        self.lib.mpkg_host_csr_destroy(h)
+        if rc:
+            raise ValueError(self.lib.gen_last_error().decode())
+        return self._take(h2)
+
+    def random_vector(self, n, seed):
+        out = np.empty(n)
+        assert self.lib.mpkg_random_vector(n, seed, out.ctypes.data) == 0
+        return out
+
+
+def config_matrix(cfg: str, seed: int):
+    """BASELINE.json config matrices from the harness generators (same seeds as bench.py)."""
+    G = HarnessGen()
+    if cfg == "c1":
+        return G.poisson3d(64, 64, 64)
+    if cfg == "c2":
+        return G.scrambled_stencil27_random_sym(160, 160, 160, seed, seed + 1)
+    if cfg == "c3":
+        return G.rmat(21, 16, seed)
+    if cfg.startswith("c4"):
+        return G.stencil27(192, 192, 192)
+    if cfg == "c5":
+        return G.poisson3d(512, 512, 512)
+    raise ValueError(cfg)

@@ -128,6 +128,36 @@ int ref_build_levels(uint32_t n, const uint32_t* rp, const uint32_t* ci, const d
     });
 }
 
+// Handle forms for full-size inputs (C5: 11.8 GB of CSR): no second host copy per call.
+int ref_build_levels_h(void* h, uint32_t* levels, uint32_t* perm, uint32_t* inv_perm,
+                       uint32_t* level_ptr, uint32_t* n_levels) {
+    return guard([&] {
+        const auto& A = *static_cast<mpk::CsrMatrix*>(h);
+        const auto ls = mpk::build_levels(A);
+        const std::size_t n = A.n_rows;
+        std::memcpy(levels, ls.levels.data(), sizeof(uint32_t) * n);
+        std::memcpy(perm, ls.perm.data(), sizeof(uint32_t) * n);
+        std::memcpy(inv_perm, ls.inv_perm.data(), sizeof(uint32_t) * n);
+        std::memcpy(level_ptr, ls.level_ptr.data(), sizeof(uint32_t) * ls.level_ptr.size());
+        *n_levels = ls.n_levels();
+    });
+}
+void* ref_permute_h(void* h, const uint32_t* perm) {
+    void* out = nullptr;
+    guard([&] {
+        const auto& A = *static_cast<mpk::CsrMatrix*>(h);
+        out = new mpk::CsrMatrix(mpk::permute(A, std::vector<index_t>(perm, perm + A.n_rows)));
+    });
+    return out;
+}
+// Borrowed views of a handle's arrays (valid until ref_csr_free).
+void ref_csr_views(void* h, uint32_t** rp, uint32_t** ci, double** v) {
+    auto* m = static_cast<mpk::CsrMatrix*>(h);
+    *rp = m->row_ptr.data();
+    *ci = m->col_idx.data();
+    *v = m->values.data();
+}
+
 int ref_permute(uint32_t n, const uint32_t* rp, const uint32_t* ci, const double* v,
                 const uint32_t* perm, uint32_t* orp, uint32_t* oci, double* ov) {
     return guard([&] {
@@ -270,6 +300,28 @@ int ref_mpk_shifted_h(void* h, const uint32_t* group_rows, uint32_t ng, int plan
         mpk::mpk_shifted(plan, A, std::vector<double>(x, x + A.n_rows), shifts_from(re, im, ns),
                          blk, threads);
         std::memcpy(block, blk.data.data(), sizeof(double) * blk.data.size());
+    });
+}
+
+// Timed shifted variants (bench --impl reference, C4): the shift list, the plan, x and the block
+// are built once outside the timed loop, as ref_mpk_t does for the plain MPK.
+void* ref_shifts_new(const double* re, const double* im, int ns) {
+    return new std::vector<std::complex<double>>(shifts_from(re, im, ns));
+}
+void ref_shifts_free(void* s) { delete static_cast<std::vector<std::complex<double>>*>(s); }
+int ref_baseline_mpk_shifted_t(void* h, void* x, void* shifts, void* blk, int threads) {
+    return guard([&] {
+        mpk::baseline_mpk_shifted(*static_cast<mpk::CsrMatrix*>(h), *static_cast<std::vector<double>*>(x),
+                                  *static_cast<std::vector<std::complex<double>>*>(shifts),
+                                  *static_cast<mpk::VectorBlock*>(blk), threads);
+    });
+}
+int ref_mpk_shifted_t(void* plan, void* h, void* x, void* shifts, void* blk, int threads) {
+    return guard([&] {
+        mpk::mpk_shifted(*static_cast<mpk::ExecutionPlan*>(plan), *static_cast<mpk::CsrMatrix*>(h),
+                         *static_cast<std::vector<double>*>(x),
+                         *static_cast<std::vector<std::complex<double>>*>(shifts),
+                         *static_cast<mpk::VectorBlock*>(blk), threads);
     });
 }
 
