@@ -180,8 +180,9 @@ int mpkg_plan_destroy(mpkg_plan_t P);
 int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets,
                         uint64_t* n_dep_tiles, uint32_t* pass_powers);
 /* How the last mpkg_mpk* on this plan ran: private row order (0 A_perm, 1 Cuthill-McKee inside
- * levels, 2 longest rows first), sweeps (1: one launch per power, 0: one fused launch), fused
- * kernel variant, rows handled outside the SELL arrays (long rows). */
+ * levels, 2 longest rows first), schedule (1: one launch per power, 2: the wave schedule, one
+ * persistent launch per pass of p' powers; 0: one fused tile-DAG launch), fused kernel variant,
+ * rows handled outside the SELL arrays (long rows). */
 int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
 
 /* execute.hpp:59-72 wavefront_schedule (pure host function; arrays hold n_groups*stages). */

@@ -379,7 +379,7 @@ class ExecutionPlan:
         check(lib.mpkg_plan_exec_mode(self.h, C.byref(o), C.byref(sw), C.byref(kn), C.byref(lr)))
         return {"tiles": t.value, "tickets": k.value, "dep_tiles": d.value,
                 "pass_powers": pp.value, "order": o.value,
-                "schedule": "sweeps" if sw.value else "fused", "kernel": kn.value,
+                "schedule": {1: "sweeps", 2: "wave"}.get(sw.value, "fused"), "kernel": kn.value,
                 "long_rows": lr.value}
 
     def __del__(self):

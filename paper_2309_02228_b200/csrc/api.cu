@@ -326,7 +326,7 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
         else if (k == "pdl")
             ctx->pdl = value != 0;
         else if (k == "schedule") {
-            require(value >= 0 && value <= 2, "ctx_set_param: schedule must be 0 (auto), 1 (fused) or 2 (sweeps)");
+            require(value >= 0 && value <= 3, "ctx_set_param: schedule must be 0 (auto), 1 (fused), 2 (sweeps) or 3 (wave)");
             ctx->schedule = value;
         }
         else if (k == "producers") {

@@ -87,6 +87,7 @@ struct Executor {
     uint32_t n_prod = 0, n_cgroups = 0;       // k_mpk_async roles
     bool sb = false;                          // poll dependencies through superblock counters
     bool last_sweep = false;                  // the last run used one launch per power
+    bool last_wave = false;                   // the last run used the wave schedule
     bool fused_ready = false;                 // build_fused() has run
     // sweep schedule: instantiated CUDA graphs by launch parameters (run_fused)
     std::vector<std::pair<std::vector<unsigned char>, cudaGraphExec_t>> graphs;
@@ -119,6 +120,20 @@ struct Executor {
     DevBuf<uint32_t> res_bar;    // k_mpk_resident grid barrier {arrivals, generation}
     int res_grid[6] = {0, 0, 0, 0, 0, 0};  // cooperative grid per (kind, sigma)
     DevBuf<uint4> coop_items, coop_multi;
+    // wave schedule (schedule knob 3): per p, the pass ticket lists and pass boundaries
+    struct Wave {
+        DevBuf<uint32_t> tickets;
+        std::vector<uint32_t> t_begin;  // first ticket of every pass (+ the end)
+        std::vector<int> q_begin;       // first power of every pass (+ p+1)
+        int pass_len = 0;
+        int64_t slack = 0;
+        uint64_t window = 0;            // simulated live window of the chosen pass length
+    };
+    std::map<int, Wave> wave;
+    int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
+    std::vector<uint32_t> wave_reach;         // per tile: furthest tile read by tiles <= T
+    DevBuf<uint32_t> wave_rec;                // per tile: kWaveRuns dependency runs (lo[], hi[])
+    int64_t sched_knob = 0;
     DevBuf<double> coop_part;
     uint32_t n_coop = 0, n_multi = 0;
 };
@@ -954,6 +969,184 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
     }
 }
 
+// ---- Wave schedule ("schedule" knob 3): cross-power L2 reuse ------------------------------------
+//
+// One persistent launch per PASS of p' consecutive powers q0..q1.  The unit of work is a ticket
+// (tile = one 32-slot SELL chunk, power q), executed by ONE WARP (lane = row): no CTA barrier ever
+// couples warps.  The pass's tickets are listed in a host-computed skewed order (wave_order:
+// ready(T, q) = ready(reach(T), q-1) + slack, reach(T) = the furthest tile T's rows read), so the
+// p' powers sweep the matrix as p' fronts a little more than one BFS level apart.  A tile's
+// matrix slice is read from HBM by the front of power q0 and from L2 by the fronts behind it as
+// long as the live window (p'-1 level lags plus the tickets in flight) fits the L2 budget; get_wave
+// picks p' by evaluating that window on the ticket order -- the plan's cache budget
+// (plan.hpp:88-115) sized for this GPU's L2.  Synchronisation is the reference's wavefront rule
+// at tile granularity (execute.hpp:59-72, cell (g, q) after (g-1..g+1, q-1)): per-tile flags
+// done[T] = last finished power.
+//
+// Per ticket a warp (1) issues its rows' first matrix group and the relaxed polls of the tile's
+// dependency flags (up to 4 runs, lane-parallel) together, (2) runs ONE fence.acq_rel.gpu that is
+// both the acquire of those flags and the release of the PREVIOUS ticket's rows, then stores that
+// ticket's flag, (3) gathers y_{q-1} (L2-only loads: rows of other SMs), sums in stored order
+// (rowdot.cuh: bitwise) and stores.  The fence therefore waits on loads the warp needs anyway.
+// A warp whose poll fails publishes its pending ticket before it spins, so deferred publication
+// can never block a dependent.  Tickets are statically assigned (ticket t of the pass runs on warp
+// t mod warps, each warp in increasing t) and the launch is cooperative (all CTAs resident): the
+// warp holding the lowest unfinished ticket has finished every earlier ticket of its own, every
+// dependency of that ticket is lower, so it progresses -- deadlock-free with no atomic ticket
+// counter serialising the ~10^7 tickets of a C5 pass.
+constexpr uint32_t kWaveRows = 32;
+constexpr int kWaveRuns = 4;  // dependency runs per tile record
+
+__device__ __forceinline__ double ld_cg(const double* p) {
+    double r;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+template <bool FIRST>
+__device__ __forceinline__ double wave_ld(const double* p) {
+    if constexpr (FIRST) return __ldg(p);  // slice q0-1: complete before the launch
+    else return ld_cg(p);                  // written by other SMs in this launch: L2 only
+}
+
+// The matrix group of entries k0..k0+7 of the lane's row (rowdot.cuh sell_row_dot layout).
+__device__ __forceinline__ void wave_group(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
+                                           uint32_t k0, uint64_t pol, uint32_t (&c)[8], double (&v)[8]) {
+    const uint32_t Lp = L & ~1u;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        const uint32_t k = k0 + j;
+        if (k + 1 < Lp) {
+            const uint64_t e = off + (k >> 1) * 64u + lane * 2u;
+            const uint2 tt = ld_mat_u2(reinterpret_cast<const uint2*>(P.cols + e), pol);
+            const double2 w = ld_mat_d2(reinterpret_cast<const double2*>(P.vals + e), pol);
+            c[j] = tt.x, c[j + 1] = tt.y, v[j] = w.x, v[j + 1] = w.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const uint32_t kk = k + i;
+                const uint64_t e = off + sell_pos(kk, Lp, lane);
+                c[j + i] = kk < L ? ld_mat_u32(P.cols + e, pol) : 0u;
+                v[j + i] = kk < L ? ld_mat_d(P.vals + e, pol) : 0.0;
+            }
+        }
+    }
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double wave_row(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
+                                           uint32_t len, const double* src, uint64_t pol, uint32_t (&c)[8],
+                                           double (&v)[8]) {
+    double acc = 0.0;
+    for (uint32_t k0 = 0;;) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = k0 + j < len ? wave_ld<FIRST>(src + c[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+        k0 += 8;
+        if (k0 >= len) break;
+        wave_group(P, off, L, lane, k0, pol, c, v);  // rows longer than 8 (27-point stencils)
+    }
+    return acc;
+}
+
+// row_epilogue with the wave's coherence rules: reads of rows finished in this launch go to L2.
+template <int KIND, bool SIGMA, bool FIRST>
+__device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, uint32_t r, uint32_t q,
+                                              const double* src, double acc) {
+    if constexpr (KIND == 1) {
+        const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
+        const double own = wave_ld<FIRST>(src + s);
+        const double own2 = b2 != 0.0 ? ld_cg(P.V + (uint64_t)(q - 2) * P.vstride + s) : 0.0;
+        acc = shift_epilogue(acc, a, b2, own, own2);
+    }
+    P.V[(uint64_t)q * P.vstride + s] = acc;
+    if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
+    if constexpr (KIND == 2) {
+        double zr;
+        if (q == 1)
+            zr = __dadd_rn(__dmul_rn(P.coef[0], wave_ld<FIRST>(src + s)), __dmul_rn(P.coef[1], acc));
+        else
+            zr = __dadd_rn(ld_cg(P.zs + s), __dmul_rn(P.coef[q], acc));
+        P.zs[s] = zr;
+        if (SIGMA && q == P.p) P.z[r] = zr;
+    }
+}
+
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(256) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
+                                                   uint32_t t1, uint32_t q0) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    uint32_t t = t0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t pend_T = 0xffffffffu, pend_q = 0;  // finished, not yet published
+    uint32_t code = t < t1 ? P.tickets[t] : 0u;
+    for (; t < t1; t += nw) {
+        const uint32_t next = t + nw < t1 ? P.tickets[t + nw] : 0u;  // one ticket ahead
+        const uint32_t T = code & 0xffffffu;
+        const uint32_t q = (code >> 24) & 63u;
+        const uint64_t pol = l2_policy(code & kLastUse);
+        const uint32_t s = T * kWaveRows + lane;
+        const uint32_t r = s < P.n_slots ? (SIGMA ? P.slot_row[s] : s) : 0xffffffffu;
+        const bool active = r < P.n_rows;
+        uint32_t len = 0, L = 0;
+        uint64_t off = 0;
+        uint32_t c[8];
+        double v[8];
+        if (active) {
+            len = P.row_len[s];
+            off = P.chunk_off[s >> 5];
+            L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
+            wave_group(P, off, L, lane, 0, pol, c, v);
+        }
+        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
+        if (q > q0) {
+            // dependency runs: lanes 8j..8j+7 poll run j, 8 tiles per round
+            const uint32_t* rec = P.dep_lo + (uint64_t)T * (2 * kWaveRuns);
+            const uint32_t lo = rec[lane >> 3], hi = rec[kWaveRuns + (lane >> 3)];
+            for (;;) {
+                bool ok = true;
+                for (uint32_t u = lo + (lane & 7u); u <= hi; u += 8)
+                    if (ld_relaxed(P.done + u) < q - 1) {
+                        ok = false;
+                        break;
+                    }
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (pend_T != 0xffffffffu) {  // never hold back a finished tile while waiting
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
+                    pend_T = 0xffffffffu;
+                }
+                __nanosleep(128);
+            }
+        }
+        // acquire of the polled flags + release of the pending ticket's rows
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (pend_T != 0xffffffffu && lane == 0)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
+        if (active) {
+            if (q > q0) {
+                const double acc = wave_row<false>(P, off, L, lane, len, src, pol, c, v);
+                wave_epilogue<KIND, SIGMA, false>(P, s, r, q, src, acc);
+            } else {
+                const double acc = wave_row<true>(P, off, L, lane, len, src, pol, c, v);
+                wave_epilogue<KIND, SIGMA, true>(P, s, r, q, src, acc);
+            }
+        }
+        // lanes of long rows may still be storing: the pending flag covers the whole warp
+        // (bar.warp.sync orders every lane's stores before lane 0's fence + flag store)
+        __syncwarp();
+        pend_T = T;
+        pend_q = q;
+        code = next;
+    }
+    if (pend_T != 0xffffffffu) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
+    }
+}
+
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
     asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n));
 }
@@ -1329,12 +1522,13 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
         P->exec->tile_knob == ctx->tile_rows && P->exec->thread_knob == ctx->threads &&
         P->exec->kernel_knob == ctx->kernel &&
         P->exec->prod_knob == ctx->producers &&
-        P->exec->cg_knob == ctx->cgroups) {
+        P->exec->cg_knob == ctx->cgroups && P->exec->sched_knob == ctx->schedule) {
         Executor& E = *P->exec;
         const std::array<int64_t, 4> k = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
         if (E.knobs != k && E.fused_ready) {
             E.tickets.clear();  // schedule knobs changed: re-plan the ticket order
             E.pass_len.clear();
+            E.wave.clear();
             const int occ = ctx->ctas_per_sm > 0 ? std::min<int>(E.occ_max, (int)ctx->ctas_per_sm) : E.occ_max;
             E.grid = occ * ctx->sm_count;
             E.slack = ctx->slack >= 0 ? ctx->slack : (int64_t)E.grid * E.stages;
@@ -1346,6 +1540,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->knobs = {ctx->slack, ctx->pass_powers, ctx->l2_budget, ctx->ctas_per_sm};
     E->order_knob = ctx->order;
     E->kernel_knob = ctx->kernel;
+    E->sched_knob = ctx->schedule;
     cudaStream_t st = ctx->stream;
     E->n_rows = A->n_rows;
     E->n_slots = (A->n_rows + 31u) & ~31u;
@@ -1371,6 +1566,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->tile_rows = ctx->tile_rows == 32 ? 32u : ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
     if (E->tile_rows == 32 && ctx->kernel != 4) E->tile_rows = 64;  // 32-row tiles: async kernel only
     if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
+    if (ctx->schedule == 3) E->tile_rows = kWaveRows;  // wave: one row per thread of a CTA
     // consumer threads: one per tile row unless forced
     E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
     if (E->threads < E->tile_rows) E->threads = E->tile_rows;
@@ -1707,6 +1903,126 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.tickets.emplace(p, std::move(d)).first->second;
 }
 
+// Wave schedule, host side.  Per tile: the dependency record (at most kWaveRuns tile runs; extra
+// runs are merged with their neighbour, which only adds polls) and reach(T) = the furthest tile
+// any run of tiles <= T touches (a prefix maximum, so ready times stay monotone in T).
+void build_wave(mpkg_ctx_s* ctx, Executor& E) {
+    const uint32_t nt = E.n_tiles;
+    std::vector<uint32_t> rec((uint64_t)nt * 2 * kWaveRuns);
+    E.wave_reach.assign(nt, 0);
+    uint32_t reach = 0;
+    std::vector<std::pair<uint32_t, uint32_t>> runs;
+    for (uint32_t T = 0; T < nt; ++T) {
+        runs.clear();
+        for (uint32_t k = E.h_ptr[T]; k < E.h_ptr[T + 1]; ++k) runs.push_back({E.h_lo[k], E.h_hi[k]});
+        while (runs.size() > (size_t)kWaveRuns) {  // merge the pair with the smallest gap
+            size_t best = 0;
+            uint64_t gap = ~0ull;
+            for (size_t i = 0; i + 1 < runs.size(); ++i)
+                if ((uint64_t)runs[i + 1].first - runs[i].second < gap) gap = runs[i + 1].first - runs[i].second, best = i;
+            runs[best].second = std::max(runs[best].second, runs[best + 1].second);
+            runs.erase(runs.begin() + best + 1);
+        }
+        for (int j = 0; j < kWaveRuns; ++j) {
+            const bool used = j < (int)runs.size();
+            rec[(uint64_t)T * 2 * kWaveRuns + j] = used ? runs[j].first : 1u;
+            rec[(uint64_t)T * 2 * kWaveRuns + kWaveRuns + j] = used ? runs[j].second : 0u;  // empty: lo > hi
+            if (used) reach = std::max(reach, runs[j].second);
+        }
+        E.wave_reach[T] = std::max(reach, T);
+    }
+    E.wave_rec.alloc(std::max<size_t>(rec.size(), 1));
+    if (!rec.empty())
+        MPKG_CUDA(cudaMemcpyAsync(E.wave_rec.p, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// Ticket order of one pass over powers q0..q1: ready(T, q0) = T, ready(T, q) = ready(reach(T),
+// q-1) + slack (monotone in T, so each power's list is sorted and the pass is their merge, ties
+// broken by power then tile).  Returns the pass's live window: the most matrix + vector bytes of
+// tiles between their first and last ticket, at any point of the order.
+uint64_t wave_order(const Executor& E, int q0, int q1, int64_t slack, std::vector<uint32_t>* codes) {
+    const uint32_t nt = E.n_tiles;
+    const int np = q1 - q0 + 1;
+    std::vector<std::vector<int64_t>> rdy(np, std::vector<int64_t>(nt));
+    for (uint32_t T = 0; T < nt; ++T) rdy[0][T] = T;
+    for (int j = 1; j < np; ++j)
+        for (uint32_t T = 0; T < nt; ++T) rdy[j][T] = rdy[j - 1][E.wave_reach[T]] + slack;
+    std::vector<uint32_t> pos(np, 0);
+    std::vector<int64_t> diff;
+    diff.reserve((uint64_t)nt * np + 1);
+    int64_t cur = 0, peak = 0;
+    // live bytes: tile T enters at its q0 ticket and leaves after its q1 ticket
+    for (;;) {
+        int best = -1;
+        for (int j = np - 1; j >= 0; --j)  // ties: the higher power first (older front)
+            if (pos[j] < nt && (best < 0 || rdy[j][pos[j]] < rdy[best][pos[best]])) best = j;
+        if (best < 0) break;
+        const uint32_t T = pos[best]++;
+        const int q = q0 + best;
+        if (best == 0) cur += (int64_t)E.tile_bytes[T];
+        peak = std::max(peak, cur);
+        if (best == np - 1) cur -= (int64_t)E.tile_bytes[T];
+        if (codes) codes->push_back((q == q1 ? kLastUse : 0u) | ((uint32_t)q << 24) | T);
+    }
+    return (uint64_t)peak;
+}
+
+// Pass length p' = the longest pass whose live window fits the budget (0.6 x L2 unless the
+// l2_budget knob says otherwise; the "pass" knob forces p'); slack (ready-time units, ~p'
+// tickets each) = 1.25 x the warps in flight / p', so a ticket's dependencies have finished when
+// its warp reaches it.  Passes are balanced (ceil(p / p') of them).
+const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
+    auto it = E.wave.find(p);
+    if (it != E.wave.end()) return it->second;
+    Executor::Wave W;
+    const uint64_t budget = ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes * 6 / 10;
+    const int64_t warps = (int64_t)E.wave_grid * 8;
+    auto slack_for = [&](int len) -> int64_t {
+        if (ctx->slack >= 0) return std::max<int64_t>(ctx->slack, 1);
+        return std::max<int64_t>(1, (warps * 5 / 4 + len - 1) / len);
+    };
+    int P = std::min(p, kMaxFusedP);
+    if (ctx->pass_powers > 0) {
+        P = std::min<int>(p, (int)ctx->pass_powers);
+        W.window = wave_order(E, 1, P, slack_for(P), nullptr);
+    } else {
+        for (; P >= 1; --P) {
+            W.window = wave_order(E, 1, P, slack_for(P), nullptr);
+            if (P == 1 || W.window <= budget) break;
+        }
+    }
+    const int n_pass = (p + P - 1) / P;
+    std::vector<uint32_t> codes;
+    codes.reserve((uint64_t)E.n_tiles * p);
+    int q0 = 1;
+    W.t_begin.push_back(0);
+    for (int j = 0; j < n_pass; ++j) {
+        const int len = p / n_pass + (j < p % n_pass ? 1 : 0);
+        W.slack = slack_for(len);
+        wave_order(E, q0, q0 + len - 1, W.slack, &codes);
+        W.q_begin.push_back(q0);
+        q0 += len;
+        W.t_begin.push_back((uint32_t)codes.size());
+    }
+    W.q_begin.push_back(q0);
+    W.pass_len = (p + n_pass - 1) / n_pass;
+    W.tickets.alloc(std::max<size_t>(codes.size(), 1));
+    if (!codes.empty())
+        MPKG_CUDA(cudaMemcpyAsync(W.tickets.p, codes.data(), sizeof(uint32_t) * codes.size(),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    E.pass_len[p] = W.pass_len;
+    return E.wave.emplace(p, std::move(W)).first->second;
+}
+
+void* wave_fn(int kind, bool sigma) {
+    static void* const fns[6] = {(void*)k_mpk_wave<0, false>, (void*)k_mpk_wave<0, true>,
+                                 (void*)k_mpk_wave<1, false>, (void*)k_mpk_wave<1, true>,
+                                 (void*)k_mpk_wave<2, false>, (void*)k_mpk_wave<2, true>};
+    return fns[kind * 2 + (sigma ? 1 : 0)];
+}
+
 template <int KIND, int G>
 void launch_g(bool sigma, int grid, int threads, uint32_t smem, cudaStream_t st,
               const FusedParams& P) {
@@ -1783,6 +2099,7 @@ void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
 
 bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
     if (ctx->schedule == 1) return false;
+    if (ctx->schedule == 3 && E.h_tile_start.empty() && E.tile_rows == kWaveRows) return false;
     // Long rows live outside the SELL arrays.  Fast mode reduces them in k_coop_rows beside the
     // sweeps; bitwise mode adds them in stored order in k_long_rows_bitwise beside the sweeps
     // (R-MAT scale 21: 2.79 ms vs 2.93 ms for the fused kernel's CTA-cooperative path; both are
@@ -1795,9 +2112,22 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     Executor& E = get_executor(ctx, Pl, A);
     if (E.n_tiles == 0) return;
     const bool sweep = use_sweeps(ctx, E, a.p);
+    const bool wave = !sweep && ctx->schedule == 3;
     if (!sweep && !E.fused_ready) build_fused(ctx, Pl, A, &E);
+    if (wave && !E.wave_grid) {
+        int occ = 1 << 30;
+        for (int k = 0; k < 6; ++k) {
+            int o = 0;
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wave_fn(k / 2, k % 2), 256, 0));
+            occ = std::min(occ, o);
+        }
+        if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
+        E.wave_grid = std::max(1, occ) * ctx->sm_count;
+        build_wave(ctx, E);
+    }
     static const DevBuf<uint32_t> no_tickets;
-    const DevBuf<uint32_t>& tk = sweep ? no_tickets : get_tickets(ctx, E, a.p);
+    const Executor::Wave* W = wave ? &get_wave(ctx, E, a.p) : nullptr;
+    const DevBuf<uint32_t>& tk = sweep ? no_tickets : wave ? W->tickets : get_tickets(ctx, E, a.p);
     const Sell& S = *E.S;
     cudaStream_t st = ctx->stream;
     const bool sigma = E.order >= 1;  // any private order (CM or length-sorted)
@@ -1895,6 +2225,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     }
     const uint32_t smem = E.stages * E.buf_bytes;
     E.last_sweep = sweep;
+    E.last_wave = wave;
     const int sv = (int)ctx->sweep_variant;
     // One power of the sweep schedule.  A_perm order with plain or shifted powers and no long
     // rows is exactly the baseline's row kernel (k_spmv_sell, fewest instructions per row); every
@@ -2103,6 +2434,30 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             launch_all();
         }
         ctx->launches += (uint64_t)a.p * per_power - 1;  // kernels the step ran
+    } else if (wave) {
+        // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
+        // host block, the pass's slices go to the host while the next pass runs
+        void* fn = wave_fn(a.kind, sigma);
+        P.dep_lo = E.wave_rec.p;  // per-tile dependency records (build_wave)
+        for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
+            uint32_t t0 = W->t_begin[j], t1 = W->t_begin[j + 1], q0 = (uint32_t)W->q_begin[j];
+            const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(E.wave_grid, (t1 - t0 + 7) / 8));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(g);
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            void* args[] = {(void*)&P, (void*)&t0, (void*)&t1, (void*)&q0};
+            MPKG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+            if (j + 2 < W->t_begin.size()) ctx->launches += 1;
+            if (to_host)
+                for (int q = W->q_begin[j]; q < W->q_begin[j + 1]; ++q) copy_slice((uint32_t)q);
+        }
+        if (to_host) join_copies();
     } else if (E.kernel == 4) {
         const int nt = (int)E.threads;
         const uint32_t sm = E.stages * E.buf_bytes;
@@ -2140,7 +2495,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     MPKG_LAUNCH_CHECK();
     timing_end(ctx, ev);
     ctx->launches += 1;
-    if (to_host && !(sweep && to_host)) {  // fused kernel or graph replay: one copy at the end
+    if (to_host && !sweep && !wave) {  // fused kernel: one copy at the end
         for (uint32_t q = 1; q <= (uint32_t)a.p; ++q) copy_slice(q);
         join_copies();
     }
@@ -2165,7 +2520,7 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
 void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows) {
     const Executor* E = P->exec.get();
     if (order) *order = E ? E->order : -1;
-    if (sweeps) *sweeps = E ? (int)E->last_sweep : 0;
+    if (sweeps) *sweeps = E ? (E->last_sweep ? 1 : E->last_wave ? 2 : 0) : 0;
     if (kernel) *kernel = E ? E->kernel : -1;
     if (long_rows) *long_rows = E ? E->long_rows : 0;
 }

@@ -170,10 +170,15 @@ def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
 
 
 DEFAULT_KNOBS = {"order": -1, "slack": -1, "schedule": 0, "kernel": 0, "tile_rows": 128,
-                 "producers": 0, "cgroups": 0, "stages": 0}
+                 "producers": 0, "cgroups": 0, "stages": 0, "pass": 0, "l2_budget": 0, "ctas_per_sm": 0}
 
 SCHEDULES = {
     "sweeps": {"schedule": 2},
+    "wave": {"schedule": 3},
+    "wave-1cta": {"schedule": 3, "ctas_per_sm": 1},
+    "wave-pass1": {"schedule": 3, "pass": 1},
+    "wave-pass2-slack1": {"schedule": 3, "pass": 2, "slack": 1},
+    "wave-pass6-tiny-budget": {"schedule": 3, "pass": 6, "slack": 0, "l2_budget": 4096},
     "fused-lean": {"schedule": 1},
     "fused-lean-slack0": {"schedule": 1, "slack": 0},
     "fused-lean-slack1": {"schedule": 1, "slack": 1},
@@ -211,7 +216,9 @@ def test_orders_and_schedules(ctx, cases, oracle, order, sched):
             assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} {sched} order={order}")
             info = plan.exec_info()
             assert info["order"] == order
-            assert info["schedule"] == ("sweeps" if sched == "sweeps" else "fused")
+            want = ("sweeps" if sched == "sweeps" else
+                    ("sweeps" if info["long_rows"] else "wave") if sched.startswith("wave") else "fused")
+            assert info["schedule"] == want
             sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0, 3.0, 0.25]
             ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
             assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, f"{name} shifted")
