@@ -132,6 +132,7 @@ struct Executor {
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
     std::vector<uint32_t> wave_reach;         // per tile: furthest tile read by tiles <= T
+    uint64_t wave_dep_tiles = 0;              // tiles polled per power, summed over tiles
     DevBuf<uint32_t> wave_rec;                // per tile: kWaveRuns dependency runs (lo[], hi[])
     int64_t sched_knob = 0;
     DevBuf<double> coop_part;
@@ -1903,38 +1904,113 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.tickets.emplace(p, std::move(d)).first->second;
 }
 
-// Wave schedule, host side.  Per tile: the dependency record (at most kWaveRuns tile runs; extra
-// runs are merged with their neighbour, which only adds polls) and reach(T) = the furthest tile
-// any run of tiles <= T touches (a prefix maximum, so ready times stay monotone in T).
-void build_wave(mpkg_ctx_s* ctx, Executor& E) {
+// Wave schedule, host side.  Dependency runs of a 32-slot tile, from six buckets: (row level -
+// tile's first level in {0, >=1}) x (column level - row level in {-1, 0, +1}), each the min / max
+// tile its columns fall in.  A tile straddling a level boundary would otherwise hull the end of
+// level l (its own rows) with the start of level l (read by its level-(l+1) rows) into one run a
+// whole level long; split this way each bucket is compact.  Runs are merged when they touch and
+// then down to kWaveRuns by closing the smallest gaps (only extra polls, never a missed tile).
+// reach(T) = the furthest tile any run of tiles <= T touches (a prefix maximum, so ready times
+// stay monotone in T).
+constexpr int kWaveBuckets = 6;
+
+__global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci, uint32_t n,
+                               const uint32_t* __restrict__ slot_row, const uint32_t* __restrict__ pos,
+                               const uint32_t* __restrict__ lp, uint32_t nl, uint32_t n_slots,
+                               uint32_t* __restrict__ bmin, uint32_t* __restrict__ bmax) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = slot_row ? slot_row[s] : (uint32_t)s;
+        if (r >= n) continue;
+        const uint32_t T = (uint32_t)(s / kWaveRows);
+        const uint32_t lt = level_of(lp, nl, T * kWaveRows);
+        const uint32_t L = level_of(lp, nl, (uint32_t)s);
+        const uint32_t rb = L > lt ? 1u : 0u;
+        const uint32_t lb = lp[L], le = lp[L + 1];
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const uint32_t c = ci[k];
+            const uint32_t d = c < lb ? 0u : (c >= le ? 2u : 1u);
+            const uint32_t tc = (pos ? pos[c] : c) / kWaveRows;
+            atomicMin(bmin + (uint64_t)T * kWaveBuckets + rb * 3 + d, tc);
+            atomicMax(bmax + (uint64_t)T * kWaveBuckets + rb * 3 + d, tc);
+        }
+    }
+}
+
+void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
+    cudaStream_t st = ctx->stream;
     const uint32_t nt = E.n_tiles;
+    {  // matrix + vector bytes one tile-power touches (the live-window model of wave_order)
+        std::vector<uint64_t> off(E.S->n_chunks + 1);
+        MPKG_CUDA(cudaMemcpyAsync(off.data(), E.S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
+        MPKG_CUDA(cudaStreamSynchronize(st));
+        E.tile_bytes.assign(nt, 0);
+        for (uint32_t T = 0; T < nt && T < E.S->n_chunks; ++T)
+            E.tile_bytes[T] = 12 * (off[T + 1] - off[T]) + 24ull * kWaveRows;
+    }
+    std::vector<uint32_t> lp = Pl->level_ptr;
+    if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
+    const uint32_t nl = (uint32_t)lp.size() - 1;
+    DevBuf<uint32_t> d_lp(lp.size()), bmin((uint64_t)nt * kWaveBuckets), bmax((uint64_t)nt * kWaveBuckets);
+    MPKG_CUDA(cudaMemcpyAsync(d_lp.p, lp.data(), 4 * lp.size(), cudaMemcpyHostToDevice, st));
+    MPKG_CUDA(cudaMemsetAsync(bmin.p, 0xff, bmin.bytes(), st));
+    MPKG_CUDA(cudaMemsetAsync(bmax.p, 0, bmax.bytes(), st));
+    if (nt) {
+        k_wave_buckets<<<grid_for(E.n_slots, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+            A->row_ptr.p, A->col_idx.p, A->n_rows, E.order ? E.slot_row.p : nullptr,
+            E.order ? E.pos.p : nullptr, d_lp.p, nl, E.n_slots, bmin.p, bmax.p);
+        MPKG_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    std::vector<uint32_t> hmin((uint64_t)nt * kWaveBuckets), hmax((uint64_t)nt * kWaveBuckets);
+    MPKG_CUDA(cudaMemcpyAsync(hmin.data(), bmin.p, bmin.bytes(), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaMemcpyAsync(hmax.data(), bmax.p, bmax.bytes(), cudaMemcpyDeviceToHost, st));
+    MPKG_CUDA(cudaStreamSynchronize(st));
     std::vector<uint32_t> rec((uint64_t)nt * 2 * kWaveRuns);
     E.wave_reach.assign(nt, 0);
+    E.wave_dep_tiles = 0;
     uint32_t reach = 0;
-    std::vector<std::pair<uint32_t, uint32_t>> runs;
+    std::vector<std::pair<uint32_t, uint32_t>> runs, merged;
     for (uint32_t T = 0; T < nt; ++T) {
         runs.clear();
-        for (uint32_t k = E.h_ptr[T]; k < E.h_ptr[T + 1]; ++k) runs.push_back({E.h_lo[k], E.h_hi[k]});
-        while (runs.size() > (size_t)kWaveRuns) {  // merge the pair with the smallest gap
+        runs.push_back({T, T});
+        for (int b = 0; b < kWaveBuckets; ++b) {
+            const uint64_t i = (uint64_t)T * kWaveBuckets + b;
+            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i], hmax[i]});
+        }
+        std::sort(runs.begin(), runs.end());
+        merged.clear();
+        for (const auto& rr : runs) {
+            if (!merged.empty() && rr.first <= merged.back().second + 1)
+                merged.back().second = std::max(merged.back().second, rr.second);
+            else
+                merged.push_back(rr);
+        }
+        while (merged.size() > (size_t)kWaveRuns) {  // close the smallest gap
             size_t best = 0;
             uint64_t gap = ~0ull;
-            for (size_t i = 0; i + 1 < runs.size(); ++i)
-                if ((uint64_t)runs[i + 1].first - runs[i].second < gap) gap = runs[i + 1].first - runs[i].second, best = i;
-            runs[best].second = std::max(runs[best].second, runs[best + 1].second);
-            runs.erase(runs.begin() + best + 1);
+            for (size_t i = 0; i + 1 < merged.size(); ++i)
+                if ((uint64_t)merged[i + 1].first - merged[i].second < gap)
+                    gap = merged[i + 1].first - merged[i].second, best = i;
+            merged[best].second = std::max(merged[best].second, merged[best + 1].second);
+            merged.erase(merged.begin() + best + 1);
         }
         for (int j = 0; j < kWaveRuns; ++j) {
-            const bool used = j < (int)runs.size();
-            rec[(uint64_t)T * 2 * kWaveRuns + j] = used ? runs[j].first : 1u;
-            rec[(uint64_t)T * 2 * kWaveRuns + kWaveRuns + j] = used ? runs[j].second : 0u;  // empty: lo > hi
-            if (used) reach = std::max(reach, runs[j].second);
+            const bool used = j < (int)merged.size();
+            rec[(uint64_t)T * 2 * kWaveRuns + j] = used ? merged[j].first : 1u;
+            rec[(uint64_t)T * 2 * kWaveRuns + kWaveRuns + j] = used ? merged[j].second : 0u;  // empty: lo > hi
+            if (used) {
+                reach = std::max(reach, merged[j].second);
+                E.wave_dep_tiles += merged[j].second - merged[j].first + 1;
+            }
         }
         E.wave_reach[T] = std::max(reach, T);
     }
     E.wave_rec.alloc(std::max<size_t>(rec.size(), 1));
     if (!rec.empty())
-        MPKG_CUDA(cudaMemcpyAsync(E.wave_rec.p, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice, ctx->stream));
-    MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
+        MPKG_CUDA(cudaMemcpyAsync(E.wave_rec.p, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice, st));
+    E.done.alloc(std::max<uint32_t>(nt, 1));
+    MPKG_CUDA(cudaStreamSynchronize(st));
 }
 
 // Ticket order of one pass over powers q0..q1: ready(T, q0) = T, ready(T, q) = ready(reach(T),
@@ -2113,7 +2189,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (E.n_tiles == 0) return;
     const bool sweep = use_sweeps(ctx, E, a.p);
     const bool wave = !sweep && ctx->schedule == 3;
-    if (!sweep && !E.fused_ready) build_fused(ctx, Pl, A, &E);
+    if (!sweep && !wave && !E.fused_ready) build_fused(ctx, Pl, A, &E);
     if (wave && !E.wave_grid) {
         int occ = 1 << 30;
         for (int k = 0; k < 6; ++k) {
@@ -2123,7 +2199,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         }
         if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
         E.wave_grid = std::max(1, occ) * ctx->sm_count;
-        build_wave(ctx, E);
+        build_wave(ctx, Pl, A, E);
     }
     static const DevBuf<uint32_t> no_tickets;
     const Executor::Wave* W = wave ? &get_wave(ctx, E, a.p) : nullptr;
@@ -2181,7 +2257,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.n_prod = E.n_prod;
     P.n_cgroups = E.n_cgroups;
     P.n_sb = (E.n_tiles + kSB - 1) / kSB;
-    if (!sweep) {
+    if (!sweep && !wave) {
         E.sb_count.ensure((uint64_t)(kMaxFusedP + 1) * P.n_sb + 1);
         P.sb_count = E.sb_count.p;
         MPKG_CUDA(cudaMemsetAsync(E.sb_count.p, 0, 4ull * (a.p + 1) * P.n_sb, st));
@@ -2221,7 +2297,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     for (int i = 0; i <= a.p; ++i) P.coef[i] = a.coef ? a.coef[i] : 0.0;
     if (!sweep) {
         MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
-        MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
+        if (!wave) MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     }
     const uint32_t smem = E.stages * E.buf_bytes;
     E.last_sweep = sweep;
@@ -2510,6 +2586,10 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
         for (const auto& kv : P->exec->tickets) k = std::max<uint64_t>(k, kv.second.n);
         for (const auto& kv : P->exec->pass_len) pp = (uint32_t)kv.second;
         for (size_t i = 0; i < P->exec->h_lo.size(); ++i) d += P->exec->h_hi[i] - P->exec->h_lo[i] + 1;
+        if (P->exec->last_wave) {
+            d = P->exec->wave_dep_tiles;
+            for (const auto& kv : P->exec->wave) k = std::max<uint64_t>(k, kv.second.tickets.n);
+        }
     }
     if (n_tiles) *n_tiles = t;
     if (n_tickets) *n_tickets = k;
