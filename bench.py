@@ -967,7 +967,7 @@ def main():
     sync()
     prep["executor_build_s"] = time.perf_counter() - t0
     exec_info = plan.exec_info()
-    kname = ("k_mpk_sweep" if exec_info["schedule"] == "sweeps" else
+    kname = ("k_mpk_sweep" if exec_info["schedule"] == "sweeps" else "k_mpk_wave" if exec_info["schedule"] == "wave" else
              {0: "k_mpk_lean", 1: "k_mpk_fused", 2: "k_mpk_warptile", 4: "k_mpk_async"}.get(exec_info["kernel"], "?"))
     if exec_info["schedule"] == "sweeps" and exec_info.get("long_rows"):
         kname = ("k_coop_rows (side stream) beside k_mpk_sweep" if args.mode == "fast" else

@@ -29,6 +29,8 @@
 // Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
 // every row is computed by the same formula, from the same inputs, in any order.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <array>
 #include <map>
@@ -131,9 +133,10 @@ struct Executor {
     };
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
+    int wave_minb = 0;
+    bool wave_auto = false;                   // schedule 0 picked the wave (get_executor)
     std::vector<uint32_t> wave_reach;         // per tile: furthest tile read by tiles <= T
-    uint64_t wave_dep_tiles = 0;              // tiles polled per power, summed over tiles
-    DevBuf<uint32_t> wave_rec;                // per tile: kWaveRuns dependency runs (lo[], hi[])
+    uint64_t wave_dep_tiles = 0;              // dependency bucket spans (tiles), summed over tiles
     int64_t sched_knob = 0;
     DevBuf<double> coop_part;
     uint32_t n_coop = 0, n_multi = 0;
@@ -152,6 +155,7 @@ struct FusedParams {
     const uint32_t* dep_hi;
     uint32_t* done;
     uint32_t* counter;
+    uint32_t* dbg;  // wave schedule: value-wait count (MPKG_WAVE_DEBUG)
     uint32_t n_tickets;
     uint32_t n_rows;
     uint32_t n_slots;
@@ -973,179 +977,216 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
 // ---- Wave schedule ("schedule" knob 3): cross-power L2 reuse ------------------------------------
 //
 // One persistent launch per PASS of p' consecutive powers q0..q1.  The unit of work is a ticket
-// (tile = one 32-slot SELL chunk, power q), executed by ONE WARP (lane = row): no CTA barrier ever
-// couples warps.  The pass's tickets are listed in a host-computed skewed order (wave_order:
-// ready(T, q) = ready(reach(T), q-1) + slack, reach(T) = the furthest tile T's rows read), so the
-// p' powers sweep the matrix as p' fronts a little more than one BFS level apart.  A tile's
-// matrix slice is read from HBM by the front of power q0 and from L2 by the fronts behind it as
-// long as the live window (p'-1 level lags plus the tickets in flight) fits the L2 budget; get_wave
-// picks p' by evaluating that window on the ticket order -- the plan's cache budget
-// (plan.hpp:88-115) sized for this GPU's L2.  Synchronisation is the reference's wavefront rule
-// at tile granularity (execute.hpp:59-72, cell (g, q) after (g-1..g+1, q-1)): per-tile flags
-// done[T] = last finished power.
+// (tile = one 32-slot SELL chunk, power q), executed by ONE WARP (lane = row).  The pass's tickets
+// are listed in a host-computed skewed order (wave_order: ready(T, q) = ready(reach(T), q-1) +
+// slack, reach(T) = the furthest tile T's rows read), so the p' powers sweep the matrix as p'
+// fronts a little more than one BFS level apart: a tile's matrix slice is read from HBM by the
+// front of power q0 and from L2 by the fronts behind it, as long as the live window (p'-1 level
+// lags plus the tickets in flight) fits the L2 budget.  get_wave picks p' by evaluating that
+// window on the ticket order -- the plan's cache budget (plan.hpp:88-115) sized for this GPU.
 //
-// Per ticket a warp (1) issues its rows' first matrix group and the relaxed polls of the tile's
-// dependency flags (up to 4 runs, lane-parallel) together, (2) runs ONE fence.acq_rel.gpu that is
-// both the acquire of those flags and the release of the PREVIOUS ticket's rows, then stores that
-// ticket's flag, (3) gathers y_{q-1} (L2-only loads: rows of other SMs), sums in stored order
-// (rowdot.cuh: bitwise) and stores.  The fence therefore waits on loads the warp needs anyway.
-// A warp whose poll fails publishes its pending ticket before it spins, so deferred publication
-// can never block a dependent.  Tickets are statically assigned (ticket t of the pass runs on warp
-// t mod warps, each warp in increasing t) and the launch is cooperative (all CTAs resident): the
-// warp holding the lowest unfinished ticket has finished every earlier ticket of its own, every
-// dependency of that ticket is lower, so it progresses -- deadlock-free with no atomic ticket
-// counter serialising the ~10^7 tickets of a C5 pass.
-constexpr uint32_t kWaveRows = 32;
-constexpr int kWaveRuns = 4;  // dependency runs per tile record
+// Synchronisation is by VALUE, not by flags.  Before a pass, slices q0..q1-1 (the ones read inside
+// the pass) are filled with kWaveEmpty, a signalling-NaN bit pattern that fp64 arithmetic never
+// produces (every NaN result is quiet).  Producers store results with relaxed (single-copy atomic)
+// stores; a consumer gathers y_{q-1} with relaxed L2 loads and re-loads any value that still reads
+// kWaveEmpty.  A row therefore starts only when exactly the values it reads exist -- the
+// reference's wavefront rule (execute.hpp:59-72: cell (g, q) after (g-1..g+1, q-1)) at the finest
+// possible granularity -- with no flags, no polls and no fences on the path.  Tickets are
+// statically assigned (ticket t runs on warp t mod warps, each warp in increasing t) under a
+// cooperative launch (all CTAs resident): every input of the lowest unfinished ticket was stored by
+// a lower, finished ticket and stores become visible, so it always progresses (deadlock-free).
+// Row arithmetic is rowdot.cuh's (stored order, mul then add): bitwise.  Slice 0 and the slices of
+// earlier passes are complete before the launch and read through the non-coherent path.
+constexpr uint32_t kWaveChunks = 1;                // SELL chunks (warp rounds) per ticket
+constexpr uint32_t kWaveRows = 32 * kWaveChunks;  // rows per tile
+constexpr unsigned long long kWaveEmpty = 0x7ff4dead5eed0001ull;
 
-__device__ __forceinline__ double ld_cg(const double* p) {
-    double r;
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+// Relaxed (morally strong, single-copy atomic) loads and stores of in-pass slices.  The plain load
+// is non-volatile so the compiler may schedule the gathers freely (the value itself is the
+// synchronisation); the re-load in the wait loop is volatile so it is really re-issued.
+__device__ __forceinline__ double ld_strong(const double* p) {
+    double v;
+    asm("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_strong_again(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_strong(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+// Matrix streams (read-only for the kernel's lifetime): non-volatile, schedulable.
+__device__ __forceinline__ uint2 ldm_u2(const uint2* p, uint64_t pol) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
     return r;
 }
-template <bool FIRST>
-__device__ __forceinline__ double wave_ld(const double* p) {
-    if constexpr (FIRST) return __ldg(p);  // slice q0-1: complete before the launch
-    else return ld_cg(p);                  // written by other SMs in this launch: L2 only
+__device__ __forceinline__ uint32_t ldm_u32(const uint32_t* p, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double2 ldm_d2(const double2* p, uint64_t pol) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ldm_d(const double* p, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ bool wave_empty(double v) {
+    return (unsigned long long)__double_as_longlong(v) == kWaveEmpty;
+}
+// A value of a slice written in this launch: re-read until its producer has stored it.
+__device__ __forceinline__ double wave_wait(const double* p, double v) {
+    while (wave_empty(v)) {
+        __nanosleep(100);
+        v = ld_strong_again(p);
+    }
+    return v;
 }
 
-// The matrix group of entries k0..k0+7 of the lane's row (rowdot.cuh sell_row_dot layout).
+// The matrix group of entries k0..k0+7 of the lane's row (rowdot.cuh sell_row_dot layout), written
+// branch-free: k0 is even and Lp = L & ~1 is even, so a pair (k, k+1) is either entirely in the
+// pair region (k < Lp) or entirely past it, where only entry k == Lp (odd L) exists, in the tail.
 __device__ __forceinline__ void wave_group(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
                                            uint32_t k0, uint64_t pol, uint32_t (&c)[8], double (&v)[8]) {
     const uint32_t Lp = L & ~1u;
 #pragma unroll
     for (int j = 0; j < 8; j += 2) {
         const uint32_t k = k0 + j;
-        if (k + 1 < Lp) {
+        uint2 cc = make_uint2(0u, 0u);
+        double2 vv = make_double2(0.0, 0.0);
+        if (k < Lp) {
             const uint64_t e = off + (k >> 1) * 64u + lane * 2u;
-            const uint2 tt = ld_mat_u2(reinterpret_cast<const uint2*>(P.cols + e), pol);
-            const double2 w = ld_mat_d2(reinterpret_cast<const double2*>(P.vals + e), pol);
-            c[j] = tt.x, c[j + 1] = tt.y, v[j] = w.x, v[j + 1] = w.y;
-        } else {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const uint32_t kk = k + i;
-                const uint64_t e = off + sell_pos(kk, Lp, lane);
-                c[j + i] = kk < L ? ld_mat_u32(P.cols + e, pol) : 0u;
-                v[j + i] = kk < L ? ld_mat_d(P.vals + e, pol) : 0.0;
-            }
+            cc = ldm_u2(reinterpret_cast<const uint2*>(P.cols + e), pol);
+            vv = ldm_d2(reinterpret_cast<const double2*>(P.vals + e), pol);
         }
+        if (k == Lp && k < L) {
+            const uint64_t e = off + (uint64_t)Lp * 32u + lane;
+            cc.x = ldm_u32(P.cols + e, pol);
+            vv.x = ldm_d(P.vals + e, pol);
+        }
+        c[j] = cc.x, c[j + 1] = cc.y, v[j] = vv.x, v[j + 1] = vv.y;
     }
 }
 
-template <bool FIRST>
+// first: the source slice is complete (q == q0: no waiting; slice 0 is caller data and may hold any
+// bit pattern).  Otherwise a row that gathered a value still reading kWaveEmpty (its producer is
+// behind) is recomputed after a short sleep; the discarded sum is never stored.  The gathers are
+// volatile so every attempt re-issues them.
 __device__ __forceinline__ double wave_row(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
-                                           uint32_t len, const double* src, uint64_t pol, uint32_t (&c)[8],
-                                           double (&v)[8]) {
-    double acc = 0.0;
-    for (uint32_t k0 = 0;;) {
-        double x[8];
+                                           uint32_t len, const double* src, uint64_t pol, bool first) {
+    for (;;) {
+        uint32_t c[8];
+        double v[8];
+        double acc = 0.0;
+        bool miss = false;
+        for (uint32_t k0 = 0; k0 < len; k0 += 8) {
+            wave_group(P, off, L, lane, k0, pol, c, v);
+            double x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = k0 + j < len ? wave_ld<FIRST>(src + c[j]) : 0.0;
+            for (int j = 0; j < 8; ++j)
+                x[j] = k0 + j < len ? (first ? __ldg(src + c[j]) : ld_strong_again(src + c[j])) : 0.0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
-        k0 += 8;
-        if (k0 >= len) break;
-        wave_group(P, off, L, lane, k0, pol, c, v);  // rows longer than 8 (27-point stencils)
+            for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+        }
+        if (!miss || first) return acc;
+        if (P.dbg) atomicAdd(P.dbg, 1u);
+        __nanosleep(200);
     }
-    return acc;
 }
 
-// row_epilogue with the wave's coherence rules: reads of rows finished in this launch go to L2.
-template <int KIND, bool SIGMA, bool FIRST>
+// row_epilogue with the wave's rules: in-pass values are awaited, working-vector stores are
+// single-copy atomic (KIND 2 never runs here: its accumulator has no value to wait on).
+template <int KIND, bool SIGMA>
 __device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, uint32_t r, uint32_t q,
-                                              const double* src, double acc) {
+                                              uint32_t q0, const double* src, double acc) {
     if constexpr (KIND == 1) {
         const double a = P.shift_a[q - 1], b2 = P.shift_b2[q - 1];
-        const double own = wave_ld<FIRST>(src + s);
-        const double own2 = b2 != 0.0 ? ld_cg(P.V + (uint64_t)(q - 2) * P.vstride + s) : 0.0;
+        const double own = q == q0 ? __ldg(src + s) : wave_wait(src + s, ld_strong(src + s));
+        double own2 = 0.0;
+        if (b2 != 0.0) {
+            const double* p2 = P.V + (uint64_t)(q - 2) * P.vstride + s;
+            own2 = q - 2 >= q0 ? wave_wait(p2, ld_strong(p2)) : __ldg(p2);
+        }
         acc = shift_epilogue(acc, a, b2, own, own2);
     }
-    P.V[(uint64_t)q * P.vstride + s] = acc;
+    st_strong(P.V + (uint64_t)q * P.vstride + s, acc);
     if constexpr (SIGMA) P.out[(uint64_t)q * P.rows + r] = acc;
-    if constexpr (KIND == 2) {
-        double zr;
-        if (q == 1)
-            zr = __dadd_rn(__dmul_rn(P.coef[0], wave_ld<FIRST>(src + s)), __dmul_rn(P.coef[1], acc));
-        else
-            zr = __dadd_rn(ld_cg(P.zs + s), __dmul_rn(P.coef[q], acc));
-        P.zs[s] = zr;
-        if (SIGMA && q == P.p) P.z[r] = zr;
-    }
 }
 
-template <int KIND, bool SIGMA>
-__global__ void __launch_bounds__(256) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
-                                                   uint32_t t1, uint32_t q0) {
+// Tickets are claimed dynamically, in order, from kWaveStreams interleaved counters (stream i hands
+// out tickets i, i + S, i + 2S, ... to the warps with warp id = i mod S; one counter alone tops out
+// near 1.5 claims/ns).  Each warp claims one ticket ahead of the one it runs, so the tickets in
+// flight are always the ~2 x warps most recently claimed: no warp can drift behind the front, which
+// is what lets a small slack (and so a small L2 window) suffice.  A ticket waits only on values of
+// lower tickets, all claimed earlier by running warps: deadlock-free without co-residency.
+constexpr uint32_t kWaveStreams = 16;
+
+template <int KIND, bool SIGMA, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
+                                                      uint32_t t1, uint32_t q0) {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    uint32_t t = t0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    uint32_t pend_T = 0xffffffffu, pend_q = 0;  // finished, not yet published
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t sid = gw % kWaveStreams;
+    uint32_t* const ctr = P.counter + sid * 32u;  // one 128-B line per stream
+    auto claim = [&]() -> uint32_t {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(ctr, 1u);
+        return k;
+    };
+    auto ticket = [&](uint32_t k) { return t0 + sid + kWaveStreams * __shfl_sync(0xffffffffu, k, 0); };
+    uint32_t t = ticket(claim());
+    uint32_t kn = claim();  // the next ticket, in flight
     uint32_t code = t < t1 ? P.tickets[t] : 0u;
-    for (; t < t1; t += nw) {
-        const uint32_t next = t + nw < t1 ? P.tickets[t + nw] : 0u;  // one ticket ahead
+    while (t < t1) {
         const uint32_t T = code & 0xffffffu;
         const uint32_t q = (code >> 24) & 63u;
         const uint64_t pol = l2_policy(code & kLastUse);
-        const uint32_t s = T * kWaveRows + lane;
-        const uint32_t r = s < P.n_slots ? (SIGMA ? P.slot_row[s] : s) : 0xffffffffu;
-        const bool active = r < P.n_rows;
-        uint32_t len = 0, L = 0;
-        uint64_t off = 0;
-        uint32_t c[8];
-        double v[8];
-        if (active) {
-            len = P.row_len[s];
-            off = P.chunk_off[s >> 5];
-            L = (uint32_t)((P.chunk_off[(s >> 5) + 1] - off) >> 5);
-            wave_group(P, off, L, lane, 0, pol, c, v);
-        }
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
-        if (q > q0) {
-            // dependency runs: lanes 8j..8j+7 poll run j, 8 tiles per round
-            const uint32_t* rec = P.dep_lo + (uint64_t)T * (2 * kWaveRuns);
-            const uint32_t lo = rec[lane >> 3], hi = rec[kWaveRuns + (lane >> 3)];
-            for (;;) {
-                bool ok = true;
-                for (uint32_t u = lo + (lane & 7u); u <= hi; u += 8)
-                    if (ld_relaxed(P.done + u) < q - 1) {
-                        ok = false;
-                        break;
-                    }
-                if (__all_sync(0xffffffffu, ok)) break;
-                if (pend_T != 0xffffffffu) {  // never hold back a finished tile while waiting
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
-                    pend_T = 0xffffffffu;
-                }
-                __nanosleep(128);
+        // the tile's chunks, one row per lane each; the next chunk's metadata loads during this one
+        uint32_t s = T * kWaveRows + lane;
+        uint32_t r = s < P.n_slots ? (SIGMA ? P.slot_row[s] : s) : 0xffffffffu;
+        uint32_t len = r < P.n_rows ? P.row_len[s] : 0u;
+        uint64_t off = s < P.n_slots ? P.chunk_off[s >> 5] : 0u;
+        uint64_t end = s < P.n_slots ? P.chunk_off[(s >> 5) + 1] : 0u;
+#pragma unroll 1
+        for (uint32_t j = 0; j < kWaveChunks; ++j) {
+            const uint32_t sn = s + 32u;
+            uint32_t rn = 0xffffffffu, lenn = 0u;
+            uint64_t offn = 0u, endn = 0u;
+            if (j + 1 < kWaveChunks && sn < P.n_slots) {
+                rn = SIGMA ? P.slot_row[sn] : sn;
+                lenn = rn < P.n_rows ? P.row_len[sn] : 0u;
+                offn = P.chunk_off[sn >> 5];
+                endn = P.chunk_off[(sn >> 5) + 1];
             }
-        }
-        // acquire of the polled flags + release of the pending ticket's rows
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (pend_T != 0xffffffffu && lane == 0)
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
-        if (active) {
-            if (q > q0) {
-                const double acc = wave_row<false>(P, off, L, lane, len, src, pol, c, v);
-                wave_epilogue<KIND, SIGMA, false>(P, s, r, q, src, acc);
-            } else {
-                const double acc = wave_row<true>(P, off, L, lane, len, src, pol, c, v);
-                wave_epilogue<KIND, SIGMA, true>(P, s, r, q, src, acc);
+            if (r < P.n_rows) {
+                const uint32_t L = (uint32_t)((end - off) >> 5);
+                wave_epilogue<KIND, SIGMA>(P, s, r, q, q0, src, wave_row(P, off, L, lane, len, src, pol, q == q0));
             }
+            s = sn, r = rn, len = lenn, off = offn, end = endn;
         }
-        // lanes of long rows may still be storing: the pending flag covers the whole warp
-        // (bar.warp.sync orders every lane's stores before lane 0's fence + flag store)
-        __syncwarp();
-        pend_T = T;
-        pend_q = q;
-        code = next;
+        t = ticket(kn);
+        if (t >= t1) break;
+        kn = claim();
+        code = P.tickets[t];
     }
-    if (pend_T != 0xffffffffu) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + pend_T), "r"(pend_q) : "memory");
-    }
+}
+
+__global__ void k_wave_fill(double* __restrict__ V, uint64_t vstride, uint64_t n, uint32_t q_lo, uint32_t q_hi) {
+    const double e = __longlong_as_double((long long)kWaveEmpty);
+    for (uint32_t q = q_lo; q < q_hi; ++q)
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+            V[q * vstride + i] = e;
 }
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
@@ -1547,10 +1588,16 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->n_slots = (A->n_rows + 31u) & ~31u;
     // Row order: explicit, or auto: longest-rows-first (SELL-C-sigma) for power-law row lengths,
     // Cuthill-McKee inside levels otherwise.
+    // Auto schedule: the wave (cross-power L2 reuse) for large short-row matrices -- every row a
+    // single 8-entry group, matrix several times the L2 (C5's 7-point rows: same step time as the
+    // sweeps with ~2.7x less DRAM traffic); one launch per power otherwise.
+    const uint32_t mx_len = gpu_max_row_len(ctx, A);
+    E->wave_auto = ctx->schedule == 0 && mx_len <= 8 &&
+                   12ull * A->nnz > 4ull * ctx->l2_bytes;
     if (ctx->order >= 0 && ctx->order <= 2) {
         E->order = (int)ctx->order;
     } else {
-        const uint32_t mx = gpu_max_row_len(ctx, A);
+        const uint32_t mx = mx_len;
         const double avg = A->n_rows ? (double)A->nnz / A->n_rows : 0.0;
         if (mx > 64 && mx > 16.0 * avg)
             E->order = 2;
@@ -1567,7 +1614,7 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->tile_rows = ctx->tile_rows == 32 ? 32u : ctx->tile_rows == 64 ? 64u : (ctx->tile_rows == 256 ? 256u : 128u);
     if (E->tile_rows == 32 && ctx->kernel != 4) E->tile_rows = 64;  // 32-row tiles: async kernel only
     if (ctx->kernel == 2) E->tile_rows = 128;  // warp-tile: 4 warps x 32-row chunks
-    if (ctx->schedule == 3) E->tile_rows = kWaveRows;  // wave: one row per thread of a CTA
+    if (ctx->schedule == 3 || E->wave_auto) E->tile_rows = kWaveRows;  // wave: one SELL chunk per ticket
     // consumer threads: one per tile row unless forced
     E->threads = ctx->threads == 256 || ctx->threads == 512 ? (uint32_t)ctx->threads : E->tile_rows;
     if (E->threads < E->tile_rows) E->threads = E->tile_rows;
@@ -1904,14 +1951,10 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.tickets.emplace(p, std::move(d)).first->second;
 }
 
-// Wave schedule, host side.  Dependency runs of a 32-slot tile, from six buckets: (row level -
-// tile's first level in {0, >=1}) x (column level - row level in {-1, 0, +1}), each the min / max
-// tile its columns fall in.  A tile straddling a level boundary would otherwise hull the end of
-// level l (its own rows) with the start of level l (read by its level-(l+1) rows) into one run a
-// whole level long; split this way each bucket is compact.  Runs are merged when they touch and
-// then down to kWaveRuns by closing the smallest gaps (only extra polls, never a missed tile).
-// reach(T) = the furthest tile any run of tiles <= T touches (a prefix maximum, so ready times
-// stay monotone in T).
+// Wave schedule, host side.  reach(T) = the furthest tile read by the rows of tiles <= T (a prefix
+// maximum, so ready times stay monotone in T), from six buckets per tile: (row level - tile's first
+// level in {0, >=1}) x (column level - row level in {-1, 0, +1}), each the min / max tile its
+// columns fall in (wave_dep_tiles, the bucket spans, is reported by mpkg_plan_exec_info).
 constexpr int kWaveBuckets = 6;
 
 __global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci, uint32_t n,
@@ -1945,8 +1988,9 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E.S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
         MPKG_CUDA(cudaStreamSynchronize(st));
         E.tile_bytes.assign(nt, 0);
-        for (uint32_t T = 0; T < nt && T < E.S->n_chunks; ++T)
-            E.tile_bytes[T] = 12 * (off[T + 1] - off[T]) + 24ull * kWaveRows;
+        for (uint32_t T = 0; T < nt && (uint64_t)T * kWaveChunks < E.S->n_chunks; ++T)
+            E.tile_bytes[T] = 12 * (off[std::min<uint64_t>((uint64_t)(T + 1) * kWaveChunks, E.S->n_chunks)] -
+                                    off[(uint64_t)T * kWaveChunks]) + 24ull * kWaveRows;
     }
     std::vector<uint32_t> lp = Pl->level_ptr;
     if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
@@ -1966,51 +2010,21 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
     MPKG_CUDA(cudaMemcpyAsync(hmin.data(), bmin.p, bmin.bytes(), cudaMemcpyDeviceToHost, st));
     MPKG_CUDA(cudaMemcpyAsync(hmax.data(), bmax.p, bmax.bytes(), cudaMemcpyDeviceToHost, st));
     MPKG_CUDA(cudaStreamSynchronize(st));
-    std::vector<uint32_t> rec((uint64_t)nt * 2 * kWaveRuns);
     E.wave_reach.assign(nt, 0);
     E.wave_dep_tiles = 0;
     uint32_t reach = 0;
-    std::vector<std::pair<uint32_t, uint32_t>> runs, merged;
     for (uint32_t T = 0; T < nt; ++T) {
-        runs.clear();
-        runs.push_back({T, T});
+        uint32_t hi = T;
         for (int b = 0; b < kWaveBuckets; ++b) {
             const uint64_t i = (uint64_t)T * kWaveBuckets + b;
-            if (hmin[i] <= hmax[i]) runs.push_back({hmin[i], hmax[i]});
-        }
-        std::sort(runs.begin(), runs.end());
-        merged.clear();
-        for (const auto& rr : runs) {
-            if (!merged.empty() && rr.first <= merged.back().second + 1)
-                merged.back().second = std::max(merged.back().second, rr.second);
-            else
-                merged.push_back(rr);
-        }
-        while (merged.size() > (size_t)kWaveRuns) {  // close the smallest gap
-            size_t best = 0;
-            uint64_t gap = ~0ull;
-            for (size_t i = 0; i + 1 < merged.size(); ++i)
-                if ((uint64_t)merged[i + 1].first - merged[i].second < gap)
-                    gap = merged[i + 1].first - merged[i].second, best = i;
-            merged[best].second = std::max(merged[best].second, merged[best + 1].second);
-            merged.erase(merged.begin() + best + 1);
-        }
-        for (int j = 0; j < kWaveRuns; ++j) {
-            const bool used = j < (int)merged.size();
-            rec[(uint64_t)T * 2 * kWaveRuns + j] = used ? merged[j].first : 1u;
-            rec[(uint64_t)T * 2 * kWaveRuns + kWaveRuns + j] = used ? merged[j].second : 0u;  // empty: lo > hi
-            if (used) {
-                reach = std::max(reach, merged[j].second);
-                E.wave_dep_tiles += merged[j].second - merged[j].first + 1;
+            if (hmin[i] <= hmax[i]) {
+                hi = std::max(hi, hmax[i]);
+                E.wave_dep_tiles += hmax[i] - hmin[i] + 1;
             }
         }
-        E.wave_reach[T] = std::max(reach, T);
+        reach = std::max(reach, hi);
+        E.wave_reach[T] = reach;
     }
-    E.wave_rec.alloc(std::max<size_t>(rec.size(), 1));
-    if (!rec.empty())
-        MPKG_CUDA(cudaMemcpyAsync(E.wave_rec.p, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice, st));
-    E.done.alloc(std::max<uint32_t>(nt, 1));
-    MPKG_CUDA(cudaStreamSynchronize(st));
 }
 
 // Ticket order of one pass over powers q0..q1: ready(T, q0) = T, ready(T, q) = ready(reach(T),
@@ -2046,8 +2060,8 @@ uint64_t wave_order(const Executor& E, int q0, int q1, int64_t slack, std::vecto
 
 // Pass length p' = the longest pass whose live window fits the budget (0.6 x L2 unless the
 // l2_budget knob says otherwise; the "pass" knob forces p'); slack (ready-time units, ~p'
-// tickets each) = 1.25 x the warps in flight / p', so a ticket's dependencies have finished when
-// its warp reaches it.  Passes are balanced (ceil(p / p') of them).
+// tickets each) = 2.2 x the warps / p' (each warp holds its ticket and the next one), so a
+// ticket's inputs are almost always stored when its warp reaches it.  Passes are balanced (ceil(p / p') of them).
 const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     auto it = E.wave.find(p);
     if (it != E.wave.end()) return it->second;
@@ -2056,7 +2070,7 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     const int64_t warps = (int64_t)E.wave_grid * 8;
     auto slack_for = [&](int len) -> int64_t {
         if (ctx->slack >= 0) return std::max<int64_t>(ctx->slack, 1);
-        return std::max<int64_t>(1, (warps * 5 / 4 + len - 1) / len);
+        return std::max<int64_t>(1, (warps * 11 / 5 + len - 1) / len);
     };
     int P = std::min(p, kMaxFusedP);
     if (ctx->pass_powers > 0) {
@@ -2092,11 +2106,14 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.wave.emplace(p, std::move(W)).first->second;
 }
 
-void* wave_fn(int kind, bool sigma) {
-    static void* const fns[6] = {(void*)k_mpk_wave<0, false>, (void*)k_mpk_wave<0, true>,
-                                 (void*)k_mpk_wave<1, false>, (void*)k_mpk_wave<1, true>,
-                                 (void*)k_mpk_wave<2, false>, (void*)k_mpk_wave<2, true>};
-    return fns[kind * 2 + (sigma ? 1 : 0)];
+// minb: resident CTAs per SM the build targets (registers 80 / 64 / 48 / 40 for 3 / 4 / 5 / 6)
+void* wave_fn(int kind, bool sigma, int minb) {
+#define MPKG_WAVE_FNS(M) {(void*)k_mpk_wave<0, false, M>, (void*)k_mpk_wave<0, true, M>, \
+                          (void*)k_mpk_wave<1, false, M>, (void*)k_mpk_wave<1, true, M>}
+    static void* const fns[4][4] = {MPKG_WAVE_FNS(3), MPKG_WAVE_FNS(4), MPKG_WAVE_FNS(5), MPKG_WAVE_FNS(6)};
+#undef MPKG_WAVE_FNS
+    const int m = minb < 3 ? 0 : minb > 6 ? 3 : minb - 3;
+    return fns[m][kind * 2 + (sigma ? 1 : 0)];
 }
 
 template <int KIND, int G>
@@ -2173,9 +2190,11 @@ void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
     MPKG_CUDA(cudaStreamSynchronize(st));
 }
 
-bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int /*p*/) {
+bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int p, int kind) {
     if (ctx->schedule == 1) return false;
-    if (ctx->schedule == 3 && E.h_tile_start.empty() && E.tile_rows == kWaveRows) return false;
+    if ((ctx->schedule == 3 || (ctx->schedule == 0 && E.wave_auto && p >= 2)) && kind != 2 && E.h_tile_start.empty() &&
+        E.tile_rows == kWaveRows)
+        return false;
     // Long rows live outside the SELL arrays.  Fast mode reduces them in k_coop_rows beside the
     // sweeps; bitwise mode adds them in stored order in k_long_rows_bitwise beside the sweeps
     // (R-MAT scale 21: 2.79 ms vs 2.93 ms for the fused kernel's CTA-cooperative path; both are
@@ -2187,19 +2206,24 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (a.p > kMaxFusedP) fail(MPKG_EINVAL, "mpk: at most 32 powers per fused launch");
     Executor& E = get_executor(ctx, Pl, A);
     if (E.n_tiles == 0) return;
-    const bool sweep = use_sweeps(ctx, E, a.p);
-    const bool wave = !sweep && ctx->schedule == 3;
+    const bool sweep = use_sweeps(ctx, E, a.p, a.kind);
+    const bool wave = !sweep && ctx->schedule != 1;
+    if (wave && a.kind == 2) fail(MPKG_EINTERNAL, "mpk: the wave schedule has no polynomial epilogue");
     if (!sweep && !wave && !E.fused_ready) build_fused(ctx, Pl, A, &E);
-    if (wave && !E.wave_grid) {
+    const int wminb = ctx->wave_minb > 0 ? (int)ctx->wave_minb : 4;
+    if (wave && (!E.wave_grid || E.wave_minb != wminb)) {
         int occ = 1 << 30;
-        for (int k = 0; k < 6; ++k) {
+        for (int k = 0; k < 4; ++k) {
             int o = 0;
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wave_fn(k / 2, k % 2), 256, 0));
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wave_fn(k / 2, k % 2, wminb), 256, 0));
             occ = std::min(occ, o);
         }
         if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
+        if (!E.wave_grid) build_wave(ctx, Pl, A, E);
         E.wave_grid = std::max(1, occ) * ctx->sm_count;
-        build_wave(ctx, Pl, A, E);
+        E.wave_minb = wminb;
+        E.wave.clear();  // the slack follows the warps in flight
+        E.counter.alloc(kWaveStreams * 32 + 32);
     }
     static const DevBuf<uint32_t> no_tickets;
     const Executor::Wave* W = wave ? &get_wave(ctx, E, a.p) : nullptr;
@@ -2295,9 +2319,9 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         P.shift_b2[i] = a.shift_b2 ? a.shift_b2[i] : 0.0;
     }
     for (int i = 0; i <= a.p; ++i) P.coef[i] = a.coef ? a.coef[i] : 0.0;
-    if (!sweep) {
+    if (!sweep && !wave) {
         MPKG_CUDA(cudaMemsetAsync(E.done.p, 0, E.done.bytes(), st));
-        if (!wave) MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
+        MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, sizeof(uint32_t), st));
     }
     const uint32_t smem = E.stages * E.buf_bytes;
     E.last_sweep = sweep;
@@ -2513,10 +2537,19 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (wave) {
         // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
         // host block, the pass's slices go to the host while the next pass runs
-        void* fn = wave_fn(a.kind, sigma);
-        P.dep_lo = E.wave_rec.p;  // per-tile dependency records (build_wave)
+        void* fn = wave_fn(a.kind, sigma, wminb);
+        P.counter = E.counter.p;
+        P.dbg = getenv("MPKG_WAVE_DEBUG") ? E.counter.p + kWaveStreams * 32 : nullptr;
         for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
             uint32_t t0 = W->t_begin[j], t1 = W->t_begin[j + 1], q0 = (uint32_t)W->q_begin[j];
+            const uint32_t q1 = (uint32_t)W->q_begin[j + 1] - 1;
+            MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, 4ull * kWaveStreams * 32, st));
+            if (q1 > q0) {  // the slices read inside the pass start out empty
+                k_wave_fill<<<grid_for(P.vstride, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                    P.V, P.vstride, sigma ? E.n_slots : A->n_rows, q0, q1);
+                MPKG_LAUNCH_CHECK();
+                ctx->launches += 1;
+            }
             const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(E.wave_grid, (t1 - t0 + 7) / 8));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(g);
@@ -2534,6 +2567,15 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
                 for (int q = W->q_begin[j]; q < W->q_begin[j + 1]; ++q) copy_slice((uint32_t)q);
         }
         if (to_host) join_copies();
+        if (getenv("MPKG_WAVE_DEBUG")) {
+            uint32_t misses = 0;
+            MPKG_CUDA(cudaMemcpyAsync(&misses, E.counter.p + kWaveStreams * 32, 4, cudaMemcpyDeviceToHost, st));
+            MPKG_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "wave: p=%d passes=%zu tickets=%zu slack=%lld window=%llu misses=%u\n", a.p,
+                    W->t_begin.size() - 1, (size_t)W->t_begin.back(), (long long)W->slack,
+                    (unsigned long long)W->window, misses);
+            MPKG_CUDA(cudaMemsetAsync(E.counter.p + kWaveStreams * 32, 0, 4, st));
+        }
     } else if (E.kernel == 4) {
         const int nt = (int)E.threads;
         const uint32_t sm = E.stages * E.buf_bytes;

@@ -215,6 +215,7 @@ def test_orders_and_schedules(ctx, cases, oracle, order, sched):
             ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 6)
             assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} {sched} order={order}")
             info = plan.exec_info()
+            assert_bitwise(ctx.mpk(plan, Ap, x, 6).as_matrix(), ref, f"{name} {sched} order={order} again")
             assert info["order"] == order
             want = ("sweeps" if sched == "sweeps" else
                     ("sweeps" if info["long_rows"] else "wave") if sched.startswith("wave") else "fused")
