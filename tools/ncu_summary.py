@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--kernel", default="k_mpk")
     ap.add_argument("--note", default="")
+    ap.add_argument("--steps", type=int, default=1, help="MPK steps inside the launch list's range")
     a = ap.parse_args()
     hdr, units, rows = raw(a.rep)
     res = {"report": a.rep.split("/")[-1], "note": a.note, "kernels": []}
@@ -76,6 +77,7 @@ def main():
     res["dram_write_bytes_per_launch"] = wr
     if a.launches:
         agg = {}
+        dram = {}
         hdr2 = None
         for r in csv.reader(open(a.launches)):
             if r and r[0] == "ID":
@@ -83,10 +85,18 @@ def main():
                 continue
             if hdr2 and len(r) == len(hdr2):
                 d = dict(zip(hdr2, r))
+                name = d["Kernel Name"].split("(")[0].split("::")[-1][:60]
+                val = float(d["Metric Value"].replace(",", ""))
+                if d["Metric Name"].startswith("dram__bytes_"):
+                    scale = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(d["Metric Unit"].lower(), 1.0)
+                    dram[name] = dram.get(name, 0.0) + val * scale
                 if d["Metric Name"] != "gpu__time_duration.sum":
                     continue
-                name = d["Kernel Name"].split("(")[0].split("::")[-1][:60]
-                agg.setdefault(name, []).append(float(d["Metric Value"].replace(",", "")))
+                agg.setdefault(name, []).append(val)
+        if dram:  # every kernel of the timed region (fills included): the step's DRAM traffic
+            res["dram_bytes_per_step"] = sum(dram.values()) / a.steps
+            res["dram_bytes_per_step_by_kernel"] = {k: v / a.steps for k, v in dram.items()}
+            res["dram_bytes_per_step_source"] = "launch list (all kernels of the timed region)"
         tot = sum(sum(v) for v in agg.values()) or 1.0
         res["launch_list"] = {k: {"launches": len(v), "total_ns": sum(v), "share": round(sum(v) / tot, 4)}
                               for k, v in sorted(agg.items(), key=lambda x: -sum(x[1]))}
