@@ -184,6 +184,12 @@ int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets,
  * persistent launch per pass of p' powers; 0: one fused tile-DAG launch), fused kernel variant,
  * rows handled outside the SELL arrays (long rows). */
 int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
+/* Schedule audit (ctx knob "trace" = 1): after an mpkg_mpk* on the fused or wave schedule, the
+ * 2 * n_tiles * (p+1) globaltimer stamps of the last call, [2 (q n_tiles + T)] = tile T's inputs for
+ * power q complete, [.. + 1] = its results about to be stored / published; out may be NULL to
+ * query n_stamps and the tile size.  The acceptance.cpp:188-251 predecessor audit replays on it. */
+int mpkg_plan_exec_trace(mpkg_plan_t P, uint64_t* out, uint64_t capacity, uint64_t* n_stamps,
+                         uint32_t* tile_rows);
 
 /* execute.hpp:59-72 wavefront_schedule (pure host function; arrays hold n_groups*stages). */
 int mpkg_wavefront_schedule(uint32_t n_groups, int stages, uint32_t* group, int* stage,

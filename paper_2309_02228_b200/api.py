@@ -382,6 +382,18 @@ class ExecutionPlan:
                 "schedule": {1: "sweeps", 2: "wave"}.get(sw.value, "fused"), "kernel": kn.value,
                 "long_rows": lr.value}
 
+    def exec_trace(self):
+        """ctx knob "trace": (flat stamps, tile_rows) of the last fused / wave MPK on this plan
+        (mpkg_plan_exec_trace); stamps reshape to [p+1, n_tiles, 2] = (inputs complete, results
+        stored).  (None, tile_rows) when the last call recorded nothing."""
+        n, tr = C.c_uint64(), C.c_uint32()
+        check(lib.mpkg_plan_exec_trace(self.h, None, 0, C.byref(n), C.byref(tr)))
+        if n.value == 0:
+            return None, tr.value
+        out = np.empty(n.value, np.uint64)
+        check(lib.mpkg_plan_exec_trace(self.h, _ptr(out), n.value, C.byref(n), C.byref(tr)))
+        return out, tr.value
+
     def __del__(self):
         if getattr(self, "h", None):
             lib.mpkg_plan_destroy(self.h)

@@ -323,6 +323,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->graphs = value != 0;
         else if (k == "resident")
             ctx->resident = value != 0;
+        else if (k == "trace")
+            ctx->trace = value != 0;
         else if (k == "wave_minb") {
             require(value >= 0 && value <= 6, "ctx_set_param: wave_minb must be 0 (default) or 3..6");
             ctx->wave_minb = value;
@@ -820,6 +822,14 @@ int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uin
     return guarded([&] {
         require(P != nullptr, "plan_exec_mode: null plan");
         exec_mode(P, order, sweeps, kernel, long_rows);
+    });
+}
+
+int mpkg_plan_exec_trace(mpkg_plan_t P, uint64_t* out, uint64_t capacity, uint64_t* n_stamps,
+                         uint32_t* tile_rows) {
+    return guarded([&] {
+        require(P != nullptr, "plan_exec_trace: null plan");
+        exec_trace(P, out, capacity, n_stamps, tile_rows);
     });
 }
 

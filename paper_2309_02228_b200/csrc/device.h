@@ -114,6 +114,7 @@ struct mpkg_ctx_s {
     int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power, 3 wave (mpk_exec.cu)
     int64_t wave_minb = 0;    // wave kernel build: resident CTAs per SM targeted (3..6; 0 = 4)
+    bool trace = false;       // record per-(tile, power) globaltimer stamps (mpkg_plan_exec_trace)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
     int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)
     uint64_t launches = 0;
@@ -308,6 +309,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& 
 void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
                uint32_t* pass_powers);
 void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
+void exec_trace(const mpkg_plan_s* P, uint64_t* out, uint64_t cap, uint64_t* n, uint32_t* tile_rows);
 
 // ortho.cu: block orthogonalisation (reference ortho.hpp)
 void gpu_block_dots(mpkg_ctx_s* ctx, const double* q, const double* v, uint64_t rows, uint32_t qcols,

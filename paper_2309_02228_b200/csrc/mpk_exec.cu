@@ -134,6 +134,8 @@ struct Executor {
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
     int wave_minb = 0;
+    DevBuf<unsigned long long> trace;         // "trace" knob (FusedParams::trace)
+    uint64_t trace_n = 0;
     bool wave_auto = false;                   // schedule 0 picked the wave (get_executor)
     std::vector<uint32_t> wave_reach;         // per tile: furthest tile read by tiles <= T
     uint64_t wave_dep_tiles = 0;              // dependency bucket spans (tiles), summed over tiles
@@ -156,6 +158,9 @@ struct FusedParams {
     uint32_t* done;
     uint32_t* counter;
     uint32_t* dbg;  // wave schedule: value-wait count (MPKG_WAVE_DEBUG)
+    // "trace" knob: per (power, tile) two globaltimer stamps, [2 (q n_tiles + T)] = inputs complete,
+    // [.. + 1] = results about to be stored / published (tests/test_gpu_trace.py audits them)
+    unsigned long long* trace;
     uint32_t n_tickets;
     uint32_t n_rows;
     uint32_t n_slots;
@@ -313,6 +318,15 @@ __device__ __forceinline__ void publish(const FusedParams& P, uint32_t T, uint32
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.done + T), "r"(q) : "memory");
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(P.sb_count + (uint64_t)q * P.n_sb + T / kSB)
                  : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_stamp(const FusedParams& P, uint32_t T, uint32_t q, uint32_t which) {
+    if (P.trace) P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + which] = global_ns();
 }
 
 __device__ __forceinline__ uint32_t level_of(const uint32_t* __restrict__ lp, uint32_t nl, uint32_t s) {
@@ -942,6 +956,7 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
             }
             __syncthreads();
         }
+        if (tid == 0) trace_stamp(P, T, q, 0);
         const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
         const uint64_t pol = l2_policy(code & kLastUse);
         const uint32_t s0 = VT ? P.tile_start[T] : T * P.tile_rows;
@@ -970,7 +985,10 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
             }
         }
         __syncthreads();
-        if (tid == 0) publish(P, T, q);
+        if (tid == 0) {
+            trace_stamp(P, T, q, 1);
+            publish(P, T, q);
+        }
     }
 }
 
@@ -1169,9 +1187,19 @@ __global__ void __launch_bounds__(256, MINB) k_mpk_wave(const __grid_constant__ 
                 offn = P.chunk_off[sn >> 5];
                 endn = P.chunk_off[(sn >> 5) + 1];
             }
-            if (r < P.n_rows) {
+            if (r < P.n_rows || P.trace) {
                 const uint32_t L = (uint32_t)((end - off) >> 5);
-                wave_epilogue<KIND, SIGMA>(P, s, r, q, q0, src, wave_row(P, off, L, lane, len, src, pol, q == q0));
+                const double acc = r < P.n_rows ? wave_row(P, off, L, lane, len, src, pol, q == q0) : 0.0;
+                if (P.trace) {  // every lane's inputs are final here, no result is stored yet
+                    __syncwarp();
+                    if (lane == 0) {
+                        const unsigned long long ts = global_ns();
+                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T)] = ts;
+                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + 1] = ts;
+                    }
+                    __syncwarp();
+                }
+                if (r < P.n_rows) wave_epilogue<KIND, SIGMA>(P, s, r, q, q0, src, acc);
             }
             s = sn, r = rn, len = lenn, off = offn, end = endn;
         }
@@ -2260,6 +2288,14 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.csr_v = A->values.p;
     P.n_tiles = E.n_tiles;
     P.long_slots = E.long_slots.p;
+    if (ctx->trace && !sweep) {
+        E.trace_n = 2ull * E.n_tiles * (a.p + 1);
+        E.trace.ensure(E.trace_n);
+        MPKG_CUDA(cudaMemsetAsync(E.trace.p, 0, 8 * E.trace_n, st));
+        P.trace = E.trace.p;
+    } else {
+        E.trace_n = 0;
+    }
     P.n_long = (uint32_t)E.long_rows;
     // fast-mode sweeps over a matrix with rows longer than kMedCap: those rows (long ones
     // included) run in k_coop_rows on a side stream, concurrently with each power's sweep
@@ -2637,6 +2673,17 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
     if (n_tickets) *n_tickets = k;
     if (n_deps) *n_deps = d;
     if (pass_powers) *pass_powers = pp;
+}
+
+void exec_trace(const mpkg_plan_s* P, uint64_t* out, uint64_t cap, uint64_t* n, uint32_t* tile_rows) {
+    const Executor* E = P->exec.get();
+    const uint64_t m = E ? E->trace_n : 0;
+    if (n) *n = m;
+    if (tile_rows) *tile_rows = E ? E->tile_rows : 0;
+    if (out && m) {
+        if (cap < m) fail(MPKG_EINVAL, "plan_exec_trace: buffer too small");
+        MPKG_CUDA(cudaMemcpy(out, E->trace.p, 8 * m, cudaMemcpyDeviceToHost));
+    }
 }
 
 void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows) {
