@@ -325,10 +325,7 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->resident = value != 0;
         else if (k == "trace")
             ctx->trace = value != 0;
-        else if (k == "wave_minb") {
-            require(value >= 0 && value <= 6, "ctx_set_param: wave_minb must be 0 (default) or 3..6");
-            ctx->wave_minb = value;
-        } else if (k == "pdl")
+        else if (k == "pdl")
             ctx->pdl = value != 0;
         else if (k == "schedule") {
             require(value >= 0 && value <= 3, "ctx_set_param: schedule must be 0 (auto), 1 (fused), 2 (sweeps) or 3 (wave)");

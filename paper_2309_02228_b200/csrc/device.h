@@ -113,7 +113,6 @@ struct mpkg_ctx_s {
     int64_t coop_min = 0;       // fast mode: rows longer than this run warp-cooperatively (0 = 128)
     int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power, 3 wave (mpk_exec.cu)
-    int64_t wave_minb = 0;    // wave kernel build: resident CTAs per SM targeted (3..6; 0 = 4)
     bool trace = false;       // record per-(tile, power) globaltimer stamps (mpkg_plan_exec_trace)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
     int64_t cgroups = 0;      // async kernel: consumer groups per CTA (0: 128 / tile_rows)

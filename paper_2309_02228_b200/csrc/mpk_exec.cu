@@ -125,6 +125,7 @@ struct Executor {
     // wave schedule (schedule knob 3): per p, the pass ticket lists and pass boundaries
     struct Wave {
         DevBuf<uint32_t> tickets;
+        DevBuf<uint4> desc;             // k_mpk_wave's ticket descriptors (k_wave_desc)
         std::vector<uint32_t> t_begin;  // first ticket of every pass (+ the end)
         std::vector<int> q_begin;       // first power of every pass (+ p+1)
         int pass_len = 0;
@@ -133,7 +134,9 @@ struct Executor {
     };
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
-    int wave_minb = 0;
+    DevBuf<char> wrec;                        // chunk records (k_wave_pack)
+    DevBuf<uint32_t> wrec_off;                // record offsets, 16-byte units (n_tiles * kWaveChunks + 1)
+    uint64_t wave_pol[2] = {0, 0};            // createpolicy evict_first / evict_last values
     DevBuf<unsigned long long> trace;         // "trace" knob (FusedParams::trace)
     uint64_t trace_n = 0;
     bool wave_auto = false;                   // schedule 0 picked the wave (get_executor)
@@ -152,6 +155,11 @@ struct FusedParams {
     const uint32_t* row_len;
     const uint32_t* slot_row;  // nullptr: identity
     const uint32_t* tickets;
+    const uint4* wdesc;        // wave schedule: ticket descriptors
+    const char* wrec;          // wave schedule: chunk records
+    const uint32_t* wrec_off;
+    uint64_t pol_first;        // L2 policies (createpolicy results, k_l2_policies)
+    uint64_t pol_last;
     const uint32_t* dep_ptr;
     const uint32_t* dep_lo;
     const uint32_t* dep_hi;
@@ -1015,7 +1023,10 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
 // a lower, finished ticket and stores become visible, so it always progresses (deadlock-free).
 // Row arithmetic is rowdot.cuh's (stored order, mul then add): bitwise.  Slice 0 and the slices of
 // earlier passes are complete before the launch and read through the non-coherent path.
-constexpr uint32_t kWaveChunks = 1;                // SELL chunks (warp rounds) per ticket
+#ifndef MPKG_WAVE_CHUNKS
+#define MPKG_WAVE_CHUNKS 1
+#endif
+constexpr uint32_t kWaveChunks = MPKG_WAVE_CHUNKS;  // SELL chunks per ticket (rows per lane)
 constexpr uint32_t kWaveRows = 32 * kWaveChunks;  // rows per tile
 constexpr unsigned long long kWaveEmpty = 0x7ff4dead5eed0001ull;
 
@@ -1035,27 +1046,6 @@ __device__ __forceinline__ double ld_strong_again(const double* p) {
 __device__ __forceinline__ void st_strong(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
-// Matrix streams (read-only for the kernel's lifetime): non-volatile, schedulable.
-__device__ __forceinline__ uint2 ldm_u2(const uint2* p, uint64_t pol) {
-    uint2 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint32_t ldm_u32(const uint32_t* p, uint64_t pol) {
-    uint32_t r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double2 ldm_d2(const double2* p, uint64_t pol) {
-    double2 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double ldm_d(const double* p, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-    return r;
-}
 __device__ __forceinline__ bool wave_empty(double v) {
     return (unsigned long long)__double_as_longlong(v) == kWaveEmpty;
 }
@@ -1068,58 +1058,120 @@ __device__ __forceinline__ double wave_wait(const double* p, double v) {
     return v;
 }
 
-// The matrix group of entries k0..k0+7 of the lane's row (rowdot.cuh sell_row_dot layout), written
-// branch-free: k0 is even and Lp = L & ~1 is even, so a pair (k, k+1) is either entirely in the
-// pair region (k < Lp) or entirely past it, where only entry k == Lp (odd L) exists, in the tail.
-__device__ __forceinline__ void wave_group(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
-                                           uint32_t k0, uint64_t pol, uint32_t (&c)[8], double (&v)[8]) {
-    const uint32_t Lp = L & ~1u;
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-        const uint32_t k = k0 + j;
-        uint2 cc = make_uint2(0u, 0u);
-        double2 vv = make_double2(0.0, 0.0);
-        if (k < Lp) {
-            const uint64_t e = off + (k >> 1) * 64u + lane * 2u;
-            cc = ldm_u2(reinterpret_cast<const uint2*>(P.cols + e), pol);
-            vv = ldm_d2(reinterpret_cast<const double2*>(P.vals + e), pol);
-        }
-        if (k == Lp && k < L) {
-            const uint64_t e = off + (uint64_t)Lp * 32u + lane;
-            cc.x = ldm_u32(P.cols + e, pol);
-            vv.x = ldm_d(P.vals + e, pol);
-        }
-        c[j] = cc.x, c[j + 1] = cc.y, v[j] = vv.x, v[j + 1] = vv.y;
-    }
+// ---- The wave engine ------------------------------------------------------------------------
+//
+// Chunk records.  The wave keeps its own packed copy of the executor's SELL-32 arrays: chunk T (32
+// rows) is ONE contiguous, 16-byte aligned record
+//   len[32] u32 | slot_row[32] u32 (private row order only) | cols[L * 32] u32 | vals[L * 32] f64
+// (cols / vals in rowdot.cuh's pair interleave, L = the chunk width), so a ticket's whole matrix
+// slice moves with one 1D bulk copy.  rec_off[T] is the record's offset in 16-byte units.
+//
+constexpr uint32_t kWaveWideL = 15;
+constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
+
+__host__ __device__ constexpr uint32_t wave_hdr_bytes(bool sigma) { return sigma ? 256u : 128u; }
+
+// Gathers of x_{q-1}: weak and L1-allocating, so the 7 gathers of a 7-point row, which share lines
+// ((i,j-1,k) and (i,j,k-1) are neighbours in level l-1), hit L1.  Every location of an in-pass
+// slice holds kWaveEmpty or its final value (written once per launch), so a non-empty value read
+// this way is final; an empty one (a producer behind, or a stale L1 copy of a line read while it
+// still held empty values) is re-read with relaxed L2 loads until its producer has stored it.
+__device__ __forceinline__ double ld_gather(const double* p) {
+    double v;
+    asm("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+    asm("" : "+l"(p));
+    return p;
+}
+__device__ __forceinline__ bool is_nan_bits(double v) {
+    return ((unsigned long long)__double_as_longlong(v) << 1) > (0x7ff0000000000000ull << 1);
 }
 
-// first: the source slice is complete (q == q0: no waiting; slice 0 is caller data and may hold any
-// bit pattern).  Otherwise a row that gathered a value still reading kWaveEmpty (its producer is
-// behind) is recomputed after a short sleep; the discarded sum is never stored.  The gathers are
-// volatile so every attempt re-issues them.
-__device__ __forceinline__ double wave_row(const FusedParams& P, uint64_t off, uint32_t L, uint32_t lane,
-                                           uint32_t len, const double* src, uint64_t pol, bool first) {
-    for (;;) {
-        uint32_t c[8];
-        double v[8];
-        double acc = 0.0;
-        bool miss = false;
-        for (uint32_t k0 = 0; k0 < len; k0 += 8) {
-            wave_group(P, off, L, lane, k0, pol, c, v);
-            double x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                x[j] = k0 + j < len ? (first ? __ldg(src + c[j]) : ld_strong_again(src + c[j])) : 0.0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (k0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+// Cold path: the row of `lane` from its record in global memory, every in-pass value awaited
+// (a gathered value was still empty, or the chunk is wider than a stage holds).
+__device__ __forceinline__ double wave_row_slow(const char* rec, uint32_t hdr, uint32_t L, uint32_t lane,
+                                                uint32_t len, const double* src, bool first, uint32_t* dbg) {
+    if (dbg) atomicAdd(dbg, 1u);
+    const uint32_t* cols = reinterpret_cast<const uint32_t*>(rec + hdr);
+    const double* vals = reinterpret_cast<const double*>(rec + hdr + 128u * L);
+    const uint32_t Lp = L & ~1u;
+    double acc = 0.0;
+    for (uint32_t k = 0; k < len; ++k) {
+        const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
+        const uint32_t c = __ldg(cols + e);
+        double x;
+        if (first) {
+            x = __ldg(src + c);
+        } else {
+            x = ld_strong_again(src + c);
+            while (wave_empty(x)) {
+                __nanosleep(64);
+                x = ld_strong_again(src + c);
+            }
         }
-        if (!miss || first) return acc;
-        if (P.dbg) atomicAdd(P.dbg, 1u);
-        __nanosleep(200);
+        acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + e), x));
     }
+    return acc;
+}
+
+// Hot path: a staged chunk of compile-time width L, one row per lane, summed in stored order.  A
+// lane's padding entries (len <= k < L, value 0.0) gather nothing and add 0.0 * 0.0 = +0, which
+// leaves the sum unchanged (it starts at +0 and round-to-nearest never makes it -0): rowdot.cuh's
+// sum over k < len, bit for bit.  x[k] (k < L) is returned for the empty-value check.
+template <int L>
+__device__ __forceinline__ double wave_dot(const char* stage, uint32_t hdr, uint32_t lane, uint32_t len,
+                                           const double* src, double (&x)[8]) {
+    constexpr int Lp = L & ~1;
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + hdr);
+    const double* sv = reinterpret_cast<const double*>(stage + hdr + 128 * L);
+#pragma unroll
+    for (int j = 0; j < Lp; j += 2) {
+        const uint2 cc = *reinterpret_cast<const uint2*>(sc + (j >> 1) * 64 + lane * 2);
+        x[j] = (uint32_t)j < len ? ld_gather(src + cc.x) : 0.0;
+        x[j + 1] = (uint32_t)j + 1 < len ? ld_gather(src + cc.y) : 0.0;
+    }
+    if (L & 1) x[Lp] = (uint32_t)Lp < len ? ld_gather(src + sc[Lp * 32 + lane]) : 0.0;
+#pragma unroll
+    for (int j = L; j < 8; ++j) x[j] = 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < Lp; j += 2) {
+        const double2 vv = *reinterpret_cast<const double2*>(sv + (j >> 1) * 64 + lane * 2);
+        acc = __dadd_rn(acc, __dmul_rn(vv.x, x[j]));
+        acc = __dadd_rn(acc, __dmul_rn(vv.y, x[j + 1]));
+    }
+    if (L & 1) acc = __dadd_rn(acc, __dmul_rn(sv[Lp * 32 + lane], x[Lp]));
+    return acc;
+}
+
+// A staged row whose gathers met empty values: re-read just those (relaxed L2 loads, all in flight,
+// then one by one until stored) and sum again from the stage, in stored order.
+__device__ __forceinline__ double wave_redo(const char* stage, uint32_t hdr, uint32_t L, uint32_t lane, uint32_t len,
+                                            const double* src, double (&x)[8], uint32_t* dbg) {
+    if (dbg) atomicAdd(dbg, 1u);
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + hdr);
+    const double* sv = reinterpret_cast<const double*>(stage + hdr + 128u * L);
+    const uint32_t Lp = L & ~1u;
+    uint32_t e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        e[k] = (uint32_t)k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1) : Lp * 32u + lane;
+        if ((uint32_t)k < len && wave_empty(x[k])) x[k] = ld_strong_again(src + sc[e[k]]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        while ((uint32_t)k < len && wave_empty(x[k])) {
+            __nanosleep(32);
+            x[k] = ld_strong_again(src + sc[e[k]]);
+        }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if ((uint32_t)k < L) acc = __dadd_rn(acc, __dmul_rn(sv[e[k]], x[k]));
+    return acc;
 }
 
 // row_epilogue with the wave's rules: in-pass values are awaited, working-vector stores are
@@ -1143,19 +1195,126 @@ __device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, 
 
 // Tickets are claimed dynamically, in order, from kWaveStreams interleaved counters (stream i hands
 // out tickets i, i + S, i + 2S, ... to the warps with warp id = i mod S; one counter alone tops out
-// near 1.5 claims/ns).  Each warp claims one ticket ahead of the one it runs, so the tickets in
-// flight are always the ~2 x warps most recently claimed: no warp can drift behind the front, which
-// is what lets a small slack (and so a small L2 window) suffice.  A ticket waits only on values of
-// lower tickets, all claimed earlier by running warps: deadlock-free without co-residency.
-constexpr uint32_t kWaveStreams = 16;
+// near 1.5 claims/ns).  Each warp holds the ticket it runs, the next one (staged) and the one
+// after (descriptor loading), plus one claim in flight, all in increasing order from its stream:
+// the tickets in flight are always the ~3 x warps most recently claimed (no warp drifts behind the
+// front, which lets a small slack, and so a small L2 window, suffice), and the lowest unfinished
+// ticket is always one a warp is running.  A ticket waits only on values of lower tickets, so it
+// always progresses: deadlock-free without co-residency.
+#ifndef MPKG_WAVE_STREAMS
+#define MPKG_WAVE_STREAMS 16
+#endif
+constexpr uint32_t kWaveStreams = MPKG_WAVE_STREAMS;
 
-template <int KIND, bool SIGMA, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
-                                                      uint32_t t1, uint32_t q0) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// Every warp owns a two-stage shared-memory ring; lane 0 stages a ticket's kWaveChunks chunk records
+// (contiguous in the record array) with ONE 1D bulk copy (cp.async.bulk, mbarrier complete_tx, L2
+// evict_last, evict_first on the tile's last use in the pass) one ticket AHEAD, so the matrix stream
+// is asynchronous and holds no registers, and a ticket costs one dependent hop: the gathers, all of
+// the tile's rows at once (kWaveChunks rows per lane in flight).  Tiles with a chunk wider than 8
+// entries are not staged (their rows take wave_row_slow from global memory).
+constexpr uint32_t kWaveRecMax = 256 + 8 * 32 * 12;                // largest staged record (3,328 B)
+constexpr uint32_t kWaveStageBytes = kWaveChunks * kWaveRecMax;
+constexpr uint32_t kWaveWarps = 8 / kWaveChunks;                   // warps per CTA (2 stages each)
+constexpr uint32_t kWaveThreads = 32 * kWaveWarps;
+constexpr uint32_t kWaveSmem = kWaveWarps * 2 * kWaveStageBytes;   // 53,248 B: 4 CTAs per SM
+
+__device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                             uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+// Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units), y = T, z = q - q0,
+// w = the chunk widths, 4 bits each (min(L, 15); 15: a wide chunk, L read from rec_off).
+__device__ __forceinline__ uint4 ld_desc(const uint4* p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ bool wave_narrow(uint32_t w) {  // every chunk width <= 8
+#pragma unroll
+    for (uint32_t c = 0; c < kWaveChunks; ++c)
+        if (((w >> (4 * c)) & 15u) > 8u) return false;
+    return true;
+}
+template <uint32_t HDR>
+__device__ __forceinline__ uint32_t wave_tile_bytes(uint32_t w) {
+    uint32_t b = 0;
+#pragma unroll
+    for (uint32_t c = 0; c < kWaveChunks; ++c) b += HDR + 384u * ((w >> (4 * c)) & 15u);
+    return b;
+}
+
+// Lane 0: stage the records of ticket descriptor d (nothing for a tile with a wide chunk).
+template <bool SIGMA>
+__device__ __forceinline__ void wave_stage(const FusedParams& P, uint4 d, uint32_t q0, uint32_t q1,
+                                           uint32_t stage, uint32_t bar) {
+    const uint32_t bytes = wave_narrow(d.w) ? wave_tile_bytes<wave_hdr_bytes(SIGMA)>(d.w) : 0u;
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    if (bytes)
+        bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar,
+                     q0 + d.z == q1 ? P.pol_first : P.pol_last);
+}
+
+// All kWaveChunks rows of a lane at compile-time width L (every chunk of the tile that wide): all
+// gathers in flight, then the sums in stored order (wave_dot's rules, bit for bit).
+template <int L, uint32_t HDR, int C>
+__device__ __forceinline__ void wave_multi(const char* stage, uint32_t lane, const uint32_t (&len)[C],
+                                           const double* src, double (&x)[C][8], double (&acc)[C]) {
+    constexpr int Lp = L & ~1;
+    constexpr uint32_t REC = HDR + 384u * L;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + c * REC + HDR);
+#pragma unroll
+        for (int j = 0; j < Lp; j += 2) {
+            const uint2 cc = *reinterpret_cast<const uint2*>(sc + (j >> 1) * 64 + lane * 2);
+            x[c][j] = (uint32_t)j < len[c] ? ld_gather(src + cc.x) : 0.0;
+            x[c][j + 1] = (uint32_t)j + 1 < len[c] ? ld_gather(src + cc.y) : 0.0;
+        }
+        if (L & 1) x[c][Lp] = (uint32_t)Lp < len[c] ? ld_gather(src + sc[Lp * 32 + lane]) : 0.0;
+#pragma unroll
+        for (int j = L; j < 8; ++j) x[c][j] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const double* sv = reinterpret_cast<const double*>(stage + c * REC + HDR + 128 * L);
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < Lp; j += 2) {
+            const double2 vv = *reinterpret_cast<const double2*>(sv + (j >> 1) * 64 + lane * 2);
+            a = __dadd_rn(a, __dmul_rn(vv.x, x[c][j]));
+            a = __dadd_rn(a, __dmul_rn(vv.y, x[c][j + 1]));
+        }
+        if (L & 1) a = __dadd_rn(a, __dmul_rn(sv[Lp * 32 + lane], x[c][Lp]));
+        acc[c] = a;
+    }
+}
+
+template <int KIND, bool SIGMA>
+__global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
+                                                            uint32_t t1, uint32_t q0, uint32_t q1) {
+    extern __shared__ __align__(128) char wsm[];
+    __shared__ __align__(8) uint64_t bars[kWaveWarps][2];
+    constexpr uint32_t hdr = wave_hdr_bytes(SIGMA);
+    constexpr int C = (int)kWaveChunks;
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * kWaveWarps + wib;
     const uint32_t sid = gw % kWaveStreams;
     uint32_t* const ctr = P.counter + sid * 32u;  // one 128-B line per stream
+    char* const ring = wsm + wib * 2u * kWaveStageBytes;
+    const uint32_t ring_s = smem_u32(ring), bar0 = smem_u32(&bars[wib][0]);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar0 + 8u));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     auto claim = [&]() -> uint32_t {
         uint32_t k = 0;
         if (lane == 0) k = atomicAdd(ctr, 1u);
@@ -1163,51 +1322,187 @@ __global__ void __launch_bounds__(256, MINB) k_mpk_wave(const __grid_constant__ 
     };
     auto ticket = [&](uint32_t k) { return t0 + sid + kWaveStreams * __shfl_sync(0xffffffffu, k, 0); };
     uint32_t t = ticket(claim());
-    uint32_t kn = claim();  // the next ticket, in flight
-    uint32_t code = t < t1 ? P.tickets[t] : 0u;
-    while (t < t1) {
-        const uint32_t T = code & 0xffffffu;
-        const uint32_t q = (code >> 24) & 63u;
-        const uint64_t pol = l2_policy(code & kLastUse);
-        const double* src = P.V + (uint64_t)(q - 1) * P.vstride;
-        // the tile's chunks, one row per lane each; the next chunk's metadata loads during this one
-        uint32_t s = T * kWaveRows + lane;
-        uint32_t r = s < P.n_slots ? (SIGMA ? P.slot_row[s] : s) : 0xffffffffu;
-        uint32_t len = r < P.n_rows ? P.row_len[s] : 0u;
-        uint64_t off = s < P.n_slots ? P.chunk_off[s >> 5] : 0u;
-        uint64_t end = s < P.n_slots ? P.chunk_off[(s >> 5) + 1] : 0u;
-#pragma unroll 1
-        for (uint32_t j = 0; j < kWaveChunks; ++j) {
-            const uint32_t sn = s + 32u;
-            uint32_t rn = 0xffffffffu, lenn = 0u;
-            uint64_t offn = 0u, endn = 0u;
-            if (j + 1 < kWaveChunks && sn < P.n_slots) {
-                rn = SIGMA ? P.slot_row[sn] : sn;
-                lenn = rn < P.n_rows ? P.row_len[sn] : 0u;
-                offn = P.chunk_off[sn >> 5];
-                endn = P.chunk_off[(sn >> 5) + 1];
-            }
-            if (r < P.n_rows || P.trace) {
-                const uint32_t L = (uint32_t)((end - off) >> 5);
-                const double acc = r < P.n_rows ? wave_row(P, off, L, lane, len, src, pol, q == q0) : 0.0;
-                if (P.trace) {  // every lane's inputs are final here, no result is stored yet
-                    __syncwarp();
-                    if (lane == 0) {
-                        const unsigned long long ts = global_ns();
-                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T)] = ts;
-                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + 1] = ts;
-                    }
-                    __syncwarp();
-                }
-                if (r < P.n_rows) wave_epilogue<KIND, SIGMA>(P, s, r, q, q0, src, acc);
-            }
-            s = sn, r = rn, len = lenn, off = offn, end = endn;
-        }
-        t = ticket(kn);
-        if (t >= t1) break;
-        kn = claim();
-        code = P.tickets[t];
+    uint32_t tn = ticket(claim());
+    uint4 d = t < t1 ? ld_desc(P.wdesc + t) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 dn = tn < t1 ? ld_desc(P.wdesc + tn) : make_uint4(0u, 0u, 0u, 0u);
+    uint32_t kc = claim();
+    if (lane == 0) {
+        if (t < t1) wave_stage<SIGMA>(P, d, q0, q1, ring_s, bar0);
+        if (tn < t1) wave_stage<SIGMA>(P, dn, q0, q1, ring_s + kWaveStageBytes, bar0 + 8u);
     }
+    uint32_t st = 0, phase = 0;  // phase: bit i = parity of stage i's next completion
+    while (t < t1) {
+        const uint32_t tnn = ticket(kc);
+        uint4 dnn = make_uint4(0u, 0u, 0u, 0u);
+        if (tnn < t1) {
+            dnn = ld_desc(P.wdesc + tnn);
+            kc = claim();
+        }
+        {  // wait for this ticket's stage
+            const uint32_t bar = bar0 + 8u * st, par = (phase >> st) & 1u;
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                    : "=r"(done)
+                    : "r"(bar), "r"(par)
+                    : "memory");
+            phase ^= 1u << st;
+        }
+        const char* stage = ring + st * kWaveStageBytes;
+        const uint32_t T = d.y;
+        const uint32_t q = q0 + d.z;
+        // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
+        // (q-1) * vstride into each gather's index arithmetic)
+        const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
+        const bool narrow = wave_narrow(d.w);
+        uint32_t rr[C], len[C];
+        double acc[C];
+        {
+            uint32_t off = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const uint32_t s = T * kWaveRows + c * 32u + lane;
+                if (narrow) {
+                    rr[c] = SIGMA ? reinterpret_cast<const uint32_t*>(stage + off + 128)[lane] : s;
+                    len[c] = rr[c] < P.n_rows ? reinterpret_cast<const uint32_t*>(stage + off)[lane] : 0u;
+                } else {
+                    const char* g = P.wrec + ((uint64_t)P.wrec_off[T * C + c]) * 16u;
+                    rr[c] = SIGMA ? __ldg(reinterpret_cast<const uint32_t*>(g + 128) + lane) : s;
+                    len[c] = rr[c] < P.n_rows ? __ldg(reinterpret_cast<const uint32_t*>(g) + lane) : 0u;
+                }
+                off += hdr + 384u * ((d.w >> (4 * c)) & 15u);
+            }
+        }
+        const uint32_t L0 = d.w & 15u;
+        bool uniform = narrow;
+#pragma unroll
+        for (int c = 1; c < C; ++c) uniform &= ((d.w >> (4 * c)) & 15u) == L0;
+        if (uniform && L0 > 0) {
+            double x[C][8];
+            switch (L0) {
+                case 1: wave_multi<1, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 2: wave_multi<2, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 3: wave_multi<3, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 4: wave_multi<4, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 5: wave_multi<5, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 6: wave_multi<6, hdr, C>(stage, lane, len, src, x, acc); break;
+                case 7: wave_multi<7, hdr, C>(stage, lane, len, src, x, acc); break;
+                default: wave_multi<8, hdr, C>(stage, lane, len, src, x, acc); break;
+            }
+            // An empty (signalling-NaN) value makes a sum NaN: only then look at the values (slice
+            // q0-1 is complete and may hold any bit pattern: never checked).
+            if (q != q0) {
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (is_nan_bits(acc[c])) {
+                        bool miss = false;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) miss |= wave_empty(x[c][j]);
+                        if (miss) acc[c] = wave_redo(stage + c * (hdr + 384u * L0), hdr, L0, lane, len[c], src, x[c], P.dbg);
+                    }
+            }
+        } else {
+            // mixed widths (or a wide chunk): chunk by chunk
+            uint32_t off = 0;
+#pragma unroll 1
+            for (int c = 0; c < C; ++c) {
+                const uint32_t Lc = (d.w >> (4 * c)) & 15u;
+                const char* sc = stage + off;
+                off += hdr + 384u * Lc;
+                if (!narrow) {
+                    const uint32_t o = P.wrec_off[T * C + c];
+                    const uint32_t L = (((P.wrec_off[T * C + c + 1] - o) * 16u) - hdr) / 384u;
+                    acc[c] = wave_row_slow(P.wrec + (uint64_t)o * 16u, hdr, L, lane, len[c], src, q == q0, P.dbg);
+                    continue;
+                }
+                double x[8];
+                double a = 0.0;
+                switch (Lc) {
+                    case 0: for (int j = 0; j < 8; ++j) x[j] = 0.0; break;
+                    case 1: a = wave_dot<1>(sc, hdr, lane, len[c], src, x); break;
+                    case 2: a = wave_dot<2>(sc, hdr, lane, len[c], src, x); break;
+                    case 3: a = wave_dot<3>(sc, hdr, lane, len[c], src, x); break;
+                    case 4: a = wave_dot<4>(sc, hdr, lane, len[c], src, x); break;
+                    case 5: a = wave_dot<5>(sc, hdr, lane, len[c], src, x); break;
+                    case 6: a = wave_dot<6>(sc, hdr, lane, len[c], src, x); break;
+                    case 7: a = wave_dot<7>(sc, hdr, lane, len[c], src, x); break;
+                    default: a = wave_dot<8>(sc, hdr, lane, len[c], src, x); break;
+                }
+                if (q != q0 && is_nan_bits(a)) {
+                    bool miss = false;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
+                    if (miss) a = wave_redo(sc, hdr, Lc, lane, len[c], src, x, P.dbg);
+                }
+                acc[c] = a;
+            }
+        }
+        __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
+        if (lane == 0 && tnn < t1) wave_stage<SIGMA>(P, dnn, q0, q1, ring_s + st * kWaveStageBytes, bar0 + 8u * st);
+        if (P.trace) {  // every lane's inputs are final here, no result is stored yet
+            if (lane == 0) {
+                const unsigned long long ts = global_ns();
+                P.trace[2ull * ((uint64_t)q * P.n_tiles + T)] = ts;
+                P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + 1] = ts;
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            if (rr[c] < P.n_rows) wave_epilogue<KIND, SIGMA>(P, T * kWaveRows + c * 32u + lane, rr[c], q, q0, src, acc[c]);
+        t = tn, d = dn, tn = tnn, dn = dnn;
+        st ^= 1u;
+    }
+}
+
+// Chunk records from the executor's SELL arrays: one warp per chunk; chunks past the SELL (the
+// last tile's padding) get an empty record (lengths 0, slot rows ~0).
+__global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __restrict__ vals,
+                            const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
+                            const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rec,
+                            const uint32_t* __restrict__ rec_off, char* __restrict__ rec) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_rec;
+         T += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        char* r = rec + (uint64_t)rec_off[T] * 16u;
+        const bool real = T < n_chunks;
+        reinterpret_cast<uint32_t*>(r)[lane] = real ? row_len[T * 32 + lane] : 0u;
+        uint32_t hdr = 128;
+        if (slot_row) {
+            reinterpret_cast<uint32_t*>(r + 128)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
+            hdr = 256;
+        }
+        if (!real) continue;
+        const uint64_t o = chunk_off[T], ne = chunk_off[T + 1] - o;
+        uint32_t* rc = reinterpret_cast<uint32_t*>(r + hdr);
+        double* rv = reinterpret_cast<double*>(r + hdr + 4 * ne);
+        for (uint64_t e = lane; e < ne; e += 32) {
+            rc[e] = cols[o + e];
+            rv[e] = vals[o + e];
+        }
+    }
+}
+
+// Descriptors of a pass's tickets from the host codes (T | q << 24, kLastUse ignored: the last use
+// is q == q1).
+__global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
+                            uint32_t hdr, uint32_t q0, uint4* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t code = codes[i];
+        const uint32_t T = code & 0xffffffu, q = (code >> 24) & 63u;
+        uint32_t w = 0;
+        for (uint32_t c = 0; c < kWaveChunks; ++c) {
+            const uint32_t L = ((rec_off[T * kWaveChunks + c + 1] - rec_off[T * kWaveChunks + c]) * 16u - hdr) / 384u;
+            w |= (L < kWaveWideL ? L : kWaveWideL) << (4 * c);
+        }
+        out[i] = make_uint4(rec_off[T * kWaveChunks], T, q - q0, w);
+    }
+}
+
+__global__ void k_l2_policies(uint64_t* out) {
+    out[0] = l2_policy_first();
+    out[1] = l2_policy_last();
 }
 
 __global__ void k_wave_fill(double* __restrict__ V, uint64_t vstride, uint64_t n, uint32_t q_lo, uint32_t q_hi) {
@@ -1953,7 +2248,7 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
     // schedule instead of by timing), unless forced with the "pass" knob.
     int P = p;
     if (ctx->pass_powers > 0) {
-        P = std::min<int>(p, (int)ctx->pass_powers);
+        P = std::min<int>({p, (int)ctx->pass_powers, kWaveMaxPass});
     } else {
         const uint64_t budget =
             ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes * 6 / 10;
@@ -2011,14 +2306,40 @@ __global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* 
 void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
     cudaStream_t st = ctx->stream;
     const uint32_t nt = E.n_tiles;
-    {  // matrix + vector bytes one tile-power touches (the live-window model of wave_order)
-        std::vector<uint64_t> off(E.S->n_chunks + 1);
+    {  // matrix + vector bytes one tile-power touches (the live-window model of wave_order), and the
+       // chunk records (kWaveChunks per tile; the last tile padded with empty records)
+        const uint32_t nc = E.S->n_chunks;
+        const uint64_t nrec = (uint64_t)nt * kWaveChunks;
+        std::vector<uint64_t> off((uint64_t)nc + 1);
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E.S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
         MPKG_CUDA(cudaStreamSynchronize(st));
+        auto ent = [&](uint64_t c) { return c < nc ? off[c + 1] - off[c] : 0ull; };
         E.tile_bytes.assign(nt, 0);
-        for (uint32_t T = 0; T < nt && (uint64_t)T * kWaveChunks < E.S->n_chunks; ++T)
-            E.tile_bytes[T] = 12 * (off[std::min<uint64_t>((uint64_t)(T + 1) * kWaveChunks, E.S->n_chunks)] -
-                                    off[(uint64_t)T * kWaveChunks]) + 24ull * kWaveRows;
+        const uint32_t hdr = wave_hdr_bytes(E.order >= 1);
+        std::vector<uint32_t> ro(nrec + 1);
+        uint64_t acc = 0;
+        for (uint64_t c = 0; c < nrec; ++c) {
+            ro[c] = (uint32_t)acc;
+            acc += (hdr + 12 * ent(c)) / 16;  // 32 L entries: 384 L bytes
+            if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
+            E.tile_bytes[c / kWaveChunks] += 12 * ent(c) + 24ull * 32;
+        }
+        ro[nrec] = (uint32_t)acc;
+        E.wrec_off.alloc(nrec + 1);
+        E.wrec.alloc(std::max<uint64_t>(acc * 16, 16));
+        MPKG_CUDA(cudaMemcpyAsync(E.wrec_off.p, ro.data(), 4 * ro.size(), cudaMemcpyHostToDevice, st));
+        if (nrec) {
+            k_wave_pack<<<grid_for(nrec * 32, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                E.S->cols.p, E.S->vals.p, E.S->row_len.p, E.order >= 1 ? E.slot_row.p : nullptr, E.S->chunk_off.p,
+                nc, (uint32_t)nrec, E.wrec_off.p, E.wrec.p);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        DevBuf<uint64_t> pol(2);
+        k_l2_policies<<<1, 1, 0, st>>>(pol.p);
+        MPKG_LAUNCH_CHECK();
+        MPKG_CUDA(cudaMemcpyAsync(E.wave_pol, pol.p, 16, cudaMemcpyDeviceToHost, st));
+        MPKG_CUDA(cudaStreamSynchronize(st));
     }
     std::vector<uint32_t> lp = Pl->level_ptr;
     if (lp.empty() || lp.back() != A->n_rows) lp = {0, A->n_rows};  // no level info: one level
@@ -2095,14 +2416,14 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     if (it != E.wave.end()) return it->second;
     Executor::Wave W;
     const uint64_t budget = ctx->l2_budget > 0 ? (uint64_t)ctx->l2_budget : ctx->l2_bytes * 6 / 10;
-    const int64_t warps = (int64_t)E.wave_grid * 8;
+    const int64_t warps = (int64_t)E.wave_grid * kWaveWarps;
     auto slack_for = [&](int len) -> int64_t {
         if (ctx->slack >= 0) return std::max<int64_t>(ctx->slack, 1);
         return std::max<int64_t>(1, (warps * 11 / 5 + len - 1) / len);
     };
-    int P = std::min(p, kMaxFusedP);
+    int P = std::min(p, kWaveMaxPass);
     if (ctx->pass_powers > 0) {
-        P = std::min<int>(p, (int)ctx->pass_powers);
+        P = std::min<int>({p, (int)ctx->pass_powers, kWaveMaxPass});
         W.window = wave_order(E, 1, P, slack_for(P), nullptr);
     } else {
         for (; P >= 1; --P) {
@@ -2126,22 +2447,29 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     W.q_begin.push_back(q0);
     W.pass_len = (p + n_pass - 1) / n_pass;
     W.tickets.alloc(std::max<size_t>(codes.size(), 1));
+    W.desc.alloc(std::max<size_t>(codes.size(), 1));
     if (!codes.empty())
         MPKG_CUDA(cudaMemcpyAsync(W.tickets.p, codes.data(), sizeof(uint32_t) * codes.size(),
                                   cudaMemcpyHostToDevice, ctx->stream));
+    for (int j = 0; j < n_pass; ++j) {
+        const uint64_t b = W.t_begin[j], e = W.t_begin[j + 1];
+        if (e > b) {
+            k_wave_desc<<<grid_for(e - b, 256, (unsigned)ctx->sm_count * 8u), 256, 0, ctx->stream>>>(
+                W.tickets.p + b, e - b, E.wrec_off.p, wave_hdr_bytes(E.order >= 1), (uint32_t)W.q_begin[j],
+                W.desc.p + b);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+    }
     MPKG_CUDA(cudaStreamSynchronize(ctx->stream));
     E.pass_len[p] = W.pass_len;
     return E.wave.emplace(p, std::move(W)).first->second;
 }
 
-// minb: resident CTAs per SM the build targets (registers 80 / 64 / 48 / 40 for 3 / 4 / 5 / 6)
-void* wave_fn(int kind, bool sigma, int minb) {
-#define MPKG_WAVE_FNS(M) {(void*)k_mpk_wave<0, false, M>, (void*)k_mpk_wave<0, true, M>, \
-                          (void*)k_mpk_wave<1, false, M>, (void*)k_mpk_wave<1, true, M>}
-    static void* const fns[4][4] = {MPKG_WAVE_FNS(3), MPKG_WAVE_FNS(4), MPKG_WAVE_FNS(5), MPKG_WAVE_FNS(6)};
-#undef MPKG_WAVE_FNS
-    const int m = minb < 3 ? 0 : minb > 6 ? 3 : minb - 3;
-    return fns[m][kind * 2 + (sigma ? 1 : 0)];
+void* wave_fn(int kind, bool sigma) {
+    static void* const fns[4] = {(void*)k_mpk_wave<0, false>, (void*)k_mpk_wave<0, true>,
+                                 (void*)k_mpk_wave<1, false>, (void*)k_mpk_wave<1, true>};
+    return fns[kind * 2 + (sigma ? 1 : 0)];
 }
 
 template <int KIND, int G>
@@ -2238,18 +2566,18 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     const bool wave = !sweep && ctx->schedule != 1;
     if (wave && a.kind == 2) fail(MPKG_EINTERNAL, "mpk: the wave schedule has no polynomial epilogue");
     if (!sweep && !wave && !E.fused_ready) build_fused(ctx, Pl, A, &E);
-    const int wminb = ctx->wave_minb > 0 ? (int)ctx->wave_minb : 4;
-    if (wave && (!E.wave_grid || E.wave_minb != wminb)) {
+    if (wave && !E.wave_grid) {
         int occ = 1 << 30;
         for (int k = 0; k < 4; ++k) {
             int o = 0;
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wave_fn(k / 2, k % 2, wminb), 256, 0));
+            void* fn = wave_fn(k / 2, k % 2);
+            MPKG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWaveSmem));
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWaveThreads, kWaveSmem));
             occ = std::min(occ, o);
         }
         if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
         if (!E.wave_grid) build_wave(ctx, Pl, A, E);
         E.wave_grid = std::max(1, occ) * ctx->sm_count;
-        E.wave_minb = wminb;
         E.wave.clear();  // the slack follows the warps in flight
         E.counter.alloc(kWaveStreams * 32 + 32);
     }
@@ -2268,6 +2596,11 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.row_len = S.row_len.p;
     P.slot_row = sigma ? E.slot_row.p : nullptr;
     P.tickets = tk.p;
+    P.wdesc = wave ? W->desc.p : nullptr;
+    P.wrec = E.wrec.p;
+    P.wrec_off = E.wrec_off.p;
+    P.pol_first = E.wave_pol[0];
+    P.pol_last = E.wave_pol[1];
     P.dep_ptr = E.dep_ptr.p;
     P.dep_lo = E.dep_lo.p;
     P.dep_hi = E.dep_hi.p;
@@ -2573,7 +2906,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (wave) {
         // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
         // host block, the pass's slices go to the host while the next pass runs
-        void* fn = wave_fn(a.kind, sigma, wminb);
+        void* fn = wave_fn(a.kind, sigma);
         P.counter = E.counter.p;
         P.dbg = getenv("MPKG_WAVE_DEBUG") ? E.counter.p + kWaveStreams * 32 : nullptr;
         for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
@@ -2586,17 +2919,20 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
                 MPKG_LAUNCH_CHECK();
                 ctx->launches += 1;
             }
-            const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(E.wave_grid, (t1 - t0 + 7) / 8));
+            const unsigned g = (unsigned)std::max<uint64_t>(
+                1, std::min<uint64_t>(E.wave_grid, (t1 - t0 + kWaveWarps - 1) / kWaveWarps));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(g);
-            cfg.blockDim = dim3(256);
+            cfg.blockDim = dim3(kWaveThreads);
+            cfg.dynamicSmemBytes = kWaveSmem;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            void* args[] = {(void*)&P, (void*)&t0, (void*)&t1, (void*)&q0};
+            uint32_t q1a = q1;
+            void* args[] = {(void*)&P, (void*)&t0, (void*)&t1, (void*)&q0, (void*)&q1a};
             MPKG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
             if (j + 2 < W->t_begin.size()) ctx->launches += 1;
             if (to_host)
