@@ -197,7 +197,7 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     pg = None
-    if world > 1:
+    if world > 1 or os.environ.get("MPKG_FORCE_SHARDED"):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # NCCL between GPUs; MPKG_DIST_BACKEND=gloo only for the single-GPU smoke test of the
@@ -631,6 +631,193 @@ def run_sharded(args, cfgd, ctx, A, ls, Ap, x_perm, p, rank, world, local, dist,
         sys.exit(3)
 
 
+def _bits_checksum(t, lo, hi):
+    """Order-sensitive 64-bit checksums of rows [lo, hi) of every slice of a (p+1, rows) block
+    (int64 views, wrap-around sums): a size-independent bitwise parity probe."""
+    import torch
+    v = t[:, lo:hi].contiguous().view(torch.int64)
+    w = (torch.arange(hi - lo, device=v.device, dtype=torch.int64) % 65521) + 1
+    return torch.stack([v.sum(1), (v * w).sum(1)], 1).cpu()
+
+
+def run_sharded_nccl(args, cfgd, rank, world, local, dist):
+    """N > 1 over NCCL through the C-ABI shard layer (mpkg_dist_*, csrc/dist.cu): rank 0 alone
+    generates the matrix, builds the levels and A_perm, and partitions the levels (balanced by nnz);
+    level_ptr and the bounds are broadcast; every rank receives only its own block A_perm[g0:g1,
+    g0:g1] and its own rows of x from rank 0.  A step = one halo exchange of x (grouped ncclSend /
+    ncclRecv into a preallocated buffer) + the local MPK; every rank owns a fixed share of ONE
+    matrix (strong scaling).  value = the global MPK flops / the slowest rank's step time."""
+    import torch
+
+    import paper_2309_02228_b200 as mpkg
+    from paper_2309_02228_b200 import multi
+    if cfgd["kind"] != "plain":
+        raise SystemExit("multi-GPU bench runs the plain MPK configs (c1, c2, c3, c5)")
+    p = cfgd["p"]
+    dev = torch.device("cuda", local)
+    ctx = mpkg.Context(local)
+    ctx.set_param("order", args.order)
+    ctx.set_param("schedule", args.schedule)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def sync():
+        ctx.synchronize()
+        torch.cuda.synchronize()
+
+    prep = {}
+    uid = [multi.NcclDist.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    D = multi.NcclDist(ctx, world, rank, uid[0])
+    t0 = time.perf_counter()
+    Ap = ls = d_full = None
+    meta = np.zeros(3, np.uint64)
+    if rank == 0:
+        A = make_matrix(args.config, args.seed)
+        dA = ctx.csr(A)
+        ls = ctx.build_levels(dA)
+        Ap = ctx.permute(dA, ls)
+        del dA
+        lp = np.asarray(ls.level_ptr, np.uint32)
+        lens = np.diff(A.row_ptr.astype(np.int64))[ls.inv_perm.astype(np.int64)]
+        nnz_before = np.concatenate([[0], np.cumsum(lens)])[lp.astype(np.int64)]
+        bounds = multi.dist_partition(lp, nnz_before, world)
+        x_perm = ctx.permute_vector(mpkg.random_vector(A.n_rows, args.seed + 2), ls.perm)
+        d_full = torch.from_numpy(x_perm).to(dev)
+        meta[:] = (len(lp) - 1, A.n_rows, A.nnz)
+        del A
+    D.bcast_host(meta, 0)
+    nl, n, nnz = (int(v) for v in meta)
+    if rank != 0:
+        lp, bounds = np.zeros(nl + 1, np.uint32), np.zeros(world + 1, np.uint32)
+    D.bcast_host(lp, 0)
+    D.bcast_host(bounds, 0)
+    prep["root_preprocess_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    D.set_plan(lp, bounds, p)
+    info = D.info()
+    o0, o1 = info["own"]
+    g0, g1 = info["local"]
+    n_local = g1 - g0
+    A_loc = D.scatter_blocks(0, Ap)
+    x_own = torch.empty(max(o1 - o0, 1), dtype=torch.float64, device=dev)
+    D.scatter_rows(0, d_full.data_ptr() if d_full is not None else 0, x_own.data_ptr())
+    L0, L1 = int(bounds[rank]), int(bounds[rank + 1])
+    llp = multi.local_level_ptr(lp, L0, L1, p)
+    ident = np.arange(n_local, dtype=np.uint32)
+    lls = ctx.levels_from_host(np.zeros(n_local, np.uint32), ident, ident, llp)
+    plan = ctx.group_levels(lls, A_loc, ctx.device_info()["l2_bytes"], p)
+    blk = torch.empty((p + 1) * max(n_local, 1), dtype=torch.float64, device=dev)
+    sync()
+    prep["shard_setup_s"] = time.perf_counter() - t0
+
+    def step():
+        D.mpk(plan, A_loc, x_own.data_ptr(), p, blk.data_ptr(), max(n_local, 1), p + 1)
+
+    step()
+    sync()
+    # parity: every rank's own rows == rank 0's single-GPU one-launch-per-power result, bit for bit
+    # (order-sensitive checksums of the bit patterns, compared on rank 0)
+    a0, a1 = o0 - g0, o1 - g0
+    mine = _bits_checksum(blk.view(p + 1, -1), a0, a1) if n_local else torch.zeros(p + 1, 2, dtype=torch.int64)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (o0, o1, mine))
+    parity = True
+    if rank == 0:
+        ref = torch.empty((p + 1) * n, dtype=torch.float64, device=dev)
+        ctx.baseline_mpk_dev(Ap, d_full.data_ptr(), p, ref.data_ptr(), n, p + 1)
+        sync()
+        for r0, r1, cs in gathered:
+            if r1 > r0:
+                parity &= bool(torch.equal(cs, _bits_checksum(ref.view(p + 1, n), r0, r1)))
+        del ref
+    del Ap, d_full
+    torch.cuda.empty_cache()
+    for _ in range(args.warmup):
+        step()
+    sync()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    sync()
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("mpk_timed")
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        sync()
+        torch.cuda.nvtx.range_pop()
+    dist.barrier()
+    launches = ctx.launch_count() - launches0
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    ctx.set_param("kernel_timing", 1)
+    for _ in range(args.steps):
+        step()
+    sync()
+    k_total, k_count, _ = ctx.kernel_times()
+    kernel_ms = k_total / max(k_count, 1)
+    ctx.set_param("kernel_timing", 0)
+    dist.barrier()
+    # e2e: own x from pinned host memory, exchange + local MPK, own rows back to the host
+    hx = x_own.cpu().pin_memory()
+    hout = torch.empty((p + 1, max(o1 - o0, 0)), dtype=torch.float64).pin_memory()
+    ts = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            x_own.copy_(hx, non_blocking=True)
+            step()
+            if o1 > o0:
+                hout.copy_(blk.view(p + 1, -1)[:, a0:a1], non_blocking=True)
+            b_.record(stream)
+        b_.synchronize()
+        ts.append(a.elapsed_time(b_))
+    e_ms = statistics.median(ts)
+    t = torch.tensor([step_ms, kernel_ms, e_ms, float(not parity)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, kernel_ms, e_ms, bad = t.tolist()
+    parity = bad == 0.0
+    flops = 2.0 * nnz * p
+    value = flops / (step_ms * 1e-3) * 1e-9
+    clocks = clk.summary()
+    b_loc = 12 * A_loc.nnz + 4 * (n_local + 1) + 8 * n_local * (1 + p)
+    peak, peak_src = measured_peak()
+    achieved = b_loc / (kernel_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators for the BASELINE.json config, DESIGN.md §6)",
+            "config": config_dict(args.config, cfgd, n, nnz, world),
+            "parity": ("own rows == single-GPU baseline bitwise (checksums of every rank's own rows)"
+                       if parity else "MISMATCH"),
+            "details": {"mode": "bitwise", "backend": "nccl (mpkg_dist_* C ABI)",
+                        "rank0_shard": {"own_rows": [o0, o1], "local_rows": [g0, g1],
+                                        "local_nnz": A_loc.nnz, "halo_send_bytes": info["send_bytes"],
+                                        "halo_recv_bytes": info["recv_bytes"]},
+                        "executor": plan.exec_info(), "preprocess_s": prep},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes": b_loc, "kernel_ms": kernel_ms,
+                         "kernel_launches_timed": k_count, "peak_source": peak_src,
+                         "note": "per rank (slowest): local single-pass bytes / local MPK time"},
+            "cpu_baseline": None,
+            "e2e": {"value": flops / (e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * (p + 1),
+                    "ms_per_step": e_ms, "note": "per rank: own x in, own rows of y_0..y_p out"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    D.close()
+    dist.destroy_process_group()
+    if not parity:
+        sys.exit(3)
+
+
 def _ncu_traffic(name):
     """DRAM read + write bytes of one step from the committed ncu summary (profiles/), or None."""
     prof = ROOT / "profiles" / f"ncu_{name}.json"
@@ -828,7 +1015,7 @@ def main():
     ap.add_argument("--order", type=int, default=-1,
                     help="-1 auto, 0 A_perm order, 1 CM inside levels, 2 longest rows first")
     ap.add_argument("--schedule", type=int, default=0,
-                    help="0 auto, 1 fused tile-DAG kernel, 2 one launch per power")
+                    help="0 auto, 1 fused tile-DAG kernel, 2 one launch per power, 3 wave (cross-power L2 reuse)")
     ap.add_argument("--mode", default="bitwise", choices=["bitwise", "fast"],
                     help="fast: long rows reduced in parallel, checked to 1e-12 inf-norm (mpkg.h)")
     ap.add_argument("--kernel", type=int, default=0, help="fused variant: 0 lean, 1 staged, 2 warp-tile, 4 async")
@@ -866,6 +1053,10 @@ def main():
     rank, world, local, dist = dist_setup(args.gpus)
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
+    if dist is not None and dist.get_backend() == "nccl":
+        # the C-ABI shard layer: only rank 0 builds the matrix (MPKG_FORCE_SHARDED=1 exercises it
+        # at world 1 as well)
+        return run_sharded_nccl(args, cfgd, rank, world, local, dist)
     p = cfgd["p"]
     t0 = time.perf_counter()
     A = make_matrix(args.config, args.seed)

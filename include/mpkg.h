@@ -59,6 +59,7 @@ typedef struct mpkg_plan_s* mpkg_plan_t;
 typedef struct mpkg_jacobi_s* mpkg_jacobi_t;
 typedef struct mpkg_gs2_s* mpkg_gs2_t;
 typedef struct mpkg_host_csr_s* mpkg_host_csr_t;
+typedef struct mpkg_dist_s* mpkg_dist_t;
 
 /* ---- errors / version ------------------------------------------------------------------- */
 const char* mpkg_last_error(void);
@@ -75,9 +76,10 @@ int mpkg_ctx_device_info(mpkg_ctx_t ctx, int* sm_count, size_t* l2_bytes, size_t
 /* Executor tuning knobs: "slack" (tickets between a dependency and its
  * consumer in the list schedule; -1 = auto), "order" (0: A_perm order, 1: Cuthill-McKee inside
  * levels), "pass" (force powers per fused pass; 0 = auto from the L2 budget), "l2_budget" (live
- * window bytes; 0 = L2/2), "tile_rows" (fixed 256); "kernel_timing" = 1 records a CUDA event
+ * window bytes; 0 = 0.6 x L2), "tile_rows" (fixed 256); "kernel_timing" = 1 records a CUDA event
  * pair around every power-kernel launch on the context stream; "schedule" (0 auto, 1 fused
- * tile-DAG kernel, 2 one launch per power); "graphs" (replay the per-power launches as one CUDA
+ * tile-DAG kernel, 2 one launch per power, 3 the wave: passes of p' powers with cross-power L2
+ * reuse); "trace" (1: per (tile, power) device timestamps, mpkg_plan_exec_trace); "graphs" (replay the per-power launches as one CUDA
  * graph, default 1); "pdl" (default 1: programmatic dependent launch between consecutive
  * powers, hiding the launch gap); "resident" (default 0; 1: a matrix that fits half the L2 together with its p+1
  * working vectors runs all powers of a device-pointer call in one cooperative launch);
@@ -204,7 +206,11 @@ int mpkg_baseline_mpk(mpkg_ctx_t ctx, mpkg_csr_t A, const double* x, int p_m, do
 int mpkg_baseline_mpk_dev(mpkg_ctx_t ctx, mpkg_csr_t A, const double* d_x, int p_m,
                           double* d_block, uint64_t block_rows, uint64_t block_slices);
 
-/* mpk.hpp:81-106 mpk: one fused, temporally blocked kernel (device-side dependency flags).
+/* mpk.hpp:81-106 mpk.  The executor picks the schedule (mpkg_ctx_set_param "schedule", 0 = auto):
+ * the wave -- one persistent launch per pass of p' powers with cross-power L2 reuse, tickets
+ * synchronised by value -- for large matrices whose rows have at most 8 entries, otherwise one
+ * launch per power replayed as a CUDA graph; the fused tile-DAG kernel (device-side completion
+ * flags) on request.  mpkg_plan_exec_info reports which ran.
  * A_perm must be level-permuted, x in permuted order; p_m <= the plan's p_m (execute.hpp:81-83).
  * Bitwise equal to mpkg_baseline_mpk on A_perm in MPKG_MODE_BITWISE. */
 int mpkg_mpk(mpkg_ctx_t ctx, mpkg_plan_t P, mpkg_csr_t A_perm, const double* x, int p_m,
@@ -327,6 +333,42 @@ int mpkg_poly_apply(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G,
 int mpkg_poly_apply_dev(mpkg_ctx_t ctx, mpkg_csr_t A, mpkg_jacobi_t J, mpkg_gs2_t G,
                         const double* re, const double* im, int degree, mpkg_plan_t P,
                         const double* d_v, double* d_z);
+
+/* ---- multi-GPU level-range shards (csrc/dist.cu) -----------------------------
+ * No reference counterpart (the reference is single-node OpenMP); this is the C++ caller's view of
+ * multi.py.  Rank r owns the BFS levels [bounds[r], bounds[r+1]) of A_perm (balanced by nnz) and
+ * holds p ghost levels on each side; one halo exchange of x per MPK call, then the local MPK of its
+ * block A_perm[g0:g1, g0:g1]; own rows are bit-identical to the single-GPU result.
+ *
+ * Pure host functions (no GPU, no NCCL): nnz_before[L] = nonzeros in levels < L (n_levels+1
+ * entries); bounds has world+1 entries.  own / local: [first, end) global rows; send / recv:
+ * 2*world entries, the row range this rank sends to / receives from each rank (empty: lo == hi). */
+int mpkg_dist_partition(const uint32_t* level_ptr, uint32_t n_levels, const uint64_t* nnz_before,
+                        int world, uint32_t* bounds);
+int mpkg_dist_halo(const uint32_t* level_ptr, uint32_t n_levels, const uint32_t* bounds, int world,
+                   int rank, int p, uint32_t* own, uint32_t* local, uint32_t* send, uint32_t* recv);
+/* NCCL communicator (libnccl.so.2 loaded at run time; MPKG_EINTERNAL if absent).  The 128-byte id
+ * comes from mpkg_dist_unique_id on one rank and reaches the others by the caller's bootstrap. */
+int mpkg_dist_unique_id(void* id128);
+int mpkg_dist_create(mpkg_ctx_t ctx, const void* id128, int world, int rank, mpkg_dist_t* out);
+int mpkg_dist_destroy(mpkg_dist_t D);
+/* Broadcast of a host buffer from root (e.g. level_ptr and bounds before mpkg_dist_set_plan). */
+int mpkg_dist_bcast_host(mpkg_dist_t D, void* buf, uint64_t bytes, int root);
+/* The rank's halo plan for p powers; preallocates the local x buffer. */
+int mpkg_dist_set_plan(mpkg_dist_t D, const uint32_t* level_ptr, uint32_t n_levels,
+                       const uint32_t* bounds, int p);
+int mpkg_dist_info(mpkg_dist_t D, uint32_t* own, uint32_t* local, uint64_t* send_bytes,
+                   uint64_t* recv_bytes);
+/* One-time setup from a root that holds A_perm (and a device vector in A_perm order): every rank
+ * receives its local block / its own rows. */
+int mpkg_dist_scatter_blocks(mpkg_dist_t D, int root, mpkg_csr_t A_perm, mpkg_csr_t* A_local);
+int mpkg_dist_scatter_rows(mpkg_dist_t D, int root, const double* d_full, double* d_own);
+/* Per step: the halo exchange (grouped ncclSend / ncclRecv on the context's stream into the
+ * preallocated local x, whose device pointer is returned), and exchange + local mpkg_mpk_dev of
+ * the block (block_rows >= local rows; the own rows sit at own[0] - local[0]). */
+int mpkg_dist_exchange(mpkg_dist_t D, const double* d_x_own, double** d_x_local);
+int mpkg_dist_mpk(mpkg_dist_t D, mpkg_plan_t P, mpkg_csr_t A_local, const double* d_x_own, int p,
+                  double* d_block, uint64_t block_rows, uint64_t block_slices);
 
 /* ---- block orthogonalisation (ortho.hpp) --------------------------------
  * Blocks are column-major with leading dimension `rows` (consecutive VectorBlock slices).  The

@@ -96,6 +96,18 @@ _SIGS = {
     "mpkg_sstep_gs2_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_sstep_jacobi_dev": [P, P, P, P, P, P, i32, P, u64, u64],
     "mpkg_wavefront_schedule": [u32, i32, P, P, pu64],
+    "mpkg_dist_partition": [P, u32, P, i32, P],
+    "mpkg_dist_halo": [P, u32, P, i32, i32, i32, P, P, P, P],
+    "mpkg_dist_unique_id": [P],
+    "mpkg_dist_create": [P, P, i32, i32, C.POINTER(P)],
+    "mpkg_dist_destroy": [P],
+    "mpkg_dist_bcast_host": [P, P, u64, i32],
+    "mpkg_dist_set_plan": [P, P, u32, P, i32],
+    "mpkg_dist_info": [P, P, P, pu64, pu64],
+    "mpkg_dist_scatter_blocks": [P, i32, P, C.POINTER(P)],
+    "mpkg_dist_scatter_rows": [P, i32, P, P],
+    "mpkg_dist_exchange": [P, P, C.POINTER(P)],
+    "mpkg_dist_mpk": [P, P, P, P, i32, P, u64, u64],
     "mpkg_baseline_mpk": [P, P, P, i32, P, u64, u64],
     "mpkg_baseline_mpk_dev": [P, P, P, i32, P, u64, u64],
     "mpkg_mpk": [P, P, P, P, i32, P, u64, u64],

@@ -59,7 +59,7 @@ def build(force: bool = False) -> pathlib.Path:
     newest = max(o.stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", *map(str, objs), "-o", str(LIB),
-               "-lgomp"]
+               "-lgomp", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

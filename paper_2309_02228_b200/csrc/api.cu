@@ -9,6 +9,10 @@
 
 #include "device.h"
 
+namespace mpkg_detail {
+int g_sm_count = 0;
+}
+
 using namespace mpkg_detail;
 
 namespace mpkg_detail {
@@ -222,6 +226,7 @@ int mpkg_ctx_create(int device, mpkg_ctx_t* out) {
                                  std::to_string(prop.major) + std::to_string(prop.minor));
         }
         c->sm_count = prop.multiProcessorCount;
+        g_sm_count = c->sm_count;
         c->l2_bytes = prop.l2CacheSize;
         c->persist_max = prop.persistingL2CacheMaxSize;
         MPKG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

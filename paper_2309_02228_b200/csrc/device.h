@@ -224,7 +224,11 @@ inline void launch_maybe_pdl(bool pdl, void (*k)(Ex...), unsigned grid, unsigned
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
     } while (0)
 
-inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 32u) {
+// SM count of the device the last context was created on (queried in mpkg_ctx_create, never
+// assumed): the default grid cap of grid-stride kernels is 32 CTAs per SM.
+extern int g_sm_count;
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 0) {
+    if (cap == 0) cap = 32u * (unsigned)(g_sm_count > 0 ? g_sm_count : 1);
     uint64_t g = (work + block - 1) / block;
     if (g < 1) g = 1;
     if (g > cap) g = cap;

@@ -1,33 +1,26 @@
-// Fused, temporally blocked matrix power kernel: ONE persistent launch computes all p powers.
+// The MPK executor: y_k = A y_{k-1} (plain, shifted, polynomial epilogues) for k = 1..p over the
+// level-permuted matrix, bit-identical to the reference (rowdot.cuh's row formula).
 //
-// Reference behaviour replaced: execute.hpp:79-113 runs every (group, power) cell of the
-// diagonal wavefront (execute.hpp:59-72) with an OpenMP team and a barrier after every cell;
-// mpk.hpp:81-106 / 184-207 are its kernels.  Here:
-//   * rows of A_perm are executed in a GPU-private order sigma that stays inside each BFS level
-//     (reorder.cu: Cuthill-McKee within levels, or the identity); the executor keeps its own
-//     SELL-32 copy of A_perm in sigma order with columns relabelled to sigma slots and keeps the
-//     working vectors in sigma order, so 32 consecutive rows gather from a few cache lines;
-//     every result is also stored at its A_perm position in the caller's block;
-//   * the unit of work is a (tile, power) ticket, a tile being 128 consecutive sigma slots (one
-//     thread per row, bitwise row formula: rowdot.cuh).  A tile's SELL slice is one contiguous
-//     range of the column and value arrays, so it is staged into shared memory with two 1D TMA
-//     bulk copies (cp.async.bulk + mbarrier, double buffered); the copy for the NEXT claimed
-//     ticket is issued before the current ticket waits for its dependencies, so the matrix
-//     stream overlaps dependency waits and compute.  L2 hints: evict_last while the tile will be
-//     re-read in this pass, evict_first on its last use;
-//   * dependencies are tile-granular and derived from the sparsity pattern: tile T at power q
-//     needs power q-1 finished on every tile holding a column of T's rows, recorded per
-//     neighbouring level as a few tile ranges ("runs").  This is the boundary-level refinement
-//     the reference leaves as future work, strictly finer than its
-//     whole-neighbour-group rule (execute.hpp:23-28);
-//   * a per-tile flag done[T] = last finished power is published with st.release.gpu; waiters
-//     poll it with relaxed loads and acquire once; there is no grid-wide barrier;
-//   * tickets are claimed through one global atomic counter in a host-computed topological order
-//     (list schedule, powers sliced into passes whose live window fits the L2 budget), so a CTA
-//     only waits on tickets claimed earlier by running CTAs: deadlock-free without any
-//     co-residency assumption.
-// Results are bit-identical to the one-launch-per-power baseline (and so to the reference):
-// every row is computed by the same formula, from the same inputs, in any order.
+// Reference behaviour replaced: execute.hpp:79-113 runs every (group, power) cell of the diagonal
+// wavefront (execute.hpp:59-72) with an OpenMP team and a barrier after every cell; mpk.hpp:81-106 /
+// 184-207 are its kernels.  On the GPU there are three schedules ("schedule" knob, 0 = auto):
+//   * wave (3) -- the default for large matrices whose rows are at most 8 entries (C5, C1-like
+//     stencils): cross-power L2 reuse.  One persistent launch per PASS of p' powers; tickets (one
+//     32-row SELL chunk, one power) run in a host-computed skewed order so the p' power fronts trail
+//     each other by about a BFS level and a chunk's matrix slice, read from HBM by the first front,
+//     is re-read from L2 by the others.  p' is the plan's cache budget applied to this GPU's L2
+//     (plan.hpp:88-115).  Synchronisation is by value (signalling-NaN sentinel fill, no flags).  Each
+//     warp stages its next ticket's chunk record with one TMA bulk copy (k_mpk_wave);
+//   * sweeps (2) -- one launch per power (k_mpk_sweep, replayed as one CUDA graph), with hub rows on
+//     a side stream (k_long_rows_bitwise / k_coop_rows): the default otherwise (27-point stencils,
+//     R-MAT), where the wave's stage would not hold a chunk;
+//   * fused tile-DAG (1) -- all p powers in one launch, per-tile completion flags, TMA-staged tiles
+//     (k_mpk_lean and variants): kept, tested, measured slower.
+// Rows execute in a GPU-private order sigma that stays inside each BFS level (reorder.cu:
+// Cuthill-McKee within levels, longest rows first, or the identity); every result is also stored
+// at its A_perm position in the caller's block.  Results are bit-identical to the
+// one-launch-per-power baseline (and so to the reference): every row is computed by the same
+// formula, from the same inputs, in any order.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

@@ -94,14 +94,14 @@ def local_level_ptr(level_ptr, L0: int, L1: int, p: int):
     return (lp[a:b + 1] - lp[a]).astype(np.uint32)
 
 
-def exchange_halo(x_own, plans: Sequence[HaloPlan], rank: int, dist, group=None):
+def exchange_halo(x_own, plans: Sequence[HaloPlan], rank: int, dist, group=None, stats=None):
     """The one collective of the level-partitioned MPK: builds this rank's local x (rows
     [g0, g1)) from the owners' pieces with grouped point-to-point transfers.  `x_own` is a torch
     tensor holding rows [o0, o1); the result lives on the same device (NCCL over NVLink between
     GPUs, gloo in the CPU tests).  Every rank calls this with its own x_own."""
     import torch
     if x_own.is_cuda and dist.get_backend(group) == "gloo":  # gloo moves host tensors only
-        return exchange_halo(x_own.cpu(), plans, rank, dist, group).to(x_own.device)
+        return exchange_halo(x_own.cpu(), plans, rank, dist, group, stats).to(x_own.device)
     me = plans[rank]
     g0, g1 = me.local_rows
     o0 = me.own_rows[0]
@@ -113,11 +113,15 @@ def exchange_halo(x_own, plans: Sequence[HaloPlan], rank: int, dist, group=None)
         for s, r0, r1 in other.pieces:
             if s == rank:
                 ops.append(dist.P2POp(dist.isend, x_own[r0 - o0:r1 - o0].contiguous(), other.rank, group))
+                if stats is not None:
+                    stats["send_bytes"] = stats.get("send_bytes", 0) + 8 * (r1 - r0)
     for s, r0, r1 in me.pieces:
         if s == rank:
             out[r0 - g0:r1 - g0] = x_own[r0 - o0:r1 - o0]
         else:
             ops.append(dist.P2POp(dist.irecv, out[r0 - g0:r1 - g0], s, group))
+            if stats is not None:
+                stats["recv_bytes"] = stats.get("recv_bytes", 0) + 8 * (r1 - r0)
     if ops:
         for rq in dist.batch_isend_irecv(ops):
             rq.wait()
@@ -221,3 +225,107 @@ class ShardedMPK:
                 self.ctx.mpk_dev(self.plan, self.A, x_loc.data_ptr(), self.p, block.data_ptr(),
                                  self.n_local, self.p + 1)
         return x_loc
+
+
+# ---- the C-ABI shard layer (csrc/dist.cu): the C++ caller's view of the same plan ------------------
+
+def _u32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def dist_partition(level_ptr, nnz_before, world: int) -> np.ndarray:
+    """mpkg_dist_partition: level bounds (world+1) balancing nnz; nnz_before[L] = nonzeros in
+    levels < L.  Same rule as partition_levels."""
+    import ctypes as C
+
+    from ._lib import check, lib
+    lp = _u32(level_ptr)
+    nb = np.ascontiguousarray(np.asarray(nnz_before, dtype=np.uint64))
+    out = np.empty(world + 1, np.uint32)
+    check(lib.mpkg_dist_partition(lp.ctypes.data, len(lp) - 1, nb.ctypes.data, world, out.ctypes.data))
+    return out
+
+
+def dist_halo(level_ptr, bounds, world: int, rank: int, p: int) -> dict:
+    """mpkg_dist_halo: own / local row ranges and the per-peer send / recv row ranges."""
+    from ._lib import check, lib
+    lp, b = _u32(level_ptr), _u32(bounds)
+    own, loc = np.empty(2, np.uint32), np.empty(2, np.uint32)
+    send, recv = np.empty(2 * world, np.uint32), np.empty(2 * world, np.uint32)
+    check(lib.mpkg_dist_halo(lp.ctypes.data, len(lp) - 1, b.ctypes.data, world, rank, p, own.ctypes.data,
+                             loc.ctypes.data, send.ctypes.data, recv.ctypes.data))
+    return {"own": tuple(int(v) for v in own), "local": tuple(int(v) for v in loc),
+            "send": [tuple(int(v) for v in send[2 * r:2 * r + 2]) for r in range(world)],
+            "recv": [tuple(int(v) for v in recv[2 * r:2 * r + 2]) for r in range(world)]}
+
+
+class NcclDist:
+    """One rank of the NCCL shard layer (mpkg_dist_*): communicator, halo plan with a
+    preallocated local-x buffer, one-time scatter of the blocks / own rows from a root, and the
+    per-step exchange + local MPK on the context's stream."""
+
+    def __init__(self, ctx, world: int, rank: int, uid: bytes):
+        import ctypes as C
+
+        from ._lib import check, lib
+        self.ctx, self.world, self.rank = ctx, world, rank
+        self._lib, self._check, self._C = lib, check, C
+        buf = C.create_string_buffer(bytes(uid), 128)
+        h = C.c_void_p()
+        check(lib.mpkg_dist_create(ctx.h, buf, world, rank, C.byref(h)))
+        self.h = h.value
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from ._lib import check, lib
+        buf = C.create_string_buffer(128)
+        check(lib.mpkg_dist_unique_id(buf))
+        return buf.raw
+
+    def bcast_host(self, arr: np.ndarray, root: int = 0) -> np.ndarray:
+        a = np.ascontiguousarray(arr)
+        self._check(self._lib.mpkg_dist_bcast_host(self.h, a.ctypes.data, a.nbytes, root))
+        return a
+
+    def set_plan(self, level_ptr, bounds, p: int):
+        lp, b = _u32(level_ptr), _u32(bounds)
+        self._check(self._lib.mpkg_dist_set_plan(self.h, lp.ctypes.data, len(lp) - 1, b.ctypes.data, p))
+        self.p = p
+
+    def info(self) -> dict:
+        C = self._C
+        own, loc = np.empty(2, np.uint32), np.empty(2, np.uint32)
+        sb, rb = C.c_uint64(), C.c_uint64()
+        self._check(self._lib.mpkg_dist_info(self.h, own.ctypes.data, loc.ctypes.data, C.byref(sb), C.byref(rb)))
+        return {"own": (int(own[0]), int(own[1])), "local": (int(loc[0]), int(loc[1])),
+                "send_bytes": sb.value, "recv_bytes": rb.value}
+
+    def scatter_blocks(self, root: int, A_perm=None):
+        from .api import DeviceCsr
+        C = self._C
+        h = C.c_void_p()
+        self._check(self._lib.mpkg_dist_scatter_blocks(self.h, root, A_perm.h if A_perm is not None else None,
+                                                       C.byref(h)))
+        return DeviceCsr(self.ctx, h.value)
+
+    def scatter_rows(self, root: int, d_full: int, d_own: int):
+        self._check(self._lib.mpkg_dist_scatter_rows(self.h, root, d_full or None, d_own or None))
+
+    def exchange(self, d_x_own: int) -> int:
+        C = self._C
+        out = C.c_void_p()
+        self._check(self._lib.mpkg_dist_exchange(self.h, d_x_own or None, C.byref(out)))
+        return out.value
+
+    def mpk(self, plan, A_local, d_x_own: int, p: int, d_block: int, rows: int, slices: int):
+        self._check(self._lib.mpkg_dist_mpk(self.h, plan.h, A_local.h, d_x_own or None, p, d_block, rows, slices))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.mpkg_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
