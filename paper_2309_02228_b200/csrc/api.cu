@@ -330,6 +330,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->resident = value != 0;
         else if (k == "trace")
             ctx->trace = value != 0;
+        else if (k == "wave_dict")
+            ctx->wave_dict = value != 0;
         else if (k == "pdl")
             ctx->pdl = value != 0;
         else if (k == "schedule") {

@@ -112,6 +112,7 @@ struct mpkg_ctx_s {
     int64_t ortho_fused = 2;    // fast ICGS: 0 unfused, 1 update+dots re-reading Q from L1/L2, 2 Q staged in smem
     int64_t coop_min = 0;       // fast mode: rows longer than this run warp-cooperatively (0 = 128)
     int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
+    int64_t wave_dict = 1;    // wave: value-dictionary chunk records when the matrix allows (0: plain)
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power, 3 wave (mpk_exec.cu)
     bool trace = false;       // record per-(tile, power) globaltimer stamps (mpkg_plan_exec_trace)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)

@@ -118,7 +118,7 @@ struct Executor {
     // wave schedule (schedule knob 3): per p, the pass ticket lists and pass boundaries
     struct Wave {
         DevBuf<uint32_t> tickets;
-        DevBuf<uint4> desc;             // k_mpk_wave's ticket descriptors (k_wave_desc)
+        DevBuf<uint2> desc;             // k_mpk_wave's ticket descriptors (k_wave_desc)
         std::vector<uint32_t> t_begin;  // first ticket of every pass (+ the end)
         std::vector<int> q_begin;       // first power of every pass (+ p+1)
         int pass_len = 0;
@@ -128,7 +128,10 @@ struct Executor {
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
     DevBuf<char> wrec;                        // chunk records (k_wave_pack)
-    DevBuf<uint32_t> wrec_off;                // record offsets, 16-byte units (n_tiles * kWaveChunks + 1)
+    DevBuf<uint32_t> wrec_off;                // record offsets, 16-byte units (n_tiles + 1)
+    int wave_fmt = 0;                         // chunk-record format: 0 plain, 1 value dictionary
+    DevBuf<double> wave_dict;                 // the distinct values (wave_fmt 1)
+    uint32_t n_dict = 0;
     uint64_t wave_pol[2] = {0, 0};            // createpolicy evict_first / evict_last values
     DevBuf<unsigned long long> trace;         // "trace" knob (FusedParams::trace)
     uint64_t trace_n = 0;
@@ -148,9 +151,11 @@ struct FusedParams {
     const uint32_t* row_len;
     const uint32_t* slot_row;  // nullptr: identity
     const uint32_t* tickets;
-    const uint4* wdesc;        // wave schedule: ticket descriptors
+    const uint2* wdesc;        // wave schedule: ticket descriptors
     const char* wrec;          // wave schedule: chunk records
     const uint32_t* wrec_off;
+    const double* dict;        // wave: distinct values (dict-format records)
+    uint32_t n_dict;
     uint64_t pol_first;        // L2 policies (createpolicy results, k_l2_policies)
     uint64_t pol_last;
     const uint32_t* dep_ptr;
@@ -1016,11 +1021,7 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
 // a lower, finished ticket and stores become visible, so it always progresses (deadlock-free).
 // Row arithmetic is rowdot.cuh's (stored order, mul then add): bitwise.  Slice 0 and the slices of
 // earlier passes are complete before the launch and read through the non-coherent path.
-#ifndef MPKG_WAVE_CHUNKS
-#define MPKG_WAVE_CHUNKS 1
-#endif
-constexpr uint32_t kWaveChunks = MPKG_WAVE_CHUNKS;  // SELL chunks per ticket (rows per lane)
-constexpr uint32_t kWaveRows = 32 * kWaveChunks;  // rows per tile
+constexpr uint32_t kWaveRows = 32;  // rows per tile: one SELL chunk, one row per lane
 constexpr unsigned long long kWaveEmpty = 0x7ff4dead5eed0001ull;
 
 // Relaxed (morally strong, single-copy atomic) loads and stores of in-pass slices.  The plain load
@@ -1054,16 +1055,53 @@ __device__ __forceinline__ double wave_wait(const double* p, double v) {
 // ---- The wave engine ------------------------------------------------------------------------
 //
 // Chunk records.  The wave keeps its own packed copy of the executor's SELL-32 arrays: chunk T (32
-// rows) is ONE contiguous, 16-byte aligned record
-//   len[32] u32 | slot_row[32] u32 (private row order only) | cols[L * 32] u32 | vals[L * 32] f64
-// (cols / vals in rowdot.cuh's pair interleave, L = the chunk width), so a ticket's whole matrix
-// slice moves with one 1D bulk copy.  rec_off[T] is the record's offset in 16-byte units.
-//
+// rows, width L) is ONE contiguous, 16-byte aligned record, so a ticket's whole matrix slice moves
+// with one 1D bulk copy.  Two formats (one per matrix):
+//   plain (F = 0): len[32] u32 | slot_row[32] u32 (private order only) | cols[32 L] u32 | vals[32 L] f64
+//   dict  (F = 1): len[32] u8  | slot_row[32] u32 (private order only) | cols[32 L] u32
+//                  | vidx[32][L8] u8 (lane-major, L8 = L rounded up to 8)
+// cols / vals in rowdot.cuh's pair interleave.  The dict format stores each value as an 8-bit
+// index into the matrix's table of distinct values (CSR-VI value compression; lossless, chosen when
+// the matrix has at most 255 distinct values and rows of at most 255 entries): 5 B per entry
+// instead of 12 on the HBM stream, and a 1,440-byte stage instead of 3,328 (more warps per SM).
+// rec_off[T] is the record's offset in 16-byte units.
 constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
+constexpr int kWaveAutoPass = 3;
+constexpr uint32_t kWaveDictMax = 255;
+#ifndef MPKG_WAVE_DICT_MINB
+#define MPKG_WAVE_DICT_MINB 4
+#endif
 
-__host__ __device__ constexpr uint32_t wave_hdr_bytes(bool sigma) { return sigma ? 256u : 128u; }
+template <int F, bool SIGMA>
+struct WaveRec {
+    static constexpr uint32_t len_bytes = F == 0 ? 128u : 32u;
+    static constexpr uint32_t hdr = len_bytes + (SIGMA ? 128u : 0u);
+    __host__ __device__ static constexpr uint32_t l8(uint32_t L) { return (L + 7u) & ~7u; }
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t L) {
+        return F == 0 ? hdr + 384u * L : hdr + 128u * L + 32u * l8(L);
+    }
+    static constexpr uint32_t max_staged = F == 0 ? 256u + 8u * 384u : 160u + 8u * 128u + 256u;
+    __device__ static uint32_t len(const char* r, uint32_t lane) {
+        if constexpr (F == 0) return reinterpret_cast<const uint32_t*>(r)[lane];
+        else return reinterpret_cast<const uint8_t*>(r)[lane];
+    }
+    __device__ static uint32_t slot(const char* r, uint32_t lane) {
+        return reinterpret_cast<const uint32_t*>(r + len_bytes)[lane];
+    }
+};
+__host__ __device__ constexpr uint32_t wave_rec_bytes(int F, bool sigma, uint32_t L) {
+    return F == 0 ? WaveRec<0, false>::bytes(L) + (sigma ? 128u : 0u) : WaveRec<1, false>::bytes(L) + (sigma ? 128u : 0u);
+}
+__host__ __device__ constexpr uint32_t wave_hdr(int F, bool sigma) {
+    return (F == 0 ? 128u : 32u) + (sigma ? 128u : 0u);
+}
 
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+    asm("" : "+l"(p));
+    return p;
+}
 // Gathers of x_{q-1}: weak and L1-allocating, so the 7 gathers of a 7-point row, which share lines
 // ((i,j-1,k) and (i,j,k-1) are neighbours in level l-1), hit L1.  Every location of an in-pass
 // slice holds kWaveEmpty or its final value (written once per launch), so a non-empty value read
@@ -1074,27 +1112,36 @@ __device__ __forceinline__ double ld_gather(const double* p) {
     asm("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
-template <typename T>
-__device__ __forceinline__ T* opaque_ptr(T* p) {
-    asm("" : "+l"(p));
-    return p;
-}
 __device__ __forceinline__ bool is_nan_bits(double v) {
     return ((unsigned long long)__double_as_longlong(v) << 1) > (0x7ff0000000000000ull << 1);
 }
 
-// Cold path: the row of `lane` from its record in global memory, every in-pass value awaited
-// (a gathered value was still empty, or the chunk is wider than a stage holds).
-__device__ __forceinline__ double wave_row_slow(const char* rec, uint32_t hdr, uint32_t L, uint32_t lane,
-                                                uint32_t len, const double* src, bool first, uint32_t* dbg) {
-    if (dbg) atomicAdd(dbg, 1u);
-    const uint32_t* cols = reinterpret_cast<const uint32_t*>(rec + hdr);
-    const double* vals = reinterpret_cast<const double*>(rec + hdr + 128u * L);
+// Entry k of `lane`'s row in a record (global or staged): its column and its value.
+template <int F>
+__device__ __forceinline__ uint32_t rec_entry(const char* body, uint32_t L, uint32_t k, uint32_t lane,
+                                              const double* dict, double& v) {
     const uint32_t Lp = L & ~1u;
+    const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
+    const uint32_t c = reinterpret_cast<const uint32_t*>(body)[e];
+    if constexpr (F == 0) {
+        v = reinterpret_cast<const double*>(body + 128u * L)[e];
+    } else {
+        const uint8_t ix = reinterpret_cast<const uint8_t*>(body + 128u * L)[lane * ((L + 7u) & ~7u) + k];
+        v = dict[ix];
+    }
+    return c;
+}
+
+// Cold path: the row of `lane` from a record (global memory for wide chunks), every in-pass value
+// awaited (first: the source slice is complete, read-only path).
+template <int F>
+__device__ __forceinline__ double wave_row_slow(const char* body, uint32_t L, uint32_t lane, uint32_t len,
+                                                const double* src, bool first, const double* dict, uint32_t* dbg) {
+    if (dbg) atomicAdd(dbg, 1u);
     double acc = 0.0;
     for (uint32_t k = 0; k < len; ++k) {
-        const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
-        const uint32_t c = __ldg(cols + e);
+        double v;
+        const uint32_t c = rec_entry<F>(body, L, k, lane, dict, v);
         double x;
         if (first) {
             x = __ldg(src + c);
@@ -1105,48 +1152,18 @@ __device__ __forceinline__ double wave_row_slow(const char* rec, uint32_t hdr, u
                 x = ld_strong_again(src + c);
             }
         }
-        acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + e), x));
+        acc = __dadd_rn(acc, __dmul_rn(v, x));
     }
-    return acc;
-}
-
-// Hot path: a staged chunk of compile-time width L, one row per lane, summed in stored order.  A
-// lane's padding entries (len <= k < L, value 0.0) gather nothing and add 0.0 * 0.0 = +0, which
-// leaves the sum unchanged (it starts at +0 and round-to-nearest never makes it -0): rowdot.cuh's
-// sum over k < len, bit for bit.  x[k] (k < L) is returned for the empty-value check.
-template <int L>
-__device__ __forceinline__ double wave_dot(const char* stage, uint32_t hdr, uint32_t lane, uint32_t len,
-                                           const double* src, double (&x)[8]) {
-    constexpr int Lp = L & ~1;
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + hdr);
-    const double* sv = reinterpret_cast<const double*>(stage + hdr + 128 * L);
-#pragma unroll
-    for (int j = 0; j < Lp; j += 2) {
-        const uint2 cc = *reinterpret_cast<const uint2*>(sc + (j >> 1) * 64 + lane * 2);
-        x[j] = (uint32_t)j < len ? ld_gather(src + cc.x) : 0.0;
-        x[j + 1] = (uint32_t)j + 1 < len ? ld_gather(src + cc.y) : 0.0;
-    }
-    if (L & 1) x[Lp] = (uint32_t)Lp < len ? ld_gather(src + sc[Lp * 32 + lane]) : 0.0;
-#pragma unroll
-    for (int j = L; j < 8; ++j) x[j] = 0.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < Lp; j += 2) {
-        const double2 vv = *reinterpret_cast<const double2*>(sv + (j >> 1) * 64 + lane * 2);
-        acc = __dadd_rn(acc, __dmul_rn(vv.x, x[j]));
-        acc = __dadd_rn(acc, __dmul_rn(vv.y, x[j + 1]));
-    }
-    if (L & 1) acc = __dadd_rn(acc, __dmul_rn(sv[Lp * 32 + lane], x[Lp]));
     return acc;
 }
 
 // A staged row whose gathers met empty values: re-read just those (relaxed L2 loads, all in flight,
 // then one by one until stored) and sum again from the stage, in stored order.
-__device__ __forceinline__ double wave_redo(const char* stage, uint32_t hdr, uint32_t L, uint32_t lane, uint32_t len,
-                                            const double* src, double (&x)[8], uint32_t* dbg) {
+template <int F>
+__device__ __forceinline__ double wave_redo(const char* body, uint32_t L, uint32_t lane, uint32_t len,
+                                            const double* src, double (&x)[8], const double* dict, uint32_t* dbg) {
     if (dbg) atomicAdd(dbg, 1u);
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + hdr);
-    const double* sv = reinterpret_cast<const double*>(stage + hdr + 128u * L);
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(body);
     const uint32_t Lp = L & ~1u;
     uint32_t e[8];
 #pragma unroll
@@ -1163,7 +1180,51 @@ __device__ __forceinline__ double wave_redo(const char* stage, uint32_t hdr, uin
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-        if ((uint32_t)k < L) acc = __dadd_rn(acc, __dmul_rn(sv[e[k]], x[k]));
+        if ((uint32_t)k < L) {
+            double v;
+            if constexpr (F == 0) v = reinterpret_cast<const double*>(body + 128u * L)[e[k]];
+            else v = dict[reinterpret_cast<const uint8_t*>(body + 128u * L)[lane * 8u + k]];
+            acc = __dadd_rn(acc, __dmul_rn(v, x[k]));
+        }
+    return acc;
+}
+
+// Hot path: a staged chunk of compile-time width L, one row per lane, summed in stored order.  A
+// lane's padding entries (len <= k < L, value 0.0) gather nothing and add 0.0 * 0.0 = +0, which
+// leaves the sum unchanged (it starts at +0 and round-to-nearest never makes it -0): rowdot.cuh's
+// sum over k < len, bit for bit.  x[k] (k < L) is returned for the empty-value check.
+template <int L, int F>
+__device__ __forceinline__ double wave_dot(const char* body, uint32_t lane, uint32_t len, const double* src,
+                                           const double* dict, double (&x)[8]) {
+    constexpr int Lp = L & ~1;
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(body);
+#pragma unroll
+    for (int j = 0; j < Lp; j += 2) {
+        const uint2 cc = *reinterpret_cast<const uint2*>(sc + (j >> 1) * 64 + lane * 2);
+        x[j] = (uint32_t)j < len ? ld_gather(src + cc.x) : 0.0;
+        x[j + 1] = (uint32_t)j + 1 < len ? ld_gather(src + cc.y) : 0.0;
+    }
+    if (L & 1) x[Lp] = (uint32_t)Lp < len ? ld_gather(src + sc[Lp * 32 + lane]) : 0.0;
+#pragma unroll
+    for (int j = L; j < 8; ++j) x[j] = 0.0;
+    double acc = 0.0;
+    if constexpr (F == 0) {
+        const double* sv = reinterpret_cast<const double*>(body + 128 * L);
+#pragma unroll
+        for (int j = 0; j < Lp; j += 2) {
+            const double2 vv = *reinterpret_cast<const double2*>(sv + (j >> 1) * 64 + lane * 2);
+            acc = __dadd_rn(acc, __dmul_rn(vv.x, x[j]));
+            acc = __dadd_rn(acc, __dmul_rn(vv.y, x[j + 1]));
+        }
+        if (L & 1) acc = __dadd_rn(acc, __dmul_rn(sv[Lp * 32 + lane], x[Lp]));
+    } else {
+        const uint2 vi = *reinterpret_cast<const uint2*>(body + 128 * L + lane * 8);
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const uint32_t ix = ((j < 4 ? vi.x : vi.y) >> (8 * (j & 3))) & 255u;
+            acc = __dadd_rn(acc, __dmul_rn(dict[ix], x[j]));
+        }
+    }
     return acc;
 }
 
@@ -1194,22 +1255,19 @@ __device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, 
 // front, which lets a small slack, and so a small L2 window, suffice), and the lowest unfinished
 // ticket is always one a warp is running.  A ticket waits only on values of lower tickets, so it
 // always progresses: deadlock-free without co-residency.
-#ifndef MPKG_WAVE_STREAMS
-#define MPKG_WAVE_STREAMS 16
-#endif
-constexpr uint32_t kWaveStreams = MPKG_WAVE_STREAMS;
+constexpr uint32_t kWaveStreams = 16;
 
-// Every warp owns a two-stage shared-memory ring; lane 0 stages a ticket's kWaveChunks chunk records
-// (contiguous in the record array) with ONE 1D bulk copy (cp.async.bulk, mbarrier complete_tx, L2
-// evict_last, evict_first on the tile's last use in the pass) one ticket AHEAD, so the matrix stream
-// is asynchronous and holds no registers, and a ticket costs one dependent hop: the gathers, all of
-// the tile's rows at once (kWaveChunks rows per lane in flight).  Tiles with a chunk wider than 8
-// entries are not staged (their rows take wave_row_slow from global memory).
-constexpr uint32_t kWaveRecMax = 256 + 8 * 32 * 12;                // largest staged record (3,328 B)
-constexpr uint32_t kWaveStageBytes = kWaveChunks * kWaveRecMax;
-constexpr uint32_t kWaveWarps = 8 / kWaveChunks;                   // warps per CTA (2 stages each)
+// Every warp owns a two-stage shared-memory ring; lane 0 stages the NEXT ticket's chunk record
+// with one 1D bulk copy (cp.async.bulk, mbarrier complete_tx, L2 evict_last, evict_first on the
+// tile's last use in the pass), so the matrix stream is asynchronous and holds no registers, and a
+// ticket costs one dependent hop: the gathers.  Records of chunks wider than 8 entries are not
+// staged (their rows take wave_row_slow from global memory).
+constexpr uint32_t kWaveWarps = 8;
 constexpr uint32_t kWaveThreads = 32 * kWaveWarps;
-constexpr uint32_t kWaveSmem = kWaveWarps * 2 * kWaveStageBytes;   // 53,248 B: 4 CTAs per SM
+template <int F>
+__host__ __device__ constexpr uint32_t wave_stage_bytes() { return WaveRec<F, true>::max_staged; }
+template <int F>
+__host__ __device__ constexpr uint32_t wave_smem() { return kWaveWarps * 2 * wave_stage_bytes<F>(); }
 
 __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
                                              uint64_t pol) {
@@ -1220,88 +1278,45 @@ __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint
         : "memory");
 }
 
-// Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units), y = T, z = q - q0,
-// w = the chunk widths, 4 bits each (min(L, 15); 15: a wide chunk, L read from rec_off).
-__device__ __forceinline__ uint4 ld_desc(const uint4* p) {
-    uint4 r;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-        : "l"(p));
+// Ticket descriptor (k_wave_desc): x = rec_off[T] (16-byte units), y = T | min(L, 15) << 24 |
+// (q - q0) << 28 (L = 15: a wide chunk, width read from the SELL offsets).
+__device__ __forceinline__ uint2 ld_desc(const uint2* p) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
-__device__ __forceinline__ bool wave_narrow(uint32_t w) {  // every chunk width <= 8
-#pragma unroll
-    for (uint32_t c = 0; c < kWaveChunks; ++c)
-        if (((w >> (4 * c)) & 15u) > 8u) return false;
-    return true;
-}
-template <uint32_t HDR>
-__device__ __forceinline__ uint32_t wave_tile_bytes(uint32_t w) {
-    uint32_t b = 0;
-#pragma unroll
-    for (uint32_t c = 0; c < kWaveChunks; ++c) b += HDR + 384u * ((w >> (4 * c)) & 15u);
-    return b;
-}
 
-// Lane 0: stage the records of ticket descriptor d (nothing for a tile with a wide chunk).
-template <bool SIGMA>
-__device__ __forceinline__ void wave_stage(const FusedParams& P, uint4 d, uint32_t q0, uint32_t q1,
+// Lane 0: stage the record of ticket descriptor d (header only for a wide chunk).
+template <int F, bool SIGMA>
+__device__ __forceinline__ void wave_stage(const FusedParams& P, uint2 d, uint32_t q0, uint32_t q1,
                                            uint32_t stage, uint32_t bar) {
-    const uint32_t bytes = wave_narrow(d.w) ? wave_tile_bytes<wave_hdr_bytes(SIGMA)>(d.w) : 0u;
+    const uint32_t Lc = (d.y >> 24) & 15u;
+    const uint32_t bytes = Lc <= 8 ? WaveRec<F, SIGMA>::bytes(Lc) : WaveRec<F, SIGMA>::hdr;
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    if (bytes)
-        bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar,
-                     q0 + d.z == q1 ? P.pol_first : P.pol_last);
+    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar, q0 + (d.y >> 28) == q1 ? P.pol_first : P.pol_last);
 }
 
-// All kWaveChunks rows of a lane at compile-time width L (every chunk of the tile that wide): all
-// gathers in flight, then the sums in stored order (wave_dot's rules, bit for bit).
-template <int L, uint32_t HDR, int C>
-__device__ __forceinline__ void wave_multi(const char* stage, uint32_t lane, const uint32_t (&len)[C],
-                                           const double* src, double (&x)[C][8], double (&acc)[C]) {
-    constexpr int Lp = L & ~1;
-    constexpr uint32_t REC = HDR + 384u * L;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-        const uint32_t* sc = reinterpret_cast<const uint32_t*>(stage + c * REC + HDR);
-#pragma unroll
-        for (int j = 0; j < Lp; j += 2) {
-            const uint2 cc = *reinterpret_cast<const uint2*>(sc + (j >> 1) * 64 + lane * 2);
-            x[c][j] = (uint32_t)j < len[c] ? ld_gather(src + cc.x) : 0.0;
-            x[c][j + 1] = (uint32_t)j + 1 < len[c] ? ld_gather(src + cc.y) : 0.0;
-        }
-        if (L & 1) x[c][Lp] = (uint32_t)Lp < len[c] ? ld_gather(src + sc[Lp * 32 + lane]) : 0.0;
-#pragma unroll
-        for (int j = L; j < 8; ++j) x[c][j] = 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-        const double* sv = reinterpret_cast<const double*>(stage + c * REC + HDR + 128 * L);
-        double a = 0.0;
-#pragma unroll
-        for (int j = 0; j < Lp; j += 2) {
-            const double2 vv = *reinterpret_cast<const double2*>(sv + (j >> 1) * 64 + lane * 2);
-            a = __dadd_rn(a, __dmul_rn(vv.x, x[c][j]));
-            a = __dadd_rn(a, __dmul_rn(vv.y, x[c][j + 1]));
-        }
-        if (L & 1) a = __dadd_rn(a, __dmul_rn(sv[Lp * 32 + lane], x[c][Lp]));
-        acc[c] = a;
-    }
-}
-
-template <int KIND, bool SIGMA>
-__global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
-                                                            uint32_t t1, uint32_t q0, uint32_t q1) {
+template <int KIND, bool SIGMA, int F>
+__global__ void __launch_bounds__(kWaveThreads, F == 0 ? 4 : MPKG_WAVE_DICT_MINB) k_mpk_wave(const __grid_constant__ FusedParams P,
+                                                                            uint32_t t0, uint32_t t1, uint32_t q0,
+                                                                            uint32_t q1, uint32_t fill_lo,
+                                                                            uint32_t fill_hi) {
     extern __shared__ __align__(128) char wsm[];
     __shared__ __align__(8) uint64_t bars[kWaveWarps][2];
-    constexpr uint32_t hdr = wave_hdr_bytes(SIGMA);
-    constexpr int C = (int)kWaveChunks;
+    __shared__ double sdict[F == 1 ? kWaveDictMax + 1 : 1];
+    using R = WaveRec<F, SIGMA>;
+    constexpr uint32_t SB = wave_stage_bytes<F>();
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     const uint32_t gw = blockIdx.x * kWaveWarps + wib;
     const uint32_t sid = gw % kWaveStreams;
     uint32_t* const ctr = P.counter + sid * 32u;  // one 128-B line per stream
-    char* const ring = wsm + wib * 2u * kWaveStageBytes;
+    char* const ring = wsm + wib * 2u * SB;
     const uint32_t ring_s = smem_u32(ring), bar0 = smem_u32(&bars[wib][0]);
+    if constexpr (F == 1) {
+        for (uint32_t i = threadIdx.x; i < P.n_dict; i += blockDim.x) sdict[i] = P.dict[i];
+        __syncthreads();
+    }
+    const double* dict = sdict;
     if (lane == 0) {
         asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar0));
         asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar0 + 8u));
@@ -1316,17 +1331,17 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
     auto ticket = [&](uint32_t k) { return t0 + sid + kWaveStreams * __shfl_sync(0xffffffffu, k, 0); };
     uint32_t t = ticket(claim());
     uint32_t tn = ticket(claim());
-    uint4 d = t < t1 ? ld_desc(P.wdesc + t) : make_uint4(0u, 0u, 0u, 0u);
-    uint4 dn = tn < t1 ? ld_desc(P.wdesc + tn) : make_uint4(0u, 0u, 0u, 0u);
+    uint2 d = t < t1 ? ld_desc(P.wdesc + t) : make_uint2(0u, 0u);
+    uint2 dn = tn < t1 ? ld_desc(P.wdesc + tn) : make_uint2(0u, 0u);
     uint32_t kc = claim();
     if (lane == 0) {
-        if (t < t1) wave_stage<SIGMA>(P, d, q0, q1, ring_s, bar0);
-        if (tn < t1) wave_stage<SIGMA>(P, dn, q0, q1, ring_s + kWaveStageBytes, bar0 + 8u);
+        if (t < t1) wave_stage<F, SIGMA>(P, d, q0, q1, ring_s, bar0);
+        if (tn < t1) wave_stage<F, SIGMA>(P, dn, q0, q1, ring_s + SB, bar0 + 8u);
     }
     uint32_t st = 0, phase = 0;  // phase: bit i = parity of stage i's next completion
     while (t < t1) {
         const uint32_t tnn = ticket(kc);
-        uint4 dnn = make_uint4(0u, 0u, 0u, 0u);
+        uint2 dnn = make_uint2(0u, 0u);
         if (tnn < t1) {
             dnn = ld_desc(P.wdesc + tnn);
             kc = claim();
@@ -1342,97 +1357,46 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                     : "memory");
             phase ^= 1u << st;
         }
-        const char* stage = ring + st * kWaveStageBytes;
-        const uint32_t T = d.y;
-        const uint32_t q = q0 + d.z;
+        const char* stage = ring + st * SB;
+        const uint32_t T = d.y & 0xffffffu;
+        const uint32_t q = q0 + (d.y >> 28);
+        const uint32_t Lc = (d.y >> 24) & 15u;
         // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
-        const bool narrow = wave_narrow(d.w);
-        uint32_t rr[C], len[C];
-        double acc[C];
-        {
-            uint32_t off = 0;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const uint32_t s = T * kWaveRows + c * 32u + lane;
-                if (narrow) {
-                    rr[c] = SIGMA ? reinterpret_cast<const uint32_t*>(stage + off + 128)[lane] : s;
-                    len[c] = rr[c] < P.n_rows ? reinterpret_cast<const uint32_t*>(stage + off)[lane] : 0u;
-                } else {
-                    const char* g = P.wrec + ((uint64_t)P.wrec_off[T * C + c]) * 16u;
-                    rr[c] = SIGMA ? __ldg(reinterpret_cast<const uint32_t*>(g + 128) + lane) : s;
-                    len[c] = rr[c] < P.n_rows ? __ldg(reinterpret_cast<const uint32_t*>(g) + lane) : 0u;
-                }
-                off += hdr + 384u * ((d.w >> (4 * c)) & 15u);
-            }
+        const uint32_t s = T * kWaveRows + lane;
+        const uint32_t rr = SIGMA ? R::slot(stage, lane) : s;
+        const uint32_t len = rr < P.n_rows ? R::len(stage, lane) : 0u;
+        const char* body = stage + R::hdr;
+        double x[8];
+        double acc = 0.0;
+        bool slow = false;
+        switch (Lc) {
+            case 0: break;
+            case 1: acc = wave_dot<1, F>(body, lane, len, src, dict, x); break;
+            case 2: acc = wave_dot<2, F>(body, lane, len, src, dict, x); break;
+            case 3: acc = wave_dot<3, F>(body, lane, len, src, dict, x); break;
+            case 4: acc = wave_dot<4, F>(body, lane, len, src, dict, x); break;
+            case 5: acc = wave_dot<5, F>(body, lane, len, src, dict, x); break;
+            case 6: acc = wave_dot<6, F>(body, lane, len, src, dict, x); break;
+            case 7: acc = wave_dot<7, F>(body, lane, len, src, dict, x); break;
+            case 8: acc = wave_dot<8, F>(body, lane, len, src, dict, x); break;
+            default: slow = true;
         }
-        const uint32_t L0 = d.w & 15u;
-        bool uniform = narrow;
+        // An empty (signalling-NaN) value makes the sum NaN: only then look at the values (slice
+        // q0-1 is complete and may hold any bit pattern: never checked).
+        if (Lc - 1u < 8u && q != q0 && is_nan_bits(acc)) {
+            bool miss = false;
 #pragma unroll
-        for (int c = 1; c < C; ++c) uniform &= ((d.w >> (4 * c)) & 15u) == L0;
-        if (uniform && L0 > 0) {
-            double x[C][8];
-            switch (L0) {
-                case 1: wave_multi<1, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 2: wave_multi<2, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 3: wave_multi<3, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 4: wave_multi<4, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 5: wave_multi<5, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 6: wave_multi<6, hdr, C>(stage, lane, len, src, x, acc); break;
-                case 7: wave_multi<7, hdr, C>(stage, lane, len, src, x, acc); break;
-                default: wave_multi<8, hdr, C>(stage, lane, len, src, x, acc); break;
-            }
-            // An empty (signalling-NaN) value makes a sum NaN: only then look at the values (slice
-            // q0-1 is complete and may hold any bit pattern: never checked).
-            if (q != q0) {
-#pragma unroll
-                for (int c = 0; c < C; ++c)
-                    if (is_nan_bits(acc[c])) {
-                        bool miss = false;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) miss |= wave_empty(x[c][j]);
-                        if (miss) acc[c] = wave_redo(stage + c * (hdr + 384u * L0), hdr, L0, lane, len[c], src, x[c], P.dbg);
-                    }
-            }
-        } else {
-            // mixed widths (or a wide chunk): chunk by chunk
-            uint32_t off = 0;
-#pragma unroll 1
-            for (int c = 0; c < C; ++c) {
-                const uint32_t Lc = (d.w >> (4 * c)) & 15u;
-                const char* sc = stage + off;
-                off += hdr + 384u * Lc;
-                if (!narrow) {
-                    const uint32_t o = P.wrec_off[T * C + c];
-                    const uint32_t L = (((P.wrec_off[T * C + c + 1] - o) * 16u) - hdr) / 384u;
-                    acc[c] = wave_row_slow(P.wrec + (uint64_t)o * 16u, hdr, L, lane, len[c], src, q == q0, P.dbg);
-                    continue;
-                }
-                double x[8];
-                double a = 0.0;
-                switch (Lc) {
-                    case 0: for (int j = 0; j < 8; ++j) x[j] = 0.0; break;
-                    case 1: a = wave_dot<1>(sc, hdr, lane, len[c], src, x); break;
-                    case 2: a = wave_dot<2>(sc, hdr, lane, len[c], src, x); break;
-                    case 3: a = wave_dot<3>(sc, hdr, lane, len[c], src, x); break;
-                    case 4: a = wave_dot<4>(sc, hdr, lane, len[c], src, x); break;
-                    case 5: a = wave_dot<5>(sc, hdr, lane, len[c], src, x); break;
-                    case 6: a = wave_dot<6>(sc, hdr, lane, len[c], src, x); break;
-                    case 7: a = wave_dot<7>(sc, hdr, lane, len[c], src, x); break;
-                    default: a = wave_dot<8>(sc, hdr, lane, len[c], src, x); break;
-                }
-                if (q != q0 && is_nan_bits(a)) {
-                    bool miss = false;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
-                    if (miss) a = wave_redo(sc, hdr, Lc, lane, len[c], src, x, P.dbg);
-                }
-                acc[c] = a;
-            }
+            for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
+            if (miss) acc = wave_redo<F>(body, Lc, lane, len, src, x, dict, P.dbg);
+        }
+        if (slow) {  // a wide chunk: its record from global memory
+            const uint32_t L = Lc != kWaveWideL ? Lc : (uint32_t)((P.chunk_off[T + 1] - P.chunk_off[T]) >> 5);
+            acc = wave_row_slow<F>(P.wrec + (uint64_t)d.x * 16u + R::hdr, L, lane, len, src, q == q0, dict, P.dbg);
         }
         __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
-        if (lane == 0 && tnn < t1) wave_stage<SIGMA>(P, dnn, q0, q1, ring_s + st * kWaveStageBytes, bar0 + 8u * st);
+        if (lane == 0 && tnn < t1) wave_stage<F, SIGMA>(P, dnn, q0, q1, ring_s + st * SB, bar0 + 8u * st);
         if (P.trace) {  // every lane's inputs are final here, no result is stored yet
             if (lane == 0) {
                 const unsigned long long ts = global_ns();
@@ -1441,38 +1405,101 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
             }
             __syncwarp();
         }
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-            if (rr[c] < P.n_rows) wave_epilogue<KIND, SIGMA>(P, T * kWaveRows + c * 32u + lane, rr[c], q, q0, src, acc[c]);
+        if (rr < P.n_rows) wave_epilogue<KIND, SIGMA>(P, s, rr, q, q0, src, acc);
+        // The tile's last power in this pass also empties its rows of the next pass's in-pass
+        // slices (never read by this pass): k_wave_fill runs once per call instead of per pass.
+        if (q == q1 && s < (SIGMA ? P.n_slots : P.n_rows)) {
+            const double e = __longlong_as_double((long long)kWaveEmpty);
+            for (uint32_t f = fill_lo; f < fill_hi; ++f) P.V[(uint64_t)f * P.vstride + s] = e;
+        }
         t = tn, d = dn, tn = tnn, dn = dnn;
         st ^= 1u;
     }
 }
 
-// Chunk records from the executor's SELL arrays: one warp per chunk; chunks past the SELL (the
-// last tile's padding) get an empty record (lengths 0, slot rows ~0).
+// Value dictionary (setup): the distinct value bit patterns of the SELL arrays (padding entries
+// are 0.0 and count), inserted into an open-addressing table of 512 slots (empty = kDictEmpty);
+// warps first merge equal values (__match_any_sync), so only warp-unique values hit the table.
+// *count = distinct values (stops counting past 512: the dict format is then not used).
+constexpr unsigned long long kDictEmpty = 0xfff8dead0000beefull;  // a NaN payload no value takes here
+constexpr uint32_t kDictSlots = 512;
+__device__ __forceinline__ uint32_t dict_hash(unsigned long long b) {
+    b ^= b >> 33;
+    b *= 0xff51afd7ed558ccdull;
+    b ^= b >> 33;
+    return (uint32_t)b & (kDictSlots - 1);
+}
+__global__ void k_dict_insert(const double* __restrict__ vals, uint64_t n, unsigned long long* table,
+                              uint32_t* count) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const bool in = i < n;
+        const unsigned long long b = in ? (unsigned long long)__double_as_longlong(vals[i]) : kDictEmpty;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const bool leader = (threadIdx.x & 31u) == (uint32_t)(__ffs(peers) - 1);
+        if (!in || !leader || b == kDictEmpty) continue;
+        if (*reinterpret_cast<volatile uint32_t*>(count) > kDictSlots / 2) return;
+        uint32_t h = dict_hash(b);
+        for (uint32_t probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+            const unsigned long long cur = table[h];
+            if (cur == b) break;
+            if (cur == kDictEmpty) {
+                const unsigned long long prev = atomicCAS(table + h, kDictEmpty, b);
+                if (prev == kDictEmpty) {
+                    atomicAdd(count, 1u);
+                    break;
+                }
+                if (prev == b) break;
+            }
+        }
+    }
+}
+__device__ __forceinline__ uint32_t dict_index(const unsigned long long* table, const uint16_t* slot_ix,
+                                               unsigned long long b) {
+    uint32_t h = dict_hash(b);
+    while (table[h] != b) h = (h + 1) & (kDictSlots - 1);
+    return slot_ix[h];
+}
+
+// Chunk records from the executor's SELL arrays: one warp per chunk.
+template <int F>
 __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __restrict__ vals,
                             const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
-                            const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rec,
-                            const uint32_t* __restrict__ rec_off, char* __restrict__ rec) {
+                            const uint64_t* __restrict__ chunk_off, uint32_t n_chunks,
+                            const uint32_t* __restrict__ rec_off, char* __restrict__ rec,
+                            const unsigned long long* __restrict__ table, const uint16_t* __restrict__ slot_ix) {
     const uint32_t lane = threadIdx.x & 31u;
-    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_rec;
+    const uint32_t lb = F == 0 ? 128u : 32u;
+    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_chunks;
          T += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         char* r = rec + (uint64_t)rec_off[T] * 16u;
-        const bool real = T < n_chunks;
-        reinterpret_cast<uint32_t*>(r)[lane] = real ? row_len[T * 32 + lane] : 0u;
-        uint32_t hdr = 128;
+        const uint32_t len = row_len[T * 32 + lane];
+        if (F == 0) reinterpret_cast<uint32_t*>(r)[lane] = len;
+        else reinterpret_cast<uint8_t*>(r)[lane] = (uint8_t)len;
+        uint32_t hdr = lb;
         if (slot_row) {
-            reinterpret_cast<uint32_t*>(r + 128)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
-            hdr = 256;
+            reinterpret_cast<uint32_t*>(r + lb)[lane] = slot_row[T * 32 + lane];
+            hdr += 128;
         }
-        if (!real) continue;
         const uint64_t o = chunk_off[T], ne = chunk_off[T + 1] - o;
+        const uint32_t L = (uint32_t)(ne >> 5);
         uint32_t* rc = reinterpret_cast<uint32_t*>(r + hdr);
-        double* rv = reinterpret_cast<double*>(r + hdr + 4 * ne);
-        for (uint64_t e = lane; e < ne; e += 32) {
-            rc[e] = cols[o + e];
-            rv[e] = vals[o + e];
+        for (uint64_t e = lane; e < ne; e += 32) rc[e] = cols[o + e];
+        if (F == 0) {
+            double* rv = reinterpret_cast<double*>(r + hdr + 4 * ne);
+            for (uint64_t e = lane; e < ne; e += 32) rv[e] = vals[o + e];
+        } else {
+            uint8_t* ri = reinterpret_cast<uint8_t*>(r + hdr + 4 * ne);
+            const uint32_t L8 = (L + 7u) & ~7u;
+            for (uint32_t k = 0; k < L8; ++k) {  // lane-major: lane's L8 bytes, padding index of 0.0
+                double v = 0.0;
+                if (k < L) {
+                    const uint32_t Lp = L & ~1u;
+                    const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
+                    v = vals[o + e];
+                }
+                ri[lane * L8 + k] = (uint8_t)dict_index(table, slot_ix, (unsigned long long)__double_as_longlong(v));
+            }
         }
     }
 }
@@ -1480,16 +1507,12 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
 // Descriptors of a pass's tickets from the host codes (T | q << 24, kLastUse ignored: the last use
 // is q == q1).
 __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
-                            uint32_t hdr, uint32_t q0, uint4* __restrict__ out) {
+                            const uint64_t* __restrict__ chunk_off, uint32_t q0, uint2* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t code = codes[i];
         const uint32_t T = code & 0xffffffu, q = (code >> 24) & 63u;
-        uint32_t w = 0;
-        for (uint32_t c = 0; c < kWaveChunks; ++c) {
-            const uint32_t L = ((rec_off[T * kWaveChunks + c + 1] - rec_off[T * kWaveChunks + c]) * 16u - hdr) / 384u;
-            w |= (L < kWaveWideL ? L : kWaveWideL) << (4 * c);
-        }
-        out[i] = make_uint4(rec_off[T * kWaveChunks], T, q - q0, w);
+        const uint64_t L = (chunk_off[T + 1] - chunk_off[T]) >> 5;
+        out[i] = make_uint2(rec_off[T], T | (uint32_t)(L < kWaveWideL ? L : kWaveWideL) << 24 | (q - q0) << 28);
     }
 }
 
@@ -2299,32 +2322,76 @@ __global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* 
 void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
     cudaStream_t st = ctx->stream;
     const uint32_t nt = E.n_tiles;
-    {  // matrix + vector bytes one tile-power touches (the live-window model of wave_order), and the
-       // chunk records (kWaveChunks per tile; the last tile padded with empty records)
+    {  // the chunk records (one per tile) and the bytes one tile-power touches (record + x read + y
+       // written: the live-window model of wave_order)
         const uint32_t nc = E.S->n_chunks;
-        const uint64_t nrec = (uint64_t)nt * kWaveChunks;
+        if (nc != nt) fail(MPKG_EINTERNAL, "wave: tiles must be the SELL chunks");
         std::vector<uint64_t> off((uint64_t)nc + 1);
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E.S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
         MPKG_CUDA(cudaStreamSynchronize(st));
-        auto ent = [&](uint64_t c) { return c < nc ? off[c + 1] - off[c] : 0ull; };
-        E.tile_bytes.assign(nt, 0);
-        const uint32_t hdr = wave_hdr_bytes(E.order >= 1);
-        std::vector<uint32_t> ro(nrec + 1);
-        uint64_t acc = 0;
-        for (uint64_t c = 0; c < nrec; ++c) {
-            ro[c] = (uint32_t)acc;
-            acc += (hdr + 12 * ent(c)) / 16;  // 32 L entries: 384 L bytes
-            if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
-            E.tile_bytes[c / kWaveChunks] += 12 * ent(c) + 24ull * 32;
+        uint64_t max_l = 0;
+        for (uint32_t c = 0; c < nc; ++c) max_l = std::max<uint64_t>(max_l, (off[c + 1] - off[c]) >> 5);
+        // value dictionary: at most kWaveDictMax distinct values and rows of at most 255 entries
+        DevBuf<unsigned long long> table(kDictSlots);
+        DevBuf<uint16_t> slot_ix(kDictSlots);
+        std::vector<double> dict;
+        E.wave_fmt = 0;
+        if (ctx->wave_dict && max_l <= 255 && E.S->n_entries) {
+            DevBuf<uint32_t> count(1);
+            std::vector<unsigned long long> empty(kDictSlots, kDictEmpty);
+            MPKG_CUDA(cudaMemcpyAsync(table.p, empty.data(), 8 * kDictSlots, cudaMemcpyHostToDevice, st));
+            MPKG_CUDA(cudaMemsetAsync(count.p, 0, 4, st));
+            k_dict_insert<<<grid_for(E.S->n_entries, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                E.S->vals.p, E.S->n_entries, table.p, count.p);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
+            uint32_t cnt = 0;
+            std::vector<unsigned long long> h(kDictSlots);
+            MPKG_CUDA(cudaMemcpyAsync(&cnt, count.p, 4, cudaMemcpyDeviceToHost, st));
+            MPKG_CUDA(cudaMemcpyAsync(h.data(), table.p, 8 * kDictSlots, cudaMemcpyDeviceToHost, st));
+            MPKG_CUDA(cudaStreamSynchronize(st));
+            if (cnt <= kWaveDictMax) {
+                std::vector<uint16_t> ix(kDictSlots, 0);
+                for (uint32_t i = 0; i < kDictSlots; ++i)
+                    if (h[i] != kDictEmpty) {
+                        ix[i] = (uint16_t)dict.size();
+                        double v;
+                        std::memcpy(&v, &h[i], 8);
+                        dict.push_back(v);
+                    }
+                MPKG_CUDA(cudaMemcpyAsync(slot_ix.p, ix.data(), 2 * kDictSlots, cudaMemcpyHostToDevice, st));
+                E.wave_dict.alloc(std::max<size_t>(dict.size(), 1));
+                if (!dict.empty())
+                    MPKG_CUDA(cudaMemcpyAsync(E.wave_dict.p, dict.data(), 8 * dict.size(), cudaMemcpyHostToDevice, st));
+                E.n_dict = (uint32_t)dict.size();
+                E.wave_fmt = 1;
+            }
         }
-        ro[nrec] = (uint32_t)acc;
-        E.wrec_off.alloc(nrec + 1);
+        const bool sigma = E.order >= 1;
+        E.tile_bytes.assign(nt, 0);
+        std::vector<uint32_t> ro((uint64_t)nc + 1);
+        uint64_t acc = 0;
+        for (uint32_t c = 0; c < nc; ++c) {
+            ro[c] = (uint32_t)acc;
+            const uint32_t rb = wave_rec_bytes(E.wave_fmt, sigma, (uint32_t)((off[c + 1] - off[c]) >> 5));
+            acc += rb / 16;
+            if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
+            E.tile_bytes[c] = rb + 16ull * 32;
+        }
+        ro[nc] = (uint32_t)acc;
+        E.wrec_off.alloc((uint64_t)nc + 1);
         E.wrec.alloc(std::max<uint64_t>(acc * 16, 16));
         MPKG_CUDA(cudaMemcpyAsync(E.wrec_off.p, ro.data(), 4 * ro.size(), cudaMemcpyHostToDevice, st));
-        if (nrec) {
-            k_wave_pack<<<grid_for(nrec * 32, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
-                E.S->cols.p, E.S->vals.p, E.S->row_len.p, E.order >= 1 ? E.slot_row.p : nullptr, E.S->chunk_off.p,
-                nc, (uint32_t)nrec, E.wrec_off.p, E.wrec.p);
+        if (nc) {
+            const unsigned g = grid_for((uint64_t)nc * 32, 256, (unsigned)ctx->sm_count * 8u);
+            if (E.wave_fmt == 1)
+                k_wave_pack<1><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
+                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc, E.wrec_off.p,
+                                                  E.wrec.p, table.p, slot_ix.p);
+            else
+                k_wave_pack<0><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
+                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc, E.wrec_off.p,
+                                                  E.wrec.p, nullptr, nullptr);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2414,7 +2481,9 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
         if (ctx->slack >= 0) return std::max<int64_t>(ctx->slack, 1);
         return std::max<int64_t>(1, (warps * 11 / 5 + len - 1) / len);
     };
-    int P = std::min(p, kWaveMaxPass);
+    // auto: at most kWaveAutoPass powers per pass (C5, chunk records in the dict format: p' = 2..4
+    // within 4%, 8 is 15% slower: the fronts' lag grows with p')
+    int P = std::min(p, kWaveAutoPass);
     if (ctx->pass_powers > 0) {
         P = std::min<int>({p, (int)ctx->pass_powers, kWaveMaxPass});
         W.window = wave_order(E, 1, P, slack_for(P), nullptr);
@@ -2448,8 +2517,7 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
         const uint64_t b = W.t_begin[j], e = W.t_begin[j + 1];
         if (e > b) {
             k_wave_desc<<<grid_for(e - b, 256, (unsigned)ctx->sm_count * 8u), 256, 0, ctx->stream>>>(
-                W.tickets.p + b, e - b, E.wrec_off.p, wave_hdr_bytes(E.order >= 1), (uint32_t)W.q_begin[j],
-                W.desc.p + b);
+                W.tickets.p + b, e - b, E.wrec_off.p, E.S->chunk_off.p, (uint32_t)W.q_begin[j], W.desc.p + b);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2459,11 +2527,15 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.wave.emplace(p, std::move(W)).first->second;
 }
 
-void* wave_fn(int kind, bool sigma) {
-    static void* const fns[4] = {(void*)k_mpk_wave<0, false>, (void*)k_mpk_wave<0, true>,
-                                 (void*)k_mpk_wave<1, false>, (void*)k_mpk_wave<1, true>};
-    return fns[kind * 2 + (sigma ? 1 : 0)];
+void* wave_fn(int kind, bool sigma, int fmt) {
+    static void* const fns[2][4] = {
+        {(void*)k_mpk_wave<0, false, 0>, (void*)k_mpk_wave<0, true, 0>, (void*)k_mpk_wave<1, false, 0>,
+         (void*)k_mpk_wave<1, true, 0>},
+        {(void*)k_mpk_wave<0, false, 1>, (void*)k_mpk_wave<0, true, 1>, (void*)k_mpk_wave<1, false, 1>,
+         (void*)k_mpk_wave<1, true, 1>}};
+    return fns[fmt][kind * 2 + (sigma ? 1 : 0)];
 }
+uint32_t wave_smem_for(int fmt) { return fmt == 1 ? wave_smem<1>() : wave_smem<0>(); }
 
 template <int KIND, int G>
 void launch_g(bool sigma, int grid, int threads, uint32_t smem, cudaStream_t st,
@@ -2560,16 +2632,17 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (wave && a.kind == 2) fail(MPKG_EINTERNAL, "mpk: the wave schedule has no polynomial epilogue");
     if (!sweep && !wave && !E.fused_ready) build_fused(ctx, Pl, A, &E);
     if (wave && !E.wave_grid) {
+        build_wave(ctx, Pl, A, E);  // picks the record format
         int occ = 1 << 30;
         for (int k = 0; k < 4; ++k) {
             int o = 0;
-            void* fn = wave_fn(k / 2, k % 2);
-            MPKG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWaveSmem));
-            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWaveThreads, kWaveSmem));
+            void* fn = wave_fn(k / 2, k % 2, E.wave_fmt);
+            const uint32_t sm = wave_smem_for(E.wave_fmt);
+            MPKG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWaveThreads, sm));
             occ = std::min(occ, o);
         }
         if (ctx->ctas_per_sm > 0) occ = std::min<int>(occ, (int)ctx->ctas_per_sm);
-        if (!E.wave_grid) build_wave(ctx, Pl, A, E);
         E.wave_grid = std::max(1, occ) * ctx->sm_count;
         E.wave.clear();  // the slack follows the warps in flight
         E.counter.alloc(kWaveStreams * 32 + 32);
@@ -2592,6 +2665,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     P.wdesc = wave ? W->desc.p : nullptr;
     P.wrec = E.wrec.p;
     P.wrec_off = E.wrec_off.p;
+    P.dict = E.wave_dict.p;
+    P.n_dict = E.n_dict;
     P.pol_first = E.wave_pol[0];
     P.pol_last = E.wave_pol[1];
     P.dep_ptr = E.dep_ptr.p;
@@ -2899,25 +2974,31 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (wave) {
         // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
         // host block, the pass's slices go to the host while the next pass runs
-        void* fn = wave_fn(a.kind, sigma);
+        void* fn = wave_fn(a.kind, sigma, E.wave_fmt);
         P.counter = E.counter.p;
         P.dbg = getenv("MPKG_WAVE_DEBUG") ? E.counter.p + kWaveStreams * 32 : nullptr;
         for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
             uint32_t t0 = W->t_begin[j], t1 = W->t_begin[j + 1], q0 = (uint32_t)W->q_begin[j];
             const uint32_t q1 = (uint32_t)W->q_begin[j + 1] - 1;
             MPKG_CUDA(cudaMemsetAsync(E.counter.p, 0, 4ull * kWaveStreams * 32, st));
-            if (q1 > q0) {  // the slices read inside the pass start out empty
+            if (j == 0 && q1 > q0) {  // the slices read inside the pass start out empty (later
+                                      // passes: filled by the pass before, fill_lo..fill_hi)
                 k_wave_fill<<<grid_for(P.vstride, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
                     P.V, P.vstride, sigma ? E.n_slots : A->n_rows, q0, q1);
                 MPKG_LAUNCH_CHECK();
                 ctx->launches += 1;
+            }
+            uint32_t fill_lo = 0, fill_hi = 0;
+            if (j + 2 < W->t_begin.size()) {
+                fill_lo = (uint32_t)W->q_begin[j + 1];
+                fill_hi = (uint32_t)W->q_begin[j + 2] - 1;
             }
             const unsigned g = (unsigned)std::max<uint64_t>(
                 1, std::min<uint64_t>(E.wave_grid, (t1 - t0 + kWaveWarps - 1) / kWaveWarps));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(g);
             cfg.blockDim = dim3(kWaveThreads);
-            cfg.dynamicSmemBytes = kWaveSmem;
+            cfg.dynamicSmemBytes = wave_smem_for(E.wave_fmt);
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeCooperative;
@@ -2925,7 +3006,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             uint32_t q1a = q1;
-            void* args[] = {(void*)&P, (void*)&t0, (void*)&t1, (void*)&q0, (void*)&q1a};
+            void* args[] = {(void*)&P, (void*)&t0, (void*)&t1, (void*)&q0, (void*)&q1a, (void*)&fill_lo, (void*)&fill_hi};
             MPKG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
             if (j + 2 < W->t_begin.size()) ctx->launches += 1;
             if (to_host)

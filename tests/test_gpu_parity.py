@@ -175,6 +175,7 @@ DEFAULT_KNOBS = {"order": -1, "slack": -1, "schedule": 0, "kernel": 0, "tile_row
 SCHEDULES = {
     "sweeps": {"schedule": 2},
     "wave": {"schedule": 3},
+    "wave-plain": {"schedule": 3, "wave_dict": 0},
     "wave-1cta": {"schedule": 3, "ctas_per_sm": 1},
     "wave-pass1": {"schedule": 3, "pass": 1},
     "wave-pass2-slack1": {"schedule": 3, "pass": 2, "slack": 1},
