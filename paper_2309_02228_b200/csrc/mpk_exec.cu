@@ -128,7 +128,8 @@ struct Executor {
     std::map<int, Wave> wave;
     int wave_grid = 0;                        // resident CTAs of k_mpk_wave (256 threads)
     DevBuf<char> wrec;                        // chunk records (k_wave_pack)
-    DevBuf<uint32_t> wrec_off;                // record offsets, 16-byte units (n_tiles + 1)
+    DevBuf<uint32_t> wrec_off;                // record offsets, 16-byte units (n_tiles * kWaveChunks + 1)
+    DevBuf<uint8_t> wave_narrow;              // per tile: every chunk at most 8 entries wide (staged)
     int wave_fmt = 0;                         // chunk-record format: 0 plain, 1 value dictionary
     DevBuf<double> wave_dict;                 // the distinct values (wave_fmt 1)
     uint32_t n_dict = 0;
@@ -1021,7 +1022,11 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
 // a lower, finished ticket and stores become visible, so it always progresses (deadlock-free).
 // Row arithmetic is rowdot.cuh's (stored order, mul then add): bitwise.  Slice 0 and the slices of
 // earlier passes are complete before the launch and read through the non-coherent path.
-constexpr uint32_t kWaveRows = 32;  // rows per tile: one SELL chunk, one row per lane
+#ifndef MPKG_WAVE_CHUNKS
+#define MPKG_WAVE_CHUNKS 2
+#endif
+constexpr uint32_t kWaveChunks = MPKG_WAVE_CHUNKS;  // SELL chunks per tile (processed one after the other)
+constexpr uint32_t kWaveRows = 32 * kWaveChunks;   // rows per tile
 constexpr unsigned long long kWaveEmpty = 0x7ff4dead5eed0001ull;
 
 // Relaxed (morally strong, single-copy atomic) loads and stores of in-pass slices.  The plain load
@@ -1076,25 +1081,25 @@ constexpr uint32_t kWaveDictMax = 255;
 template <int F, bool SIGMA>
 struct WaveRec {
     static constexpr uint32_t len_bytes = F == 0 ? 128u : 32u;
-    static constexpr uint32_t hdr = len_bytes + (SIGMA ? 128u : 0u);
+    static constexpr uint32_t info = len_bytes;                      // u32 {tile, L, 0, 0}
+    static constexpr uint32_t hdr = len_bytes + 16u + (SIGMA ? 128u : 0u);
     __host__ __device__ static constexpr uint32_t l8(uint32_t L) { return (L + 7u) & ~7u; }
     __host__ __device__ static constexpr uint32_t bytes(uint32_t L) {
         return F == 0 ? hdr + 384u * L : hdr + 128u * L + 32u * l8(L);
     }
-    static constexpr uint32_t max_staged = F == 0 ? 256u + 8u * 384u : 160u + 8u * 128u + 256u;
+    static constexpr uint32_t max_staged = bytes(8);
     __device__ static uint32_t len(const char* r, uint32_t lane) {
         if constexpr (F == 0) return reinterpret_cast<const uint32_t*>(r)[lane];
         else return reinterpret_cast<const uint8_t*>(r)[lane];
     }
     __device__ static uint32_t slot(const char* r, uint32_t lane) {
-        return reinterpret_cast<const uint32_t*>(r + len_bytes)[lane];
+        return reinterpret_cast<const uint32_t*>(r + len_bytes + 16u)[lane];
     }
+    __device__ static uint2 tile_l(const char* r) { return *reinterpret_cast<const uint2*>(r + info); }
 };
 __host__ __device__ constexpr uint32_t wave_rec_bytes(int F, bool sigma, uint32_t L) {
-    return F == 0 ? WaveRec<0, false>::bytes(L) + (sigma ? 128u : 0u) : WaveRec<1, false>::bytes(L) + (sigma ? 128u : 0u);
-}
-__host__ __device__ constexpr uint32_t wave_hdr(int F, bool sigma) {
-    return (F == 0 ? 128u : 32u) + (sigma ? 128u : 0u);
+    return F == 0 ? (sigma ? WaveRec<0, true>::bytes(L) : WaveRec<0, false>::bytes(L))
+                  : (sigma ? WaveRec<1, true>::bytes(L) : WaveRec<1, false>::bytes(L));
 }
 
 template <typename T>
@@ -1265,7 +1270,7 @@ constexpr uint32_t kWaveStreams = 16;
 constexpr uint32_t kWaveWarps = 8;
 constexpr uint32_t kWaveThreads = 32 * kWaveWarps;
 template <int F>
-__host__ __device__ constexpr uint32_t wave_stage_bytes() { return WaveRec<F, true>::max_staged; }
+__host__ __device__ constexpr uint32_t wave_stage_bytes() { return kWaveChunks * WaveRec<F, true>::max_staged; }
 template <int F>
 __host__ __device__ constexpr uint32_t wave_smem() { return kWaveWarps * 2 * wave_stage_bytes<F>(); }
 
@@ -1278,29 +1283,30 @@ __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint
         : "memory");
 }
 
-// Ticket descriptor (k_wave_desc): x = rec_off[T] (16-byte units), y = T | min(L, 15) << 24 |
-// (q - q0) << 28 (L = 15: a wide chunk, width read from the SELL offsets).
+// Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units, the tile's first
+// chunk record; its records are contiguous), y = the bytes to stage / 16 (0: a chunk wider than 8
+// entries, nothing staged but the first header) | (q - q0) << 16.  The tile index and the chunk
+// widths travel in the record headers.
 __device__ __forceinline__ uint2 ld_desc(const uint2* p) {
     uint2 r;
     asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
 
-// Lane 0: stage the record of ticket descriptor d (header only for a wide chunk).
+// Lane 0: stage the records of ticket descriptor d.
 template <int F, bool SIGMA>
 __device__ __forceinline__ void wave_stage(const FusedParams& P, uint2 d, uint32_t q0, uint32_t q1,
                                            uint32_t stage, uint32_t bar) {
-    const uint32_t Lc = (d.y >> 24) & 15u;
-    const uint32_t bytes = Lc <= 8 ? WaveRec<F, SIGMA>::bytes(Lc) : WaveRec<F, SIGMA>::hdr;
+    const uint32_t b16 = d.y & 0xffffu;
+    const uint32_t bytes = b16 ? b16 * 16u : WaveRec<F, SIGMA>::hdr;
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar, q0 + (d.y >> 28) == q1 ? P.pol_first : P.pol_last);
+    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar, q0 + (d.y >> 16) == q1 ? P.pol_first : P.pol_last);
 }
 
-template <int KIND, bool SIGMA, int F>
-__global__ void __launch_bounds__(kWaveThreads, F == 0 ? 4 : MPKG_WAVE_DICT_MINB) k_mpk_wave(const __grid_constant__ FusedParams P,
-                                                                            uint32_t t0, uint32_t t1, uint32_t q0,
-                                                                            uint32_t q1, uint32_t fill_lo,
-                                                                            uint32_t fill_hi) {
+template <int KIND, bool SIGMA, int F, bool TRACE>
+__global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
+                                                            uint32_t t1, uint32_t q0, uint32_t q1, uint32_t fill_lo,
+                                                            uint32_t fill_hi) {
     extern __shared__ __align__(128) char wsm[];
     __shared__ __align__(8) uint64_t bars[kWaveWarps][2];
     __shared__ double sdict[F == 1 ? kWaveDictMax + 1 : 1];
@@ -1358,60 +1364,83 @@ __global__ void __launch_bounds__(kWaveThreads, F == 0 ? 4 : MPKG_WAVE_DICT_MINB
             phase ^= 1u << st;
         }
         const char* stage = ring + st * SB;
-        const uint32_t T = d.y & 0xffffffu;
-        const uint32_t q = q0 + (d.y >> 28);
-        const uint32_t Lc = (d.y >> 24) & 15u;
+        const uint32_t q = q0 + (d.y >> 16);
+        const bool staged = (d.y & 0xffffu) != 0;
+        const uint32_t T = R::tile_l(stage).x;
         // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
-        const uint32_t s = T * kWaveRows + lane;
-        const uint32_t rr = SIGMA ? R::slot(stage, lane) : s;
-        const uint32_t len = rr < P.n_rows ? R::len(stage, lane) : 0u;
-        const char* body = stage + R::hdr;
-        double x[8];
-        double acc = 0.0;
-        bool slow = false;
-        switch (Lc) {
-            case 0: break;
-            case 1: acc = wave_dot<1, F>(body, lane, len, src, dict, x); break;
-            case 2: acc = wave_dot<2, F>(body, lane, len, src, dict, x); break;
-            case 3: acc = wave_dot<3, F>(body, lane, len, src, dict, x); break;
-            case 4: acc = wave_dot<4, F>(body, lane, len, src, dict, x); break;
-            case 5: acc = wave_dot<5, F>(body, lane, len, src, dict, x); break;
-            case 6: acc = wave_dot<6, F>(body, lane, len, src, dict, x); break;
-            case 7: acc = wave_dot<7, F>(body, lane, len, src, dict, x); break;
-            case 8: acc = wave_dot<8, F>(body, lane, len, src, dict, x); break;
-            default: slow = true;
-        }
-        // An empty (signalling-NaN) value makes the sum NaN: only then look at the values (slice
-        // q0-1 is complete and may hold any bit pattern: never checked).
-        if (Lc - 1u < 8u && q != q0 && is_nan_bits(acc)) {
-            bool miss = false;
+        const char* rec = stage;
+        uint64_t grec = (uint64_t)d.x * 16u;  // the chunk's record in global memory (wide tiles)
+        double tr_acc[TRACE ? kWaveChunks : 1];
+        uint32_t tr_off[TRACE ? kWaveChunks : 1];
+#pragma unroll 1
+        for (uint32_t c = 0; c < kWaveChunks; ++c) {
+            if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
+            const char* h = staged ? rec : P.wrec + grec;
+            const uint32_t L = R::tile_l(h).y;
+            const uint32_t s = T * kWaveRows + c * 32u + lane;
+            const uint32_t rr = SIGMA ? R::slot(h, lane) : s;
+            const uint32_t len = rr < P.n_rows ? R::len(h, lane) : 0u;
+            const char* body = h + R::hdr;
+            double x[8];
+            double acc = 0.0;
+            if (staged) {
+                switch (L) {
+                    case 0: break;
+                    case 1: acc = wave_dot<1, F>(body, lane, len, src, dict, x); break;
+                    case 2: acc = wave_dot<2, F>(body, lane, len, src, dict, x); break;
+                    case 3: acc = wave_dot<3, F>(body, lane, len, src, dict, x); break;
+                    case 4: acc = wave_dot<4, F>(body, lane, len, src, dict, x); break;
+                    case 5: acc = wave_dot<5, F>(body, lane, len, src, dict, x); break;
+                    case 6: acc = wave_dot<6, F>(body, lane, len, src, dict, x); break;
+                    case 7: acc = wave_dot<7, F>(body, lane, len, src, dict, x); break;
+                    default: acc = wave_dot<8, F>(body, lane, len, src, dict, x); break;
+                }
+                // An empty (signalling-NaN) value makes the sum NaN: only then look at the values
+                // (slice q0-1 is complete and may hold any bit pattern: never checked).
+                if (L != 0 && q != q0 && is_nan_bits(acc)) {
+                    bool miss = false;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
-            if (miss) acc = wave_redo<F>(body, Lc, lane, len, src, x, dict, P.dbg);
-        }
-        if (slow) {  // a wide chunk: its record from global memory
-            const uint32_t L = Lc != kWaveWideL ? Lc : (uint32_t)((P.chunk_off[T + 1] - P.chunk_off[T]) >> 5);
-            acc = wave_row_slow<F>(P.wrec + (uint64_t)d.x * 16u + R::hdr, L, lane, len, src, q == q0, dict, P.dbg);
+                    for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
+                    if (miss) acc = wave_redo<F>(body, L, lane, len, src, x, dict, P.dbg);
+                }
+            } else {  // a tile with a wide chunk: its records from global memory
+                acc = wave_row_slow<F>(body, L, lane, len, src, q == q0, dict, P.dbg);
+            }
+            if constexpr (TRACE) {  // audit build: every chunk's results are stored after the
+                                    // whole tile's inputs are final (one stamp between the two)
+                tr_acc[c] = acc;
+                if (c + 1 == kWaveChunks) {
+                    __syncwarp();
+                    if (lane == 0) {
+                        const unsigned long long ts = global_ns();
+                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T)] = ts;
+                        P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + 1] = ts;
+                    }
+                    __syncwarp();
+                    for (uint32_t c2 = 0; c2 < kWaveChunks; ++c2) {
+                        const uint32_t s2 = T * kWaveRows + c2 * 32u + lane;
+                        const char* h2 = staged ? stage + tr_off[c2] : P.wrec + (uint64_t)d.x * 16u + tr_off[c2];
+                        const uint32_t r2 = SIGMA ? R::slot(h2, lane) : s2;
+                        if (r2 < P.n_rows) wave_epilogue<KIND, SIGMA>(P, s2, r2, q, q0, src, tr_acc[c2]);
+                    }
+                }
+            } else if (rr < P.n_rows) {
+                wave_epilogue<KIND, SIGMA>(P, s, rr, q, q0, src, acc);
+            }
+            // The tile's last power in this pass also empties its rows of the next pass's in-pass
+            // slices (never read by this pass): k_wave_fill runs once per call instead of per pass.
+            if (q == q1 && s < (SIGMA ? P.n_slots : P.n_rows)) {
+                const double e = __longlong_as_double((long long)kWaveEmpty);
+                for (uint32_t f = fill_lo; f < fill_hi; ++f) P.V[(uint64_t)f * P.vstride + s] = e;
+            }
+            const uint32_t rb = R::bytes(L);
+            rec += rb;
+            grec += rb;
         }
         __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
         if (lane == 0 && tnn < t1) wave_stage<F, SIGMA>(P, dnn, q0, q1, ring_s + st * SB, bar0 + 8u * st);
-        if (P.trace) {  // every lane's inputs are final here, no result is stored yet
-            if (lane == 0) {
-                const unsigned long long ts = global_ns();
-                P.trace[2ull * ((uint64_t)q * P.n_tiles + T)] = ts;
-                P.trace[2ull * ((uint64_t)q * P.n_tiles + T) + 1] = ts;
-            }
-            __syncwarp();
-        }
-        if (rr < P.n_rows) wave_epilogue<KIND, SIGMA>(P, s, rr, q, q0, src, acc);
-        // The tile's last power in this pass also empties its rows of the next pass's in-pass
-        // slices (never read by this pass): k_wave_fill runs once per call instead of per pass.
-        if (q == q1 && s < (SIGMA ? P.n_slots : P.n_rows)) {
-            const double e = __longlong_as_double((long long)kWaveEmpty);
-            for (uint32_t f = fill_lo; f < fill_hi; ++f) P.V[(uint64_t)f * P.vstride + s] = e;
-        }
         t = tn, d = dn, tn = tnn, dn = dnn;
         st ^= 1u;
     }
@@ -1461,28 +1490,31 @@ __device__ __forceinline__ uint32_t dict_index(const unsigned long long* table, 
     return slot_ix[h];
 }
 
-// Chunk records from the executor's SELL arrays: one warp per chunk.
+// Chunk records from the executor's SELL arrays: one warp per chunk; records past the SELL (the
+// last tile's padding) are empty (lengths 0, width 0, slot rows ~0).
 template <int F>
 __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __restrict__ vals,
                             const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
-                            const uint64_t* __restrict__ chunk_off, uint32_t n_chunks,
+                            const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rec,
                             const uint32_t* __restrict__ rec_off, char* __restrict__ rec,
                             const unsigned long long* __restrict__ table, const uint16_t* __restrict__ slot_ix) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lb = F == 0 ? 128u : 32u;
-    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_chunks;
+    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_rec;
          T += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         char* r = rec + (uint64_t)rec_off[T] * 16u;
-        const uint32_t len = row_len[T * 32 + lane];
+        const bool real = T < n_chunks;
+        const uint32_t len = real ? row_len[T * 32 + lane] : 0u;
         if (F == 0) reinterpret_cast<uint32_t*>(r)[lane] = len;
         else reinterpret_cast<uint8_t*>(r)[lane] = (uint8_t)len;
-        uint32_t hdr = lb;
+        const uint64_t o = real ? chunk_off[T] : 0, ne = real ? chunk_off[T + 1] - o : 0;
+        const uint32_t L = (uint32_t)(ne >> 5);
+        if (lane < 4) reinterpret_cast<uint32_t*>(r + lb)[lane] = lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : 0u;
+        uint32_t hdr = lb + 16;
         if (slot_row) {
-            reinterpret_cast<uint32_t*>(r + lb)[lane] = slot_row[T * 32 + lane];
+            reinterpret_cast<uint32_t*>(r + hdr)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
             hdr += 128;
         }
-        const uint64_t o = chunk_off[T], ne = chunk_off[T + 1] - o;
-        const uint32_t L = (uint32_t)(ne >> 5);
         uint32_t* rc = reinterpret_cast<uint32_t*>(r + hdr);
         for (uint64_t e = lane; e < ne; e += 32) rc[e] = cols[o + e];
         if (F == 0) {
@@ -1505,14 +1537,15 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
 }
 
 // Descriptors of a pass's tickets from the host codes (T | q << 24, kLastUse ignored: the last use
-// is q == q1).
+// is q == q1); max_l: every chunk of a staged tile is at most 8 entries wide.
 __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
-                            const uint64_t* __restrict__ chunk_off, uint32_t q0, uint2* __restrict__ out) {
+                            const uint8_t* __restrict__ narrow, uint32_t q0, uint2* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t code = codes[i];
         const uint32_t T = code & 0xffffffu, q = (code >> 24) & 63u;
-        const uint64_t L = (chunk_off[T + 1] - chunk_off[T]) >> 5;
-        out[i] = make_uint2(rec_off[T], T | (uint32_t)(L < kWaveWideL ? L : kWaveWideL) << 24 | (q - q0) << 28);
+        const uint32_t o = rec_off[(uint64_t)T * kWaveChunks];
+        const uint32_t b16 = narrow[T] ? rec_off[(uint64_t)(T + 1) * kWaveChunks] - o : 0u;
+        out[i] = make_uint2(o, b16 | (q - q0) << 16);
     }
 }
 
@@ -2325,7 +2358,8 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
     {  // the chunk records (one per tile) and the bytes one tile-power touches (record + x read + y
        // written: the live-window model of wave_order)
         const uint32_t nc = E.S->n_chunks;
-        if (nc != nt) fail(MPKG_EINTERNAL, "wave: tiles must be the SELL chunks");
+        const uint64_t nrec = (uint64_t)nt * kWaveChunks;  // the last tile padded with empty records
+        if (nrec < nc) fail(MPKG_EINTERNAL, "wave: tiles do not cover the SELL chunks");
         std::vector<uint64_t> off((uint64_t)nc + 1);
         MPKG_CUDA(cudaMemcpyAsync(off.data(), E.S->chunk_off.p, 8 * off.size(), cudaMemcpyDeviceToHost, st));
         MPKG_CUDA(cudaStreamSynchronize(st));
@@ -2369,29 +2403,34 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
         }
         const bool sigma = E.order >= 1;
         E.tile_bytes.assign(nt, 0);
-        std::vector<uint32_t> ro((uint64_t)nc + 1);
+        std::vector<uint32_t> ro(nrec + 1);
+        std::vector<uint8_t> narrow(nt, 1);
         uint64_t acc = 0;
-        for (uint32_t c = 0; c < nc; ++c) {
+        for (uint64_t c = 0; c < nrec; ++c) {
             ro[c] = (uint32_t)acc;
-            const uint32_t rb = wave_rec_bytes(E.wave_fmt, sigma, (uint32_t)((off[c + 1] - off[c]) >> 5));
+            const uint32_t L = c < nc ? (uint32_t)((off[c + 1] - off[c]) >> 5) : 0u;
+            const uint32_t rb = wave_rec_bytes(E.wave_fmt, sigma, L);
             acc += rb / 16;
             if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
-            E.tile_bytes[c] = rb + 16ull * 32;
+            E.tile_bytes[c / kWaveChunks] += rb + 16ull * 32;
+            if (L > 8) narrow[c / kWaveChunks] = 0;
         }
-        ro[nc] = (uint32_t)acc;
-        E.wrec_off.alloc((uint64_t)nc + 1);
+        ro[nrec] = (uint32_t)acc;
+        E.wrec_off.alloc(nrec + 1);
         E.wrec.alloc(std::max<uint64_t>(acc * 16, 16));
+        E.wave_narrow.alloc(std::max<uint64_t>(nt, 1));
         MPKG_CUDA(cudaMemcpyAsync(E.wrec_off.p, ro.data(), 4 * ro.size(), cudaMemcpyHostToDevice, st));
-        if (nc) {
-            const unsigned g = grid_for((uint64_t)nc * 32, 256, (unsigned)ctx->sm_count * 8u);
+        if (nt) MPKG_CUDA(cudaMemcpyAsync(E.wave_narrow.p, narrow.data(), nt, cudaMemcpyHostToDevice, st));
+        if (nrec) {
+            const unsigned g = grid_for(nrec * 32, 256, (unsigned)ctx->sm_count * 8u);
             if (E.wave_fmt == 1)
                 k_wave_pack<1><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
-                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc, E.wrec_off.p,
-                                                  E.wrec.p, table.p, slot_ix.p);
+                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
+                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, table.p, slot_ix.p);
             else
                 k_wave_pack<0><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
-                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc, E.wrec_off.p,
-                                                  E.wrec.p, nullptr, nullptr);
+                                                  sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
+                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, nullptr, nullptr);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2517,7 +2556,7 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
         const uint64_t b = W.t_begin[j], e = W.t_begin[j + 1];
         if (e > b) {
             k_wave_desc<<<grid_for(e - b, 256, (unsigned)ctx->sm_count * 8u), 256, 0, ctx->stream>>>(
-                W.tickets.p + b, e - b, E.wrec_off.p, E.S->chunk_off.p, (uint32_t)W.q_begin[j], W.desc.p + b);
+                W.tickets.p + b, e - b, E.wrec_off.p, E.wave_narrow.p, (uint32_t)W.q_begin[j], W.desc.p + b);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2527,13 +2566,14 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.wave.emplace(p, std::move(W)).first->second;
 }
 
-void* wave_fn(int kind, bool sigma, int fmt) {
-    static void* const fns[2][4] = {
-        {(void*)k_mpk_wave<0, false, 0>, (void*)k_mpk_wave<0, true, 0>, (void*)k_mpk_wave<1, false, 0>,
-         (void*)k_mpk_wave<1, true, 0>},
-        {(void*)k_mpk_wave<0, false, 1>, (void*)k_mpk_wave<0, true, 1>, (void*)k_mpk_wave<1, false, 1>,
-         (void*)k_mpk_wave<1, true, 1>}};
-    return fns[fmt][kind * 2 + (sigma ? 1 : 0)];
+void* wave_fn(int kind, bool sigma, int fmt, bool trace) {
+#define MPKG_WAVE_FNS(F, TR)                                                                         \
+    {(void*)k_mpk_wave<0, false, F, TR>, (void*)k_mpk_wave<0, true, F, TR>, (void*)k_mpk_wave<1, false, F, TR>, \
+     (void*)k_mpk_wave<1, true, F, TR>}
+    static void* const fns[2][2][4] = {{MPKG_WAVE_FNS(0, false), MPKG_WAVE_FNS(0, true)},
+                                       {MPKG_WAVE_FNS(1, false), MPKG_WAVE_FNS(1, true)}};
+#undef MPKG_WAVE_FNS
+    return fns[fmt][trace ? 1 : 0][kind * 2 + (sigma ? 1 : 0)];
 }
 uint32_t wave_smem_for(int fmt) { return fmt == 1 ? wave_smem<1>() : wave_smem<0>(); }
 
@@ -2636,9 +2676,11 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         int occ = 1 << 30;
         for (int k = 0; k < 4; ++k) {
             int o = 0;
-            void* fn = wave_fn(k / 2, k % 2, E.wave_fmt);
+            void* fn = wave_fn(k / 2, k % 2, E.wave_fmt, false);
             const uint32_t sm = wave_smem_for(E.wave_fmt);
             MPKG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            MPKG_CUDA(cudaFuncSetAttribute(wave_fn(k / 2, k % 2, E.wave_fmt, true),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             MPKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWaveThreads, sm));
             occ = std::min(occ, o);
         }
@@ -2974,7 +3016,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (wave) {
         // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
         // host block, the pass's slices go to the host while the next pass runs
-        void* fn = wave_fn(a.kind, sigma, E.wave_fmt);
+        void* fn = wave_fn(a.kind, sigma, E.wave_fmt, P.trace != nullptr);
         P.counter = E.counter.p;
         P.dbg = getenv("MPKG_WAVE_DEBUG") ? E.counter.p + kWaveStreams * 32 : nullptr;
         for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
