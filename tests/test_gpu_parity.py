@@ -598,3 +598,35 @@ def test_config1_full_size_bitwise(ctx, oracle):
     plan = ctx.group_levels(ls, Ap, 100 << 20, 4)
     ref = oracle.baseline_mpk(prp, pci, pv, x, 4)
     assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref)
+
+
+@pytest.mark.parametrize("dict_fmt", [1, 0])
+def test_wave_special_values_and_sentinel_pattern(ctx, oracle, dict_fmt):
+    """The wave schedule synchronises by value (a signalling-NaN sentinel in the slices a pass
+    writes): caller data in x may hold any bit pattern, including Inf, NaN and the sentinel itself,
+    and must flow through exactly as in the reference's row loop.  NaN payloads are compared as
+    NaN (CPU and GPU quiet a signalling NaN differently); every other value bitwise."""
+    A = mpkg.poisson3d(24, 24, 24)
+    dA = ctx.csr(A)
+    ls = ctx.build_levels(dA)
+    Ap = ctx.permute(dA, ls)
+    P = Ap.download()
+    x = mpkg.random_vector(A.n_rows, 5)
+    x[17] = np.inf
+    x[2000] = -np.inf
+    x[4000] = np.nan
+    x[9000:9001].view(np.uint64)[0] = np.uint64(0x7FF4DEAD5EED0001)  # kWaveEmpty, as caller data
+    try:
+        set_knobs(ctx, {"schedule": 3, "pass": 3})
+        ctx.set_param("wave_dict", dict_fmt)
+        plan = ctx.group_levels(ls, Ap, 1 << 20, 6)
+        got = ctx.mpk(plan, Ap, x, 6).as_matrix()
+        assert plan.exec_info()["schedule"] == "wave"
+    finally:
+        set_knobs(ctx, {})
+        ctx.set_param("wave_dict", 1)
+    ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 6)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    assert_bitwise(got[ok], ref[ok], "non-NaN values")
+    assert np.isnan(got[1:]).sum() > 100  # the NaNs really spread through the powers
