@@ -1074,9 +1074,6 @@ constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
 constexpr int kWaveAutoPass = 3;
 constexpr uint32_t kWaveDictMax = 255;
-#ifndef MPKG_WAVE_DICT_MINB
-#define MPKG_WAVE_DICT_MINB 4
-#endif
 
 template <int F, bool SIGMA>
 struct WaveRec {
@@ -1377,15 +1374,15 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
 #pragma unroll 1
         for (uint32_t c = 0; c < kWaveChunks; ++c) {
             if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
-            const char* h = staged ? rec : P.wrec + grec;
-            const uint32_t L = R::tile_l(h).y;
             const uint32_t s = T * kWaveRows + c * 32u + lane;
-            const uint32_t rr = SIGMA ? R::slot(h, lane) : s;
-            const uint32_t len = rr < P.n_rows ? R::len(h, lane) : 0u;
-            const char* body = h + R::hdr;
-            double x[8];
+            uint32_t L, rr, len;
             double acc = 0.0;
-            if (staged) {
+            if (staged) {  // the record in shared memory (every load below is an LDS)
+                L = R::tile_l(rec).y;
+                rr = SIGMA ? R::slot(rec, lane) : s;
+                len = rr < P.n_rows ? R::len(rec, lane) : 0u;
+                const char* body = rec + R::hdr;
+                double x[8];
                 switch (L) {
                     case 0: break;
                     case 1: acc = wave_dot<1, F>(body, lane, len, src, dict, x); break;
@@ -1406,7 +1403,11 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                     if (miss) acc = wave_redo<F>(body, L, lane, len, src, x, dict, P.dbg);
                 }
             } else {  // a tile with a wide chunk: its records from global memory
-                acc = wave_row_slow<F>(body, L, lane, len, src, q == q0, dict, P.dbg);
+                const char* h = P.wrec + grec;
+                L = R::tile_l(h).y;
+                rr = SIGMA ? R::slot(h, lane) : s;
+                len = rr < P.n_rows ? R::len(h, lane) : 0u;
+                acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg);
             }
             if constexpr (TRACE) {  // audit build: every chunk's results are stored after the
                                     // whole tile's inputs are final (one stamp between the two)
