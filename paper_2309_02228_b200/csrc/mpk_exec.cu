@@ -1093,6 +1093,7 @@ struct WaveRec {
         return reinterpret_cast<const uint32_t*>(r + len_bytes + 16u)[lane];
     }
     __device__ static uint2 tile_l(const char* r) { return *reinterpret_cast<const uint2*>(r + info); }
+    __device__ static uint4 info4(const char* r) { return *reinterpret_cast<const uint4*>(r + info); }
 };
 __host__ __device__ constexpr uint32_t wave_rec_bytes(int F, bool sigma, uint32_t L) {
     return F == 0 ? (sigma ? WaveRec<0, true>::bytes(L) : WaveRec<0, false>::bytes(L))
@@ -1368,17 +1369,18 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
         const char* rec = stage;
-        uint64_t grec = (uint64_t)d.x * 16u;  // the chunk's record in global memory (wide tiles)
         double tr_acc[TRACE ? kWaveChunks : 1];
         uint32_t tr_off[TRACE ? kWaveChunks : 1];
 #pragma unroll 1
         for (uint32_t c = 0; c < kWaveChunks; ++c) {
             if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
             const uint32_t s = T * kWaveRows + c * 32u + lane;
-            uint32_t L, rr, len;
+            uint32_t L, rr, len, rb;
             double acc = 0.0;
             if (staged) {  // the record in shared memory (every load below is an LDS)
-                L = R::tile_l(rec).y;
+                const uint4 inf = R::info4(rec);
+                L = inf.y;
+                rb = inf.z;
                 rr = SIGMA ? R::slot(rec, lane) : s;
                 len = rr < P.n_rows ? R::len(rec, lane) : 0u;
                 const char* body = rec + R::hdr;
@@ -1405,8 +1407,10 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                     if (miss) acc = wave_redo<F>(body, L, lane, len, src, x, dict, P.dbg);
                 }
             } else {  // a tile with a wide chunk: its records from global memory
-                const char* h = P.wrec + grec;
-                L = R::tile_l(h).y;
+                const char* h = P.wrec + (uint64_t)d.x * 16u + (uint64_t)(rec - stage);
+                const uint4 inf = R::info4(h);
+                L = inf.y;
+                rb = inf.z;
                 rr = SIGMA ? R::slot(h, lane) : s;
                 len = rr < P.n_rows ? R::len(h, lane) : 0u;
                 acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg);
@@ -1438,9 +1442,7 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                 const double e = __longlong_as_double((long long)kWaveEmpty);
                 for (uint32_t f = fill_lo; f < fill_hi; ++f) P.V[(uint64_t)f * P.vstride + s] = e;
             }
-            const uint32_t rb = R::bytes(L);
             rec += rb;
-            grec += rb;
         }
         __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
         if (lane == 0 && tnn < t1) wave_stage<F, SIGMA>(P, dnn, q0, q1, ring_s + st * SB, bar0 + 8u * st);
@@ -1512,7 +1514,9 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
         else reinterpret_cast<uint8_t*>(r)[lane] = (uint8_t)len;
         const uint64_t o = real ? chunk_off[T] : 0, ne = real ? chunk_off[T + 1] - o : 0;
         const uint32_t L = (uint32_t)(ne >> 5);
-        if (lane < 4) reinterpret_cast<uint32_t*>(r + lb)[lane] = lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : 0u;
+        if (lane < 4)  // info: tile, width, this record's bytes
+            reinterpret_cast<uint32_t*>(r + lb)[lane] =
+                lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : lane == 2 ? (rec_off[T + 1] - rec_off[T]) * 16u : 0u;
         uint32_t hdr = lb + 16;
         if (slot_row) {
             reinterpret_cast<uint32_t*>(r + hdr)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
