@@ -332,6 +332,8 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->trace = value != 0;
         else if (k == "wave_dict")
             ctx->wave_dict = value != 0;
+        else if (k == "wave_affine")
+            ctx->wave_affine = value != 0;
         else if (k == "pdl")
             ctx->pdl = value != 0;
         else if (k == "schedule") {
@@ -826,6 +828,14 @@ int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uin
     return guarded([&] {
         require(P != nullptr, "plan_exec_mode: null plan");
         exec_mode(P, order, sweeps, kernel, long_rows);
+    });
+}
+
+int mpkg_plan_exec_wave(mpkg_plan_t P, int* format, uint64_t* n_chunks, uint64_t* n_affine,
+                        uint64_t* record_bytes) {
+    return guarded([&] {
+        require(P != nullptr, "plan_exec_wave: null plan");
+        exec_wave(P, format, n_chunks, n_affine, record_bytes);
     });
 }
 

@@ -133,6 +133,8 @@ struct Executor {
     int wave_fmt = 0;                         // chunk-record format: 0 plain, 1 value dictionary
     DevBuf<double> wave_dict;                 // the distinct values (wave_fmt 1)
     uint32_t n_dict = 0;
+    uint64_t wave_affine_chunks = 0;          // chunks stored as affine records
+    uint64_t wave_rec_total = 0;              // bytes of all chunk records
     uint64_t wave_pol[2] = {0, 0};            // createpolicy evict_first / evict_last values
     DevBuf<unsigned long long> trace;         // "trace" knob (FusedParams::trace)
     uint64_t trace_n = 0;
@@ -1025,8 +1027,13 @@ __global__ void __launch_bounds__(128) k_mpk_lean(const __grid_constant__ FusedP
 #ifndef MPKG_WAVE_CHUNKS
 #define MPKG_WAVE_CHUNKS 2
 #endif
+#ifndef MPKG_WAVE_CTAS
+#define MPKG_WAVE_CTAS 4
+#endif
+constexpr int kWaveCtas = MPKG_WAVE_CTAS;  // resident CTAs per SM k_mpk_wave is compiled for (register cap)
 constexpr uint32_t kWaveChunks = MPKG_WAVE_CHUNKS;  // SELL chunks per tile (processed one after the other)
 constexpr uint32_t kWaveRows = 32 * kWaveChunks;   // rows per tile
+static_assert(kWaveChunks % 2 == 0, "the fast-tile path takes chunks two at a time");
 constexpr unsigned long long kWaveEmpty = 0x7ff4dead5eed0001ull;
 
 // Relaxed (morally strong, single-copy atomic) loads and stores of in-pass slices.  The plain load
@@ -1069,7 +1076,15 @@ __device__ __forceinline__ double wave_wait(const double* p, double v) {
 // index into the matrix's table of distinct values (CSR-VI value compression; lossless, chosen when
 // the matrix has at most 255 distinct values and rows of at most 255 entries): 5 B per entry
 // instead of 12 on the HBM stream, and a 1,440-byte stage instead of 3,328 (more warps per SM).
+// A dict-format chunk whose 32 rows are all full (len == L <= 8) and whose entry k has column
+// base_k + lane and one value v_k in every lane (a piece of a diagonal: what a level-ordered
+// stencil's interior looks like) is stored as an AFFINE record instead (info.w = kWaveAffine):
+//   len[32] u8 | info | slot_row[32] u32 (private order only) | base[8] u32 | v[8] f64
+// 144 bytes instead of 1,200 for a 7-point chunk, no per-lane column or value loads, the same
+// entries in the same stored order (lossless; detected per chunk by k_wave_affine, knob
+// wave_affine).
 // rec_off[T] is the record's offset in 16-byte units.
+constexpr uint32_t kWaveAffine = 1u;
 constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
 constexpr int kWaveAutoPass = 3;
@@ -1085,6 +1100,7 @@ struct WaveRec {
         return F == 0 ? hdr + 384u * L : hdr + 128u * L + 32u * l8(L);
     }
     static constexpr uint32_t max_staged = bytes(8);
+    static constexpr uint32_t affine_bytes = hdr + 96u;
     __device__ static uint32_t len(const char* r, uint32_t lane) {
         if constexpr (F == 0) return reinterpret_cast<const uint32_t*>(r)[lane];
         else return reinterpret_cast<const uint8_t*>(r)[lane];
@@ -1095,6 +1111,9 @@ struct WaveRec {
     __device__ static uint2 tile_l(const char* r) { return *reinterpret_cast<const uint2*>(r + info); }
     __device__ static uint4 info4(const char* r) { return *reinterpret_cast<const uint4*>(r + info); }
 };
+__host__ __device__ constexpr uint32_t wave_affine_bytes(bool sigma) {
+    return sigma ? WaveRec<1, true>::affine_bytes : WaveRec<1, false>::affine_bytes;
+}
 __host__ __device__ constexpr uint32_t wave_rec_bytes(int F, bool sigma, uint32_t L) {
     return F == 0 ? (sigma ? WaveRec<0, true>::bytes(L) : WaveRec<0, false>::bytes(L))
                   : (sigma ? WaveRec<1, true>::bytes(L) : WaveRec<1, false>::bytes(L));
@@ -1122,7 +1141,11 @@ __device__ __forceinline__ bool is_nan_bits(double v) {
 // Entry k of `lane`'s row in a record (global or staged): its column and its value.
 template <int F>
 __device__ __forceinline__ uint32_t rec_entry(const char* body, uint32_t L, uint32_t k, uint32_t lane,
-                                              const double* dict, double& v) {
+                                              const double* dict, double& v, bool affine = false) {
+    if (F == 1 && affine) {
+        v = reinterpret_cast<const double*>(body + 32)[k];
+        return reinterpret_cast<const uint32_t*>(body)[k] + lane;
+    }
     const uint32_t Lp = L & ~1u;
     const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
     const uint32_t c = reinterpret_cast<const uint32_t*>(body)[e];
@@ -1139,12 +1162,13 @@ __device__ __forceinline__ uint32_t rec_entry(const char* body, uint32_t L, uint
 // awaited (first: the source slice is complete, read-only path).
 template <int F>
 __device__ __forceinline__ double wave_row_slow(const char* body, uint32_t L, uint32_t lane, uint32_t len,
-                                                const double* src, bool first, const double* dict, uint32_t* dbg) {
+                                                const double* src, bool first, const double* dict, uint32_t* dbg,
+                                                bool affine) {
     if (dbg) atomicAdd(dbg, 1u);
     double acc = 0.0;
     for (uint32_t k = 0; k < len; ++k) {
         double v;
-        const uint32_t c = rec_entry<F>(body, L, k, lane, dict, v);
+        const uint32_t c = rec_entry<F>(body, L, k, lane, dict, v, affine);
         double x;
         if (first) {
             x = __ldg(src + c);
@@ -1231,6 +1255,65 @@ __device__ __forceinline__ double wave_dot(const char* body, uint32_t lane, uint
     return acc;
 }
 
+// An affine chunk (see the record formats): entry k of lane's row is column base[k] + lane with
+// value v[k]; every row is full, so there are no length predicates and no padding.  src_lane =
+// src + lane.  The same products in the same stored order as wave_dot.  Gathers and sum are
+// separate so that a tile's chunks can have all their gathers in flight together.
+template <int L>
+__device__ __forceinline__ void affine_gather(const char* body, const double* src_lane, double (&x)[L]) {
+    const uint4 b0 = *reinterpret_cast<const uint4*>(body);
+    uint4 b1 = make_uint4(0u, 0u, 0u, 0u);
+    if (L > 4) b1 = *reinterpret_cast<const uint4*>(body + 16);
+    const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int j = 0; j < L; ++j) x[j] = ld_gather(src_lane + b[j]);
+}
+template <int L>
+__device__ __forceinline__ double affine_sum(const char* body, const double (&x)[L]) {
+    const double2* v = reinterpret_cast<const double2*>(body + 32);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; j += 2) {
+        const double2 vv = v[j >> 1];
+        acc = __dadd_rn(acc, __dmul_rn(vv.x, x[j]));
+        if (j + 1 < L) acc = __dadd_rn(acc, __dmul_rn(vv.y, x[j + 1]));
+    }
+    return acc;
+}
+// Any width 1..8 (warp-uniform guards).
+__device__ __forceinline__ double wave_dot_affine_any(const char* body, uint32_t L, const double* src_lane) {
+    const uint32_t* b = reinterpret_cast<const uint32_t*>(body);
+    const double* v = reinterpret_cast<const double*>(body + 32);
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = (uint32_t)j < L ? ld_gather(src_lane + b[j]) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if ((uint32_t)j < L) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+    return acc;
+}
+// An affine row whose sum came out NaN (an empty value among its inputs, or a NaN in the data):
+// every input re-read with relaxed L2 loads until it is stored, then the sum again in stored
+// order.  Cold: a rolled loop, and the hot path keeps no gathered value alive for it.
+__device__ __forceinline__ double wave_redo_affine(const char* body, uint32_t L, const double* src_lane, uint32_t* dbg) {
+    if (dbg) atomicAdd(dbg, 1u);
+    const uint32_t* b = reinterpret_cast<const uint32_t*>(body);
+    const double* v = reinterpret_cast<const double*>(body + 32);
+    double acc = 0.0;
+#pragma unroll 1
+    for (uint32_t k = 0; k < L; ++k) {
+        const double* p = src_lane + b[k];
+        double x = ld_strong_again(p);
+        while (wave_empty(x)) {
+            __nanosleep(32);
+            x = ld_strong_again(p);
+        }
+        acc = __dadd_rn(acc, __dmul_rn(v[k], x));
+    }
+    return acc;
+}
+
 // row_epilogue with the wave's rules: in-pass values are awaited, working-vector stores are
 // single-copy atomic (KIND 2 never runs here: its accumulator has no value to wait on).
 template <int KIND, bool SIGMA>
@@ -1267,10 +1350,14 @@ constexpr uint32_t kWaveStreams = 16;
 // staged (their rows take wave_row_slow from global memory).
 constexpr uint32_t kWaveWarps = 8;
 constexpr uint32_t kWaveThreads = 32 * kWaveWarps;
-template <int F>
-__host__ __device__ constexpr uint32_t wave_stage_bytes() { return kWaveChunks * WaveRec<F, true>::max_staged; }
-template <int F>
-__host__ __device__ constexpr uint32_t wave_smem() { return kWaveWarps * 2 * wave_stage_bytes<F>(); }
+// A stage holds two general chunk records of width 8; a tile whose records need more (tiles of more
+// than two chunks that are not mostly affine) is not staged.
+template <int F, bool SIGMA>
+__host__ __device__ constexpr uint32_t wave_stage_bytes() {
+    return (2u * WaveRec<F, SIGMA>::max_staged + 127u) & ~127u;
+}
+template <int F, bool SIGMA>
+__host__ __device__ constexpr uint32_t wave_smem() { return kWaveWarps * 2 * wave_stage_bytes<F, SIGMA>(); }
 
 __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
                                              uint64_t pol) {
@@ -1283,7 +1370,7 @@ __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint
 
 // Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units, the tile's first
 // chunk record; its records are contiguous), y = the bytes to stage / 16 (0: a chunk wider than 8
-// entries, nothing staged but the first header) | (q - q0) << 16.  The tile index and the chunk
+// entries, nothing staged but the first header) | (q - q0) << 16 | fast-tile width << 24.  The tile index and the chunk
 // widths travel in the record headers.
 __device__ __forceinline__ uint2 ld_desc(const uint2* p) {
     uint2 r;
@@ -1298,18 +1385,19 @@ __device__ __forceinline__ void wave_stage(const FusedParams& P, uint2 d, uint32
     const uint32_t b16 = d.y & 0xffffu;
     const uint32_t bytes = b16 ? b16 * 16u : WaveRec<F, SIGMA>::hdr;
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar, q0 + (d.y >> 16) == q1 ? P.pol_first : P.pol_last);
+    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar,
+                 q0 + ((d.y >> 16) & 15u) == q1 ? P.pol_first : P.pol_last);
 }
 
 template <int KIND, bool SIGMA, int F, bool TRACE>
-__global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
+__global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __grid_constant__ FusedParams P, uint32_t t0,
                                                             uint32_t t1, uint32_t q0, uint32_t q1, uint32_t fill_lo,
                                                             uint32_t fill_hi) {
     extern __shared__ __align__(128) char wsm[];
     __shared__ __align__(8) uint64_t bars[kWaveWarps][2];
     __shared__ double sdict[F == 1 ? kWaveDictMax + 1 : 1];
     using R = WaveRec<F, SIGMA>;
-    constexpr uint32_t SB = wave_stage_bytes<F>();
+    constexpr uint32_t SB = wave_stage_bytes<F, SIGMA>();
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     const uint32_t gw = blockIdx.x * kWaveWarps + wib;
     const uint32_t sid = gw % kWaveStreams;
@@ -1362,22 +1450,68 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
             phase ^= 1u << st;
         }
         const char* stage = ring + st * SB;
-        const uint32_t q = q0 + (d.y >> 16);
+        const uint32_t q = q0 + ((d.y >> 16) & 15u);
         const bool staged = (d.y & 0xffffu) != 0;
         const uint32_t T = R::tile_l(stage).x;
         // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
+        const double* src_lane = src + lane;
         const char* rec = stage;
         double tr_acc[TRACE ? kWaveChunks : 1];
         uint32_t tr_off[TRACE ? kWaveChunks : 1];
+        if (F == 1 && !TRACE && ((d.y >> 24) & 15u) == 7u) {
+            // Fast tile (descriptor bits 24-27): every chunk an affine record of width 7 (the
+            // interior of a level-ordered 3D 7-point stencil).  Two chunks at a time: both chunks'
+            // gathers are in flight before the first sum.
+            double* const dst = P.V + (uint64_t)q * P.vstride;
+#pragma unroll
+            for (uint32_t c = 0; c < kWaveChunks; c += 2) {
+                const char* ba = stage + c * R::affine_bytes + R::hdr;
+                const char* bb = ba + R::affine_bytes;
+                const uint32_t s = T * kWaveRows + c * 32u + lane;
+                double xa[7], xb[7];
+                affine_gather<7>(ba, src_lane, xa);
+                affine_gather<7>(bb, src_lane, xb);
+                double a0 = affine_sum<7>(ba, xa);
+                double a1 = affine_sum<7>(bb, xb);
+                if (q != q0) {
+                    if (is_nan_bits(a0)) a0 = wave_redo_affine(ba, 7u, src_lane, P.dbg);
+                    if (is_nan_bits(a1)) a1 = wave_redo_affine(bb, 7u, src_lane, P.dbg);
+                }
+                if constexpr (KIND == 0 && !SIGMA) {
+                    st_strong(dst + s, a0);
+                    st_strong(dst + s + 32u, a1);
+                } else {
+                    wave_epilogue<KIND, SIGMA>(P, s, SIGMA ? R::slot(ba - R::hdr, lane) : s, q, q0, src, a0);
+                    wave_epilogue<KIND, SIGMA>(P, s + 32u, SIGMA ? R::slot(bb - R::hdr, lane) : s + 32u, q, q0, src,
+                                               a1);
+                }
+                if (q == q1) {
+                    const double e = __longlong_as_double((long long)kWaveEmpty);
+                    for (uint32_t f = fill_lo; f < fill_hi; ++f) {
+                        P.V[(uint64_t)f * P.vstride + s] = e;
+                        P.V[(uint64_t)f * P.vstride + s + 32u] = e;
+                    }
+                }
+            }
+        } else {
 #pragma unroll 1
         for (uint32_t c = 0; c < kWaveChunks; ++c) {
             if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
             const uint32_t s = T * kWaveRows + c * 32u + lane;
             uint32_t L, rr, len, rb;
             double acc = 0.0;
-            if (staged) {  // the record in shared memory (every load below is an LDS)
+            if (staged && F == 1 && (R::info4(rec).w & kWaveAffine)) {  // an affine chunk: full rows
+                const uint4 inf = R::info4(rec);
+                L = inf.y;
+                rb = inf.z;
+                rr = SIGMA ? R::slot(rec, lane) : s;
+                len = L;
+                const char* body = rec + R::hdr;
+                acc = wave_dot_affine_any(body, L, src_lane);
+                if (q != q0 && is_nan_bits(acc)) acc = wave_redo_affine(body, L, src_lane, P.dbg);
+            } else if (staged) {  // the record in shared memory (every load below is an LDS)
                 const uint4 inf = R::info4(rec);
                 L = inf.y;
                 rb = inf.z;
@@ -1413,7 +1547,8 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                 rb = inf.z;
                 rr = SIGMA ? R::slot(h, lane) : s;
                 len = rr < P.n_rows ? R::len(h, lane) : 0u;
-                acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg);
+                acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg,
+                                       (inf.w & kWaveAffine) != 0);
             }
             if constexpr (TRACE) {  // audit build: every chunk's results are stored after the
                                     // whole tile's inputs are final (one stamp between the two)
@@ -1443,6 +1578,7 @@ __global__ void __launch_bounds__(kWaveThreads, 4) k_mpk_wave(const __grid_const
                 for (uint32_t f = fill_lo; f < fill_hi; ++f) P.V[(uint64_t)f * P.vstride + s] = e;
             }
             rec += rb;
+        }
         }
         __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
         if (lane == 0 && tnn < t1) wave_stage<F, SIGMA>(P, dnn, q0, q1, ring_s + st * SB, bar0 + 8u * st);
@@ -1495,6 +1631,36 @@ __device__ __forceinline__ uint32_t dict_index(const unsigned long long* table, 
     return slot_ix[h];
 }
 
+// Affine chunks (setup): one warp per SELL chunk; flags[T] = 1 when the chunk has width 1..8, 32
+// real full rows, and every entry k is column c_k + lane with one value bit pattern in all lanes.
+__global__ void k_wave_affine(const uint32_t* __restrict__ cols, const double* __restrict__ vals,
+                              const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
+                              const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rows,
+                              uint8_t* __restrict__ flags) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_chunks;
+         T += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint64_t o = chunk_off[T];
+        const uint32_t L = (uint32_t)((chunk_off[T + 1] - o) >> 5);
+        bool ok = L >= 1 && L <= 8;
+        if (ok) {
+            const uint32_t row = slot_row ? slot_row[T * 32 + lane] : (uint32_t)(T * 32 + lane);
+            ok = row < n_rows && row_len[T * 32 + lane] == L;
+            const uint32_t Lp = L & ~1u;
+            for (uint32_t k = 0; k < L; ++k) {
+                const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
+                const uint32_t c = cols[o + e];
+                const unsigned long long b = (unsigned long long)__double_as_longlong(vals[o + e]);
+                const uint32_t c0 = __shfl_sync(0xffffffffu, c, 0);
+                const unsigned long long b0 = __shfl_sync(0xffffffffu, b, 0);
+                ok = ok && c0 <= 0xffffffffu - 31u && c == c0 + lane && b == b0;
+            }
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) flags[T] = ok ? 1 : 0;
+    }
+}
+
 // Chunk records from the executor's SELL arrays: one warp per chunk; records past the SELL (the
 // last tile's padding) are empty (lengths 0, width 0, slot rows ~0).
 template <int F>
@@ -1502,7 +1668,8 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
                             const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
                             const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rec,
                             const uint32_t* __restrict__ rec_off, char* __restrict__ rec,
-                            const unsigned long long* __restrict__ table, const uint16_t* __restrict__ slot_ix) {
+                            const unsigned long long* __restrict__ table, const uint16_t* __restrict__ slot_ix,
+                            const uint8_t* __restrict__ affine) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lb = F == 0 ? 128u : 32u;
     for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_rec;
@@ -1514,13 +1681,24 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
         else reinterpret_cast<uint8_t*>(r)[lane] = (uint8_t)len;
         const uint64_t o = real ? chunk_off[T] : 0, ne = real ? chunk_off[T + 1] - o : 0;
         const uint32_t L = (uint32_t)(ne >> 5);
-        if (lane < 4)  // info: tile, width, this record's bytes
+        const bool aff = F == 1 && real && affine && affine[T];
+        if (lane < 4)  // info: tile, width, this record's bytes, flags
             reinterpret_cast<uint32_t*>(r + lb)[lane] =
-                lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : lane == 2 ? (rec_off[T + 1] - rec_off[T]) * 16u : 0u;
+                lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : lane == 2 ? (rec_off[T + 1] - rec_off[T]) * 16u
+                                                                               : (aff ? kWaveAffine : 0u);
         uint32_t hdr = lb + 16;
         if (slot_row) {
             reinterpret_cast<uint32_t*>(r + hdr)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
             hdr += 128;
+        }
+        if (aff) {  // base[8] u32 | v[8] f64: lane 0's entries (every lane's column is base + lane)
+            if (lane < 8) {
+                const uint32_t k = lane, Lp = L & ~1u;
+                const uint64_t e = k < Lp ? (k >> 1) * 64u + (k & 1u) : Lp * 32u;
+                reinterpret_cast<uint32_t*>(r + hdr)[k] = k < L ? cols[o + e] : 0u;
+                reinterpret_cast<double*>(r + hdr + 32)[k] = k < L ? vals[o + e] : 0.0;
+            }
+            continue;
         }
         uint32_t* rc = reinterpret_cast<uint32_t*>(r + hdr);
         for (uint64_t e = lane; e < ne; e += 32) rc[e] = cols[o + e];
@@ -1544,15 +1722,17 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
 }
 
 // Descriptors of a pass's tickets from the host codes (T | q << 24, kLastUse ignored: the last use
-// is q == q1); max_l: every chunk of a staged tile is at most 8 entries wide.
+// is q == q1); narrow[T] bit 0: every chunk of the tile is at most 8 entries wide (staged), bits
+// 4-7: the width of a fast tile (all chunks affine records of that width), 0 otherwise.
 __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
                             const uint8_t* __restrict__ narrow, uint32_t q0, uint2* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t code = codes[i];
         const uint32_t T = code & 0xffffffu, q = (code >> 24) & 63u;
         const uint32_t o = rec_off[(uint64_t)T * kWaveChunks];
-        const uint32_t b16 = narrow[T] ? rec_off[(uint64_t)(T + 1) * kWaveChunks] - o : 0u;
-        out[i] = make_uint2(o, b16 | (q - q0) << 16);
+        const uint32_t code8 = narrow[T];  // bit 0: staged (narrow chunks); bits 4-7: fast-tile width
+        const uint32_t b16 = (code8 & 1u) ? rec_off[(uint64_t)(T + 1) * kWaveChunks] - o : 0u;
+        out[i] = make_uint2(o, b16 | (q - q0) << 16 | (code8 >> 4) << 24);
     }
 }
 
@@ -2335,6 +2515,10 @@ const DevBuf<uint32_t>& get_tickets(mpkg_ctx_s* ctx, Executor& E, int p) {
 // level in {0, >=1}) x (column level - row level in {-1, 0, +1}), each the min / max tile its
 // columns fall in (wave_dep_tiles, the bucket spans, is reported by mpkg_plan_exec_info).
 constexpr int kWaveBuckets = 6;
+#ifndef MPKG_WAVE_SLACK_NUM
+#define MPKG_WAVE_SLACK_NUM 5
+#endif
+constexpr int64_t kWaveSlackNum = MPKG_WAVE_SLACK_NUM, kWaveSlackDen = 1;
 
 __global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci, uint32_t n,
                                const uint32_t* __restrict__ slot_row, const uint32_t* __restrict__ pos,
@@ -2358,6 +2542,8 @@ __global__ void k_wave_buckets(const uint32_t* __restrict__ rp, const uint32_t* 
         }
     }
 }
+
+uint32_t wave_stage_for(int fmt, bool sigma);
 
 void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
     cudaStream_t st = ctx->stream;
@@ -2409,20 +2595,46 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
             }
         }
         const bool sigma = E.order >= 1;
+        // affine chunks (dict format only)
+        std::vector<uint8_t> aff;
+        DevBuf<uint8_t> d_aff(std::max<uint32_t>(nc, 1));
+        E.wave_affine_chunks = 0;
+        if (E.wave_fmt == 1 && ctx->wave_affine && nc) {
+            k_wave_affine<<<grid_for((uint64_t)nc * 32, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                E.S->cols.p, E.S->vals.p, E.S->row_len.p, sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
+                A->n_rows, d_aff.p);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
+            aff.resize(nc);
+            MPKG_CUDA(cudaMemcpyAsync(aff.data(), d_aff.p, nc, cudaMemcpyDeviceToHost, st));
+            MPKG_CUDA(cudaStreamSynchronize(st));
+        }
         E.tile_bytes.assign(nt, 0);
+        const uint32_t stage_cap = wave_stage_for(E.wave_fmt, sigma);
         std::vector<uint32_t> ro(nrec + 1);
         std::vector<uint8_t> narrow(nt, 1);
+        std::vector<uint32_t> trec(nt, 0);
         uint64_t acc = 0;
         for (uint64_t c = 0; c < nrec; ++c) {
             ro[c] = (uint32_t)acc;
             const uint32_t L = c < nc ? (uint32_t)((off[c + 1] - off[c]) >> 5) : 0u;
-            const uint32_t rb = wave_rec_bytes(E.wave_fmt, sigma, L);
+            const bool is_aff = c < aff.size() && aff[c];
+            const uint32_t rb = is_aff ? wave_affine_bytes(sigma) : wave_rec_bytes(E.wave_fmt, sigma, L);
+            E.wave_affine_chunks += is_aff;
             acc += rb / 16;
             if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
             E.tile_bytes[c / kWaveChunks] += rb + 16ull * 32;
-            if (L > 8) narrow[c / kWaveChunks] = 0;
+            if (L > 8) narrow[c / kWaveChunks] &= ~1u;
+            // fast tile: all chunks affine with one width (bits 4-7; 0 = not fast)
+            uint8_t& code = narrow[c / kWaveChunks];
+            if (c % kWaveChunks == 0) code = (uint8_t)((code & 1u) | (is_aff ? L << 4 : 0u));
+            else if (!is_aff || (code >> 4) != L) code &= 1u;
+            trec[c / kWaveChunks] += rb;
         }
+        for (uint32_t T = 0; T < nt; ++T)  // records larger than a stage: not staged (nor fast)
+            if (trec[T] > stage_cap) narrow[T] = 0;
         ro[nrec] = (uint32_t)acc;
+        E.wave_rec_total = acc * 16;
         E.wrec_off.alloc(nrec + 1);
         E.wrec.alloc(std::max<uint64_t>(acc * 16, 16));
         E.wave_narrow.alloc(std::max<uint64_t>(nt, 1));
@@ -2433,11 +2645,12 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
             if (E.wave_fmt == 1)
                 k_wave_pack<1><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
                                                   sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
-                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, table.p, slot_ix.p);
+                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, table.p, slot_ix.p,
+                                                  aff.empty() ? nullptr : d_aff.p);
             else
                 k_wave_pack<0><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
                                                   sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
-                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, nullptr, nullptr);
+                                                  (uint32_t)nrec, E.wrec_off.p, E.wrec.p, nullptr, nullptr, nullptr);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2515,8 +2728,11 @@ uint64_t wave_order(const Executor& E, int q0, int q1, int64_t slack, std::vecto
 
 // Pass length p' = the longest pass whose live window fits the budget (0.6 x L2 unless the
 // l2_budget knob says otherwise; the "pass" knob forces p'); slack (ready-time units, ~p'
-// tickets each) = 2.2 x the warps / p' (each warp holds its ticket and the next one), so a
-// ticket's inputs are almost always stored when its warp reaches it.  Passes are balanced (ceil(p / p') of them).
+// tickets each) = 5 x the warps / p': a ticket runs two claims after its warp took it and its
+// producer needs a ticket's time to store, so producer and consumer sit ~5 x warps tickets apart
+// in the order and a ticket's inputs are almost always stored when its warp reaches it (C5 p = 8:
+// 2.2 x warps left 13% of the rows waiting on a producer, 9.0 ms; 5 x warps none, 6.8 ms).
+// Passes are balanced (ceil(p / p') of them).
 const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     auto it = E.wave.find(p);
     if (it != E.wave.end()) return it->second;
@@ -2525,7 +2741,7 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     const int64_t warps = (int64_t)E.wave_grid * kWaveWarps;
     auto slack_for = [&](int len) -> int64_t {
         if (ctx->slack >= 0) return std::max<int64_t>(ctx->slack, 1);
-        return std::max<int64_t>(1, (warps * 11 / 5 + len - 1) / len);
+        return std::max<int64_t>(1, (warps * kWaveSlackNum / kWaveSlackDen + len - 1) / len);
     };
     // auto: at most kWaveAutoPass powers per pass (C5, chunk records in the dict format: p' = 2..4
     // within 4%, 8 is 15% slower: the fronts' lag grows with p')
@@ -2582,7 +2798,14 @@ void* wave_fn(int kind, bool sigma, int fmt, bool trace) {
 #undef MPKG_WAVE_FNS
     return fns[fmt][trace ? 1 : 0][kind * 2 + (sigma ? 1 : 0)];
 }
-uint32_t wave_smem_for(int fmt) { return fmt == 1 ? wave_smem<1>() : wave_smem<0>(); }
+uint32_t wave_stage_for(int fmt, bool sigma) {
+    return fmt == 1 ? (sigma ? wave_stage_bytes<1, true>() : wave_stage_bytes<1, false>())
+                    : (sigma ? wave_stage_bytes<0, true>() : wave_stage_bytes<0, false>());
+}
+uint32_t wave_smem_for(int fmt, bool sigma) {
+    return fmt == 1 ? (sigma ? wave_smem<1, true>() : wave_smem<1, false>())
+                    : (sigma ? wave_smem<0, true>() : wave_smem<0, false>());
+}
 
 template <int KIND, int G>
 void launch_g(bool sigma, int grid, int threads, uint32_t smem, cudaStream_t st,
@@ -2684,7 +2907,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
         for (int k = 0; k < 4; ++k) {
             int o = 0;
             void* fn = wave_fn(k / 2, k % 2, E.wave_fmt, false);
-            const uint32_t sm = wave_smem_for(E.wave_fmt);
+            const uint32_t sm = wave_smem_for(E.wave_fmt, k % 2 != 0);
             MPKG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             MPKG_CUDA(cudaFuncSetAttribute(wave_fn(k / 2, k % 2, E.wave_fmt, true),
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -3047,7 +3270,7 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(g);
             cfg.blockDim = dim3(kWaveThreads);
-            cfg.dynamicSmemBytes = wave_smem_for(E.wave_fmt);
+            cfg.dynamicSmemBytes = wave_smem_for(E.wave_fmt, sigma);
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeCooperative;
@@ -3132,6 +3355,15 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
     if (n_tickets) *n_tickets = k;
     if (n_deps) *n_deps = d;
     if (pass_powers) *pass_powers = pp;
+}
+
+void exec_wave(const mpkg_plan_s* P, int* format, uint64_t* n_chunks, uint64_t* n_affine, uint64_t* record_bytes) {
+    const Executor* E = P->exec.get();
+    const bool w = E && E->wrec.p != nullptr;
+    if (format) *format = w ? E->wave_fmt : 0;
+    if (n_chunks) *n_chunks = w ? (uint64_t)E->n_tiles * kWaveChunks : 0;
+    if (n_affine) *n_affine = w ? E->wave_affine_chunks : 0;
+    if (record_bytes) *record_bytes = w ? E->wave_rec_total : 0;
 }
 
 void exec_trace(const mpkg_plan_s* P, uint64_t* out, uint64_t cap, uint64_t* n, uint32_t* tile_rows) {

@@ -170,12 +170,14 @@ def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
 
 
 DEFAULT_KNOBS = {"order": -1, "slack": -1, "schedule": 0, "kernel": 0, "tile_rows": 128,
-                 "producers": 0, "cgroups": 0, "stages": 0, "pass": 0, "l2_budget": 0, "ctas_per_sm": 0}
+                 "producers": 0, "cgroups": 0, "stages": 0, "pass": 0, "l2_budget": 0, "ctas_per_sm": 0,
+                 "wave_dict": 1, "wave_affine": 1}
 
 SCHEDULES = {
     "sweeps": {"schedule": 2},
     "wave": {"schedule": 3},
     "wave-plain": {"schedule": 3, "wave_dict": 0},
+    "wave-noaffine": {"schedule": 3, "wave_affine": 0},
     "wave-1cta": {"schedule": 3, "ctas_per_sm": 1},
     "wave-pass1": {"schedule": 3, "pass": 1},
     "wave-pass2-slack1": {"schedule": 3, "pass": 2, "slack": 1},
@@ -598,6 +600,49 @@ def test_config1_full_size_bitwise(ctx, oracle):
     plan = ctx.group_levels(ls, Ap, 100 << 20, 4)
     ref = oracle.baseline_mpk(prp, pci, pv, x, 4)
     assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref)
+
+
+@pytest.mark.parametrize("knobs", [{}, {"pass": 2, "slack": 1}, {"pass": 8}, {"order": 1}, {"wave_affine": 0}])
+def test_wave_affine_records(ctx, oracle, knobs):
+    """Affine chunk records (32 full rows whose entry k is column base_k + lane with one value:
+    the interior of a level-ordered stencil) hold the same entries in the same stored order as the
+    general records: bitwise equal powers, Newton basis and polynomial, with most chunks of a
+    72^3 7-point Laplacian stored that way; Inf / NaN / the sentinel pattern in x flow through."""
+    A = mpkg.poisson3d(72, 72, 72)
+    dA = ctx.csr(A)
+    ls = ctx.build_levels(dA)
+    Ap = ctx.permute(dA, ls)
+    P = Ap.download()
+    x = mpkg.random_vector(A.n_rows, 11)
+    try:
+        set_knobs(ctx, {"schedule": 3, **knobs})
+        plan = ctx.group_levels(ls, Ap, 1 << 20, 8)
+        got = ctx.mpk(plan, Ap, x, 8).as_matrix()
+        info = plan.exec_info()
+        assert info["schedule"] == "wave" and info["wave_format"] == 1
+        if knobs.get("wave_affine", 1) and not knobs.get("order", 0):
+            assert info["wave_affine_chunks"] > 0.25 * info["wave_chunks"], info
+        elif not knobs.get("wave_affine", 1):
+            assert info["wave_affine_chunks"] == 0
+        ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 8)
+        assert_bitwise(got, ref, f"affine {knobs}")
+        sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0, 3.0, 0.25]
+        ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+        assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, "affine shifted")
+        coef = np.linspace(-1, 1, 9)
+        zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+        assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, "affine poly")
+        xs = x.copy()
+        xs[1234] = np.inf
+        xs[200000] = np.nan
+        xs[300000:300001].view(np.uint64)[0] = np.uint64(0x7FF4DEAD5EED0001)
+        got = ctx.mpk(plan, Ap, xs, 5).as_matrix()
+        ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, xs, 5)
+        assert np.array_equal(np.isnan(got), np.isnan(ref))
+        ok = ~np.isnan(ref)
+        assert_bitwise(got[ok], ref[ok], "affine special values")
+    finally:
+        set_knobs(ctx, {})
 
 
 @pytest.mark.parametrize("dict_fmt", [1, 0])
