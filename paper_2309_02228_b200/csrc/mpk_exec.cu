@@ -1184,46 +1184,15 @@ __device__ __forceinline__ double wave_row_slow(const char* body, uint32_t L, ui
     return acc;
 }
 
-// A staged row whose gathers met empty values: re-read just those (relaxed L2 loads, all in flight,
-// then one by one until stored) and sum again from the stage, in stored order.
-template <int F>
-__device__ __forceinline__ double wave_redo(const char* body, uint32_t L, uint32_t lane, uint32_t len,
-                                            const double* src, double (&x)[8], const double* dict, uint32_t* dbg) {
-    if (dbg) atomicAdd(dbg, 1u);
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(body);
-    const uint32_t Lp = L & ~1u;
-    uint32_t e[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        e[k] = (uint32_t)k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1) : Lp * 32u + lane;
-        if ((uint32_t)k < len && wave_empty(x[k])) x[k] = ld_strong_again(src + sc[e[k]]);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        while ((uint32_t)k < len && wave_empty(x[k])) {
-            __nanosleep(32);
-            x[k] = ld_strong_again(src + sc[e[k]]);
-        }
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if ((uint32_t)k < L) {
-            double v;
-            if constexpr (F == 0) v = reinterpret_cast<const double*>(body + 128u * L)[e[k]];
-            else v = dict[reinterpret_cast<const uint8_t*>(body + 128u * L)[lane * 8u + k]];
-            acc = __dadd_rn(acc, __dmul_rn(v, x[k]));
-        }
-    return acc;
-}
-
 // Hot path: a staged chunk of compile-time width L, one row per lane, summed in stored order.  A
 // lane's padding entries (len <= k < L, value 0.0) gather nothing and add 0.0 * 0.0 = +0, which
 // leaves the sum unchanged (it starts at +0 and round-to-nearest never makes it -0): rowdot.cuh's
-// sum over k < len, bit for bit.  x[k] (k < L) is returned for the empty-value check.
+// sum over k < len, bit for bit.
 template <int L, int F>
 __device__ __forceinline__ double wave_dot(const char* body, uint32_t lane, uint32_t len, const double* src,
-                                           const double* dict, double (&x)[8]) {
+                                           const double* dict) {
     constexpr int Lp = L & ~1;
+    double x[8];
     const uint32_t* sc = reinterpret_cast<const uint32_t*>(body);
 #pragma unroll
     for (int j = 0; j < Lp; j += 2) {
@@ -1456,7 +1425,7 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
-        const double* src_lane = src + lane;
+        const double* src_lane = opaque_ptr(src + lane);  // opaque: one IMAD.WIDE per affine gather
         const char* rec = stage;
         double tr_acc[TRACE ? kWaveChunks : 1];
         uint32_t tr_off[TRACE ? kWaveChunks : 1];
@@ -1518,28 +1487,24 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                 rr = SIGMA ? R::slot(rec, lane) : s;
                 len = rr < P.n_rows ? R::len(rec, lane) : 0u;
                 const char* body = rec + R::hdr;
-                double x[8];
                 // 7 tested first: the 3D 7-point stencil is the schedule's main customer
-                if (__builtin_expect(L == 7, 1)) acc = wave_dot<7, F>(body, lane, len, src, dict, x);
+                if (__builtin_expect(L == 7, 1)) acc = wave_dot<7, F>(body, lane, len, src, dict);
                 else switch (L) {
                     case 0: break;
-                    case 1: acc = wave_dot<1, F>(body, lane, len, src, dict, x); break;
-                    case 2: acc = wave_dot<2, F>(body, lane, len, src, dict, x); break;
-                    case 3: acc = wave_dot<3, F>(body, lane, len, src, dict, x); break;
-                    case 4: acc = wave_dot<4, F>(body, lane, len, src, dict, x); break;
-                    case 5: acc = wave_dot<5, F>(body, lane, len, src, dict, x); break;
-                    case 6: acc = wave_dot<6, F>(body, lane, len, src, dict, x); break;
+                    case 1: acc = wave_dot<1, F>(body, lane, len, src, dict); break;
+                    case 2: acc = wave_dot<2, F>(body, lane, len, src, dict); break;
+                    case 3: acc = wave_dot<3, F>(body, lane, len, src, dict); break;
+                    case 4: acc = wave_dot<4, F>(body, lane, len, src, dict); break;
+                    case 5: acc = wave_dot<5, F>(body, lane, len, src, dict); break;
+                    case 6: acc = wave_dot<6, F>(body, lane, len, src, dict); break;
                     case 7: break;
-                    default: acc = wave_dot<8, F>(body, lane, len, src, dict, x); break;
+                    default: acc = wave_dot<8, F>(body, lane, len, src, dict); break;
                 }
-                // An empty (signalling-NaN) value makes the sum NaN: only then look at the values
-                // (slice q0-1 is complete and may hold any bit pattern: never checked).
-                if (L != 0 && q != q0 && is_nan_bits(acc)) {
-                    bool miss = false;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) miss |= wave_empty(x[j]);
-                    if (miss) acc = wave_redo<F>(body, L, lane, len, src, x, dict, P.dbg);
-                }
+                // An empty (signalling-NaN) value makes the sum NaN: the row again with every input
+                // awaited (slice q0-1 is complete and may hold any bit pattern: never checked).  A
+                // NaN in the data takes the same detour and gets the same sum.
+                if (L != 0 && q != q0 && is_nan_bits(acc))
+                    acc = wave_row_slow<F>(body, L, lane, len, src, false, dict, P.dbg, false);
             } else {  // a tile with a wide chunk: its records from global memory
                 const char* h = P.wrec + (uint64_t)d.x * 16u + (uint64_t)(rec - stage);
                 const uint4 inf = R::info4(h);
