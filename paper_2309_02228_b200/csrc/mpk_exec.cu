@@ -1224,6 +1224,44 @@ __device__ __forceinline__ double wave_dot(const char* body, uint32_t lane, uint
     return acc;
 }
 
+// Shared-memory loads by 32-bit shared address (the fast-tile path forms no generic pointer into
+// the stage); volatile so they stay behind the stage's mbarrier wait.
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 r;
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+template <int L>
+__device__ __forceinline__ void affine_gather_s(uint32_t body, const double* src_lane, double (&x)[L]) {
+    const uint4 b0 = lds_v4(body);
+    uint4 b1 = make_uint4(0u, 0u, 0u, 0u);
+    if (L > 4) b1 = lds_v4(body + 16u);
+    const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int j = 0; j < L; ++j) x[j] = ld_gather(src_lane + b[j]);
+}
+template <int L>
+__device__ __forceinline__ double affine_sum_s(uint32_t body, const double (&x)[L]) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; j += 2) {
+        const double2 vv = lds_d2(body + 32u + 8u * j);
+        acc = __dadd_rn(acc, __dmul_rn(vv.x, x[j]));
+        if (j + 1 < L) acc = __dadd_rn(acc, __dmul_rn(vv.y, x[j + 1]));
+    }
+    return acc;
+}
+
 // An affine chunk (see the record formats): entry k of lane's row is column base[k] + lane with
 // value v[k]; every row is full, so there are no length predicates and no padding.  src_lane =
 // src + lane.  The same products in the same stored order as wave_dot.  Gathers and sum are
@@ -1339,7 +1377,8 @@ __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint
 
 // Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units, the tile's first
 // chunk record; its records are contiguous), y = the bytes to stage / 16 (0: a chunk wider than 8
-// entries, nothing staged but the first header) | (q - q0) << 16 | fast-tile width << 24.  The tile index and the chunk
+// entries, nothing staged but the first header) | (q - q0) << 16 | fast-tile width << 24 |
+// pair tile << 28.  The tile index and the chunk
 // widths travel in the record headers.
 __device__ __forceinline__ uint2 ld_desc(const uint2* p) {
     uint2 r;
@@ -1372,7 +1411,8 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
     const uint32_t sid = gw % kWaveStreams;
     uint32_t* const ctr = P.counter + sid * 32u;  // one 128-B line per stream
     char* const ring = wsm + wib * 2u * SB;
-    const uint32_t ring_s = smem_u32(ring), bar0 = smem_u32(&bars[wib][0]);
+    uint32_t ring_s = smem_u32(ring), bar0 = smem_u32(&bars[wib][0]);
+    asm volatile("" : "+r"(ring_s), "+r"(bar0));  // opaque: kept in registers, not re-derived per ticket
     if constexpr (F == 1) {
         for (uint32_t i = threadIdx.x; i < P.n_dict; i += blockDim.x) sdict[i] = P.dict[i];
         __syncthreads();
@@ -1389,7 +1429,9 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         if (lane == 0) k = atomicAdd(ctr, 1u);
         return k;
     };
-    auto ticket = [&](uint32_t k) { return t0 + sid + kWaveStreams * __shfl_sync(0xffffffffu, k, 0); };
+    uint32_t tbase = t0 + sid;
+    asm volatile("" : "+r"(tbase));  // opaque, as above
+    auto ticket = [&](uint32_t k) { return tbase + kWaveStreams * __shfl_sync(0xffffffffu, k, 0); };
     uint32_t t = ticket(claim());
     uint32_t tn = ticket(claim());
     uint2 d = t < t1 ? ld_desc(P.wdesc + t) : make_uint2(0u, 0u);
@@ -1399,8 +1441,9 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         if (t < t1) wave_stage<F, SIGMA>(P, d, q0, q1, ring_s, bar0);
         if (tn < t1) wave_stage<F, SIGMA>(P, dn, q0, q1, ring_s + SB, bar0 + 8u);
     }
-    uint32_t st = 0, phase = 0;  // phase: bit i = parity of stage i's next completion
+    uint32_t it = 0;  // tickets done: stage it & 1, whose completions alternate parity (it >> 1) & 1
     while (t < t1) {
+        const uint32_t st = it & 1u;
         const uint32_t tnn = ticket(kc);
         uint2 dnn = make_uint2(0u, 0u);
         if (tnn < t1) {
@@ -1408,7 +1451,7 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
             kc = claim();
         }
         {  // wait for this ticket's stage
-            const uint32_t bar = bar0 + 8u * st, par = (phase >> st) & 1u;
+            const uint32_t bar = bar0 + 8u * st, par = (it >> 1) & 1u;
             uint32_t done = 0;
             while (!done)
                 asm volatile(
@@ -1416,17 +1459,14 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                     : "=r"(done)
                     : "r"(bar), "r"(par)
                     : "memory");
-            phase ^= 1u << st;
         }
-        const char* stage = ring + st * SB;
+        const uint32_t stage_s = ring_s + st * SB;
         const uint32_t q = q0 + ((d.y >> 16) & 15u);
-        const bool staged = (d.y & 0xffffu) != 0;
-        const uint32_t T = R::tile_l(stage).x;
+        const uint32_t T = lds_u32(stage_s + R::info);
         // opaque: every gather is then one IMAD.WIDE off this base (otherwise the compiler folds
         // (q-1) * vstride into each gather's index arithmetic)
         const double* src = opaque_ptr(P.V + (uint64_t)(q - 1) * P.vstride);
         const double* src_lane = opaque_ptr(src + lane);  // opaque: one IMAD.WIDE per affine gather
-        const char* rec = stage;
         double tr_acc[TRACE ? kWaveChunks : 1];
         uint32_t tr_off[TRACE ? kWaveChunks : 1];
         if (F == 1 && !TRACE && ((d.y >> 24) & 15u) == 7u) {
@@ -1436,25 +1476,48 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
             double* const dst = P.V + (uint64_t)q * P.vstride;
 #pragma unroll
             for (uint32_t c = 0; c < kWaveChunks; c += 2) {
-                const char* ba = stage + c * R::affine_bytes + R::hdr;
-                const char* bb = ba + R::affine_bytes;
+                const uint32_t sa = stage_s + c * R::affine_bytes + R::hdr, sb = sa + R::affine_bytes;
                 const uint32_t s = T * kWaveRows + c * 32u + lane;
                 double xa[7], xb[7];
-                affine_gather<7>(ba, src_lane, xa);
-                affine_gather<7>(bb, src_lane, xb);
-                double a0 = affine_sum<7>(ba, xa);
-                double a1 = affine_sum<7>(bb, xb);
-                if (q != q0) {
+                double a0, a1;
+                if (d.y & (1u << 28)) {  // pair tile: chunk b = chunk a 32 rows down the same diagonals
+                    const uint4 b0 = lds_v4(sa), b1 = lds_v4(sa + 16u);
+                    const uint32_t b[7] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z};
+                    const double* src_lane32 = src_lane + 32;
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) xa[j] = ld_gather(src_lane + b[j]);
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) xb[j] = ld_gather(src_lane32 + b[j]);
+                    a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 7; j += 2) {
+                        const double2 vv = lds_d2(sa + 32u + 8u * j);
+                        a0 = __dadd_rn(a0, __dmul_rn(vv.x, xa[j]));
+                        a1 = __dadd_rn(a1, __dmul_rn(vv.x, xb[j]));
+                        if (j + 1 < 7) {
+                            a0 = __dadd_rn(a0, __dmul_rn(vv.y, xa[j + 1]));
+                            a1 = __dadd_rn(a1, __dmul_rn(vv.y, xb[j + 1]));
+                        }
+                    }
+                } else {
+                    affine_gather_s<7>(sa, src_lane, xa);
+                    affine_gather_s<7>(sb, src_lane, xb);
+                    a0 = affine_sum_s<7>(sa, xa);
+                    a1 = affine_sum_s<7>(sb, xb);
+                }
+                if (q != q0 && (is_nan_bits(a0) || is_nan_bits(a1))) {
+                    const char* ba = ring + st * SB + c * R::affine_bytes + R::hdr;
                     if (is_nan_bits(a0)) a0 = wave_redo_affine(ba, 7u, src_lane, P.dbg);
-                    if (is_nan_bits(a1)) a1 = wave_redo_affine(bb, 7u, src_lane, P.dbg);
+                    if (is_nan_bits(a1)) a1 = wave_redo_affine(ba + R::affine_bytes, 7u, src_lane, P.dbg);
                 }
                 if constexpr (KIND == 0 && !SIGMA) {
                     st_strong(dst + s, a0);
                     st_strong(dst + s + 32u, a1);
                 } else {
-                    wave_epilogue<KIND, SIGMA>(P, s, SIGMA ? R::slot(ba - R::hdr, lane) : s, q, q0, src, a0);
-                    wave_epilogue<KIND, SIGMA>(P, s + 32u, SIGMA ? R::slot(bb - R::hdr, lane) : s + 32u, q, q0, src,
-                                               a1);
+                    const char* ra = ring + st * SB + c * R::affine_bytes;
+                    wave_epilogue<KIND, SIGMA>(P, s, SIGMA ? R::slot(ra, lane) : s, q, q0, src, a0);
+                    wave_epilogue<KIND, SIGMA>(P, s + 32u, SIGMA ? R::slot(ra + R::affine_bytes, lane) : s + 32u, q,
+                                               q0, src, a1);
                 }
                 if (q == q1) {
                     const double e = __longlong_as_double((long long)kWaveEmpty);
@@ -1465,6 +1528,9 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                 }
             }
         } else {
+        const char* stage = ring + st * SB;
+        const bool staged = (d.y & 0xffffu) != 0;
+        const char* rec = stage;
 #pragma unroll 1
         for (uint32_t c = 0; c < kWaveChunks; ++c) {
             if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
@@ -1548,7 +1614,7 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         __syncwarp();  // every lane is done with the stage: refill it with ticket tnn
         if (lane == 0 && tnn < t1) wave_stage<F, SIGMA>(P, dnn, q0, q1, ring_s + st * SB, bar0 + 8u * st);
         t = tn, d = dn, tn = tnn, dn = dnn;
-        st ^= 1u;
+        ++it;
     }
 }
 
@@ -1686,9 +1752,34 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
     }
 }
 
+// Pair tiles (setup, after k_wave_pack): a fast tile whose odd chunks are their even predecessors
+// 32 rows further down the same diagonals (bases + 32, the same values) gets bit 1 of its tile
+// code: the engine then reads one record per chunk pair.  One thread per tile.
+__global__ void k_wave_pairs(const char* __restrict__ rec, const uint32_t* __restrict__ rec_off, uint32_t n_tiles,
+                             uint32_t hdr, uint8_t* __restrict__ code) {
+    for (uint64_t T = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; T < n_tiles;
+         T += (uint64_t)gridDim.x * blockDim.x) {
+        if ((code[T] >> 4) == 0) continue;  // not a fast tile
+        bool ok = true;
+        for (uint32_t c = 0; c < kWaveChunks && ok; c += 2) {
+            const char* a = rec + (uint64_t)rec_off[T * kWaveChunks + c] * 16u + hdr;
+            const char* b = rec + (uint64_t)rec_off[T * kWaveChunks + c + 1] * 16u + hdr;
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t ba = reinterpret_cast<const uint32_t*>(a)[k], bb = reinterpret_cast<const uint32_t*>(b)[k];
+                const unsigned long long va = reinterpret_cast<const unsigned long long*>(a + 32)[k];
+                const unsigned long long vb = reinterpret_cast<const unsigned long long*>(b + 32)[k];
+                const bool used = (uint32_t)k < (uint32_t)(code[T] >> 4);
+                ok = ok && va == vb && (used ? bb == ba + 32u : bb == ba);
+            }
+        }
+        if (ok) code[T] |= 2u;
+    }
+}
+
 // Descriptors of a pass's tickets from the host codes (T | q << 24, kLastUse ignored: the last use
 // is q == q1); narrow[T] bit 0: every chunk of the tile is at most 8 entries wide (staged), bits
-// 4-7: the width of a fast tile (all chunks affine records of that width), 0 otherwise.
+// 4-7: the width of a fast tile (all chunks affine records of that width), 0 otherwise, bit 1:
+// a pair tile (k_wave_pairs).
 __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
                             const uint8_t* __restrict__ narrow, uint32_t q0, uint2* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -1697,7 +1788,7 @@ __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, cons
         const uint32_t o = rec_off[(uint64_t)T * kWaveChunks];
         const uint32_t code8 = narrow[T];  // bit 0: staged (narrow chunks); bits 4-7: fast-tile width
         const uint32_t b16 = (code8 & 1u) ? rec_off[(uint64_t)(T + 1) * kWaveChunks] - o : 0u;
-        out[i] = make_uint2(o, b16 | (q - q0) << 16 | (code8 >> 4) << 24);
+        out[i] = make_uint2(o, b16 | (q - q0) << 16 | (code8 >> 4) << 24 | ((code8 >> 1) & 1u) << 28);
     }
 }
 
@@ -2616,6 +2707,12 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
                 k_wave_pack<0><<<g, 256, 0, st>>>(E.S->cols.p, E.S->vals.p, E.S->row_len.p,
                                                   sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
                                                   (uint32_t)nrec, E.wrec_off.p, E.wrec.p, nullptr, nullptr, nullptr);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        if (nt && !aff.empty()) {
+            k_wave_pairs<<<grid_for(nt, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                E.wrec.p, E.wrec_off.p, nt, sigma ? WaveRec<1, true>::hdr : WaveRec<1, false>::hdr, E.wave_narrow.p);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
