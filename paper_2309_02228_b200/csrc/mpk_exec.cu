@@ -1378,7 +1378,7 @@ __device__ __forceinline__ void bulk_g2s_cta(uint32_t dst, const void* src, uint
 // Ticket descriptor (k_wave_desc): x = rec_off[kWaveChunks T] (16-byte units, the tile's first
 // chunk record; its records are contiguous), y = the bytes to stage / 16 (0: a chunk wider than 8
 // entries, nothing staged but the first header) | (q - q0) << 16 | fast-tile width << 24 |
-// pair tile << 28.  The tile index and the chunk
+// pair tile << 28 | the tile's last power in the pass << 29 (its records are then evict_first).  The tile index and the chunk
 // widths travel in the record headers.
 __device__ __forceinline__ uint2 ld_desc(const uint2* p) {
     uint2 r;
@@ -1393,8 +1393,7 @@ __device__ __forceinline__ void wave_stage(const FusedParams& P, uint2 d, uint32
     const uint32_t b16 = d.y & 0xffffu;
     const uint32_t bytes = b16 ? b16 * 16u : WaveRec<F, SIGMA>::hdr;
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar,
-                 q0 + ((d.y >> 16) & 15u) == q1 ? P.pol_first : P.pol_last);
+    bulk_g2s_cta(stage, P.wrec + (uint64_t)d.x * 16u, bytes, bar, (d.y & (1u << 29)) ? P.pol_first : P.pol_last);
 }
 
 template <int KIND, bool SIGMA, int F, bool TRACE>
@@ -1544,7 +1543,13 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                 rr = SIGMA ? R::slot(rec, lane) : s;
                 len = L;
                 const char* body = rec + R::hdr;
-                acc = wave_dot_affine_any(body, L, src_lane);
+                if (L == 7) {
+                    double x7[7];
+                    affine_gather<7>(body, src_lane, x7);
+                    acc = affine_sum<7>(body, x7);
+                } else {
+                    acc = wave_dot_affine_any(body, L, src_lane);
+                }
                 if (q != q0 && is_nan_bits(acc)) acc = wave_redo_affine(body, L, src_lane, P.dbg);
             } else if (staged) {  // the record in shared memory (every load below is an LDS)
                 const uint4 inf = R::info4(rec);
@@ -1781,14 +1786,15 @@ __global__ void k_wave_pairs(const char* __restrict__ rec, const uint32_t* __res
 // 4-7: the width of a fast tile (all chunks affine records of that width), 0 otherwise, bit 1:
 // a pair tile (k_wave_pairs).
 __global__ void k_wave_desc(const uint32_t* __restrict__ codes, uint64_t n, const uint32_t* __restrict__ rec_off,
-                            const uint8_t* __restrict__ narrow, uint32_t q0, uint2* __restrict__ out) {
+                            const uint8_t* __restrict__ narrow, uint32_t q0, uint32_t q1, uint2* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t code = codes[i];
         const uint32_t T = code & 0xffffffu, q = (code >> 24) & 63u;
         const uint32_t o = rec_off[(uint64_t)T * kWaveChunks];
         const uint32_t code8 = narrow[T];  // bit 0: staged (narrow chunks); bits 4-7: fast-tile width
         const uint32_t b16 = (code8 & 1u) ? rec_off[(uint64_t)(T + 1) * kWaveChunks] - o : 0u;
-        out[i] = make_uint2(o, b16 | (q - q0) << 16 | (code8 >> 4) << 24 | ((code8 >> 1) & 1u) << 28);
+        out[i] = make_uint2(o, b16 | (q - q0) << 16 | (code8 >> 4) << 24 | ((code8 >> 1) & 1u) << 28 |
+                                   (q == q1 ? 1u << 29 : 0u));
     }
 }
 
@@ -2823,7 +2829,9 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     int q0 = 1;
     W.t_begin.push_back(0);
     for (int j = 0; j < n_pass; ++j) {
-        const int len = p / n_pass + (j < p % n_pass ? 1 : 0);
+        // the shorter passes first: the first pass's in-pass slices are the ones k_wave_fill has to
+        // empty (every later pass's are emptied by the pass before it)
+        const int len = p / n_pass + (j >= n_pass - p % n_pass ? 1 : 0);
         W.slack = slack_for(len);
         wave_order(E, q0, q0 + len - 1, W.slack, &codes);
         W.q_begin.push_back(q0);
@@ -2841,7 +2849,8 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
         const uint64_t b = W.t_begin[j], e = W.t_begin[j + 1];
         if (e > b) {
             k_wave_desc<<<grid_for(e - b, 256, (unsigned)ctx->sm_count * 8u), 256, 0, ctx->stream>>>(
-                W.tickets.p + b, e - b, E.wrec_off.p, E.wave_narrow.p, (uint32_t)W.q_begin[j], W.desc.p + b);
+                W.tickets.p + b, e - b, E.wrec_off.p, E.wave_narrow.p, (uint32_t)W.q_begin[j],
+                (uint32_t)W.q_begin[j + 1] - 1u, W.desc.p + b);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
