@@ -188,9 +188,10 @@ int mpkg_plan_exec_info(mpkg_plan_t P, uint32_t* n_tiles, uint64_t* n_tickets,
 int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
 /* The wave schedule's private matrix copy (chunk records of 32 rows): record format (0 plain, 1
  * value dictionary), chunks, chunks stored as affine records (diagonal pieces: 8 column bases and 8
- * values for the whole chunk), and the bytes of all records.  Zeros when the plan has no wave. */
+ * values for the whole chunk), chunks stored as banded records (rows that are sub-sequences of two
+ * such templates), and the bytes of all records.  Zeros when the plan has no wave. */
 int mpkg_plan_exec_wave(mpkg_plan_t P, int* format, uint64_t* n_chunks, uint64_t* n_affine,
-                        uint64_t* record_bytes);
+                        uint64_t* n_banded, uint64_t* record_bytes);
 /* Schedule audit (ctx knob "trace" = 1): after an mpkg_mpk* on the fused or wave schedule, the
  * 2 * n_tiles * (p+1) globaltimer stamps of the last call, [2 (q n_tiles + T)] = tile T's inputs for
  * power q complete, [.. + 1] = its results about to be stored / published; out may be NULL to

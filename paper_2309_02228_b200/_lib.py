@@ -59,7 +59,7 @@ _SIGS = {
     "mpkg_plan_destroy": [P],
     "mpkg_plan_exec_info": [P, pu32, pu64, pu64, pu32],
     "mpkg_plan_exec_mode": [P, pint, pint, pint, pu64],
-    "mpkg_plan_exec_wave": [P, pint, pu64, pu64, pu64],
+    "mpkg_plan_exec_wave": [P, pint, pu64, pu64, pu64, pu64],
     "mpkg_plan_exec_trace": [P, P, u64, pu64, pu32],
     "mpkg_jacobi_setup": [P, P, i32, C.POINTER(P)],
     "mpkg_jacobi_info": [P, pu32, pint],

@@ -377,13 +377,14 @@ class ExecutionPlan:
         check(lib.mpkg_plan_exec_info(self.h, C.byref(t), C.byref(k), C.byref(d), C.byref(pp)))
         o, sw, kn, lr = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
         check(lib.mpkg_plan_exec_mode(self.h, C.byref(o), C.byref(sw), C.byref(kn), C.byref(lr)))
-        wf, wc, wa, wb = C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_uint64()
-        check(lib.mpkg_plan_exec_wave(self.h, C.byref(wf), C.byref(wc), C.byref(wa), C.byref(wb)))
+        wf, wc, wa, wn, wb = C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib.mpkg_plan_exec_wave(self.h, C.byref(wf), C.byref(wc), C.byref(wa), C.byref(wn), C.byref(wb)))
         return {"tiles": t.value, "tickets": k.value, "dep_tiles": d.value,
                 "pass_powers": pp.value, "order": o.value,
                 "schedule": {1: "sweeps", 2: "wave"}.get(sw.value, "fused"), "kernel": kn.value,
                 "long_rows": lr.value, "wave_format": wf.value, "wave_chunks": wc.value,
-                "wave_affine_chunks": wa.value, "wave_record_bytes": wb.value}
+                "wave_affine_chunks": wa.value, "wave_banded_chunks": wn.value,
+                "wave_record_bytes": wb.value}
 
     def exec_trace(self):
         """ctx knob "trace": (flat stamps, tile_rows) of the last fused / wave MPK on this plan

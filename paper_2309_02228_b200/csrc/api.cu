@@ -332,8 +332,10 @@ int mpkg_ctx_set_param(mpkg_ctx_t ctx, const char* key, int64_t value) {
             ctx->trace = value != 0;
         else if (k == "wave_dict")
             ctx->wave_dict = value != 0;
-        else if (k == "wave_affine")
-            ctx->wave_affine = value != 0;
+        else if (k == "wave_affine") {
+            require(value >= 0 && value <= 2, "ctx_set_param: wave_affine must be 0 (off), 1 (affine) or 2 (affine + banded)");
+            ctx->wave_affine = value;
+        }
         else if (k == "pdl")
             ctx->pdl = value != 0;
         else if (k == "schedule") {
@@ -832,10 +834,10 @@ int mpkg_plan_exec_mode(mpkg_plan_t P, int* order, int* sweeps, int* kernel, uin
 }
 
 int mpkg_plan_exec_wave(mpkg_plan_t P, int* format, uint64_t* n_chunks, uint64_t* n_affine,
-                        uint64_t* record_bytes) {
+                        uint64_t* n_banded, uint64_t* record_bytes) {
     return guarded([&] {
         require(P != nullptr, "plan_exec_wave: null plan");
-        exec_wave(P, format, n_chunks, n_affine, record_bytes);
+        exec_wave(P, format, n_chunks, n_affine, n_banded, record_bytes);
     });
 }
 

@@ -113,7 +113,8 @@ struct mpkg_ctx_s {
     int64_t coop_min = 0;       // fast mode: rows longer than this run warp-cooperatively (0 = 128)
     int64_t coop_variant = 0;   // k_coop_rows: bit 0 = 16 gathers in flight, bit 1 = L2-only gathers
     int64_t wave_dict = 1;    // wave: value-dictionary chunk records when the matrix allows (0: plain)
-    int64_t wave_affine = 1;  // wave: affine records for diagonal-piece chunks (dict format; 0: off)
+    int64_t wave_affine = 2;  // wave, dict format: 1 affine records for diagonal-piece chunks, 2 also banded
+                              // records where the diagonals break (0: neither)
     int64_t schedule = 0;     // 0 auto, 1 fused kernel, 2 one launch per power, 3 wave (mpk_exec.cu)
     bool trace = false;       // record per-(tile, power) globaltimer stamps (mpkg_plan_exec_trace)
     int64_t producers = 0;    // async kernel: producer warps per CTA (0: 4)
@@ -314,7 +315,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A, const FusedArgs& 
 void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uint64_t* n_deps,
                uint32_t* pass_powers);
 void exec_mode(const mpkg_plan_s* P, int* order, int* sweeps, int* kernel, uint64_t* long_rows);
-void exec_wave(const mpkg_plan_s* P, int* format, uint64_t* n_chunks, uint64_t* n_affine, uint64_t* record_bytes);
+void exec_wave(const mpkg_plan_s* P, int* format, uint64_t* n_chunks, uint64_t* n_affine, uint64_t* n_banded,
+               uint64_t* record_bytes);
 void exec_trace(const mpkg_plan_s* P, uint64_t* out, uint64_t cap, uint64_t* n, uint32_t* tile_rows);
 
 // ortho.cu: block orthogonalisation (reference ortho.hpp)

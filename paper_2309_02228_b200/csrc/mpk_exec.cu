@@ -134,6 +134,7 @@ struct Executor {
     DevBuf<double> wave_dict;                 // the distinct values (wave_fmt 1)
     uint32_t n_dict = 0;
     uint64_t wave_affine_chunks = 0;          // chunks stored as affine records
+    uint64_t wave_banded_chunks = 0;          // chunks stored as banded records
     uint64_t wave_rec_total = 0;              // bytes of all chunk records
     uint64_t wave_pol[2] = {0, 0};            // createpolicy evict_first / evict_last values
     DevBuf<unsigned long long> trace;         // "trace" knob (FusedParams::trace)
@@ -1085,6 +1086,14 @@ __device__ __forceinline__ double wave_wait(const double* p, double v) {
 // wave_affine).
 // rec_off[T] is the record's offset in 16-byte units.
 constexpr uint32_t kWaveAffine = 1u;
+// A dict-format chunk of width <= 8 whose rows are not all alike, but each a sub-sequence of one of
+// at most TWO row templates (entry k: column base[t][k] + lane, value v[t][k]) is stored as a BANDED
+// record (info.w = kWaveBanded): the chunks where a level-ordered stencil's diagonals break (a run
+// of grid points ends, boundary rows miss a neighbour).
+//   len[32] u8 | info | slot_row[32] u32 (private order only) | meta[32] u16 | base[2][8] u32 | v[2][8] f64
+// meta = the lane's template (bit 8) and which of its 8 entries the row has (bits 0-7), in stored
+// order: 304 bytes instead of 1,200 (k_wave_affine decides, k_wave_pack fills).
+constexpr uint32_t kWaveBanded = 2u;
 constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
 constexpr int kWaveAutoPass = 3;
@@ -1101,6 +1110,7 @@ struct WaveRec {
     }
     static constexpr uint32_t max_staged = bytes(8);
     static constexpr uint32_t affine_bytes = hdr + 96u;
+    static constexpr uint32_t banded_bytes = hdr + 256u;
     __device__ static uint32_t len(const char* r, uint32_t lane) {
         if constexpr (F == 0) return reinterpret_cast<const uint32_t*>(r)[lane];
         else return reinterpret_cast<const uint8_t*>(r)[lane];
@@ -1113,6 +1123,9 @@ struct WaveRec {
 };
 __host__ __device__ constexpr uint32_t wave_affine_bytes(bool sigma) {
     return sigma ? WaveRec<1, true>::affine_bytes : WaveRec<1, false>::affine_bytes;
+}
+__host__ __device__ constexpr uint32_t wave_banded_bytes(bool sigma) {
+    return sigma ? WaveRec<1, true>::banded_bytes : WaveRec<1, false>::banded_bytes;
 }
 __host__ __device__ constexpr uint32_t wave_rec_bytes(int F, bool sigma, uint32_t L) {
     return F == 0 ? (sigma ? WaveRec<0, true>::bytes(L) : WaveRec<0, false>::bytes(L))
@@ -1315,6 +1328,50 @@ __device__ __forceinline__ double wave_redo_affine(const char* body, uint32_t L,
         while (wave_empty(x)) {
             __nanosleep(32);
             x = ld_strong_again(p);
+        }
+        acc = __dadd_rn(acc, __dmul_rn(v[k], x));
+    }
+    return acc;
+}
+
+// A banded chunk (see the record formats).  The row's entries are the template entries its mask
+// names, in template (= stored) order: the same products and sums as wave_dot.
+__device__ __forceinline__ double wave_dot_banded(const char* body, uint32_t lane, const double* src) {
+    const uint32_t meta = reinterpret_cast<const uint16_t*>(body)[lane];
+    const char* tb = body + 64 + (meta >> 8) * 32u;
+    const uint4 b0 = *reinterpret_cast<const uint4*>(tb), b1 = *reinterpret_cast<const uint4*>(tb + 16);
+    const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = (meta >> j) & 1u ? ld_gather(src + (b[j] + lane)) : 0.0;
+    const double* v = reinterpret_cast<const double*>(body + 128 + (meta >> 8) * 64u);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if ((meta >> j) & 1u) acc = __dadd_rn(acc, __dmul_rn(v[j], x[j]));
+    return acc;
+}
+// The same row with every in-pass input awaited (first: the source slice is complete); rolled.
+__device__ __forceinline__ double wave_row_banded_slow(const char* body, uint32_t lane, const double* src, bool first,
+                                                       uint32_t* dbg) {
+    if (dbg) atomicAdd(dbg, 1u);
+    const uint32_t meta = reinterpret_cast<const uint16_t*>(body)[lane];
+    const uint32_t* b = reinterpret_cast<const uint32_t*>(body + 64 + (meta >> 8) * 32u);
+    const double* v = reinterpret_cast<const double*>(body + 128 + (meta >> 8) * 64u);
+    double acc = 0.0;
+#pragma unroll 1
+    for (uint32_t k = 0; k < 8; ++k) {
+        if (!((meta >> k) & 1u)) continue;
+        const double* p = src + (b[k] + lane);
+        double x;
+        if (first) {
+            x = __ldg(p);
+        } else {
+            x = ld_strong_again(p);
+            while (wave_empty(x)) {
+                __nanosleep(32);
+                x = ld_strong_again(p);
+            }
         }
         acc = __dadd_rn(acc, __dmul_rn(v[k], x));
     }
@@ -1551,6 +1608,15 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                     acc = wave_dot_affine_any(body, L, src_lane);
                 }
                 if (q != q0 && is_nan_bits(acc)) acc = wave_redo_affine(body, L, src_lane, P.dbg);
+            } else if (staged && F == 1 && (R::info4(rec).w & kWaveBanded)) {  // a banded chunk
+                const uint4 inf = R::info4(rec);
+                L = inf.y;
+                rb = inf.z;
+                rr = SIGMA ? R::slot(rec, lane) : s;
+                len = rr < P.n_rows ? R::len(rec, lane) : 0u;
+                const char* body = rec + R::hdr;
+                acc = wave_dot_banded(body, lane, src);
+                if (q != q0 && is_nan_bits(acc)) acc = wave_row_banded_slow(body, lane, src, false, P.dbg);
             } else if (staged) {  // the record in shared memory (every load below is an LDS)
                 const uint4 inf = R::info4(rec);
                 L = inf.y;
@@ -1583,8 +1649,11 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
                 rb = inf.z;
                 rr = SIGMA ? R::slot(h, lane) : s;
                 len = rr < P.n_rows ? R::len(h, lane) : 0u;
-                acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg,
-                                       (inf.w & kWaveAffine) != 0);
+                if (F == 1 && (inf.w & kWaveBanded))
+                    acc = wave_row_banded_slow(h + R::hdr, lane, src, q == q0, P.dbg);
+                else
+                    acc = wave_row_slow<F>(h + R::hdr, L, lane, len, src, q == q0, dict, P.dbg,
+                                           (inf.w & kWaveAffine) != 0);
             }
             if constexpr (TRACE) {  // audit build: every chunk's results are stored after the
                                     // whole tile's inputs are final (one stamp between the two)
@@ -1667,21 +1736,91 @@ __device__ __forceinline__ uint32_t dict_index(const unsigned long long* table, 
     return slot_ix[h];
 }
 
-// Affine chunks (setup): one warp per SELL chunk; flags[T] = 1 when the chunk has width 1..8, 32
-// real full rows, and every entry k is column c_k + lane with one value bit pattern in all lanes.
+// A chunk's rows against at most two row templates (banded records): the lane's keys (column -
+// lane) and value bits; template t = the longest row not yet matched (lowest lane on ties); a row
+// matches when each of its entries equals a template entry (key and value) at increasing template
+// positions.  Returns whether every real row matched; meta = template << 8 | entry mask, tk / tv =
+// the templates (unused positions 0), tl[t] = their lengths.
+__device__ bool banded_match(const uint32_t* __restrict__ cols, const double* __restrict__ vals, uint64_t o,
+                             uint32_t L, uint32_t len, uint32_t lane, uint32_t& meta, uint32_t (&tk)[2][8],
+                             unsigned long long (&tv)[2][8], uint32_t (&tl)[2]) {
+    uint32_t key[8];
+    unsigned long long vb[8];
+    const uint32_t Lp = L & ~1u;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        key[k] = 0;
+        vb[k] = 0;
+        if (k < len) {
+            const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
+            key[k] = cols[o + e] - lane;
+            vb[k] = (unsigned long long)__double_as_longlong(vals[o + e]);
+        }
+    }
+    bool open = true;
+    meta = 0;
+    tl[0] = tl[1] = 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const uint32_t want = open ? len + 1u : 0u;
+        const uint32_t best = __reduce_max_sync(0xffffffffu, want);
+        const uint32_t src = best ? (uint32_t)__ffs(__ballot_sync(0xffffffffu, want == best)) - 1u : 0u;
+        const uint32_t T_len = best ? best - 1u : 0u;
+        tl[t] = T_len;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t kk = __shfl_sync(0xffffffffu, key[k], src);
+            const unsigned long long vv = __shfl_sync(0xffffffffu, vb[k], src);
+            tk[t][k] = (uint32_t)k < T_len ? kk : 0u;
+            tv[t][k] = (uint32_t)k < T_len ? vv : 0ull;
+        }
+        if (open) {
+            uint32_t mk = 0;
+            int last = -1;
+            bool all = true;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if ((uint32_t)j >= len) continue;
+                int at = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if ((uint32_t)k < T_len && tk[t][k] == key[j] && tv[t][k] == vb[j] && k > last && at < 0) at = k;
+                if (at < 0) all = false;
+                else {
+                    mk |= 1u << at;
+                    last = at;
+                }
+            }
+            if (all) {
+                open = false;
+                meta = mk | (uint32_t)t << 8;
+            }
+        }
+    }
+    return !__any_sync(0xffffffffu, open);
+}
+
+// Affine and banded chunks (setup): one warp per SELL chunk; flags[T] = 1 (affine) when the chunk
+// has width 1..8, 32 real full rows, and every entry k is column c_k + lane with one value bit
+// pattern in all lanes; else 2 (banded) when its rows fit two templates (banded_match); else 0.
 __global__ void k_wave_affine(const uint32_t* __restrict__ cols, const double* __restrict__ vals,
                               const uint32_t* __restrict__ row_len, const uint32_t* __restrict__ slot_row,
                               const uint64_t* __restrict__ chunk_off, uint32_t n_chunks, uint32_t n_rows,
-                              uint8_t* __restrict__ flags) {
+                              int banded, uint8_t* __restrict__ flags) {
     const uint32_t lane = threadIdx.x & 31u;
     for (uint64_t T = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; T < n_chunks;
          T += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const uint64_t o = chunk_off[T];
         const uint32_t L = (uint32_t)((chunk_off[T + 1] - o) >> 5);
-        bool ok = L >= 1 && L <= 8;
-        if (ok) {
+        const bool narrow = L >= 1 && L <= 8;
+        bool ok = narrow;
+        uint32_t len = 0;
+        bool real = false;
+        if (narrow) {
             const uint32_t row = slot_row ? slot_row[T * 32 + lane] : (uint32_t)(T * 32 + lane);
-            ok = row < n_rows && row_len[T * 32 + lane] == L;
+            real = row < n_rows;
+            len = real ? row_len[T * 32 + lane] : 0u;
+            ok = real && len == L;
             const uint32_t Lp = L & ~1u;
             for (uint32_t k = 0; k < L; ++k) {
                 const uint32_t e = k < Lp ? (k >> 1) * 64u + lane * 2u + (k & 1u) : Lp * 32u + lane;
@@ -1693,7 +1832,13 @@ __global__ void k_wave_affine(const uint32_t* __restrict__ cols, const double* _
             }
         }
         ok = __all_sync(0xffffffffu, ok);
-        if (lane == 0) flags[T] = ok ? 1 : 0;
+        uint32_t f = ok ? 1u : 0u;
+        if (!ok && narrow && banded) {
+            uint32_t meta, tk[2][8], tl[2];
+            unsigned long long tv[2][8];
+            if (banded_match(cols, vals, o, L, len, lane, meta, tk, tv, tl)) f = 2u;
+        }
+        if (lane == 0) flags[T] = (uint8_t)f;
     }
 }
 
@@ -1717,11 +1862,12 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
         else reinterpret_cast<uint8_t*>(r)[lane] = (uint8_t)len;
         const uint64_t o = real ? chunk_off[T] : 0, ne = real ? chunk_off[T + 1] - o : 0;
         const uint32_t L = (uint32_t)(ne >> 5);
-        const bool aff = F == 1 && real && affine && affine[T];
+        const bool aff = F == 1 && real && affine && affine[T] == 1;
+        const bool band = F == 1 && real && affine && affine[T] == 2;
         if (lane < 4)  // info: tile, width, this record's bytes, flags
             reinterpret_cast<uint32_t*>(r + lb)[lane] =
                 lane == 0 ? (uint32_t)(T / kWaveChunks) : lane == 1 ? L : lane == 2 ? (rec_off[T + 1] - rec_off[T]) * 16u
-                                                                               : (aff ? kWaveAffine : 0u);
+                                                                               : (aff ? kWaveAffine : band ? kWaveBanded : 0u);
         uint32_t hdr = lb + 16;
         if (slot_row) {
             reinterpret_cast<uint32_t*>(r + hdr)[lane] = real ? slot_row[T * 32 + lane] : 0xffffffffu;
@@ -1733,6 +1879,27 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
                 const uint64_t e = k < Lp ? (k >> 1) * 64u + (k & 1u) : Lp * 32u;
                 reinterpret_cast<uint32_t*>(r + hdr)[k] = k < L ? cols[o + e] : 0u;
                 reinterpret_cast<double*>(r + hdr + 32)[k] = k < L ? vals[o + e] : 0.0;
+            }
+            continue;
+        }
+        if (band) {  // meta[32] u16 | base[2][8] u32 | v[2][8] f64
+            uint32_t meta, tk[2][8], tl[2];
+            unsigned long long tv[2][8];
+            banded_match(cols, vals, o, L, len, lane, meta, tk, tv, tl);
+            reinterpret_cast<uint16_t*>(r + hdr)[lane] = (uint16_t)meta;
+            if (lane < 16) {
+                uint32_t kv = 0;
+                unsigned long long vv = 0;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (lane == (uint32_t)(t * 8 + k)) {
+                            kv = tk[t][k];
+                            vv = tv[t][k];
+                        }
+                reinterpret_cast<uint32_t*>(r + hdr + 64)[lane] = kv;
+                reinterpret_cast<unsigned long long*>(r + hdr + 128)[lane] = vv;
             }
             continue;
         }
@@ -2661,10 +2828,11 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
         std::vector<uint8_t> aff;
         DevBuf<uint8_t> d_aff(std::max<uint32_t>(nc, 1));
         E.wave_affine_chunks = 0;
+        E.wave_banded_chunks = 0;
         if (E.wave_fmt == 1 && ctx->wave_affine && nc) {
             k_wave_affine<<<grid_for((uint64_t)nc * 32, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
                 E.S->cols.p, E.S->vals.p, E.S->row_len.p, sigma ? E.slot_row.p : nullptr, E.S->chunk_off.p, nc,
-                A->n_rows, d_aff.p);
+                A->n_rows, ctx->wave_affine >= 2 ? 1 : 0, d_aff.p);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
             aff.resize(nc);
@@ -2680,9 +2848,12 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
         for (uint64_t c = 0; c < nrec; ++c) {
             ro[c] = (uint32_t)acc;
             const uint32_t L = c < nc ? (uint32_t)((off[c + 1] - off[c]) >> 5) : 0u;
-            const bool is_aff = c < aff.size() && aff[c];
-            const uint32_t rb = is_aff ? wave_affine_bytes(sigma) : wave_rec_bytes(E.wave_fmt, sigma, L);
+            const bool is_aff = c < aff.size() && aff[c] == 1;
+            const bool is_band = c < aff.size() && aff[c] == 2;
+            const uint32_t rb = is_aff ? wave_affine_bytes(sigma)
+                                : is_band ? wave_banded_bytes(sigma) : wave_rec_bytes(E.wave_fmt, sigma, L);
             E.wave_affine_chunks += is_aff;
+            E.wave_banded_chunks += is_band;
             acc += rb / 16;
             if (acc > 0xffffffffull) fail(MPKG_EINVAL, "mpk: matrix too large for the wave schedule's records");
             E.tile_bytes[c / kWaveChunks] += rb + 16ull * 32;
@@ -3428,12 +3599,14 @@ void exec_info(const mpkg_plan_s* P, uint32_t* n_tiles, uint64_t* n_tickets, uin
     if (pass_powers) *pass_powers = pp;
 }
 
-void exec_wave(const mpkg_plan_s* P, int* format, uint64_t* n_chunks, uint64_t* n_affine, uint64_t* record_bytes) {
+void exec_wave(const mpkg_plan_s* P, int* format, uint64_t* n_chunks, uint64_t* n_affine, uint64_t* n_banded,
+               uint64_t* record_bytes) {
     const Executor* E = P->exec.get();
     const bool w = E && E->wrec.p != nullptr;
     if (format) *format = w ? E->wave_fmt : 0;
     if (n_chunks) *n_chunks = w ? (uint64_t)E->n_tiles * kWaveChunks : 0;
     if (n_affine) *n_affine = w ? E->wave_affine_chunks : 0;
+    if (n_banded) *n_banded = w ? E->wave_banded_chunks : 0;
     if (record_bytes) *record_bytes = w ? E->wave_rec_total : 0;
 }
 

@@ -171,13 +171,14 @@ def test_fused_mpk_corpus_all_p(ctx, cases, oracle):
 
 DEFAULT_KNOBS = {"order": -1, "slack": -1, "schedule": 0, "kernel": 0, "tile_rows": 128,
                  "producers": 0, "cgroups": 0, "stages": 0, "pass": 0, "l2_budget": 0, "ctas_per_sm": 0,
-                 "wave_dict": 1, "wave_affine": 1}
+                 "wave_dict": 1, "wave_affine": 2}
 
 SCHEDULES = {
     "sweeps": {"schedule": 2},
     "wave": {"schedule": 3},
     "wave-plain": {"schedule": 3, "wave_dict": 0},
     "wave-noaffine": {"schedule": 3, "wave_affine": 0},
+    "wave-affine-only": {"schedule": 3, "wave_affine": 1},
     "wave-1cta": {"schedule": 3, "ctas_per_sm": 1},
     "wave-pass1": {"schedule": 3, "pass": 1},
     "wave-pass2-slack1": {"schedule": 3, "pass": 2, "slack": 1},
@@ -602,7 +603,8 @@ def test_config1_full_size_bitwise(ctx, oracle):
     assert_bitwise(ctx.mpk(plan, Ap, x, 4).as_matrix(), ref)
 
 
-@pytest.mark.parametrize("knobs", [{}, {"pass": 2, "slack": 1}, {"pass": 8}, {"order": 1}, {"wave_affine": 0}])
+@pytest.mark.parametrize("knobs", [{}, {"pass": 2, "slack": 1}, {"pass": 8}, {"order": 1}, {"wave_affine": 0},
+                                   {"wave_affine": 1}, {"pass": 3, "ctas_per_sm": 1}])
 def test_wave_affine_records(ctx, oracle, knobs):
     """Affine chunk records (32 full rows whose entry k is column base_k + lane with one value:
     the interior of a level-ordered stencil) hold the same entries in the same stored order as the
@@ -620,10 +622,16 @@ def test_wave_affine_records(ctx, oracle, knobs):
         got = ctx.mpk(plan, Ap, x, 8).as_matrix()
         info = plan.exec_info()
         assert info["schedule"] == "wave" and info["wave_format"] == 1
-        if knobs.get("wave_affine", 1) and not knobs.get("order", 0):
+        if knobs.get("wave_affine", 2) and not knobs.get("order", 0):
             assert info["wave_affine_chunks"] > 0.25 * info["wave_chunks"], info
-        elif not knobs.get("wave_affine", 1):
+        elif not knobs.get("wave_affine", 2):
             assert info["wave_affine_chunks"] == 0
+        if knobs.get("wave_affine", 2) == 2 and not knobs.get("order", 0):
+            # the chunks where the grid's diagonals break are banded: almost nothing stays general
+            assert info["wave_banded_chunks"] > 0.25 * info["wave_chunks"], info
+            assert info["wave_affine_chunks"] + info["wave_banded_chunks"] > 0.9 * info["wave_chunks"], info
+        elif knobs.get("wave_affine", 2) < 2:
+            assert info["wave_banded_chunks"] == 0
         ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 8)
         assert_bitwise(got, ref, f"affine {knobs}")
         sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0, 3.0, 0.25]

@@ -15,7 +15,7 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 
 DEFAULTS = {"order": -1, "slack": -1, "pass": 0, "l2_budget": 0, "ctas_per_sm": 0, "group": 8,
-            "stages": 0, "tile_rows": 128, "threads": 0, "kernel": 0, "producers": 0, "cgroups": 0, "schedule": 0, "sweep_variant": 0, "coop_variant": 0, "wave_dict": 1, "wave_affine": 1}
+            "stages": 0, "tile_rows": 128, "threads": 0, "kernel": 0, "producers": 0, "cgroups": 0, "schedule": 0, "sweep_variant": 0, "coop_variant": 0, "wave_dict": 1, "wave_affine": 2}
 
 
 def main():
