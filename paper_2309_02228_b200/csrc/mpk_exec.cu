@@ -1094,6 +1094,9 @@ constexpr uint32_t kWaveAffine = 1u;
 // meta = the lane's template (bit 8) and which of its 8 entries the row has (bits 0-7), in stored
 // order: 304 bytes instead of 1,200 (k_wave_affine decides, k_wave_pack fills).
 constexpr uint32_t kWaveBanded = 2u;
+// info.w bit 2 of a pair's first record (k_wave_pairs): both chunks affine of width 7 and the second
+// continues the first one's diagonals (bases + 32, same values): one record serves both.
+constexpr uint32_t kWavePair7 = 4u;
 constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
 constexpr int kWaveAutoPass = 3;
@@ -1525,63 +1528,70 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         const double* src_lane = opaque_ptr(src + lane);  // opaque: one IMAD.WIDE per affine gather
         double tr_acc[TRACE ? kWaveChunks : 1];
         uint32_t tr_off[TRACE ? kWaveChunks : 1];
+        // One record for a chunk pair (kWavePair7): chunk b = chunk a 32 rows down the same diagonals.
+        auto pair7 = [&](uint32_t sa, double& a0, double& a1) {
+            double xa[7], xb[7];
+            const uint4 b0 = lds_v4(sa), b1 = lds_v4(sa + 16u);
+            const uint32_t b[7] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z};
+            const double* src_lane32 = src_lane + 32;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) xa[j] = ld_gather(src_lane + b[j]);
+#pragma unroll
+            for (int j = 0; j < 7; ++j) xb[j] = ld_gather(src_lane32 + b[j]);
+            a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 7; j += 2) {
+                const double2 vv = lds_d2(sa + 32u + 8u * j);
+                a0 = __dadd_rn(a0, __dmul_rn(vv.x, xa[j]));
+                a1 = __dadd_rn(a1, __dmul_rn(vv.x, xb[j]));
+                if (j + 1 < 7) {
+                    a0 = __dadd_rn(a0, __dmul_rn(vv.y, xa[j + 1]));
+                    a1 = __dadd_rn(a1, __dmul_rn(vv.y, xb[j + 1]));
+                }
+            }
+        };
+        // Stores and next-pass fills of a pair whose rows are all real (affine chunks).
+        auto pair_store = [&](const char* ra, uint32_t s, double a0, double a1) {
+            if (q != q0 && (is_nan_bits(a0) || is_nan_bits(a1))) {
+                if (is_nan_bits(a0)) a0 = wave_redo_affine(ra + R::hdr, 7u, src_lane, P.dbg);
+                if (is_nan_bits(a1)) a1 = wave_redo_affine(ra + R::affine_bytes + R::hdr, 7u, src_lane, P.dbg);
+            }
+            if constexpr (KIND == 0 && !SIGMA) {
+                double* const dst = P.V + (uint64_t)q * P.vstride;
+                st_strong(dst + s, a0);
+                st_strong(dst + s + 32u, a1);
+            } else {
+                wave_epilogue<KIND, SIGMA>(P, s, SIGMA ? R::slot(ra, lane) : s, q, q0, src, a0);
+                wave_epilogue<KIND, SIGMA>(P, s + 32u, SIGMA ? R::slot(ra + R::affine_bytes, lane) : s + 32u, q, q0,
+                                           src, a1);
+            }
+            if (q == q1) {
+                const double e = __longlong_as_double((long long)kWaveEmpty);
+                for (uint32_t f = fill_lo; f < fill_hi; ++f) {
+                    P.V[(uint64_t)f * P.vstride + s] = e;
+                    P.V[(uint64_t)f * P.vstride + s + 32u] = e;
+                }
+            }
+        };
         if (F == 1 && !TRACE && ((d.y >> 24) & 15u) == 7u) {
             // Fast tile (descriptor bits 24-27): every chunk an affine record of width 7 (the
             // interior of a level-ordered 3D 7-point stencil).  Two chunks at a time: both chunks'
             // gathers are in flight before the first sum.
-            double* const dst = P.V + (uint64_t)q * P.vstride;
 #pragma unroll
             for (uint32_t c = 0; c < kWaveChunks; c += 2) {
                 const uint32_t sa = stage_s + c * R::affine_bytes + R::hdr, sb = sa + R::affine_bytes;
                 const uint32_t s = T * kWaveRows + c * 32u + lane;
-                double xa[7], xb[7];
                 double a0, a1;
-                if (d.y & (1u << 28)) {  // pair tile: chunk b = chunk a 32 rows down the same diagonals
-                    const uint4 b0 = lds_v4(sa), b1 = lds_v4(sa + 16u);
-                    const uint32_t b[7] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z};
-                    const double* src_lane32 = src_lane + 32;
-#pragma unroll
-                    for (int j = 0; j < 7; ++j) xa[j] = ld_gather(src_lane + b[j]);
-#pragma unroll
-                    for (int j = 0; j < 7; ++j) xb[j] = ld_gather(src_lane32 + b[j]);
-                    a0 = 0.0, a1 = 0.0;
-#pragma unroll
-                    for (int j = 0; j < 7; j += 2) {
-                        const double2 vv = lds_d2(sa + 32u + 8u * j);
-                        a0 = __dadd_rn(a0, __dmul_rn(vv.x, xa[j]));
-                        a1 = __dadd_rn(a1, __dmul_rn(vv.x, xb[j]));
-                        if (j + 1 < 7) {
-                            a0 = __dadd_rn(a0, __dmul_rn(vv.y, xa[j + 1]));
-                            a1 = __dadd_rn(a1, __dmul_rn(vv.y, xb[j + 1]));
-                        }
-                    }
+                if (d.y & (1u << 28)) {  // pair tile
+                    pair7(sa, a0, a1);
                 } else {
+                    double xa[7], xb[7];
                     affine_gather_s<7>(sa, src_lane, xa);
                     affine_gather_s<7>(sb, src_lane, xb);
                     a0 = affine_sum_s<7>(sa, xa);
                     a1 = affine_sum_s<7>(sb, xb);
                 }
-                if (q != q0 && (is_nan_bits(a0) || is_nan_bits(a1))) {
-                    const char* ba = ring + st * SB + c * R::affine_bytes + R::hdr;
-                    if (is_nan_bits(a0)) a0 = wave_redo_affine(ba, 7u, src_lane, P.dbg);
-                    if (is_nan_bits(a1)) a1 = wave_redo_affine(ba + R::affine_bytes, 7u, src_lane, P.dbg);
-                }
-                if constexpr (KIND == 0 && !SIGMA) {
-                    st_strong(dst + s, a0);
-                    st_strong(dst + s + 32u, a1);
-                } else {
-                    const char* ra = ring + st * SB + c * R::affine_bytes;
-                    wave_epilogue<KIND, SIGMA>(P, s, SIGMA ? R::slot(ra, lane) : s, q, q0, src, a0);
-                    wave_epilogue<KIND, SIGMA>(P, s + 32u, SIGMA ? R::slot(ra + R::affine_bytes, lane) : s + 32u, q,
-                                               q0, src, a1);
-                }
-                if (q == q1) {
-                    const double e = __longlong_as_double((long long)kWaveEmpty);
-                    for (uint32_t f = fill_lo; f < fill_hi; ++f) {
-                        P.V[(uint64_t)f * P.vstride + s] = e;
-                        P.V[(uint64_t)f * P.vstride + s + 32u] = e;
-                    }
-                }
+                pair_store(ring + st * SB + c * R::affine_bytes, s, a0, a1);
             }
         } else {
         const char* stage = ring + st * SB;
@@ -1591,6 +1601,17 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveCtas) k_mpk_wave(const __gr
         for (uint32_t c = 0; c < kWaveChunks; ++c) {
             if constexpr (TRACE) tr_off[c] = (uint32_t)(rec - stage);
             const uint32_t s = T * kWaveRows + c * 32u + lane;
+            if constexpr (F == 1 && !TRACE && kWaveChunks > 2) {
+                // a pair of a mixed tile that is itself a width-7 pair: the fast tile's pair code
+                if (staged && !(c & 1u) && (R::info4(rec).w & kWavePair7)) {
+                    double a0, a1;
+                    pair7(stage_s + (uint32_t)(rec - stage) + R::hdr, a0, a1);
+                    pair_store(rec, s, a0, a1);
+                    rec += 2u * R::affine_bytes;
+                    ++c;
+                    continue;
+                }
+            }
             uint32_t L, rr, len, rb;
             double acc = 0.0;
             if (staged && F == 1 && (R::info4(rec).w & kWaveAffine)) {  // an affine chunk: full rows
@@ -1924,27 +1945,34 @@ __global__ void k_wave_pack(const uint32_t* __restrict__ cols, const double* __r
     }
 }
 
-// Pair tiles (setup, after k_wave_pack): a fast tile whose odd chunks are their even predecessors
-// 32 rows further down the same diagonals (bases + 32, the same values) gets bit 1 of its tile
-// code: the engine then reads one record per chunk pair.  One thread per tile.
-__global__ void k_wave_pairs(const char* __restrict__ rec, const uint32_t* __restrict__ rec_off, uint32_t n_tiles,
-                             uint32_t hdr, uint8_t* __restrict__ code) {
+// Pairs (setup, after k_wave_pack): a chunk pair (2i, 2i+1 of a tile) whose records are both
+// affine of one width and whose second chunk is the first 32 rows further down the same diagonals
+// (bases + 32, the same values) is marked in the first record (info.w |= kWavePair7 when the width
+// is 7); a fast tile all of whose pairs are such gets bit 1 of its tile code (pair tile): the
+// engine then reads one record per chunk pair.  One thread per tile.
+__global__ void k_wave_pairs(char* __restrict__ rec, const uint32_t* __restrict__ rec_off, uint32_t n_tiles,
+                             uint32_t len_bytes, uint32_t hdr, uint8_t* __restrict__ code) {
     for (uint64_t T = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; T < n_tiles;
          T += (uint64_t)gridDim.x * blockDim.x) {
-        if ((code[T] >> 4) == 0) continue;  // not a fast tile
-        bool ok = true;
-        for (uint32_t c = 0; c < kWaveChunks && ok; c += 2) {
-            const char* a = rec + (uint64_t)rec_off[T * kWaveChunks + c] * 16u + hdr;
-            const char* b = rec + (uint64_t)rec_off[T * kWaveChunks + c + 1] * 16u + hdr;
-            for (int k = 0; k < 8; ++k) {
+        bool all = true;
+        for (uint32_t c = 0; c < kWaveChunks; c += 2) {
+            char* ra = rec + (uint64_t)rec_off[T * kWaveChunks + c] * 16u;
+            const char* rb = rec + (uint64_t)rec_off[T * kWaveChunks + c + 1] * 16u;
+            uint32_t* ia = reinterpret_cast<uint32_t*>(ra + len_bytes);
+            const uint32_t* ib = reinterpret_cast<const uint32_t*>(rb + len_bytes);
+            bool ok = (ia[3] & kWaveAffine) && (ib[3] & kWaveAffine) && ia[1] == ib[1];
+            const uint32_t L = ia[1];
+            const char *a = ra + hdr, *b = rb + hdr;
+            for (int k = 0; k < 8 && ok; ++k) {
                 const uint32_t ba = reinterpret_cast<const uint32_t*>(a)[k], bb = reinterpret_cast<const uint32_t*>(b)[k];
                 const unsigned long long va = reinterpret_cast<const unsigned long long*>(a + 32)[k];
                 const unsigned long long vb = reinterpret_cast<const unsigned long long*>(b + 32)[k];
-                const bool used = (uint32_t)k < (uint32_t)(code[T] >> 4);
-                ok = ok && va == vb && (used ? bb == ba + 32u : bb == ba);
+                ok = va == vb && ((uint32_t)k < L ? bb == ba + 32u : bb == ba);
             }
+            if (ok && L == 7) ia[3] |= kWavePair7;
+            all = all && ok;
         }
-        if (ok) code[T] |= 2u;
+        if (all && (code[T] >> 4) != 0) code[T] |= 2u;
     }
 }
 
@@ -2889,7 +2917,8 @@ void build_wave(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, Executor& E) {
         }
         if (nt && !aff.empty()) {
             k_wave_pairs<<<grid_for(nt, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
-                E.wrec.p, E.wrec_off.p, nt, sigma ? WaveRec<1, true>::hdr : WaveRec<1, false>::hdr, E.wave_narrow.p);
+                E.wrec.p, E.wrec_off.p, nt, WaveRec<1, false>::len_bytes,
+                sigma ? WaveRec<1, true>::hdr : WaveRec<1, false>::hdr, E.wave_narrow.p);
             MPKG_LAUNCH_CHECK();
             ctx->launches += 1;
         }
