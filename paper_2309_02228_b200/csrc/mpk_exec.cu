@@ -1408,7 +1408,10 @@ __device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, 
 // front, which lets a small slack, and so a small L2 window, suffice), and the lowest unfinished
 // ticket is always one a warp is running.  A ticket waits only on values of lower tickets, so it
 // always progresses: deadlock-free without co-residency.
-constexpr uint32_t kWaveStreams = 16;
+#ifndef MPKG_WAVE_STREAMS
+#define MPKG_WAVE_STREAMS 16
+#endif
+constexpr uint32_t kWaveStreams = MPKG_WAVE_STREAMS;
 
 // Every warp owns a two-stage shared-memory ring; lane 0 stages the NEXT ticket's chunk record
 // with one 1D bulk copy (cp.async.bulk, mbarrier complete_tx, L2 evict_last, evict_first on the
