@@ -2407,12 +2407,12 @@ Executor& get_executor(mpkg_ctx_s* ctx, mpkg_plan_s* P, mpkg_csr_s* A) {
     E->n_slots = (A->n_rows + 31u) & ~31u;
     // Row order: explicit, or auto: longest-rows-first (SELL-C-sigma) for power-law row lengths,
     // Cuthill-McKee inside levels otherwise.
-    // Auto schedule: the wave (cross-power L2 reuse) for large short-row matrices -- every row a
-    // single 8-entry group, matrix several times the L2 (C5's 7-point rows: same step time as the
-    // sweeps with ~2.7x less DRAM traffic); one launch per power otherwise.
+    // Auto schedule: the wave (cross-power L2 reuse) for short-row matrices larger than the L2 --
+    // every row a single 8-entry group (7-point Laplacians, p = 8, tools/wave_threshold.py: 128^3 /
+    // 175 MB 146 vs 288 us for the sweeps, 256^3 0.77 vs 2.58 ms, C5 5.4 vs 20.2 ms; 64^3, which
+    // sits in L2, 69 vs 46 us); one launch per power otherwise.
     const uint32_t mx_len = gpu_max_row_len(ctx, A);
-    E->wave_auto = ctx->schedule == 0 && mx_len <= 8 &&
-                   12ull * A->nnz > 4ull * ctx->l2_bytes;
+    E->wave_auto = ctx->schedule == 0 && mx_len <= 8 && 12ull * A->nnz > 1ull * ctx->l2_bytes;
     if (ctx->order >= 0 && ctx->order <= 2) {
         E->order = (int)ctx->order;
     } else {
