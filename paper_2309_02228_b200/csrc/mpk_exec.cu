@@ -1097,7 +1097,6 @@ constexpr uint32_t kWaveBanded = 2u;
 // info.w bit 2 of a pair's first record (k_wave_pairs): both chunks affine of width 7 and the second
 // continues the first one's diagonals (bases + 32, same values): one record serves both.
 constexpr uint32_t kWavePair7 = 4u;
-constexpr uint32_t kWaveWideL = 15;
 constexpr int kWaveMaxPass = 16;  // q - q0 has 4 bits
 constexpr int kWaveAutoPass = 3;
 constexpr uint32_t kWaveDictMax = 255;
