@@ -4,13 +4,15 @@
 // Reference behaviour replaced: execute.hpp:79-113 runs every (group, power) cell of the diagonal
 // wavefront (execute.hpp:59-72) with an OpenMP team and a barrier after every cell; mpk.hpp:81-106 /
 // 184-207 are its kernels.  On the GPU there are three schedules ("schedule" knob, 0 = auto):
-//   * wave (3) -- the default for large matrices whose rows are at most 8 entries (C5, C1-like
-//     stencils): cross-power L2 reuse.  One persistent launch per PASS of p' powers; tickets (one
-//     32-row SELL chunk, one power) run in a host-computed skewed order so the p' power fronts trail
-//     each other by about a BFS level and a chunk's matrix slice, read from HBM by the first front,
-//     is re-read from L2 by the others.  p' is the plan's cache budget applied to this GPU's L2
-//     (plan.hpp:88-115).  Synchronisation is by value (signalling-NaN sentinel fill, no flags).  Each
-//     warp stages its next ticket's chunk record with one TMA bulk copy (k_mpk_wave);
+//   * wave (3) -- the default for matrices larger than the L2 whose rows are at most 8 entries
+//     (C5): cross-power L2 reuse.  One persistent launch per PASS of p' powers; tickets (a tile of
+//     two 32-row SELL chunks, one power) run in a host-computed skewed order so the p' power fronts
+//     trail each other by about a BFS level and a tile's matrix slice, read from HBM by the first
+//     front, is re-read from L2 by the others.  p' is the plan's cache budget applied to this GPU's
+//     L2 (plan.hpp:88-115).  Synchronisation is by value (signalling-NaN sentinel fill, no flags).
+//     The matrix is kept as chunk records -- general (value dictionary or plain), affine, banded;
+//     see "The wave engine" below -- and each warp stages its next ticket's records with one TMA
+//     bulk copy (k_mpk_wave);
 //   * sweeps (2) -- one launch per power (k_mpk_sweep, replayed as one CUDA graph), with hub rows on
 //     a side stream (k_long_rows_bitwise / k_coop_rows): the default otherwise (27-point stencils,
 //     R-MAT), where the wave's stage would not hold a chunk;
