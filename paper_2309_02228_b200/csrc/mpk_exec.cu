@@ -135,6 +135,7 @@ struct Executor {
     int wave_fmt = 0;                         // chunk-record format: 0 plain, 1 value dictionary
     DevBuf<double> wave_dict;                 // the distinct values (wave_fmt 1)
     uint32_t n_dict = 0;
+    DevBuf<double> poly_coef;                 // k_poly_combine's coefficients
     uint64_t wave_affine_chunks = 0;          // chunks stored as affine records
     uint64_t wave_banded_chunks = 0;          // chunks stored as banded records
     uint64_t wave_rec_total = 0;              // bytes of all chunk records
@@ -1383,7 +1384,8 @@ __device__ __forceinline__ double wave_row_banded_slow(const char* body, uint32_
 }
 
 // row_epilogue with the wave's rules: in-pass values are awaited, working-vector stores are
-// single-copy atomic (KIND 2 never runs here: its accumulator has no value to wait on).
+// single-copy atomic (KIND 2 never runs here: the polynomial runs the plain powers on the wave and
+// forms z from the finished slices, k_poly_combine).
 template <int KIND, bool SIGMA>
 __device__ __forceinline__ void wave_epilogue(const FusedParams& P, uint32_t s, uint32_t r, uint32_t q,
                                               uint32_t q0, const double* src, double acc) {
@@ -3064,6 +3066,18 @@ const Executor::Wave& get_wave(mpkg_ctx_s* ctx, Executor& E, int p) {
     return E.wave.emplace(p, std::move(W)).first->second;
 }
 
+// The coefficient polynomial from finished slices (wave schedule): z = c_0 x + c_1 y_1, then
+// z += c_q y_q for q = 2..p, the order and the separate multiply / add of row_epilogue<2> (and of
+// the reference harness): bit-identical to the sweeps' running accumulator.
+__global__ void k_poly_combine(const double* __restrict__ blk, uint64_t stride, uint32_t n, uint32_t p,
+                               const double* __restrict__ coef, double* __restrict__ z) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+        double zr = __dadd_rn(__dmul_rn(coef[0], blk[r]), __dmul_rn(coef[1], blk[stride + r]));
+        for (uint32_t q = 2; q <= p; ++q) zr = __dadd_rn(zr, __dmul_rn(coef[q], blk[(uint64_t)q * stride + r]));
+        z[r] = zr;
+    }
+}
+
 void* wave_fn(int kind, bool sigma, int fmt, bool trace) {
 #define MPKG_WAVE_FNS(F, TR)                                                                         \
     {(void*)k_mpk_wave<0, false, F, TR>, (void*)k_mpk_wave<0, true, F, TR>, (void*)k_mpk_wave<1, false, F, TR>, \
@@ -3158,7 +3172,7 @@ void build_coop(mpkg_ctx_s* ctx, Executor& E, mpkg_csr_s* A) {
 
 bool use_sweeps(const mpkg_ctx_s* ctx, const Executor& E, int p, int kind) {
     if (ctx->schedule == 1) return false;
-    if ((ctx->schedule == 3 || (ctx->schedule == 0 && E.wave_auto && p >= 2)) && kind != 2 && E.h_tile_start.empty() &&
+    if ((ctx->schedule == 3 || (ctx->schedule == 0 && E.wave_auto && p >= 2)) && E.h_tile_start.empty() &&
         E.tile_rows == kWaveRows)
         return false;
     // Long rows live outside the SELL arrays.  Fast mode reduces them in k_coop_rows beside the
@@ -3174,7 +3188,6 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     if (E.n_tiles == 0) return;
     const bool sweep = use_sweeps(ctx, E, a.p, a.kind);
     const bool wave = !sweep && ctx->schedule != 1;
-    if (wave && a.kind == 2) fail(MPKG_EINTERNAL, "mpk: the wave schedule has no polynomial epilogue");
     if (!sweep && !wave && !E.fused_ready) build_fused(ctx, Pl, A, &E);
     if (wave && !E.wave_grid) {
         build_wave(ctx, Pl, A, E);  // picks the record format
@@ -3521,7 +3534,8 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
     } else if (wave) {
         // one cooperative launch per pass (all CTAs resident: static ticket assignment); with a
         // host block, the pass's slices go to the host while the next pass runs
-        void* fn = wave_fn(a.kind, sigma, E.wave_fmt, P.trace != nullptr);
+        // (the polynomial: plain powers here, then z from the finished slices, k_poly_combine)
+        void* fn = wave_fn(a.kind == 2 ? 0 : a.kind, sigma, E.wave_fmt, P.trace != nullptr);
         P.counter = E.counter.p;
         P.dbg = getenv("MPKG_WAVE_DEBUG") ? E.counter.p + kWaveStreams * 32 : nullptr;
         for (size_t j = 0; j + 1 < W->t_begin.size(); ++j) {
@@ -3558,6 +3572,15 @@ void run_fused(mpkg_ctx_s* ctx, mpkg_plan_s* Pl, mpkg_csr_s* A, const FusedArgs&
             if (j + 2 < W->t_begin.size()) ctx->launches += 1;
             if (to_host)
                 for (int q = W->q_begin[j]; q < W->q_begin[j + 1]; ++q) copy_slice((uint32_t)q);
+        }
+        if (a.kind == 2) {
+            DevBuf<double>& cf = E.poly_coef;
+            cf.ensure(kMaxFusedP + 1);
+            MPKG_CUDA(cudaMemcpyAsync(cf.p, P.coef, sizeof(double) * (a.p + 1), cudaMemcpyHostToDevice, st));
+            k_poly_combine<<<grid_for(A->n_rows, 256, (unsigned)ctx->sm_count * 8u), 256, 0, st>>>(
+                a.block, a.rows, A->n_rows, (uint32_t)a.p, cf.p, a.z);
+            MPKG_LAUNCH_CHECK();
+            ctx->launches += 1;
         }
         if (to_host) join_copies();
         if (getenv("MPKG_WAVE_DEBUG")) {
