@@ -653,6 +653,32 @@ def test_wave_affine_records(ctx, oracle, knobs):
         set_knobs(ctx, {})
 
 
+def test_auto_schedule_picks_the_wave_above_l2(ctx, oracle):
+    """Auto schedule: a short-row matrix larger than the L2 (128^3 7-point Laplacian, 175 MB) runs
+    on the wave, powers / Newton basis / polynomial (plain powers + k_poly_combine) all bitwise; a
+    64^3 one (22 MB, L2-resident) stays on the sweeps."""
+    set_knobs(ctx, {})
+    for n, want in ((128, "wave"), (64, "sweeps")):
+        A = mpkg.poisson3d(n, n, n)
+        dA = ctx.csr(A)
+        ls = ctx.build_levels(dA)
+        Ap = ctx.permute(dA, ls)
+        P = Ap.download()
+        x = mpkg.random_vector(A.n_rows, 21)
+        plan = ctx.group_levels(ls, Ap, ctx.device_info()["l2_bytes"], 4)
+        got = ctx.mpk(plan, Ap, x, 4).as_matrix()
+        assert plan.exec_info()["schedule"] == want, plan.exec_info()
+        ref = oracle.baseline_mpk(P.row_ptr, P.col_idx, P.values, x, 4)
+        assert_bitwise(got, ref, f"auto {n}^3")
+        coef = np.linspace(-1, 1, 5)
+        zr, _ = oracle.poly(P.row_ptr, P.col_idx, P.values, x, coef)
+        assert_bitwise(ctx.mpk_poly(plan, Ap, x, coef), zr, f"auto poly {n}^3")
+        assert plan.exec_info()["schedule"] == want
+        sh = [0.5, 1.0 + 2.0j, 1.0 - 2.0j, -1.0]
+        ref = oracle.baseline_mpk_shifted(P.row_ptr, P.col_idx, P.values, x, sh)
+        assert_bitwise(ctx.mpk_shifted(plan, Ap, x, sh).as_matrix(), ref, f"auto shifted {n}^3")
+
+
 @pytest.mark.parametrize("dict_fmt", [1, 0])
 def test_wave_special_values_and_sentinel_pattern(ctx, oracle, dict_fmt):
     """The wave schedule synchronises by value (a signalling-NaN sentinel in the slices a pass
